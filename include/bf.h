@@ -1,0 +1,180 @@
+/*
+ * bf.h -- C ABI of the B200-native IBF-MAT apply (arXiv:1803.04128, H. Yang).
+ *
+ * The library applies a complementary-low-rank butterfly factorization (BF) of
+ * the phase matrix e^{2 pi i Phi}, together with a low-rank amplitude split
+ * alpha(x,xi) ~ sum_k a_k(x) b_k(xi), to a batch of right-hand sides:
+ *
+ *      G = sum_k a_k o BF(b_k o F)                       eqn:tg
+ *
+ * where BF is the factor form eqn:BFM  K ~ U^L G^{L-1}...G^h M^h (H^h)*...(H^1)*(V^0)*
+ * whose blocks are produced by Algorithm 4.1.
+ *
+ * Notation (0-based; DESIGN.md sections 2-3):
+ *   N = 2^LN (LN even), leaf n0 = 2^l0 (r <= n0, 2 l0 <= LN), D = LN - l0, h = LN/2.
+ *   Level l in [l0, D]:  A(l,a) = rows [a N/2^l, (a+1) N/2^l),  a < 2^l
+ *                        B(l,b) = cols [b 2^l, (b+1) 2^l),       b < 2^(LN-l)
+ *   Pairs (A,B) at level l have l_A + l_B = LN (width product 1);
+ *   there are N pairs per level, pair index p = a * 2^(LN-l) + b.
+ *   r = block rank (number of interpolation points r_eps); n_amp = number of
+ *   amplitude terms k.
+ *
+ * Complex values are interleaved {re, im} single precision (complex64), little
+ * endian.  Every factor block is stored COLUMN-MAJOR: element (row, col) of an
+ * m x k block sits at col*m + row.  Blocks of one stage are stored in pair order.
+ *
+ * Stages of one apply (all FP32 FFMA accumulation):
+ *   V0   (S0)  per pair at level l0 an r x n0 block  (initialization eqn:1, P:698-702;
+ *              A = A(l0,a), B = B(l0,b) is a leaf of n0 columns)
+ *   XFER       per transfer level l = l0+1..D and pair an r x 2r block acting on
+ *              [delta_{l-1}(a>>1, 2b); delta_{l-1}(a>>1, 2b+1)]
+ *              (first half l <= h: eqn:2 P:748-752; second half l > h: eqn:3 P:780-785)
+ *   SW         per pair at level h an r x r block (switch)
+ *   U    (SL)  per pair at level D an n0 x r block; the n0 pairs (a, b<n0) of a
+ *              T_X leaf a are summed (termination eqn:bf3)
+ *
+ * Errors: every call returns a bf_status_t; nothing throws or aborts across the
+ * ABI.  Argument, shape and alignment errors are detected synchronously.  Kernel
+ * launch errors are reported by the launching call; asynchronous device faults
+ * surface at the next synchronizing call (bf_plan_destroy, bf_apply_host, or the
+ * caller's own stream synchronization).  bf_last_error() returns a thread-local
+ * message describing the last non-OK status of the calling thread.
+ */
+#ifndef BF_H_
+#define BF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BF_ABI_VERSION 1
+
+typedef struct { float re, im; } bf_c64;   /* complex64, layout-compatible with float2 */
+
+typedef enum {
+    BF_OK = 0,
+    BF_ERR_INVALID_ARG = 1,   /* null pointer, negative count, bad stage id, ...            */
+    BF_ERR_SHAPE = 2,         /* N / leaf / rank / n_amp combination not supported          */
+    BF_ERR_ALIGNMENT = 3,     /* F/G/workspace not 16-byte aligned, ld too small            */
+    BF_ERR_OOM = 4,           /* device or pinned-host allocation failed                    */
+    BF_ERR_CUDA = 5,          /* CUDA runtime error (message in bf_last_error)              */
+    BF_ERR_NCCL = 6,          /* reserved for the index-sharded plan                        */
+    BF_ERR_NOT_SUPPORTED = 7, /* e.g. odd rank, rank > 16, n_amp not in {1,2,4}             */
+    BF_ERR_STATE = 8          /* plan not finalized / stage not uploaded / already final    */
+} bf_status_t;
+
+/* stage ids for bf_plan_upload */
+#define BF_STAGE_V0 0
+#define BF_STAGE_SW 1
+#define BF_STAGE_U 2
+#define BF_STAGE_AMP_A 3   /* blocks = the n_amp rows of N values each */
+#define BF_STAGE_AMP_B 4
+#define BF_STAGE_XFER0 16  /* BF_STAGE_XFER0 + i is transfer level l = l0 + 1 + i, i < D - l0 */
+
+#define BF_MEM_HOST 0
+#define BF_MEM_DEVICE 1
+
+typedef struct bf_plan_s *bf_plan_t;
+
+/* Factor arrays of one BF (see the stage list above for shapes).
+ *   amp_a  [n_amp][N]        a_k(x_i)
+ *   amp_b  [n_amp][N]        b_k(xi_j)
+ *   v0     [N][n0][r]        pair p = a (N/n0) + b at level l0; block r x n0 column-major
+ *   xfer   D-l0 pointers; xfer[i] is [N][2r][r] for level l = l0+1+i, pair p = a 2^(LN-l) + b;
+ *          column c r + s of a block multiplies delta_{l-1}(a>>1, 2b+c)[s]
+ *   sw     [N][r][r]         pair p = a 2^h + b at level h
+ *   u      [N][r][n0]        pair p = a n0 + b at level D (a < N/n0 a T_X leaf, b < n0);
+ *                            block n0 x r column-major: row j is output x = a n0 + j
+ * Any of the array pointers may be NULL in a descriptor passed to bf_plan_alloc. */
+typedef struct {
+    int32_t abi_version;       /* BF_ABI_VERSION */
+    int32_t log2n;             /* LN, even, 2 <= LN <= 26 */
+    int32_t log2leaf;          /* l0, 1 <= l0, 2 l0 <= LN */
+    int32_t rank;              /* r, even, 2 <= r <= 16, r <= n0 */
+    int32_t n_amp;             /* n_amp in {1, 2, 4} */
+    int32_t memory;            /* BF_MEM_HOST or BF_MEM_DEVICE: where the arrays below live */
+    const bf_c64 *amp_a;
+    const bf_c64 *amp_b;
+    const bf_c64 *v0;
+    const bf_c64 *const *xfer;
+    const bf_c64 *sw;
+    const bf_c64 *u;
+} bf_desc_t;
+
+typedef struct {
+    int32_t log2n, log2leaf, rank, n_amp, switch_level, n_xfer;
+    int64_t n;
+    int64_t max_nrhs_chunk;
+    int64_t factor_bytes;        /* device bytes of all factor + amplitude arrays */
+    int64_t workspace_bytes;     /* device bytes of the plan-owned coefficient workspace */
+    int32_t launches_per_chunk;  /* kernels one RHS chunk of bf_apply launches */
+    int32_t device;
+} bf_plan_info_t;
+
+/* Create a plan on `device` from complete factor arrays.  The plan deep-copies
+ * every array into device memory it owns (the caller may free its arrays when
+ * the call returns) and allocates a coefficient workspace for RHS chunks of at
+ * most max_nrhs_chunk columns (2 arrays of N r max_nrhs_chunk n_amp complex64).
+ * The plan is immutable afterwards. */
+bf_status_t bf_plan_create(const bf_desc_t *desc, int device, int64_t max_nrhs_chunk, bf_plan_t *out);
+
+/* Streaming construction (factors larger than host RAM): allocate the plan from the
+ * shape fields of `meta` (array pointers ignored), upload stage blocks in any order
+ * and ranges, then finalize.  block_begin/block_count count blocks of the stage
+ * (pairs; for BF_STAGE_AMP_* the amplitude rows).  src is host (pageable or pinned)
+ * or device memory per src_memory; the copy is complete when the call returns. */
+bf_status_t bf_plan_alloc(const bf_desc_t *meta, int device, int64_t max_nrhs_chunk, bf_plan_t *out);
+bf_status_t bf_plan_upload(bf_plan_t plan, int32_t stage, int64_t block_begin, int64_t block_count,
+                           const bf_c64 *src, int32_t src_memory);
+/* Fails with BF_ERR_STATE unless every block of every stage was uploaded. */
+bf_status_t bf_plan_finalize(bf_plan_t plan);
+
+/* G = sum_k a_k o BF(b_k o F) for nrhs columns.  F and G are DEVICE buffers,
+ * column-major N x nrhs with leading dimension N, 16-byte aligned, not aliasing.
+ * Only enqueues work on `stream` (a cudaStream_t; NULL = legacy default stream):
+ * no allocation, no synchronization, CUDA-graph capturable.  RHS are processed in
+ * chunks of at most max_nrhs_chunk columns.  nrhs = 0 is a no-op.  One apply per
+ * plan may be in flight at a time (the workspace is shared) unless bf_apply_ex is
+ * given its own workspace. */
+bf_status_t bf_apply(bf_plan_t plan, const bf_c64 *F, bf_c64 *G, int64_t nrhs, void *stream);
+
+/* As bf_apply with leading dimensions (ldf, ldg >= N, even) and an optional
+ * caller workspace (device, 16-byte aligned, >= bf_workspace_bytes(plan, chunk)). */
+bf_status_t bf_apply_ex(bf_plan_t plan, const bf_c64 *F, int64_t ldf, bf_c64 *G, int64_t ldg, int64_t nrhs,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* End-to-end apply with HOST buffers (N x nrhs column-major, ld = N; pinned memory
+ * recommended): per RHS chunk, host->device copy of F, the apply, device->host copy
+ * of G, all on `stream`; returns after the stream has completed the work. */
+bf_status_t bf_apply_host(bf_plan_t plan, const bf_c64 *F_host, bf_c64 *G_host, int64_t nrhs, void *stream);
+
+/* Workspace bytes one chunk of `nrhs_chunk` columns needs. */
+size_t bf_workspace_bytes(bf_plan_t plan, int64_t nrhs_chunk);
+
+bf_status_t bf_plan_get_info(bf_plan_t plan, bf_plan_info_t *info);
+
+/* Per-kernel device timing (for the roofline report).  When enabled, every launch
+ * of bf_apply is bracketed by CUDA events on the launching stream; bf_plan_timing
+ * synchronizes on the last event and returns the accumulated milliseconds and
+ * launch counts per kernel class: [0] S0, [1] first-half transfer, [2] switch-fused
+ * transfer / switch, [3] second-half transfer, [4] SL.  Arrays have BF_NUM_KCLASS
+ * entries.  Enabling resets the accumulators. */
+#define BF_NUM_KCLASS 5
+bf_status_t bf_plan_set_timing(bf_plan_t plan, int32_t enable);
+bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
+
+/* Wait for the plan's outstanding work, then free everything it owns. */
+bf_status_t bf_plan_destroy(bf_plan_t plan);
+
+/* Thread-local description of the last non-OK status ("" if none). */
+const char *bf_last_error(void);
+
+int32_t bf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BF_H_ */

@@ -30,7 +30,7 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (C11, -O2, OpenMP). Building the checker is not using it."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-std=gnu11", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"]
+        cmd = ["gcc", "-std=gnu11", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"]
         subprocess.check_call(cmd)
     return _LIB
 

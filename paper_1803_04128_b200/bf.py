@@ -1,0 +1,224 @@
+"""Thin ctypes binding of the C ABI in include/bf.h and include/bf_build.h.
+
+Argument marshalling only: every step of the apply runs in the CUDA kernels of
+``libbfapply.so``; the factors are built by the library's host builder.  There
+is no Python or CPU fallback: if the library is missing or a call fails, an
+exception is raised.  Torch is used by callers only for device memory and
+streams (pass ``tensor.data_ptr()`` and ``torch.cuda.current_stream().cuda_stream``
+or hand tensors directly to the helpers below).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbfapply.so")
+
+BF_ABI_VERSION = 1
+BF_MEM_HOST, BF_MEM_DEVICE = 0, 1
+BF_STAGE_V0, BF_STAGE_SW, BF_STAGE_U, BF_STAGE_AMP_A, BF_STAGE_AMP_B, BF_STAGE_XFER0 = 0, 1, 2, 3, 4, 16
+BF_NUM_KCLASS = 5
+KCLASS_NAMES = ("s0", "xfer_first_half", "xfer_switch", "xfer_second_half", "sl")
+STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALIGNMENT", 4: "BF_ERR_OOM",
+          5: "BF_ERR_CUDA", 6: "BF_ERR_NCCL", 7: "BF_ERR_NOT_SUPPORTED", 8: "BF_ERR_STATE"}
+
+# every symbol include/*.h declares (checked by tests/test_abi.py)
+EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finalize", "bf_apply", "bf_apply_ex",
+           "bf_apply_host", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing",
+           "bf_plan_destroy", "bf_last_error", "bf_abi_version", "bf_build_n_amp", "bf_build_amp", "bf_build_blocks",
+           "bf_build_block_elems", "bf_plan_build_fio")
+
+
+class BFError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class bf_desc_t(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_int32), ("log2n", ctypes.c_int32), ("log2leaf", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("n_amp", ctypes.c_int32), ("memory", ctypes.c_int32),
+                ("amp_a", ctypes.c_void_p), ("amp_b", ctypes.c_void_p), ("v0", ctypes.c_void_p),
+                ("xfer", ctypes.POINTER(ctypes.c_void_p)), ("sw", ctypes.c_void_p), ("u", ctypes.c_void_p)]
+
+
+class bf_plan_info_t(ctypes.Structure):
+    _fields_ = [("log2n", ctypes.c_int32), ("log2leaf", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("n_amp", ctypes.c_int32), ("switch_level", ctypes.c_int32), ("n_xfer", ctypes.c_int32),
+                ("n", ctypes.c_int64), ("max_nrhs_chunk", ctypes.c_int64), ("factor_bytes", ctypes.c_int64),
+                ("workspace_bytes", ctypes.c_int64), ("launches_per_chunk", ctypes.c_int32),
+                ("device", ctypes.c_int32)]
+
+
+class bf_fio_t(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_int32), ("kernel", ctypes.c_int32), ("amp", ctypes.c_int32),
+                ("log2n", ctypes.c_int32), ("log2leaf", ctypes.c_int32), ("rank", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libbfapply.so (fails loudly when the CUDA extension is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        P = ctypes.POINTER
+        sigs = {
+            "bf_plan_create": ([P(bf_desc_t), ctypes.c_int, i64, P(vp)], i32),
+            "bf_plan_alloc": ([P(bf_desc_t), ctypes.c_int, i64, P(vp)], i32),
+            "bf_plan_upload": ([vp, i32, i64, i64, vp, i32], i32),
+            "bf_plan_finalize": ([vp], i32),
+            "bf_apply": ([vp, vp, vp, i64, vp], i32),
+            "bf_apply_ex": ([vp, vp, i64, vp, i64, i64, vp, sz, vp], i32),
+            "bf_apply_host": ([vp, vp, vp, i64, vp], i32),
+            "bf_workspace_bytes": ([vp, i64], sz),
+            "bf_plan_get_info": ([vp, P(bf_plan_info_t)], i32),
+            "bf_plan_set_timing": ([vp, i32], i32),
+            "bf_plan_timing": ([vp, P(ctypes.c_double), P(i64)], i32),
+            "bf_plan_destroy": ([vp], i32),
+            "bf_last_error": ([], ctypes.c_char_p),
+            "bf_abi_version": ([], i32),
+            "bf_build_n_amp": ([i32], i32),
+            "bf_build_amp": ([P(bf_fio_t), vp, vp], i32),
+            "bf_build_blocks": ([P(bf_fio_t), i32, i64, i64, vp], i32),
+            "bf_build_block_elems": ([P(bf_fio_t), i32], i64),
+            "bf_plan_build_fio": ([P(bf_fio_t), ctypes.c_int, i64, i64, P(vp)], i32),
+        }
+        for name, (args, res) in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        if L.bf_abi_version() != BF_ABI_VERSION:
+            raise ImportError("libbfapply.so ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise BFError(status, lib().bf_last_error().decode())
+
+
+def fio(kernel: int, amp: int, log2n: int, log2leaf: int, rank: int) -> bf_fio_t:
+    return bf_fio_t(BF_ABI_VERSION, kernel, amp, log2n, log2leaf, rank)
+
+
+def fio_of(w) -> bf_fio_t:
+    """bf_fio_t of a workloads.Workload."""
+    return fio(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank)
+
+
+def build_amp(k: bf_fio_t):
+    """(a, b) complex64 [n_amp][N] from the host builder."""
+    na = lib().bf_build_n_amp(k.amp)
+    if na < 1:
+        raise BFError(1, f"unknown amplitude id {k.amp}")
+    n = 1 << k.log2n
+    a = np.zeros((na, n), np.complex64)
+    b = np.zeros((na, n), np.complex64)
+    _check(lib().bf_build_amp(ctypes.byref(k), a.ctypes.data, b.ctypes.data))
+    return a, b
+
+
+def build_blocks(k: bf_fio_t, stage: int, begin: int, count: int) -> np.ndarray:
+    """count blocks of `stage` from the host builder, complex64, each flattened (bf.h layouts)."""
+    e = lib().bf_build_block_elems(ctypes.byref(k), stage)
+    if e <= 0:
+        raise ValueError("bad stage")
+    out = np.zeros((count, e), np.complex64)
+    _check(lib().bf_build_blocks(ctypes.byref(k), stage, begin, count, out.ctypes.data))
+    return out
+
+
+def _ptr(x) -> int:
+    """Device/host pointer of a torch tensor, numpy array or raw int."""
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Plan:
+    """Owns a bf_plan_t."""
+
+    def __init__(self, handle: int):
+        self._h = ctypes.c_void_p(handle)
+
+    # -- construction ------------------------------------------------------------
+    @classmethod
+    def build_fio(cls, k: bf_fio_t, device: int = 0, max_nrhs_chunk: int = 1, staging_bytes: int = 256 << 20):
+        """Host builder -> streaming upload -> finalized plan (bf_plan_build_fio)."""
+        h = ctypes.c_void_p()
+        _check(lib().bf_plan_build_fio(ctypes.byref(k), device, max_nrhs_chunk, staging_bytes, ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_arrays(cls, log2n, log2leaf, rank, amp_a, amp_b, v0, xfer, sw, u, device=0, max_nrhs_chunk=1,
+                    memory=BF_MEM_HOST):
+        """bf_plan_create from complete factor arrays (numpy complex64 host arrays or device tensors)."""
+        xs = (ctypes.c_void_p * max(1, len(xfer)))(*[_ptr(x) for x in xfer])
+        d = bf_desc_t(BF_ABI_VERSION, log2n, log2leaf, rank, amp_a.shape[0], memory, _ptr(amp_a), _ptr(amp_b),
+                      _ptr(v0), ctypes.cast(xs, ctypes.POINTER(ctypes.c_void_p)), _ptr(sw), _ptr(u))
+        h = ctypes.c_void_p()
+        _check(lib().bf_plan_create(ctypes.byref(d), device, max_nrhs_chunk, ctypes.byref(h)))
+        return cls(h.value)
+
+    # -- apply ---------------------------------------------------------------------
+    def apply(self, F, G, nrhs: int, stream=None):
+        """G = sum_k a_k o BF(b_k o F) on device buffers (N x nrhs column-major, ld = N)."""
+        _check(lib().bf_apply(self._h, _ptr(F), _ptr(G), nrhs, _stream(stream)))
+
+    def apply_ex(self, F, ldf, G, ldg, nrhs, workspace=None, workspace_bytes=0, stream=None):
+        _check(lib().bf_apply_ex(self._h, _ptr(F), ldf, _ptr(G), ldg, nrhs,
+                                 None if workspace is None else _ptr(workspace), workspace_bytes, _stream(stream)))
+
+    def apply_host(self, F_host, G_host, nrhs: int, stream=None):
+        """End to end with host buffers (copies inside the call)."""
+        _check(lib().bf_apply_host(self._h, _ptr(F_host), _ptr(G_host), nrhs, _stream(stream)))
+
+    # -- introspection -------------------------------------------------------------
+    def info(self) -> dict:
+        i = bf_plan_info_t()
+        _check(lib().bf_plan_get_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in bf_plan_info_t._fields_}
+
+    def workspace_bytes(self, nrhs_chunk: int) -> int:
+        return int(lib().bf_workspace_bytes(self._h, nrhs_chunk))
+
+    def set_timing(self, enable: bool):
+        _check(lib().bf_plan_set_timing(self._h, int(enable)))
+
+    def timing(self):
+        ms = (ctypes.c_double * BF_NUM_KCLASS)()
+        n = (ctypes.c_int64 * BF_NUM_KCLASS)()
+        _check(lib().bf_plan_timing(self._h, ms, n))
+        return {KCLASS_NAMES[i]: (ms[i], n[i]) for i in range(BF_NUM_KCLASS)}
+
+    def destroy(self):
+        if self._h is not None and self._h.value:
+            _check(lib().bf_plan_destroy(self._h))
+        self._h = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                lib().bf_plan_destroy(self._h)
+        except Exception:
+            pass

@@ -1,0 +1,393 @@
+// bf_build.cpp -- host-side (untimed) FP64 construction of the IBF-MAT factors
+// (include/bf_build.h).  Independent of the oracle: every block is assembled in
+// the factored form of Algorithm 2 (eqn:ab1/eqn:ab2),
+//     block = diag(row phases) . (Lagrange matrix shared by the level) . diag(column phases),
+// because the Mock-Chebyshev grids of one level are translates of each other
+// (eqn:gdA/gdB: "we can simply shift the grid points").
+#include <cuda_runtime.h>
+#include <omp.h>
+
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <vector>
+
+#include "../../include/bf.h"
+#include "../../include/bf_build.h"
+#include "bf_plan_internal.h"
+
+namespace {
+
+using cd = std::complex<double>;
+
+struct Shape {
+    int kernel, amp, LN, l0, r, D, h;
+    int64_t N, n0;
+};
+
+bool make_shape(const bf_fio_t* k, Shape* s)
+{
+    if (!k || k->abi_version != BF_ABI_VERSION) return false;
+    if (k->kernel < 0 || k->kernel > 3 || bf_build_n_amp(k->amp) < 1) return false;
+    if (k->log2n < 2 || k->log2n > 30 || k->log2n % 2 || k->log2leaf < 1 || 2 * k->log2leaf > k->log2n) return false;
+    if (k->rank < 2 || k->rank > 64 || k->rank > (1 << k->log2leaf)) return false;
+    s->kernel = k->kernel;
+    s->amp = k->amp;
+    s->LN = k->log2n;
+    s->l0 = k->log2leaf;
+    s->r = k->rank;
+    s->N = int64_t(1) << s->LN;
+    s->n0 = int64_t(1) << s->l0;
+    s->D = s->LN - s->l0;
+    s->h = s->LN / 2;
+    return true;
+}
+
+// c(x) of Phi(x, xi) = x xi + c(x)|xi|  (BASELINE configs); cfg3 builds the BF on this smooth part.
+inline double cfun(int kernel, double x)
+{
+    if (kernel == BF_KERNEL_DFT) return 0.0;
+    const double amp = (kernel == BF_KERNEL_FIO_PAPER) ? 0.2 : 1.0;
+    return (2.0 + amp * std::sin(2.0 * M_PI * x)) / 16.0;
+}
+
+// e^{sgn 2 pi i Phi(x_i, xi_j)}, Phi reduced mod 1 first: the x xi = i (j - N/2)/N part exactly in integers.
+inline cd expphi(const Shape& S, int64_t i, int64_t j, double sgn)
+{
+    const int64_t xi = j - S.N / 2;
+    const int64_t m = (i * xi) & (S.N - 1);   // two's complement: i xi mod N in [0, N)
+    double f = std::ldexp(double(m), -S.LN);
+    const double t = cfun(S.kernel, std::ldexp(double(i), -S.LN)) * double(xi < 0 ? -xi : xi);
+    f += t - std::floor(t);
+    f -= std::floor(f);
+    double sn, cs;
+    sincos(2.0 * M_PI * f, &sn, &cs);
+    return cd(cs, sgn * sn);
+}
+
+// Mock-Chebyshev nodes of a block of n indices, relative to its first index: eqn:gdA with z_t ascending
+// (DESIGN R2) and Round half away from zero (R3).  The expression is evaluated exactly as written so
+// that exact .5 ties are decided by the same IEEE arithmetic everywhere.
+std::vector<int64_t> nodes(int64_t n, int r)
+{
+    std::vector<int64_t> g(r);
+    for (int t = 1; t <= r; t++) g[t - 1] = int64_t(std::llround(t + (n - r) * (0.5 - 0.5 * std::cos((t - 1) * M_PI / (r - 1))))) - 1;
+    return g;
+}
+
+// Lagrange basis M_t(q) on nodes g.
+inline double lag(const std::vector<int64_t>& g, int t, double q)
+{
+    double v = 1.0;
+    for (size_t j = 0; j < g.size(); j++)
+        if (int(j) != t) v *= (q - double(g[j])) / double(g[t] - g[j]);
+    return v;
+}
+
+inline int64_t mid(int64_t lo, int64_t n) { return lo + (n - 1) / 2; }   // center, ties low (R4)
+
+inline bf_c64 c64(cd z) { return bf_c64{float(z.real()), float(z.imag())}; }
+
+int64_t block_elems(const Shape& S, int stage)
+{
+    switch (stage) {
+    case BF_STAGE_V0: return S.r * S.n0;
+    case BF_STAGE_SW: return int64_t(S.r) * S.r;
+    case BF_STAGE_U: return S.n0 * S.r;
+    default:
+        if (stage >= BF_STAGE_XFER0 && stage < BF_STAGE_XFER0 + (S.D - S.l0)) return 2 * int64_t(S.r) * S.r;
+        return 0;
+    }
+}
+
+// V0 (initialization eqn:1): A = A(l0,a), B = B(l0,b) a leaf of n0 columns.
+// block r x n0 column-major: [j][t] = e^{-i..Phi(c_A, xi_t^B)} M_t^B(xi_j) e^{i..Phi(c_A, xi_j)}
+void build_v0(const Shape& S, int64_t p0, int64_t cnt, bf_c64* out)
+{
+    const int r = S.r;
+    const int64_t n0 = S.n0, nleaf = S.N >> S.l0, nA = S.N >> S.l0;
+    const auto g = nodes(n0, r);
+    std::vector<double> L(r * n0);
+    for (int t = 0; t < r; t++)
+        for (int64_t j = 0; j < n0; j++) L[t * n0 + j] = lag(g, t, double(j));
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < cnt; q++) {
+        const int64_t p = p0 + q, a = p / nleaf, b = p % nleaf;
+        const int64_t cA = mid(a * nA, nA), loB = b * n0;
+        cd rowp[64], colp[128];
+        for (int t = 0; t < r; t++) rowp[t] = expphi(S, cA, loB + g[t], -1.0);
+        for (int64_t j = 0; j < n0; j++) colp[j] = expphi(S, cA, loB + j, +1.0);
+        bf_c64* o = out + q * r * n0;
+        for (int64_t j = 0; j < n0; j++)
+            for (int t = 0; t < r; t++) o[j * r + t] = c64(rowp[t] * L[t * n0 + j] * colp[j]);
+    }
+}
+
+// Transfer level l, first half (eqn:2): A = A(l,a), B = B(l,b), C_c = B(l-1, 2b+c).
+// block r x 2r column-major: [(c r + s)][t] = e^{-..Phi(c_A, xi_t^B)} M_t^B(xi_s^{C_c}) e^{..Phi(c_A, xi_s^{C_c})}
+// Second half (eqn:3): P = A(l-1, a>>1):
+// [(c r + s)][t] = e^{..Phi(x_t^A, c_{C_c})} M_s^P(x_t^A) e^{-..Phi(x_s^P, c_{C_c})}
+void build_xfer(const Shape& S, int l, int64_t p0, int64_t cnt, bf_c64* out)
+{
+    const int r = S.r;
+    const int sh = S.LN - l;
+    const int64_t nB = int64_t(1) << l, nC = nB / 2;   // |B(l,.)|, |B(l-1,.)|
+    const int64_t nA = S.N >> l, nP = nA * 2;          // |A(l,.)|, |A(l-1,.)|
+    if (l <= S.h) {
+        const auto gB = nodes(nB, r), gC = nodes(nC, r);
+        std::vector<double> L(r * 2 * r);   // [t][c r + s], relative to B's first index
+        for (int t = 0; t < r; t++)
+            for (int c = 0; c < 2; c++)
+                for (int s = 0; s < r; s++) L[t * 2 * r + c * r + s] = lag(gB, t, double(c * nC + gC[s]));
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < cnt; q++) {
+            const int64_t p = p0 + q, a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
+            const int64_t cA = mid(a * nA, nA), loB = b * nB;
+            cd rowp[64], colp[128];
+            for (int t = 0; t < r; t++) rowp[t] = expphi(S, cA, loB + gB[t], -1.0);
+            for (int c = 0; c < 2; c++)
+                for (int s = 0; s < r; s++) colp[c * r + s] = expphi(S, cA, loB + c * nC + gC[s], +1.0);
+            bf_c64* o = out + q * 2 * r * r;
+            for (int k = 0; k < 2 * r; k++)
+                for (int t = 0; t < r; t++) o[k * r + t] = c64(rowp[t] * L[t * 2 * r + k] * colp[k]);
+        }
+    } else {
+        const auto gA = nodes(nA, r), gP = nodes(nP, r);
+        std::vector<double> L(2 * r * r);   // [e][t][s] = M_s^P(x_t^A), A the e-th child of P
+        for (int e = 0; e < 2; e++)
+            for (int t = 0; t < r; t++)
+                for (int s = 0; s < r; s++) L[(e * r + t) * r + s] = lag(gP, s, double(e * nA + gA[t]));
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < cnt; q++) {
+            const int64_t p = p0 + q, a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
+            const int64_t loA = a * nA, loP = (a >> 1) * nP;
+            const int e = int(a & 1);
+            bf_c64* o = out + q * 2 * r * r;
+            for (int c = 0; c < 2; c++) {
+                const int64_t cC = mid((2 * b + c) * nC, nC);
+                cd rowp[64], colp[64];
+                for (int t = 0; t < r; t++) rowp[t] = expphi(S, loA + gA[t], cC, +1.0);
+                for (int s = 0; s < r; s++) colp[s] = expphi(S, loP + gP[s], cC, -1.0);
+                for (int s = 0; s < r; s++)
+                    for (int t = 0; t < r; t++)
+                        o[(c * r + s) * r + t] = c64(rowp[t] * L[(e * r + t) * r + s] * colp[s]);
+            }
+        }
+    }
+}
+
+// Switch: A = A(h,a), B = B(h,b); block r x r column-major: [s][t] = e^{..Phi(x_t^A, xi_s^B)}
+void build_sw(const Shape& S, int64_t p0, int64_t cnt, bf_c64* out)
+{
+    const int r = S.r, sh = S.LN - S.h;
+    const int64_t nA = S.N >> S.h, nB = int64_t(1) << S.h;
+    const auto gA = nodes(nA, r), gB = nodes(nB, r);
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < cnt; q++) {
+        const int64_t p = p0 + q, a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
+        bf_c64* o = out + q * r * r;
+        for (int s = 0; s < r; s++)
+            for (int t = 0; t < r; t++) o[s * r + t] = c64(expphi(S, a * nA + gA[t], b * nB + gB[s], +1.0));
+    }
+}
+
+// U (termination eqn:bf3): A = A(D,a) a leaf of n0 rows, B = B(D,b), b < n0.
+// block n0 x r column-major: [t][j] = e^{..Phi(x_j, c_B)} M_t^A(x_j) e^{-..Phi(x_t^A, c_B)}
+void build_u(const Shape& S, int64_t p0, int64_t cnt, bf_c64* out)
+{
+    const int r = S.r;
+    const int64_t n0 = S.n0, nB = S.N >> S.l0;
+    const auto g = nodes(n0, r);
+    std::vector<double> L(n0 * r);
+    for (int64_t j = 0; j < n0; j++)
+        for (int t = 0; t < r; t++) L[j * r + t] = lag(g, t, double(j));
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < cnt; q++) {
+        const int64_t p = p0 + q, a = p / n0, b = p % n0;
+        const int64_t loA = a * n0, cB = mid(b * nB, nB);
+        cd rowp[128], colp[64];
+        for (int64_t j = 0; j < n0; j++) rowp[j] = expphi(S, loA + j, cB, +1.0);
+        for (int t = 0; t < r; t++) colp[t] = expphi(S, loA + g[t], cB, -1.0);
+        bf_c64* o = out + q * n0 * r;
+        for (int t = 0; t < r; t++)
+            for (int64_t j = 0; j < n0; j++) o[t * n0 + j] = c64(rowp[j] * L[j * r + t] * colp[t]);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t bf_build_n_amp(int32_t amp)
+{
+    switch (amp) {
+    case BF_AMP_ONE: return 1;
+    case BF_AMP_CFG1:
+    case BF_AMP_CFG2: return 2;
+    case BF_AMP_CFG3: return 4;
+    default: return -1;
+    }
+}
+
+int64_t bf_build_block_elems(const bf_fio_t* k, int32_t stage)
+{
+    Shape S;
+    if (!make_shape(k, &S)) return 0;
+    return block_elems(S, stage);
+}
+
+// Amplitude split of DESIGN R11 (jump of cfg3 folded into b_k, R8).
+bf_status_t bf_build_amp(const bf_fio_t* k, bf_c64* amp_a, bf_c64* amp_b)
+{
+    Shape S;
+    if (!make_shape(k, &S) || !amp_a || !amp_b) return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_amp: bad arguments");
+    const int64_t N = S.N;
+    const double Nd = double(N);
+    const int na = bf_build_n_amp(S.amp);
+#pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; n++) {
+        const double x = std::ldexp(double(n), -S.LN), xi = double(n - N / 2);
+        for (int kk = 0; kk < na; kk++) {
+            cd av(1.0, 0.0), bv(1.0, 0.0);
+            switch (S.amp) {
+            case BF_AMP_CFG1:   // alpha = 1 + 0.5 cos(2 pi x) cos(pi xi/N)
+                if (kk == 1) {
+                    av = 0.5 * std::cos(2.0 * M_PI * x);
+                    bv = std::cos(M_PI * xi / Nd);
+                }
+                break;
+            case BF_AMP_CFG2:   // alpha = (1 + 0.3 sin 2 pi x)(1 + 0.3 cos(2 pi xi/N)), held as two terms
+                av = 1.0 + 0.3 * std::sin(2.0 * M_PI * x);
+                if (kk == 1) bv = 0.3 * std::cos(2.0 * M_PI * xi / Nd);
+                break;
+            case BF_AMP_CFG3: {   // alpha = exp(-(x-1/2)^2)(1 + 0.2 sin(4 pi xi/N)) e^{2 pi i 0.25 sign(x-1/3) xi}
+                const double s = (kk < 2) ? 1.0 : -1.0;
+                const double sx = (3 * n > N) ? 1.0 : -1.0;
+                av = (sx == s) ? std::exp(-(x - 0.5) * (x - 0.5)) : 0.0;
+                double jp = 0.25 * s * xi;
+                jp -= std::floor(jp);
+                bv = cd(std::cos(2.0 * M_PI * jp), std::sin(2.0 * M_PI * jp));
+                if (kk % 2 == 1) bv *= 0.2 * std::sin(4.0 * M_PI * xi / Nd);
+                break;
+            }
+            default: break;
+            }
+            amp_a[kk * N + n] = c64(av);
+            amp_b[kk * N + n] = c64(bv);
+        }
+    }
+    return BF_OK;
+}
+
+bf_status_t bf_build_blocks(const bf_fio_t* k, int32_t stage, int64_t block_begin, int64_t block_count, bf_c64* out)
+{
+    Shape S;
+    if (!make_shape(k, &S)) return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_blocks: bad kernel descriptor");
+    if (S.n0 > 64 || S.r > 64) return bfp_fail(BF_ERR_NOT_SUPPORTED, "bf_build_blocks: leaf > 64 or rank > 64");
+    if (block_elems(S, stage) == 0) return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_blocks: bad stage");
+    if (block_begin < 0 || block_count < 0 || block_begin + block_count > S.N || (!out && block_count))
+        return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_blocks: bad block range");
+    switch (stage) {
+    case BF_STAGE_V0: build_v0(S, block_begin, block_count, out); break;
+    case BF_STAGE_SW: build_sw(S, block_begin, block_count, out); break;
+    case BF_STAGE_U: build_u(S, block_begin, block_count, out); break;
+    default: build_xfer(S, S.l0 + 1 + (stage - BF_STAGE_XFER0), block_begin, block_count, out); break;
+    }
+    return BF_OK;
+}
+
+bf_status_t bf_plan_build_fio(const bf_fio_t* k, int device, int64_t max_nrhs_chunk, int64_t staging_bytes,
+                              bf_plan_t* out)
+{
+    Shape S;
+    if (!out) return bfp_fail(BF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!make_shape(k, &S)) return bfp_fail(BF_ERR_INVALID_ARG, "bf_plan_build_fio: bad kernel descriptor");
+    bf_desc_t meta{};
+    meta.abi_version = BF_ABI_VERSION;
+    meta.log2n = S.LN;
+    meta.log2leaf = S.l0;
+    meta.rank = S.r;
+    meta.n_amp = bf_build_n_amp(S.amp);
+    meta.memory = BF_MEM_HOST;
+    bf_plan_t plan = nullptr;
+    bf_status_t st = bf_plan_alloc(&meta, device, max_nrhs_chunk, &plan);
+    if (st != BF_OK) return st;
+
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (staging_bytes < (int64_t(1) << 20)) staging_bytes = int64_t(1) << 20;
+    // two pinned staging slices: build slice i+1 on the host while slice i is copied
+    bf_c64* stage_buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t cs = nullptr;
+    auto cleanup = [&]() {
+        if (cs) cudaStreamSynchronize(cs);
+        for (int i = 0; i < 2; i++) {
+            if (stage_buf[i]) cudaFreeHost(stage_buf[i]);
+            if (ev[i]) cudaEventDestroy(ev[i]);
+        }
+        if (cs) cudaStreamDestroy(cs);
+        if (prev >= 0) cudaSetDevice(prev);
+    };
+    if (cudaMallocHost(reinterpret_cast<void**>(&stage_buf[0]), size_t(staging_bytes)) != cudaSuccess ||
+        cudaMallocHost(reinterpret_cast<void**>(&stage_buf[1]), size_t(staging_bytes)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        cleanup();
+        bf_plan_destroy(plan);
+        return bfp_fail(BF_ERR_OOM, "bf_plan_build_fio: pinned staging allocation failed");
+    }
+    // amplitudes
+    {
+        std::vector<bf_c64> a(size_t(meta.n_amp) * S.N), b(size_t(meta.n_amp) * S.N);
+        bf_build_amp(k, a.data(), b.data());
+        if ((st = bf_plan_upload(plan, BF_STAGE_AMP_A, 0, meta.n_amp, a.data(), BF_MEM_HOST)) != BF_OK ||
+            (st = bf_plan_upload(plan, BF_STAGE_AMP_B, 0, meta.n_amp, b.data(), BF_MEM_HOST)) != BF_OK) {
+            cleanup();
+            bf_plan_destroy(plan);
+            return st;
+        }
+    }
+    std::vector<int> stages = {BF_STAGE_V0, BF_STAGE_SW, BF_STAGE_U};
+    for (int i = 0; i < S.D - S.l0; i++) stages.push_back(BF_STAGE_XFER0 + i);
+    int cur = 0;
+    bool used[2] = {false, false};
+    for (int stage : stages) {
+        const int64_t elems = block_elems(S, stage);
+        const int64_t per = std::max<int64_t>(1, staging_bytes / (elems * int64_t(sizeof(bf_c64))));
+        for (int64_t b0 = 0; b0 < S.N; b0 += per) {
+            const int64_t cnt = std::min(per, S.N - b0);
+            if (used[cur]) cudaEventSynchronize(ev[cur]);   // slice buffer free again
+            bf_build_blocks(k, stage, b0, cnt, stage_buf[cur]);
+            void* dst = nullptr;
+            if ((st = bfp_stage_dst(plan, stage, b0, cnt, &dst)) != BF_OK) {
+                cleanup();
+                bf_plan_destroy(plan);
+                return st;
+            }
+            if (cudaMemcpyAsync(dst, stage_buf[cur], size_t(cnt * elems) * sizeof(bf_c64), cudaMemcpyHostToDevice,
+                                cs) != cudaSuccess) {
+                cudaGetLastError();
+                cleanup();
+                bf_plan_destroy(plan);
+                return bfp_fail(BF_ERR_CUDA, "bf_plan_build_fio: upload failed");
+            }
+            cudaEventRecord(ev[cur], cs);
+            used[cur] = true;
+            cur ^= 1;
+        }
+    }
+    cleanup();
+    if ((st = bf_plan_finalize(plan)) != BF_OK) {
+        bf_plan_destroy(plan);
+        return st;
+    }
+    *out = plan;
+    return BF_OK;
+}
+
+}  // extern "C"
