@@ -94,17 +94,26 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
 
 
-def stage_model(w, nvec):
-    """Algorithmic flops and bytes per launch of each kernel class."""
+def stage_model(w, nvec, info):
+    """Algorithmic flops and bytes per launch of each kernel class.
+    Transfer classes: a launch performs class_levels/class_launches fused levels; each launch reads and
+    writes the coefficient array once; the switch adds r x r per pair."""
     N, n0, r, na, nrhs = w.n, w.leaf, w.rank, w.n_amp, nvec // w.n_amp
     c = 8  # bytes per complex64
-    return {
+    out = {
         "s0": (8 * N * n0 * r * nvec + 6 * N * nvec, c * (N * nrhs + na * N + N * n0 * r + N * r * nvec)),
-        "xfer_first_half": (16 * N * r * r * nvec, c * (2 * N * r * nvec + 2 * N * r * r)),
-        "xfer_switch": (24 * N * r * r * nvec, c * (2 * N * r * nvec + 3 * N * r * r)),
-        "xfer_second_half": (16 * N * r * r * nvec, c * (2 * N * r * nvec + 2 * N * r * r)),
         "sl": (8 * N * n0 * r * nvec + 8 * N * nvec, c * (N * r * nvec + N * n0 * r + na * N + N * nrhs)),
     }
+    for k in ("xfer_first_half", "xfer_switch", "xfer_second_half"):
+        n, lv = info["class_launches"][k], info["class_levels"][k]
+        if n == 0:
+            out[k] = (0, 0)
+            continue
+        sw = 1 if k == "xfer_switch" else 0
+        flops = (lv * 16 * N * r * r * nvec + sw * 8 * N * r * r * nvec) / n
+        byts = c * (2 * N * r * nvec) + c * (lv * 2 * N * r * r + sw * N * r * r) / n
+        out[k] = (flops, byts)
+    return out
 
 
 def cpu_oracle_sample(w):
@@ -157,6 +166,7 @@ def main():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--nrhs", type=int, default=None, help="RHS per rank (default: the config's)")
     ap.add_argument("--chunk", type=int, default=None, help="max_nrhs_chunk (default: all RHS in one chunk)")
+    ap.add_argument("--log2n", type=int, default=None, help="override N (profiling of a smaller instance only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -167,6 +177,8 @@ def main():
     w = W.CONFIGS[args.config]
     if args.nrhs:
         w = w.with_(nrhs=args.nrhs)
+    if args.log2n:
+        w = w.with_(log2n=args.log2n)
 
     if args.impl == "reference":
         run_reference(args, w, rank, world)
@@ -224,8 +236,8 @@ def main():
 
     # ---- roofline of the dominant kernel class ----
     hbm, hbm_src = _peaks()
-    model = stage_model(w, min(chunk, w.nrhs) * w.n_amp)
-    dom = max(ktimes, key=lambda k: ktimes[k][0])
+    model = stage_model(w, min(chunk, w.nrhs) * w.n_amp, info)
+    dom = max(ktimes, key=lambda k: ktimes[k][0])   # largest share of the timed region
     dms, dn = ktimes[dom]
     flops, byts = model[dom]
     avg_s = dms / dn / 1e3

@@ -110,8 +110,10 @@ typedef struct {
     int64_t max_nrhs_chunk;
     int64_t factor_bytes;        /* device bytes of all factor + amplitude arrays */
     int64_t workspace_bytes;     /* device bytes of the plan-owned coefficient workspace */
-    int32_t launches_per_chunk;  /* kernels one RHS chunk of bf_apply launches */
+    int32_t launches_per_chunk;  /* kernels one full RHS chunk (max_nrhs_chunk columns) launches */
     int32_t device;
+    int32_t class_launches[5];   /* per kernel class (see bf_plan_timing): launches per full chunk */
+    int32_t class_levels[5];     /* per kernel class: transfer levels those launches perform */
 } bf_plan_info_t;
 
 /* Create a plan on `device` from complete factor arrays.  The plan deep-copies

@@ -50,7 +50,8 @@ class bf_plan_info_t(ctypes.Structure):
                 ("n_amp", ctypes.c_int32), ("switch_level", ctypes.c_int32), ("n_xfer", ctypes.c_int32),
                 ("n", ctypes.c_int64), ("max_nrhs_chunk", ctypes.c_int64), ("factor_bytes", ctypes.c_int64),
                 ("workspace_bytes", ctypes.c_int64), ("launches_per_chunk", ctypes.c_int32),
-                ("device", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("class_launches", ctypes.c_int32 * 5),
+                ("class_levels", ctypes.c_int32 * 5)]
 
 
 class bf_fio_t(ctypes.Structure):
@@ -197,7 +198,10 @@ class Plan:
     def info(self) -> dict:
         i = bf_plan_info_t()
         _check(lib().bf_plan_get_info(self._h, ctypes.byref(i)))
-        return {f: getattr(i, f) for f, _ in bf_plan_info_t._fields_}
+        out = {f: getattr(i, f) for f, _ in bf_plan_info_t._fields_}
+        out["class_launches"] = dict(zip(KCLASS_NAMES, list(i.class_launches)))
+        out["class_levels"] = dict(zip(KCLASS_NAMES, list(i.class_levels)))
+        return out
 
     def workspace_bytes(self, nrhs_chunk: int) -> int:
         return int(lib().bf_workspace_bytes(self._h, nrhs_chunk))

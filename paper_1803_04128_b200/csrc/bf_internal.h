@@ -26,6 +26,12 @@ cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2*
 cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, const float2* Sw,
                         int nv, cudaStream_t s);
 
+// Band of K (1 or 2) transfer levels l_first .. l_first+K-1 fused in shared memory; W[m] are the
+// weights of level l_first+m; with m_sw in 1..K the switch Sw is applied after band level m_sw.
+bool band_supported(int R, int nv);
+cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W,
+                        const float2* Sw, int m_sw, int nv, cudaStream_t s);
+
 // Switch alone (used when no transfer level precedes it, h == l0).
 cudaError_t launch_switch(const Dims& d, const float2* in, float2* out, const float2* Sw, int nv, cudaStream_t s);
 

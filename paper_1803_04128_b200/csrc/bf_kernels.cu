@@ -247,6 +247,180 @@ __global__ void __launch_bounds__(128) switch_kernel(const float2* __restrict__ 
     for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, res[t]);
 }
 
+
+// ---------------------------------------------------------------------------
+// Band: K consecutive transfer levels fused in one CTA (SURVEY 8(a) "fusion
+// geometry").  A group of 2^K pairs closed under K levels -- fixed a0 at the
+// input level l_first-1 and 2^K consecutive b's -- is loaded once per vector
+// tile into shared memory (cp.async), carried through the K levels in place,
+// and only the last level is written to HBM: the coefficient traffic of the
+// band is one read + one write instead of K of each.  The weights of all K
+// levels (and the switch blocks when the band contains level h) stay resident
+// in shared memory while the CTA sweeps the vector tiles.
+//
+// In place: at band level m the unit (e', i) reads the physical slots
+// phi_{m-1}(e', 2i+c) = (2i+c) 2^(m-1) + bitrev_{m-1}(e') and writes its two
+// outputs back into the same two slots (phi_m(E, i) = i 2^m + bitrev_m(E)), so
+// a thread only ever touches its own (slot, vector) cells within a level and
+// one barrier per level suffices.
+// ---------------------------------------------------------------------------
+struct BandArgs {
+    const float2* W[4];   // weights of band levels 1..K (bf.h XFER layout)
+    const float2* Sw;     // switch blocks (level h), used when m_sw > 0
+    int m_sw;             // band level after which the switch is applied (1..K), 0 = none
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int K>
+__host__ __device__ constexpr int band_vt() { return (256 >> (K - 1)) * 2; }
+
+template <int R, int K>
+__host__ __device__ constexpr size_t band_smem_bytes()
+{
+    return (size_t((1 << K) * R * band_vt<K>()) + size_t(K * (1 << (K - 1)) * 4 * R * R) + size_t((1 << K) * R * R)) *
+           sizeof(float2);
+}
+
+template <int R, int K>
+__global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
+    band_kernel(const float2* __restrict__ in, float2* __restrict__ out, const BandArgs args, int LN, int l_first, int nv)
+{
+    constexpr int TN = 2;
+    constexpr int U = 1 << (K - 1);   // butterfly units per level
+    constexpr int P = 1 << K;         // pairs per group
+    constexpr int COLS = 256 / U;     // thread columns per unit
+    constexpr int VT = COLS * TN;     // vectors per tile
+    extern __shared__ float4 smem_band[];
+    float2* X = reinterpret_cast<float2*>(smem_band);   // [P][R][VT]
+    float2* Ws = X + P * R * VT;                         // [K][U][2R (k)][2R (e R + t)]
+    float2* Ss = Ws + K * U * 4 * R * R;                 // [P (E 2^(K-m_sw) + i)][R (s)][R (t)]
+
+    const int lin = l_first - 1;   // input level
+    const int shg = LN - lin - K;
+    const int64_t g = blockIdx.x;
+    const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+    const int tid = threadIdx.x;
+    const int u = tid / COLS, col = tid % COLS;
+
+#pragma unroll
+    for (int m = 1; m <= K; m++) {
+        const int sh = LN - lin - m;   // log2 of the b-range at level lin + m
+        for (int idx = tid; idx < U * 4 * R * R; idx += 256) {
+            const int t = idx % R, k = (idx / R) % (2 * R), e = (idx / (2 * R * R)) & 1, uu = idx / (4 * R * R);
+            const int ep = uu >> (K - m), i = uu & ((1 << (K - m)) - 1);
+            const int64_t p = (((a0 << m) + 2 * ep + e) << sh) + (bq << (K - m)) + i;
+            Ws[(((m - 1) * U + uu) * 2 * R + k) * 2 * R + e * R + t] = __ldg(args.W[m - 1] + p * 2 * R * R + k * R + t);
+        }
+    }
+    if (args.m_sw) {
+        const int m = args.m_sw, sh = LN - lin - m, ilog = K - m;
+        for (int idx = tid; idx < P * R * R; idx += 256) {
+            const int q = idx / (R * R), st = idx % (R * R);
+            const int E = q >> ilog, i = q & ((1 << ilog) - 1);
+            const int64_t p = (((a0 << m) + E) << sh) + (bq << ilog) + i;
+            Ss[idx] = __ldg(args.Sw + p * R * R + st);
+        }
+    }
+
+    const int nvt = (nv + VT - 1) / VT;
+    for (int vt = 0; vt < nvt; vt++) {
+        const int v0 = vt * VT;
+        const int vw = min(VT, nv - v0);
+        __syncthreads();   // the previous tile is consumed; weights are in place
+        const float2* src = in + (g * P) * R * int64_t(nv) + v0;
+        for (int idx = tid; idx < P * R * (VT / 2); idx += 256) {
+            const int vv = (idx % (VT / 2)) * 2, row = idx / (VT / 2);
+            if (vv < vw) cp_async16(X + row * VT + vv, src + int64_t(row) * nv + vv);
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+
+        const bool active = col * TN < vw;
+#pragma unroll
+        for (int m = 1; m <= K; m++) {
+            const int ep = u >> (K - m), i = u & ((1 << (K - m)) - 1);
+            const int br = (m > 1) ? int(__brev(unsigned(ep)) >> (33 - m)) : 0;
+            const int s0 = (2 * i) * (1 << (m - 1)) + br, s1 = s0 + (1 << (m - 1));
+            float2 acc[2][R][TN];
+#pragma unroll
+            for (int e = 0; e < 2; e++)
+#pragma unroll
+                for (int t = 0; t < R; t++)
+#pragma unroll
+                    for (int q = 0; q < TN; q++) acc[e][t][q] = make_float2(0.f, 0.f);
+            if (active) {
+                const float2* W = Ws + ((m - 1) * U + u) * 4 * R * R;
+#pragma unroll
+                for (int k = 0; k < 2 * R; k++) {
+                    const int s = (k < R) ? s0 : s1;
+                    float2 x[TN], w[R];
+                    ldc<TN>(x, X + (s * R + (k % R)) * VT + col * TN);
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        ldc<R>(w, W + k * 2 * R + e * R);
+#pragma unroll
+                        for (int t = 0; t < R; t++)
+#pragma unroll
+                            for (int q = 0; q < TN; q++) cmac(acc[e][t][q], w[t], x[q]);
+                    }
+                }
+                if (m == args.m_sw) {   // switch on the two level-h pairs this thread holds
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        const float2* S = Ss + (((2 * ep + e) << (K - m)) + i) * R * R;
+                        float2 res[R][TN];
+#pragma unroll
+                        for (int t = 0; t < R; t++)
+#pragma unroll
+                            for (int q = 0; q < TN; q++) res[t][q] = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int ss = 0; ss < R; ss++) {
+                            float2 w[R];
+                            ldc<R>(w, S + ss * R);
+#pragma unroll
+                            for (int t = 0; t < R; t++)
+#pragma unroll
+                                for (int q = 0; q < TN; q++) cmac(res[t][q], w[t], acc[e][ss][q]);
+                        }
+#pragma unroll
+                        for (int t = 0; t < R; t++)
+#pragma unroll
+                            for (int q = 0; q < TN; q++) acc[e][t][q] = res[t][q];
+                    }
+                }
+            }
+            if (m < K) {
+                if (active) {
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        const int s = e ? s1 : s0;
+#pragma unroll
+                        for (int t = 0; t < R; t++) stc<TN>(X + (s * R + t) * VT + col * TN, acc[e][t]);
+                    }
+                }
+                __syncthreads();
+            } else if (active) {
+                const int sho = LN - lin - K;
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const int64_t p = (((a0 << K) + 2 * ep + e) << sho) + bq;
+                    float2* o = out + p * R * int64_t(nv) + v0 + col * TN;
+#pragma unroll
+                    for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, acc[e][t]);
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // SL: leaf evaluation (eqn:bf3) + amplitude post-scale and sum over
 // k (eqn:tg).  CTA = 32 columns (T_X leaf a, vector group) x n0/JT
@@ -413,6 +587,50 @@ cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const fl
     if (tn == 4) BF_DISPATCH_R(d.R, (sl_go<RR, 4, 1>(d, in, U, ampa, G, ldg, nv, s)))
     if (tn == 2) BF_DISPATCH_R(d.R, (sl_go<RR, 2, 1>(d, in, U, ampa, G, ldg, nv, s)))
     BF_DISPATCH_R(d.R, (sl_go<RR, 1, 1>(d, in, U, ampa, G, ldg, nv, s)))
+}
+
+
+bool band_supported(int R, int nv) { return (R == 6 || R == 8 || R == 10 || R == 12) && nv % 2 == 0 && nv >= 128; }
+
+template <int R, int K>
+static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W,
+                           const float2* Sw, int m_sw, int nv, cudaStream_t s)
+{
+    BandArgs a{};
+    for (int m = 0; m < K; m++) a.W[m] = W[m];
+    a.Sw = Sw;
+    a.m_sw = m_sw;
+    const size_t shm = band_smem_bytes<R, K>();
+    auto kern = band_kernel<R, K>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+    if (e != cudaSuccess) return e;
+    const int64_t groups = d.N >> K;
+    kern<<<unsigned(groups), 256, shm, s>>>(in, out, a, d.LN, l_first, nv);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W,
+                        const float2* Sw, int m_sw, int nv, cudaStream_t s)
+{
+    if (K == 2) {
+        switch (d.R) {
+        case 6: return band_go<6, 2>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+        case 8: return band_go<8, 2>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+        case 10: return band_go<10, 2>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+        case 12: return band_go<12, 2>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+        default: return cudaErrorInvalidValue;
+        }
+    }
+    if (K == 1) {
+        switch (d.R) {
+        case 6: return band_go<6, 1>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+        case 8: return band_go<8, 1>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+        case 10: return band_go<10, 1>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+        case 12: return band_go<12, 1>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+        default: return cudaErrorInvalidValue;
+        }
+    }
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace bfk

@@ -204,6 +204,37 @@ cudaError_t timed(bf_plan_s* p, int cls, cudaStream_t s, F&& launch)
     return e;
 }
 
+// One kernel launch of the apply: what it runs and how it is accounted.
+struct Step {
+    enum Kind { S0, SWITCH, XFER, BAND, SL } kind;
+    int l_first = 0;   // XFER: the level; BAND: first level
+    int K = 1;         // BAND: levels fused
+    int m_sw = 0;      // BAND: band level after which the switch applies (0 = none)
+    int cls = 0;       // bfk::KClass
+    int levels = 0;    // transfer levels this launch performs
+};
+
+// The launch sequence of one RHS chunk of nv vectors: S0, transfer levels l0+1..D (fused in bands of 2
+// when the band kernel supports the shape, the switch applied inside the launch that produces level h),
+// SL.  With no transfer level (h == l0) the switch runs alone after S0.
+std::vector<Step> schedule(const bfk::Dims& d, int nv)
+{
+    std::vector<Step> st;
+    st.push_back({Step::S0, 0, 1, 0, bfk::KC_S0, 0});
+    if (d.h == d.l0) st.push_back({Step::SWITCH, 0, 1, 0, bfk::KC_SWITCH, 0});
+    const bool band = bfk::band_supported(d.R, nv);
+    for (int l = d.l0 + 1; l <= d.D;) {
+        const int K = band ? std::min(2, d.D - l + 1) : 1;
+        const int last = l + K - 1;
+        const int cls = (l <= d.h && d.h <= last) ? bfk::KC_SWITCH : (last < d.h ? bfk::KC_XFER1 : bfk::KC_XFER2);
+        const int m_sw = (l <= d.h && d.h <= last) ? d.h - l + 1 : 0;
+        st.push_back({band ? Step::BAND : Step::XFER, l, K, m_sw, cls, K});
+        l += K;
+    }
+    st.push_back({Step::SL, 0, 1, 0, bfk::KC_SL, 0});
+    return st;
+}
+
 bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, int64_t ldg, int64_t nrhs, float2* ws,
                        cudaStream_t s)
 {
@@ -215,28 +246,25 @@ bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, in
         const int nv = int(nc * d.n_amp);
         float2* cur = ws;
         float2* oth = ws + pair_elems * nv;
-        cudaError_t e = timed(p, bfk::KC_S0, s, [&] {
-            return bfk::launch_s0(d, F + c0 * ldf, ldf, p->amp_b, p->v0, cur, nv, s);
-        });
-        if (e != cudaSuccess) return cuda_fail(e, "S0 launch");
-        if (d.h == d.l0) {
-            e = timed(p, bfk::KC_SWITCH, s, [&] { return bfk::launch_switch(d, cur, oth, p->sw, nv, s); });
-            if (e != cudaSuccess) return cuda_fail(e, "switch launch");
-            std::swap(cur, oth);
-        }
-        for (int l = d.l0 + 1; l <= d.D; l++) {
-            const bool sw = (l == d.h);
-            const int cls = l < d.h ? bfk::KC_XFER1 : (sw ? bfk::KC_SWITCH : bfk::KC_XFER2);
-            e = timed(p, cls, s, [&] {
-                return bfk::launch_xfer(d, l, cur, oth, p->xfer[l - d.l0 - 1], sw ? p->sw : nullptr, nv, s);
+        for (const Step& stp : schedule(d, nv)) {
+            cudaError_t e = timed(p, stp.cls, s, [&]() -> cudaError_t {
+                switch (stp.kind) {
+                case Step::S0: return bfk::launch_s0(d, F + c0 * ldf, ldf, p->amp_b, p->v0, cur, nv, s);
+                case Step::SWITCH: return bfk::launch_switch(d, cur, oth, p->sw, nv, s);
+                case Step::XFER:
+                    return bfk::launch_xfer(d, stp.l_first, cur, oth, p->xfer[stp.l_first - d.l0 - 1],
+                                            stp.l_first == d.h ? p->sw : nullptr, nv, s);
+                case Step::BAND: {
+                    const float2* W[2] = {p->xfer[stp.l_first - d.l0 - 1],
+                                          stp.K > 1 ? p->xfer[stp.l_first - d.l0] : nullptr};
+                    return bfk::launch_band(d, stp.l_first, stp.K, cur, oth, W, p->sw, stp.m_sw, nv, s);
+                }
+                default: return bfk::launch_sl(d, cur, p->u, p->amp_a, G + c0 * ldg, ldg, nv, s);
+                }
             });
-            if (e != cudaSuccess) return cuda_fail(e, "transfer launch");
-            std::swap(cur, oth);
+            if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+            if (stp.kind == Step::SWITCH || stp.kind == Step::XFER || stp.kind == Step::BAND) std::swap(cur, oth);
         }
-        e = timed(p, bfk::KC_SL, s, [&] {
-            return bfk::launch_sl(d, cur, p->u, p->amp_a, G + c0 * ldg, ldg, nv, s);
-        });
-        if (e != cudaSuccess) return cuda_fail(e, "SL launch");
     }
     cudaEventRecord(p->done, s);
     return BF_OK;
@@ -479,7 +507,13 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     info->max_nrhs_chunk = p->max_chunk;
     info->factor_bytes = 8 * (2 * p->d.n_amp * N + 2 * N * r * n0 + N * r * r + int64_t(nx) * N * 2 * r * r);
     info->workspace_bytes = int64_t(p->ws_bytes);
-    info->launches_per_chunk = 2 + nx + (p->d.h == p->d.l0 ? 1 : 0);
+    const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp));
+    info->launches_per_chunk = int32_t(st.size());
+    for (int i = 0; i < BF_NUM_KCLASS; i++) info->class_launches[i] = info->class_levels[i] = 0;
+    for (const auto& x : st) {
+        info->class_launches[x.cls] += 1;
+        info->class_levels[x.cls] += x.levels;
+    }
     info->device = p->device;
     return BF_OK;
 }
