@@ -25,9 +25,10 @@ __device__ __forceinline__ void cmac(float2& acc, const float2 w, const float2 v
     acc.y = fmaf(w.y, v.x, acc.y);
 }
 
+// explicit FMAs: every kernel variant rounds a product the same way (bitwise batch consistency)
 __device__ __forceinline__ float2 cmul(const float2 a, const float2 b)
 {
-    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    return make_float2(fmaf(a.x, b.x, -(a.y * b.y)), fmaf(a.x, b.y, a.y * b.x));
 }
 
 // Load / store K consecutive complex values (16-byte vectors where possible).
@@ -75,6 +76,14 @@ __device__ __forceinline__ void stc(float2* p, const float2 (&v)[K])
         for (int i = 0; i < K; i++) p[i] = v[i];
     }
 }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // S0: amplitude pre-scale + leaf interpolation (eqn:1; eqn:tg P:24-28).
@@ -249,6 +258,217 @@ __global__ void __launch_bounds__(128) switch_kernel(const float2* __restrict__ 
 
 
 // ---------------------------------------------------------------------------
+constexpr int S0T_VT = 128;   // vectors per tile
+constexpr int S0T_AG = 8;     // values of a per chunk (= warps)
+constexpr int S0T_PAD = 2;    // Y row padding (complex) against bank conflicts of the fill
+
+template <int R>
+__host__ __device__ constexpr size_t s0t_smem_bytes(int n0)
+{
+    return (size_t(n0) * (S0T_VT + S0T_PAD) + size_t(2) * S0T_AG * n0 * R) * sizeof(float2);
+}
+
+// ---------------------------------------------------------------------------
+// S0, tiled (large nv): CTA = one leaf b x 128 vectors, looping over all n0 values of a in chunks of 8.
+// Y = b_k o F (n0 x 128) is staged in shared memory once; the V0 blocks of the next chunk of 8 pairs
+// are prefetched with cp.async while the current chunk is computed (double buffer).  Warp w computes
+// pair (a, b), a = 8 chunk + w, for its 128 vectors (lane: 4 consecutive vectors x all R rows), every
+// operand from shared memory (weights: warp-uniform broadcast LDS.128).
+template <int R>
+__global__ void __launch_bounds__(256, 1) s0_tile_kernel(const float2* __restrict__ F, int64_t ldf,
+                                                         const float2* __restrict__ ampb,
+                                                         const float2* __restrict__ V0, float2* __restrict__ out,
+                                                         int LN, int l0, int n_amp, int nv)
+{
+    constexpr int TN = 4, VT = S0T_VT, YS = S0T_VT + S0T_PAD;
+    extern __shared__ float4 smem_s0t[];
+    const int n0 = 1 << l0;
+    float2* Ys = reinterpret_cast<float2*>(smem_s0t);   // [n0][YS]
+    float2* Vs = Ys + n0 * YS;                          // [2][8][n0 (j)][R (t)]
+    const int64_t N = int64_t(1) << LN;
+    const int64_t nleaf = N >> l0;
+    const int64_t b = blockIdx.x;
+    const int v0 = blockIdx.y * VT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nchunk = n0 / S0T_AG;
+    const int blk = n0 * R;   // complex per V0 block
+
+    auto load_v0 = [&](int ch, int buf) {
+        float2* dst = Vs + buf * S0T_AG * blk;
+        for (int idx = tid; idx < S0T_AG * blk / 2; idx += 256) {
+            const int w = idx / (blk / 2), o = idx % (blk / 2);
+            const int64_t p = int64_t(ch * S0T_AG + w) * nleaf + b;
+            cp_async16(dst + w * blk + 2 * o, V0 + p * blk + 2 * o);
+        }
+        cp_async_commit();
+    };
+    load_v0(0, 0);
+    // Y[j][v] = b_k(x) F[x, c],  x = b n0 + j, v = c n_amp + k  (zero beyond nv); 8 loads in flight per thread
+    for (int base = tid; base < n0 * VT; base += 256 * 8) {
+        float2 fv[8], bv[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int idx = base + q * 256;
+            fv[q] = bv[q] = make_float2(0.f, 0.f);
+            const int j = idx % n0, v = v0 + idx / n0;
+            if (idx < n0 * VT && v < nv) {
+                const int c = v / n_amp, k = v - c * n_amp;
+                const int64_t x = b * n0 + j;
+                fv[q] = __ldg(F + x + c * ldf);
+                bv[q] = __ldg(ampb + k * N + x);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int idx = base + q * 256;
+            if (idx < n0 * VT) Ys[(idx % n0) * YS + idx / n0] = cmul(bv[q], fv[q]);
+        }
+    }
+
+    const int v = v0 + lane * TN;
+    for (int ch = 0; ch < nchunk; ch++) {
+        const int buf = ch & 1;
+        if (ch + 1 < nchunk) {
+            load_v0(ch + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            cp_async_wait_all();
+        }
+        __syncthreads();
+        const float2* Vb = Vs + (buf * S0T_AG + warp) * blk;
+        float2 acc[R][TN];
+#pragma unroll
+        for (int t = 0; t < R; t++)
+#pragma unroll
+            for (int i = 0; i < TN; i++) acc[t][i] = make_float2(0.f, 0.f);
+#pragma unroll 2
+        for (int j = 0; j < n0; j++) {
+            float2 y[TN], w[R];
+            ldc<TN>(y, Ys + j * YS + lane * TN);
+            ldc<R>(w, Vb + j * R);
+#pragma unroll
+            for (int t = 0; t < R; t++)
+#pragma unroll
+                for (int i = 0; i < TN; i++) cmac(acc[t][i], w[t], y[i]);
+        }
+        if (v < nv) {   // nv % 4 == 0: a lane's 4 vectors are all valid or all invalid
+            const int64_t p = int64_t(ch * S0T_AG + warp) * nleaf + b;
+            float2* o = out + p * R * nv + v;
+#pragma unroll
+            for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, acc[t]);
+        }
+        __syncthreads();   // buffer `buf` is refilled by the next iteration's prefetch
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SL, tiled (large nv): CTA = one T_X leaf a x 128 vectors, n0/8 warps; warp w
+// owns output rows j in [8w, 8w+8), lane 4 consecutive vectors.  The K = n0 R
+// reduction (b, t) streams through shared memory in chunks of 2 pairs
+// (coefficients [2R][128] and U blocks [2][R][n0]), double-buffered with
+// cp.async.  Epilogue: a_k(x) scaling and the sum over k in registers, then the
+// G tile is transposed through shared memory so each RHS column is written as
+// n0 contiguous complex values.
+// ---------------------------------------------------------------------------
+constexpr int SLT_VT = 128;
+constexpr int SLT_BC = 2;   // pairs per K chunk
+
+template <int R>
+__host__ __device__ constexpr size_t slt_smem_bytes(int n0)
+{
+    return size_t(2) * (size_t(SLT_BC) * R * SLT_VT + size_t(SLT_BC) * R * n0) * sizeof(float2);
+}
+
+template <int R, int NA>
+__global__ void __launch_bounds__(256, 2) sl_tile_kernel(const float2* __restrict__ in, const float2* __restrict__ U,
+                                                         const float2* __restrict__ ampa, float2* __restrict__ G,
+                                                         int64_t ldg, int LN, int l0, int nv)
+{
+    constexpr int TN = 4, JT = 8, VT = SLT_VT, BC = SLT_BC;
+    static_assert(TN % NA == 0, "a thread owns whole RHS columns");
+    extern __shared__ float4 smem_slt[];
+    const int n0 = 1 << l0;
+    float2* Ds = reinterpret_cast<float2*>(smem_slt);   // [2][BC R][VT]
+    float2* Us = Ds + 2 * BC * R * VT;                   // [2][BC][R][n0]
+    const int64_t N = int64_t(1) << LN;
+    const int64_t a = blockIdx.x;
+    const int v0 = blockIdx.y * VT;
+    const int vw = min(VT, nv - v0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    const int j0 = warp * JT;
+
+    auto load_chunk = [&](int ch, int buf) {
+        const int64_t p0 = a * n0 + int64_t(ch) * BC;   // first pair of the chunk (level D)
+        float2* D = Ds + buf * BC * R * VT;
+        for (int idx = tid; idx < BC * R * (VT / 2); idx += nthr) {
+            const int row = idx / (VT / 2), vv = (idx % (VT / 2)) * 2;
+            if (vv < vw) cp_async16(D + row * VT + vv, in + (p0 * R + row) * int64_t(nv) + v0 + vv);
+        }
+        float2* Ub = Us + buf * BC * R * n0;
+        for (int idx = tid; idx < BC * R * n0 / 2; idx += nthr) cp_async16(Ub + 2 * idx, U + p0 * R * n0 + 2 * idx);
+        cp_async_commit();
+    };
+
+    float2 acc[JT][TN];
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+        for (int i = 0; i < TN; i++) acc[jj][i] = make_float2(0.f, 0.f);
+
+    const int nch = n0 / BC;
+    load_chunk(0, 0);
+    for (int ch = 0; ch < nch; ch++) {
+        const int buf = ch & 1;
+        if (ch + 1 < nch) {
+            load_chunk(ch + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            cp_async_wait_all();
+        }
+        __syncthreads();
+        const float2* D = Ds + buf * BC * R * VT + lane * TN;
+        const float2* Ub = Us + buf * BC * R * n0 + j0;
+#pragma unroll 2
+        for (int k = 0; k < BC * R; k++) {
+            float2 xv[TN], w[JT];
+            ldc<TN>(xv, D + k * VT);
+            ldc<JT>(w, Ub + k * n0);
+#pragma unroll
+            for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+                for (int i = 0; i < TN; i++) cmac(acc[jj][i], w[jj], xv[i]);
+        }
+        __syncthreads();   // buffer `buf` is reloaded two chunks later
+    }
+
+    // epilogue: g(x, c) = sum_k a_k(x) u_k(x), staged as Gs[c_local][j] (reuses the chunk buffers)
+    constexpr int CPT = TN / NA;                 // RHS columns per thread
+    constexpr int CT = VT / NA;                  // RHS columns per tile
+    float2* Gs = Ds;                             // [CT][n0 + 1]
+    const int GS = n0 + 1;
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+        const int64_t x = a * n0 + j0 + jj;
+        float2 ak[NA];
+#pragma unroll
+        for (int k = 0; k < NA; k++) ak[k] = __ldg(ampa + k * N + x);
+#pragma unroll
+        for (int cc = 0; cc < CPT; cc++) {
+            float2 g = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < NA; k++) cmac(g, ak[k], acc[jj][cc * NA + k]);
+            Gs[(lane * CPT + cc) * GS + j0 + jj] = g;
+        }
+    }
+    __syncthreads();
+    const int c0 = v0 / NA, cw = vw / NA;
+    for (int idx = tid; idx < CT * n0; idx += nthr) {
+        const int j = idx % n0, cl = idx / n0;
+        if (cl < cw) G[a * n0 + j + int64_t(c0 + cl) * ldg] = Gs[cl * GS + j];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Band: K consecutive transfer levels fused in one CTA (SURVEY 8(a) "fusion
 // geometry").  A group of 2^K pairs closed under K levels -- fixed a0 at the
 // input level l_first-1 and 2^K consecutive b's -- is loaded once per vector
@@ -270,13 +490,6 @@ struct BandArgs {
     int m_sw;             // band level after which the switch is applied (1..K), 0 = none
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
-{
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <int K>
 __host__ __device__ constexpr int band_vt() { return (256 >> (K - 1)) * 2; }
@@ -358,18 +571,22 @@ __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
                     for (int q = 0; q < TN; q++) acc[e][t][q] = make_float2(0.f, 0.f);
             if (active) {
                 const float2* W = Ws + ((m - 1) * U + u) * 4 * R * R;
+#pragma unroll 1
+                for (int c = 0; c < 2; c++) {
+                    const float2* xs = X + (c ? s1 : s0) * R * VT + col * TN;
+                    const float2* wc = W + c * R * 2 * R;
+#pragma unroll 2
+                    for (int k = 0; k < R; k++) {
+                        float2 x[TN], w[R];
+                        ldc<TN>(x, xs + k * VT);
 #pragma unroll
-                for (int k = 0; k < 2 * R; k++) {
-                    const int s = (k < R) ? s0 : s1;
-                    float2 x[TN], w[R];
-                    ldc<TN>(x, X + (s * R + (k % R)) * VT + col * TN);
+                        for (int e = 0; e < 2; e++) {
+                            ldc<R>(w, wc + k * 2 * R + e * R);
 #pragma unroll
-                    for (int e = 0; e < 2; e++) {
-                        ldc<R>(w, W + k * 2 * R + e * R);
+                            for (int t = 0; t < R; t++)
 #pragma unroll
-                        for (int t = 0; t < R; t++)
-#pragma unroll
-                            for (int q = 0; q < TN; q++) cmac(acc[e][t][q], w[t], x[q]);
+                                for (int q = 0; q < TN; q++) cmac(acc[e][t][q], w[t], x[q]);
+                        }
                     }
                 }
                 if (m == args.m_sw) {   // switch on the two level-h pairs this thread holds
@@ -545,9 +762,26 @@ static cudaError_t sl_go(const Dims& d, const float2* in, const float2* U, const
     default: return cudaErrorInvalidValue;                                                                             \
     }
 
+template <int R>
+static cudaError_t s0t_go(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float2* V0,
+                          float2* out, int nv, cudaStream_t s)
+{
+    const int n0 = 1 << d.l0;
+    const size_t shm = s0t_smem_bytes<R>(n0);
+    auto kern = s0_tile_kernel<R>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+    if (e != cudaSuccess) return e;
+    dim3 grid(unsigned(d.N >> d.l0), unsigned((nv + S0T_VT - 1) / S0T_VT));
+    kern<<<grid, 256, shm, s>>>(F, ldf, ampb, V0, out, d.LN, d.l0, d.n_amp, nv);
+    return cudaGetLastError();
+}
+
+static bool tiled_ok(const Dims& d, int nv) { return nv >= 64 && nv % 4 == 0 && d.l0 <= 6; }
+
 cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float2* V0, float2* out,
                       int nv, cudaStream_t s)
 {
+    if (tiled_ok(d, nv)) BF_DISPATCH_R(d.R, (s0t_go<RR>(d, F, ldf, ampb, V0, out, nv, s)))
     const int tn = pick_tn(nv, 4);
     if (tn == 4) BF_DISPATCH_R(d.R, (s0_go<RR, 4>(d, F, ldf, ampb, V0, out, nv, s)))
     if (tn == 2) BF_DISPATCH_R(d.R, (s0_go<RR, 2>(d, F, ldf, ampb, V0, out, nv, s)))
@@ -573,9 +807,30 @@ cudaError_t launch_switch(const Dims& d, const float2* in, float2* out, const fl
     BF_DISPATCH_R(d.R, (sw_go<RR, 1>(d, in, out, Sw, nv, s)))
 }
 
+template <int R, int NA>
+static cudaError_t slt_go(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,
+                          int nv, cudaStream_t s)
+{
+    const int n0 = 1 << d.l0;
+    size_t shm = slt_smem_bytes<R>(n0);
+    const size_t gsb = size_t(SLT_VT / NA) * (n0 + 1) * sizeof(float2);   // epilogue staging reuses the buffers
+    if (gsb > shm) shm = gsb;
+    auto kern = sl_tile_kernel<R, NA>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+    if (e != cudaSuccess) return e;
+    dim3 grid(unsigned(d.N >> d.l0), unsigned((nv + SLT_VT - 1) / SLT_VT));
+    kern<<<grid, 32 * (n0 / 8), shm, s>>>(in, U, ampa, G, ldg, d.LN, d.l0, nv);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,
                       int nv, cudaStream_t s)
 {
+    if (tiled_ok(d, nv)) {
+        if (d.n_amp == 4) BF_DISPATCH_R(d.R, (slt_go<RR, 4>(d, in, U, ampa, G, ldg, nv, s)))
+        if (d.n_amp == 2) BF_DISPATCH_R(d.R, (slt_go<RR, 2>(d, in, U, ampa, G, ldg, nv, s)))
+        BF_DISPATCH_R(d.R, (slt_go<RR, 1>(d, in, U, ampa, G, ldg, nv, s)))
+    }
     // a thread must own whole RHS columns (all n_amp terms of a column): TN % n_amp == 0
     int tn = pick_tn(nv, 4);
     if (tn % d.n_amp != 0) tn = d.n_amp;
@@ -588,7 +843,6 @@ cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const fl
     if (tn == 2) BF_DISPATCH_R(d.R, (sl_go<RR, 2, 1>(d, in, U, ampa, G, ldg, nv, s)))
     BF_DISPATCH_R(d.R, (sl_go<RR, 1, 1>(d, in, U, ampa, G, ldg, nv, s)))
 }
-
 
 bool band_supported(int R, int nv) { return (R == 6 || R == 8 || R == 10 || R == 12) && nv % 2 == 0 && nv >= 128; }
 

@@ -98,6 +98,10 @@ EDGE = [
     (W.K_DFT, W.A_CFG1, 14, 6, 14, 7, 7),          # r = 14, nv = 14
     (W.K_FIO, W.A_CFG1, 16, 6, 10, 8, 8),          # cfg5's shape at reduced N (nv = 16)
     (W.K_FIO, W.A_CFG1, 14, 5, 10, 33, 33),        # nv = 66: multi-tile vector columns + tail
+    (W.K_FIO, W.A_CFG1, 14, 5, 10, 70, 70),        # nv = 140: tiled S0/SL + bands, ragged second vector tile
+    (W.K_FIO_JUMP, W.A_CFG3, 12, 4, 8, 25, 25),    # nv = 100: tiled leaf kernels with leaf 16, n_amp 4
+    (W.K_FIO, W.A_ONE, 14, 6, 12, 132, 132),       # nv = 132, n_amp 1, r = 12 bands
+    (W.K_FIO, W.A_CFG2, 16, 6, 10, 96, 40),        # chunks of 80 + 80 + 32 vectors (tiled, tiled, fallback)
 ]
 
 
