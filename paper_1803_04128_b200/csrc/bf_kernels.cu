@@ -85,6 +85,31 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+
+// A lane's 4 vectors as two 2-vector chunks, HALF apart: every LDS.128/STG.128 instruction of a warp
+// then covers 32 x 16 contiguous bytes (conflict-free, fully coalesced).  pos(i) is the vector offset
+// (within the tile) of the lane's i-th vector.
+template <int HALF>
+__device__ __forceinline__ int qpos(int col, int i) { return (i < 2 ? 0 : HALF) + 2 * col + (i & 1); }
+
+template <int HALF>
+__device__ __forceinline__ void ldq(float2 (&v)[4], const float2* base, int col)
+{
+    float4 a = *reinterpret_cast<const float4*>(base + 2 * col);
+    float4 b = *reinterpret_cast<const float4*>(base + HALF + 2 * col);
+    v[0] = make_float2(a.x, a.y);
+    v[1] = make_float2(a.z, a.w);
+    v[2] = make_float2(b.x, b.y);
+    v[3] = make_float2(b.z, b.w);
+}
+
+template <int HALF>
+__device__ __forceinline__ void stq(float2* base, int col, const float2 (&v)[4], bool lo_ok, bool hi_ok)
+{
+    if (lo_ok) *reinterpret_cast<float4*>(base + 2 * col) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+    if (hi_ok) *reinterpret_cast<float4*>(base + HALF + 2 * col) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+}
+
 // ---------------------------------------------------------------------------
 // S0: amplitude pre-scale + leaf interpolation (eqn:1; eqn:tg P:24-28).
 // CTA = 32 columns (lanes) x 8 warps.  A column is (leaf b, vector group vg).
@@ -265,17 +290,17 @@ constexpr int S0T_PAD = 2;    // Y row padding (complex) against bank conflicts 
 template <int R>
 __host__ __device__ constexpr size_t s0t_smem_bytes(int n0)
 {
-    return (size_t(n0) * (S0T_VT + S0T_PAD) + size_t(2) * S0T_AG * n0 * R) * sizeof(float2);
+    return (size_t(n0) * (S0T_VT + S0T_PAD) + size_t(S0T_AG) * n0 * R) * sizeof(float2);
 }
 
 // ---------------------------------------------------------------------------
 // S0, tiled (large nv): CTA = one leaf b x 128 vectors, looping over all n0 values of a in chunks of 8.
-// Y = b_k o F (n0 x 128) is staged in shared memory once; the V0 blocks of the next chunk of 8 pairs
-// are prefetched with cp.async while the current chunk is computed (double buffer).  Warp w computes
+// Y = b_k o F (n0 x 128) is staged in shared memory once; the V0 blocks of each chunk of 8 pairs are
+// loaded with cp.async (single buffer: two CTAs per SM cover each other's loads).  Warp w computes
 // pair (a, b), a = 8 chunk + w, for its 128 vectors (lane: 4 consecutive vectors x all R rows), every
 // operand from shared memory (weights: warp-uniform broadcast LDS.128).
 template <int R>
-__global__ void __launch_bounds__(256, 1) s0_tile_kernel(const float2* __restrict__ F, int64_t ldf,
+__global__ void __launch_bounds__(256, 2) s0_tile_kernel(const float2* __restrict__ F, int64_t ldf,
                                                          const float2* __restrict__ ampb,
                                                          const float2* __restrict__ V0, float2* __restrict__ out,
                                                          int LN, int l0, int n_amp, int nv)
@@ -284,7 +309,7 @@ __global__ void __launch_bounds__(256, 1) s0_tile_kernel(const float2* __restric
     extern __shared__ float4 smem_s0t[];
     const int n0 = 1 << l0;
     float2* Ys = reinterpret_cast<float2*>(smem_s0t);   // [n0][YS]
-    float2* Vs = Ys + n0 * YS;                          // [2][8][n0 (j)][R (t)]
+    float2* Vs = Ys + n0 * YS;                          // [8][n0 (j)][R (t)]
     const int64_t N = int64_t(1) << LN;
     const int64_t nleaf = N >> l0;
     const int64_t b = blockIdx.x;
@@ -293,8 +318,8 @@ __global__ void __launch_bounds__(256, 1) s0_tile_kernel(const float2* __restric
     const int nchunk = n0 / S0T_AG;
     const int blk = n0 * R;   // complex per V0 block
 
-    auto load_v0 = [&](int ch, int buf) {
-        float2* dst = Vs + buf * S0T_AG * blk;
+    auto load_v0 = [&](int ch) {
+        float2* dst = Vs;
         for (int idx = tid; idx < S0T_AG * blk / 2; idx += 256) {
             const int w = idx / (blk / 2), o = idx % (blk / 2);
             const int64_t p = int64_t(ch * S0T_AG + w) * nleaf + b;
@@ -302,7 +327,7 @@ __global__ void __launch_bounds__(256, 1) s0_tile_kernel(const float2* __restric
         }
         cp_async_commit();
     };
-    load_v0(0, 0);
+    load_v0(0);
     // Y[j][v] = b_k(x) F[x, c],  x = b n0 + j, v = c n_amp + k  (zero beyond nv); 8 loads in flight per thread
     for (int base = tid; base < n0 * VT; base += 256 * 8) {
         float2 fv[8], bv[8];
@@ -325,17 +350,12 @@ __global__ void __launch_bounds__(256, 1) s0_tile_kernel(const float2* __restric
         }
     }
 
-    const int v = v0 + lane * TN;
+    const int v_lo = v0 + 2 * lane, v_hi = v0 + VT / 2 + 2 * lane;   // nv % 4 == 0: chunks all-or-nothing
     for (int ch = 0; ch < nchunk; ch++) {
-        const int buf = ch & 1;
-        if (ch + 1 < nchunk) {
-            load_v0(ch + 1, buf ^ 1);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        } else {
-            cp_async_wait_all();
-        }
+        if (ch > 0) load_v0(ch);
+        cp_async_wait_all();
         __syncthreads();
-        const float2* Vb = Vs + (buf * S0T_AG + warp) * blk;
+        const float2* Vb = Vs + warp * blk;
         float2 acc[R][TN];
 #pragma unroll
         for (int t = 0; t < R; t++)
@@ -344,20 +364,20 @@ __global__ void __launch_bounds__(256, 1) s0_tile_kernel(const float2* __restric
 #pragma unroll 2
         for (int j = 0; j < n0; j++) {
             float2 y[TN], w[R];
-            ldc<TN>(y, Ys + j * YS + lane * TN);
+            ldq<VT / 2>(y, Ys + j * YS, lane);
             ldc<R>(w, Vb + j * R);
 #pragma unroll
             for (int t = 0; t < R; t++)
 #pragma unroll
                 for (int i = 0; i < TN; i++) cmac(acc[t][i], w[t], y[i]);
         }
-        if (v < nv) {   // nv % 4 == 0: a lane's 4 vectors are all valid or all invalid
+        __syncthreads();   // the V0 chunk is consumed: the next iteration refills it
+        {
             const int64_t p = int64_t(ch * S0T_AG + warp) * nleaf + b;
-            float2* o = out + p * R * nv + v;
+            float2* o = out + p * R * nv + v0;
 #pragma unroll
-            for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, acc[t]);
+            for (int t = 0; t < R; t++) stq<VT / 2>(o + int64_t(t) * nv, lane, acc[t], v_lo < nv, v_hi < nv);
         }
-        __syncthreads();   // buffer `buf` is refilled by the next iteration's prefetch
     }
 }
 
@@ -426,12 +446,13 @@ __global__ void __launch_bounds__(256, 2) sl_tile_kernel(const float2* __restric
             cp_async_wait_all();
         }
         __syncthreads();
-        const float2* D = Ds + buf * BC * R * VT + lane * TN;
+        const float2* D = Ds + buf * BC * R * VT;
         const float2* Ub = Us + buf * BC * R * n0 + j0;
 #pragma unroll 2
         for (int k = 0; k < BC * R; k++) {
             float2 xv[TN], w[JT];
-            ldc<TN>(xv, D + k * VT);
+            if constexpr (NA <= 2) ldq<VT / 2>(xv, D + k * VT, lane);
+            else ldc<TN>(xv, D + k * VT + lane * TN);
             ldc<JT>(w, Ub + k * n0);
 #pragma unroll
             for (int jj = 0; jj < JT; jj++)
@@ -441,11 +462,11 @@ __global__ void __launch_bounds__(256, 2) sl_tile_kernel(const float2* __restric
         __syncthreads();   // buffer `buf` is reloaded two chunks later
     }
 
-    // epilogue: g(x, c) = sum_k a_k(x) u_k(x), staged as Gs[c_local][j] (reuses the chunk buffers)
+    // epilogue: g(x, c) = sum_k a_k(x) u_k(x), staged as Gs[j][c_local] (reuses the chunk buffers) so that
+    // each RHS column leaves as n0 contiguous complex values
     constexpr int CPT = TN / NA;                 // RHS columns per thread
     constexpr int CT = VT / NA;                  // RHS columns per tile
-    float2* Gs = Ds;                             // [CT][n0 + 1]
-    const int GS = n0 + 1;
+    float2* Gs = Ds;                             // [n0][CT + 1]
 #pragma unroll
     for (int jj = 0; jj < JT; jj++) {
         const int64_t x = a * n0 + j0 + jj;
@@ -457,14 +478,15 @@ __global__ void __launch_bounds__(256, 2) sl_tile_kernel(const float2* __restric
             float2 g = make_float2(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < NA; k++) cmac(g, ak[k], acc[jj][cc * NA + k]);
-            Gs[(lane * CPT + cc) * GS + j0 + jj] = g;
+            const int cl = (NA <= 2 ? qpos<VT / 2>(lane, cc * NA) : lane * TN + cc * NA) / NA;
+            Gs[(j0 + jj) * (CT + 1) + cl] = g;
         }
     }
     __syncthreads();
     const int c0 = v0 / NA, cw = vw / NA;
     for (int idx = tid; idx < CT * n0; idx += nthr) {
         const int j = idx % n0, cl = idx / n0;
-        if (cl < cw) G[a * n0 + j + int64_t(c0 + cl) * ldg] = Gs[cl * GS + j];
+        if (cl < cw) G[a * n0 + j + int64_t(c0 + cl) * ldg] = Gs[j * (CT + 1) + cl];
     }
 }
 
@@ -492,7 +514,7 @@ struct BandArgs {
 
 
 template <int K>
-__host__ __device__ constexpr int band_vt() { return (256 >> (K - 1)) * 2; }
+__host__ __device__ constexpr int band_vt() { return 1024 >> K; }   // 256 threads = U units x 2 outputs x VT/4
 
 template <int R, int K>
 __host__ __device__ constexpr size_t band_smem_bytes()
@@ -501,15 +523,18 @@ __host__ __device__ constexpr size_t band_smem_bytes()
            sizeof(float2);
 }
 
+// One thread owns ONE output pair (e) of a unit x 4 vectors (R x 4 accumulators: each weight is reused
+// across 4 vectors, each vector element across R rows).  Both threads of a unit read the same two
+// input slots, so the in-place write-back waits for a barrier after the reads.
 template <int R, int K>
 __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
     band_kernel(const float2* __restrict__ in, float2* __restrict__ out, const BandArgs args, int LN, int l_first, int nv)
 {
-    constexpr int TN = 2;
+    constexpr int TN = 4;
     constexpr int U = 1 << (K - 1);   // butterfly units per level
     constexpr int P = 1 << K;         // pairs per group
-    constexpr int COLS = 256 / U;     // thread columns per unit
-    constexpr int VT = COLS * TN;     // vectors per tile
+    constexpr int VT = band_vt<K>();  // vectors per tile
+    constexpr int COLS = VT / TN;     // thread columns per (unit, output)
     extern __shared__ float4 smem_band[];
     float2* X = reinterpret_cast<float2*>(smem_band);   // [P][R][VT]
     float2* Ws = X + P * R * VT;                         // [K][U][2R (k)][2R (e R + t)]
@@ -520,16 +545,16 @@ __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
     const int64_t g = blockIdx.x;
     const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
     const int tid = threadIdx.x;
-    const int u = tid / COLS, col = tid % COLS;
+    const int col = tid % COLS, e = (tid / COLS) & 1, u = tid / (2 * COLS);
 
 #pragma unroll
     for (int m = 1; m <= K; m++) {
         const int sh = LN - lin - m;   // log2 of the b-range at level lin + m
         for (int idx = tid; idx < U * 4 * R * R; idx += 256) {
-            const int t = idx % R, k = (idx / R) % (2 * R), e = (idx / (2 * R * R)) & 1, uu = idx / (4 * R * R);
+            const int t = idx % R, k = (idx / R) % (2 * R), ee = (idx / (2 * R * R)) & 1, uu = idx / (4 * R * R);
             const int ep = uu >> (K - m), i = uu & ((1 << (K - m)) - 1);
-            const int64_t p = (((a0 << m) + 2 * ep + e) << sh) + (bq << (K - m)) + i;
-            Ws[(((m - 1) * U + uu) * 2 * R + k) * 2 * R + e * R + t] = __ldg(args.W[m - 1] + p * 2 * R * R + k * R + t);
+            const int64_t p = (((a0 << m) + 2 * ep + ee) << sh) + (bq << (K - m)) + i;
+            Ws[(((m - 1) * U + uu) * 2 * R + k) * 2 * R + ee * R + t] = __ldg(args.W[m - 1] + p * 2 * R * R + k * R + t);
         }
     }
     if (args.m_sw) {
@@ -556,84 +581,72 @@ __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
         cp_async_wait_all();
         __syncthreads();
 
-        const bool active = col * TN < vw;
-#pragma unroll
+        // vectors {2 col, 2 col + 1} and {VT/2 + 2 col, ...}: each 2-vector chunk is valid or not as a whole
+        const bool lo_ok = 2 * col < vw, hi_ok = VT / 2 + 2 * col < vw, active = lo_ok;
+#pragma unroll 1
         for (int m = 1; m <= K; m++) {
             const int ep = u >> (K - m), i = u & ((1 << (K - m)) - 1);
             const int br = (m > 1) ? int(__brev(unsigned(ep)) >> (33 - m)) : 0;
             const int s0 = (2 * i) * (1 << (m - 1)) + br, s1 = s0 + (1 << (m - 1));
-            float2 acc[2][R][TN];
+            float2 acc[R][TN];
 #pragma unroll
-            for (int e = 0; e < 2; e++)
+            for (int t = 0; t < R; t++)
 #pragma unroll
-                for (int t = 0; t < R; t++)
-#pragma unroll
-                    for (int q = 0; q < TN; q++) acc[e][t][q] = make_float2(0.f, 0.f);
+                for (int q = 0; q < TN; q++) acc[t][q] = make_float2(0.f, 0.f);
             if (active) {
-                const float2* W = Ws + ((m - 1) * U + u) * 4 * R * R;
+                const float2* W = Ws + ((m - 1) * U + u) * 4 * R * R + e * R;
 #pragma unroll 1
                 for (int c = 0; c < 2; c++) {
-                    const float2* xs = X + (c ? s1 : s0) * R * VT + col * TN;
+                    const float2* xs = X + (c ? s1 : s0) * R * VT;
                     const float2* wc = W + c * R * 2 * R;
-#pragma unroll 2
+#pragma unroll 1
                     for (int k = 0; k < R; k++) {
                         float2 x[TN], w[R];
-                        ldc<TN>(x, xs + k * VT);
-#pragma unroll
-                        for (int e = 0; e < 2; e++) {
-                            ldc<R>(w, wc + k * 2 * R + e * R);
-#pragma unroll
-                            for (int t = 0; t < R; t++)
-#pragma unroll
-                                for (int q = 0; q < TN; q++) cmac(acc[e][t][q], w[t], x[q]);
-                        }
-                    }
-                }
-                if (m == args.m_sw) {   // switch on the two level-h pairs this thread holds
-#pragma unroll
-                    for (int e = 0; e < 2; e++) {
-                        const float2* S = Ss + (((2 * ep + e) << (K - m)) + i) * R * R;
-                        float2 res[R][TN];
+                        ldq<VT / 2>(x, xs + k * VT, col);
+                        ldc<R>(w, wc + k * 2 * R);
 #pragma unroll
                         for (int t = 0; t < R; t++)
 #pragma unroll
-                            for (int q = 0; q < TN; q++) res[t][q] = make_float2(0.f, 0.f);
+                            for (int q = 0; q < TN; q++) cmac(acc[t][q], w[t], x[q]);
+                    }
+                }
+            }
+            if (m < K) __syncthreads();   // both outputs of every unit have read the input slots
+            if (active) {
+                // destination of output row t: the thread's own slot (in place) or, at the last level, HBM
+                float2* dst;
+                int64_t rstride;
+                if (m < K) {
+                    dst = X + ((e ? s1 : s0) * R) * VT;
+                    rstride = VT;
+                } else {
+                    const int64_t p = (((a0 << K) + 2 * ep + e) << (LN - lin - K)) + bq;
+                    dst = out + p * R * int64_t(nv) + v0;
+                    rstride = nv;
+                }
+                if (m == args.m_sw) {
+                    // switch on the level-h pair this thread holds, one output row at a time
+                    // (the R x 4 inputs stay in registers; each row is stored as soon as it is formed)
+                    const float2* S = Ss + (((2 * ep + e) << (K - m)) + i) * R * R;
+#pragma unroll
+                    for (int t = 0; t < R; t++) {
+                        float2 res[TN];
+#pragma unroll
+                        for (int q = 0; q < TN; q++) res[q] = make_float2(0.f, 0.f);
 #pragma unroll
                         for (int ss = 0; ss < R; ss++) {
-                            float2 w[R];
-                            ldc<R>(w, S + ss * R);
+                            const float2 w = S[ss * R + t];
 #pragma unroll
-                            for (int t = 0; t < R; t++)
-#pragma unroll
-                                for (int q = 0; q < TN; q++) cmac(res[t][q], w[t], acc[e][ss][q]);
+                            for (int q = 0; q < TN; q++) cmac(res[q], w, acc[ss][q]);
                         }
-#pragma unroll
-                        for (int t = 0; t < R; t++)
-#pragma unroll
-                            for (int q = 0; q < TN; q++) acc[e][t][q] = res[t][q];
+                        stq<VT / 2>(dst + t * rstride, col, res, lo_ok, hi_ok);
                     }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < R; t++) stq<VT / 2>(dst + t * rstride, col, acc[t], lo_ok, hi_ok);
                 }
             }
-            if (m < K) {
-                if (active) {
-#pragma unroll
-                    for (int e = 0; e < 2; e++) {
-                        const int s = e ? s1 : s0;
-#pragma unroll
-                        for (int t = 0; t < R; t++) stc<TN>(X + (s * R + t) * VT + col * TN, acc[e][t]);
-                    }
-                }
-                __syncthreads();
-            } else if (active) {
-                const int sho = LN - lin - K;
-#pragma unroll
-                for (int e = 0; e < 2; e++) {
-                    const int64_t p = (((a0 << K) + 2 * ep + e) << sho) + bq;
-                    float2* o = out + p * R * int64_t(nv) + v0 + col * TN;
-#pragma unroll
-                    for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, acc[e][t]);
-                }
-            }
+            if (m < K) __syncthreads();
         }
     }
 }
@@ -813,7 +826,7 @@ static cudaError_t slt_go(const Dims& d, const float2* in, const float2* U, cons
 {
     const int n0 = 1 << d.l0;
     size_t shm = slt_smem_bytes<R>(n0);
-    const size_t gsb = size_t(SLT_VT / NA) * (n0 + 1) * sizeof(float2);   // epilogue staging reuses the buffers
+    const size_t gsb = size_t(SLT_VT / NA + 1) * n0 * sizeof(float2);   // epilogue staging reuses the buffers
     if (gsb > shm) shm = gsb;
     auto kern = sl_tile_kernel<R, NA>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
@@ -844,7 +857,7 @@ cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const fl
     BF_DISPATCH_R(d.R, (sl_go<RR, 1, 1>(d, in, U, ampa, G, ldg, nv, s)))
 }
 
-bool band_supported(int R, int nv) { return (R == 6 || R == 8 || R == 10 || R == 12) && nv % 2 == 0 && nv >= 128; }
+bool band_supported(int R, int nv) { return (R == 6 || R == 8 || R == 10 || R == 12) && nv % 4 == 0 && nv >= 128; }
 
 template <int R, int K>
 static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W,
