@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--nrhs", type=int, default=None, help="RHS per rank (default: the config's)")
     ap.add_argument("--chunk", type=int, default=None, help="max_nrhs_chunk (default: all RHS in one chunk)")
     ap.add_argument("--log2n", type=int, default=None, help="override N (profiling of a smaller instance only)")
+    ap.add_argument("--index-shard", action="store_true",
+                    help="split ONE batch by index over the ranks (NCCL all-to-all at level h; cfg5's mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -198,11 +200,21 @@ def main():
 
     chunk = args.chunk or w.nrhs
     t0 = time.perf_counter()
-    plan = bf.Plan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=chunk)
+    if args.index_shard:
+        # one batch split by index: rank q owns xi-rows and x-rows [q N/G, (q+1) N/G) (strong scaling)
+        obj = [bf.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        plan = bf.Plan.build_fio_sharded(bf.fio_of(w), rank, world, obj[0], device=local, max_nrhs_chunk=chunk)
+        F = W.rhs(w.n, w.nrhs, w.seed)
+        rows = w.n // world
+        F = np.asfortranarray(F[rank * rows:(rank + 1) * rows])
+    else:
+        plan = bf.Plan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=chunk)
+        # this rank's RHS: columns [rank*nrhs, (rank+1)*nrhs) of the seeded global batch (weak scaling)
+        F = W.rhs(w.n, w.nrhs, w.seed + 1000 * rank)
     t_build = time.perf_counter() - t0
     info = plan.info()
-    # this rank's RHS: columns [rank*nrhs, (rank+1)*nrhs) of the seeded global batch (weak scaling)
-    F = W.rhs(w.n, w.nrhs, w.seed + 1000 * rank)
     Fd = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()
     Gd = torch.empty_like(Fd)
     stream = torch.cuda.current_stream()
@@ -232,12 +244,16 @@ def main():
         ms = float(t.item())
     chunks = -(-w.nrhs // chunk)
     launches = info["launches_per_chunk"] * chunks * args.steps
-    value = w.n * w.nrhs * world / (ms / 1e3)
+    jobs = 1 if args.index_shard else world   # batches processed by the whole job per step
+    value = w.n * w.nrhs * jobs / (ms / 1e3)
 
     # ---- roofline of the dominant kernel class ----
     hbm, hbm_src = _peaks()
-    model = stage_model(w, min(chunk, w.nrhs) * w.n_amp, info)
-    dom = max(ktimes, key=lambda k: ktimes[k][0])   # largest share of the timed region
+    wl = w.with_(log2n=w.log2n - (world.bit_length() - 1)) if args.index_shard else w   # this rank's share
+    model = stage_model(wl, min(chunk, w.nrhs) * w.n_amp, info)
+    # the level-h exchange moves (G-1)/G of the local coefficients out and as much in
+    model["exchange"] = (0, 2 * 8 * wl.n * w.rank * min(chunk, w.nrhs) * w.n_amp * (world - 1) // world)
+    dom = max((k for k in ktimes if k != "exchange"), key=lambda k: ktimes[k][0])   # largest share of the step
     dms, dn = ktimes[dom]
     flops, byts = model[dom]
     avg_s = dms / dn / 1e3
@@ -256,9 +272,9 @@ def main():
     # whole-step roofline fractions (level-by-level and fused), DESIGN.md section 5
     tot_f = sum(model[k][0] * ktimes[k][1] for k in model) / args.steps
     lbl = sum(max(model[k][0] / (FP32_PEAK_TFLOPS * 1e12), model[k][1] / (hbm * 1e9)) * ktimes[k][1]
-              for k in model) / args.steps
+              for k in model if k != "exchange") / args.steps
     fused = max(tot_f / (FP32_PEAK_TFLOPS * 1e12),
-                (16 * w.n * w.nrhs + info["factor_bytes"]) / (hbm * 1e9))
+                (16 * wl.n * w.nrhs + info["factor_bytes"]) / (hbm * 1e9))
 
     # ---- end to end: host buffers through the C ABI (bf_apply_host), copies inside the timed region ----
     e2e = None
@@ -276,8 +292,8 @@ def main():
             t = torch.tensor([te], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        nb = w.n * w.nrhs * 8
-        e2e = {"value": w.n * w.nrhs * world / te, "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+        nb = Fd.numel() * 8
+        e2e = {"value": w.n * w.nrhs * jobs / te, "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
                "ms_per_step": te * 1e3, "steps": ne}
 
     cpu = None
@@ -287,12 +303,15 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if args.index_shard else "weak",
             "vs_baseline": None, "dtype": "c64 (fp32 FFMA)",
             "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel; factors from the host builder)",
             "config": {"workload": args.config, "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
-                       "nrhs_per_gpu": w.nrhs, "global_batch": w.nrhs * world, "max_nrhs_chunk": chunk,
-                       "parallelism": f"rhs-sharded x{world} (no collective)",
+                       "nrhs_per_gpu": w.nrhs if not args.index_shard else w.nrhs,
+                       "global_batch": w.nrhs * jobs, "max_nrhs_chunk": chunk,
+                       "parallelism": (f"index-sharded x{world} (NCCL all-to-all at level h)" if args.index_shard
+                                       else f"rhs-sharded x{world} (no collective)"),
                        "l2": "no flush: the working set (F 2.1 GB, coefficients 43 GB/level, factors 25 GB) "
                              "exceeds the 126 MB L2"},
             "roofline": roof,

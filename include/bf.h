@@ -112,9 +112,18 @@ typedef struct {
     int64_t workspace_bytes;     /* device bytes of the plan-owned coefficient workspace */
     int32_t launches_per_chunk;  /* kernels one full RHS chunk (max_nrhs_chunk columns) launches */
     int32_t device;
-    int32_t class_launches[5];   /* per kernel class (see bf_plan_timing): launches per full chunk */
-    int32_t class_levels[5];     /* per kernel class: transfer levels those launches perform */
+    int32_t class_launches[6];   /* per kernel class (see bf_plan_timing): launches per full chunk */
+    int32_t class_levels[6];     /* per kernel class: transfer levels those launches perform */
+    int32_t world;               /* index shards (1 unless sharded) */
+    int32_t shard_rank;          /* this plan's shard (BF_SHARD_NCCL) */
+    int32_t sharding;            /* BF_SHARD_NONE / BF_SHARD_NCCL / BF_SHARD_EMULATED */
+    int64_t rows_local;          /* rows of F and G bf_apply expects: N, or N/world for BF_SHARD_NCCL */
 } bf_plan_info_t;
+
+/* index sharding modes */
+#define BF_SHARD_NONE 0
+#define BF_SHARD_NCCL 1      /* one shard per process/GPU; the level-h exchange is an NCCL all-to-all */
+#define BF_SHARD_EMULATED 2  /* all `world` shards on one device; the exchange is device copies */
 
 /* Create a plan on `device` from complete factor arrays.  The plan deep-copies
  * every array into device memory it owns (the caller may free its arrays when
@@ -162,14 +171,38 @@ bf_status_t bf_plan_get_info(bf_plan_t plan, bf_plan_info_t *info);
  * of bf_apply is bracketed by CUDA events on the launching stream; bf_plan_timing
  * synchronizes on the last event and returns the accumulated milliseconds and
  * launch counts per kernel class: [0] S0, [1] first-half transfer, [2] switch-fused
- * transfer / switch, [3] second-half transfer, [4] SL.  Arrays have BF_NUM_KCLASS
- * entries.  Enabling resets the accumulators. */
-#define BF_NUM_KCLASS 5
+ * transfer / switch, [3] second-half transfer, [4] SL, [5] level-h exchange (index-
+ * sharded plans).  Arrays have BF_NUM_KCLASS entries.  Enabling resets the accumulators. */
+#define BF_NUM_KCLASS 6
 bf_status_t bf_plan_set_timing(bf_plan_t plan, int32_t enable);
 bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
 
 /* Wait for the plan's outstanding work, then free everything it owns. */
 bf_status_t bf_plan_destroy(bf_plan_t plan);
+
+/* ---- index-sharded plans: one long vector split by index over world = 2^g ranks ----
+ * (no paper passage: the paper is serial.)  Rank q owns the xi-rows
+ * [q N/G, (q+1) N/G) of F (levels l <= h: pairs whose b has top g bits q) and the x-rows
+ * [q N/G, (q+1) N/G) of G (levels l > h: pairs whose a has top g bits q).  The only
+ * communication is one all-to-all of the level-h coefficients (N r nv / G^2 complex per
+ * rank pair), issued by bf_apply on its stream as grouped ncclSend/ncclRecv.
+ * Local factor blocks (desc of bf_plan_create_sharded), each stage in local pair order:
+ *   first-half stages (V0, XFER of levels l <= h, SW): local pair a 2^(LN-l-g) + b_l is
+ *       global pair a 2^(LN-l) + q 2^(LN-l-g) + b_l;
+ *   second-half stages (XFER of levels l > h, U): local pair i is global pair q N/G + i;
+ *   amp_b: b_k on xi-rows [q N/G, (q+1) N/G); amp_a: a_k on x-rows [q N/G, (q+1) N/G).
+ * bf_apply on such a plan takes the LOCAL rows: F and G are (N/G) x nrhs (ld >= N/G).
+ * world = 1 is allowed (no communication).  Requires h - g >= 2 and LN - g >= 2 l0. */
+bf_status_t bf_nccl_get_unique_id(void *id128);   /* 128 bytes, to be broadcast to all ranks */
+bf_status_t bf_plan_alloc_sharded(const bf_desc_t *meta, int device, int64_t max_nrhs_chunk, int32_t rank,
+                                  int32_t world, const void *nccl_unique_id, bf_plan_t *out);
+bf_status_t bf_plan_create_sharded(const bf_desc_t *local, int device, int64_t max_nrhs_chunk, int32_t rank,
+                                   int32_t world, const void *nccl_unique_id, bf_plan_t *out);
+/* Host-only layout query (for tests of the exchange): the N/G global level-h pair indices of rank
+ * `rank` in the order of its send buffer (which = 0), its receive buffer (which = 1), or its
+ * second-half local order (which = 2). */
+bf_status_t bf_shard_pairs(int32_t log2n, int32_t log2leaf, int32_t world, int32_t rank, int32_t which,
+                           int64_t *out);
 
 /* Thread-local description of the last non-OK status ("" if none). */
 const char *bf_last_error(void);

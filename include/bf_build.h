@@ -64,6 +64,18 @@ int64_t bf_build_block_elems(const bf_fio_t *k, int32_t stage);
 bf_status_t bf_plan_build_fio(const bf_fio_t *k, int device, int64_t max_nrhs_chunk, int64_t staging_bytes,
                               bf_plan_t *out);
 
+/* Index-sharded construction (bf.h, "index-sharded plans"): rank `rank` of `world` builds only
+ * its own blocks (1/world of every stage) and joins the NCCL communicator of nccl_unique_id. */
+bf_status_t bf_plan_build_fio_sharded(const bf_fio_t *k, int device, int32_t rank, int32_t world,
+                                      const void *nccl_unique_id, int64_t max_nrhs_chunk, int64_t staging_bytes,
+                                      bf_plan_t *out);
+
+/* All `world` shards of the index-sharded plan on ONE device, the exchange done by device copies
+ * (validation of the sharded path without a multi-GPU box).  bf_apply takes the full N-row F/G and
+ * returns the same result as the unsharded plan. */
+bf_status_t bf_plan_build_fio_emulated(const bf_fio_t *k, int device, int32_t world, int64_t max_nrhs_chunk,
+                                       int64_t staging_bytes, bf_plan_t *out);
+
 #ifdef __cplusplus
 }
 #endif

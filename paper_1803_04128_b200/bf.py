@@ -20,8 +20,9 @@ LIB_PATH = os.path.join(HERE, "libbfapply.so")
 BF_ABI_VERSION = 1
 BF_MEM_HOST, BF_MEM_DEVICE = 0, 1
 BF_STAGE_V0, BF_STAGE_SW, BF_STAGE_U, BF_STAGE_AMP_A, BF_STAGE_AMP_B, BF_STAGE_XFER0 = 0, 1, 2, 3, 4, 16
-BF_NUM_KCLASS = 5
-KCLASS_NAMES = ("s0", "xfer_first_half", "xfer_switch", "xfer_second_half", "sl")
+BF_NUM_KCLASS = 6
+KCLASS_NAMES = ("s0", "xfer_first_half", "xfer_switch", "xfer_second_half", "sl", "exchange")
+BF_SHARD_NONE, BF_SHARD_NCCL, BF_SHARD_EMULATED = 0, 1, 2
 STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALIGNMENT", 4: "BF_ERR_OOM",
           5: "BF_ERR_CUDA", 6: "BF_ERR_NCCL", 7: "BF_ERR_NOT_SUPPORTED", 8: "BF_ERR_STATE"}
 
@@ -29,7 +30,8 @@ STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALI
 EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finalize", "bf_apply", "bf_apply_ex",
            "bf_apply_host", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing",
            "bf_plan_destroy", "bf_last_error", "bf_abi_version", "bf_build_n_amp", "bf_build_amp", "bf_build_blocks",
-           "bf_build_block_elems", "bf_plan_build_fio")
+           "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
+           "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated")
 
 
 class BFError(RuntimeError):
@@ -50,8 +52,9 @@ class bf_plan_info_t(ctypes.Structure):
                 ("n_amp", ctypes.c_int32), ("switch_level", ctypes.c_int32), ("n_xfer", ctypes.c_int32),
                 ("n", ctypes.c_int64), ("max_nrhs_chunk", ctypes.c_int64), ("factor_bytes", ctypes.c_int64),
                 ("workspace_bytes", ctypes.c_int64), ("launches_per_chunk", ctypes.c_int32),
-                ("device", ctypes.c_int32), ("class_launches", ctypes.c_int32 * 5),
-                ("class_levels", ctypes.c_int32 * 5)]
+                ("device", ctypes.c_int32), ("class_launches", ctypes.c_int32 * 6),
+                ("class_levels", ctypes.c_int32 * 6), ("world", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
+                ("sharding", ctypes.c_int32), ("rows_local", ctypes.c_int64)]
 
 
 class bf_fio_t(ctypes.Structure):
@@ -91,6 +94,12 @@ def lib():
             "bf_build_blocks": ([P(bf_fio_t), i32, i64, i64, vp], i32),
             "bf_build_block_elems": ([P(bf_fio_t), i32], i64),
             "bf_plan_build_fio": ([P(bf_fio_t), ctypes.c_int, i64, i64, P(vp)], i32),
+            "bf_nccl_get_unique_id": ([vp], i32),
+            "bf_plan_alloc_sharded": ([P(bf_desc_t), ctypes.c_int, i64, i32, i32, vp, P(vp)], i32),
+            "bf_plan_create_sharded": ([P(bf_desc_t), ctypes.c_int, i64, i32, i32, vp, P(vp)], i32),
+            "bf_shard_pairs": ([i32, i32, i32, i32, i32, vp], i32),
+            "bf_plan_build_fio_sharded": ([P(bf_fio_t), ctypes.c_int, i32, i32, vp, i64, i64, P(vp)], i32),
+            "bf_plan_build_fio_emulated": ([P(bf_fio_t), ctypes.c_int, i32, i64, i64, P(vp)], i32),
         }
         for name, (args, res) in sigs.items():
             f = getattr(L, name)
@@ -138,6 +147,20 @@ def build_blocks(k: bf_fio_t, stage: int, begin: int, count: int) -> np.ndarray:
     return out
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (to broadcast to every rank of an index-sharded plan)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().bf_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+def shard_pairs(log2n: int, log2leaf: int, world: int, rank: int, which: int) -> np.ndarray:
+    """Global level-h pair indices of a rank's send buffer (0), receive buffer (1) or second-half order (2)."""
+    out = np.zeros((1 << log2n) // world, np.int64)
+    _check(lib().bf_shard_pairs(log2n, log2leaf, world, rank, which, out.ctypes.data))
+    return out
+
+
 def _ptr(x) -> int:
     """Device/host pointer of a torch tensor, numpy array or raw int."""
     if isinstance(x, int):
@@ -168,6 +191,25 @@ class Plan:
         """Host builder -> streaming upload -> finalized plan (bf_plan_build_fio)."""
         h = ctypes.c_void_p()
         _check(lib().bf_plan_build_fio(ctypes.byref(k), device, max_nrhs_chunk, staging_bytes, ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def build_fio_sharded(cls, k: bf_fio_t, rank: int, world: int, nccl_id: bytes, device: int = 0,
+                          max_nrhs_chunk: int = 1, staging_bytes: int = 256 << 20):
+        """This rank's shard of the index-sharded plan; bf_apply then takes the local N/world rows."""
+        h = ctypes.c_void_p()
+        idb = ctypes.create_string_buffer(nccl_id, 128)
+        _check(lib().bf_plan_build_fio_sharded(ctypes.byref(k), device, rank, world, idb, max_nrhs_chunk,
+                                               staging_bytes, ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def build_fio_emulated(cls, k: bf_fio_t, world: int, device: int = 0, max_nrhs_chunk: int = 1,
+                           staging_bytes: int = 256 << 20):
+        """All `world` index shards on one device (exchange by device copies); full N-row F/G."""
+        h = ctypes.c_void_p()
+        _check(lib().bf_plan_build_fio_emulated(ctypes.byref(k), device, world, max_nrhs_chunk, staging_bytes,
+                                                ctypes.byref(h)))
         return cls(h.value)
 
     @classmethod

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <omp.h>
 
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -296,59 +297,63 @@ bf_status_t bf_build_blocks(const bf_fio_t* k, int32_t stage, int64_t block_begi
     return BF_OK;
 }
 
-bf_status_t bf_plan_build_fio(const bf_fio_t* k, int device, int64_t max_nrhs_chunk, int64_t staging_bytes,
-                              bf_plan_t* out)
-{
-    Shape S;
-    if (!out) return bfp_fail(BF_ERR_INVALID_ARG, "out is NULL");
-    *out = nullptr;
-    if (!make_shape(k, &S)) return bfp_fail(BF_ERR_INVALID_ARG, "bf_plan_build_fio: bad kernel descriptor");
-    bf_desc_t meta{};
-    meta.abi_version = BF_ABI_VERSION;
-    meta.log2n = S.LN;
-    meta.log2leaf = S.l0;
-    meta.rank = S.r;
-    meta.n_amp = bf_build_n_amp(S.amp);
-    meta.memory = BF_MEM_HOST;
-    bf_plan_t plan = nullptr;
-    bf_status_t st = bf_plan_alloc(&meta, device, max_nrhs_chunk, &plan);
-    if (st != BF_OK) return st;
+}  // extern "C"
 
+namespace {
+
+// Build shard slot `si` (representing rank q of 2^g) of plan p: every stage's local blocks, in slices of
+// at most staging_bytes through two pinned buffers (build of slice i+1 overlaps the upload of slice i).
+// Local -> global block map (include/bf.h "index-sharded plans"): first-half stages (V0, SW, XFER of
+// levels <= h) hold runs of 2^(LN-l-g) consecutive global blocks per a; second-half stages (XFER of
+// levels > h, U) the contiguous range [q N/G, (q+1) N/G).
+bf_status_t stream_build(bf_plan_t plan, const bf_fio_t* k, const Shape& S, int si, int q, int g,
+                         int64_t staging_bytes)
+{
+    const int na = bf_build_n_amp(S.amp);
+    const int64_t nloc = S.N >> g;
+    bf_status_t st = BF_OK;
     int prev = -1;
     cudaGetDevice(&prev);
-    cudaSetDevice(device);
-    if (staging_bytes < (int64_t(1) << 20)) staging_bytes = int64_t(1) << 20;
-    // two pinned staging slices: build slice i+1 on the host while slice i is copied
-    bf_c64* stage_buf[2] = {nullptr, nullptr};
+    cudaSetDevice(bfp_device(plan));
+    bf_c64* buf[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaStream_t cs = nullptr;
     auto cleanup = [&]() {
         if (cs) cudaStreamSynchronize(cs);
         for (int i = 0; i < 2; i++) {
-            if (stage_buf[i]) cudaFreeHost(stage_buf[i]);
+            if (buf[i]) cudaFreeHost(buf[i]);
             if (ev[i]) cudaEventDestroy(ev[i]);
         }
         if (cs) cudaStreamDestroy(cs);
         if (prev >= 0) cudaSetDevice(prev);
     };
-    if (cudaMallocHost(reinterpret_cast<void**>(&stage_buf[0]), size_t(staging_bytes)) != cudaSuccess ||
-        cudaMallocHost(reinterpret_cast<void**>(&stage_buf[1]), size_t(staging_bytes)) != cudaSuccess ||
+    if (cudaMallocHost(reinterpret_cast<void**>(&buf[0]), size_t(staging_bytes)) != cudaSuccess ||
+        cudaMallocHost(reinterpret_cast<void**>(&buf[1]), size_t(staging_bytes)) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
         cudaGetLastError();
         cleanup();
-        bf_plan_destroy(plan);
-        return bfp_fail(BF_ERR_OOM, "bf_plan_build_fio: pinned staging allocation failed");
+        return bfp_fail(BF_ERR_OOM, "factor upload: pinned staging allocation failed");
     }
-    // amplitudes
+    // amplitudes: a_k on this shard's x-rows, b_k on its xi-rows (both [q N/G, (q+1) N/G))
     {
-        std::vector<bf_c64> a(size_t(meta.n_amp) * S.N), b(size_t(meta.n_amp) * S.N);
+        std::vector<bf_c64> a(size_t(na) * S.N), b(size_t(na) * S.N);
         bf_build_amp(k, a.data(), b.data());
-        if ((st = bf_plan_upload(plan, BF_STAGE_AMP_A, 0, meta.n_amp, a.data(), BF_MEM_HOST)) != BF_OK ||
-            (st = bf_plan_upload(plan, BF_STAGE_AMP_B, 0, meta.n_amp, b.data(), BF_MEM_HOST)) != BF_OK) {
+        for (int which = 0; which < 2 && st == BF_OK; which++) {
+            const std::vector<bf_c64>& src = which ? b : a;
+            void* dst = nullptr;
+            if ((st = bfp_stage_dst(plan, si, which ? BF_STAGE_AMP_B : BF_STAGE_AMP_A, 0, na, &dst)) != BF_OK) break;
+            for (int kk = 0; kk < na; kk++)
+                if (cudaMemcpy(static_cast<bf_c64*>(dst) + kk * nloc, src.data() + kk * S.N + q * nloc,
+                               size_t(nloc) * sizeof(bf_c64), cudaMemcpyHostToDevice) != cudaSuccess) {
+                    cudaGetLastError();
+                    st = bfp_fail(BF_ERR_CUDA, "factor upload: amplitude copy failed");
+                    break;
+                }
+        }
+        if (st != BF_OK) {
             cleanup();
-            bf_plan_destroy(plan);
             return st;
         }
     }
@@ -357,24 +362,38 @@ bf_status_t bf_plan_build_fio(const bf_fio_t* k, int device, int64_t max_nrhs_ch
     int cur = 0;
     bool used[2] = {false, false};
     for (int stage : stages) {
+        const int lvl = stage == BF_STAGE_V0 ? S.l0 : stage == BF_STAGE_SW ? S.h : stage == BF_STAGE_U ? S.D
+                                                                                       : S.l0 + 1 + (stage - BF_STAGE_XFER0);
+        const bool first = (stage == BF_STAGE_SW) || lvl <= S.h;
+        const int sb = S.LN - lvl - g;   // first half: log2 of a local b-run
         const int64_t elems = block_elems(S, stage);
         const int64_t per = std::max<int64_t>(1, staging_bytes / (elems * int64_t(sizeof(bf_c64))));
-        for (int64_t b0 = 0; b0 < S.N; b0 += per) {
-            const int64_t cnt = std::min(per, S.N - b0);
+        for (int64_t b0 = 0; b0 < nloc; b0 += per) {
+            const int64_t cnt = std::min(per, nloc - b0);
             if (used[cur]) cudaEventSynchronize(ev[cur]);   // slice buffer free again
-            bf_build_blocks(k, stage, b0, cnt, stage_buf[cur]);
+            for (int64_t pos = b0; pos < b0 + cnt;) {
+                int64_t glob, run;
+                if (first) {
+                    const int64_t a = pos >> sb, bl = pos & ((int64_t(1) << sb) - 1);
+                    run = std::min((int64_t(1) << sb) - bl, b0 + cnt - pos);
+                    glob = (a << (S.LN - lvl)) + (int64_t(q) << sb) + bl;
+                } else {
+                    run = b0 + cnt - pos;
+                    glob = int64_t(q) * nloc + pos;
+                }
+                bf_build_blocks(k, stage, glob, run, buf[cur] + (pos - b0) * elems);
+                pos += run;
+            }
             void* dst = nullptr;
-            if ((st = bfp_stage_dst(plan, stage, b0, cnt, &dst)) != BF_OK) {
+            if ((st = bfp_stage_dst(plan, si, stage, b0, cnt, &dst)) != BF_OK) {
                 cleanup();
-                bf_plan_destroy(plan);
                 return st;
             }
-            if (cudaMemcpyAsync(dst, stage_buf[cur], size_t(cnt * elems) * sizeof(bf_c64), cudaMemcpyHostToDevice,
-                                cs) != cudaSuccess) {
+            if (cudaMemcpyAsync(dst, buf[cur], size_t(cnt * elems) * sizeof(bf_c64), cudaMemcpyHostToDevice, cs) !=
+                cudaSuccess) {
                 cudaGetLastError();
                 cleanup();
-                bf_plan_destroy(plan);
-                return bfp_fail(BF_ERR_CUDA, "bf_plan_build_fio: upload failed");
+                return bfp_fail(BF_ERR_CUDA, "factor upload failed");
             }
             cudaEventRecord(ev[cur], cs);
             used[cur] = true;
@@ -382,12 +401,62 @@ bf_status_t bf_plan_build_fio(const bf_fio_t* k, int device, int64_t max_nrhs_ch
         }
     }
     cleanup();
-    if ((st = bf_plan_finalize(plan)) != BF_OK) {
-        bf_plan_destroy(plan);
+    return BF_OK;
+}
+
+bf_status_t build_plan(const bf_fio_t* k, int device, int world, int rank, int mode, const void* nccl_id,
+                       int64_t max_nrhs_chunk, int64_t staging_bytes, bf_plan_t* out)
+{
+    Shape S;
+    if (!out) return bfp_fail(BF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!make_shape(k, &S)) return bfp_fail(BF_ERR_INVALID_ARG, "bad kernel descriptor");
+    bf_desc_t meta{};
+    meta.abi_version = BF_ABI_VERSION;
+    meta.log2n = S.LN;
+    meta.log2leaf = S.l0;
+    meta.rank = S.r;
+    meta.n_amp = bf_build_n_amp(S.amp);
+    meta.memory = BF_MEM_HOST;
+    bf_plan_t plan = nullptr;
+    bf_status_t st = bfp_plan_alloc_sharded(&meta, device, max_nrhs_chunk, world, rank, mode, nccl_id, &plan);
+    if (st != BF_OK) return st;
+    int g = 0;
+    while ((1 << g) < world) g++;
+    if (staging_bytes < (int64_t(1) << 20)) staging_bytes = int64_t(1) << 20;
+    const int nsh = bfp_num_shards(plan);
+    for (int si = 0; si < nsh && st == BF_OK; si++)
+        st = stream_build(plan, k, S, si, mode == BF_SHARD_EMULATED ? si : rank, g, staging_bytes);
+    if (st == BF_OK) st = bf_plan_finalize(plan);
+    if (st != BF_OK) {
+        bfp_plan_free(plan);
         return st;
     }
     *out = plan;
     return BF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+bf_status_t bf_plan_build_fio(const bf_fio_t* k, int device, int64_t max_nrhs_chunk, int64_t staging_bytes,
+                              bf_plan_t* out)
+{
+    return build_plan(k, device, 1, 0, BF_SHARD_NONE, nullptr, max_nrhs_chunk, staging_bytes, out);
+}
+
+bf_status_t bf_plan_build_fio_sharded(const bf_fio_t* k, int device, int32_t rank, int32_t world,
+                                      const void* nccl_unique_id, int64_t max_nrhs_chunk, int64_t staging_bytes,
+                                      bf_plan_t* out)
+{
+    return build_plan(k, device, world, rank, BF_SHARD_NCCL, nccl_unique_id, max_nrhs_chunk, staging_bytes, out);
+}
+
+bf_status_t bf_plan_build_fio_emulated(const bf_fio_t* k, int device, int32_t world, int64_t max_nrhs_chunk,
+                                       int64_t staging_bytes, bf_plan_t* out)
+{
+    return build_plan(k, device, world, 0, BF_SHARD_EMULATED, nullptr, max_nrhs_chunk, staging_bytes, out);
 }
 
 }  // extern "C"

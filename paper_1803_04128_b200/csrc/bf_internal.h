@@ -23,14 +23,15 @@ cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2*
 
 // Transfer level l (eqn:2 / eqn:3): out[p](t) = sum_{c,s} W[p](t, c r + s) in[(a>>1) 2^(LN-l+1) + 2b + c](s);
 // with Sw != nullptr (only at l == h) the switch block Sw[p] is applied to the result.
+// rh > 0: `in` is a receive buffer of the index-sharded exchange (input pair p at bfs::recv_index(p, rh, rhg)).
 cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, const float2* Sw,
-                        int nv, cudaStream_t s);
+                        int nv, cudaStream_t s, int rh = 0, int rhg = 0);
 
 // Band of K (1 or 2) transfer levels l_first .. l_first+K-1 fused in shared memory; W[m] are the
 // weights of level l_first+m; with m_sw in 1..K the switch Sw is applied after band level m_sw.
 bool band_supported(int R, int nv);
 cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W,
-                        const float2* Sw, int m_sw, int nv, cudaStream_t s);
+                        const float2* Sw, int m_sw, int nv, cudaStream_t s, int rh = 0, int rhg = 0);
 
 // Switch alone (used when no transfer level precedes it, h == l0).
 cudaError_t launch_switch(const Dims& d, const float2* in, float2* out, const float2* Sw, int nv, cudaStream_t s);

@@ -14,6 +14,7 @@
 #include <cstdint>
 
 #include "bf_internal.h"
+#include "bf_shard.h"
 
 namespace bfk {
 
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(256) s0_kernel(const float2* __restrict__ F, i
 template <int R, int TN, bool SW>
 __global__ void __launch_bounds__(128) xfer_kernel(const float2* __restrict__ in, float2* __restrict__ out,
                                                    const float2* __restrict__ Wl, const float2* __restrict__ Sw,
-                                                   int LN, int l, int nv)
+                                                   int LN, int l, int nv, int rh, int rhg)
 {
     const int64_t N = int64_t(1) << LN;
     const int cpu = nv / TN;
@@ -192,7 +193,9 @@ __global__ void __launch_bounds__(128) xfer_kernel(const float2* __restrict__ in
     const int sh = LN - l;
     const int64_t P = u >> sh, b = u & ((int64_t(1) << sh) - 1);
     const int64_t p0 = (2 * P << sh) + b, p1 = p0 + (int64_t(1) << sh);
-    const float2* x = in + 2 * u * R * nv + vg * TN;
+    // inputs: pairs 2u, 2u+1 of level l-1 (in a receive buffer of the index-sharded exchange when rh > 0)
+    const int64_t pin = rh ? bfs::recv_index(2 * u, rh, rhg) : 2 * u;
+    const float2* x = in + pin * R * nv + vg * TN;
     const float2* W0 = Wl + p0 * 2 * R * R;   // column-major r x 2r: column k at k*R
     const float2* W1 = Wl + p1 * 2 * R * R;
 
@@ -510,6 +513,7 @@ struct BandArgs {
     const float2* W[4];   // weights of band levels 1..K (bf.h XFER layout)
     const float2* Sw;     // switch blocks (level h), used when m_sw > 0
     int m_sw;             // band level after which the switch is applied (1..K), 0 = none
+    int rh, rhg;          // > 0: the input is a receive buffer of the index-sharded exchange (bf_shard.h)
 };
 
 
@@ -572,7 +576,8 @@ __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
         const int v0 = vt * VT;
         const int vw = min(VT, nv - v0);
         __syncthreads();   // the previous tile is consumed; weights are in place
-        const float2* src = in + (g * P) * R * int64_t(nv) + v0;
+        const int64_t pin = args.rh ? bfs::recv_index(g * P, args.rh, args.rhg) : g * P;   // P pairs contiguous
+        const float2* src = in + pin * R * int64_t(nv) + v0;
         for (int idx = tid; idx < P * R * (VT / 2); idx += 256) {
             const int vv = (idx % (VT / 2)) * 2, row = idx / (VT / 2);
             if (vv < vw) cp_async16(X + row * VT + vv, src + int64_t(row) * nv + vv);
@@ -738,10 +743,10 @@ static cudaError_t s0_go(const Dims& d, const float2* F, int64_t ldf, const floa
 
 template <int R, bool SW, int TN>
 static cudaError_t xfer_go(const Dims& d, int l, const float2* in, float2* out, const float2* W, const float2* Sw, int nv,
-                           cudaStream_t s)
+                           int rh, int rhg, cudaStream_t s)
 {
     const int64_t threads = (d.N / 2) * (nv / TN);
-    xfer_kernel<R, TN, SW><<<unsigned((threads + 127) / 128), 128, 0, s>>>(in, out, W, Sw, d.LN, l, nv);
+    xfer_kernel<R, TN, SW><<<unsigned((threads + 127) / 128), 128, 0, s>>>(in, out, W, Sw, d.LN, l, nv, rh, rhg);
     return cudaGetLastError();
 }
 
@@ -802,15 +807,15 @@ cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2*
 }
 
 cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, const float2* Sw, int nv,
-                        cudaStream_t s)
+                        cudaStream_t s, int rh, int rhg)
 {
     const int tn = pick_tn(nv, 2);
     if (Sw) {
-        if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, true, 2>(d, l, in, out, W, Sw, nv, s)))
-        BF_DISPATCH_R(d.R, (xfer_go<RR, true, 1>(d, l, in, out, W, Sw, nv, s)))
+        if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, true, 2>(d, l, in, out, W, Sw, nv, rh, rhg, s)))
+        BF_DISPATCH_R(d.R, (xfer_go<RR, true, 1>(d, l, in, out, W, Sw, nv, rh, rhg, s)))
     }
-    if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, false, 2>(d, l, in, out, W, Sw, nv, s)))
-    BF_DISPATCH_R(d.R, (xfer_go<RR, false, 1>(d, l, in, out, W, Sw, nv, s)))
+    if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, false, 2>(d, l, in, out, W, Sw, nv, rh, rhg, s)))
+    BF_DISPATCH_R(d.R, (xfer_go<RR, false, 1>(d, l, in, out, W, Sw, nv, rh, rhg, s)))
 }
 
 cudaError_t launch_switch(const Dims& d, const float2* in, float2* out, const float2* Sw, int nv, cudaStream_t s)
@@ -861,12 +866,14 @@ bool band_supported(int R, int nv) { return (R == 6 || R == 8 || R == 10 || R ==
 
 template <int R, int K>
 static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W,
-                           const float2* Sw, int m_sw, int nv, cudaStream_t s)
+                           const float2* Sw, int m_sw, int nv, cudaStream_t s, int rh, int rhg)
 {
     BandArgs a{};
     for (int m = 0; m < K; m++) a.W[m] = W[m];
     a.Sw = Sw;
     a.m_sw = m_sw;
+    a.rh = rh;
+    a.rhg = rhg;
     const size_t shm = band_smem_bytes<R, K>();
     auto kern = band_kernel<R, K>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
@@ -877,26 +884,23 @@ static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2*
 }
 
 cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W,
-                        const float2* Sw, int m_sw, int nv, cudaStream_t s)
+                        const float2* Sw, int m_sw, int nv, cudaStream_t s, int rh, int rhg)
 {
+#define BF_BAND_CASE(RR, KK) \
+    case RR: return band_go<RR, KK>(d, l_first, in, out, W, Sw, m_sw, nv, s, rh, rhg);
     if (K == 2) {
         switch (d.R) {
-        case 6: return band_go<6, 2>(d, l_first, in, out, W, Sw, m_sw, nv, s);
-        case 8: return band_go<8, 2>(d, l_first, in, out, W, Sw, m_sw, nv, s);
-        case 10: return band_go<10, 2>(d, l_first, in, out, W, Sw, m_sw, nv, s);
-        case 12: return band_go<12, 2>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+            BF_BAND_CASE(6, 2) BF_BAND_CASE(8, 2) BF_BAND_CASE(10, 2) BF_BAND_CASE(12, 2)
         default: return cudaErrorInvalidValue;
         }
     }
     if (K == 1) {
         switch (d.R) {
-        case 6: return band_go<6, 1>(d, l_first, in, out, W, Sw, m_sw, nv, s);
-        case 8: return band_go<8, 1>(d, l_first, in, out, W, Sw, m_sw, nv, s);
-        case 10: return band_go<10, 1>(d, l_first, in, out, W, Sw, m_sw, nv, s);
-        case 12: return band_go<12, 1>(d, l_first, in, out, W, Sw, m_sw, nv, s);
+            BF_BAND_CASE(6, 1) BF_BAND_CASE(8, 1) BF_BAND_CASE(10, 1) BF_BAND_CASE(12, 1)
         default: return cudaErrorInvalidValue;
         }
     }
+#undef BF_BAND_CASE
     return cudaErrorInvalidValue;
 }
 

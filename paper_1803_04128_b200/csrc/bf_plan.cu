@@ -1,11 +1,14 @@
 // bf_plan.cu -- the C ABI of include/bf.h: plan creation / streaming upload,
 // bf_apply orchestration (one stream, RHS chunks, no allocation), end-to-end
-// host apply, per-kernel event timing.
+// host apply, per-kernel event timing, and the index-sharded plan (NCCL
+// all-to-all at level h, or G shards emulated on one device).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -13,6 +16,7 @@
 #include "../../include/bf.h"
 #include "bf_internal.h"
 #include "bf_plan_internal.h"
+#include "bf_shard.h"
 
 namespace {
 
@@ -51,6 +55,63 @@ struct DeviceGuard {
     }
 };
 
+// ---------------------------------------------------------------------------
+// NCCL, loaded on first use (only index-sharded plans need it; the library has
+// no link-time dependency on it).  Types as in nccl.h.
+// ---------------------------------------------------------------------------
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+    char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int kNcclUint8 = 1;
+
+struct Nccl {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl& nccl()
+{
+    static Nccl n;
+    static bool tried = false;
+    if (tried) return n;
+    tried = true;
+    const char* cands[] = {getenv("BF_NCCL_LIB"), "libnccl.so.2", "libnccl.so",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    void* h = nullptr;
+    for (const char* c : cands)
+        if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return n;
+#define BF_NCCL_SYM(field, name) n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name))
+    BF_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
+    BF_NCCL_SYM(CommInitRank, "ncclCommInitRank");
+    BF_NCCL_SYM(CommDestroy, "ncclCommDestroy");
+    BF_NCCL_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    BF_NCCL_SYM(Send, "ncclSend");
+    BF_NCCL_SYM(Recv, "ncclRecv");
+    BF_NCCL_SYM(GroupStart, "ncclGroupStart");
+    BF_NCCL_SYM(GroupEnd, "ncclGroupEnd");
+    BF_NCCL_SYM(GetErrorString, "ncclGetErrorString");
+#undef BF_NCCL_SYM
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Send && n.Recv && n.GroupStart && n.GroupEnd &&
+           n.GetErrorString && n.CommGetAsyncError;
+    return n;
+}
+
+bf_status_t nccl_fail(ncclResult_t r, const char* what)
+{
+    return fail(BF_ERR_NCCL, "%s: NCCL error %d (%s)", what, r, nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+}
+
 }  // namespace
 
 struct TimedLaunch {
@@ -58,22 +119,28 @@ struct TimedLaunch {
     cudaEvent_t start, stop;
 };
 
-struct bf_plan_s {
-    int device = 0;
-    bfk::Dims d{};
-    int64_t max_chunk = 0;
-    // factors (device)
-    float2* amp_a = nullptr;
-    float2* amp_b = nullptr;
+// The factors and workspace of one index shard (the whole problem when the plan is not sharded).
+struct Shard {
+    float2* amp_a = nullptr;   // [n_amp][N/G]   a_k on this shard's x rows
+    float2* amp_b = nullptr;   // [n_amp][N/G]   b_k on this shard's xi rows
     float2* v0 = nullptr;
     float2* sw = nullptr;
     float2* u = nullptr;
     std::vector<float2*> xfer;
-    std::vector<int64_t> uploaded;   // blocks uploaded per stage slot
+    float2* ws = nullptr;      // two coefficient arrays of (N/G) R nv_max
+};
+
+struct bf_plan_s {
+    int device = 0;
+    bfk::Dims d{};             // GLOBAL dims
+    int64_t max_chunk = 0;
+    int world = 1, rank = 0, g = 0;
+    int mode = BF_SHARD_NONE;  // BF_SHARD_NONE / BF_SHARD_NCCL / BF_SHARD_EMULATED
+    std::vector<Shard> sh;     // 1 shard, or `world` shards when emulated
+    ncclComm_t comm = nullptr;
+    std::vector<std::vector<int64_t>> uploaded;   // [shard][stage slot]
     bool finalized = false;
-    // workspace (two coefficient arrays)
-    float2* ws = nullptr;
-    size_t ws_bytes = 0;
+    size_t ws_bytes = 0;       // per shard
     // end-to-end staging (lazily allocated by bf_apply_host)
     float2* dF = nullptr;
     float2* dG = nullptr;
@@ -84,24 +151,36 @@ struct bf_plan_s {
     double ms[BF_NUM_KCLASS] = {0};
     int64_t nlaunch[BF_NUM_KCLASS] = {0};
     cudaEvent_t done = nullptr;
+
+    int64_t nloc() const { return d.N >> g; }   // pairs / rows per shard
+    bfk::Dims local() const
+    {
+        bfk::Dims l = d;
+        l.LN = d.LN - g;
+        l.N = d.N >> g;
+        return l;
+    }
 };
 
 namespace {
+
+constexpr int KC_EXCHANGE = 5;   // timing class of the level-h all-to-all (BF_NUM_KCLASS)
 
 // stage slot index: 0 V0, 1 SW, 2 U, 3 AMP_A, 4 AMP_B, 5 + i XFER i
 int slot_of(const bf_plan_s* p, int stage)
 {
     if (stage >= BF_STAGE_XFER0) {
         const int i = stage - BF_STAGE_XFER0;
-        return i < int(p->xfer.size()) ? 5 + i : -1;
+        return i < int(p->sh[0].xfer.size()) ? 5 + i : -1;
     }
     return (stage >= 0 && stage <= 4) ? stage : -1;
 }
 
+// blocks of a stage in ONE shard
 int64_t stage_blocks(const bf_plan_s* p, int stage)
 {
     if (stage == BF_STAGE_AMP_A || stage == BF_STAGE_AMP_B) return p->d.n_amp;
-    return p->d.N;
+    return p->nloc();
 }
 
 int64_t stage_elems(const bf_plan_s* p, int stage)
@@ -112,20 +191,20 @@ int64_t stage_elems(const bf_plan_s* p, int stage)
     case BF_STAGE_SW: return r * r;
     case BF_STAGE_U: return n0 * r;
     case BF_STAGE_AMP_A:
-    case BF_STAGE_AMP_B: return p->d.N;
+    case BF_STAGE_AMP_B: return p->nloc();
     default: return 2 * r * r;
     }
 }
 
-float2* stage_base(bf_plan_s* p, int stage)
+float2* stage_base(Shard& s, int stage)
 {
     switch (stage) {
-    case BF_STAGE_V0: return p->v0;
-    case BF_STAGE_SW: return p->sw;
-    case BF_STAGE_U: return p->u;
-    case BF_STAGE_AMP_A: return p->amp_a;
-    case BF_STAGE_AMP_B: return p->amp_b;
-    default: return p->xfer[stage - BF_STAGE_XFER0];
+    case BF_STAGE_V0: return s.v0;
+    case BF_STAGE_SW: return s.sw;
+    case BF_STAGE_U: return s.u;
+    case BF_STAGE_AMP_A: return s.amp_a;
+    case BF_STAGE_AMP_B: return s.amp_b;
+    default: return s.xfer[stage - BF_STAGE_XFER0];
     }
 }
 
@@ -145,6 +224,21 @@ bf_status_t validate_shape(const bf_desc_t* d)
     return BF_OK;
 }
 
+// index sharding over world = 2^g ranks: the first half on a shard is the butterfly of size 2^(LN-g), the
+// exchange needs >= 4 b's per source block at level h (h - g >= 2: a band group of 4 pairs never straddles
+// two sources), and every shard holds whole leaves on both sides (LN - g >= 2 l0).
+bf_status_t validate_sharding(const bf_desc_t* d, int world, int rank)
+{
+    if (world < 1 || (world & (world - 1))) return fail(BF_ERR_INVALID_ARG, "world=%d is not a power of two", world);
+    if (rank < 0 || rank >= world) return fail(BF_ERR_INVALID_ARG, "rank=%d not in [0,%d)", rank, world);
+    int g = 0;
+    while ((1 << g) < world) g++;
+    const int h = d->log2n / 2;
+    if (g > 0 && (h - g < 2 || d->log2n - g < 2 * d->log2leaf))
+        return fail(BF_ERR_SHAPE, "world=%d too large for log2n=%d, log2leaf=%d", world, d->log2n, d->log2leaf);
+    return BF_OK;
+}
+
 void free_plan(bf_plan_s* p)
 {
     if (!p) return;
@@ -156,15 +250,18 @@ void free_plan(bf_plan_s* p)
     }
     for (auto e : p->pool) cudaEventDestroy(e);
     if (p->done) cudaEventDestroy(p->done);
-    cudaFree(p->amp_a);
-    cudaFree(p->amp_b);
-    cudaFree(p->v0);
-    cudaFree(p->sw);
-    cudaFree(p->u);
-    for (auto x : p->xfer) cudaFree(x);
-    cudaFree(p->ws);
+    for (auto& s : p->sh) {
+        cudaFree(s.amp_a);
+        cudaFree(s.amp_b);
+        cudaFree(s.v0);
+        cudaFree(s.sw);
+        cudaFree(s.u);
+        for (auto x : s.xfer) cudaFree(x);
+        cudaFree(s.ws);
+    }
     cudaFree(p->dF);
     cudaFree(p->dG);
+    if (p->comm) nccl().CommDestroy(p->comm);
     delete p;
 }
 
@@ -174,7 +271,8 @@ bf_status_t dalloc(float2** ptr, int64_t elems, const char* what)
     if (e != cudaSuccess) {
         cudaGetLastError();
         *ptr = nullptr;
-        return fail(BF_ERR_OOM, "cudaMalloc(%s, %lld B) failed: %s", what, (long long)(elems * 8), cudaGetErrorString(e));
+        return fail(BF_ERR_OOM, "cudaMalloc(%s, %lld B) failed: %s", what, (long long)(elems * 8),
+                    cudaGetErrorString(e));
     }
     return BF_OK;
 }
@@ -206,114 +304,190 @@ cudaError_t timed(bf_plan_s* p, int cls, cudaStream_t s, F&& launch)
 
 // One kernel launch of the apply: what it runs and how it is accounted.
 struct Step {
-    enum Kind { S0, SWITCH, XFER, BAND, SL } kind;
-    int l_first = 0;   // XFER: the level; BAND: first level
+    enum Kind { S0, SWITCH, XFER, BAND, SL, EXCHANGE } kind;
+    int l_first = 0;   // XFER: the level; BAND: first level (global level numbering)
     int K = 1;         // BAND: levels fused
     int m_sw = 0;      // BAND: band level after which the switch applies (0 = none)
-    int cls = 0;       // bfk::KClass
+    int cls = 0;       // bfk::KClass or KC_EXCHANGE
     int levels = 0;    // transfer levels this launch performs
 };
 
+void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool band)
+{
+    for (int l = lo; l <= hi;) {
+        const int K = band ? std::min(2, hi - l + 1) : 1;
+        const int last = l + K - 1;
+        const bool has_h = (l <= d.h && d.h <= last);
+        const int cls = has_h ? bfk::KC_SWITCH : (last < d.h ? bfk::KC_XFER1 : bfk::KC_XFER2);
+        st.push_back({band ? Step::BAND : Step::XFER, l, K, has_h ? d.h - l + 1 : 0, cls, K});
+        l += K;
+    }
+}
+
 // The launch sequence of one RHS chunk of nv vectors: S0, transfer levels l0+1..D (fused in bands of 2
 // when the band kernel supports the shape, the switch applied inside the launch that produces level h),
-// SL.  With no transfer level (h == l0) the switch runs alone after S0.
-std::vector<Step> schedule(const bfk::Dims& d, int nv)
+// SL.  With no transfer level (h == l0) the switch runs alone after S0.  Sharded: the bands stop at h,
+// the exchange follows, then the second half.
+std::vector<Step> schedule(const bfk::Dims& d, int nv, bool sharded)
 {
     std::vector<Step> st;
     st.push_back({Step::S0, 0, 1, 0, bfk::KC_S0, 0});
     if (d.h == d.l0) st.push_back({Step::SWITCH, 0, 1, 0, bfk::KC_SWITCH, 0});
     const bool band = bfk::band_supported(d.R, nv);
-    for (int l = d.l0 + 1; l <= d.D;) {
-        const int K = band ? std::min(2, d.D - l + 1) : 1;
-        const int last = l + K - 1;
-        const int cls = (l <= d.h && d.h <= last) ? bfk::KC_SWITCH : (last < d.h ? bfk::KC_XFER1 : bfk::KC_XFER2);
-        const int m_sw = (l <= d.h && d.h <= last) ? d.h - l + 1 : 0;
-        st.push_back({band ? Step::BAND : Step::XFER, l, K, m_sw, cls, K});
-        l += K;
+    if (!sharded) {
+        push_levels(st, d, d.l0 + 1, d.D, band);
+    } else {
+        push_levels(st, d, d.l0 + 1, d.h, band);
+        st.push_back({Step::EXCHANGE, 0, 1, 0, KC_EXCHANGE, 0});
+        push_levels(st, d, d.h + 1, d.D, band);
     }
     st.push_back({Step::SL, 0, 1, 0, bfk::KC_SL, 0});
     return st;
 }
 
-bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, int64_t ldg, int64_t nrhs, float2* ws,
+// Level-h exchange of one RHS chunk: block d (of G equal blocks) of every shard's send buffer goes to
+// shard d's receive buffer at block q.  ws[i] is shard i's workspace base.
+bf_status_t exchange(bf_plan_s* p, float2* const* ws, int send_buf, int nv, cudaStream_t s)
+{
+    const int G = p->world;
+    const int64_t blk_pairs = p->nloc() / G;
+    const int64_t bel = blk_pairs * p->d.R * nv;   // elements of one block
+    const size_t blk_bytes = size_t(bel) * sizeof(float2);
+    const int64_t arr = p->nloc() * p->d.R * nv;   // elements of one coefficient array of a shard
+    if (p->mode == BF_SHARD_EMULATED) {
+        for (int q = 0; q < G; q++)
+            for (int dd = 0; dd < G; dd++) {
+                cudaError_t e = cudaMemcpyAsync(ws[dd] + (1 - send_buf) * arr + q * bel, ws[q] + send_buf * arr + dd * bel,
+                                                blk_bytes, cudaMemcpyDeviceToDevice, s);
+                if (e != cudaSuccess) return cuda_fail(e, "exchange copy");
+            }
+        return BF_OK;
+    }
+    // NCCL: grouped send/recv with every peer (the last first-half launch wrote the blocks in destination order)
+    const float2* sb = ws[0] + send_buf * arr;
+    float2* rb = ws[0] + (1 - send_buf) * arr;
+    cudaError_t e = cudaMemcpyAsync(rb + p->rank * bel, sb + p->rank * bel, blk_bytes, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "exchange self copy");
+    if (G == 1) return BF_OK;
+    Nccl& n = nccl();
+    ncclResult_t r = n.GroupStart();
+    if (r) return nccl_fail(r, "ncclGroupStart");
+    for (int peer = 0; peer < G; peer++) {
+        if (peer == p->rank) continue;
+        if ((r = n.Send(sb + peer * bel, blk_bytes, kNcclUint8, peer, p->comm, s))) break;
+        if ((r = n.Recv(rb + peer * bel, blk_bytes, kNcclUint8, peer, p->comm, s))) break;
+    }
+    ncclResult_t r2 = n.GroupEnd();
+    if (r) return nccl_fail(r, "ncclSend/ncclRecv");
+    if (r2) return nccl_fail(r2, "ncclGroupEnd");
+    return BF_OK;
+}
+
+// Run steps [s_begin, s_end) of the schedule for one shard; `cur` is the coefficient buffer (0/1) holding
+// the current level, updated in place.  remap_first: the first transfer launch reads the receive layout.
+bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size_t s_begin, size_t s_end,
+                      const float2* F, int64_t ldf, float2* G, int64_t ldg, int nv, int& cur, bool remap_first,
+                      float2* ws, cudaStream_t s)
+{
+    const bfk::Dims dl = p->local();
+    const int64_t arr = p->nloc() * p->d.R * nv;
+    bool remap = remap_first;
+    for (size_t k = s_begin; k < s_end; k++) {
+        const Step& stp = st[k];
+        float2* in = ws + cur * arr;
+        float2* out = ws + (1 - cur) * arr;
+        // kernel level: first half runs at the global level, second half at level - g (bf_shard.h)
+        const int lk = (stp.l_first > p->d.h) ? stp.l_first - p->g : stp.l_first;
+        const int rh = remap ? p->d.h : 0, rhg = remap ? p->d.h - p->g : 0;
+        cudaError_t e = timed(p, stp.cls, s, [&]() -> cudaError_t {
+            switch (stp.kind) {
+            case Step::S0: return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
+            case Step::SWITCH: return bfk::launch_switch(dl, in, out, sh.sw, nv, s);
+            case Step::XFER:
+                return bfk::launch_xfer(dl, lk, in, out, sh.xfer[stp.l_first - p->d.l0 - 1],
+                                        stp.l_first == p->d.h ? sh.sw : nullptr, nv, s, rh, rhg);
+            case Step::BAND: {
+                const float2* W[2] = {sh.xfer[stp.l_first - p->d.l0 - 1],
+                                      stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
+                return bfk::launch_band(dl, lk, stp.K, in, out, W, sh.sw, stp.m_sw, nv, s, rh, rhg);
+            }
+            case Step::SL: return bfk::launch_sl(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
+            default: return cudaErrorInvalidValue;
+            }
+        });
+        if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+        if (stp.kind == Step::SWITCH || stp.kind == Step::XFER || stp.kind == Step::BAND) {
+            cur = 1 - cur;
+            remap = false;
+        }
+    }
+    return BF_OK;
+}
+
+bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, int64_t ldg, int64_t nrhs, float2* ws0,
                        cudaStream_t s)
 {
-    const bfk::Dims& d = p->d;
     const int64_t chunk = p->max_chunk;
-    const int64_t pair_elems = d.N * d.R;   // complex per vector per coefficient array
+    const bool sharded = p->mode != BF_SHARD_NONE;
+    const int nsh = int(p->sh.size());
+    std::vector<float2*> ws(nsh);
+    for (int i = 0; i < nsh; i++) ws[i] = (i == 0) ? ws0 : p->sh[i].ws;
     for (int64_t c0 = 0; c0 < nrhs; c0 += chunk) {
         const int64_t nc = std::min(chunk, nrhs - c0);
-        const int nv = int(nc * d.n_amp);
-        float2* cur = ws;
-        float2* oth = ws + pair_elems * nv;
-        for (const Step& stp : schedule(d, nv)) {
-            cudaError_t e = timed(p, stp.cls, s, [&]() -> cudaError_t {
-                switch (stp.kind) {
-                case Step::S0: return bfk::launch_s0(d, F + c0 * ldf, ldf, p->amp_b, p->v0, cur, nv, s);
-                case Step::SWITCH: return bfk::launch_switch(d, cur, oth, p->sw, nv, s);
-                case Step::XFER:
-                    return bfk::launch_xfer(d, stp.l_first, cur, oth, p->xfer[stp.l_first - d.l0 - 1],
-                                            stp.l_first == d.h ? p->sw : nullptr, nv, s);
-                case Step::BAND: {
-                    const float2* W[2] = {p->xfer[stp.l_first - d.l0 - 1],
-                                          stp.K > 1 ? p->xfer[stp.l_first - d.l0] : nullptr};
-                    return bfk::launch_band(d, stp.l_first, stp.K, cur, oth, W, p->sw, stp.m_sw, nv, s);
-                }
-                default: return bfk::launch_sl(d, cur, p->u, p->amp_a, G + c0 * ldg, ldg, nv, s);
-                }
-            });
-            if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-            if (stp.kind == Step::SWITCH || stp.kind == Step::XFER || stp.kind == Step::BAND) std::swap(cur, oth);
+        const int nv = int(nc * p->d.n_amp);
+        const auto st = schedule(p->d, nv, sharded);
+        const float2* Fc = F + c0 * ldf;
+        float2* Gc = G + c0 * ldg;
+        if (!sharded) {
+            int cur = 0;
+            bf_status_t r = run_steps(p, p->sh[0], st, 0, st.size(), Fc, ldf, Gc, ldg, nv, cur, false, ws[0], s);
+            if (r != BF_OK) return r;
+            continue;
+        }
+        size_t ex = 0;
+        while (st[ex].kind != Step::EXCHANGE) ex++;
+        // rows of shard i: emulated plans take the full F/G (shard i at row offset i N/G), NCCL plans the
+        // local rows
+        int cur = 0;
+        for (int i = 0; i < nsh; i++) {
+            const int64_t off = (p->mode == BF_SHARD_EMULATED) ? int64_t(i) * p->nloc() : 0;
+            cur = 0;
+            bf_status_t r = run_steps(p, p->sh[i], st, 0, ex, Fc + off, ldf, nullptr, ldg, nv, cur, false, ws[i], s);
+            if (r != BF_OK) return r;
+        }
+        bf_status_t xr = BF_OK;
+        cudaError_t e = timed(p, KC_EXCHANGE, s, [&]() -> cudaError_t {
+            xr = exchange(p, ws.data(), cur, nv, s);
+            return cudaSuccess;
+        });
+        if (xr != BF_OK) return xr;
+        if (e != cudaSuccess) return cuda_fail(e, "exchange");
+        for (int i = 0; i < nsh; i++) {
+            const int64_t off = (p->mode == BF_SHARD_EMULATED) ? int64_t(i) * p->nloc() : 0;
+            int c = 1 - cur;   // the exchange wrote the other buffer
+            bf_status_t r = run_steps(p, p->sh[i], st, ex + 1, st.size(), nullptr, ldf, Gc + off, ldg, nv, c, true,
+                                      ws[i], s);
+            if (r != BF_OK) return r;
         }
     }
     cudaEventRecord(p->done, s);
     return BF_OK;
 }
 
-}  // namespace
-
-// ---------------------------------------------------------------------------
-// internal helpers for the streaming builder (bf_build.cpp)
-// ---------------------------------------------------------------------------
-bf_status_t bfp_stage_dst(bf_plan_t p, int32_t stage, int64_t begin, int64_t count, void** dst)
-{
-    if (!p || !dst) return fail(BF_ERR_INVALID_ARG, "NULL argument");
-    if (p->finalized) return fail(BF_ERR_STATE, "plan already finalized");
-    const int slot = slot_of(p, stage);
-    if (slot < 0) return fail(BF_ERR_INVALID_ARG, "bad stage id %d", stage);
-    if (begin < 0 || count < 0 || begin + count > stage_blocks(p, stage))
-        return fail(BF_ERR_INVALID_ARG, "block range [%lld,%lld) out of [0,%lld)", (long long)begin,
-                    (long long)(begin + count), (long long)stage_blocks(p, stage));
-    *dst = stage_base(p, stage) + begin * stage_elems(p, stage);
-    p->uploaded[slot] += count;
-    return BF_OK;
-}
-
-int bfp_device(bf_plan_t p) { return p ? p->device : -1; }
-
-bf_status_t bfp_fail(bf_status_t s, const char* msg) { return fail(s, "%s", msg); }
-
-// ---------------------------------------------------------------------------
-// ABI
-// ---------------------------------------------------------------------------
-extern "C" {
-
-int32_t bf_abi_version(void) { return BF_ABI_VERSION; }
-
-const char* bf_last_error(void) { return g_err.c_str(); }
-
-bf_status_t bf_plan_alloc(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk, bf_plan_t* out)
+bf_status_t alloc_plan(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk, int world, int rank, int mode,
+                       bf_plan_t* out)
 {
     if (!out) return fail(BF_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     bf_status_t st = validate_shape(meta);
     if (st != BF_OK) return st;
+    if ((st = validate_sharding(meta, world, rank)) != BF_OK) return st;
     if (max_nrhs_chunk < 1) return fail(BF_ERR_INVALID_ARG, "max_nrhs_chunk=%lld < 1", (long long)max_nrhs_chunk);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
     if (device < 0 || device >= ndev) return fail(BF_ERR_INVALID_ARG, "device %d not in [0,%d)", device, ndev);
-    DeviceGuard g(device);
+    DeviceGuard dg(device);
 
     auto* p = new bf_plan_s();
     p->device = device;
@@ -325,26 +499,31 @@ bf_status_t bf_plan_alloc(const bf_desc_t* meta, int device, int64_t max_nrhs_ch
     p->d.h = p->d.LN / 2;
     p->d.D = p->d.LN - p->d.l0;
     p->max_chunk = max_nrhs_chunk;
+    p->world = world;
+    p->rank = rank;
+    while ((1 << p->g) < world) p->g++;
+    p->mode = mode;
+    const int nsh = (mode == BF_SHARD_EMULATED) ? world : 1;
+    p->sh.resize(nsh);
     const int nx = p->d.D - p->d.l0;
-    p->xfer.assign(nx, nullptr);
-    p->uploaded.assign(5 + nx, 0);
-    const int64_t N = p->d.N, r = p->d.R, n0 = int64_t(1) << p->d.l0;
-    if ((st = dalloc(&p->amp_a, p->d.n_amp * N, "amp_a")) || (st = dalloc(&p->amp_b, p->d.n_amp * N, "amp_b")) ||
-        (st = dalloc(&p->v0, N * r * n0, "v0")) || (st = dalloc(&p->sw, N * r * r, "sw")) ||
-        (st = dalloc(&p->u, N * r * n0, "u"))) {
-        free_plan(p);
-        return st;
-    }
-    for (int i = 0; i < nx; i++)
-        if ((st = dalloc(&p->xfer[i], N * 2 * r * r, "xfer"))) {
+    p->uploaded.assign(nsh, std::vector<int64_t>(5 + nx, 0));
+    const int64_t n = p->nloc(), r = p->d.R, n0 = int64_t(1) << p->d.l0;
+    const int64_t nv = max_nrhs_chunk * p->d.n_amp;
+    p->ws_bytes = size_t(2) * size_t(n * r) * size_t(nv) * sizeof(float2);
+    for (auto& s : p->sh) {
+        s.xfer.assign(nx, nullptr);
+        if ((st = dalloc(&s.amp_a, p->d.n_amp * n, "amp_a")) || (st = dalloc(&s.amp_b, p->d.n_amp * n, "amp_b")) ||
+            (st = dalloc(&s.v0, n * r * n0, "v0")) || (st = dalloc(&s.sw, n * r * r, "sw")) ||
+            (st = dalloc(&s.u, n * r * n0, "u")) ||
+            (st = dalloc(&s.ws, int64_t(p->ws_bytes / sizeof(float2)), "workspace"))) {
             free_plan(p);
             return st;
         }
-    const int64_t nv = max_nrhs_chunk * p->d.n_amp;
-    p->ws_bytes = size_t(2) * size_t(N * r) * size_t(nv) * sizeof(float2);
-    if ((st = dalloc(&p->ws, int64_t(p->ws_bytes / sizeof(float2)), "workspace"))) {
-        free_plan(p);
-        return st;
+        for (int i = 0; i < nx; i++)
+            if ((st = dalloc(&s.xfer[i], n * 2 * r * r, "xfer"))) {
+                free_plan(p);
+                return st;
+            }
     }
     if ((e = cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming)) != cudaSuccess) {
         free_plan(p);
@@ -354,19 +533,107 @@ bf_status_t bf_plan_alloc(const bf_desc_t* meta, int device, int64_t max_nrhs_ch
     return BF_OK;
 }
 
+bf_status_t upload_desc(const bf_desc_t* desc, bf_plan_t p);
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// internal helpers for the streaming builder (bf_build.cpp)
+// ---------------------------------------------------------------------------
+bf_status_t bfp_stage_dst(bf_plan_t p, int shard, int32_t stage, int64_t begin, int64_t count, void** dst)
+{
+    if (!p || !dst) return fail(BF_ERR_INVALID_ARG, "NULL argument");
+    if (p->finalized) return fail(BF_ERR_STATE, "plan already finalized");
+    if (shard < 0 || shard >= int(p->sh.size())) return fail(BF_ERR_INVALID_ARG, "bad shard %d", shard);
+    const int slot = slot_of(p, stage);
+    if (slot < 0) return fail(BF_ERR_INVALID_ARG, "bad stage id %d", stage);
+    if (begin < 0 || count < 0 || begin + count > stage_blocks(p, stage))
+        return fail(BF_ERR_INVALID_ARG, "block range [%lld,%lld) out of [0,%lld)", (long long)begin,
+                    (long long)(begin + count), (long long)stage_blocks(p, stage));
+    *dst = stage_base(p->sh[shard], stage) + begin * stage_elems(p, stage);
+    p->uploaded[shard][slot] += count;
+    return BF_OK;
+}
+
+int bfp_device(bf_plan_t p) { return p ? p->device : -1; }
+int bfp_num_shards(bf_plan_t p) { return p ? int(p->sh.size()) : 0; }
+int bfp_rank(bf_plan_t p) { return p ? p->rank : 0; }
+
+bf_status_t bfp_fail(bf_status_t s, const char* msg) { return fail(s, "%s", msg); }
+
+bf_status_t bfp_plan_alloc_sharded(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk, int world, int rank,
+                                   int mode, const void* nccl_id, bf_plan_t* out)
+{
+    bf_status_t st = alloc_plan(meta, device, max_nrhs_chunk, world, rank, mode, out);
+    if (st != BF_OK || mode != BF_SHARD_NCCL) return st;
+    Nccl& n = nccl();
+    if (!n.ok || !nccl_id) {
+        free_plan(*out);
+        *out = nullptr;
+        return n.ok ? fail(BF_ERR_INVALID_ARG, "nccl_unique_id is NULL")
+                    : fail(BF_ERR_NCCL, "NCCL library not found (set BF_NCCL_LIB)");
+    }
+    DeviceGuard dg(device);
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof id);
+    ncclResult_t r = n.CommInitRank(&(*out)->comm, world, id, rank);
+    if (r) {
+        (*out)->comm = nullptr;
+        free_plan(*out);
+        *out = nullptr;
+        return nccl_fail(r, "ncclCommInitRank");
+    }
+    return BF_OK;
+}
+
+void bfp_plan_free(bf_plan_t p) { free_plan(p); }
+
+// ---------------------------------------------------------------------------
+// ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int32_t bf_abi_version(void) { return BF_ABI_VERSION; }
+
+const char* bf_last_error(void) { return g_err.c_str(); }
+
+bf_status_t bf_nccl_get_unique_id(void* id128)
+{
+    if (!id128) return fail(BF_ERR_INVALID_ARG, "id is NULL");
+    Nccl& n = nccl();
+    if (!n.ok) return fail(BF_ERR_NCCL, "NCCL library not found (set BF_NCCL_LIB)");
+    ncclUniqueId id;
+    ncclResult_t r = n.GetUniqueId(&id);
+    if (r) return nccl_fail(r, "ncclGetUniqueId");
+    memcpy(id128, &id, sizeof id);
+    return BF_OK;
+}
+
+bf_status_t bf_plan_alloc(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk, bf_plan_t* out)
+{
+    return alloc_plan(meta, device, max_nrhs_chunk, 1, 0, BF_SHARD_NONE, out);
+}
+
+bf_status_t bf_plan_alloc_sharded(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk, int32_t rank,
+                                  int32_t world, const void* nccl_unique_id, bf_plan_t* out)
+{
+    return bfp_plan_alloc_sharded(meta, device, max_nrhs_chunk, world, rank, BF_SHARD_NCCL, nccl_unique_id, out);
+}
+
 bf_status_t bf_plan_upload(bf_plan_t p, int32_t stage, int64_t block_begin, int64_t block_count, const bf_c64* src,
                            int32_t src_memory)
 {
     if (!p || (!src && block_count > 0)) return fail(BF_ERR_INVALID_ARG, "NULL argument");
     if (src_memory != BF_MEM_HOST && src_memory != BF_MEM_DEVICE)
         return fail(BF_ERR_INVALID_ARG, "src_memory=%d", src_memory);
+    if (p->sh.size() != 1) return fail(BF_ERR_STATE, "emulated plans are built by bf_plan_build_fio_emulated");
     DeviceGuard g(p->device);
     void* dst = nullptr;
-    bf_status_t st = bfp_stage_dst(p, stage, block_begin, block_count, &dst);
+    bf_status_t st = bfp_stage_dst(p, 0, stage, block_begin, block_count, &dst);
     if (st != BF_OK) return st;
     const size_t bytes = size_t(block_count) * size_t(stage_elems(p, stage)) * sizeof(float2);
-    cudaError_t e = cudaMemcpy(dst, src, bytes, src_memory == BF_MEM_HOST ? cudaMemcpyHostToDevice
-                                                                          : cudaMemcpyDeviceToDevice);
+    cudaError_t e = cudaMemcpy(dst, src, bytes,
+                               src_memory == BF_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(upload)");
     return BF_OK;
 }
@@ -375,13 +642,14 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
     if (p->finalized) return fail(BF_ERR_STATE, "plan already finalized");
-    const int nx = int(p->xfer.size());
-    for (int slot = 0; slot < 5 + nx; slot++) {
-        const int stage = slot < 5 ? slot : BF_STAGE_XFER0 + (slot - 5);
-        if (p->uploaded[slot] < stage_blocks(p, stage))
-            return fail(BF_ERR_STATE, "stage %d: %lld of %lld blocks uploaded", stage, (long long)p->uploaded[slot],
-                        (long long)stage_blocks(p, stage));
-    }
+    const int nx = int(p->sh[0].xfer.size());
+    for (size_t i = 0; i < p->sh.size(); i++)
+        for (int slot = 0; slot < 5 + nx; slot++) {
+            const int stage = slot < 5 ? slot : BF_STAGE_XFER0 + (slot - 5);
+            if (p->uploaded[i][slot] < stage_blocks(p, stage))
+                return fail(BF_ERR_STATE, "shard %zu stage %d: %lld of %lld blocks uploaded", i, stage,
+                            (long long)p->uploaded[i][slot], (long long)stage_blocks(p, stage));
+        }
     DeviceGuard g(p->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
@@ -391,31 +659,26 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
 
 bf_status_t bf_plan_create(const bf_desc_t* desc, int device, int64_t max_nrhs_chunk, bf_plan_t* out)
 {
-    bf_status_t st = validate_shape(desc);
-    if (st != BF_OK) return st;
-    const int nx = desc->log2n - 2 * desc->log2leaf;
-    if (!desc->amp_a || !desc->amp_b || !desc->v0 || !desc->sw || !desc->u || (nx > 0 && !desc->xfer))
-        return fail(BF_ERR_INVALID_ARG, "a factor array pointer is NULL");
-    for (int i = 0; i < nx; i++)
-        if (!desc->xfer[i]) return fail(BF_ERR_INVALID_ARG, "xfer[%d] is NULL", i);
+    if (!out) return fail(BF_ERR_INVALID_ARG, "out is NULL");
     bf_plan_t p = nullptr;
-    if ((st = bf_plan_alloc(desc, device, max_nrhs_chunk, &p)) != BF_OK) return st;
-    const int mem = desc->memory;
-    const int64_t N = p->d.N;
-    if ((st = bf_plan_upload(p, BF_STAGE_AMP_A, 0, p->d.n_amp, desc->amp_a, mem)) ||
-        (st = bf_plan_upload(p, BF_STAGE_AMP_B, 0, p->d.n_amp, desc->amp_b, mem)) ||
-        (st = bf_plan_upload(p, BF_STAGE_V0, 0, N, desc->v0, mem)) ||
-        (st = bf_plan_upload(p, BF_STAGE_SW, 0, N, desc->sw, mem)) ||
-        (st = bf_plan_upload(p, BF_STAGE_U, 0, N, desc->u, mem))) {
+    bf_status_t st = bf_plan_alloc(desc, device, max_nrhs_chunk, &p);
+    if (st != BF_OK) return st;
+    if ((st = upload_desc(desc, p)) != BF_OK) {
         free_plan(p);
         return st;
     }
-    for (int i = 0; i < nx; i++)
-        if ((st = bf_plan_upload(p, BF_STAGE_XFER0 + i, 0, N, desc->xfer[i], mem))) {
-            free_plan(p);
-            return st;
-        }
-    if ((st = bf_plan_finalize(p))) {
+    *out = p;
+    return BF_OK;
+}
+
+bf_status_t bf_plan_create_sharded(const bf_desc_t* local, int device, int64_t max_nrhs_chunk, int32_t rank,
+                                   int32_t world, const void* nccl_unique_id, bf_plan_t* out)
+{
+    if (!out) return fail(BF_ERR_INVALID_ARG, "out is NULL");
+    bf_plan_t p = nullptr;
+    bf_status_t st = bf_plan_alloc_sharded(local, device, max_nrhs_chunk, rank, world, nccl_unique_id, &p);
+    if (st != BF_OK) return st;
+    if ((st = upload_desc(local, p)) != BF_OK) {
         free_plan(p);
         return st;
     }
@@ -426,7 +689,7 @@ bf_status_t bf_plan_create(const bf_desc_t* desc, int device, int64_t max_nrhs_c
 size_t bf_workspace_bytes(bf_plan_t p, int64_t nrhs_chunk)
 {
     if (!p || nrhs_chunk < 1) return 0;
-    return size_t(2) * size_t(p->d.N * p->d.R) * size_t(nrhs_chunk * p->d.n_amp) * sizeof(float2);
+    return size_t(2) * size_t(p->nloc() * p->d.R) * size_t(nrhs_chunk * p->d.n_amp) * sizeof(float2);
 }
 
 bf_status_t bf_apply_ex(bf_plan_t p, const bf_c64* F, int64_t ldf, bf_c64* G, int64_t ldg, int64_t nrhs,
@@ -437,13 +700,15 @@ bf_status_t bf_apply_ex(bf_plan_t p, const bf_c64* F, int64_t ldf, bf_c64* G, in
     if (nrhs < 0) return fail(BF_ERR_INVALID_ARG, "nrhs=%lld < 0", (long long)nrhs);
     if (nrhs == 0) return BF_OK;
     if (!F || !G) return fail(BF_ERR_INVALID_ARG, "F or G is NULL");
-    if (ldf < p->d.N || ldg < p->d.N)
-        return fail(BF_ERR_ALIGNMENT, "ldf=%lld / ldg=%lld < N=%lld", (long long)ldf, (long long)ldg,
-                    (long long)p->d.N);
+    const int64_t rows = (p->mode == BF_SHARD_NCCL) ? p->nloc() : p->d.N;
+    if (ldf < rows || ldg < rows)
+        return fail(BF_ERR_ALIGNMENT, "ldf=%lld / ldg=%lld < rows=%lld", (long long)ldf, (long long)ldg,
+                    (long long)rows);
     if ((reinterpret_cast<uintptr_t>(F) | reinterpret_cast<uintptr_t>(G)) % 8)
         return fail(BF_ERR_ALIGNMENT, "F/G not 8-byte aligned");
-    float2* ws = p->ws;
+    float2* ws = p->sh[0].ws;
     if (workspace) {
+        if (p->mode == BF_SHARD_EMULATED) return fail(BF_ERR_NOT_SUPPORTED, "emulated plans use their own workspace");
         if (reinterpret_cast<uintptr_t>(workspace) % 16) return fail(BF_ERR_ALIGNMENT, "workspace not 16-byte aligned");
         if (workspace_bytes < bf_workspace_bytes(p, std::min(nrhs, p->max_chunk)))
             return fail(BF_ERR_INVALID_ARG, "workspace of %zu B < %zu B", workspace_bytes,
@@ -453,7 +718,7 @@ bf_status_t bf_apply_ex(bf_plan_t p, const bf_c64* F, int64_t ldf, bf_c64* G, in
     // F and G must not alias
     const char* f0 = reinterpret_cast<const char*>(F);
     const char* g0 = reinterpret_cast<const char*>(G);
-    const size_t fb = size_t((nrhs - 1) * ldf + p->d.N) * 8, gb = size_t((nrhs - 1) * ldg + p->d.N) * 8;
+    const size_t fb = size_t((nrhs - 1) * ldf + rows) * 8, gb = size_t((nrhs - 1) * ldg + rows) * 8;
     if (f0 < g0 + gb && g0 < f0 + fb) return fail(BF_ERR_INVALID_ARG, "F and G overlap");
     DeviceGuard g(p->device);
     return apply_impl(p, reinterpret_cast<const float2*>(F), ldf, reinterpret_cast<float2*>(G), ldg, nrhs, ws,
@@ -463,7 +728,8 @@ bf_status_t bf_apply_ex(bf_plan_t p, const bf_c64* F, int64_t ldf, bf_c64* G, in
 bf_status_t bf_apply(bf_plan_t p, const bf_c64* F, bf_c64* G, int64_t nrhs, void* stream)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
-    return bf_apply_ex(p, F, p->d.N, G, p->d.N, nrhs, nullptr, 0, stream);
+    const int64_t rows = (p->mode == BF_SHARD_NCCL) ? p->nloc() : p->d.N;
+    return bf_apply_ex(p, F, rows, G, rows, nrhs, nullptr, 0, stream);
 }
 
 bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int64_t nrhs, void* stream)
@@ -473,18 +739,18 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
     if (nrhs < 0 || (nrhs > 0 && (!F_host || !G_host))) return fail(BF_ERR_INVALID_ARG, "bad arguments");
     if (nrhs == 0) return BF_OK;
     DeviceGuard g(p->device);
-    const int64_t N = p->d.N, chunk = p->max_chunk;
+    const int64_t rows = (p->mode == BF_SHARD_NCCL) ? p->nloc() : p->d.N, chunk = p->max_chunk;
     bf_status_t st;
-    if (!p->dF && ((st = dalloc(&p->dF, N * chunk, "e2e F")) || (st = dalloc(&p->dG, N * chunk, "e2e G"))))
+    if (!p->dF && ((st = dalloc(&p->dF, rows * chunk, "e2e F")) || (st = dalloc(&p->dG, rows * chunk, "e2e G"))))
         return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     for (int64_t c0 = 0; c0 < nrhs; c0 += chunk) {
         const int64_t nc = std::min(chunk, nrhs - c0);
-        const size_t bytes = size_t(N * nc) * sizeof(float2);
-        cudaError_t e = cudaMemcpyAsync(p->dF, F_host + c0 * N, bytes, cudaMemcpyHostToDevice, s);
+        const size_t bytes = size_t(rows * nc) * sizeof(float2);
+        cudaError_t e = cudaMemcpyAsync(p->dF, F_host + c0 * rows, bytes, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e, "H2D");
-        if ((st = apply_impl(p, p->dF, N, p->dG, N, nc, p->ws, s)) != BF_OK) return st;
-        e = cudaMemcpyAsync(G_host + c0 * N, p->dG, bytes, cudaMemcpyDeviceToHost, s);
+        if ((st = apply_impl(p, p->dF, rows, p->dG, rows, nc, p->sh[0].ws, s)) != BF_OK) return st;
+        e = cudaMemcpyAsync(G_host + c0 * rows, p->dG, bytes, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return cuda_fail(e, "D2H");
     }
     cudaError_t e = cudaStreamSynchronize(s);
@@ -495,26 +761,33 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
 bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
 {
     if (!p || !info) return fail(BF_ERR_INVALID_ARG, "NULL argument");
-    const int64_t N = p->d.N, r = p->d.R, n0 = int64_t(1) << p->d.l0;
-    const int nx = int(p->xfer.size());
+    const int64_t n = p->nloc(), r = p->d.R, n0 = int64_t(1) << p->d.l0;
+    const int nx = int(p->sh[0].xfer.size());
+    const int64_t nsh = int64_t(p->sh.size());
     info->log2n = p->d.LN;
     info->log2leaf = p->d.l0;
     info->rank = p->d.R;
     info->n_amp = p->d.n_amp;
     info->switch_level = p->d.h;
     info->n_xfer = nx;
-    info->n = N;
+    info->n = p->d.N;
     info->max_nrhs_chunk = p->max_chunk;
-    info->factor_bytes = 8 * (2 * p->d.n_amp * N + 2 * N * r * n0 + N * r * r + int64_t(nx) * N * 2 * r * r);
-    info->workspace_bytes = int64_t(p->ws_bytes);
-    const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp));
-    info->launches_per_chunk = int32_t(st.size());
+    info->factor_bytes = nsh * 8 * (2 * p->d.n_amp * n + 2 * n * r * n0 + n * r * r + int64_t(nx) * n * 2 * r * r);
+    info->workspace_bytes = nsh * int64_t(p->ws_bytes);
+    const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp), p->mode != BF_SHARD_NONE);
+    info->launches_per_chunk = 0;
     for (int i = 0; i < BF_NUM_KCLASS; i++) info->class_launches[i] = info->class_levels[i] = 0;
     for (const auto& x : st) {
-        info->class_launches[x.cls] += 1;
-        info->class_levels[x.cls] += x.levels;
+        const int mult = (x.kind == Step::EXCHANGE) ? 1 : int(nsh);   // emulated: every shard launches
+        info->class_launches[x.cls] += mult;
+        info->class_levels[x.cls] += mult * x.levels;
+        if (x.kind != Step::EXCHANGE) info->launches_per_chunk += mult;
     }
     info->device = p->device;
+    info->world = p->world;
+    info->shard_rank = p->rank;
+    info->sharding = p->mode;
+    info->rows_local = (p->mode == BF_SHARD_NCCL) ? n : p->d.N;
     return BF_OK;
 }
 
@@ -569,4 +842,53 @@ bf_status_t bf_plan_destroy(bf_plan_t p)
     return BF_OK;
 }
 
+bf_status_t bf_shard_pairs(int32_t log2n, int32_t log2leaf, int32_t world, int32_t rank, int32_t which, int64_t* out)
+{
+    bf_desc_t d{};
+    d.abi_version = BF_ABI_VERSION;
+    d.log2n = log2n;
+    d.log2leaf = log2leaf;
+    bf_status_t st = validate_sharding(&d, world, rank);
+    if (st != BF_OK) return st;
+    if (!out || which < 0 || which > 2) return fail(BF_ERR_INVALID_ARG, "bad arguments");
+    int g = 0;
+    while ((1 << g) < world) g++;
+    const int h = log2n / 2;
+    const int64_t n = (int64_t(1) << log2n) >> g;
+    for (int64_t loc = 0; loc < n; loc++) {
+        if (which == 0)   // send buffer = first-half local order at level h
+            out[loc] = bfs::first_half_global(loc, log2n, h, g, rank);
+        else if (which == 2)   // second-half local order at level h
+            out[loc] = bfs::second_half_global(loc, log2n, g, rank);
+        else   // receive buffer: position recv_index(p) holds second-half local pair p
+            out[bfs::recv_index(loc, h, h - g)] = bfs::second_half_global(loc, log2n, g, rank);
+    }
+    return BF_OK;
+}
+
 }  // extern "C"
+
+namespace {
+
+bf_status_t upload_desc(const bf_desc_t* desc, bf_plan_t p)
+{
+    const int nx = desc->log2n - 2 * desc->log2leaf;
+    if (!desc->amp_a || !desc->amp_b || !desc->v0 || !desc->sw || !desc->u || (nx > 0 && !desc->xfer))
+        return fail(BF_ERR_INVALID_ARG, "a factor array pointer is NULL");
+    for (int i = 0; i < nx; i++)
+        if (!desc->xfer[i]) return fail(BF_ERR_INVALID_ARG, "xfer[%d] is NULL", i);
+    const int mem = desc->memory;
+    const int64_t n = p->nloc();
+    bf_status_t st;
+    if ((st = bf_plan_upload(p, BF_STAGE_AMP_A, 0, p->d.n_amp, desc->amp_a, mem)) ||
+        (st = bf_plan_upload(p, BF_STAGE_AMP_B, 0, p->d.n_amp, desc->amp_b, mem)) ||
+        (st = bf_plan_upload(p, BF_STAGE_V0, 0, n, desc->v0, mem)) ||
+        (st = bf_plan_upload(p, BF_STAGE_SW, 0, n, desc->sw, mem)) ||
+        (st = bf_plan_upload(p, BF_STAGE_U, 0, n, desc->u, mem)))
+        return st;
+    for (int i = 0; i < nx; i++)
+        if ((st = bf_plan_upload(p, BF_STAGE_XFER0 + i, 0, n, desc->xfer[i], mem))) return st;
+    return bf_plan_finalize(p);
+}
+
+}  // namespace
