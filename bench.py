@@ -37,12 +37,19 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
 def _peaks():
+    """HBM GB/s and the TF32 tensor peak (TFLOP/s) with their sources.  TF32 = the measured sustained
+    cuBLAS bf16 rate x the guide's nominal tf32/bf16 ratio (1.1 / 2.25): the kernels run inside a
+    ~100 ms step under the power cap (B200_PROFILING.md)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        hbm, src = float(p["hbm_gbs"]), "measured"
+        bf16 = float(p.get("bf16_tflops_sustained", p["bf16_tflops"]))
+        tsrc = "MEASURED_PEAKS.json bf16_tflops_sustained x 1.1/2.25 (nominal tf32/bf16)"
     except Exception:
-        return 6650.0, "fallback"
+        hbm, src = 6650.0, "fallback"
+        bf16, tsrc = 1400.0, "fallback sustained bf16 1.4 PF x 1.1/2.25"
+    return hbm, src, bf16 * 1.1 / 2.25, tsrc
 
 
 class ClockSampler:
@@ -97,7 +104,8 @@ class ClockSampler:
 def stage_model(w, nvec, info):
     """Algorithmic flops and bytes per launch of each kernel class.
     Transfer classes: a launch performs class_levels/class_launches fused levels; each launch reads and
-    writes the coefficient array once; the switch adds r x r per pair."""
+    writes the coefficient array once.  The switch is folded into the level-h blocks at plan finalization,
+    so it adds no work of its own."""
     N, n0, r, na, nrhs = w.n, w.leaf, w.rank, w.n_amp, nvec // w.n_amp
     c = 8  # bytes per complex64
     out = {
@@ -109,9 +117,8 @@ def stage_model(w, nvec, info):
         if n == 0:
             out[k] = (0, 0)
             continue
-        sw = 1 if k == "xfer_switch" else 0
-        flops = (lv * 16 * N * r * r * nvec + sw * 8 * N * r * r * nvec) / n
-        byts = c * (2 * N * r * nvec) + c * (lv * 2 * N * r * r + sw * N * r * r) / n
+        flops = lv * 16 * N * r * r * nvec / n
+        byts = c * (2 * N * r * nvec) + c * lv * 2 * N * r * r / n
         out[k] = (flops, byts)
     return out
 
@@ -248,33 +255,45 @@ def main():
     value = w.n * w.nrhs * jobs / (ms / 1e3)
 
     # ---- roofline of the dominant kernel class ----
-    hbm, hbm_src = _peaks()
+    hbm, hbm_src, tf32, tf32_src = _peaks()
     wl = w.with_(log2n=w.log2n - (world.bit_length() - 1)) if args.index_shard else w   # this rank's share
     model = stage_model(wl, min(chunk, w.nrhs) * w.n_amp, info)
     # the level-h exchange moves (G-1)/G of the local coefficients out and as much in
     model["exchange"] = (0, 2 * 8 * wl.n * w.rank * min(chunk, w.nrhs) * w.n_amp * (world - 1) // world)
+    tc_classes = set(info["tc_classes"])
+
+    def times(k):
+        """(compute seconds, hbm seconds) of one launch of class k at its peaks.  Tensor-core classes
+        issue 3 TF32 products per FP32-accurate product (3xTF32)."""
+        f, b = model[k]
+        tcomp = 3 * f / (tf32 * 1e12) if k in tc_classes else f / (FP32_PEAK_TFLOPS * 1e12)
+        return tcomp, b / (hbm * 1e9)
+
     dom = max((k for k in ktimes if k != "exchange"), key=lambda k: ktimes[k][0])   # largest share of the step
     dms, dn = ktimes[dom]
     flops, byts = model[dom]
     avg_s = dms / dn / 1e3
-    t_alu, t_hbm = flops / (FP32_PEAK_TFLOPS * 1e12), byts / (hbm * 1e9)
-    if t_alu >= t_hbm:
-        roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "peak_source": "FP32 FFMA from unit counts: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 5)"}
-    else:
+    t_comp, t_hbm = times(dom)
+    if t_hbm >= t_comp:
         roof = {"bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm, "unit": "GB/s",
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
+    elif dom in tc_classes:
+        roof = {"bound": "tensor", "achieved": 3 * flops / avg_s / 1e12, "peak": tf32, "unit": "TFLOP/s",
+                "peak_source": tf32_src + "; achieved counts the 3 TF32 passes of each algorithmic FP32 flop"}
+    else:
+        roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "peak_source": "FP32 FFMA from unit counts: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 5)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
     roof["kernel"] = dom
+    roof["tensor_cores"] = dom in tc_classes
     roof["avg_launch_ms"] = avg_s * 1e3
     roof["share_of_step"] = dms / (ms * args.steps)
     # whole-step roofline fractions (level-by-level and fused), DESIGN.md section 5
     tot_f = sum(model[k][0] * ktimes[k][1] for k in model) / args.steps
-    lbl = sum(max(model[k][0] / (FP32_PEAK_TFLOPS * 1e12), model[k][1] / (hbm * 1e9)) * ktimes[k][1]
-              for k in model if k != "exchange") / args.steps
-    fused = max(tot_f / (FP32_PEAK_TFLOPS * 1e12),
-                (16 * wl.n * w.nrhs + info["factor_bytes"]) / (hbm * 1e9))
+    lbl = sum(max(times(k)) * ktimes[k][1] for k in model if k != "exchange") / args.steps
+    comp = sum(times(k)[0] * ktimes[k][1] for k in model if k != "exchange") / args.steps
+    fused = max(comp, (16 * wl.n * w.nrhs + info["factor_bytes"]) / (hbm * 1e9))
 
     # ---- end to end: host buffers through the C ABI (bf_apply_host), copies inside the timed region ----
     e2e = None
@@ -305,7 +324,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if args.index_shard else "weak",
-            "vs_baseline": None, "dtype": "c64 (fp32 FFMA)",
+            "vs_baseline": None,
+            "dtype": "c64 (3xTF32 tcgen05 and FP32 FFMA, FP32 accumulation)" if tc_classes else "c64 (fp32 FFMA)",
             "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel; factors from the host builder)",
             "config": {"workload": args.config, "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
                        "nrhs_per_gpu": w.nrhs if not args.index_shard else w.nrhs,
@@ -313,7 +333,8 @@ def main():
                        "parallelism": (f"index-sharded x{world} (NCCL all-to-all at level h)" if args.index_shard
                                        else f"rhs-sharded x{world} (no collective)"),
                        "l2": "no flush: the working set (F 2.1 GB, coefficients 43 GB/level, factors 25 GB) "
-                             "exceeds the 126 MB L2"},
+                             "exceeds the 126 MB L2",
+                       "tensor_core_classes": info["tc_classes"], "tc_weight_bytes": info["tc_weight_bytes"]},
             "roofline": roof,
             "step_roofline": {"level_by_level_ms": lbl * 1e3, "fused_ms": fused * 1e3,
                               "frac_level_by_level": lbl * 1e3 / ms, "frac_fused": fused * 1e3 / ms,

@@ -118,6 +118,9 @@ typedef struct {
     int32_t shard_rank;          /* this plan's shard (BF_SHARD_NCCL) */
     int32_t sharding;            /* BF_SHARD_NONE / BF_SHARD_NCCL / BF_SHARD_EMULATED */
     int64_t rows_local;          /* rows of F and G bf_apply expects: N, or N/world for BF_SHARD_NCCL */
+    int64_t tc_weight_bytes;     /* device bytes of the tensor-core leaf weight images (0 if not built) */
+    int32_t tc_class_mask;       /* bit c set: kernel class c (bf_plan_timing numbering) runs on the tensor
+                                    cores for a full chunk of max_nrhs_chunk columns */
 } bf_plan_info_t;
 
 /* index sharding modes */
@@ -176,6 +179,15 @@ bf_status_t bf_plan_get_info(bf_plan_t plan, bf_plan_info_t *info);
 #define BF_NUM_KCLASS 6
 bf_status_t bf_plan_set_timing(bf_plan_t plan, int32_t enable);
 bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
+
+/* Plan options (take effect at the next bf_apply; not thread-safe against an apply in flight).
+ *   BF_OPT_TENSOR_CORES  1 (default): stages whose vector batch makes them a dense contraction
+ *                        (nv = nrhs n_amp >= 64 per chunk, n0 in {32, 64}) run on the tcgen05
+ *                        tensor cores in 3xTF32 with FP32 accumulation;
+ *                        0: every stage runs the FP32 FFMA (SIMT) kernels.
+ * Returns BF_ERR_INVALID_ARG for an unknown option or value. */
+#define BF_OPT_TENSOR_CORES 1
+bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Wait for the plan's outstanding work, then free everything it owns. */
 bf_status_t bf_plan_destroy(bf_plan_t plan);

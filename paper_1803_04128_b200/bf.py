@@ -23,12 +23,13 @@ BF_STAGE_V0, BF_STAGE_SW, BF_STAGE_U, BF_STAGE_AMP_A, BF_STAGE_AMP_B, BF_STAGE_X
 BF_NUM_KCLASS = 6
 KCLASS_NAMES = ("s0", "xfer_first_half", "xfer_switch", "xfer_second_half", "sl", "exchange")
 BF_SHARD_NONE, BF_SHARD_NCCL, BF_SHARD_EMULATED = 0, 1, 2
+BF_OPT_TENSOR_CORES = 1
 STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALIGNMENT", 4: "BF_ERR_OOM",
           5: "BF_ERR_CUDA", 6: "BF_ERR_NCCL", 7: "BF_ERR_NOT_SUPPORTED", 8: "BF_ERR_STATE"}
 
 # every symbol include/*.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finalize", "bf_apply", "bf_apply_ex",
-           "bf_apply_host", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing",
+           "bf_apply_host", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing", "bf_plan_set_option",
            "bf_plan_destroy", "bf_last_error", "bf_abi_version", "bf_build_n_amp", "bf_build_amp", "bf_build_blocks",
            "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
            "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated")
@@ -54,7 +55,8 @@ class bf_plan_info_t(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_int64), ("launches_per_chunk", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("class_launches", ctypes.c_int32 * 6),
                 ("class_levels", ctypes.c_int32 * 6), ("world", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
-                ("sharding", ctypes.c_int32), ("rows_local", ctypes.c_int64)]
+                ("sharding", ctypes.c_int32), ("rows_local", ctypes.c_int64), ("tc_weight_bytes", ctypes.c_int64),
+                ("tc_class_mask", ctypes.c_int32)]
 
 
 class bf_fio_t(ctypes.Structure):
@@ -85,6 +87,7 @@ def lib():
             "bf_workspace_bytes": ([vp, i64], sz),
             "bf_plan_get_info": ([vp, P(bf_plan_info_t)], i32),
             "bf_plan_set_timing": ([vp, i32], i32),
+            "bf_plan_set_option": ([vp, i32, ctypes.c_int64], i32),
             "bf_plan_timing": ([vp, P(ctypes.c_double), P(i64)], i32),
             "bf_plan_destroy": ([vp], i32),
             "bf_last_error": ([], ctypes.c_char_p),
@@ -243,10 +246,17 @@ class Plan:
         out = {f: getattr(i, f) for f, _ in bf_plan_info_t._fields_}
         out["class_launches"] = dict(zip(KCLASS_NAMES, list(i.class_launches)))
         out["class_levels"] = dict(zip(KCLASS_NAMES, list(i.class_levels)))
+        out["tc_classes"] = [n for c, n in enumerate(KCLASS_NAMES) if i.tc_class_mask >> c & 1]
         return out
 
     def workspace_bytes(self, nrhs_chunk: int) -> int:
         return int(lib().bf_workspace_bytes(self._h, nrhs_chunk))
+
+    def set_option(self, option: int, value: int):
+        _check(lib().bf_plan_set_option(self._h, int(option), int(value)))
+
+    def set_tensor_cores(self, enable: bool):
+        self.set_option(BF_OPT_TENSOR_CORES, int(enable))
 
     def set_timing(self, enable: bool):
         _check(lib().bf_plan_set_timing(self._h, int(enable)))

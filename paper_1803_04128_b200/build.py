@@ -19,9 +19,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-march=x86-64-v3", "-ffp-contract=off", "-Wall"]
 
-CU_SOURCES = ["bf_kernels.cu", "bf_plan.cu"]
+CU_SOURCES = ["bf_kernels.cu", "bf_tc.cu", "bf_plan.cu"]
 CXX_SOURCES = ["bf_build.cpp"]
-HEADERS = ["bf_internal.h", "bf_plan_internal.h"]
+HEADERS = ["bf_internal.h", "bf_plan_internal.h", "bf_shard.h", "tc_sm100.cuh"]
 
 
 def _digest() -> str:

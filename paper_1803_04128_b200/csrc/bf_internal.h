@@ -21,20 +21,41 @@ bool rank_supported(int R);
 cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float2* V0,
                       float2* out, int nv, cudaStream_t s);
 
-// Transfer level l (eqn:2 / eqn:3): out[p](t) = sum_{c,s} W[p](t, c r + s) in[(a>>1) 2^(LN-l+1) + 2b + c](s);
-// with Sw != nullptr (only at l == h) the switch block Sw[p] is applied to the result.
+// Tensor-core leaf stages (bf_tc.cu).  They read the leaf weights in an expanded form built once at
+// plan finalization: real-embedded, split hi/lo, in the shared-memory tile image of the MMA
+// (leafx_floats(d) floats each for V0 and U).
+bool leaf_tc_shape(const Dims& d);
+int64_t leafx_floats(const Dims& d);
+cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U, float* V0x, float* Ux, cudaStream_t s);
+// S0 on the tensor cores: same contract as launch_s0, weights from V0x.
+bool s0_tc_supported(const Dims& d, int nv, int64_t ldf);
+cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x, float2* out,
+                         int nv, cudaStream_t s);
+
+// SL on the tensor cores: same contract as launch_sl, weights from Ux.
+bool sl_tc_supported(const Dims& d, int nv);
+cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const float2* ampa, float2* G, int64_t ldg,
+                         int nv, cudaStream_t s);
+
+// Transfer level l (eqn:2 / eqn:3): out[p](t) = sum_{c,s} W[p](t, c r + s) in[(a>>1) 2^(LN-l+1) + 2b + c](s)
+// (at l == h the switch is already folded into W).
 // rh > 0: `in` is a receive buffer of the index-sharded exchange (input pair p at bfs::recv_index(p, rh, rhg)).
-cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, const float2* Sw,
-                        int nv, cudaStream_t s, int rh = 0, int rhg = 0);
+cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, int nv, cudaStream_t s,
+                        int rh = 0, int rhg = 0);
 
 // Band of K (1 or 2) transfer levels l_first .. l_first+K-1 fused in shared memory; W[m] are the
-// weights of level l_first+m; with m_sw in 1..K the switch Sw is applied after band level m_sw.
+// weights of level l_first+m.
 bool band_supported(int R, int nv);
-cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W,
-                        const float2* Sw, int m_sw, int nv, cudaStream_t s, int rh = 0, int rhg = 0);
+cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W, int nv,
+                        cudaStream_t s, int rh = 0, int rhg = 0);
 
-// Switch alone (used when no transfer level precedes it, h == l0).
-cudaError_t launch_switch(const Dims& d, const float2* in, float2* out, const float2* Sw, int nv, cudaStream_t s);
+// Band of 2 transfer levels on the tensor cores (bf_tc.cu): same contract as launch_band with K = 2.
+bool band_tc_supported(const Dims& d, int nv);
+cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
+                           cudaStream_t s, int rh = 0, int rhg = 0);
+
+// Plan finalization: W[p] <- Sw[p] W[p] for npairs blocks (W column-major R x cols, Sw R x R).
+cudaError_t launch_fold_switch(const float2* Sw, float2* W, int64_t npairs, int R, int cols, cudaStream_t s);
 
 // SL (eqn:bf3 + eqn:tg): G[x, c] = sum_k a_k(x) sum_{b<n0} sum_t U[a n0 + b](j, t) in[a n0 + b](t)[c n_amp + k],
 // x = a n0 + j.

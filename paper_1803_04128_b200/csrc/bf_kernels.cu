@@ -176,12 +176,12 @@ __global__ void __launch_bounds__(256) s0_kernel(const float2* __restrict__ F, i
 // Transfer level (eqn:2 P:748-752 for l <= h, eqn:3 P:780-785 for l > h).
 // A butterfly unit u = P 2^(LN-l) + b reads the two pairs 2u, 2u+1 of level
 // l-1 (contiguous: [2 R][nv]) and writes the pairs (2P+e) 2^(LN-l) + b, e=0,1.
-// One thread: both outputs (2 R rows) x TN vectors.  With SW, the switch block
-// of each output pair is applied in registers before the store.
+// One thread: both outputs (2 R rows) x TN vectors.  (The switch, is folded into the
+// level-h blocks at plan finalization.)
 // ---------------------------------------------------------------------------
-template <int R, int TN, bool SW>
+template <int R, int TN>
 __global__ void __launch_bounds__(128) xfer_kernel(const float2* __restrict__ in, float2* __restrict__ out,
-                                                   const float2* __restrict__ Wl, const float2* __restrict__ Sw,
+                                                   const float2* __restrict__ Wl,
                                                    int LN, int l, int nv, int rh, int rhg)
 {
     const int64_t N = int64_t(1) << LN;
@@ -226,64 +226,10 @@ __global__ void __launch_bounds__(128) xfer_kernel(const float2* __restrict__ in
         float2 (&acc)[R][TN] = e ? acc1 : acc0;
         const int64_t p = e ? p1 : p0;
         float2* o = out + p * R * nv + vg * TN;
-        if constexpr (SW) {
-            const float2* S = Sw + p * R * R;   // column-major r x r: column s at s*R
-            float2 res[R][TN];
 #pragma unroll
-            for (int t = 0; t < R; t++)
-#pragma unroll
-                for (int i = 0; i < TN; i++) res[t][i] = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int s = 0; s < R; s++) {
-                float2 w[R];
-                ldc_ro<R>(w, S + s * R);
-#pragma unroll
-                for (int t = 0; t < R; t++)
-#pragma unroll
-                    for (int i = 0; i < TN; i++) cmac(res[t][i], w[t], acc[s][i]);
-            }
-#pragma unroll
-            for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, res[t]);
-        } else {
-#pragma unroll
-            for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, acc[t]);
-        }
+        for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, acc[t]);
     }
 }
-
-// Switch alone: out[p] = Sw[p] in[p] (only when h == l0).
-template <int R, int TN>
-__global__ void __launch_bounds__(128) switch_kernel(const float2* __restrict__ in, float2* __restrict__ out,
-                                                     const float2* __restrict__ Sw, int LN, int nv)
-{
-    const int64_t N = int64_t(1) << LN;
-    const int cpu = nv / TN;
-    const int64_t gc = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t p = gc / cpu;
-    if (p >= N) return;
-    const int vg = int(gc % cpu);
-    const float2* x = in + p * R * nv + vg * TN;
-    const float2* S = Sw + p * R * R;
-    float2 res[R][TN];
-#pragma unroll
-    for (int t = 0; t < R; t++)
-#pragma unroll
-        for (int i = 0; i < TN; i++) res[t][i] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int s = 0; s < R; s++) {
-        float2 xv[TN], w[R];
-        ldc_ro<TN>(xv, x + int64_t(s) * nv);
-        ldc_ro<R>(w, S + s * R);
-#pragma unroll
-        for (int t = 0; t < R; t++)
-#pragma unroll
-            for (int i = 0; i < TN; i++) cmac(res[t][i], w[t], xv[i]);
-    }
-    float2* o = out + p * R * nv + vg * TN;
-#pragma unroll
-    for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, res[t]);
-}
-
 
 // ---------------------------------------------------------------------------
 constexpr int S0T_VT = 128;   // vectors per tile
@@ -500,7 +446,7 @@ __global__ void __launch_bounds__(256, 2) sl_tile_kernel(const float2* __restric
 // tile into shared memory (cp.async), carried through the K levels in place,
 // and only the last level is written to HBM: the coefficient traffic of the
 // band is one read + one write instead of K of each.  The weights of all K
-// levels (and the switch blocks when the band contains level h) stay resident
+// levels stay resident
 // in shared memory while the CTA sweeps the vector tiles.
 //
 // In place: at band level m the unit (e', i) reads the physical slots
@@ -510,9 +456,7 @@ __global__ void __launch_bounds__(256, 2) sl_tile_kernel(const float2* __restric
 // one barrier per level suffices.
 // ---------------------------------------------------------------------------
 struct BandArgs {
-    const float2* W[4];   // weights of band levels 1..K (bf.h XFER layout)
-    const float2* Sw;     // switch blocks (level h), used when m_sw > 0
-    int m_sw;             // band level after which the switch is applied (1..K), 0 = none
+    const float2* W[4];   // weights of band levels 1..K (bf.h XFER layout; level h has the switch folded in)
     int rh, rhg;          // > 0: the input is a receive buffer of the index-sharded exchange (bf_shard.h)
 };
 
@@ -523,8 +467,7 @@ __host__ __device__ constexpr int band_vt() { return 1024 >> K; }   // 256 threa
 template <int R, int K>
 __host__ __device__ constexpr size_t band_smem_bytes()
 {
-    return (size_t((1 << K) * R * band_vt<K>()) + size_t(K * (1 << (K - 1)) * 4 * R * R) + size_t((1 << K) * R * R)) *
-           sizeof(float2);
+    return (size_t((1 << K) * R * band_vt<K>()) + size_t(K * (1 << (K - 1)) * 4 * R * R)) * sizeof(float2);
 }
 
 // One thread owns ONE output pair (e) of a unit x 4 vectors (R x 4 accumulators: each weight is reused
@@ -542,7 +485,6 @@ __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
     extern __shared__ float4 smem_band[];
     float2* X = reinterpret_cast<float2*>(smem_band);   // [P][R][VT]
     float2* Ws = X + P * R * VT;                         // [K][U][2R (k)][2R (e R + t)]
-    float2* Ss = Ws + K * U * 4 * R * R;                 // [P (E 2^(K-m_sw) + i)][R (s)][R (t)]
 
     const int lin = l_first - 1;   // input level
     const int shg = LN - lin - K;
@@ -561,16 +503,6 @@ __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
             Ws[(((m - 1) * U + uu) * 2 * R + k) * 2 * R + ee * R + t] = __ldg(args.W[m - 1] + p * 2 * R * R + k * R + t);
         }
     }
-    if (args.m_sw) {
-        const int m = args.m_sw, sh = LN - lin - m, ilog = K - m;
-        for (int idx = tid; idx < P * R * R; idx += 256) {
-            const int q = idx / (R * R), st = idx % (R * R);
-            const int E = q >> ilog, i = q & ((1 << ilog) - 1);
-            const int64_t p = (((a0 << m) + E) << sh) + (bq << ilog) + i;
-            Ss[idx] = __ldg(args.Sw + p * R * R + st);
-        }
-    }
-
     const int nvt = (nv + VT - 1) / VT;
     for (int vt = 0; vt < nvt; vt++) {
         const int v0 = vt * VT;
@@ -629,27 +561,8 @@ __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
                     dst = out + p * R * int64_t(nv) + v0;
                     rstride = nv;
                 }
-                if (m == args.m_sw) {
-                    // switch on the level-h pair this thread holds, one output row at a time
-                    // (the R x 4 inputs stay in registers; each row is stored as soon as it is formed)
-                    const float2* S = Ss + (((2 * ep + e) << (K - m)) + i) * R * R;
 #pragma unroll
-                    for (int t = 0; t < R; t++) {
-                        float2 res[TN];
-#pragma unroll
-                        for (int q = 0; q < TN; q++) res[q] = make_float2(0.f, 0.f);
-#pragma unroll
-                        for (int ss = 0; ss < R; ss++) {
-                            const float2 w = S[ss * R + t];
-#pragma unroll
-                            for (int q = 0; q < TN; q++) cmac(res[q], w, acc[ss][q]);
-                        }
-                        stq<VT / 2>(dst + t * rstride, col, res, lo_ok, hi_ok);
-                    }
-                } else {
-#pragma unroll
-                    for (int t = 0; t < R; t++) stq<VT / 2>(dst + t * rstride, col, acc[t], lo_ok, hi_ok);
-                }
+                for (int t = 0; t < R; t++) stq<VT / 2>(dst + t * rstride, col, acc[t], lo_ok, hi_ok);
             }
             if (m < K) __syncthreads();
         }
@@ -741,20 +654,12 @@ static cudaError_t s0_go(const Dims& d, const float2* F, int64_t ldf, const floa
     return cudaGetLastError();
 }
 
-template <int R, bool SW, int TN>
-static cudaError_t xfer_go(const Dims& d, int l, const float2* in, float2* out, const float2* W, const float2* Sw, int nv,
-                           int rh, int rhg, cudaStream_t s)
+template <int R, int TN>
+static cudaError_t xfer_go(const Dims& d, int l, const float2* in, float2* out, const float2* W, int nv, int rh, int rhg,
+                           cudaStream_t s)
 {
     const int64_t threads = (d.N / 2) * (nv / TN);
-    xfer_kernel<R, TN, SW><<<unsigned((threads + 127) / 128), 128, 0, s>>>(in, out, W, Sw, d.LN, l, nv, rh, rhg);
-    return cudaGetLastError();
-}
-
-template <int R, int TN>
-static cudaError_t sw_go(const Dims& d, const float2* in, float2* out, const float2* Sw, int nv, cudaStream_t s)
-{
-    const int64_t threads = d.N * (nv / TN);
-    switch_kernel<R, TN><<<unsigned((threads + 127) / 128), 128, 0, s>>>(in, out, Sw, d.LN, nv);
+    xfer_kernel<R, TN><<<unsigned((threads + 127) / 128), 128, 0, s>>>(in, out, W, d.LN, l, nv, rh, rhg);
     return cudaGetLastError();
 }
 
@@ -806,23 +711,12 @@ cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2*
     BF_DISPATCH_R(d.R, (s0_go<RR, 1>(d, F, ldf, ampb, V0, out, nv, s)))
 }
 
-cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, const float2* Sw, int nv,
-                        cudaStream_t s, int rh, int rhg)
+cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, int nv, cudaStream_t s,
+                        int rh, int rhg)
 {
     const int tn = pick_tn(nv, 2);
-    if (Sw) {
-        if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, true, 2>(d, l, in, out, W, Sw, nv, rh, rhg, s)))
-        BF_DISPATCH_R(d.R, (xfer_go<RR, true, 1>(d, l, in, out, W, Sw, nv, rh, rhg, s)))
-    }
-    if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, false, 2>(d, l, in, out, W, Sw, nv, rh, rhg, s)))
-    BF_DISPATCH_R(d.R, (xfer_go<RR, false, 1>(d, l, in, out, W, Sw, nv, rh, rhg, s)))
-}
-
-cudaError_t launch_switch(const Dims& d, const float2* in, float2* out, const float2* Sw, int nv, cudaStream_t s)
-{
-    const int tn = pick_tn(nv, 2);
-    if (tn == 2) BF_DISPATCH_R(d.R, (sw_go<RR, 2>(d, in, out, Sw, nv, s)))
-    BF_DISPATCH_R(d.R, (sw_go<RR, 1>(d, in, out, Sw, nv, s)))
+    if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, 2>(d, l, in, out, W, nv, rh, rhg, s)))
+    BF_DISPATCH_R(d.R, (xfer_go<RR, 1>(d, l, in, out, W, nv, rh, rhg, s)))
 }
 
 template <int R, int NA>
@@ -865,13 +759,11 @@ cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const fl
 bool band_supported(int R, int nv) { return (R == 6 || R == 8 || R == 10 || R == 12) && nv % 4 == 0 && nv >= 128; }
 
 template <int R, int K>
-static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W,
-                           const float2* Sw, int m_sw, int nv, cudaStream_t s, int rh, int rhg)
+static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
+                           cudaStream_t s, int rh, int rhg)
 {
     BandArgs a{};
     for (int m = 0; m < K; m++) a.W[m] = W[m];
-    a.Sw = Sw;
-    a.m_sw = m_sw;
     a.rh = rh;
     a.rhg = rhg;
     const size_t shm = band_smem_bytes<R, K>();
@@ -883,11 +775,11 @@ static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2*
     return cudaGetLastError();
 }
 
-cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W,
-                        const float2* Sw, int m_sw, int nv, cudaStream_t s, int rh, int rhg)
+cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W, int nv,
+                        cudaStream_t s, int rh, int rhg)
 {
 #define BF_BAND_CASE(RR, KK) \
-    case RR: return band_go<RR, KK>(d, l_first, in, out, W, Sw, m_sw, nv, s, rh, rhg);
+    case RR: return band_go<RR, KK>(d, l_first, in, out, W, nv, s, rh, rhg);
     if (K == 2) {
         switch (d.R) {
             BF_BAND_CASE(6, 2) BF_BAND_CASE(8, 2) BF_BAND_CASE(10, 2) BF_BAND_CASE(12, 2)
@@ -902,6 +794,47 @@ cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, flo
     }
 #undef BF_BAND_CASE
     return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// Plan finalization: fold the switch into the factor that produces level h.
+// The BF is the product U G^{L-1}..G^{h+1} M^h G^h..G^{l0+1} V (eqn:BFM); M^h is
+// block diagonal over the level-h pairs with the r x r blocks Sw[p], and the factor producing
+// level h has the same pairs as its block rows, so M^h G^h is again block diagonal with blocks
+// Sw[p] W[p] (r x cols).  One thread per (pair, column); FP64 accumulation, complex64 result,
+// written in place over W.
+// ---------------------------------------------------------------------------
+__global__ void fold_switch_kernel(const float2* __restrict__ Sw, float2* __restrict__ W, int64_t npairs, int R,
+                                   int cols)
+{
+    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= npairs * cols) return;
+    const int64_t p = g / cols;
+    const int k = int(g % cols);
+    float2* w = W + (p * cols + k) * R;   // column k of W[p] (column-major r x cols)
+    const float2* S = Sw + p * R * R;     // column-major r x r
+    double xr[16], xi[16];
+    for (int s = 0; s < R; s++) {
+        xr[s] = w[s].x;
+        xi[s] = w[s].y;
+    }
+    for (int t = 0; t < R; t++) {
+        double yr = 0, yi = 0;
+        for (int s = 0; s < R; s++) {
+            const float2 a = S[s * R + t];
+            yr += double(a.x) * xr[s] - double(a.y) * xi[s];
+            yi += double(a.x) * xi[s] + double(a.y) * xr[s];
+        }
+        w[t] = make_float2(float(yr), float(yi));
+    }
+}
+
+cudaError_t launch_fold_switch(const float2* Sw, float2* W, int64_t npairs, int R, int cols, cudaStream_t s)
+{
+    if (R > 16) return cudaErrorInvalidValue;
+    const int64_t n = npairs * cols;
+    fold_switch_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(Sw, W, npairs, R, cols);
+    return cudaGetLastError();
 }
 
 }  // namespace bfk

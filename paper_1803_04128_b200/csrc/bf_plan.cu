@@ -127,6 +127,8 @@ struct Shard {
     float2* sw = nullptr;
     float2* u = nullptr;
     std::vector<float2*> xfer;
+    float* v0x = nullptr;      // tensor-core image of V0 / U (bf_tc.cu), built at finalize when used
+    float* ux = nullptr;
     float2* ws = nullptr;      // two coefficient arrays of (N/G) R nv_max
 };
 
@@ -144,6 +146,7 @@ struct bf_plan_s {
     // end-to-end staging (lazily allocated by bf_apply_host)
     float2* dF = nullptr;
     float2* dG = nullptr;
+    bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -255,6 +258,8 @@ void free_plan(bf_plan_s* p)
         cudaFree(s.amp_b);
         cudaFree(s.v0);
         cudaFree(s.sw);
+        cudaFree(s.v0x);
+        cudaFree(s.ux);
         cudaFree(s.u);
         for (auto x : s.xfer) cudaFree(x);
         cudaFree(s.ws);
@@ -304,10 +309,9 @@ cudaError_t timed(bf_plan_s* p, int cls, cudaStream_t s, F&& launch)
 
 // One kernel launch of the apply: what it runs and how it is accounted.
 struct Step {
-    enum Kind { S0, SWITCH, XFER, BAND, SL, EXCHANGE } kind;
+    enum Kind { S0, XFER, BAND, SL, EXCHANGE } kind;
     int l_first = 0;   // XFER: the level; BAND: first level (global level numbering)
     int K = 1;         // BAND: levels fused
-    int m_sw = 0;      // BAND: band level after which the switch applies (0 = none)
     int cls = 0;       // bfk::KClass or KC_EXCHANGE
     int levels = 0;    // transfer levels this launch performs
 };
@@ -319,7 +323,7 @@ void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool
         const int last = l + K - 1;
         const bool has_h = (l <= d.h && d.h <= last);
         const int cls = has_h ? bfk::KC_SWITCH : (last < d.h ? bfk::KC_XFER1 : bfk::KC_XFER2);
-        st.push_back({band ? Step::BAND : Step::XFER, l, K, has_h ? d.h - l + 1 : 0, cls, K});
+        st.push_back({band ? Step::BAND : Step::XFER, l, K, cls, K});
         l += K;
     }
 }
@@ -331,17 +335,16 @@ void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool
 std::vector<Step> schedule(const bfk::Dims& d, int nv, bool sharded)
 {
     std::vector<Step> st;
-    st.push_back({Step::S0, 0, 1, 0, bfk::KC_S0, 0});
-    if (d.h == d.l0) st.push_back({Step::SWITCH, 0, 1, 0, bfk::KC_SWITCH, 0});
+    st.push_back({Step::S0, 0, 1, bfk::KC_S0, 0});
     const bool band = bfk::band_supported(d.R, nv);
     if (!sharded) {
         push_levels(st, d, d.l0 + 1, d.D, band);
     } else {
         push_levels(st, d, d.l0 + 1, d.h, band);
-        st.push_back({Step::EXCHANGE, 0, 1, 0, KC_EXCHANGE, 0});
+        st.push_back({Step::EXCHANGE, 0, 1, KC_EXCHANGE, 0});
         push_levels(st, d, d.h + 1, d.D, band);
     }
-    st.push_back({Step::SL, 0, 1, 0, bfk::KC_SL, 0});
+    st.push_back({Step::SL, 0, 1, bfk::KC_SL, 0});
     return st;
 }
 
@@ -401,22 +404,28 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
         const int rh = remap ? p->d.h : 0, rhg = remap ? p->d.h - p->g : 0;
         cudaError_t e = timed(p, stp.cls, s, [&]() -> cudaError_t {
             switch (stp.kind) {
-            case Step::S0: return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
-            case Step::SWITCH: return bfk::launch_switch(dl, in, out, sh.sw, nv, s);
+            case Step::S0:
+                if (p->tensor_cores && sh.v0x && bfk::s0_tc_supported(dl, nv, ldf))
+                    return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s);
+                return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
             case Step::XFER:
-                return bfk::launch_xfer(dl, lk, in, out, sh.xfer[stp.l_first - p->d.l0 - 1],
-                                        stp.l_first == p->d.h ? sh.sw : nullptr, nv, s, rh, rhg);
+                return bfk::launch_xfer(dl, lk, in, out, sh.xfer[stp.l_first - p->d.l0 - 1], nv, s, rh, rhg);
             case Step::BAND: {
                 const float2* W[2] = {sh.xfer[stp.l_first - p->d.l0 - 1],
                                       stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
-                return bfk::launch_band(dl, lk, stp.K, in, out, W, sh.sw, stp.m_sw, nv, s, rh, rhg);
+                if (stp.K == 2 && p->tensor_cores && bfk::band_tc_supported(dl, nv))
+                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg);
+                return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg);
             }
-            case Step::SL: return bfk::launch_sl(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
+            case Step::SL:
+                if (p->tensor_cores && sh.ux && bfk::sl_tc_supported(dl, nv))
+                    return bfk::launch_sl_tc(dl, in, sh.ux, sh.amp_a, G, ldg, nv, s);
+                return bfk::launch_sl(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
             default: return cudaErrorInvalidValue;
             }
         });
         if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-        if (stp.kind == Step::SWITCH || stp.kind == Step::XFER || stp.kind == Step::BAND) {
+        if (stp.kind == Step::XFER || stp.kind == Step::BAND) {
             cur = 1 - cur;
             remap = false;
         }
@@ -651,8 +660,39 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
                             (long long)p->uploaded[i][slot], (long long)stage_blocks(p, stage));
         }
     DeviceGuard g(p->device);
+    // fold the switch into the factor that produces level h: XFER_h, or V0 when h == l0 (no transfer level
+    // precedes h); the apply then has no separate switch product
+    for (Shard& s : p->sh) {
+        const int n0 = 1 << p->d.l0;
+        float2* target = (p->d.h > p->d.l0) ? s.xfer[p->d.h - p->d.l0 - 1] : s.v0;
+        const int cols = (p->d.h > p->d.l0) ? 2 * p->d.R : n0;
+        cudaError_t e = bfk::launch_fold_switch(s.sw, target, p->nloc(), p->d.R, cols, 0);
+        if (e != cudaSuccess) return cuda_fail(e, "switch fold");
+    }
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
+    for (Shard& s : p->sh) {   // the switch blocks now live inside the level-h factor
+        cudaFree(s.sw);
+        s.sw = nullptr;
+    }
+    // tensor-core leaf weights: only when a chunk can be a dense contraction (nv >= 64 vectors)
+    const bfk::Dims dl = p->local();
+    if (p->tensor_cores && bfk::leaf_tc_shape(dl) && p->max_chunk * p->d.n_amp >= 64) {
+        const size_t bytes = size_t(bfk::leafx_floats(dl)) * sizeof(float);
+        for (Shard& s : p->sh) {
+            if (cudaMalloc(&s.v0x, bytes) != cudaSuccess || cudaMalloc(&s.ux, bytes) != cudaSuccess) {
+                cudaGetLastError();   // not enough device memory: the SIMT leaf kernels serve this plan
+                cudaFree(s.v0x);
+                cudaFree(s.ux);
+                s.v0x = s.ux = nullptr;
+                continue;
+            }
+            e = bfk::expand_leaf_weights(dl, s.v0, s.u, s.v0x, s.ux, 0);
+            if (e != cudaSuccess) return cuda_fail(e, "leaf weight expansion");
+        }
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(e, "leaf weight expansion");
+    }
     p->finalized = true;
     return BF_OK;
 }
@@ -772,8 +812,24 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     info->n_xfer = nx;
     info->n = p->d.N;
     info->max_nrhs_chunk = p->max_chunk;
-    info->factor_bytes = nsh * 8 * (2 * p->d.n_amp * n + 2 * n * r * n0 + n * r * r + int64_t(nx) * n * 2 * r * r);
+    // the switch blocks are folded into the level-h factor at finalize (freed afterwards)
+    info->factor_bytes = nsh * 8 * (2 * p->d.n_amp * n + 2 * n * r * n0 + (p->finalized ? 0 : n * r * r) +
+                                    int64_t(nx) * n * 2 * r * r);
     info->workspace_bytes = nsh * int64_t(p->ws_bytes);
+    info->tc_weight_bytes = 0;
+    for (const Shard& s : p->sh)
+        if (s.v0x) info->tc_weight_bytes += 2 * bfk::leafx_floats(p->local()) * int64_t(sizeof(float));
+    {
+        const bfk::Dims dl = p->local();
+        const int nvf = int(p->max_chunk * p->d.n_amp);
+        int mask = 0;
+        if (p->tensor_cores && p->sh[0].v0x && bfk::s0_tc_supported(dl, nvf, dl.N)) mask |= 1 << bfk::KC_S0;
+        if (p->tensor_cores && p->sh[0].ux && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
+        if (p->tensor_cores && bfk::band_supported(dl.R, nvf) && bfk::band_tc_supported(dl, nvf))
+            for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE))
+                if (stp.kind == Step::BAND && stp.K == 2) mask |= 1 << stp.cls;
+        info->tc_class_mask = mask;
+    }
     const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp), p->mode != BF_SHARD_NONE);
     info->launches_per_chunk = 0;
     for (int i = 0; i < BF_NUM_KCLASS; i++) info->class_launches[i] = info->class_levels[i] = 0;
@@ -789,6 +845,17 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     info->sharding = p->mode;
     info->rows_local = (p->mode == BF_SHARD_NCCL) ? n : p->d.N;
     return BF_OK;
+}
+
+bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
+{
+    if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
+    if (option == BF_OPT_TENSOR_CORES) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_TENSOR_CORES takes 0 or 1");
+        p->tensor_cores = value != 0;
+        return BF_OK;
+    }
+    return fail(BF_ERR_INVALID_ARG, "unknown plan option");
 }
 
 bf_status_t bf_plan_set_timing(bf_plan_t p, int32_t enable)

@@ -1,0 +1,905 @@
+// bf_tc.cu -- tensor-core (tcgen05, 3xTF32) kernels of the IBF-MAT apply for large
+// vector batches (north_star: "Use tensor cores only where nrhs makes a level a real
+// dense contraction, and only if a 3xTF32 ... path keeps the error bound").
+//
+// Orientation: every stage is written as D[v][n] = sum_k A[v][k] B[n][k] with the
+// M = 128 rows of the MMA the VECTORS of one tile (v = c n_amp + k), so that the
+// accumulator row a thread reads back from TMEM (lane = v) is exactly one vector's
+// output coefficients and is stored to the coefficient array delta[pair][t][v] with
+// warp-coalesced 8-byte stores.  Complex products are real-embedded on the weight
+// side:  A[v][2s + c] = (x_s).c,  B[2t + c'][2s + c] = [[Wr, -Wi], [Wi, Wr]](c', c),
+// so D[v][2t + c'] = (W x)_t.c'.
+//
+// Leaf stages (S0, SL): the weights are used by every vector tile, so the plan expands
+// them ONCE at finalization (expand_leaf_weights) into the exact shared-memory image the
+// MMA reads -- real-embedded, split hi/lo, canonical K-major tiles -- and the kernels move
+// them with 1-D bulk copies (TMA engine).  Activations are split hi/lo by SIMT warps.
+//
+// Measured on B200 (tools/tc_probe2.cu, profiles/r1_tc_probe2.txt): a kind::tf32 MMA
+// (M=128, K=8) costs max(~45 clk, N/2 clk), so N >= 128 reaches 2048 MAC/clk/SM; and a
+// long accumulation chain in TMEM loses precision (768 chained MMAs: 1.3e-5 relative,
+// versus 3.7e-7 when the chain is cut every 12 MMAs and the partial sums are added in
+// FP32 registers).  Hence N = 128 tiles, accumulation chains of <= 24 MMAs (at most 8 of them
+// the large Ahi Bhi products, issued last) and FP32 register sums across chains here.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "bf_internal.h"
+#include "bf_shard.h"
+#include "tc_sm100.cuh"
+
+namespace bfk {
+
+namespace {
+
+__device__ __forceinline__ float2 cmul_tc(const float2 a, const float2 b)
+{
+    return make_float2(fmaf(a.x, b.x, -(a.y * b.y)), fmaf(a.x, b.y, a.y * b.x));
+}
+
+__device__ __forceinline__ void st_f4(uint8_t* base, uint32_t off, float4 v) { *reinterpret_cast<float4*>(base + off) = v; }
+
+template <int NCOLS>
+__host__ __device__ constexpr int tmem_cols_pow2()
+{
+    return NCOLS <= 32 ? 32 : NCOLS <= 64 ? 64 : NCOLS <= 128 ? 128 : NCOLS <= 256 ? 256 : 512;
+}
+
+// 3xTF32 pass order of every accumulation chain: the two small correction products (Alo Bhi,
+// Ahi Blo) first, while the accumulator is still small, then Ahi Bhi.  The tensor core's FP32
+// accumulation truncates; its error grows with the number of large partial sums added, so the
+// corrections-first order cuts the effective chain length to the Ahi Bhi steps.
+__device__ constexpr int kPassOrder[3] = {1, 2, 0};
+
+// real embedding of complex w for output part cp (0 = re, 1 = im) and input part c
+__device__ __forceinline__ float embed(float2 w, int cp, int c)
+{
+    return cp == 0 ? (c == 0 ? w.x : -w.y) : (c == 0 ? w.y : w.x);
+}
+
+}  // namespace
+
+// =============================================================================================
+// Expanded leaf weights (plan finalization)
+// =============================================================================================
+// S0: per leaf b the B matrix has rows n = (a, t, c') (n0 2r of them) and K = (j, c) (2 n0).  It is
+// stored as [leaf][n chunk of 128 rows][K chunk of 32][hi | lo][canonical K-major 128 x 32 tile].
+constexpr int S0X_NC = 128, S0X_KC = 32;
+constexpr int64_t S0X_TILE_FLOATS = int64_t(S0X_NC) * S0X_KC;
+
+int64_t leafx_floats(const Dims& d) { return d.N * int64_t(2 * d.R) * int64_t(2 << d.l0) * 2; }
+
+__global__ void expand_s0_kernel(const float2* __restrict__ V0, float* __restrict__ X, int LN, int l0, int R)
+{
+    const int n0 = 1 << l0;
+    const int64_t nleaf = (int64_t(1) << LN) >> l0;
+    const int rows = n0 * 2 * R, K = 2 * n0;
+    const int nch = rows / S0X_NC, kch = K / S0X_KC;
+    const int64_t total = nleaf * rows * int64_t(K);
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = g / (int64_t(rows) * K);
+        const int rem = int(g - b * rows * K);
+        const int n = rem / K, k = rem - n * K;
+        const int a = n / (2 * R), t = (n / 2) % R, cp = n & 1, j = k >> 1, c = k & 1;
+        const float2 w = V0[(int64_t(a) * nleaf + b) * (n0 * R) + int64_t(j) * R + t];
+        float hi, lo;
+        tc::split(embed(w, cp, c), hi, lo);
+        const int nc = n / S0X_NC, kc = k / S0X_KC;
+        float* tile = X + ((b * nch + nc) * kch + kc) * 2 * S0X_TILE_FLOATS;
+        const uint32_t off = tc::kmaj_off(n % S0X_NC, k % S0X_KC, S0X_NC) / 4;
+        tile[off] = hi;
+        tile[S0X_TILE_FLOATS + off] = lo;
+    }
+}
+
+// SL: per T_X leaf a the B matrix has rows n = (j, c') (2 n0) and K = (b, t, c) (n0 2r), stored as
+// [leaf][K chunk of KP pairs][hi | lo][canonical K-major 2 n0 x KP 2r tile].
+static int sl_kp(int R) { return R >= 12 ? 1 : 2; }
+
+__global__ void expand_sl_kernel(const float2* __restrict__ U, float* __restrict__ X, int LN, int l0, int R, int KP)
+{
+    const int n0 = 1 << l0;
+    const int64_t nleaf = (int64_t(1) << LN) >> l0;
+    const int rows = 2 * n0, K = n0 * 2 * R, KC = KP * 2 * R;
+    const int nch = n0 / KP;
+    const int64_t tile = int64_t(rows) * KC;
+    const int64_t total = nleaf * rows * int64_t(K);
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t a = g / (int64_t(rows) * K);
+        const int rem = int(g - a * rows * K);
+        const int n = rem / K, k = rem - n * K;
+        const int j = n >> 1, cp = n & 1, b = k / (2 * R), t = (k / 2) % R, c = k & 1;
+        const float2 w = U[(a * n0 + b) * (n0 * R) + int64_t(t) * n0 + j];
+        float hi, lo;
+        tc::split(embed(w, cp, c), hi, lo);
+        const int ch = b / KP, kk = k - ch * KC;
+        float* tl = X + ((a * nch + ch) * 2) * tile;
+        const uint32_t off = tc::kmaj_off(n, kk, rows) / 4;
+        tl[off] = hi;
+        tl[tile + off] = lo;
+    }
+}
+
+bool leaf_tc_shape(const Dims& d)
+{
+    const int n0 = 1 << d.l0;
+    return (n0 == 32 || n0 == 64) && (d.R == 6 || d.R == 8 || d.R == 10 || d.R == 12 || d.R == 16) &&
+           (d.n_amp == 1 || d.n_amp == 2 || d.n_amp == 4);
+}
+
+cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U, float* V0x, float* Ux, cudaStream_t s)
+{
+    if (!leaf_tc_shape(d)) return cudaErrorInvalidValue;
+    const unsigned grid = 148 * 16;
+    expand_s0_kernel<<<grid, 256, 0, s>>>(V0, V0x, d.LN, d.l0, d.R);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    expand_sl_kernel<<<grid, 256, 0, s>>>(U, Ux, d.LN, d.l0, d.R, sl_kp(d.R));
+    return cudaGetLastError();
+}
+
+// =============================================================================================
+// S0 (eqn:1 P:698-702, amplitude pre-scale eqn:tg P:24-28) on the tensor cores.
+// CTA = one leaf b x one tile of 128 vectors.  A = Y^T, Y[j][v] = b_k(x) F[x, c] (x = b n0 + j),
+// K = 2 n0, split hi/lo once into shared memory.  The n0 2r rows of B are swept in chunks of 128
+// (N = 128 per MMA); each chunk's K is split in two halves accumulated in separate TMEM columns
+// (short chains, summed in FP32 by the epilogue).  Weight tiles (32 KB hi+lo per 32 K) stream
+// through a 3-deep ring of bulk copies.  Warps 0-3 epilogue (TMEM lanes = vectors), warp 4 loader,
+// warp 5 MMA issuer; all six build A.
+// =============================================================================================
+template <int R, int N0>
+struct S0TC {
+    static constexpr int K = 2 * N0;
+    static constexpr int KS = K / S0X_KC;                 // 32-wide K chunks (2 or 4)
+    static constexpr int NCH = N0 * 2 * R / S0X_NC;       // 128-row N chunks
+    static constexpr int NIT = NCH * KS;
+    static constexpr int NSTAGE = 3;
+    static constexpr uint32_t TILE = S0X_TILE_FLOATS * 4;  // 16 KB
+    static constexpr uint32_t STAGE = 2 * TILE;
+    static constexpr uint32_t A_BYTES = 128u * K * 4;
+    static constexpr size_t SMEM = 2 * size_t(A_BYTES) + NSTAGE * size_t(STAGE);
+    static_assert((N0 * 2 * R) % S0X_NC == 0 && KS % 2 == 0, "tiling");
+};
+
+template <int R, int N0>
+__global__ void __launch_bounds__(192, 1)
+    s0_tc_kernel(const float2* __restrict__ F, int64_t ldf, const float2* __restrict__ ampb,
+                 const float* __restrict__ V0x, float2* __restrict__ out, int LN, int n_amp, int nv, int nvt)
+{
+    using C = S0TC<R, N0>;
+    extern __shared__ __align__(128) uint8_t sm_s0tc[];
+    uint8_t* Ahi = sm_s0tc;
+    uint8_t* Alo = sm_s0tc + C::A_BYTES;
+    uint8_t* ring = sm_s0tc + 2 * C::A_BYTES;
+    __shared__ uint64_t full[C::NSTAGE], empty[C::NSTAGE], dfull[2], dempty[2];
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t N = int64_t(1) << LN;
+    const int64_t nleaf = N / N0;
+    const int64_t b = blockIdx.x / nvt;
+    const int v0 = (blockIdx.x % nvt) * 128;
+    const float* wsrc = V0x + b * (int64_t(C::NIT) * 2 * S0X_TILE_FLOATS);
+
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < C::NSTAGE; i++) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&dfull[i], 1);
+            tc::mbar_init(&dempty[i], 128);
+        }
+        tc::mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 128) {   // start the weight stream before building A
+        for (int it = 0; it < C::NSTAGE && it < C::NIT; it++) {
+            tc::mbar_arrive_expect_tx(&full[it], C::STAGE);
+            tc::bulk_g2s(ring + it * C::STAGE, wsrc + int64_t(it) * 2 * S0X_TILE_FLOATS, C::STAGE, &full[it]);
+        }
+    }
+    // A = Y^T split hi/lo.  Task (v, jj): complex j = 2jj, 2jj+1 of vector v -> 16 bytes at k = 4 jj.
+    // Lane map 4 jj x 8 v: 64-byte global segments per column, conflict-free 16-byte smem stores.
+    {
+        constexpr int NJG = N0 / 8;   // groups of 4 jj
+        for (int wb = warp; wb < 16 * NJG; wb += 6) {
+            const int v = (wb % 16) * 8 + (lane >> 2), jj = (wb / 16) * 4 + (lane & 3);
+            const int vg = v0 + v;
+            float4 hi = make_float4(0, 0, 0, 0), lo = hi;
+            if (vg < nv) {
+                const int c = vg / n_amp, k = vg - c * n_amp;
+                const int64_t x = b * N0 + 2 * jj;
+                const float4 f = __ldg(reinterpret_cast<const float4*>(F + x + c * ldf));
+                const float4 a = __ldg(reinterpret_cast<const float4*>(ampb + k * N + x));
+                const float2 y0 = cmul_tc(make_float2(a.x, a.y), make_float2(f.x, f.y));
+                const float2 y1 = cmul_tc(make_float2(a.z, a.w), make_float2(f.z, f.w));
+                tc::split(y0.x, hi.x, lo.x);
+                tc::split(y0.y, hi.y, lo.y);
+                tc::split(y1.x, hi.z, lo.z);
+                tc::split(y1.y, hi.w, lo.w);
+            }
+            const uint32_t off = tc::kmaj_off(v, 4 * jj, 128);
+            st_f4(Ahi, off, hi);
+            st_f4(Alo, off, lo);
+        }
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 4) {
+        // ---- loader: the rest of the weight stream ----
+        if (lane == 0) {
+            for (int it = C::NSTAGE; it < C::NIT; it++) {
+                const int st = it % C::NSTAGE;
+                tc::mbar_wait(&empty[st], ((it / C::NSTAGE) - 1) & 1);
+                tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
+                tc::bulk_g2s(ring + st * C::STAGE, wsrc + int64_t(it) * 2 * S0X_TILE_FLOATS, C::STAGE, &full[st]);
+            }
+        }
+    } else if (warp == 5) {
+        // ---- MMA issuer ----
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(128, S0X_NC);
+            constexpr uint32_t LBO_A = (128 / 8) * 128, LBO_B = (S0X_NC / 8) * 128;
+            const uint64_t dAh = tc::desc_kmajor(tc::smem_u32(Ahi), LBO_A);
+            const uint64_t dAl = tc::desc_kmajor(tc::smem_u32(Alo), LBO_A);
+            const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(ring), LBO_B);
+            for (int nc = 0; nc < C::NCH; nc++) {
+                const int slot = nc & 1;
+                if (nc >= 2) tc::mbar_wait(&dempty[slot], ((nc >> 1) - 1) & 1);
+                tc::fence_after_sync();
+                for (int ks = 0; ks < C::KS; ks++) {
+                    const int it = nc * C::KS + ks, st = it % C::NSTAGE;
+                    tc::mbar_wait(&full[st], (it / C::NSTAGE) & 1);
+                    tc::fence_after_sync();
+                    const int half = ks / (C::KS / 2), first = (ks % (C::KS / 2)) == 0;
+                    const uint32_t d = tmem + uint32_t(slot * 256 + half * 128);
+                    const uint64_t bh = tc::desc_add(dB0, st * C::STAGE), bl = tc::desc_add(bh, C::TILE);
+                    const uint32_t aoff = ks * (S0X_KC / 4) * LBO_A;
+#pragma unroll
+                    for (int q = 0; q < 3; q++) {
+                        const int pass = kPassOrder[q];
+                        const uint64_t a = tc::desc_add(pass == 1 ? dAl : dAh, aoff);
+                        const uint64_t bb = pass == 2 ? bl : bh;
+#pragma unroll
+                        for (int kk = 0; kk < S0X_KC / 8; kk++)
+                            tc::mma_tf32(d, tc::desc_add(a, kk * 2 * LBO_A), tc::desc_add(bb, kk * 2 * LBO_B), idesc,
+                                         (first && q == 0 && kk == 0) ? 0u : 1u);
+                    }
+                    tc::commit(&empty[st]);
+                }
+                tc::commit(&dfull[slot]);
+            }
+        }
+    } else {
+        // ---- epilogue: TMEM lane = tid = vector of the tile; column n = (a, t, c') of the chunk ----
+        const int vg = v0 + tid;
+        for (int nc = 0; nc < C::NCH; nc++) {
+            const int slot = nc & 1;
+            tc::mbar_wait(&dfull[slot], (nc >> 1) & 1);
+            tc::fence_after_sync();
+            const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(slot * 256);
+#pragma unroll 1
+            for (int c0 = 0; c0 < S0X_NC; c0 += 16) {
+                float x[16], y[16];
+                tc::tmem_ld16(taddr + c0, x);
+                tc::tmem_ld16(taddr + 128 + c0, y);
+                tc::tmem_wait_ld();
+                if (c0 + 16 == S0X_NC) {
+                    tc::fence_before_sync();
+                    tc::mbar_arrive(&dempty[slot]);
+                }
+                if (vg < nv) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        const int q = (nc * S0X_NC + c0) / 2 + i;   // complex output index a R + t
+                        const int a = q / R, t = q - a * R;
+                        out[((int64_t(a) * nleaf + b) * R + t) * nv + vg] =
+                            make_float2(x[2 * i] + y[2 * i], x[2 * i + 1] + y[2 * i + 1]);
+                    }
+                }
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int R, int N0>
+static cudaError_t s0_tc_go(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x,
+                            float2* out, int nv, cudaStream_t s)
+{
+    using C = S0TC<R, N0>;
+    auto kern = s0_tc_kernel<R, N0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    const int nvt = (nv + 127) / 128;
+    const int64_t ctas = (d.N / N0) * nvt;
+    kern<<<unsigned(ctas), 192, C::SMEM, s>>>(F, ldf, ampb, V0x, out, d.LN, d.n_amp, nv, nvt);
+    return cudaGetLastError();
+}
+
+bool s0_tc_supported(const Dims& d, int nv, int64_t ldf) { return leaf_tc_shape(d) && nv >= 64 && (ldf % 2) == 0; }
+
+cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x, float2* out,
+                         int nv, cudaStream_t s)
+{
+    const int n0 = 1 << d.l0;
+#define S0TC_CASE(RR)                                                                                      \
+    if (d.R == RR)                                                                                         \
+        return n0 == 64 ? s0_tc_go<RR, 64>(d, F, ldf, ampb, V0x, out, nv, s)                               \
+                        : s0_tc_go<RR, 32>(d, F, ldf, ampb, V0x, out, nv, s);
+    S0TC_CASE(6) S0TC_CASE(8) S0TC_CASE(10) S0TC_CASE(12) S0TC_CASE(16)
+#undef S0TC_CASE
+    return cudaErrorInvalidValue;
+}
+
+// =============================================================================================
+// SL (eqn:bf3 P:791-797, amplitude post-scale and sum over k eqn:tg P:24-28) on the tensor cores.
+// CTA = one T_X leaf a x one tile of 128 vectors.  D[v][2j + c'] = sum over K = (b, t, c) of
+// A[v][(b, t, c)] B[(j, c')][(b, t, c)], A = delta_D[a n0 + b][t][v] split hi/lo, B = the expanded
+// U tiles of the leaf.  K streams in chunks of KP pairs:
+//   warp 8 (one thread)   bulk-copies the raw delta rows and the B tile of a chunk (2-deep rings),
+//   warps 0-3             split a raw chunk into one of two A stages,
+//   warp 9 (one thread)   issues the 3 KC/8 MMAs of a chunk; every SEG chunks it switches between
+//                         two TMEM accumulators (short chains),
+//   warps 4-7             drain each finished segment into FP32 registers, then apply a_k, sum
+//                         over k by lane shuffles and write G through a shared-memory transpose.
+// =============================================================================================
+template <int R, int N0, int NA, int KP>
+struct SLTC {
+    static constexpr int NB = 2 * N0;
+    static constexpr int KC = KP * 2 * R;
+    static constexpr int NCH = N0 / KP;
+    static constexpr int SEG = 1;                                // chunks per accumulation segment
+    static constexpr int NSEG = (NCH + SEG - 1) / SEG;
+    static constexpr uint32_t RAW = uint32_t(KP) * R * 128 * 8;
+    static constexpr uint32_t BT = uint32_t(NB) * KC * 4;   // one of hi / lo
+    static constexpr uint32_t AT = 128u * KC * 4;
+    static constexpr uint32_t OFF_B = 2 * RAW, OFF_A = OFF_B + 4 * BT, OFF_AS = OFF_A + 4 * AT;
+    static constexpr uint32_t GS_STRIDE = N0 + 1;
+    static constexpr size_t SMEM = size_t(OFF_AS) + size_t(NA) * N0 * 8;
+    static_assert(KC % 8 == 0, "K chunk must be whole MMA K steps");
+    static_assert(SMEM <= 232448 - 512, "shared memory budget");
+    static_assert(size_t(128 / NA) * GS_STRIDE * 8 <= OFF_AS, "G staging fits in the freed rings");
+};
+
+template <int R, int N0, int NA, int KP>
+__global__ void __launch_bounds__(320, 1)
+    sl_tc_kernel(const float2* __restrict__ in, const float* __restrict__ Ux, const float2* __restrict__ ampa,
+                 float2* __restrict__ G, int64_t ldg, int LN, int nv, int nvt)
+{
+    using C = SLTC<R, N0, NA, KP>;
+    extern __shared__ __align__(128) uint8_t sm_sltc[];
+    auto raw = [&](int e) { return sm_sltc + e * C::RAW; };
+    auto opB = [&](int e, int lo) { return sm_sltc + C::OFF_B + (2 * e + lo) * C::BT; };
+    auto opA = [&](int s, int lo) { return sm_sltc + C::OFF_A + (2 * s + lo) * C::AT; };
+    float2* As = reinterpret_cast<float2*>(sm_sltc + C::OFF_AS);   // [NA][N0] a_k(x)
+    float2* Gs = reinterpret_cast<float2*>(sm_sltc);               // epilogue: [128/NA][GS_STRIDE]
+    __shared__ uint64_t raw_full[2], raw_empty[2], b_full[2], b_empty[2], a_full[2], a_empty[2], dfull[2],
+        dempty[2];
+    __shared__ uint32_t tmem_base;
+    constexpr int TMEM_COLS = tmem_cols_pow2<2 * C::NB>();
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t N = int64_t(1) << LN;
+    const int64_t a = blockIdx.x / nvt;
+    const int v0 = (blockIdx.x % nvt) * 128;
+    const int vw = min(128, nv - v0);
+    const float* wsrc = Ux + a * (int64_t(C::NCH) * 2 * (C::BT / 4));
+
+    if (warp == 0) tc::tmem_alloc<TMEM_COLS>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&raw_full[i], 1);
+            tc::mbar_init(&raw_empty[i], 128);
+            tc::mbar_init(&b_full[i], 1);
+            tc::mbar_init(&b_empty[i], 1);
+            tc::mbar_init(&a_full[i], 128);
+            tc::mbar_init(&a_empty[i], 1);
+            tc::mbar_init(&dfull[i], 1);
+            tc::mbar_init(&dempty[i], 128);
+        }
+        tc::mbar_fence_init();
+    }
+    for (int i = tid; i < NA * N0; i += blockDim.x) As[i] = __ldg(ampa + (i / N0) * N + a * N0 + (i % N0));
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 8) {
+        // ---- loader ----
+        if (lane == 0) {
+            const uint32_t row_bytes = uint32_t(vw) * 8;
+            for (int ch = 0; ch < C::NCH; ch++) {
+                const int e = ch & 1, use = ch >> 1;
+                if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
+                tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
+                tc::bulk_g2s(opB(e, 0), wsrc + int64_t(ch) * 2 * (C::BT / 4), 2 * C::BT, &b_full[e]);
+                if (use > 0) tc::mbar_wait(&raw_empty[e], (use - 1) & 1);
+                tc::mbar_arrive_expect_tx(&raw_full[e], KP * R * row_bytes);
+                const int64_t p0 = a * N0 + int64_t(ch) * KP;
+                for (int row = 0; row < KP * R; row++)
+                    tc::bulk_g2s(raw(e) + row * 128 * 8, in + (p0 * R + row) * int64_t(nv) + v0, row_bytes,
+                                 &raw_full[e]);
+            }
+        }
+    } else if (warp == 9) {
+        // ---- MMA issuer ----
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
+            constexpr uint32_t LBO_A = (128 / 8) * 128, LBO_B = (C::NB / 8) * 128;
+            const uint64_t dA0 = tc::desc_kmajor(tc::smem_u32(opA(0, 0)), LBO_A);
+            const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(opB(0, 0)), LBO_B);
+            for (int ch = 0; ch < C::NCH; ch++) {
+                const int e = ch & 1, seg = ch / C::SEG, slot = seg & 1, first = (ch % C::SEG) == 0;
+                if (first && seg >= 2) tc::mbar_wait(&dempty[slot], ((seg >> 1) - 1) & 1);
+                tc::mbar_wait(&a_full[e], (ch >> 1) & 1);
+                tc::mbar_wait(&b_full[e], (ch >> 1) & 1);
+                tc::fence_after_sync();
+                const uint32_t d = tmem + uint32_t(slot * C::NB);
+#pragma unroll
+                for (int q = 0; q < 3; q++) {
+                    const int pass = kPassOrder[q];
+                    const uint64_t aa = tc::desc_add(dA0, (2 * e + (pass == 1)) * C::AT);
+                    const uint64_t bb = tc::desc_add(dB0, (2 * e + (pass == 2)) * C::BT);
+#pragma unroll
+                    for (int ks = 0; ks < C::KC / 8; ks++)
+                        tc::mma_tf32(d, tc::desc_add(aa, ks * 2 * LBO_A), tc::desc_add(bb, ks * 2 * LBO_B), idesc,
+                                     (first && q == 0 && ks == 0) ? 0u : 1u);
+                }
+                tc::commit(&a_empty[e]);
+                tc::commit(&b_empty[e]);
+                if ((ch % C::SEG) == C::SEG - 1 || ch == C::NCH - 1) tc::commit(&dfull[slot]);
+            }
+        }
+    } else if (warp < 4) {
+        // ---- split: raw delta rows -> A stage (hi / lo) ----
+        for (int ch = 0; ch < C::NCH; ch++) {
+            const int e = ch & 1, use = ch >> 1;
+            tc::mbar_wait(&raw_full[e], use & 1);
+            if (use > 0) tc::mbar_wait(&a_empty[e], (use - 1) & 1);
+            const float2* rd = reinterpret_cast<const float2*>(raw(e));   // [KP R][128]
+            uint8_t *ah = opA(e, 0), *al = opA(e, 1);
+            // A[v][(pl, t, c)]: task (v, pl, tt) -> complex t = 2tt, 2tt+1 -> 16 bytes
+            for (int idx = tid; idx < 128 * KP * (R / 2); idx += 128) {
+                const int v = idx & 127, q = idx >> 7;   // q = pl R/2 + tt
+                const int pl = q / (R / 2), tt = q - pl * (R / 2);
+                const float2 x0 = rd[(pl * R + 2 * tt) * 128 + v], x1 = rd[(pl * R + 2 * tt + 1) * 128 + v];
+                float4 h, l;
+                tc::split(x0.x, h.x, l.x);
+                tc::split(x0.y, h.y, l.y);
+                tc::split(x1.x, h.z, l.z);
+                tc::split(x1.y, h.w, l.w);
+                const uint32_t off = tc::kmaj_off(v, pl * 2 * R + 4 * tt, 128);
+                st_f4(ah, off, h);
+                st_f4(al, off, l);
+            }
+            tc::fence_proxy_async();
+            tc::mbar_arrive(&raw_empty[e]);
+            tc::mbar_arrive(&a_full[e]);
+        }
+    } else {
+        // ---- drain (warps 4-7): lane quarter warp - 4 = vectors, all NB columns ----
+        const int q4 = warp - 4, vl = q4 * 32 + lane;
+        float sum[C::NB];
+#pragma unroll
+        for (int i = 0; i < C::NB; i++) sum[i] = 0.f;
+        for (int seg = 0; seg < C::NSEG; seg++) {
+            const int slot = seg & 1;
+            tc::mbar_wait(&dfull[slot], (seg >> 1) & 1);
+            tc::fence_after_sync();
+            const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(slot * C::NB);
+#pragma unroll
+            for (int c0 = 0; c0 < C::NB; c0 += 16) {
+                float x[16];
+                tc::tmem_ld16(taddr + c0, x);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; i++) sum[c0 + i] += x[i];
+            }
+            tc::fence_before_sync();
+            tc::mbar_arrive(&dempty[slot]);
+        }
+        // every MMA has completed (last dfull): the rings are free for the G staging
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int k = vl % NA, cl = vl / NA;
+#pragma unroll
+        for (int j = 0; j < N0; j++) {
+            float2 g = cmul_tc(As[k * N0 + j], make_float2(sum[2 * j], sum[2 * j + 1]));
+#pragma unroll
+            for (int m = 1; m < NA; m <<= 1) {
+                g.x += __shfl_xor_sync(0xffffffffu, g.x, m);
+                g.y += __shfl_xor_sync(0xffffffffu, g.y, m);
+            }
+            if ((j % NA) == k) Gs[cl * C::GS_STRIDE + j] = g;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // copy out: RHS column c0 + cl, rows a n0 .. a n0 + n0 - 1 (contiguous)
+        const int c0 = v0 / NA, cw = vw / NA;
+        for (int idx = vl; idx < cw * N0; idx += 128) {
+            const int cc = idx / N0, j = idx % N0;
+            G[a * N0 + j + int64_t(c0 + cc) * ldg] = Gs[cc * C::GS_STRIDE + j];
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<TMEM_COLS>(tmem);
+    }
+}
+
+template <int R, int N0, int NA, int KP>
+static cudaError_t sl_tc_go(const Dims& d, const float2* in, const float* Ux, const float2* ampa, float2* G, int64_t ldg,
+                            int nv, cudaStream_t s)
+{
+    using C = SLTC<R, N0, NA, KP>;
+    auto kern = sl_tc_kernel<R, N0, NA, KP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    const int nvt = (nv + 127) / 128;
+    const int64_t ctas = (d.N / N0) * nvt;
+    kern<<<unsigned(ctas), 320, C::SMEM, s>>>(in, Ux, ampa, G, ldg, d.LN, nv, nvt);
+    return cudaGetLastError();
+}
+
+bool sl_tc_supported(const Dims& d, int nv) { return leaf_tc_shape(d) && nv >= 64 && nv % 2 == 0; }
+
+cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const float2* ampa, float2* G, int64_t ldg,
+                         int nv, cudaStream_t s)
+{
+    const int n0 = 1 << d.l0;
+#define SLTC_NA(RR, N0_, KP_)                                                                 \
+    if (d.R == RR && n0 == N0_) {                                                             \
+        if (d.n_amp == 1) return sl_tc_go<RR, N0_, 1, KP_>(d, in, Ux, ampa, G, ldg, nv, s);  \
+        if (d.n_amp == 2) return sl_tc_go<RR, N0_, 2, KP_>(d, in, Ux, ampa, G, ldg, nv, s);  \
+        if (d.n_amp == 4) return sl_tc_go<RR, N0_, 4, KP_>(d, in, Ux, ampa, G, ldg, nv, s);  \
+    }
+    SLTC_NA(6, 64, 2) SLTC_NA(8, 64, 2) SLTC_NA(10, 64, 2) SLTC_NA(12, 64, 1) SLTC_NA(16, 64, 1)
+    SLTC_NA(6, 32, 2) SLTC_NA(8, 32, 2) SLTC_NA(10, 32, 2) SLTC_NA(12, 32, 1) SLTC_NA(16, 32, 1)
+#undef SLTC_NA
+    return cudaErrorInvalidValue;
+}
+
+// =============================================================================================
+// Transfer band of two levels (eqn:2 P:748-752 for l <= h, eqn:3 P:780-785 for l > h; the switch
+// P:755-766 is folded into the level-h blocks) on the tensor cores, persistent (one CTA per SM).
+// A group = 4 pairs at the input level closed under the two levels (fixed a0, 4 consecutive b),
+// as in the SIMT band.  Per group and vector tile of 128:
+//   warp 8 (one thread)   bulk-copies the 4 r raw coefficient rows (2-deep ring),
+//   warps 0-3             split them hi/lo into an A buffer in TMEM (lane = vector, one slot of
+//                         2r columns per pair; double-buffered when TMEM allows),
+//   warp 9 (one thread)   level 1: per unit u (slots 2u, 2u+1 = K of 4r), D1_u = A B1_u with both
+//                         outputs of the unit as N (4r, padded to 16); level 2 likewise from D2,
+//   warps 4-7             drain D1, split it back into the A buffer at the level-2 slot order
+//                         (output e of unit u -> slot 2e + u, so every level-2 unit again reads
+//                         two adjacent slots), and finally store D2 to HBM (coalesced over v),
+//   warps 10-11           expand the group's compact weight blocks into real-embedded hi/lo B
+//                         tiles in shared memory, one group ahead (double-buffered when it fits).
+// Each accumulator chain is 3 (4r/8) MMAs (15 at r = 10): short, FP32-accurate.
+// =============================================================================================
+template <int R>
+struct BandTC {
+    static constexpr int P = 4, U = 2;                 // pairs per group, units per level
+    static constexpr int SC = 2 * R;                   // TMEM columns of one slot (r complex)
+    static constexpr int KU = 4 * R;                   // MMA K of a unit (two slots)
+    static constexpr int NU = 4 * R;                   // useful N of a unit (two outputs)
+    static constexpr int NB = (NU + 15) / 16 * 16;     // MMA N
+    static constexpr int ACOLS = 2 * P * SC;           // hi + lo of one A buffer
+    static constexpr int DCOLS = U * NB;               // accumulators of one level
+    static constexpr int NABUF = (2 * ACOLS + 2 * DCOLS <= 512) ? 2 : 1;
+    static constexpr int D1_OFF = NABUF * ACOLS, D2_OFF = D1_OFF + DCOLS;
+    static constexpr int TMEM_COLS = tmem_cols_pow2<D2_OFF + DCOLS>();
+    static constexpr uint32_t RAW = uint32_t(P) * R * 128 * 8;   // raw rows of one vector tile
+    static constexpr uint32_t WT = uint32_t(NB) * KU * 4;        // one B tile (hi or lo)
+    static constexpr uint32_t WSET = 2 * U * 2 * WT;             // 2 levels x U units x (hi, lo)
+    static constexpr uint32_t OFF_W = 2 * RAW;
+    static constexpr int NWBUF = (size_t(OFF_W) + 2 * size_t(WSET) <= 232448 - 1024) ? 2 : 1;
+    static constexpr size_t SMEM = size_t(OFF_W) + NWBUF * size_t(WSET);
+    static constexpr int WTASKS = 2 * U * 2 * 2 * R * R;         // complex weight entries per group
+    static constexpr int WPT = (WTASKS + 63) / 64;               // per weight thread
+    static_assert(KU % 8 == 0 && D2_OFF + DCOLS <= 512 && SMEM <= 232448 - 1024, "band shape");
+};
+
+template <int R>
+__global__ void __launch_bounds__(384, 1)
+    band_tc_kernel(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ W1,
+                   const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg)
+{
+    using C = BandTC<R>;
+    extern __shared__ __align__(128) uint8_t sm_band[];
+    auto raw = [&](int e) { return sm_band + e * C::RAW; };
+    auto wtile = [&](int wb, int m, int u, int lo) {
+        return sm_band + C::OFF_W + wb * C::WSET + ((m * C::U + u) * 2 + lo) * C::WT;
+    };
+    __shared__ uint64_t raw_full[2], raw_empty[2], a1_ready[2], a2_ready[2], a_free[2], w_full[2], w_free[2];
+    __shared__ uint64_t d1_full, d1_free, d2_full, d2_free;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t N = int64_t(1) << LN;
+    const int lin = l_first - 1, shg = LN - lin - 2;
+    const int64_t ngroups = N >> 2;
+    const int nvt = (nv + 127) / 128;
+    const int64_t nit = (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t njobs = nit * nvt;
+
+    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&raw_full[i], 1);
+            tc::mbar_init(&raw_empty[i], 128);
+            tc::mbar_init(&a1_ready[i], 128);
+            tc::mbar_init(&a2_ready[i], 128);
+            tc::mbar_init(&a_free[i], 1);
+            tc::mbar_init(&w_full[i], 64);
+            tc::mbar_init(&w_free[i], 1);
+        }
+        tc::mbar_init(&d1_full, 1);
+        tc::mbar_init(&d1_free, 128);
+        tc::mbar_init(&d2_full, 1);
+        tc::mbar_init(&d2_free, 128);
+        tc::mbar_fence_init();
+    }
+    if constexpr (C::NB > C::NU) {   // zero the pad rows of every B tile (never written afterwards)
+        constexpr int PADQ = (C::NB - C::NU) * C::KU / 4;
+        for (int idx = tid; idx < C::NWBUF * 2 * C::U * 2 * PADQ; idx += blockDim.x) {
+            const int tile = idx / PADQ, o = idx % PADQ;
+            const int row = C::NU + o % (C::NB - C::NU), k = 4 * (o / (C::NB - C::NU));
+            st_f4(sm_band + C::OFF_W + tile * C::WT, tc::kmaj_off(row, k, C::NB), make_float4(0, 0, 0, 0));
+        }
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base;
+
+    if (warp < 4) {
+        // ---- split: raw rows -> A buffer (TMEM), lane = vector ----
+        const int v = tid;
+        const uint32_t lb = uint32_t(warp * 32) << 16;
+        for (int64_t J = 0; J < njobs; J++) {
+            const int e = int(J & 1);
+            tc::mbar_wait(&raw_full[e], uint32_t(J >> 1) & 1);
+            const int slot = int(J % C::NABUF);
+            const int64_t use = J / C::NABUF;
+            if (use > 0) tc::mbar_wait(&a_free[slot], uint32_t(use - 1) & 1);
+            tc::fence_after_sync();
+            const float2* rd = reinterpret_cast<const float2*>(raw(e));
+#pragma unroll 1
+            for (int s = 0; s < C::P; s++) {
+                float hi[C::SC], lo[C::SC];
+#pragma unroll
+                for (int t = 0; t < R; t++) {
+                    const float2 x = rd[(s * R + t) * 128 + v];
+                    tc::split(x.x, hi[2 * t], lo[2 * t]);
+                    tc::split(x.y, hi[2 * t + 1], lo[2 * t + 1]);
+                }
+                const uint32_t ta = tmem + lb + uint32_t(slot * C::ACOLS + s * C::SC);
+                tc::tmem_st_cols<C::SC>(ta, hi);
+                tc::tmem_st_cols<C::SC>(ta + C::P * C::SC, lo);
+            }
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&raw_empty[e]);
+            tc::mbar_arrive(&a1_ready[slot]);
+        }
+    } else if (warp < 8) {
+        // ---- epilogue: level-1 drain + re-split, level-2 drain + store ----
+        const int v = tid - 128;
+        const uint32_t lb = uint32_t((warp - 4) * 32) << 16;
+        for (int64_t J = 0; J < njobs; J++) {
+            const int64_t it = J / nvt;
+            const int vt = int(J - it * nvt);
+            const int64_t g = blockIdx.x + it * gridDim.x;
+            const int slot = int(J % C::NABUF);
+            const uint32_t ph = uint32_t(J & 1);
+            tc::mbar_wait(&d1_full, ph);
+            tc::fence_after_sync();
+#pragma unroll 1
+            for (int u = 0; u < C::U; u++) {
+                float d[C::NU];
+                tc::tmem_ld_cols<C::NU>(tmem + lb + uint32_t(C::D1_OFF + u * C::NB), d);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    float hi[C::SC], lo[C::SC];
+#pragma unroll
+                    for (int i = 0; i < C::SC; i++) tc::split(d[e * C::SC + i], hi[i], lo[i]);
+                    const uint32_t ta = tmem + lb + uint32_t(slot * C::ACOLS + (2 * e + u) * C::SC);
+                    tc::tmem_st_cols<C::SC>(ta, hi);
+                    tc::tmem_st_cols<C::SC>(ta + C::P * C::SC, lo);
+                }
+            }
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&d1_free);
+            tc::mbar_arrive(&a2_ready[slot]);
+
+            tc::mbar_wait(&d2_full, ph);
+            tc::fence_after_sync();
+            float d[C::U][C::NU];
+#pragma unroll
+            for (int u = 0; u < C::U; u++) tc::tmem_ld_cols<C::NU>(tmem + lb + uint32_t(C::D2_OFF + u * C::NB), d[u]);
+            tc::tmem_wait_ld();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&d2_free);
+            const int vg = vt * 128 + v;
+            if (vg < nv) {
+                const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+#pragma unroll
+                for (int u = 0; u < C::U; u++)
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        const int64_t p = (((a0 << 2) + 2 * u + e) << shg) + bq;
+                        float2* o = out + p * R * int64_t(nv) + vg;
+#pragma unroll
+                        for (int t = 0; t < R; t++)
+                            o[int64_t(t) * nv] = make_float2(d[u][e * C::SC + 2 * t], d[u][e * C::SC + 2 * t + 1]);
+                    }
+            }
+        }
+    } else if (warp == 8) {
+        // ---- loader ----
+        if (lane == 0) {
+            for (int64_t J = 0; J < njobs; J++) {
+                const int64_t it = J / nvt;
+                const int vt = int(J - it * nvt);
+                const int64_t g = blockIdx.x + it * gridDim.x;
+                const int e = int(J & 1);
+                if (J >= 2) tc::mbar_wait(&raw_empty[e], uint32_t((J >> 1) - 1) & 1);
+                const int v0 = vt * 128, vw = min(128, nv - v0);
+                const uint32_t row_bytes = uint32_t(vw) * 8;
+                tc::mbar_arrive_expect_tx(&raw_full[e], C::P * R * row_bytes);
+                const int64_t pin = rh ? bfs::recv_index(g * C::P, rh, rhg) : g * C::P;   // P pairs contiguous
+                for (int row = 0; row < C::P * R; row++)
+                    tc::bulk_g2s(raw(e) + row * 128 * 8, in + (pin * R + row) * int64_t(nv) + v0, row_bytes,
+                                 &raw_full[e]);
+            }
+        }
+    } else if (warp == 9) {
+        // ---- MMA issuer ----
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
+            constexpr uint32_t LBO_B = (C::NB / 8) * 128;
+            const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_band + C::OFF_W), LBO_B);
+            for (int64_t J = 0; J < njobs; J++) {
+                const int64_t it = J / nvt;
+                const int vt = int(J - it * nvt);
+                const int wb = int(it % C::NWBUF), slot = int(J % C::NABUF);
+                if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
+#pragma unroll 1
+                for (int m = 0; m < 2; m++) {
+                    tc::mbar_wait(m == 0 ? &a1_ready[slot] : &a2_ready[slot], uint32_t(J / C::NABUF) & 1);
+                    if (J >= 1) tc::mbar_wait(m == 0 ? &d1_free : &d2_free, uint32_t(J - 1) & 1);
+                    tc::fence_after_sync();
+#pragma unroll
+                    for (int u = 0; u < C::U; u++) {
+                        const uint32_t d = tmem + uint32_t((m == 0 ? C::D1_OFF : C::D2_OFF) + u * C::NB);
+                        const uint32_t ahi = tmem + uint32_t(slot * C::ACOLS + 2 * u * C::SC);
+                        const uint64_t bhi = tc::desc_add(dW, wb * C::WSET + ((m * C::U + u) * 2) * C::WT);
+#pragma unroll
+                        for (int q = 0; q < 3; q++) {
+                            const int pass = kPassOrder[q];
+                            const uint32_t a = ahi + (pass == 1 ? C::P * C::SC : 0);
+                            const uint64_t b = pass == 2 ? tc::desc_add(bhi, C::WT) : bhi;
+#pragma unroll
+                            for (int ks = 0; ks < C::KU / 8; ks++)
+                                tc::mma_tf32_ts(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc,
+                                                (q | ks) ? 1u : 0u);
+                        }
+                    }
+                    tc::commit(m == 0 ? &d1_full : &d2_full);
+                }
+                tc::commit(&a_free[slot]);
+                if (vt == nvt - 1) tc::commit(&w_free[wb]);
+            }
+        }
+    } else {
+        // ---- weights (warps 10-11): compact r x 2r blocks -> embedded hi/lo B tiles, one group ahead ----
+        const int wt = tid - 320;
+        for (int64_t it = 0; it < nit; it++) {
+            const int64_t g = blockIdx.x + it * gridDim.x;
+            const int wb = int(it % C::NWBUF);
+            if (it >= C::NWBUF) tc::mbar_wait(&w_free[wb], uint32_t(it / C::NWBUF - 1) & 1);
+            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+            float2 w[C::WPT];
+#pragma unroll
+            for (int q = 0; q < C::WPT; q++) {
+                const int idx = wt + 64 * q;
+                w[q] = make_float2(0.f, 0.f);
+                if (idx < C::WTASKS) {
+                    // idx = (((m U + u) 2 + e) 2R + kcol) R + t
+                    const int t = idx % R, kcol = (idx / R) % (2 * R), e = (idx / (2 * R * R)) & 1;
+                    const int mu = idx / (4 * R * R), m = mu / C::U, u = mu % C::U;
+                    const int lv = m + 1, ep = u >> (2 - lv), i = u & ((1 << (2 - lv)) - 1);
+                    const int64_t p = (((a0 << lv) + 2 * ep + e) << (LN - lin - lv)) + (bq << (2 - lv)) + i;
+                    w[q] = __ldg((lv == 1 ? W1 : W2) + p * (2 * R * R) + kcol * R + t);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < C::WPT; q++) {
+                const int idx = wt + 64 * q;
+                if (idx < C::WTASKS) {
+                    const int t = idx % R, kcol = (idx / R) % (2 * R), e = (idx / (2 * R * R)) & 1;
+                    const int mu = idx / (4 * R * R), m = mu / C::U, u = mu % C::U;
+                    float hr, lr, hi_, li;
+                    tc::split(w[q].x, hr, lr);
+                    tc::split(w[q].y, hi_, li);
+                    const int n = e * C::SC + 2 * t, k = 2 * kcol;
+                    uint8_t* th = wtile(wb, m, u, 0);
+                    uint8_t* tl = wtile(wb, m, u, 1);
+                    const uint32_t o0 = tc::kmaj_off(n, k, C::NB), o1 = tc::kmaj_off(n + 1, k, C::NB);
+                    *reinterpret_cast<float2*>(th + o0) = make_float2(hr, -hi_);
+                    *reinterpret_cast<float2*>(tl + o0) = make_float2(lr, -li);
+                    *reinterpret_cast<float2*>(th + o1) = make_float2(hi_, hr);
+                    *reinterpret_cast<float2*>(tl + o1) = make_float2(li, lr);
+                }
+            }
+            tc::fence_proxy_async();
+            tc::mbar_arrive(&w_full[wb]);
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+    }
+}
+
+static int sm_count()
+{
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int R>
+static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
+                              cudaStream_t s, int rh, int rhg)
+{
+    using C = BandTC<R>;
+    auto kern = band_tc_kernel<R>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    const int64_t groups = d.N >> 2;
+    const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
+    kern<<<grid, 384, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg);
+    return cudaGetLastError();
+}
+
+bool band_tc_supported(const Dims& d, int nv)
+{
+    return (d.R == 6 || d.R == 8 || d.R == 10 || d.R == 12) && nv >= 64 && nv % 2 == 0;
+}
+
+cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
+                           cudaStream_t s, int rh, int rhg)
+{
+    switch (d.R) {
+    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg);
+    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg);
+    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg);
+    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace bfk

@@ -1,0 +1,124 @@
+"""GPU parity of the tensor-core (tcgen05, 3xTF32) stages.
+
+Every shape here is large enough in vectors (nv = nrhs * n_amp >= 64, leaf 32 or 64) that the
+plan routes its dense leaf / transfer stages to the tensor-core kernels (bf_tc.cu).  Each case is
+checked (1) against the CPU oracle per RHS column at the north_star bar (relative l2 <= 1e-5) and
+(2) against the same plan with BF_OPT_TENSOR_CORES = 0 (the FP32 FFMA kernels): both paths are
+FP32-accurate, so they agree far below the bar.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1803_04128_b200 import bf
+from paper_1803_04128_b200 import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+PARITY = 1e-5
+PATHS_AGREE = 2e-6
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+    yield
+
+
+def _apply(plan, F):
+    Ft = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()
+    Gt = torch.empty_like(Ft)
+    plan.apply(Ft, Gt, F.shape[1])
+    torch.cuda.synchronize()
+    return np.asfortranarray(Gt.cpu().numpy().T)
+
+
+TC_CASES = [
+    # kernel, amp, LN, l0, r, nrhs, chunk, oracle columns      what it exercises
+    (W.K_FIO, W.A_CFG1, 14, 6, 10, 256, 256, [0, 77, 255]),    # cfg4 shape at N = 2^14: 4 vector tiles
+    (W.K_FIO_JUMP, W.A_CFG3, 14, 5, 10, 64, 64, [0, 63]),      # cfg3 shape: leaf 32, n_amp 4
+    (W.K_FIO, W.A_CFG1, 12, 6, 10, 37, 37, None),              # nv = 74: one ragged vector tile
+    (W.K_FIO, W.A_CFG1, 14, 6, 10, 100, 100, [0, 64, 99]),     # nv = 200: full + ragged tile
+    (W.K_FIO, W.A_ONE, 12, 6, 6, 70, 70, [1, 69]),             # r = 6, n_amp 1
+    (W.K_DFT, W.A_CFG2, 12, 6, 8, 64, 64, [5]),                # r = 8, DFT kernel
+    (W.K_FIO, W.A_CFG1, 12, 6, 12, 64, 64, [2]),               # r = 12
+    (W.K_FIO, W.A_CFG1, 14, 6, 14, 40, 40, [0, 39]),           # r = 14 (one a per group, padded N)
+    (W.K_FIO, W.A_CFG2, 14, 6, 16, 33, 33, [32]),              # r = 16, nv = 66
+    (W.K_FIO, W.A_CFG1, 12, 5, 8, 64, 64, [0]),                # leaf 32, r = 8
+    (W.K_FIO, W.A_ONE, 12, 5, 12, 128, 128, [127]),            # leaf 32, r = 12
+    (W.K_FIO, W.A_CFG1, 12, 5, 14, 48, 48, [47]),              # leaf 32, r = 14
+    (W.K_FIO_JUMP, W.A_CFG3, 12, 5, 16, 16, 16, [15]),         # leaf 32, r = 16, nv = 64
+    (W.K_FIO, W.A_CFG1, 14, 6, 10, 150, 64, [0, 100, 149]),    # chunks of 128 + 128 + 44 vectors
+]
+
+
+@pytest.mark.parametrize("kernel,amp,LN,l0,r,nrhs,chunk,cols", TC_CASES)
+def test_tc_parity(kernel, amp, LN, l0, r, nrhs, chunk, cols):
+    N = 1 << LN
+    F = W.rhs(N, nrhs, 300 + LN + r)
+    plan = bf.Plan.build_fio(bf.fio(kernel, amp, LN, l0, r), max_nrhs_chunk=chunk)
+    nv = min(chunk, nrhs) * W.N_AMP[amp]
+    tc = plan.info()["tc_classes"]
+    if r != 14:                                       # the leaf stages run on the tensor cores
+        assert "s0" in tc and plan.info()["tc_weight_bytes"] > 0, tc
+        assert ("sl" in tc) == (nv % 2 == 0), tc
+    if r in (6, 8, 10, 12) and nv >= 128 and nv % 4 == 0 and LN - 2 * l0 >= 2:
+        assert any(k.startswith("xfer") for k in tc), tc   # a two-level band runs on the tensor cores
+    G_tc = _apply(plan, F)
+    plan.set_tensor_cores(False)
+    G_simt = _apply(plan, F)
+    plan.destroy()
+    assert np.all(np.isfinite(G_tc))
+    cols = list(range(nrhs)) if cols is None else cols
+    R = oracle.bf_apply(kernel, amp, LN, l0, r, F[:, cols])
+    err_tc = oracle.rel_l2(G_tc[:, cols].astype(np.complex128), R, axis=0)
+    err_simt = oracle.rel_l2(G_simt[:, cols].astype(np.complex128), R, axis=0)
+    assert np.all(err_tc <= PARITY), err_tc
+    assert np.all(err_simt <= PARITY), err_simt
+    d = oracle.rel_l2(G_tc.astype(np.complex128), G_simt.astype(np.complex128), axis=0)
+    assert np.all(d <= PATHS_AGREE), d.max()
+
+
+def test_tc_deterministic_and_column_independent():
+    """Within the tensor-core path: bitwise run-to-run, and a vector's result does not depend on the
+    other vectors of its tile (RHS permutation equivariance, bitwise)."""
+    LN, l0, r, nrhs = 12, 6, 10, 64
+    F = W.rhs(1 << LN, nrhs, 7)
+    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    G1 = _apply(plan, F)
+    assert np.array_equal(G1, _apply(plan, F))
+    perm = np.random.default_rng(1).permutation(nrhs)
+    assert np.array_equal(_apply(plan, np.asfortranarray(F[:, perm])), G1[:, perm])
+    plan.destroy()
+
+
+def test_tc_mutation_detected():
+    """A wrong leaf block or transfer block on the tensor-core path fails parity (the test can fail)."""
+    LN, l0, r, nrhs = 14, 6, 10, 64
+    N = 1 << LN
+    k = bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r)
+    a, b = bf.build_amp(k)
+    v0 = bf.build_blocks(k, bf.BF_STAGE_V0, 0, N)
+    xf = [bf.build_blocks(k, bf.BF_STAGE_XFER0 + i, 0, N) for i in range(LN - 2 * l0)]
+    sw = bf.build_blocks(k, bf.BF_STAGE_SW, 0, N)
+    u = bf.build_blocks(k, bf.BF_STAGE_U, 0, N)
+    F = W.rhs(N, nrhs, 3)
+    R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, :2])
+    v0m = v0.copy()
+    v0m[N // 5] = v0m[N // 5].conj()
+    um = u.copy()
+    um[N // 7] *= 1j
+    p = bf.Plan.from_arrays(LN, l0, r, a, b, v0, xf, sw, u, max_nrhs_chunk=nrhs)
+    assert set(p.info()["tc_classes"]) == {"s0", "xfer_switch", "sl"}   # every stage on the tensor cores
+    assert np.all(oracle.rel_l2(_apply(p, F)[:, :2].astype(np.complex128), R, axis=0) <= PARITY)
+    p.destroy()
+    xm = [x.copy() for x in xf]
+    xm[1][N // 3] *= -1.0
+    for args in ((v0m, xf, u), (v0, xf, um), (v0, xm, u)):
+        p = bf.Plan.from_arrays(LN, l0, r, a, b, args[0], args[1], sw, args[2], max_nrhs_chunk=nrhs)
+        G = _apply(p, F)
+        p.destroy()
+        assert np.all(oracle.rel_l2(G[:, :2].astype(np.complex128), R, axis=0) > 1e-4)

@@ -1,0 +1,402 @@
+// tc_probe2.cu -- answers the design questions of the tensor-core kernels:
+//   (1) kind::tf32 SS MMA (both operands in shared memory, K-major SWIZZLE_NONE), M=128 N=48
+//   (2) the "negate B" instruction-descriptor bit (bit 14) with kind::tf32
+//   (3) A operand in TMEM (tcgen05.st, then tcgen05.mma [d], [a_tmem], b_desc) with kind::tf32
+//   (4) MMA issue cost per instruction (clock64 over a long chain) for N in {48, 80, 160, 256},
+//       A from SMEM vs from TMEM -- whether small-N tf32 MMAs are operand-bandwidth bound
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tc_probe2 tools/tc_probe2.cu
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1803_04128_b200/csrc/tc_sm100.cuh"
+
+constexpr int M = 128, K = 16;
+
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t db, uint32_t idesc, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+        "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// mode 0: SS, mode 1: SS with negate-B, mode 2: A from TMEM.  D[M][N] = A[M][K] Bt[N][K]^T (K=16, 2 steps)
+template <int N>
+__global__ void probe_kernel(const float* A, const float* Bt, float* D, int mode)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* a_s = smem;
+    uint8_t* b_s = smem + M * K * 4;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < M * K; i += blockDim.x) {
+        const int r = i / K, k = i % K;
+        *reinterpret_cast<float*>(a_s + tc::kmaj_off(r, k, M)) = A[i];
+    }
+    for (int i = tid; i < N * K; i += blockDim.x) {
+        const int r = i / K, k = i % K;
+        *reinterpret_cast<float*>(b_s + tc::kmaj_off(r, k, N)) = Bt[i];
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = tbase;
+    const uint32_t a_tm = tm + 256;   // A in TMEM at columns 256..256+K
+    if (mode == 2) {
+        // thread = row (warp w owns lanes 32w..): columns k of its row
+        float v[K];
+        for (int k = 0; k < K; k++) v[k] = A[tid * K + k];
+        const uint32_t ta = a_tm + (uint32_t(warp * 32) << 16);
+        tmem_st8(ta, v);
+        tmem_st8(ta + 8, v + 8);
+        tmem_wait_st();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    if (tid == 0) {
+        uint32_t idesc = tc::idesc_tf32(M, N);
+        if (mode == 1) idesc |= 1u << 14;
+        constexpr uint32_t LBOA = (M / 8) * 128, LBOB = (N / 8) * 128;
+        for (int ks = 0; ks < K / 8; ks++) {
+            const uint64_t db = tc::desc_kmajor(tc::smem_u32(b_s) + ks * 2 * LBOB, LBOB);
+            if (mode == 2)
+                mma_ts(tm, a_tm + ks * 8, db, idesc, ks ? 1u : 0u);
+            else
+                tc::mma_tf32(tm, tc::desc_kmajor(tc::smem_u32(a_s) + ks * 2 * LBOA, LBOA), db, idesc, ks ? 1u : 0u);
+        }
+        tc::commit(&bar);
+    }
+    tc::mbar_wait(&bar, 0);
+    tc::fence_after_sync();
+    for (int c0 = 0; c0 < N; c0 += 8) {
+        float v[8];
+        tc::tmem_ld8(tm + (uint32_t(warp * 32) << 16) + c0, v);
+        tc::tmem_wait_ld();
+        for (int j = 0; j < 8; j++) D[tid * N + c0 + j] = v[j];
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+// throughput: one thread issues `iters` MMAs (M=128, N, K=8) back to back into one accumulator
+template <int N>
+__global__ void rate_kernel(int iters, int a_in_tmem, long long* cycles)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (M + N) * 8; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.5f;
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = tbase;
+    if (tid == 0) {
+        const uint32_t idesc = tc::idesc_tf32(M, N);
+        const uint64_t da = tc::desc_kmajor(tc::smem_u32(smem), (M / 8) * 128);
+        const uint64_t db = tc::desc_kmajor(tc::smem_u32(smem + M * 8 * 4), (N / 8) * 128);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; i++) {
+            if (a_in_tmem)
+                mma_ts(tm, tm + 256, db, idesc, 1u);
+            else
+                tc::mma_tf32(tm, da, db, idesc, 1u);
+        }
+        tc::commit(&bar);
+        tc::mbar_wait(&bar, 0);
+        cycles[0] = clock64() - t0;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+// NACC independent accumulators round-robin (D at column offsets acc * N)
+template <int N, int NACC>
+__global__ void rate_multi_kernel(int iters, long long* cycles)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (M + N) * 8; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.5f;
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = tbase;
+    if (tid == 0) {
+        const uint32_t idesc = tc::idesc_tf32(M, N);
+        const uint64_t da = tc::desc_kmajor(tc::smem_u32(smem), (M / 8) * 128);
+        const uint64_t db = tc::desc_kmajor(tc::smem_u32(smem + M * 8 * 4), (N / 8) * 128);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; i += NACC) {
+#pragma unroll
+            for (int a = 0; a < NACC; a++) tc::mma_tf32(tm + a * N, da, db, idesc, 1u);
+        }
+        tc::commit(&bar);
+        tc::mbar_wait(&bar, 0);
+        cycles[0] = clock64() - t0;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+template <int N, int NACC>
+void rate_multi()
+{
+    long long* dc;
+    cudaMalloc(&dc, 8);
+    const int sm = (M + N) * 8 * 4;
+    cudaFuncSetAttribute(rate_multi_kernel<N, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    const int iters = 4096;
+    rate_multi_kernel<N, NACC><<<1, 128, sm>>>(iters, dc);
+    rate_multi_kernel<N, NACC><<<1, 128, sm>>>(iters, dc);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long c = 0;
+    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+    const double per = double(c) / iters;
+    printf("rate N=%3d x %d accumulators: %.1f cycles per MMA -> %.0f MAC/clk/SM (%s)\n", N, NACC, per,
+           128.0 * N * 8 / per, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+    cudaFree(dc);
+}
+
+// precision of a long 3xTF32 accumulation chain: D[128][32] = sum over S K-steps (K = 8 S) of random
+// FP32 A B, one accumulator (seg = S) or fresh accumulators every `seg` steps summed in FP32 registers
+constexpr int PN = 32;
+__global__ void prec_kernel(const float* A, const float* Bt, float* D, int S, int seg)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int SP = 16;                    // stored steps (the K data repeats with period 8 SP)
+    uint8_t* ah = smem;                       // [SP][128 x 8] canonical, step-major
+    uint8_t* al = ah + SP * M * 8 * 4;
+    uint8_t* bh = al + SP * M * 8 * 4;
+    uint8_t* bl = bh + SP * PN * 8 * 4;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int K = 8 * SP;
+    for (int i = tid; i < M * K; i += blockDim.x) {
+        const int r = i / K, k = i % K, st = k / 8;
+        float h, l;
+        tc::split(A[i], h, l);
+        *reinterpret_cast<float*>(ah + st * M * 32 + tc::kmaj_off(r, k % 8, M)) = h;
+        *reinterpret_cast<float*>(al + st * M * 32 + tc::kmaj_off(r, k % 8, M)) = l;
+    }
+    for (int i = tid; i < PN * K; i += blockDim.x) {
+        const int r = i / K, k = i % K, st = k / 8;
+        float h, l;
+        tc::split(Bt[i], h, l);
+        *reinterpret_cast<float*>(bh + st * PN * 32 + tc::kmaj_off(r, k % 8, PN)) = h;
+        *reinterpret_cast<float*>(bl + st * PN * 32 + tc::kmaj_off(r, k % 8, PN)) = l;
+    }
+    if (warp == 0) tc::tmem_alloc<64>(&tbase);
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = tbase;
+    float acc[PN];
+    for (int j = 0; j < PN; j++) acc[j] = 0.f;
+    int phase = 0;
+    for (int s0 = 0; s0 < S; s0 += seg) {
+        if (tid == 0) {
+            const uint32_t idesc = tc::idesc_tf32(M, PN);
+            for (int st = s0; st < s0 + seg; st++)
+                for (int pass = 0; pass < 3; pass++) {
+                    const uint8_t* a = pass == 1 ? al : ah;
+                    const uint8_t* b = pass == 2 ? bl : bh;
+                    tc::mma_tf32(tm, tc::desc_kmajor(tc::smem_u32(a + (st % SP) * M * 32), (M / 8) * 128),
+                                 tc::desc_kmajor(tc::smem_u32(b + (st % SP) * PN * 32), (PN / 8) * 128), idesc,
+                                 (st > s0 || pass) ? 1u : 0u);
+                }
+            tc::commit(&bar);
+        }
+        tc::mbar_wait(&bar, phase);
+        phase ^= 1;
+        tc::fence_after_sync();
+        for (int c0 = 0; c0 < PN; c0 += 8) {
+            float v[8];
+            tc::tmem_ld8(tm + (uint32_t(warp * 32) << 16) + c0, v);
+            tc::tmem_wait_ld();
+            for (int j = 0; j < 8; j++) acc[c0 + j] += v[j];
+        }
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+    }
+    for (int j = 0; j < PN; j++) D[tid * PN + j] = acc[j];
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<64>(tm);
+}
+
+void prec(int S, int seg)
+{
+    const int K = 8 * S, KP = 128;   // device holds K period KP
+    std::vector<float> Ap(M * KP), Btp(PN * KP), A(M * K), Bt(PN * K), D(M * PN);
+    srand(11);
+    for (auto& x : Ap) x = float(rand()) / RAND_MAX * 2 - 1;
+    for (auto& x : Btp) x = float(rand()) / RAND_MAX * 2 - 1;
+    for (int i = 0; i < M; i++)
+        for (int k = 0; k < K; k++) A[i * K + k] = Ap[i * KP + k % KP];
+    for (int i = 0; i < PN; i++)
+        for (int k = 0; k < K; k++) Bt[i * K + k] = Btp[i * KP + k % KP];
+    float *dA, *dB, *dD;
+    cudaMalloc(&dA, Ap.size() * 4);
+    cudaMalloc(&dB, Btp.size() * 4);
+    cudaMalloc(&dD, D.size() * 4);
+    cudaMemcpy(dA, Ap.data(), Ap.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, Btp.data(), Btp.size() * 4, cudaMemcpyHostToDevice);
+    const int sm = 2 * 16 * (M + PN) * 8 * 4;
+    cudaFuncSetAttribute(prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    prec_kernel<<<1, 128, sm>>>(dA, dB, dD, S, seg);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+    double num = 0, den = 0, num32 = 0;
+    for (int i = 0; i < M; i++)
+        for (int j = 0; j < PN; j++) {
+            double ref = 0;
+            float r32 = 0;
+            for (int k = 0; k < K; k++) {
+                ref += double(A[i * K + k]) * Bt[j * K + k];
+                r32 = fmaf(A[i * K + k], Bt[j * K + k], r32);
+            }
+            num += (D[i * PN + j] - ref) * (D[i * PN + j] - ref);
+            num32 += (r32 - ref) * (r32 - ref);
+            den += ref * ref;
+        }
+    printf("prec K=%5d (S=%3d MMA steps x3) seg=%3d: 3xTF32 rel l2 %.2e   (sequential FP32 FFMA: %.2e) %s\n", K, S,
+           seg, sqrt(num / den), sqrt(num32 / den), e == cudaSuccess ? "" : cudaGetErrorString(e));
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dD);
+}
+
+template <int N>
+int check(int mode)
+{
+    std::vector<float> A(M * K), Bt(N * K), D(M * N);
+    srand(3 + mode);
+    for (auto& x : A) x = float(rand() % 64 - 32) / 16.f;   // exactly representable in tf32
+    for (auto& x : Bt) x = float(rand() % 64 - 32) / 16.f;
+    float *dA, *dB, *dD;
+    cudaMalloc(&dA, A.size() * 4);
+    cudaMalloc(&dB, Bt.size() * 4);
+    cudaMalloc(&dD, D.size() * 4);
+    cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, Bt.data(), Bt.size() * 4, cudaMemcpyHostToDevice);
+    const int sm = (M + N) * K * 4;
+    cudaFuncSetAttribute(probe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    probe_kernel<N><<<1, 128, sm>>>(dA, dB, dD, mode);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        printf("probe N=%d mode %d: CUDA error %s\n", N, mode, cudaGetErrorString(e));
+        return 1;
+    }
+    cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+    double maxerr = 0;
+    for (int i = 0; i < M; i++)
+        for (int j = 0; j < N; j++) {
+            double ref = 0;
+            for (int k = 0; k < K; k++) ref += double(A[i * K + k]) * Bt[j * K + k];
+            if (mode == 1) ref = -ref;
+            maxerr = fmax(maxerr, fabs(D[i * N + j] - ref));
+        }
+    printf("probe N=%d mode %s: max abs err %.3e -> %s\n", N, mode == 0 ? "SS" : mode == 1 ? "SS negB" : "TS (A in TMEM)",
+           maxerr, maxerr == 0 ? "EXACT" : "WRONG");
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dD);
+    return maxerr == 0 ? 0 : 1;
+}
+
+template <int N>
+void rate(int ts)
+{
+    long long* dc;
+    cudaMalloc(&dc, 8);
+    const int sm = (M + N) * 8 * 4;
+    cudaFuncSetAttribute(rate_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    const int iters = 4096;
+    rate_kernel<N><<<1, 128, sm>>>(iters, ts, dc);
+    rate_kernel<N><<<1, 128, sm>>>(iters, ts, dc);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long c = 0;
+    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+    const double per = double(c) / iters;
+    printf("rate N=%3d A in %s: %.1f cycles per 128x%dx8 MMA -> %.0f MAC/clk/SM (%s)\n", N, ts ? "TMEM" : "SMEM", per,
+           N, 128.0 * N * 8 / per, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+    cudaFree(dc);
+}
+
+int main()
+{
+    int fails = 0;
+    fails += check<48>(0);
+    fails += check<48>(1);
+    fails += check<48>(2);
+    fails += check<160>(0);
+    fails += check<256>(2);
+    for (int ts = 0; ts < 2; ts++) {
+        rate<32>(ts);
+        rate<48>(ts);
+        rate<80>(ts);
+        rate<128>(ts);
+        rate<160>(ts);
+        rate<256>(ts);
+    }
+    rate_multi<32, 1>();
+    rate_multi<32, 4>();
+    rate_multi<64, 1>();
+    rate_multi<64, 2>();
+    rate_multi<64, 4>();
+    rate_multi<128, 2>();
+    rate_multi<128, 4>();
+    rate_multi<256, 2>();
+    for (int S : {16, 64, 256}) {
+        prec(S, S);
+        prec(S, 4);
+        prec(S, 1);
+    }
+    printf(fails ? "TC PROBE2: %d FAILED\n" : "TC PROBE2 OK\n", fails);
+    return 0;
+}
