@@ -189,6 +189,11 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
 #define BF_OPT_TENSOR_CORES 1
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
+/* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band
+ * launch on the current device recorded for CTA 0 -- its first 64 jobs x 12 event slots (clock64
+ * values; 0 = not recorded) -- into out[0 .. n).  Synchronous. */
+bf_status_t bf_debug_band_trace(int64_t *out, int32_t n);
+
 /* Wait for the plan's outstanding work, then free everything it owns. */
 bf_status_t bf_plan_destroy(bf_plan_t plan);
 

@@ -54,6 +54,9 @@ bool band_tc_supported(const Dims& d, int nv);
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
                            cudaStream_t s, int rh = 0, int rhg = 0);
 
+// Diagnostic: SM-clock timeline of the last band_tc launch (CTA 0, first 64 jobs x 12 events).
+cudaError_t band_trace(long long* out, int n);
+
 // Plan finalization: W[p] <- Sw[p] W[p] for npairs blocks (W column-major R x cols, Sw R x R).
 cudaError_t launch_fold_switch(const float2* Sw, float2* W, int64_t npairs, int R, int cols, cudaStream_t s);
 

@@ -847,6 +847,13 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     return BF_OK;
 }
 
+bf_status_t bf_debug_band_trace(int64_t* out, int32_t n)
+{
+    if (!out || n < 0) return fail(BF_ERR_INVALID_ARG, "bad argument");
+    cudaError_t e = bfk::band_trace(reinterpret_cast<long long*>(out), n);
+    return e == cudaSuccess ? BF_OK : cuda_fail(e, "band trace");
+}
+
 bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");

@@ -144,8 +144,8 @@ cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U
 // K = 2 n0, split hi/lo once into shared memory.  The n0 2r rows of B are swept in chunks of 128
 // (N = 128 per MMA); each chunk's K is split in two halves accumulated in separate TMEM columns
 // (short chains, summed in FP32 by the epilogue).  Weight tiles (32 KB hi+lo per 32 K) stream
-// through a 3-deep ring of bulk copies.  Warps 0-3 epilogue (TMEM lanes = vectors), warp 4 loader,
-// warp 5 MMA issuer; all six build A.
+// through a 3-deep ring of bulk copies.  Warps 0-3 and 6-9 epilogue (TMEM lanes = vectors, half the
+// columns each), warp 4 loader, warp 5 MMA issuer; all ten build A.
 // =============================================================================================
 template <int R, int N0>
 struct S0TC {
@@ -162,7 +162,7 @@ struct S0TC {
 };
 
 template <int R, int N0>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     s0_tc_kernel(const float2* __restrict__ F, int64_t ldf, const float2* __restrict__ ampb,
                  const float* __restrict__ V0x, float2* __restrict__ out, int LN, int n_amp, int nv, int nvt)
 {
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int i = 0; i < 2; i++) {
             tc::mbar_init(&dfull[i], 1);
-            tc::mbar_init(&dempty[i], 128);
+            tc::mbar_init(&dempty[i], 256);
         }
         tc::mbar_fence_init();
     }
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(192, 1)
     // Lane map 4 jj x 8 v: 64-byte global segments per column, conflict-free 16-byte smem stores.
     {
         constexpr int NJG = N0 / 8;   // groups of 4 jj
-        for (int wb = warp; wb < 16 * NJG; wb += 6) {
+        for (int wb = warp; wb < 16 * NJG; wb += 10) {
             const int v = (wb % 16) * 8 + (lane >> 2), jj = (wb / 16) * 4 + (lane & 3);
             const int vg = v0 + v;
             float4 hi = make_float4(0, 0, 0, 0), lo = hi;
@@ -277,27 +277,31 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
     } else {
-        // ---- epilogue: TMEM lane = tid = vector of the tile; column n = (a, t, c') of the chunk ----
-        const int vg = v0 + tid;
+        // ---- epilogue (warps 0-3 and 6-9): TMEM lane quarter warp % 4 = vectors; warps 0-3 take the
+        // columns [0, 64) of each 128-column chunk, warps 6-9 the columns [64, 128).  Column n of chunk nc
+        // is the output (a, t, c') with a R + t = (128 nc + n) / 2.
+        const int q4 = warp & 3, vg = v0 + q4 * 32 + lane, cbase = warp < 4 ? 0 : 64;
         for (int nc = 0; nc < C::NCH; nc++) {
             const int slot = nc & 1;
             tc::mbar_wait(&dfull[slot], (nc >> 1) & 1);
             tc::fence_after_sync();
-            const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(slot * 256);
+            const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(slot * 256 + cbase);
 #pragma unroll 1
-            for (int c0 = 0; c0 < S0X_NC; c0 += 16) {
-                float x[16], y[16];
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                float x[32], y[32];
                 tc::tmem_ld16(taddr + c0, x);
+                tc::tmem_ld16(taddr + c0 + 16, x + 16);
                 tc::tmem_ld16(taddr + 128 + c0, y);
+                tc::tmem_ld16(taddr + 128 + c0 + 16, y + 16);
                 tc::tmem_wait_ld();
-                if (c0 + 16 == S0X_NC) {
+                if (c0 == 32) {
                     tc::fence_before_sync();
                     tc::mbar_arrive(&dempty[slot]);
                 }
                 if (vg < nv) {
 #pragma unroll
-                    for (int i = 0; i < 8; i++) {
-                        const int q = (nc * S0X_NC + c0) / 2 + i;   // complex output index a R + t
+                    for (int i = 0; i < 16; i++) {
+                        const int q = (nc * S0X_NC + cbase + c0) / 2 + i;   // complex output index a R + t
                         const int a = q / R, t = q - a * R;
                         out[((int64_t(a) * nleaf + b) * R + t) * nv + vg] =
                             make_float2(x[2 * i] + y[2 * i], x[2 * i + 1] + y[2 * i + 1]);
@@ -324,7 +328,7 @@ static cudaError_t s0_tc_go(const Dims& d, const float2* F, int64_t ldf, const f
     if (e != cudaSuccess) return e;
     const int nvt = (nv + 127) / 128;
     const int64_t ctas = (d.N / N0) * nvt;
-    kern<<<unsigned(ctas), 192, C::SMEM, s>>>(F, ldf, ampb, V0x, out, d.LN, d.n_amp, nv, nvt);
+    kern<<<unsigned(ctas), 320, C::SMEM, s>>>(F, ldf, ampb, V0x, out, d.LN, d.n_amp, nv, nvt);
     return cudaGetLastError();
 }
 
@@ -348,19 +352,20 @@ cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const floa
 // CTA = one T_X leaf a x one tile of 128 vectors.  D[v][2j + c'] = sum over K = (b, t, c) of
 // A[v][(b, t, c)] B[(j, c')][(b, t, c)], A = delta_D[a n0 + b][t][v] split hi/lo, B = the expanded
 // U tiles of the leaf.  K streams in chunks of KP pairs:
-//   warp 8 (one thread)   bulk-copies the raw delta rows and the B tile of a chunk (2-deep rings),
+//   warp 12 (one thread)  bulk-copies the raw delta rows and the B tile of a chunk (2-deep rings),
 //   warps 0-3             split a raw chunk into one of two A stages,
-//   warp 9 (one thread)   issues the 3 KC/8 MMAs of a chunk; every SEG chunks it switches between
+//   warp 13 (one thread)  issues the 3 KC/8 MMAs of a chunk; every SEG chunks it switches between
 //                         two TMEM accumulators (short chains),
-//   warps 4-7             drain each finished segment into FP32 registers, then apply a_k, sum
-//                         over k by lane shuffles and write G through a shared-memory transpose.
+//   warps 4-11            drain each finished segment into FP32 registers (lane quarter = vectors,
+//                         half the columns each), then apply a_k, sum over k by lane shuffles and
+//                         write G through a shared-memory transpose.
 // =============================================================================================
 template <int R, int N0, int NA, int KP>
 struct SLTC {
     static constexpr int NB = 2 * N0;
     static constexpr int KC = KP * 2 * R;
     static constexpr int NCH = N0 / KP;
-    static constexpr int SEG = 1;                                // chunks per accumulation segment
+    static constexpr int SEG = 2;                                // chunks per accumulation segment
     static constexpr int NSEG = (NCH + SEG - 1) / SEG;
     static constexpr uint32_t RAW = uint32_t(KP) * R * 128 * 8;
     static constexpr uint32_t BT = uint32_t(NB) * KC * 4;   // one of hi / lo
@@ -374,7 +379,7 @@ struct SLTC {
 };
 
 template <int R, int N0, int NA, int KP>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(448, 1)
     sl_tc_kernel(const float2* __restrict__ in, const float* __restrict__ Ux, const float2* __restrict__ ampa,
                  float2* __restrict__ G, int64_t ldg, int LN, int nv, int nvt)
 {
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(320, 1)
             tc::mbar_init(&a_full[i], 128);
             tc::mbar_init(&a_empty[i], 1);
             tc::mbar_init(&dfull[i], 1);
-            tc::mbar_init(&dempty[i], 128);
+            tc::mbar_init(&dempty[i], 256);
         }
         tc::mbar_fence_init();
     }
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(320, 1)
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base;
 
-    if (warp == 8) {
+    if (warp == 12) {
         // ---- loader ----
         if (lane == 0) {
             const uint32_t row_bytes = uint32_t(vw) * 8;
@@ -434,7 +439,7 @@ __global__ void __launch_bounds__(320, 1)
                                  &raw_full[e]);
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == 13) {
         // ---- MMA issuer ----
         if (lane == 0) {
             constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
@@ -490,33 +495,35 @@ __global__ void __launch_bounds__(320, 1)
             tc::mbar_arrive(&a_full[e]);
         }
     } else {
-        // ---- drain (warps 4-7): lane quarter warp - 4 = vectors, all NB columns ----
-        const int q4 = warp - 4, vl = q4 * 32 + lane;
-        float sum[C::NB];
+        // ---- drain (warps 4-11): lane quarter warp % 4 = vectors, column half (warp - 4) / 4 ----
+        constexpr int HC = C::NB / 2;   // columns per drain thread (j in a half of the leaf)
+        const int q4 = warp & 3, half = (warp - 4) >> 2, vl = q4 * 32 + lane;
+        float sum[HC];
 #pragma unroll
-        for (int i = 0; i < C::NB; i++) sum[i] = 0.f;
+        for (int i = 0; i < HC; i++) sum[i] = 0.f;
         for (int seg = 0; seg < C::NSEG; seg++) {
             const int slot = seg & 1;
             tc::mbar_wait(&dfull[slot], (seg >> 1) & 1);
             tc::fence_after_sync();
-            const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(slot * C::NB);
+            const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(slot * C::NB + half * HC);
 #pragma unroll
-            for (int c0 = 0; c0 < C::NB; c0 += 16) {
-                float x[16];
-                tc::tmem_ld16(taddr + c0, x);
+            for (int c0 = 0; c0 < HC; c0 += 32) {
+                float x[32];
+                tc::tmem_ld_cols<(HC < 32 ? HC : 32)>(taddr + c0, x);
                 tc::tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 16; i++) sum[c0 + i] += x[i];
+                for (int i = 0; i < (HC < 32 ? HC : 32); i++) sum[c0 + i] += x[i];
             }
             tc::fence_before_sync();
             tc::mbar_arrive(&dempty[slot]);
         }
         // every MMA has completed (last dfull): the rings are free for the G staging
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         const int k = vl % NA, cl = vl / NA;
 #pragma unroll
-        for (int j = 0; j < N0; j++) {
-            float2 g = cmul_tc(As[k * N0 + j], make_float2(sum[2 * j], sum[2 * j + 1]));
+        for (int jj = 0; jj < HC / 2; jj++) {
+            const int j = half * (HC / 2) + jj;
+            float2 g = cmul_tc(As[k * N0 + j], make_float2(sum[2 * jj], sum[2 * jj + 1]));
 #pragma unroll
             for (int m = 1; m < NA; m <<= 1) {
                 g.x += __shfl_xor_sync(0xffffffffu, g.x, m);
@@ -524,10 +531,10 @@ __global__ void __launch_bounds__(320, 1)
             }
             if ((j % NA) == k) Gs[cl * C::GS_STRIDE + j] = g;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         // copy out: RHS column c0 + cl, rows a n0 .. a n0 + n0 - 1 (contiguous)
-        const int c0 = v0 / NA, cw = vw / NA;
-        for (int idx = vl; idx < cw * N0; idx += 128) {
+        const int c0 = v0 / NA, cw = vw / NA, dt = (warp - 4) * 32 + lane;
+        for (int idx = dt; idx < cw * N0; idx += 256) {
             const int cc = idx / N0, j = idx % N0;
             G[a * N0 + j + int64_t(c0 + cc) * ldg] = Gs[cc * C::GS_STRIDE + j];
         }
@@ -550,7 +557,7 @@ static cudaError_t sl_tc_go(const Dims& d, const float2* in, const float* Ux, co
     if (e != cudaSuccess) return e;
     const int nvt = (nv + 127) / 128;
     const int64_t ctas = (d.N / N0) * nvt;
-    kern<<<unsigned(ctas), 320, C::SMEM, s>>>(in, Ux, ampa, G, ldg, d.LN, nv, nvt);
+    kern<<<unsigned(ctas), 448, C::SMEM, s>>>(in, Ux, ampa, G, ldg, d.LN, nv, nvt);
     return cudaGetLastError();
 }
 
@@ -570,6 +577,14 @@ cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const
     SLTC_NA(6, 32, 2) SLTC_NA(8, 32, 2) SLTC_NA(10, 32, 2) SLTC_NA(12, 32, 1) SLTC_NA(16, 32, 1)
 #undef SLTC_NA
     return cudaErrorInvalidValue;
+}
+
+// ---- timeline trace of the band kernel (diagnostic; CTA 0, first BT_JOBS jobs, SM clock) ----
+constexpr int BT_JOBS = 64, BT_EV = 12;
+__device__ long long g_band_trace[BT_JOBS * BT_EV];
+__device__ __forceinline__ void btrace(int64_t J, int ev)
+{
+    if (blockIdx.x == 0 && J < BT_JOBS) g_band_trace[J * BT_EV + ev] = clock64();
 }
 
 // =============================================================================================
@@ -677,6 +692,7 @@ __global__ void __launch_bounds__(384, 1)
             const int64_t use = J / C::NABUF;
             if (use > 0) tc::mbar_wait(&a_free[slot], uint32_t(use - 1) & 1);
             tc::fence_after_sync();
+            if (tid == 0) btrace(J, 0);
             const float2* rd = reinterpret_cast<const float2*>(raw(e));
 #pragma unroll 1
             for (int s = 0; s < C::P; s++) {
@@ -693,6 +709,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             tc::tmem_wait_st();
             tc::fence_before_sync();
+            if (tid == 0) btrace(J, 1);
             tc::mbar_arrive(&raw_empty[e]);
             tc::mbar_arrive(&a1_ready[slot]);
         }
@@ -708,6 +725,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t ph = uint32_t(J & 1);
             tc::mbar_wait(&d1_full, ph);
             tc::fence_after_sync();
+            if (v == 0) btrace(J, 3);
 #pragma unroll 1
             for (int u = 0; u < C::U; u++) {
                 float d[C::NU];
@@ -725,11 +743,13 @@ __global__ void __launch_bounds__(384, 1)
             }
             tc::tmem_wait_st();
             tc::fence_before_sync();
+            if (v == 0) btrace(J, 4);
             tc::mbar_arrive(&d1_free);
             tc::mbar_arrive(&a2_ready[slot]);
 
             tc::mbar_wait(&d2_full, ph);
             tc::fence_after_sync();
+            if (v == 0) btrace(J, 6);
             float d[C::U][C::NU];
 #pragma unroll
             for (int u = 0; u < C::U; u++) tc::tmem_ld_cols<C::NU>(tmem + lb + uint32_t(C::D2_OFF + u * C::NB), d[u]);
@@ -760,6 +780,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int64_t g = blockIdx.x + it * gridDim.x;
                 const int e = int(J & 1);
                 if (J >= 2) tc::mbar_wait(&raw_empty[e], uint32_t((J >> 1) - 1) & 1);
+                btrace(J, 8);
                 const int v0 = vt * 128, vw = min(128, nv - v0);
                 const uint32_t row_bytes = uint32_t(vw) * 8;
                 tc::mbar_arrive_expect_tx(&raw_full[e], C::P * R * row_bytes);
@@ -770,42 +791,43 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp == 9) {
-        // ---- MMA issuer ----
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
-            constexpr uint32_t LBO_B = (C::NB / 8) * 128;
-            const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_band + C::OFF_W), LBO_B);
-            for (int64_t J = 0; J < njobs; J++) {
-                const int64_t it = J / nvt;
-                const int vt = int(J - it * nvt);
-                const int wb = int(it % C::NWBUF), slot = int(J % C::NABUF);
-                if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
+        // ---- MMA issuer (whole warp, one elected lane issues) ----
+        constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
+        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
+        const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_band + C::OFF_W), LBO_B);
+        for (int64_t J = 0; J < njobs; J++) {
+            const int64_t it = J / nvt;
+            const int vt = int(J - it * nvt);
+            const int wb = int(it % C::NWBUF), slot = int(J % C::NABUF);
+            if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
 #pragma unroll 1
-                for (int m = 0; m < 2; m++) {
-                    tc::mbar_wait(m == 0 ? &a1_ready[slot] : &a2_ready[slot], uint32_t(J / C::NABUF) & 1);
-                    if (J >= 1) tc::mbar_wait(m == 0 ? &d1_free : &d2_free, uint32_t(J - 1) & 1);
-                    tc::fence_after_sync();
+            for (int m = 0; m < 2; m++) {
+                if (lane == 0) btrace(J, m == 0 ? 9 : 10);
+                tc::mbar_wait(m == 0 ? &a1_ready[slot] : &a2_ready[slot], uint32_t(J / C::NABUF) & 1);
+                if (J >= 1) tc::mbar_wait(m == 0 ? &d1_free : &d2_free, uint32_t(J - 1) & 1);
+                tc::fence_after_sync();
 #pragma unroll
-                    for (int u = 0; u < C::U; u++) {
-                        const uint32_t d = tmem + uint32_t((m == 0 ? C::D1_OFF : C::D2_OFF) + u * C::NB);
-                        const uint32_t ahi = tmem + uint32_t(slot * C::ACOLS + 2 * u * C::SC);
-                        const uint64_t bhi = tc::desc_add(dW, wb * C::WSET + ((m * C::U + u) * 2) * C::WT);
+                for (int u = 0; u < C::U; u++) {
+                    const uint32_t d = tmem + uint32_t((m == 0 ? C::D1_OFF : C::D2_OFF) + u * C::NB);
+                    const uint32_t ahi = tmem + uint32_t(slot * C::ACOLS + 2 * u * C::SC);
+                    const uint64_t bhi = tc::desc_add(dW, wb * C::WSET + ((m * C::U + u) * 2) * C::WT);
 #pragma unroll
-                        for (int q = 0; q < 3; q++) {
-                            const int pass = kPassOrder[q];
-                            const uint32_t a = ahi + (pass == 1 ? C::P * C::SC : 0);
-                            const uint64_t b = pass == 2 ? tc::desc_add(bhi, C::WT) : bhi;
+                    for (int q = 0; q < 3; q++) {
+                        const int pass = kPassOrder[q];
+                        const uint32_t a = ahi + (pass == 1 ? C::P * C::SC : 0);
+                        const uint64_t b = pass == 2 ? tc::desc_add(bhi, C::WT) : bhi;
 #pragma unroll
-                            for (int ks = 0; ks < C::KU / 8; ks++)
-                                tc::mma_tf32_ts(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc,
-                                                (q | ks) ? 1u : 0u);
-                        }
+                        for (int ks = 0; ks < C::KU / 8; ks++)
+                            tc::mma_tf32_ts_warp(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc,
+                                                 (q | ks) ? 1u : 0u);
                     }
-                    tc::commit(m == 0 ? &d1_full : &d2_full);
                 }
-                tc::commit(&a_free[slot]);
-                if (vt == nvt - 1) tc::commit(&w_free[wb]);
+                if (lane == 0) btrace(J, m == 0 ? 2 : 5);
+                tc::commit_warp(m == 0 ? &d1_full : &d2_full);
             }
+            tc::commit_warp(&a_free[slot]);
+            if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
+            __syncwarp();
         }
     } else {
         // ---- weights (warps 10-11): compact r x 2r blocks -> embedded hi/lo B tiles, one group ahead ----
@@ -883,6 +905,12 @@ static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, floa
     const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
     kern<<<grid, 384, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg);
     return cudaGetLastError();
+}
+
+cudaError_t band_trace(long long* out, int n)
+{
+    if (n > BT_JOBS * BT_EV) n = BT_JOBS * BT_EV;
+    return cudaMemcpyFromSymbol(out, g_band_trace, size_t(n) * sizeof(long long));
 }
 
 bool band_tc_supported(const Dims& d, int nv)

@@ -1,0 +1,25 @@
+"""Timeline of the tensor-core band kernel (CTA 0): per job, SM-clock events relative to job 0's start."""
+import os
+import sys
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1803_04128_b200 import bf  # noqa: E402
+from paper_1803_04128_b200 import workloads as W  # noqa: E402
+
+w = W.CONFIGS["cfg4"].with_(log2n=int(sys.argv[1]) if len(sys.argv) > 1 else 18)
+plan = bf.Plan.build_fio(bf.fio_of(w), max_nrhs_chunk=w.nrhs)
+F = torch.randn(w.nrhs, w.n, dtype=torch.complex64, device="cuda")
+G = torch.empty_like(F)
+for _ in range(2):
+    plan.apply(F, G, w.nrhs)
+torch.cuda.synchronize()
+T = bf.debug_band_trace()   # the last band launch of the apply (second half)
+names = ["split0", "split1", "L1iss", "E1beg", "E1end", "L2iss", "E2beg", "E2end", "load", "L1wait", "L2wait", "-"]
+t0 = T[0, 8]
+print("job " + " ".join(f"{n:>7s}" for n in names[:11]))
+for j in range(0, 40):
+    print(f"{j:3d} " + " ".join(f"{(T[j, k] - t0) if T[j, k] else -1:7d}" for k in range(11)))
+d = np.diff(T[8:40, 2])
+print("steady-state clocks per job (L1 issue to L1 issue):", np.median(d))

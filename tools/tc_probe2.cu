@@ -140,7 +140,7 @@ __global__ void rate_kernel(int iters, int a_in_tmem, long long* cycles)
 }
 
 // NACC independent accumulators round-robin (D at column offsets acc * N)
-template <int N, int NACC>
+template <int N, int NACC, bool TS = false>
 __global__ void rate_multi_kernel(int iters, long long* cycles)
 {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -165,7 +165,12 @@ __global__ void rate_multi_kernel(int iters, long long* cycles)
         const long long t0 = clock64();
         for (int i = 0; i < iters; i += NACC) {
 #pragma unroll
-            for (int a = 0; a < NACC; a++) tc::mma_tf32(tm + a * N, da, db, idesc, 1u);
+            for (int a = 0; a < NACC; a++) {
+                if constexpr (TS)
+                    mma_ts(tm + a * N, tm + 480, db, idesc, 1u);
+                else
+                    tc::mma_tf32(tm + a * N, da, db, idesc, 1u);
+            }
         }
         tc::commit(&bar);
         tc::mbar_wait(&bar, 0);
@@ -176,22 +181,194 @@ __global__ void rate_multi_kernel(int iters, long long* cycles)
     if (warp == 0) tc::tmem_dealloc<512>(tm);
 }
 
-template <int N, int NACC>
+template <int N, int NACC, bool TS = false>
 void rate_multi()
 {
     long long* dc;
     cudaMalloc(&dc, 8);
     const int sm = (M + N) * 8 * 4;
-    cudaFuncSetAttribute(rate_multi_kernel<N, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(rate_multi_kernel<N, NACC, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     const int iters = 4096;
-    rate_multi_kernel<N, NACC><<<1, 128, sm>>>(iters, dc);
-    rate_multi_kernel<N, NACC><<<1, 128, sm>>>(iters, dc);
+    rate_multi_kernel<N, NACC, TS><<<1, 128, sm>>>(iters, dc);
+    rate_multi_kernel<N, NACC, TS><<<1, 128, sm>>>(iters, dc);
     cudaError_t e = cudaDeviceSynchronize();
     long long c = 0;
     cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
     const double per = double(c) / iters;
-    printf("rate N=%3d x %d accumulators: %.1f cycles per MMA -> %.0f MAC/clk/SM (%s)\n", N, NACC, per,
+    printf("rate N=%3d x %d accumulators, A in %s: %.1f cycles per MMA -> %.0f MAC/clk/SM (%s)\n", N, NACC,
+           TS ? "TMEM" : "SMEM", per,
            128.0 * N * 8 / per, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+    cudaFree(dc);
+}
+
+// MMA rate (N=48, A in TMEM or SMEM) while 4 other warps stream tcgen05.st / tcgen05.ld traffic to other
+// TMEM columns (the band kernel's split / epilogue load) -- is the MMA slowed by TMEM contention?
+template <bool TS, int MODE>   // MODE 0: none, 1: st, 2: ld, 3: st+ld heavy (8 warps), 4: LDS, 5: STG
+__global__ void contention_kernel(int iters, long long* cycles, float2* gbuf)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    __shared__ volatile int stop;
+    constexpr int N = 48;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < (M + N) * 8; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.5f;
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::mbar_fence_init();
+        stop = 0;
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = tbase;
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_tf32(M, N);
+            const uint64_t da = tc::desc_kmajor(tc::smem_u32(smem), (M / 8) * 128);
+            const uint64_t db = tc::desc_kmajor(tc::smem_u32(smem + M * 8 * 4), (N / 8) * 128);
+            const long long t0 = clock64();
+            for (int i = 0; i < iters; i += 2) {
+                if constexpr (TS) {
+                    mma_ts(tm, tm + 200, db, idesc, 1u);
+                    mma_ts(tm + 48, tm + 208, db, idesc, 1u);
+                } else {
+                    tc::mma_tf32(tm, da, db, idesc, 1u);
+                    tc::mma_tf32(tm + 48, da, db, idesc, 1u);
+                }
+            }
+            tc::commit(&bar);
+            tc::mbar_wait(&bar, 0);
+            cycles[0] = clock64() - t0;
+            stop = 1;
+        }
+        __syncwarp();
+    } else if (MODE > 0) {
+        const uint32_t ta = tm + (uint32_t((warp & 3) * 32) << 16) + 256;
+        float v[16];
+        for (int i = 0; i < 16; i++) v[i] = float(i);
+        float acc = 0.f;
+        int it = 0;
+        while (!stop) {
+            if constexpr (MODE == 1 || MODE == 2) {
+                for (int r = 0; r < 8; r++) {
+                    if constexpr (MODE == 1) tc::tmem_st16(ta + r * 16, v); else tc::tmem_ld16(ta + r * 16, v);
+                }
+                if constexpr (MODE == 1) tc::tmem_wait_st(); else tc::tmem_wait_ld();
+            } else if constexpr (MODE == 3) {
+                for (int r = 0; r < 10; r++) tc::tmem_st16(ta + r * 16, v);
+                for (int r = 0; r < 5; r++) tc::tmem_ld16(ta + 160 + r * 16, v);
+                tc::tmem_wait_st();
+                tc::tmem_wait_ld();
+            } else if constexpr (MODE == 4) {
+                const float4* sp = reinterpret_cast<const float4*>(smem);
+                for (int r = 0; r < 16; r++) {
+                    const float4 q = sp[(r * 256 + threadIdx.x) % 1024];
+                    acc += q.x + q.w;
+                }
+            } else {
+                for (int r = 0; r < 16; r++) gbuf[(int64_t(it) * 16 + r) * 512 % (1 << 24) + threadIdx.x] = make_float2(acc, 1.f);
+                it++;
+            }
+        }
+        if (v[3] == 12345.f || acc == 12345.f) cycles[1] = 1;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+template <bool TS, int MODE>
+void contention()
+{
+    long long* dc;
+    cudaMalloc(&dc, 16);
+    const int sm = (M + 48) * 8 * 4;
+    cudaFuncSetAttribute(contention_kernel<TS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    float2* gb;
+    cudaMalloc(&gb, (size_t(1) << 24) * 8 + 4096 * 8);
+    const int threads = MODE >= 3 ? 288 : 160;
+    contention_kernel<TS, MODE><<<1, threads, sm>>>(4096, dc, gb);
+    contention_kernel<TS, MODE><<<1, threads, sm>>>(4096, dc, gb);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long c = 0;
+    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+    printf("contention: N=48 A in %s, other warps %s: %.1f cycles per MMA (%s)\n", TS ? "TMEM" : "SMEM",
+           MODE == 0 ? "idle" : MODE == 1 ? "tcgen05.st" : MODE == 2 ? "tcgen05.ld" : MODE == 3 ? "st+ld x8 warps" : MODE == 4 ? "LDS x8 warps" : "STG x8 warps", double(c) / 4096,
+           e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+    cudaFree(dc);
+}
+
+// The band kernel's exact MMA sequence (r = 10): per level 2 units x 3 passes x 5 K steps, A in TMEM
+// (hi slots at +0, lo at +80), B = 4 distinct 48 x 40 K-major tiles in smem.  VARIANT 0: as the band;
+// 1: B always tile 0; 2: A always columns 0..7; 3: B tiles in SWIZZLE_NONE but N=48 rows padded to 64.
+template <int VARIANT>
+__global__ void bandseq_kernel(int reps, long long* cycles)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    constexpr int NB = VARIANT == 3 ? 64 : 48, KU = 40;
+    constexpr uint32_t WT = NB * KU * 4;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 4 * NB * KU; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.001f * (i % 97);
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = tbase;
+    if (tid == 0) {
+        constexpr uint32_t idesc = tc::idesc_tf32(128, NB);
+        constexpr uint32_t LBO_B = (NB / 8) * 128;
+        const uint64_t dW = tc::desc_kmajor(tc::smem_u32(smem), LBO_B);
+        const long long t0 = clock64();
+        for (int r = 0; r < reps; r++) {
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                const uint32_t d = tm + 160 + u * NB;
+                const uint32_t ahi = tm + (VARIANT == 2 ? 0 : 2 * u * 20);
+                const uint64_t bhi = tc::desc_add(dW, (VARIANT == 1 ? 0 : u * 2) * WT);
+#pragma unroll
+                for (int q = 0; q < 3; q++) {
+                    const int pass = q == 0 ? 1 : q == 1 ? 2 : 0;
+                    const uint32_t a = ahi + (pass == 1 && VARIANT != 2 ? 80 : 0);
+                    const uint64_t b = pass == 2 && VARIANT != 1 ? tc::desc_add(bhi, WT) : bhi;
+#pragma unroll
+                    for (int ks = 0; ks < KU / 8; ks++)
+                        mma_ts(d, a + (VARIANT == 2 ? 0 : ks * 8), tc::desc_add(b, ks * 2 * LBO_B), idesc, (q | ks) ? 1u : 0u);
+                }
+            }
+        }
+        tc::commit(&bar);
+        tc::mbar_wait(&bar, 0);
+        cycles[0] = clock64() - t0;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+template <int VARIANT>
+void bandseq()
+{
+    long long* dc;
+    cudaMalloc(&dc, 8);
+    const int sm = 4 * 64 * 40 * 4;
+    cudaFuncSetAttribute(bandseq_kernel<VARIANT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    bandseq_kernel<VARIANT><<<1, 128, sm>>>(200, dc);
+    bandseq_kernel<VARIANT><<<1, 128, sm>>>(200, dc);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long c = 0;
+    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+    printf("bandseq variant %d: %.1f cycles per MMA (%s)\n", VARIANT, double(c) / (200 * 30),
+           e == cudaSuccess ? "ok" : cudaGetErrorString(e));
     cudaFree(dc);
 }
 
@@ -392,6 +569,24 @@ int main()
     rate_multi<128, 2>();
     rate_multi<128, 4>();
     rate_multi<256, 2>();
+    rate_multi<48, 1, true>();
+    rate_multi<48, 2, true>();
+    rate_multi<64, 1, true>();
+    rate_multi<128, 2, true>();
+    rate_multi<48, 2>();
+    bandseq<0>();
+    bandseq<1>();
+    bandseq<2>();
+    bandseq<3>();
+    contention<true, 0>();
+    contention<true, 1>();
+    contention<true, 2>();
+    contention<false, 0>();
+    contention<false, 1>();
+    contention<false, 2>();
+    contention<true, 3>();
+    contention<true, 4>();
+    contention<true, 5>();
     for (int S : {16, 64, 256}) {
         prec(S, S);
         prec(S, 4);
