@@ -139,49 +139,72 @@ cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U
 }
 
 // =============================================================================================
-// S0 (eqn:1 P:698-702, amplitude pre-scale eqn:tg P:24-28) on the tensor cores.
-// CTA = one leaf b x one tile of 128 vectors.  A = Y^T, Y[j][v] = b_k(x) F[x, c] (x = b n0 + j),
-// K = 2 n0, split hi/lo once into shared memory.  The n0 2r rows of B are swept in chunks of 128
-// (N = 128 per MMA); each chunk's K is split in two halves accumulated in separate TMEM columns
-// (short chains, summed in FP32 by the epilogue).  Weight tiles (32 KB hi+lo per 32 K) stream
-// through a 3-deep ring of bulk copies.  Warps 0-3 and 6-9 epilogue (TMEM lanes = vectors, half the
-// columns each), warp 4 loader, warp 5 MMA issuer; all ten build A.
+// S0 (eqn:1 P:698-702, amplitude pre-scale eqn:tg P:24-28) on the tensor cores, persistent.
+// A job = one leaf b x one tile of 128 vectors (vector tile fastest, so the CTAs working at the same
+// time share each leaf's weights in L2).  D[v][n] = sum_k A[v][k] B[n][k] with A = Y^T,
+// Y[j][v] = b_k(x) F[x, c] (x = b n0 + j, K = 2 n0) split hi/lo into TMEM, and B = the expanded V0
+// tiles of the leaf (n = (a, t, c'), swept in chunks of 128 = MMA N).  Each chunk is one accumulation
+// chain over its K tiles of 32, each tile's passes ordered corrections first;
+// a tile is released as soon as its passes are issued, so the ring streams KS + 1 tiles ahead.
+// Warp roles:
+//   warp 4 (one thread)  bulk-copies the job's F columns + b_k rows into a padded staging tile, and
+//                        streams the weight tiles (ring),
+//   warps 0-3            build A in TMEM (lane = vector) from the staging tile,
+//   warp 5               issues the MMAs (elected lane) into one of two TMEM accumulators,
+//   warps 6-13           epilogue: lane quarter = vectors, half the columns of a chunk each; store
+//                        delta_l0[a N/n0 + b][t][v] (coalesced over v).
 // =============================================================================================
+static int sm_count()
+{
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
 template <int R, int N0>
 struct S0TC {
     static constexpr int K = 2 * N0;
-    static constexpr int KS = K / S0X_KC;                 // 32-wide K chunks (2 or 4)
-    static constexpr int NCH = N0 * 2 * R / S0X_NC;       // 128-row N chunks
-    static constexpr int NIT = NCH * KS;
-    static constexpr int NSTAGE = 3;
+    static constexpr int KS = K / S0X_KC;                 // 32-wide K tiles per chunk (2 or 4)
+    static constexpr int NCH = N0 * 2 * R / S0X_NC;       // 128-row N chunks per job
+    static constexpr int NSTAGE = KS + 1;                 // weight ring depth (32 KB tiles)
     static constexpr uint32_t TILE = S0X_TILE_FLOATS * 4;  // 16 KB
-    static constexpr uint32_t STAGE = 2 * TILE;
-    static constexpr uint32_t A_BYTES = 128u * K * 4;
-    static constexpr size_t SMEM = 2 * size_t(A_BYTES) + NSTAGE * size_t(STAGE);
-    static_assert((N0 * 2 * R) % S0X_NC == 0 && KS % 2 == 0, "tiling");
+    static constexpr uint32_t STAGE = 2 * TILE;            // hi + lo
+    // staging row stride (complex): padded (bank spread) where shared memory allows, else dense
+    static constexpr int FS = (N0 == 64) ? N0 : N0 + 2;
+    static constexpr uint32_t FBYTES = 128u * FS * 8;      // up to 128 F columns (n_amp = 1)
+    static constexpr uint32_t OFF_F = NSTAGE * STAGE, OFF_BK = OFF_F + FBYTES;
+    static constexpr size_t SMEM = size_t(OFF_BK) + 4 * N0 * 8;
+    static constexpr int A_COLS = K;                       // hi at +0, lo at +K
+    static constexpr int D_OFF = 2 * K;                    // two accumulators of 128 columns
+    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * S0X_NC>();
+    static_assert((N0 * 2 * R) % S0X_NC == 0 && KS >= 2, "tiling");
+    static_assert(SMEM <= 232448 - 1024 && D_OFF + 2 * S0X_NC <= 512, "budget");
 };
 
 template <int R, int N0>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(448, 1)
     s0_tc_kernel(const float2* __restrict__ F, int64_t ldf, const float2* __restrict__ ampb,
                  const float* __restrict__ V0x, float2* __restrict__ out, int LN, int n_amp, int nv, int nvt)
 {
     using C = S0TC<R, N0>;
     extern __shared__ __align__(128) uint8_t sm_s0tc[];
-    uint8_t* Ahi = sm_s0tc;
-    uint8_t* Alo = sm_s0tc + C::A_BYTES;
-    uint8_t* ring = sm_s0tc + 2 * C::A_BYTES;
-    __shared__ uint64_t full[C::NSTAGE], empty[C::NSTAGE], dfull[2], dempty[2];
+    uint8_t* ring = sm_s0tc;
+    float2* Fs = reinterpret_cast<float2*>(sm_s0tc + C::OFF_F);    // [column][FS]
+    float2* Bk = reinterpret_cast<float2*>(sm_s0tc + C::OFF_BK);   // [k][N0] b_k(x)
+    __shared__ uint64_t full[C::NSTAGE], empty[C::NSTAGE], dfull[2], dempty[2], f_full, f_empty, a_full, a_free;
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t N = int64_t(1) << LN;
     const int64_t nleaf = N / N0;
-    const int64_t b = blockIdx.x / nvt;
-    const int v0 = (blockIdx.x % nvt) * 128;
-    const float* wsrc = V0x + b * (int64_t(C::NIT) * 2 * S0X_TILE_FLOATS);
+    const int64_t njobs_all = nleaf * nvt;
+    const int64_t njobs = (njobs_all - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
-    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
     if (tid == 0) {
         for (int i = 0; i < C::NSTAGE; i++) {
             tc::mbar_init(&full[i], 1);
@@ -191,120 +214,152 @@ __global__ void __launch_bounds__(320, 1)
             tc::mbar_init(&dfull[i], 1);
             tc::mbar_init(&dempty[i], 256);
         }
+        tc::mbar_init(&f_full, 1);
+        tc::mbar_init(&f_empty, 128);
+        tc::mbar_init(&a_full, 128);
+        tc::mbar_init(&a_free, 1);
         tc::mbar_fence_init();
     }
-    __syncthreads();
-    if (tid == 128) {   // start the weight stream before building A
-        for (int it = 0; it < C::NSTAGE && it < C::NIT; it++) {
-            tc::mbar_arrive_expect_tx(&full[it], C::STAGE);
-            tc::bulk_g2s(ring + it * C::STAGE, wsrc + int64_t(it) * 2 * S0X_TILE_FLOATS, C::STAGE, &full[it]);
-        }
-    }
-    // A = Y^T split hi/lo.  Task (v, jj): complex j = 2jj, 2jj+1 of vector v -> 16 bytes at k = 4 jj.
-    // Lane map 4 jj x 8 v: 64-byte global segments per column, conflict-free 16-byte smem stores.
-    {
-        constexpr int NJG = N0 / 8;   // groups of 4 jj
-        for (int wb = warp; wb < 16 * NJG; wb += 10) {
-            const int v = (wb % 16) * 8 + (lane >> 2), jj = (wb / 16) * 4 + (lane & 3);
-            const int vg = v0 + v;
-            float4 hi = make_float4(0, 0, 0, 0), lo = hi;
-            if (vg < nv) {
-                const int c = vg / n_amp, k = vg - c * n_amp;
-                const int64_t x = b * N0 + 2 * jj;
-                const float4 f = __ldg(reinterpret_cast<const float4*>(F + x + c * ldf));
-                const float4 a = __ldg(reinterpret_cast<const float4*>(ampb + k * N + x));
-                const float2 y0 = cmul_tc(make_float2(a.x, a.y), make_float2(f.x, f.y));
-                const float2 y1 = cmul_tc(make_float2(a.z, a.w), make_float2(f.z, f.w));
-                tc::split(y0.x, hi.x, lo.x);
-                tc::split(y0.y, hi.y, lo.y);
-                tc::split(y1.x, hi.z, lo.z);
-                tc::split(y1.y, hi.w, lo.w);
-            }
-            const uint32_t off = tc::kmaj_off(v, 4 * jj, 128);
-            st_f4(Ahi, off, hi);
-            st_f4(Alo, off, lo);
-        }
-    }
-    tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base;
 
     if (warp == 4) {
-        // ---- loader: the rest of the weight stream ----
+        // ---- loader: per job the F staging tile, and the weight ring (all jobs, in order) ----
         if (lane == 0) {
-            for (int it = C::NSTAGE; it < C::NIT; it++) {
-                const int st = it % C::NSTAGE;
-                tc::mbar_wait(&empty[st], ((it / C::NSTAGE) - 1) & 1);
-                tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
-                tc::bulk_g2s(ring + st * C::STAGE, wsrc + int64_t(it) * 2 * S0X_TILE_FLOATS, C::STAGE, &full[st]);
+            int64_t it = 0;   // weight tiles issued
+            const int64_t total_it = njobs * C::NCH * C::KS;
+            auto issue_weights = [&](int64_t upto) {
+                for (; it < upto && it < total_it; it++) {
+                    const int st = int(it % C::NSTAGE);
+                    if (it >= C::NSTAGE) tc::mbar_wait(&empty[st], uint32_t(it / C::NSTAGE - 1) & 1);
+                    const int64_t jl = it / (C::NCH * C::KS);   // local job
+                    const int64_t b = (blockIdx.x + jl * gridDim.x) / nvt;
+                    const int64_t w = it % (C::NCH * C::KS);
+                    tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
+                    tc::bulk_g2s(ring + st * C::STAGE, V0x + (b * (C::NCH * C::KS) + w) * 2 * S0X_TILE_FLOATS,
+                                 C::STAGE, &full[st]);
+                }
+            };
+            for (int64_t jl = 0; jl < njobs; jl++) {
+                const int64_t job = blockIdx.x + jl * gridDim.x;
+                const int64_t b = job / nvt;
+                const int v0 = int(job % nvt) * 128, vw = min(128, nv - v0);
+                const int c0 = v0 / n_amp, cw = (vw + n_amp - 1) / n_amp;
+                if (jl > 0) tc::mbar_wait(&f_empty, uint32_t(jl - 1) & 1);
+                tc::mbar_arrive_expect_tx(&f_full, uint32_t(cw) * N0 * 8 + uint32_t(n_amp) * N0 * 8);
+                for (int cl = 0; cl < cw; cl++)
+                    tc::bulk_g2s(Fs + cl * C::FS, F + b * N0 + int64_t(c0 + cl) * ldf, N0 * 8, &f_full);
+                for (int k = 0; k < n_amp; k++) tc::bulk_g2s(Bk + k * N0, ampb + k * N + b * N0, N0 * 8, &f_full);
+                issue_weights((jl + 1) * C::NCH * C::KS);   // this job's weight tiles (bounded by the ring)
             }
         }
+    } else if (warp < 4) {
+        // ---- A = Y^T (hi, lo) into TMEM; thread = vector ----
+        const int v = tid;
+        const uint32_t lb = uint32_t(warp * 32) << 16;
+        for (int64_t jl = 0; jl < njobs; jl++) {
+            const int64_t job = blockIdx.x + jl * gridDim.x;
+            const int v0 = int(job % nvt) * 128, vg = v0 + v;
+            const int c0 = v0 / n_amp;
+            tc::mbar_wait(&f_full, uint32_t(jl & 1));
+            if (jl > 0) tc::mbar_wait(&a_free, uint32_t(jl - 1) & 1);
+            tc::fence_after_sync();
+            const bool ok = vg < nv;
+            const int cl = ok ? vg / n_amp - c0 : 0, k = ok ? vg % n_amp : 0;
+            const float2* fc = Fs + cl * C::FS;
+            const float2* bk = Bk + k * N0;
+#pragma unroll 1
+            for (int j0 = 0; j0 < N0; j0 += 8) {
+                float hi[16], lo[16];
+#pragma unroll
+                for (int jj = 0; jj < 8; jj += 2) {
+                    const float4 f = *reinterpret_cast<const float4*>(fc + j0 + jj);
+                    const float4 a = *reinterpret_cast<const float4*>(bk + j0 + jj);
+                    float2 y0 = cmul_tc(make_float2(a.x, a.y), make_float2(f.x, f.y));
+                    float2 y1 = cmul_tc(make_float2(a.z, a.w), make_float2(f.z, f.w));
+                    if (!ok) y0 = y1 = make_float2(0.f, 0.f);
+                    tc::split(y0.x, hi[2 * jj], lo[2 * jj]);
+                    tc::split(y0.y, hi[2 * jj + 1], lo[2 * jj + 1]);
+                    tc::split(y1.x, hi[2 * jj + 2], lo[2 * jj + 2]);
+                    tc::split(y1.y, hi[2 * jj + 3], lo[2 * jj + 3]);
+                }
+                tc::tmem_st16(tmem + lb + uint32_t(2 * j0), hi);
+                tc::tmem_st16(tmem + lb + uint32_t(C::A_COLS + 2 * j0), lo);
+            }
+            tc::fence_before_sync();
+            tc::mbar_arrive(&f_empty);   // the staging tile may be refilled for the next job
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&a_full);
+        }
     } else if (warp == 5) {
-        // ---- MMA issuer ----
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_tf32(128, S0X_NC);
-            constexpr uint32_t LBO_A = (128 / 8) * 128, LBO_B = (S0X_NC / 8) * 128;
-            const uint64_t dAh = tc::desc_kmajor(tc::smem_u32(Ahi), LBO_A);
-            const uint64_t dAl = tc::desc_kmajor(tc::smem_u32(Alo), LBO_A);
-            const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(ring), LBO_B);
-            for (int nc = 0; nc < C::NCH; nc++) {
-                const int slot = nc & 1;
-                if (nc >= 2) tc::mbar_wait(&dempty[slot], ((nc >> 1) - 1) & 1);
-                tc::fence_after_sync();
+        // ---- MMA issuer (whole warp, one elected lane issues) ----
+        constexpr uint32_t idesc = tc::idesc_tf32(128, S0X_NC);
+        constexpr uint32_t LBO_B = (S0X_NC / 8) * 128;
+        const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(ring), LBO_B);
+        int64_t gc = 0;   // global chunk counter (accumulator slots alternate across jobs)
+        for (int64_t jl = 0; jl < njobs; jl++) {
+            tc::mbar_wait(&a_full, uint32_t(jl & 1));
+            tc::fence_after_sync();
+            for (int nc = 0; nc < C::NCH; nc++, gc++) {
+                const int slot = int(gc & 1);
+                if (gc >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gc >> 1) - 1) & 1);
+                const int64_t it0 = gc * C::KS;
+                const uint32_t d = tmem + uint32_t(C::D_OFF + slot * S0X_NC);
                 for (int ks = 0; ks < C::KS; ks++) {
-                    const int it = nc * C::KS + ks, st = it % C::NSTAGE;
-                    tc::mbar_wait(&full[st], (it / C::NSTAGE) & 1);
+                    const int st = int((it0 + ks) % C::NSTAGE);
+                    tc::mbar_wait(&full[st], uint32_t((it0 + ks) / C::NSTAGE) & 1);
                     tc::fence_after_sync();
-                    const int half = ks / (C::KS / 2), first = (ks % (C::KS / 2)) == 0;
-                    const uint32_t d = tmem + uint32_t(slot * 256 + half * 128);
-                    const uint64_t bh = tc::desc_add(dB0, st * C::STAGE), bl = tc::desc_add(bh, C::TILE);
-                    const uint32_t aoff = ks * (S0X_KC / 4) * LBO_A;
 #pragma unroll
                     for (int q = 0; q < 3; q++) {
                         const int pass = kPassOrder[q];
-                        const uint64_t a = tc::desc_add(pass == 1 ? dAl : dAh, aoff);
-                        const uint64_t bb = pass == 2 ? bl : bh;
+                        const uint64_t b = tc::desc_add(dB0, st * C::STAGE + (pass == 2 ? C::TILE : 0));
+                        const uint32_t a = tmem + uint32_t((pass == 1 ? C::A_COLS : 0) + ks * S0X_KC);
 #pragma unroll
                         for (int kk = 0; kk < S0X_KC / 8; kk++)
-                            tc::mma_tf32(d, tc::desc_add(a, kk * 2 * LBO_A), tc::desc_add(bb, kk * 2 * LBO_B), idesc,
-                                         (first && q == 0 && kk == 0) ? 0u : 1u);
+                            tc::mma_tf32_ts_warp(d, a + kk * 8, tc::desc_add(b, kk * 2 * LBO_B), idesc,
+                                                 (q | ks | kk) ? 1u : 0u);
                     }
-                    tc::commit(&empty[st]);
+                    tc::commit_warp(&empty[st]);   // the tile is free once its 3 passes are done
                 }
-                tc::commit(&dfull[slot]);
+                tc::commit_warp(&dfull[slot]);
+                __syncwarp();
             }
+            tc::commit_warp(&a_free);
+            __syncwarp();
         }
     } else {
-        // ---- epilogue (warps 0-3 and 6-9): TMEM lane quarter warp % 4 = vectors; warps 0-3 take the
-        // columns [0, 64) of each 128-column chunk, warps 6-9 the columns [64, 128).  Column n of chunk nc
-        // is the output (a, t, c') with a R + t = (128 nc + n) / 2.
-        const int q4 = warp & 3, vg = v0 + q4 * 32 + lane, cbase = warp < 4 ? 0 : 64;
-        for (int nc = 0; nc < C::NCH; nc++) {
-            const int slot = nc & 1;
-            tc::mbar_wait(&dfull[slot], (nc >> 1) & 1);
-            tc::fence_after_sync();
-            const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(slot * 256 + cbase);
+        // ---- epilogue (warps 6-13): lane quarter warp % 4 = vectors, column half (warp - 6) / 4 ----
+        const int q4 = warp & 3, cbase = ((warp - 6) >> 2) * 64;
+        int64_t gc = 0;
+        for (int64_t jl = 0; jl < njobs; jl++) {
+            const int64_t job = blockIdx.x + jl * gridDim.x;
+            const int64_t b = job / nvt;
+            const int vg = int(job % nvt) * 128 + q4 * 32 + lane;
+            for (int nc = 0; nc < C::NCH; nc++, gc++) {
+                const int slot = int(gc & 1);
+                tc::mbar_wait(&dfull[slot], uint32_t(gc >> 1) & 1);
+                tc::fence_after_sync();
+                const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * S0X_NC + cbase);
 #pragma unroll 1
-            for (int c0 = 0; c0 < 64; c0 += 32) {
-                float x[32], y[32];
-                tc::tmem_ld16(taddr + c0, x);
-                tc::tmem_ld16(taddr + c0 + 16, x + 16);
-                tc::tmem_ld16(taddr + 128 + c0, y);
-                tc::tmem_ld16(taddr + 128 + c0 + 16, y + 16);
-                tc::tmem_wait_ld();
-                if (c0 == 32) {
-                    tc::fence_before_sync();
-                    tc::mbar_arrive(&dempty[slot]);
-                }
-                if (vg < nv) {
+                for (int c0 = 0; c0 < 64; c0 += 32) {
+                    float x[32];
+                    tc::tmem_ld16(taddr + c0, x);
+                    tc::tmem_ld16(taddr + c0 + 16, x + 16);
+                    tc::tmem_wait_ld();
+                    if (c0 == 32) {
+                        tc::fence_before_sync();
+                        tc::mbar_arrive(&dempty[slot]);
+                    }
+                    if (vg < nv) {
 #pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const int q = (nc * S0X_NC + cbase + c0) / 2 + i;   // complex output index a R + t
-                        const int a = q / R, t = q - a * R;
-                        out[((int64_t(a) * nleaf + b) * R + t) * nv + vg] =
-                            make_float2(x[2 * i] + y[2 * i], x[2 * i + 1] + y[2 * i + 1]);
+                        for (int i = 0; i < 16; i++) {
+                            const int q = (nc * S0X_NC + cbase + c0) / 2 + i;   // complex output index a R + t
+                            const int a = q / R, t = q - a * R;
+                            out[((int64_t(a) * nleaf + b) * R + t) * nv + vg] = make_float2(x[2 * i], x[2 * i + 1]);
+                        }
                     }
                 }
             }
@@ -314,7 +369,7 @@ __global__ void __launch_bounds__(320, 1)
     __syncthreads();
     if (warp == 0) {
         tc::fence_after_sync();
-        tc::tmem_dealloc<512>(tmem);
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
     }
 }
 
@@ -327,8 +382,9 @@ static cudaError_t s0_tc_go(const Dims& d, const float2* F, int64_t ldf, const f
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
     const int nvt = (nv + 127) / 128;
-    const int64_t ctas = (d.N / N0) * nvt;
-    kern<<<unsigned(ctas), 320, C::SMEM, s>>>(F, ldf, ampb, V0x, out, d.LN, d.n_amp, nv, nvt);
+    const int64_t jobs = (d.N / N0) * nvt;
+    const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
+    kern<<<grid, 448, C::SMEM, s>>>(F, ldf, ampb, V0x, out, d.LN, d.n_amp, nv, nvt);
     return cudaGetLastError();
 }
 
@@ -352,8 +408,9 @@ cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const floa
 // CTA = one T_X leaf a x one tile of 128 vectors.  D[v][2j + c'] = sum over K = (b, t, c) of
 // A[v][(b, t, c)] B[(j, c')][(b, t, c)], A = delta_D[a n0 + b][t][v] split hi/lo, B = the expanded
 // U tiles of the leaf.  K streams in chunks of KP pairs:
-//   warp 12 (one thread)  bulk-copies the raw delta rows and the B tile of a chunk (2-deep rings),
-//   warps 0-3             split a raw chunk into one of two A stages,
+//   warp 12 (one thread)  bulk-copies the raw delta rows and the B tile of a chunk (3-deep rings),
+//   warps 0-3             split a raw chunk into one of two A stages in TMEM (lane = vector; the
+//                         MMAs read A from TMEM, so shared memory carries only B),
 //   warp 13 (one thread)  issues the 3 KC/8 MMAs of a chunk; every SEG chunks it switches between
 //                         two TMEM accumulators (short chains),
 //   warps 4-11            drain each finished segment into FP32 registers (lane quarter = vectors,
@@ -369,11 +426,15 @@ struct SLTC {
     static constexpr int NSEG = (NCH + SEG - 1) / SEG;
     static constexpr uint32_t RAW = uint32_t(KP) * R * 128 * 8;
     static constexpr uint32_t BT = uint32_t(NB) * KC * 4;   // one of hi / lo
-    static constexpr uint32_t AT = 128u * KC * 4;
-    static constexpr uint32_t OFF_B = 2 * RAW, OFF_A = OFF_B + 4 * BT, OFF_AS = OFF_A + 4 * AT;
+    static constexpr int NR = 3;                            // ring depth (raw rows and B tiles)
+    static constexpr uint32_t OFF_B = NR * RAW, OFF_AS = OFF_B + 2 * NR * BT;
     static constexpr uint32_t GS_STRIDE = N0 + 1;
     static constexpr size_t SMEM = size_t(OFF_AS) + size_t(NA) * N0 * 8;
+    // TMEM: two A stages (hi KC columns, then lo KC columns) and two accumulators of NB columns
+    static constexpr int A_COLS = 2 * KC, D_OFF = 2 * A_COLS;
+    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * NB>();
     static_assert(KC % 8 == 0, "K chunk must be whole MMA K steps");
+    static_assert(D_OFF + 2 * NB <= 512, "TMEM budget");
     static_assert(SMEM <= 232448 - 512, "shared memory budget");
     static_assert(size_t(128 / NA) * GS_STRIDE * 8 <= OFF_AS, "G staging fits in the freed rings");
 };
@@ -387,13 +448,12 @@ __global__ void __launch_bounds__(448, 1)
     extern __shared__ __align__(128) uint8_t sm_sltc[];
     auto raw = [&](int e) { return sm_sltc + e * C::RAW; };
     auto opB = [&](int e, int lo) { return sm_sltc + C::OFF_B + (2 * e + lo) * C::BT; };
-    auto opA = [&](int s, int lo) { return sm_sltc + C::OFF_A + (2 * s + lo) * C::AT; };
     float2* As = reinterpret_cast<float2*>(sm_sltc + C::OFF_AS);   // [NA][N0] a_k(x)
     float2* Gs = reinterpret_cast<float2*>(sm_sltc);               // epilogue: [128/NA][GS_STRIDE]
-    __shared__ uint64_t raw_full[2], raw_empty[2], b_full[2], b_empty[2], a_full[2], a_empty[2], dfull[2],
-        dempty[2];
+    __shared__ uint64_t raw_full[C::NR], raw_empty[C::NR], b_full[C::NR], b_empty[C::NR], a_full[2], a_empty[2],
+        dfull[2], dempty[2];
     __shared__ uint32_t tmem_base;
-    constexpr int TMEM_COLS = tmem_cols_pow2<2 * C::NB>();
+    constexpr int TMEM_COLS = C::TMEM_COLS;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t N = int64_t(1) << LN;
@@ -404,11 +464,13 @@ __global__ void __launch_bounds__(448, 1)
 
     if (warp == 0) tc::tmem_alloc<TMEM_COLS>(&tmem_base);
     if (tid == 0) {
-        for (int i = 0; i < 2; i++) {
+        for (int i = 0; i < C::NR; i++) {
             tc::mbar_init(&raw_full[i], 1);
             tc::mbar_init(&raw_empty[i], 128);
             tc::mbar_init(&b_full[i], 1);
             tc::mbar_init(&b_empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
             tc::mbar_init(&a_full[i], 128);
             tc::mbar_init(&a_empty[i], 1);
             tc::mbar_init(&dfull[i], 1);
@@ -427,7 +489,7 @@ __global__ void __launch_bounds__(448, 1)
         if (lane == 0) {
             const uint32_t row_bytes = uint32_t(vw) * 8;
             for (int ch = 0; ch < C::NCH; ch++) {
-                const int e = ch & 1, use = ch >> 1;
+                const int e = ch % C::NR, use = ch / C::NR;
                 if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
                 tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
                 tc::bulk_g2s(opB(e, 0), wsrc + int64_t(ch) * 2 * (C::BT / 4), 2 * C::BT, &b_full[e]);
@@ -440,59 +502,57 @@ __global__ void __launch_bounds__(448, 1)
             }
         }
     } else if (warp == 13) {
-        // ---- MMA issuer ----
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
-            constexpr uint32_t LBO_A = (128 / 8) * 128, LBO_B = (C::NB / 8) * 128;
-            const uint64_t dA0 = tc::desc_kmajor(tc::smem_u32(opA(0, 0)), LBO_A);
-            const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(opB(0, 0)), LBO_B);
-            for (int ch = 0; ch < C::NCH; ch++) {
-                const int e = ch & 1, seg = ch / C::SEG, slot = seg & 1, first = (ch % C::SEG) == 0;
-                if (first && seg >= 2) tc::mbar_wait(&dempty[slot], ((seg >> 1) - 1) & 1);
-                tc::mbar_wait(&a_full[e], (ch >> 1) & 1);
-                tc::mbar_wait(&b_full[e], (ch >> 1) & 1);
-                tc::fence_after_sync();
-                const uint32_t d = tmem + uint32_t(slot * C::NB);
+        // ---- MMA issuer (whole warp, one elected lane issues) ----
+        constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
+        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
+        const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(opB(0, 0)), LBO_B);
+        for (int ch = 0; ch < C::NCH; ch++) {
+            const int e = ch % C::NR, sa = ch & 1, seg = ch / C::SEG, slot = seg & 1, first = (ch % C::SEG) == 0;
+            if (first && seg >= 2) tc::mbar_wait(&dempty[slot], ((seg >> 1) - 1) & 1);
+            tc::mbar_wait(&a_full[sa], (ch >> 1) & 1);
+            tc::mbar_wait(&b_full[e], (ch / C::NR) & 1);
+            tc::fence_after_sync();
+            const uint32_t d = tmem + uint32_t(C::D_OFF + slot * C::NB);
 #pragma unroll
-                for (int q = 0; q < 3; q++) {
-                    const int pass = kPassOrder[q];
-                    const uint64_t aa = tc::desc_add(dA0, (2 * e + (pass == 1)) * C::AT);
-                    const uint64_t bb = tc::desc_add(dB0, (2 * e + (pass == 2)) * C::BT);
+            for (int q = 0; q < 3; q++) {
+                const int pass = kPassOrder[q];
+                const uint32_t aa = tmem + uint32_t(sa * C::A_COLS + (pass == 1 ? C::KC : 0));
+                const uint64_t bb = tc::desc_add(dB0, (2 * e + (pass == 2)) * C::BT);
 #pragma unroll
-                    for (int ks = 0; ks < C::KC / 8; ks++)
-                        tc::mma_tf32(d, tc::desc_add(aa, ks * 2 * LBO_A), tc::desc_add(bb, ks * 2 * LBO_B), idesc,
-                                     (first && q == 0 && ks == 0) ? 0u : 1u);
-                }
-                tc::commit(&a_empty[e]);
-                tc::commit(&b_empty[e]);
-                if ((ch % C::SEG) == C::SEG - 1 || ch == C::NCH - 1) tc::commit(&dfull[slot]);
+                for (int ks = 0; ks < C::KC / 8; ks++)
+                    tc::mma_tf32_ts_warp(d, aa + ks * 8, tc::desc_add(bb, ks * 2 * LBO_B), idesc,
+                                         (first && q == 0 && ks == 0) ? 0u : 1u);
             }
+            tc::commit_warp(&a_empty[sa]);
+            tc::commit_warp(&b_empty[e]);
+            if ((ch % C::SEG) == C::SEG - 1 || ch == C::NCH - 1) tc::commit_warp(&dfull[slot]);
+            __syncwarp();
         }
     } else if (warp < 4) {
-        // ---- split: raw delta rows -> A stage (hi / lo) ----
+        // ---- split: raw delta rows -> A stage (hi / lo) in TMEM; thread = vector (its lane) ----
+        const int v = tid;
+        const uint32_t lb = uint32_t(warp * 32) << 16;
         for (int ch = 0; ch < C::NCH; ch++) {
-            const int e = ch & 1, use = ch >> 1;
-            tc::mbar_wait(&raw_full[e], use & 1);
-            if (use > 0) tc::mbar_wait(&a_empty[e], (use - 1) & 1);
+            const int e = ch % C::NR, sa = ch & 1;
+            tc::mbar_wait(&raw_full[e], (ch / C::NR) & 1);
+            if (ch >= 2) tc::mbar_wait(&a_empty[sa], ((ch >> 1) - 1) & 1);
+            tc::fence_after_sync();
             const float2* rd = reinterpret_cast<const float2*>(raw(e));   // [KP R][128]
-            uint8_t *ah = opA(e, 0), *al = opA(e, 1);
-            // A[v][(pl, t, c)]: task (v, pl, tt) -> complex t = 2tt, 2tt+1 -> 16 bytes
-            for (int idx = tid; idx < 128 * KP * (R / 2); idx += 128) {
-                const int v = idx & 127, q = idx >> 7;   // q = pl R/2 + tt
-                const int pl = q / (R / 2), tt = q - pl * (R / 2);
-                const float2 x0 = rd[(pl * R + 2 * tt) * 128 + v], x1 = rd[(pl * R + 2 * tt + 1) * 128 + v];
-                float4 h, l;
-                tc::split(x0.x, h.x, l.x);
-                tc::split(x0.y, h.y, l.y);
-                tc::split(x1.x, h.z, l.z);
-                tc::split(x1.y, h.w, l.w);
-                const uint32_t off = tc::kmaj_off(v, pl * 2 * R + 4 * tt, 128);
-                st_f4(ah, off, h);
-                st_f4(al, off, l);
+            float hi[C::KC], lo[C::KC];   // column (pl, t, c) = pl 2R + 2t + c
+#pragma unroll
+            for (int row = 0; row < KP * R; row++) {
+                const float2 x = rd[row * 128 + v];
+                tc::split(x.x, hi[2 * row], lo[2 * row]);
+                tc::split(x.y, hi[2 * row + 1], lo[2 * row + 1]);
             }
-            tc::fence_proxy_async();
-            tc::mbar_arrive(&raw_empty[e]);
-            tc::mbar_arrive(&a_full[e]);
+            tc::fence_before_sync();
+            tc::mbar_arrive(&raw_empty[e]);   // the raw rows are in registers now
+            const uint32_t ta = tmem + lb + uint32_t(sa * C::A_COLS);
+            tc::tmem_st_cols<C::KC>(ta, hi);
+            tc::tmem_st_cols<C::KC>(ta + C::KC, lo);
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&a_full[sa]);
         }
     } else {
         // ---- drain (warps 4-11): lane quarter warp % 4 = vectors, column half (warp - 4) / 4 ----
@@ -505,7 +565,7 @@ __global__ void __launch_bounds__(448, 1)
             const int slot = seg & 1;
             tc::mbar_wait(&dfull[slot], (seg >> 1) & 1);
             tc::fence_after_sync();
-            const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(slot * C::NB + half * HC);
+            const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * C::NB + half * HC);
 #pragma unroll
             for (int c0 = 0; c0 < HC; c0 += 32) {
                 float x[32];
@@ -880,17 +940,6 @@ __global__ void __launch_bounds__(384, 1)
         tc::fence_after_sync();
         tc::tmem_dealloc<C::TMEM_COLS>(tmem);
     }
-}
-
-static int sm_count()
-{
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-    }
-    return n;
 }
 
 template <int R>
