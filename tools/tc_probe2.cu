@@ -265,7 +265,7 @@ __global__ void contention_kernel(int iters, long long* cycles, float2* gbuf)
             } else if constexpr (MODE == 4) {
                 const float4* sp = reinterpret_cast<const float4*>(smem);
                 for (int r = 0; r < 16; r++) {
-                    const float4 q = sp[(r * 256 + threadIdx.x) % 1024];
+                    const float4 q = sp[(r * 256 + threadIdx.x) % 352];
                     acc += q.x + q.w;
                 }
             } else {
