@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(448, 1)
                     const int st = int(it % C::NSTAGE);
                     if (it >= C::NSTAGE) tc::mbar_wait(&empty[st], uint32_t(it / C::NSTAGE - 1) & 1);
                     const int64_t jl = it / (C::NCH * C::KS);   // local job
-                    const int64_t b = (blockIdx.x + jl * gridDim.x) / nvt;
+                    const int64_t b = unsigned(blockIdx.x + jl * gridDim.x) / unsigned(nvt);
                     const int64_t w = it % (C::NCH * C::KS);
                     tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
                     tc::bulk_g2s(ring + st * C::STAGE, V0x + (b * (C::NCH * C::KS) + w) * 2 * S0X_TILE_FLOATS,
@@ -243,9 +243,9 @@ __global__ void __launch_bounds__(448, 1)
                 }
             };
             for (int64_t jl = 0; jl < njobs; jl++) {
-                const int64_t job = blockIdx.x + jl * gridDim.x;
-                const int64_t b = job / nvt;
-                const int v0 = int(job % nvt) * 128, vw = min(128, nv - v0);
+                const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
+                const int64_t b = job / unsigned(nvt);
+                const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
                 const int c0 = v0 / n_amp, cw = (vw + n_amp - 1) / n_amp;
                 if (jl > 0) tc::mbar_wait(&f_empty, uint32_t(jl - 1) & 1);
                 tc::mbar_arrive_expect_tx(&f_full, uint32_t(cw) * N0 * 8 + uint32_t(n_amp) * N0 * 8);
@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(448, 1)
         const int v = tid;
         const uint32_t lb = uint32_t(warp * 32) << 16;
         for (int64_t jl = 0; jl < njobs; jl++) {
-            const int64_t job = blockIdx.x + jl * gridDim.x;
-            const int v0 = int(job % nvt) * 128, vg = v0 + v;
+            const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
+            const int v0 = int(job % unsigned(nvt)) * 128, vg = v0 + v;
             const int c0 = v0 / n_amp;
             tc::mbar_wait(&f_full, uint32_t(jl & 1));
             if (jl > 0) tc::mbar_wait(&a_free, uint32_t(jl - 1) & 1);
@@ -335,9 +335,9 @@ __global__ void __launch_bounds__(448, 1)
         const int q4 = warp & 3, cbase = ((warp - 6) >> 2) * 64;
         int64_t gc = 0;
         for (int64_t jl = 0; jl < njobs; jl++) {
-            const int64_t job = blockIdx.x + jl * gridDim.x;
-            const int64_t b = job / nvt;
-            const int vg = int(job % nvt) * 128 + q4 * 32 + lane;
+            const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
+            const int64_t b = job / unsigned(nvt);
+            const int vg = int(job % unsigned(nvt)) * 128 + q4 * 32 + lane;
             for (int nc = 0; nc < C::NCH; nc++, gc++) {
                 const int slot = int(gc & 1);
                 tc::mbar_wait(&dfull[slot], uint32_t(gc >> 1) & 1);
@@ -745,11 +745,11 @@ __global__ void __launch_bounds__(384, 1)
         // ---- split: raw rows -> A buffer (TMEM), lane = vector ----
         const int v = tid;
         const uint32_t lb = uint32_t(warp * 32) << 16;
-        for (int64_t J = 0; J < njobs; J++) {
+        for (int J = 0; J < int(njobs); J++) {
             const int e = int(J & 1);
             tc::mbar_wait(&raw_full[e], uint32_t(J >> 1) & 1);
             const int slot = int(J % C::NABUF);
-            const int64_t use = J / C::NABUF;
+            const int use = J / C::NABUF;
             if (use > 0) tc::mbar_wait(&a_free[slot], uint32_t(use - 1) & 1);
             tc::fence_after_sync();
             if (tid == 0) btrace(J, 0);
@@ -777,10 +777,10 @@ __global__ void __launch_bounds__(384, 1)
         // ---- epilogue: level-1 drain + re-split, level-2 drain + store ----
         const int v = tid - 128;
         const uint32_t lb = uint32_t((warp - 4) * 32) << 16;
-        for (int64_t J = 0; J < njobs; J++) {
-            const int64_t it = J / nvt;
-            const int vt = int(J - it * nvt);
-            const int64_t g = blockIdx.x + it * gridDim.x;
+        for (int J = 0; J < int(njobs); J++) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
             const int slot = int(J % C::NABUF);
             const uint32_t ph = uint32_t(J & 1);
             tc::mbar_wait(&d1_full, ph);
@@ -834,10 +834,10 @@ __global__ void __launch_bounds__(384, 1)
     } else if (warp == 8) {
         // ---- loader ----
         if (lane == 0) {
-            for (int64_t J = 0; J < njobs; J++) {
-                const int64_t it = J / nvt;
-                const int vt = int(J - it * nvt);
-                const int64_t g = blockIdx.x + it * gridDim.x;
+            for (int J = 0; J < int(njobs); J++) {
+                const int it = int(unsigned(J) / unsigned(nvt));
+                const int vt = J - it * nvt;
+                const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
                 const int e = int(J & 1);
                 if (J >= 2) tc::mbar_wait(&raw_empty[e], uint32_t((J >> 1) - 1) & 1);
                 btrace(J, 8);
@@ -855,9 +855,9 @@ __global__ void __launch_bounds__(384, 1)
         constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
         constexpr uint32_t LBO_B = (C::NB / 8) * 128;
         const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_band + C::OFF_W), LBO_B);
-        for (int64_t J = 0; J < njobs; J++) {
-            const int64_t it = J / nvt;
-            const int vt = int(J - it * nvt);
+        for (int J = 0; J < int(njobs); J++) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
             const int wb = int(it % C::NWBUF), slot = int(J % C::NABUF);
             if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
 #pragma unroll 1
@@ -892,8 +892,8 @@ __global__ void __launch_bounds__(384, 1)
     } else {
         // ---- weights (warps 10-11): compact r x 2r blocks -> embedded hi/lo B tiles, one group ahead ----
         const int wt = tid - 320;
-        for (int64_t it = 0; it < nit; it++) {
-            const int64_t g = blockIdx.x + it * gridDim.x;
+        for (int it = 0; it < int(nit); it++) {
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
             const int wb = int(it % C::NWBUF);
             if (it >= C::NWBUF) tc::mbar_wait(&w_free[wb], uint32_t(it / C::NWBUF - 1) & 1);
             const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
