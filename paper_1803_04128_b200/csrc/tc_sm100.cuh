@@ -221,28 +221,35 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar)
 {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
 }
-// Waits for the phase with the given parity.  try_wait with a suspend-time hint parks the warp in
-// hardware until the phase completes (or the hint elapses), so waiting warps take no issue slots from
-// the MMA / epilogue warps.  Watchdog: a wait that has not completed after ~4e9 cycles (~2 s) traps
-// (a reported kernel fault instead of a hung GPU).
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+// Waits for the phase with the given parity: a try_wait spin (the hardware try_wait already blocks
+// for a short system-defined time per probe).  With BF_TC_WAIT_HINT the probe carries a suspend-time hint
+// instead (compiles to NANOSLEEP.SYNCS between probes; measured slower wake-ups on the critical path).
+// Watchdog: a wait that has not completed after ~4e9 cycles (~2 s) traps (a reported kernel fault instead
+// of a hung GPU).
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity)
 {
     uint32_t done = 0;
+#ifdef BF_TC_WAIT_HINT
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680)
         : "memory");
-    if (done) return;
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+#endif
+    return done != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    if (mbar_try_wait(bar, parity)) return;
     const long long t0 = clock64();
-    do {
+    while (!mbar_try_wait(bar, parity))
         if (clock64() - t0 > 4000000000LL) __trap();
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680)
-            : "memory");
-    } while (!done);
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
 {
