@@ -146,6 +146,7 @@ struct bf_plan_s {
     // end-to-end staging (lazily allocated by bf_apply_host)
     float2* dF = nullptr;
     float2* dG = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the pipelined bf_apply_host
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
     // timing
     bool timing = false;
@@ -266,6 +267,8 @@ void free_plan(bf_plan_s* p)
     }
     cudaFree(p->dF);
     cudaFree(p->dG);
+    if (p->h2d) cudaStreamDestroy(p->h2d);
+    if (p->d2h) cudaStreamDestroy(p->d2h);
     if (p->comm) nccl().CommDestroy(p->comm);
     delete p;
 }
@@ -783,18 +786,57 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
     bf_status_t st;
     if (!p->dF && ((st = dalloc(&p->dF, rows * chunk, "e2e F")) || (st = dalloc(&p->dG, rows * chunk, "e2e G"))))
         return st;
+    cudaError_t e;
+    if (!p->h2d && ((e = cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+                    (e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking)) != cudaSuccess))
+        return cuda_fail(e, "copy streams");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    for (int64_t c0 = 0; c0 < nrhs; c0 += chunk) {
-        const int64_t nc = std::min(chunk, nrhs - c0);
-        const size_t bytes = size_t(rows * nc) * sizeof(float2);
-        cudaError_t e = cudaMemcpyAsync(p->dF, F_host + c0 * rows, bytes, cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D");
-        if ((st = apply_impl(p, p->dF, rows, p->dG, rows, nc, p->sh[0].ws, s)) != BF_OK) return st;
-        e = cudaMemcpyAsync(G_host + c0 * rows, p->dG, bytes, cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) return cuda_fail(e, "D2H");
+    // Pipeline over pieces of half a chunk (ping-pong halves of the staging buffers): the host->device
+    // copy of piece i+1 and the device->host copy of piece i-1 run on their own streams while piece i is
+    // applied on `stream` (PCIe is full duplex).  Hazards are ordered with events: a staging half is
+    // refilled only after the apply that read it, and rewritten only after the copy-out that read it.
+    const int64_t piece = chunk >= 2 ? (chunk + 1) / 2 : chunk;
+    const int64_t npieces = (nrhs + piece - 1) / piece;
+    std::vector<cudaEvent_t> ev(3 * size_t(npieces), nullptr);   // [h2d done, apply done, d2h done] per piece
+    for (auto& x : ev)
+        if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) break;
+    auto cleanup = [&]() {
+        for (auto& x : ev)
+            if (x) cudaEventDestroy(x);
+    };
+    if (e != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e, "events");
     }
-    cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_fail(e, "bf_apply_host");
+    st = BF_OK;
+    for (int64_t i = 0; i < npieces && st == BF_OK; i++) {
+        const int64_t c0 = i * piece, nc = std::min(piece, nrhs - c0), buf = i & 1;
+        const size_t bytes = size_t(rows * nc) * sizeof(float2);
+        float2* dF = p->dF + buf * piece * rows;
+        float2* dG = p->dG + buf * piece * rows;
+        cudaEvent_t* E = &ev[3 * size_t(i)];
+        if (i >= 2) cudaStreamWaitEvent(p->h2d, ev[3 * size_t(i - 2) + 1], 0);
+        if ((e = cudaMemcpyAsync(dF, F_host + c0 * rows, bytes, cudaMemcpyHostToDevice, p->h2d)) != cudaSuccess) {
+            st = cuda_fail(e, "H2D");
+            break;
+        }
+        cudaEventRecord(E[0], p->h2d);
+        cudaStreamWaitEvent(s, E[0], 0);
+        if (i >= 2) cudaStreamWaitEvent(s, ev[3 * size_t(i - 2) + 2], 0);
+        if ((st = apply_impl(p, dF, rows, dG, rows, nc, p->sh[0].ws, s)) != BF_OK) break;
+        cudaEventRecord(E[1], s);
+        cudaStreamWaitEvent(p->d2h, E[1], 0);
+        if ((e = cudaMemcpyAsync(G_host + c0 * rows, dG, bytes, cudaMemcpyDeviceToHost, p->d2h)) != cudaSuccess) {
+            st = cuda_fail(e, "D2H");
+            break;
+        }
+        cudaEventRecord(E[2], p->d2h);
+    }
+    cudaError_t e1 = cudaStreamSynchronize(p->h2d), e2 = cudaStreamSynchronize(p->d2h), e3 = cudaStreamSynchronize(s);
+    cleanup();
+    if (st != BF_OK) return st;
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+        return cuda_fail(e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3, "bf_apply_host");
     return BF_OK;
 }
 

@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(384, 1)
         return sm_band + C::OFF_W + wb * C::WSET + ((m * C::U + u) * 2 + lo) * C::WT;
     };
     __shared__ uint64_t raw_full[2], raw_empty[2], a1_ready[2], a2_ready[2], a_free[2], w_full[2], w_free[2];
-    __shared__ uint64_t d1_full[2], d1_free, d2_full, d2_free;   // d1_full per level-1 unit
+    __shared__ uint64_t d1_full, d1_free, d2_full, d2_free;
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -721,8 +721,7 @@ __global__ void __launch_bounds__(384, 1)
             tc::mbar_init(&w_full[i], 64);
             tc::mbar_init(&w_free[i], 1);
         }
-        tc::mbar_init(&d1_full[0], 1);
-        tc::mbar_init(&d1_full[1], 1);
+        tc::mbar_init(&d1_full, 1);
         tc::mbar_init(&d1_free, 128);
         tc::mbar_init(&d2_full, 1);
         tc::mbar_init(&d2_free, 128);
@@ -784,12 +783,13 @@ __global__ void __launch_bounds__(384, 1)
             const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
             const int slot = int(J % C::NABUF);
             const uint32_t ph = uint32_t(J & 1);
+            // every level-1 MMA must be complete before the in-place re-split (an output slot of unit 0 is an
+            // input slot of unit 1)
+            tc::mbar_wait(&d1_full, ph);
+            tc::fence_after_sync();
             if (v == 0) btrace(J, 3);
 #pragma unroll 1
             for (int u = 0; u < C::U; u++) {
-                // unit 0 is drained while the tensor pipe still runs unit 1's level-1 MMAs
-                tc::mbar_wait(&d1_full[u], ph);
-                tc::fence_after_sync();
                 float d[C::NU];
                 tc::tmem_ld_cols<C::NU>(tmem + lb + uint32_t(C::D1_OFF + u * C::NB), d);
                 tc::tmem_wait_ld();
@@ -883,10 +883,9 @@ __global__ void __launch_bounds__(384, 1)
                             tc::mma_tf32_ts_warp(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc,
                                                  (q | ks) ? 1u : 0u);
                     }
-                    if (m == 0) tc::commit_warp(&d1_full[u]);
                 }
                 if (lane == 0) btrace(J, m == 0 ? 2 : 5);
-                if (m == 1) tc::commit_warp(&d2_full);
+                tc::commit_warp(m == 0 ? &d1_full : &d2_full);
             }
             tc::commit_warp(&a_free[slot]);
             if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);

@@ -122,3 +122,18 @@ def test_tc_mutation_detected():
         G = _apply(p, F)
         p.destroy()
         assert np.all(oracle.rel_l2(G[:, :2].astype(np.complex128), R, axis=0) > 1e-4)
+
+
+def test_tc_apply_host_pipelined():
+    """bf_apply_host pipelines half-chunk pieces over copy streams; with tensor-core pieces the result
+    equals the device-buffer apply of the same plan bitwise (each vector's arithmetic is independent of
+    the other vectors of its tile)."""
+    LN, l0, r, nrhs = 12, 6, 10, 96
+    F = W.rhs(1 << LN, nrhs, 21)
+    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=64)   # pieces of 32
+    ref = _apply(plan, F)
+    Fh = torch.from_numpy(np.ascontiguousarray(F.T)).pin_memory()
+    Gh = torch.empty_like(Fh).pin_memory()
+    plan.apply_host(Fh, Gh, nrhs)
+    plan.destroy()
+    assert np.array_equal(np.asfortranarray(Gh.numpy().T), ref)
