@@ -178,6 +178,8 @@ def main():
                     help="split ONE batch by index over the ranks (NCCL all-to-all at level h; cfg5's mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--band-pipelines", type=int, default=None, choices=[1, 2],
+                    help="tensor-core band variant (tuning; default: the library's)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -221,6 +223,8 @@ def main():
         # this rank's RHS: columns [rank*nrhs, (rank+1)*nrhs) of the seeded global batch (weak scaling)
         F = W.rhs(w.n, w.nrhs, w.seed + 1000 * rank)
     t_build = time.perf_counter() - t0
+    if args.band_pipelines:
+        plan.set_option(bf.BF_OPT_BAND_PIPELINES, args.band_pipelines)
     info = plan.info()
     Fd = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()
     Gd = torch.empty_like(Fd)

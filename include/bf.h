@@ -187,6 +187,12 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        0: every stage runs the FP32 FFMA (SIMT) kernels.
  * Returns BF_ERR_INVALID_ARG for an unknown option or value. */
 #define BF_OPT_TENSOR_CORES 1
+/*   BF_OPT_BAND_PIPELINES 1 (default): the tensor-core band kernel runs one job at a time per SM;
+ *                        2: jobs alternate between two TMEM pipelines where TMEM allows (r <= 10; measured
+ *                        slower at cfg4).  Process-wide tuning knob. */
+#define BF_OPT_BAND_PIPELINES 2
+/*   BF_OPT_BAND_TRACE_J0 (diagnostic): first job recorded by bf_debug_band_trace (default 0). */
+#define BF_OPT_BAND_TRACE_J0 3
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band

@@ -904,6 +904,15 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
         p->tensor_cores = value != 0;
         return BF_OK;
     }
+    if (option == BF_OPT_BAND_TRACE_J0) {
+        bfk::band_trace_window(int(value));
+        return BF_OK;
+    }
+    if (option == BF_OPT_BAND_PIPELINES) {
+        if (value != 1 && value != 2) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_PIPELINES takes 1 or 2");
+        bfk::band_set_single_pipeline(value == 1);
+        return BF_OK;
+    }
     return fail(BF_ERR_INVALID_ARG, "unknown plan option");
 }
 

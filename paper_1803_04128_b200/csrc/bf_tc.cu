@@ -639,12 +639,28 @@ cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const
     return cudaErrorInvalidValue;
 }
 
+// Band variant switch (BF_OPT_BAND_PIPELINES): 1 = single TMEM pipeline (default), 0 = two pipelines where
+// they fit.  Measured at cfg4 (tools/band_trace.py, profiles/r1_band_variants.txt): the two-pipeline kernel
+// halves the per-job cycle count on some SMs, but its concurrent tcgen05.st/ld traffic (two epilogues plus
+// the split) slows the tensor pipe on others, and the launch is 1.4x slower overall.
+static int g_band_single_pipeline = 1;
+void band_set_single_pipeline(int v) { g_band_single_pipeline = v; }
+
 // ---- timeline trace of the band kernel (diagnostic; CTA 0, first BT_JOBS jobs, SM clock) ----
 constexpr int BT_JOBS = 64, BT_EV = 12;
 __device__ long long g_band_trace[BT_JOBS * BT_EV];
+__device__ int g_band_trace_j0 = 0;    // first traced job (BF_OPT_BAND_TRACE_J0: job + 65536 * cta)
+__device__ int g_band_trace_cta = 0;   // traced CTA
 __device__ __forceinline__ void btrace(int64_t J, int ev)
 {
-    if (blockIdx.x == 0 && J < BT_JOBS) g_band_trace[J * BT_EV + ev] = clock64();
+    const int64_t j = J - g_band_trace_j0;
+    if (int(blockIdx.x) == g_band_trace_cta && j >= 0 && j < BT_JOBS) g_band_trace[j * BT_EV + ev] = clock64();
+}
+void band_trace_window(int v)
+{
+    const int j0 = v & 65535, cta = v >> 16;
+    cudaMemcpyToSymbol(g_band_trace_j0, &j0, sizeof(int));
+    cudaMemcpyToSymbol(g_band_trace_cta, &cta, sizeof(int));
 }
 
 // =============================================================================================
@@ -890,6 +906,7 @@ __global__ void __launch_bounds__(384, 1)
             tc::commit_warp(&a_free[slot]);
             if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
             __syncwarp();
+            if (lane == 0) btrace(J, 11);
         }
     } else {
         // ---- weights (warps 10-11): compact r x 2r blocks -> embedded hi/lo B tiles, one group ahead ----
@@ -944,16 +961,308 @@ __global__ void __launch_bounds__(384, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Two-pipeline variant of the band (r <= 10; selectable with BF_OPT_BAND_PIPELINES = 2, not the default): jobs alternate between two TMEM pipelines (A buffer +
+// one accumulator region shared by both levels), so while one job's level-1 accumulator is drained and
+// re-split (E1) the tensor pipe runs the other job's MMAs.  Warp roles: 0-3 split (all jobs, in order),
+// 4-7 / 8-11 epilogue of pipeline 0 / 1 (E1 and E2 of its jobs), 12 loader, 13 MMA, 14-15 weights.
+// MMA order: L1(J), L1(J+1), L2(J), L2(J+1), L1(J+2), ...
+// ---------------------------------------------------------------------------------------------
+template <int R>
+struct Band2P {
+    using B = BandTC<R>;
+    static constexpr int PCOLS = B::ACOLS + B::DCOLS;   // one pipeline: A (hi, lo) + accumulators
+    static constexpr bool FITS = 2 * PCOLS <= 512;
+    static constexpr int TMEM_COLS = 512;
+};
+
+template <int R>
+__global__ void __launch_bounds__(512, 1)
+    band_tc2p_kernel(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ W1,
+                     const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg)
+{
+    using C = BandTC<R>;
+    using Q = Band2P<R>;
+    extern __shared__ __align__(128) uint8_t sm_band[];
+    auto raw = [&](int e) { return sm_band + e * C::RAW; };
+    auto wtile = [&](int wb, int m, int u, int lo) {
+        return sm_band + C::OFF_W + wb * C::WSET + ((m * C::U + u) * 2 + lo) * C::WT;
+    };
+    __shared__ uint64_t raw_full[2], raw_empty[2], w_full[2], w_free[2];
+    __shared__ uint64_t a1_ready[2], a2_ready[2], a_free[2], d1_full[2], d2_full[2], d2_free[2];   // per pipeline
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t N = int64_t(1) << LN;
+    const int lin = l_first - 1, shg = LN - lin - 2;
+    const int64_t ngroups = N >> 2;
+    const int nvt = (nv + 127) / 128;
+    const int nit = int((ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const int njobs = nit * nvt;
+
+    if (warp == 0) tc::tmem_alloc<Q::TMEM_COLS>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&raw_full[i], 1);
+            tc::mbar_init(&raw_empty[i], 128);
+            tc::mbar_init(&w_full[i], 64);
+            tc::mbar_init(&w_free[i], 1);
+            tc::mbar_init(&a1_ready[i], 128);
+            tc::mbar_init(&a2_ready[i], 128);
+            tc::mbar_init(&a_free[i], 1);
+            tc::mbar_init(&d1_full[i], 1);
+            tc::mbar_init(&d2_full[i], 1);
+            tc::mbar_init(&d2_free[i], 128);
+        }
+        tc::mbar_fence_init();
+    }
+    if constexpr (C::NB > C::NU) {   // zero the pad rows of every B tile (never written afterwards)
+        constexpr int PADQ = (C::NB - C::NU) * C::KU / 4;
+        for (int idx = tid; idx < C::NWBUF * 2 * C::U * 2 * PADQ; idx += blockDim.x) {
+            const int tile = idx / PADQ, o = idx % PADQ;
+            const int row = C::NU + o % (C::NB - C::NU), k = 4 * (o / (C::NB - C::NU));
+            st_f4(sm_band + C::OFF_W + tile * C::WT, tc::kmaj_off(row, k, C::NB), make_float4(0, 0, 0, 0));
+        }
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base;
+    auto abuf = [&](int p) { return tmem + uint32_t(p * Q::PCOLS); };               // hi at +0, lo at +P SC
+    auto dbuf = [&](int p) { return tmem + uint32_t(p * Q::PCOLS + C::ACOLS); };    // unit u at +u NB
+
+    if (warp < 4) {
+        // ---- split: raw rows -> the job's pipeline A buffer (TMEM), lane = vector ----
+        const int v = tid;
+        const uint32_t lb = uint32_t(warp * 32) << 16;
+        for (int J = 0; J < njobs; J++) {
+            const int e = J & 1, p = J & 1, use = J >> 1;
+            tc::mbar_wait(&raw_full[e], uint32_t(use & 1));
+            if (use > 0) tc::mbar_wait(&a_free[p], uint32_t(use - 1) & 1);
+            tc::fence_after_sync();
+            if (tid == 0) btrace(J, 0);
+            const float2* rd = reinterpret_cast<const float2*>(raw(e));
+#pragma unroll 1
+            for (int s = 0; s < C::P; s++) {
+                float hi[C::SC], lo[C::SC];
+#pragma unroll
+                for (int t = 0; t < R; t++) {
+                    const float2 x = rd[(s * R + t) * 128 + v];
+                    tc::split(x.x, hi[2 * t], lo[2 * t]);
+                    tc::split(x.y, hi[2 * t + 1], lo[2 * t + 1]);
+                }
+                const uint32_t ta = abuf(p) + lb + uint32_t(s * C::SC);
+                tc::tmem_st_cols<C::SC>(ta, hi);
+                tc::tmem_st_cols<C::SC>(ta + C::P * C::SC, lo);
+            }
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            if (tid == 0) btrace(J, 1);
+            tc::mbar_arrive(&raw_empty[e]);
+            tc::mbar_arrive(&a1_ready[p]);
+        }
+    } else if (warp < 12) {
+        // ---- epilogue of pipeline p: level-1 drain + re-split, level-2 drain + store ----
+        const int p = (warp - 4) >> 2;
+        const int v = ((warp - 4) & 3) * 32 + lane;
+        const uint32_t lb = uint32_t(((warp - 4) & 3) * 32) << 16;
+        for (int J = p; J < njobs; J += 2) {
+            const int use = J >> 1;
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+            const uint32_t ph = uint32_t(use & 1);
+            tc::mbar_wait(&d1_full[p], ph);
+            tc::fence_after_sync();
+            if (v == 0) btrace(J, 3);
+#pragma unroll 1
+            for (int u = 0; u < C::U; u++) {
+                float d[C::NU];
+                tc::tmem_ld_cols<C::NU>(dbuf(p) + lb + uint32_t(u * C::NB), d);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    float hi[C::SC], lo[C::SC];
+#pragma unroll
+                    for (int i = 0; i < C::SC; i++) tc::split(d[e * C::SC + i], hi[i], lo[i]);
+                    const uint32_t ta = abuf(p) + lb + uint32_t((2 * e + u) * C::SC);
+                    tc::tmem_st_cols<C::SC>(ta, hi);
+                    tc::tmem_st_cols<C::SC>(ta + C::P * C::SC, lo);
+                }
+            }
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            if (v == 0) btrace(J, 4);
+            tc::mbar_arrive(&a2_ready[p]);   // A is ready for level 2 and the accumulator is drained
+
+            tc::mbar_wait(&d2_full[p], ph);
+            tc::fence_after_sync();
+            if (v == 0) btrace(J, 6);
+            float d[C::U][C::NU];
+#pragma unroll
+            for (int u = 0; u < C::U; u++) tc::tmem_ld_cols<C::NU>(dbuf(p) + lb + uint32_t(u * C::NB), d[u]);
+            tc::tmem_wait_ld();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&d2_free[p]);
+            const int vg = vt * 128 + v;
+            if (vg < nv) {
+                const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+#pragma unroll
+                for (int u = 0; u < C::U; u++)
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        const int64_t q = (((a0 << 2) + 2 * u + e) << shg) + bq;
+                        float2* o = out + q * R * int64_t(nv) + vg;
+#pragma unroll
+                        for (int t = 0; t < R; t++)
+                            o[int64_t(t) * nv] = make_float2(d[u][e * C::SC + 2 * t], d[u][e * C::SC + 2 * t + 1]);
+                    }
+            }
+        }
+    } else if (warp == 12) {
+        // ---- loader ----
+        if (lane == 0) {
+            for (int J = 0; J < njobs; J++) {
+                const int it = int(unsigned(J) / unsigned(nvt));
+                const int vt = J - it * nvt;
+                const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+                const int e = J & 1;
+                if (J >= 2) tc::mbar_wait(&raw_empty[e], uint32_t((J >> 1) - 1) & 1);
+                btrace(J, 8);
+                const int v0 = vt * 128, vw = min(128, nv - v0);
+                const uint32_t row_bytes = uint32_t(vw) * 8;
+                tc::mbar_arrive_expect_tx(&raw_full[e], C::P * R * row_bytes);
+                const int64_t pin = rh ? bfs::recv_index(g * C::P, rh, rhg) : g * C::P;   // P pairs contiguous
+                for (int row = 0; row < C::P * R; row++)
+                    tc::bulk_g2s(raw(e) + row * 128 * 8, in + (pin * R + row) * int64_t(nv) + v0, row_bytes,
+                                 &raw_full[e]);
+            }
+        }
+    } else if (warp == 13) {
+        // ---- MMA issuer (whole warp, one elected lane issues) ----
+        constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
+        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
+        const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_band + C::OFF_W), LBO_B);
+        auto level = [&](int J, int m) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int wb = it % C::NWBUF, p = J & 1, use = J >> 1;
+            if (lane == 0) btrace(J, m == 0 ? 9 : 10);
+            if (m == 0) {
+                if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
+                tc::mbar_wait(&a1_ready[p], uint32_t(use & 1));
+                if (use > 0) tc::mbar_wait(&d2_free[p], uint32_t(use - 1) & 1);
+            } else {
+                tc::mbar_wait(&a2_ready[p], uint32_t(use & 1));
+            }
+            tc::fence_after_sync();
+#pragma unroll
+            for (int u = 0; u < C::U; u++) {
+                const uint32_t d = dbuf(p) + uint32_t(u * C::NB);
+                const uint32_t ahi = abuf(p) + uint32_t(2 * u * C::SC);
+                const uint64_t bhi = tc::desc_add(dW, wb * C::WSET + ((m * C::U + u) * 2) * C::WT);
+#pragma unroll
+                for (int q = 0; q < 3; q++) {
+                    const int pass = kPassOrder[q];
+                    const uint32_t a = ahi + (pass == 1 ? C::P * C::SC : 0);
+                    const uint64_t b = pass == 2 ? tc::desc_add(bhi, C::WT) : bhi;
+#pragma unroll
+                    for (int ks = 0; ks < C::KU / 8; ks++)
+                        tc::mma_tf32_ts_warp(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc, (q | ks) ? 1u : 0u);
+                }
+            }
+            if (lane == 0) btrace(J, m == 0 ? 2 : 5);
+            if (m == 0) {
+                tc::commit_warp(&d1_full[p]);
+            } else {
+                tc::commit_warp(&d2_full[p]);
+                tc::commit_warp(&a_free[p]);
+                if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
+            }
+            __syncwarp();
+        };
+        for (int J0 = 0; J0 < njobs; J0 += 2) {
+            level(J0, 0);
+            if (J0 + 1 < njobs) level(J0 + 1, 0);
+            level(J0, 1);
+            if (J0 + 1 < njobs) level(J0 + 1, 1);
+        }
+    } else {
+        // ---- weights (warps 14-15): compact r x 2r blocks -> embedded hi/lo B tiles, one group ahead ----
+        const int wt = tid - 448;
+        for (int it = 0; it < nit; it++) {
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+            const int wb = it % C::NWBUF;
+            if (it >= C::NWBUF) tc::mbar_wait(&w_free[wb], uint32_t(it / C::NWBUF - 1) & 1);
+            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+            constexpr int BATCH = 13;   // loads in flight per thread (bounded registers)
+#pragma unroll 1
+            for (int q0 = 0; q0 < C::WPT; q0 += BATCH) {
+                float2 w[BATCH];
+#pragma unroll
+                for (int q = 0; q < BATCH; q++) {
+                    const int idx = wt + 64 * (q0 + q);
+                    w[q] = make_float2(0.f, 0.f);
+                    if (q0 + q < C::WPT && idx < C::WTASKS) {
+                        const int t = idx % R, kcol = (idx / R) % (2 * R), e = (idx / (2 * R * R)) & 1;
+                        const int mu = idx / (4 * R * R), m = mu / C::U, u = mu % C::U;
+                        const int lv = m + 1, ep = u >> (2 - lv), i = u & ((1 << (2 - lv)) - 1);
+                        const int64_t pr = (((a0 << lv) + 2 * ep + e) << (LN - lin - lv)) + (bq << (2 - lv)) + i;
+                        w[q] = __ldg((lv == 1 ? W1 : W2) + pr * (2 * R * R) + kcol * R + t);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < BATCH; q++) {
+                    const int idx = wt + 64 * (q0 + q);
+                    if (q0 + q < C::WPT && idx < C::WTASKS) {
+                        const int t = idx % R, kcol = (idx / R) % (2 * R), e = (idx / (2 * R * R)) & 1;
+                        const int mu = idx / (4 * R * R), m = mu / C::U, u = mu % C::U;
+                        float hr, lr, hi_, li;
+                        tc::split(w[q].x, hr, lr);
+                        tc::split(w[q].y, hi_, li);
+                        const int n = e * C::SC + 2 * t, k = 2 * kcol;
+                        uint8_t* th = wtile(wb, m, u, 0);
+                        uint8_t* tl = wtile(wb, m, u, 1);
+                        const uint32_t o0 = tc::kmaj_off(n, k, C::NB), o1 = tc::kmaj_off(n + 1, k, C::NB);
+                        *reinterpret_cast<float2*>(th + o0) = make_float2(hr, -hi_);
+                        *reinterpret_cast<float2*>(tl + o0) = make_float2(lr, -li);
+                        *reinterpret_cast<float2*>(th + o1) = make_float2(hi_, hr);
+                        *reinterpret_cast<float2*>(tl + o1) = make_float2(li, lr);
+                    }
+                }
+            }
+            tc::fence_proxy_async();
+            tc::mbar_arrive(&w_full[wb]);
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<Q::TMEM_COLS>(tmem);
+    }
+}
+
 template <int R>
 static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
                               cudaStream_t s, int rh, int rhg)
 {
     using C = BandTC<R>;
+    const int64_t groups = d.N >> 2;
+    const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
+    if constexpr (Band2P<R>::FITS) {
+        if (!g_band_single_pipeline) {
+            auto kern = band_tc2p_kernel<R>;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+            if (e != cudaSuccess) return e;
+            kern<<<grid, 512, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg);
+            return cudaGetLastError();
+        }
+    }
     auto kern = band_tc_kernel<R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
-    const int64_t groups = d.N >> 2;
-    const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
     kern<<<grid, 384, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg);
     return cudaGetLastError();
 }
