@@ -191,7 +191,8 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        2: jobs alternate between two TMEM pipelines where TMEM allows (r <= 10; measured
  *                        slower at cfg4).  Process-wide tuning knob. */
 #define BF_OPT_BAND_PIPELINES 2
-/*   BF_OPT_BAND_TRACE_J0 (diagnostic): first job recorded by bf_debug_band_trace (default 0). */
+/*   BF_OPT_BAND_TRACE_J0 (diagnostic): enables the band timeline trace of bf_debug_band_trace for CTA
+ *                        value >> 16, jobs from value & 65535 (off by default). */
 #define BF_OPT_BAND_TRACE_J0 3
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 

@@ -404,18 +404,20 @@ cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const floa
 }
 
 // =============================================================================================
-// SL (eqn:bf3 P:791-797, amplitude post-scale and sum over k eqn:tg P:24-28) on the tensor cores.
-// CTA = one T_X leaf a x one tile of 128 vectors.  D[v][2j + c'] = sum over K = (b, t, c) of
-// A[v][(b, t, c)] B[(j, c')][(b, t, c)], A = delta_D[a n0 + b][t][v] split hi/lo, B = the expanded
-// U tiles of the leaf.  K streams in chunks of KP pairs:
-//   warp 12 (one thread)  bulk-copies the raw delta rows and the B tile of a chunk (3-deep rings),
+// SL (eqn:bf3 P:791-797, amplitude post-scale and sum over k eqn:tg P:24-28) on the tensor cores,
+// persistent.  A job = one T_X leaf a x one tile of 128 vectors (vector tile fastest).
+// D[v][2j + c'] = sum over K = (b, t, c) of A[v][(b, t, c)] B[(j, c')][(b, t, c)], A = delta_D[a n0 + b][t][v]
+// split hi/lo, B = the expanded U tiles of the leaf.  K streams in chunks of KP pairs, continuously across
+// the CTA's jobs:
+//   warp 12 (one thread)  bulk-copies the raw delta rows and the B tile of a chunk (NR-deep rings),
 //   warps 0-3             split a raw chunk into one of two A stages in TMEM (lane = vector; the
 //                         MMAs read A from TMEM, so shared memory carries only B),
-//   warp 13 (one thread)  issues the 3 KC/8 MMAs of a chunk; every SEG chunks it switches between
-//                         two TMEM accumulators (short chains),
-//   warps 4-11            drain each finished segment into FP32 registers (lane quarter = vectors,
-//                         half the columns each), then apply a_k, sum over k by lane shuffles and
-//                         write G through a shared-memory transpose.
+//   warp 13               issues the 3 KC/8 MMAs of a chunk (elected lane); every SEG chunks it switches
+//                         between two TMEM accumulators (short chains),
+//   warps 4-11            drain each finished segment into FP32 registers (lane quarter = vectors, half
+//                         the columns each); at the end of a job apply a_k, sum over k by lane shuffles
+//                         and write G through a dedicated shared-memory transpose buffer, while the
+//                         other roles already stream the next job.
 // =============================================================================================
 template <int R, int N0, int NA, int KP>
 struct SLTC {
@@ -426,17 +428,18 @@ struct SLTC {
     static constexpr int NSEG = (NCH + SEG - 1) / SEG;
     static constexpr uint32_t RAW = uint32_t(KP) * R * 128 * 8;
     static constexpr uint32_t BT = uint32_t(NB) * KC * 4;   // one of hi / lo
-    static constexpr int NR = 3;                            // ring depth (raw rows and B tiles)
-    static constexpr uint32_t OFF_B = NR * RAW, OFF_AS = OFF_B + 2 * NR * BT;
     static constexpr uint32_t GS_STRIDE = N0 + 1;
-    static constexpr size_t SMEM = size_t(OFF_AS) + size_t(NA) * N0 * 8;
+    static constexpr uint32_t GS_BYTES = uint32_t(128 / NA) * GS_STRIDE * 8;
+    static constexpr uint32_t AS_BYTES = uint32_t(NA) * N0 * 8;
+    static constexpr int NR = (3 * (RAW + 2 * BT) + GS_BYTES + AS_BYTES <= 232448 - 1024) ? 3 : 2;   // ring depth
+    static constexpr uint32_t OFF_B = NR * RAW, OFF_GS = OFF_B + 2 * NR * BT, OFF_AS = OFF_GS + GS_BYTES;
+    static constexpr size_t SMEM = size_t(OFF_AS) + AS_BYTES;
     // TMEM: two A stages (hi KC columns, then lo KC columns) and two accumulators of NB columns
     static constexpr int A_COLS = 2 * KC, D_OFF = 2 * A_COLS;
     static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * NB>();
     static_assert(KC % 8 == 0, "K chunk must be whole MMA K steps");
     static_assert(D_OFF + 2 * NB <= 512, "TMEM budget");
-    static_assert(SMEM <= 232448 - 512, "shared memory budget");
-    static_assert(size_t(128 / NA) * GS_STRIDE * 8 <= OFF_AS, "G staging fits in the freed rings");
+    static_assert(SMEM <= 232448 - 1024, "shared memory budget");
 };
 
 template <int R, int N0, int NA, int KP>
@@ -448,8 +451,8 @@ __global__ void __launch_bounds__(448, 1)
     extern __shared__ __align__(128) uint8_t sm_sltc[];
     auto raw = [&](int e) { return sm_sltc + e * C::RAW; };
     auto opB = [&](int e, int lo) { return sm_sltc + C::OFF_B + (2 * e + lo) * C::BT; };
-    float2* As = reinterpret_cast<float2*>(sm_sltc + C::OFF_AS);   // [NA][N0] a_k(x)
-    float2* Gs = reinterpret_cast<float2*>(sm_sltc);               // epilogue: [128/NA][GS_STRIDE]
+    float2* Gs = reinterpret_cast<float2*>(sm_sltc + C::OFF_GS);   // [128/NA][GS_STRIDE]
+    float2* As = reinterpret_cast<float2*>(sm_sltc + C::OFF_AS);   // [NA][N0] a_k(x) of the current job
     __shared__ uint64_t raw_full[C::NR], raw_empty[C::NR], b_full[C::NR], b_empty[C::NR], a_full[2], a_empty[2],
         dfull[2], dempty[2];
     __shared__ uint32_t tmem_base;
@@ -457,10 +460,9 @@ __global__ void __launch_bounds__(448, 1)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t N = int64_t(1) << LN;
-    const int64_t a = blockIdx.x / nvt;
-    const int v0 = (blockIdx.x % nvt) * 128;
-    const int vw = min(128, nv - v0);
-    const float* wsrc = Ux + a * (int64_t(C::NCH) * 2 * (C::BT / 4));
+    const int64_t njobs_all = (N / N0) * nvt;
+    const int njobs = int((njobs_all - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const int nch_all = njobs * C::NCH;
 
     if (warp == 0) tc::tmem_alloc<TMEM_COLS>(&tmem_base);
     if (tid == 0) {
@@ -478,22 +480,25 @@ __global__ void __launch_bounds__(448, 1)
         }
         tc::mbar_fence_init();
     }
-    for (int i = tid; i < NA * N0; i += blockDim.x) As[i] = __ldg(ampa + (i / N0) * N + a * N0 + (i % N0));
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base;
 
     if (warp == 12) {
-        // ---- loader ----
+        // ---- loader: the chunk stream of all this CTA's jobs ----
         if (lane == 0) {
-            const uint32_t row_bytes = uint32_t(vw) * 8;
-            for (int ch = 0; ch < C::NCH; ch++) {
-                const int e = ch % C::NR, use = ch / C::NR;
+            for (int gch = 0; gch < nch_all; gch++) {
+                const int jl = gch / C::NCH, ch = gch - jl * C::NCH;
+                const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
+                const int64_t a = job / unsigned(nvt);
+                const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
+                const int e = gch % C::NR, use = gch / C::NR;
                 if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
                 tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
-                tc::bulk_g2s(opB(e, 0), wsrc + int64_t(ch) * 2 * (C::BT / 4), 2 * C::BT, &b_full[e]);
+                tc::bulk_g2s(opB(e, 0), Ux + (a * C::NCH + ch) * 2 * (C::BT / 4), 2 * C::BT, &b_full[e]);
                 if (use > 0) tc::mbar_wait(&raw_empty[e], (use - 1) & 1);
+                const uint32_t row_bytes = uint32_t(vw) * 8;
                 tc::mbar_arrive_expect_tx(&raw_full[e], KP * R * row_bytes);
                 const int64_t p0 = a * N0 + int64_t(ch) * KP;
                 for (int row = 0; row < KP * R; row++)
@@ -506,11 +511,14 @@ __global__ void __launch_bounds__(448, 1)
         constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
         constexpr uint32_t LBO_B = (C::NB / 8) * 128;
         const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(opB(0, 0)), LBO_B);
-        for (int ch = 0; ch < C::NCH; ch++) {
-            const int e = ch % C::NR, sa = ch & 1, seg = ch / C::SEG, slot = seg & 1, first = (ch % C::SEG) == 0;
-            if (first && seg >= 2) tc::mbar_wait(&dempty[slot], ((seg >> 1) - 1) & 1);
-            tc::mbar_wait(&a_full[sa], (ch >> 1) & 1);
-            tc::mbar_wait(&b_full[e], (ch / C::NR) & 1);
+        int gseg = 0;   // accumulation segments issued (slots alternate across jobs)
+        for (int gch = 0; gch < nch_all; gch++) {
+            const int ch = gch % C::NCH;
+            const int e = gch % C::NR, sa = gch & 1, slot = gseg & 1, first = (ch % C::SEG) == 0;
+            const bool last = (ch % C::SEG) == C::SEG - 1 || ch == C::NCH - 1;
+            if (first && gseg >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gseg >> 1) - 1) & 1);
+            tc::mbar_wait(&a_full[sa], uint32_t(gch >> 1) & 1);
+            tc::mbar_wait(&b_full[e], uint32_t(gch / C::NR) & 1);
             tc::fence_after_sync();
             const uint32_t d = tmem + uint32_t(C::D_OFF + slot * C::NB);
 #pragma unroll
@@ -525,17 +533,20 @@ __global__ void __launch_bounds__(448, 1)
             }
             tc::commit_warp(&a_empty[sa]);
             tc::commit_warp(&b_empty[e]);
-            if ((ch % C::SEG) == C::SEG - 1 || ch == C::NCH - 1) tc::commit_warp(&dfull[slot]);
+            if (last) {
+                tc::commit_warp(&dfull[slot]);
+                gseg++;
+            }
             __syncwarp();
         }
     } else if (warp < 4) {
         // ---- split: raw delta rows -> A stage (hi / lo) in TMEM; thread = vector (its lane) ----
         const int v = tid;
         const uint32_t lb = uint32_t(warp * 32) << 16;
-        for (int ch = 0; ch < C::NCH; ch++) {
-            const int e = ch % C::NR, sa = ch & 1;
-            tc::mbar_wait(&raw_full[e], (ch / C::NR) & 1);
-            if (ch >= 2) tc::mbar_wait(&a_empty[sa], ((ch >> 1) - 1) & 1);
+        for (int gch = 0; gch < nch_all; gch++) {
+            const int e = gch % C::NR, sa = gch & 1;
+            tc::mbar_wait(&raw_full[e], uint32_t(gch / C::NR) & 1);
+            if (gch >= 2) tc::mbar_wait(&a_empty[sa], uint32_t((gch >> 1) - 1) & 1);
             tc::fence_after_sync();
             const float2* rd = reinterpret_cast<const float2*>(raw(e));   // [KP R][128]
             float hi[C::KC], lo[C::KC];   // column (pl, t, c) = pl 2R + 2t + c
@@ -555,48 +566,57 @@ __global__ void __launch_bounds__(448, 1)
             tc::mbar_arrive(&a_full[sa]);
         }
     } else {
-        // ---- drain (warps 4-11): lane quarter warp % 4 = vectors, column half (warp - 4) / 4 ----
+        // ---- drain + epilogue (warps 4-11): lane quarter warp % 4 = vectors, column half (warp - 4) / 4 ----
         constexpr int HC = C::NB / 2;   // columns per drain thread (j in a half of the leaf)
-        const int q4 = warp & 3, half = (warp - 4) >> 2, vl = q4 * 32 + lane;
-        float sum[HC];
-#pragma unroll
-        for (int i = 0; i < HC; i++) sum[i] = 0.f;
-        for (int seg = 0; seg < C::NSEG; seg++) {
-            const int slot = seg & 1;
-            tc::mbar_wait(&dfull[slot], (seg >> 1) & 1);
-            tc::fence_after_sync();
-            const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * C::NB + half * HC);
-#pragma unroll
-            for (int c0 = 0; c0 < HC; c0 += 32) {
-                float x[32];
-                tc::tmem_ld_cols<(HC < 32 ? HC : 32)>(taddr + c0, x);
-                tc::tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < (HC < 32 ? HC : 32); i++) sum[c0 + i] += x[i];
-            }
-            tc::fence_before_sync();
-            tc::mbar_arrive(&dempty[slot]);
-        }
-        // every MMA has completed (last dfull): the rings are free for the G staging
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int q4 = warp & 3, half = (warp - 4) >> 2, vl = q4 * 32 + lane, dt = (warp - 4) * 32 + lane;
         const int k = vl % NA, cl = vl / NA;
+        int gseg = 0;
+        for (int jl = 0; jl < njobs; jl++) {
+            const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
+            const int64_t a = job / unsigned(nvt);
+            const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
+            float sum[HC];
 #pragma unroll
-        for (int jj = 0; jj < HC / 2; jj++) {
-            const int j = half * (HC / 2) + jj;
-            float2 g = cmul_tc(As[k * N0 + j], make_float2(sum[2 * jj], sum[2 * jj + 1]));
+            for (int i = 0; i < HC; i++) sum[i] = 0.f;
+            for (int seg = 0; seg < C::NSEG; seg++, gseg++) {
+                const int slot = gseg & 1;
+                tc::mbar_wait(&dfull[slot], uint32_t(gseg >> 1) & 1);
+                tc::fence_after_sync();
+                const uint32_t taddr =
+                    tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * C::NB + half * HC);
 #pragma unroll
-            for (int m = 1; m < NA; m <<= 1) {
-                g.x += __shfl_xor_sync(0xffffffffu, g.x, m);
-                g.y += __shfl_xor_sync(0xffffffffu, g.y, m);
+                for (int c0 = 0; c0 < HC; c0 += 32) {
+                    float x[32];
+                    tc::tmem_ld_cols<(HC < 32 ? HC : 32)>(taddr + c0, x);
+                    tc::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < (HC < 32 ? HC : 32); i++) sum[c0 + i] += x[i];
+                }
+                tc::fence_before_sync();
+                tc::mbar_arrive(&dempty[slot]);
             }
-            if ((j % NA) == k) Gs[cl * C::GS_STRIDE + j] = g;
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        // copy out: RHS column c0 + cl, rows a n0 .. a n0 + n0 - 1 (contiguous)
-        const int c0 = v0 / NA, cw = vw / NA, dt = (warp - 4) * 32 + lane;
-        for (int idx = dt; idx < cw * N0; idx += 256) {
-            const int cc = idx / N0, j = idx % N0;
-            G[a * N0 + j + int64_t(c0 + cc) * ldg] = Gs[cc * C::GS_STRIDE + j];
+            // epilogue of the job: a_k(x) (staged per job), sum over k, G transposed through Gs
+            asm volatile("bar.sync 1, 256;" ::: "memory");   // the previous job's copy-out is done with Gs / As
+            for (int i = dt; i < NA * N0; i += 256) As[i] = __ldg(ampa + (i / N0) * N + a * N0 + (i % N0));
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll
+            for (int jj = 0; jj < HC / 2; jj++) {
+                const int j = half * (HC / 2) + jj;
+                float2 g = cmul_tc(As[k * N0 + j], make_float2(sum[2 * jj], sum[2 * jj + 1]));
+#pragma unroll
+                for (int m = 1; m < NA; m <<= 1) {
+                    g.x += __shfl_xor_sync(0xffffffffu, g.x, m);
+                    g.y += __shfl_xor_sync(0xffffffffu, g.y, m);
+                }
+                if ((j % NA) == k) Gs[cl * C::GS_STRIDE + j] = g;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            // copy out: RHS column c0 + cl, rows a n0 .. a n0 + n0 - 1 (contiguous)
+            const int c0 = v0 / NA, cw = vw / NA;
+            for (int idx = dt; idx < cw * N0; idx += 256) {
+                const int cc = idx / N0, j = idx % N0;
+                G[a * N0 + j + int64_t(c0 + cc) * ldg] = Gs[cc * C::GS_STRIDE + j];
+            }
         }
     }
     tc::fence_before_sync();
@@ -616,8 +636,9 @@ static cudaError_t sl_tc_go(const Dims& d, const float2* in, const float* Ux, co
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
     const int nvt = (nv + 127) / 128;
-    const int64_t ctas = (d.N / N0) * nvt;
-    kern<<<unsigned(ctas), 448, C::SMEM, s>>>(in, Ux, ampa, G, ldg, d.LN, nv, nvt);
+    const int64_t jobs = (d.N / N0) * nvt;
+    const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
+    kern<<<grid, 448, C::SMEM, s>>>(in, Ux, ampa, G, ldg, d.LN, nv, nvt);
     return cudaGetLastError();
 }
 
@@ -649,8 +670,9 @@ void band_set_single_pipeline(int v) { g_band_single_pipeline = v; }
 // ---- timeline trace of the band kernel (diagnostic; CTA 0, first BT_JOBS jobs, SM clock) ----
 constexpr int BT_JOBS = 64, BT_EV = 12;
 __device__ long long g_band_trace[BT_JOBS * BT_EV];
-__device__ int g_band_trace_j0 = 0;    // first traced job (BF_OPT_BAND_TRACE_J0: job + 65536 * cta)
-__device__ int g_band_trace_cta = 0;   // traced CTA
+// (constant bank: the check costs no memory round trip; tracing is off until BF_OPT_BAND_TRACE_J0 is set)
+__constant__ int g_band_trace_j0 = 0;     // first traced job (BF_OPT_BAND_TRACE_J0: job + 65536 * cta)
+__constant__ int g_band_trace_cta = -1;   // traced CTA (-1: off)
 __device__ __forceinline__ void btrace(int64_t J, int ev)
 {
     const int64_t j = J - g_band_trace_j0;

@@ -12,8 +12,7 @@ w = W.CONFIGS["cfg4"].with_(log2n=int(sys.argv[1]) if len(sys.argv) > 1 else 18)
 plan = bf.Plan.build_fio(bf.fio_of(w), max_nrhs_chunk=w.nrhs)
 if len(sys.argv) > 2:
     plan.set_option(bf.BF_OPT_BAND_PIPELINES, int(sys.argv[2]))
-if len(sys.argv) > 3:
-    plan.set_option(bf.BF_OPT_BAND_TRACE_J0, int(sys.argv[3]))
+plan.set_option(bf.BF_OPT_BAND_TRACE_J0, int(sys.argv[3]) if len(sys.argv) > 3 else 0)
 F = torch.randn(w.nrhs, w.n, dtype=torch.complex64, device="cuda")
 G = torch.empty_like(F)
 for _ in range(2):
