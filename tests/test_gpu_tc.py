@@ -137,3 +137,23 @@ def test_tc_apply_host_pipelined():
     plan.apply_host(Fh, Gh, nrhs)
     plan.destroy()
     assert np.array_equal(np.asfortranarray(Gh.numpy().T), ref)
+
+
+def test_tc_band_two_pipeline_variant():
+    """The selectable two-TMEM-pipeline band kernel (BF_OPT_BAND_PIPELINES = 2) computes the same
+    result as the default single-pipeline kernel (same MMAs and order per job: bitwise)."""
+    LN, l0, r, nrhs = 14, 5, 10, 64          # two two-level bands (levels 6..9), nv = 128
+    F = W.rhs(1 << LN, nrhs, 31)
+    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    with pytest.raises(bf.BFError):
+        plan.set_option(bf.BF_OPT_BAND_PIPELINES, 3)
+    G1 = _apply(plan, F)
+    plan.set_option(bf.BF_OPT_BAND_PIPELINES, 2)
+    try:
+        G2 = _apply(plan, F)
+    finally:
+        plan.set_option(bf.BF_OPT_BAND_PIPELINES, 1)
+    plan.destroy()
+    assert np.array_equal(G1, G2)
+    R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, :3])
+    assert np.all(oracle.rel_l2(G2[:, :3].astype(np.complex128), R, axis=0) <= PARITY)
