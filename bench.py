@@ -101,6 +101,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
 
 
+def _ncu_traffic(workload, cls):
+    """DRAM bytes per launch of kernel class `cls` from the committed ncu capture of this workload
+    (profiles/r1_traffic_<workload>.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"r1_traffic_{workload}.json")) as f:
+            return json.load(f)["bytes_per_launch"].get(cls)
+    except Exception:
+        return None
+
+
 def stage_model(w, nvec, info):
     """Algorithmic flops and bytes per launch of each kernel class.
     Transfer classes: a launch performs class_levels/class_launches fused levels; each launch reads and
@@ -288,7 +298,7 @@ def main():
         roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "peak_source": "FP32 FFMA from unit counts: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 5)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = _ncu_traffic(args.config if not args.log2n else None, dom)
     roof["kernel"] = dom
     roof["tensor_cores"] = dom in tc_classes
     roof["avg_launch_ms"] = avg_s * 1e3

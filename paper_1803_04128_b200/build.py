@@ -17,6 +17,7 @@ BUILD_DIR = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+NVCC_FLAGS += [f"-D{m}" for m in os.environ.get("BF_NVCC_DEFINES", "").split()]   # tuning experiments only
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-march=x86-64-v3", "-ffp-contract=off", "-Wall"]
 
 CU_SOURCES = ["bf_kernels.cu", "bf_tc.cu", "bf_plan.cu"]
