@@ -195,6 +195,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if local_world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # the untimed host factor builder is OpenMP: share the host cores between the ranks of this node
+        # (must be set before the library / OpenMP runtime is loaded)
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_world))
     w = W.CONFIGS[args.config]
     if args.nrhs:
         w = w.with_(nrhs=args.nrhs)
