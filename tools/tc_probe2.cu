@@ -545,9 +545,64 @@ void rate(int ts)
     cudaFree(dc);
 }
 
+// How does kind::tf32 consume an FP32 operand: truncation or round-to-nearest of the low 13 bits?
+// A = 1 + 3 2^-12 (0.75 tf32 ulp above 1), B = 1 (K = 8, one nonzero term): D = 1 (truncate) or 1 + 2^-10 (round).
+__global__ void tf32_rounding_kernel(float* out)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (M + 32) * 8; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.f;
+    __syncthreads();
+    if (tid == 0) {
+        *reinterpret_cast<float*>(smem + tc::kmaj_off(0, 0, M)) = 1.0f + 3.0f / 4096.0f;            // A[0][0]
+        *reinterpret_cast<float*>(smem + M * 8 * 4 + tc::kmaj_off(0, 0, 32)) = 1.0f;                // B[0][0]
+        *reinterpret_cast<float*>(smem + tc::kmaj_off(1, 0, M)) = -(1.0f + 3.0f / 4096.0f);         // A[1][0]
+        *reinterpret_cast<float*>(smem + tc::kmaj_off(2, 0, M)) = 1.0f + 1.0f / 4096.0f;            // 0.25 ulp
+    }
+    if (warp == 0) tc::tmem_alloc<32>(&tbase);
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = tbase;
+    if (tid == 0) {
+        tc::mma_tf32(tm, tc::desc_kmajor(tc::smem_u32(smem), (M / 8) * 128),
+                     tc::desc_kmajor(tc::smem_u32(smem + M * 8 * 4), (32 / 8) * 128), tc::idesc_tf32(M, 32), 0u);
+        tc::commit(&bar);
+    }
+    tc::mbar_wait(&bar, 0);
+    tc::fence_after_sync();
+    float v[8];
+    tc::tmem_ld8(tm + (uint32_t(warp * 32) << 16), v);
+    tc::tmem_wait_ld();
+    if (tid < 3) out[tid] = v[0];
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<32>(tm);
+}
+
 int main()
 {
     int fails = 0;
+    {
+        float* d;
+        cudaMalloc(&d, 16);
+        cudaFuncSetAttribute(tf32_rounding_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (M + 32) * 32);
+        tf32_rounding_kernel<<<1, 128, (M + 32) * 32>>>(d);
+        float h[3] = {0, 0, 0};
+        cudaError_t e = cudaDeviceSynchronize();
+        cudaMemcpy(h, d, 12, cudaMemcpyDeviceToHost);
+        printf("tf32 operand conversion: 1+0.75ulp -> %.9g, -(1+0.75ulp) -> %.9g, 1+0.25ulp -> %.9g  => %s (%s)\n", h[0],
+               h[1], h[2], h[0] == 1.0f ? "TRUNCATION" : (h[0] == 1.0f + 1.0f / 1024 ? "ROUND-TO-NEAREST" : "?"),
+               e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+        cudaFree(d);
+    }
     fails += check<48>(0);
     fails += check<48>(1);
     fails += check<48>(2);
