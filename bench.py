@@ -188,6 +188,8 @@ def main():
                     help="split ONE batch by index over the ranks (NCCL all-to-all at level h; cfg5's mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=["copy", "fused"], default="copy",
+                    help="index-shard exchange: NCCL send/recv step, or peer stores from the level-h launch")
     ap.add_argument("--band-pipelines", type=int, default=None, choices=[1, 2],
                     help="tensor-core band variant (tuning; default: the library's)")
     args = ap.parse_args()
@@ -230,6 +232,8 @@ def main():
         if world > 1:
             dist.broadcast_object_list(obj, src=0)
         plan = bf.Plan.build_fio_sharded(bf.fio_of(w), rank, world, obj[0], device=local, max_nrhs_chunk=chunk)
+        if args.exchange == "fused":
+            plan.set_option(bf.BF_OPT_EXCHANGE, 1)   # collective: every rank
         F = W.rhs(w.n, w.nrhs, w.seed)
         rows = w.n // world
         F = np.asfortranarray(F[rank * rows:(rank + 1) * rows])
@@ -349,7 +353,9 @@ def main():
             "config": {"workload": args.config, "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
                        "nrhs_per_gpu": w.nrhs if not args.index_shard else w.nrhs,
                        "global_batch": w.nrhs * jobs, "max_nrhs_chunk": chunk,
-                       "parallelism": (f"index-sharded x{world} (NCCL all-to-all at level h)" if args.index_shard
+                       "parallelism": (f"index-sharded x{world} (level-h exchange: "
+                                       + ("peer stores from the level-h launch)" if args.exchange == "fused"
+                                          else "NCCL all-to-all)") if args.index_shard
                                        else f"rhs-sharded x{world} (no collective)"),
                        "l2": "no flush: the working set (F 2.1 GB, coefficients 43 GB/level, factors 25 GB) "
                              "exceeds the 126 MB L2",

@@ -194,6 +194,15 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
 /*   BF_OPT_BAND_TRACE_J0 (diagnostic): enables the band timeline trace of bf_debug_band_trace for CTA
  *                        value >> 16, jobs from value & 65535 (off by default). */
 #define BF_OPT_BAND_TRACE_J0 3
+/*   BF_OPT_EXCHANGE (index-sharded plans): 0 (default) = the level-h exchange is a separate step (NCCL
+ *                        grouped send/recv, or device copies between emulated shards); 1 = fused exchange:
+ *                        the launch that produces level h stores each output pair directly into its
+ *                        destination shard's receive array (peer memory over NVLink via CUDA IPC for one
+ *                        shard per GPU; the same device for emulated shards), ordered by stream-ordered
+ *                        barriers.  Enabling it is collective for NCCL plans (every rank must call it).
+ *                        Not available when h == l0 or with a caller workspace (bf_apply_ex), where the
+ *                        separate exchange is used. */
+#define BF_OPT_EXCHANGE 4
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band

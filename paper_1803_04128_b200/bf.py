@@ -26,6 +26,7 @@ BF_SHARD_NONE, BF_SHARD_NCCL, BF_SHARD_EMULATED = 0, 1, 2
 BF_OPT_TENSOR_CORES = 1
 BF_OPT_BAND_PIPELINES = 2
 BF_OPT_BAND_TRACE_J0 = 3
+BF_OPT_EXCHANGE = 4
 STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALIGNMENT", 4: "BF_ERR_OOM",
           5: "BF_ERR_CUDA", 6: "BF_ERR_NCCL", 7: "BF_ERR_NOT_SUPPORTED", 8: "BF_ERR_STATE"}
 

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "bf_shard.h"
+
 namespace bfk {
 
 // Shape of one butterfly (notation of include/bf.h).
@@ -40,19 +42,20 @@ cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const
 // Transfer level l (eqn:2 / eqn:3): out[p](t) = sum_{c,s} W[p](t, c r + s) in[(a>>1) 2^(LN-l+1) + 2b + c](s)
 // (at l == h the switch is already folded into W).
 // rh > 0: `in` is a receive buffer of the index-sharded exchange (input pair p at bfs::recv_index(p, rh, rhg)).
+// po (fused exchange): the output pairs go to their destination shards' receive arrays (bf_shard.h).
 cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, int nv, cudaStream_t s,
-                        int rh = 0, int rhg = 0);
+                        int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr);
 
 // Band of K (1 or 2) transfer levels l_first .. l_first+K-1 fused in shared memory; W[m] are the
 // weights of level l_first+m.
 bool band_supported(int R, int nv);
 cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W, int nv,
-                        cudaStream_t s, int rh = 0, int rhg = 0);
+                        cudaStream_t s, int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr);
 
 // Band of 2 transfer levels on the tensor cores (bf_tc.cu): same contract as launch_band with K = 2.
 bool band_tc_supported(const Dims& d, int nv);
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh = 0, int rhg = 0);
+                           cudaStream_t s, int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr);
 
 // Diagnostic: SM-clock timeline of the last band_tc launch (CTA 0, first 64 jobs x 12 events).
 cudaError_t band_trace(long long* out, int n);

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) s0_kernel(const float2* __restrict__ F, i
 template <int R, int TN>
 __global__ void __launch_bounds__(128) xfer_kernel(const float2* __restrict__ in, float2* __restrict__ out,
                                                    const float2* __restrict__ Wl,
-                                                   int LN, int l, int nv, int rh, int rhg)
+                                                   int LN, int l, int nv, int rh, int rhg, const bfs::PeerOut po)
 {
     const int64_t N = int64_t(1) << LN;
     const int cpu = nv / TN;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(128) xfer_kernel(const float2* __restrict__ in
     for (int e = 0; e < 2; e++) {
         float2 (&acc)[R][TN] = e ? acc1 : acc0;
         const int64_t p = e ? p1 : p0;
-        float2* o = out + p * R * nv + vg * TN;
+        float2* o = bfs::pair_out(out, po, p, R, nv) + vg * TN;
 #pragma unroll
         for (int t = 0; t < R; t++) stc<TN>(o + int64_t(t) * nv, acc[t]);
     }
@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(256, 2) sl_tile_kernel(const float2* __restric
 // ---------------------------------------------------------------------------
 struct BandArgs {
     const float2* W[4];   // weights of band levels 1..K (bf.h XFER layout; level h has the switch folded in)
+    bfs::PeerOut po;      // fused exchange: peer stores of the last level (po.on)
     int rh, rhg;          // > 0: the input is a receive buffer of the index-sharded exchange (bf_shard.h)
 };
 
@@ -558,7 +559,7 @@ __global__ void __launch_bounds__(256, (R <= 10 ? 2 : 1))
                     rstride = VT;
                 } else {
                     const int64_t p = (((a0 << K) + 2 * ep + e) << (LN - lin - K)) + bq;
-                    dst = out + p * R * int64_t(nv) + v0;
+                    dst = bfs::pair_out(out, args.po, p, R, nv) + v0;
                     rstride = nv;
                 }
 #pragma unroll
@@ -656,10 +657,10 @@ static cudaError_t s0_go(const Dims& d, const float2* F, int64_t ldf, const floa
 
 template <int R, int TN>
 static cudaError_t xfer_go(const Dims& d, int l, const float2* in, float2* out, const float2* W, int nv, int rh, int rhg,
-                           cudaStream_t s)
+                           const bfs::PeerOut& po, cudaStream_t s)
 {
     const int64_t threads = (d.N / 2) * (nv / TN);
-    xfer_kernel<R, TN><<<unsigned((threads + 127) / 128), 128, 0, s>>>(in, out, W, d.LN, l, nv, rh, rhg);
+    xfer_kernel<R, TN><<<unsigned((threads + 127) / 128), 128, 0, s>>>(in, out, W, d.LN, l, nv, rh, rhg, po);
     return cudaGetLastError();
 }
 
@@ -712,11 +713,12 @@ cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2*
 }
 
 cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, const float2* W, int nv, cudaStream_t s,
-                        int rh, int rhg)
+                        int rh, int rhg, const bfs::PeerOut* po)
 {
+    const bfs::PeerOut pz = po ? *po : bfs::PeerOut{};
     const int tn = pick_tn(nv, 2);
-    if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, 2>(d, l, in, out, W, nv, rh, rhg, s)))
-    BF_DISPATCH_R(d.R, (xfer_go<RR, 1>(d, l, in, out, W, nv, rh, rhg, s)))
+    if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, 2>(d, l, in, out, W, nv, rh, rhg, pz, s)))
+    BF_DISPATCH_R(d.R, (xfer_go<RR, 1>(d, l, in, out, W, nv, rh, rhg, pz, s)))
 }
 
 template <int R, int NA>
@@ -760,10 +762,11 @@ bool band_supported(int R, int nv) { return (R == 6 || R == 8 || R == 10 || R ==
 
 template <int R, int K>
 static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh, int rhg)
+                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po)
 {
     BandArgs a{};
     for (int m = 0; m < K; m++) a.W[m] = W[m];
+    if (po) a.po = *po;
     a.rh = rh;
     a.rhg = rhg;
     const size_t shm = band_smem_bytes<R, K>();
@@ -776,10 +779,10 @@ static cudaError_t band_go(const Dims& d, int l_first, const float2* in, float2*
 }
 
 cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W, int nv,
-                        cudaStream_t s, int rh, int rhg)
+                        cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po)
 {
 #define BF_BAND_CASE(RR, KK) \
-    case RR: return band_go<RR, KK>(d, l_first, in, out, W, nv, s, rh, rhg);
+    case RR: return band_go<RR, KK>(d, l_first, in, out, W, nv, s, rh, rhg, po);
     if (K == 2) {
         switch (d.R) {
             BF_BAND_CASE(6, 2) BF_BAND_CASE(8, 2) BF_BAND_CASE(10, 2) BF_BAND_CASE(12, 2)

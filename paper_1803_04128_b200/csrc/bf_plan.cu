@@ -140,6 +140,11 @@ struct bf_plan_s {
     int mode = BF_SHARD_NONE;  // BF_SHARD_NONE / BF_SHARD_NCCL / BF_SHARD_EMULATED
     std::vector<Shard> sh;     // 1 shard, or `world` shards when emulated
     ncclComm_t comm = nullptr;
+    // fused exchange (BF_OPT_EXCHANGE = 1): the level-h launch stores into the destination shards' arrays
+    bool exchange_peer = false;
+    float2* peer_ws[bfs::kMaxShards] = {};   // workspace base of every shard (IPC-mapped for NCCL plans)
+    bool peer_ipc[bfs::kMaxShards] = {};     // opened with cudaIpcOpenMemHandle (closed at destroy)
+    char* bar_buf = nullptr;                 // 2 x world bytes for the stream-ordered NCCL barrier
     std::vector<std::vector<int64_t>> uploaded;   // [shard][stage slot]
     bool finalized = false;
     size_t ws_bytes = 0;       // per shard
@@ -247,6 +252,9 @@ void free_plan(bf_plan_s* p)
 {
     if (!p) return;
     DeviceGuard g(p->device);
+    for (int i = 0; i < bfs::kMaxShards; i++)
+        if (p->peer_ipc[i]) cudaIpcCloseMemHandle(p->peer_ws[i]);
+    cudaFree(p->bar_buf);
     if (p->done) cudaEventSynchronize(p->done);
     for (auto& tl : p->pending) {
         cudaEventDestroy(tl.start);
@@ -393,7 +401,7 @@ bf_status_t exchange(bf_plan_s* p, float2* const* ws, int send_buf, int nv, cuda
 // the current level, updated in place.  remap_first: the first transfer launch reads the receive layout.
 bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size_t s_begin, size_t s_end,
                       const float2* F, int64_t ldf, float2* G, int64_t ldg, int nv, int& cur, bool remap_first,
-                      float2* ws, cudaStream_t s)
+                      float2* ws, cudaStream_t s, const bfs::PeerOut* po = nullptr)
 {
     const bfk::Dims dl = p->local();
     const int64_t arr = p->nloc() * p->d.R * nv;
@@ -412,13 +420,13 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                     return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s);
                 return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
             case Step::XFER:
-                return bfk::launch_xfer(dl, lk, in, out, sh.xfer[stp.l_first - p->d.l0 - 1], nv, s, rh, rhg);
+                return bfk::launch_xfer(dl, lk, in, out, sh.xfer[stp.l_first - p->d.l0 - 1], nv, s, rh, rhg, po);
             case Step::BAND: {
                 const float2* W[2] = {sh.xfer[stp.l_first - p->d.l0 - 1],
                                       stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
                 if (stp.K == 2 && p->tensor_cores && bfk::band_tc_supported(dl, nv))
-                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg);
-                return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg);
+                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po);
+                return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
             }
             case Step::SL:
                 if (p->tensor_cores && sh.ux && bfk::sl_tc_supported(dl, nv))
@@ -432,6 +440,69 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
             cur = 1 - cur;
             remap = false;
         }
+    }
+    return BF_OK;
+}
+
+// Stream-ordered barrier over the NCCL ranks: every rank sends one byte to and receives one byte from
+// every peer; the group completes on a rank's stream only after every peer has reached the same point.
+bf_status_t nccl_barrier(bf_plan_s* p, cudaStream_t s)
+{
+    if (p->mode != BF_SHARD_NCCL || p->world == 1) return BF_OK;
+    Nccl& n = nccl();
+    ncclResult_t r = n.GroupStart();
+    if (r) return nccl_fail(r, "ncclGroupStart");
+    for (int peer = 0; peer < p->world; peer++) {
+        if (peer == p->rank) continue;
+        if ((r = n.Send(p->bar_buf + p->rank, 1, kNcclUint8, peer, p->comm, s))) break;
+        if ((r = n.Recv(p->bar_buf + p->world + peer, 1, kNcclUint8, peer, p->comm, s))) break;
+    }
+    ncclResult_t r2 = n.GroupEnd();
+    if (r) return nccl_fail(r, "barrier send/recv");
+    if (r2) return nccl_fail(r2, "barrier ncclGroupEnd");
+    return BF_OK;
+}
+
+// One RHS chunk of a sharded plan with the fused exchange: (A) every shard runs its first half up to the
+// launch that produces level h; (B) that launch stores its output pairs straight into the destination
+// shards' receive arrays (peer memory over NVLink for one shard per GPU); (C) the second halves read their
+// receive arrays in place.  NCCL plans order A/B/C across the ranks with stream-ordered barriers (B writes
+// into arrays the peers' last phase-A launch reads; C reads what every peer's B wrote).
+bf_status_t apply_chunk_peer(bf_plan_s* p, const std::vector<Step>& st, size_t ex, const std::vector<float2*>& ws,
+                             const float2* Fc, int64_t ldf, float2* Gc, int64_t ldg, int nv, cudaStream_t s)
+{
+    const int nsh = int(p->sh.size());
+    const int64_t arr = p->nloc() * p->d.R * nv;
+    std::vector<int> cur(nsh, 0);
+    for (int i = 0; i < nsh; i++) {   // (A)
+        const int64_t off = (p->mode == BF_SHARD_EMULATED) ? int64_t(i) * p->nloc() : 0;
+        bf_status_t r = run_steps(p, p->sh[i], st, 0, ex - 1, Fc + off, ldf, nullptr, ldg, nv, cur[i], false, ws[i], s);
+        if (r != BF_OK) return r;
+    }
+    bf_status_t r = nccl_barrier(p, s);
+    if (r != BF_OK) return r;
+    const int c = cur[0];   // every shard runs the same schedule: the same array parity
+    int lb = 0;
+    while ((int64_t(1) << lb) < p->nloc() / p->world) lb++;
+    for (int i = 0; i < nsh; i++) {   // (B)
+        bfs::PeerOut po{};
+        po.on = 1;
+        po.lb = lb;
+        po.src = (p->mode == BF_SHARD_EMULATED) ? i : p->rank;
+        for (int d = 0; d < p->world; d++) po.dst[d] = p->peer_ws[d] + (1 - c) * arr;
+        int ci = cur[i];
+        if ((r = run_steps(p, p->sh[i], st, ex - 1, ex, nullptr, ldf, nullptr, ldg, nv, ci, false, ws[i], s, &po)) !=
+            BF_OK)
+            return r;
+        cur[i] = ci;
+    }
+    if ((r = nccl_barrier(p, s)) != BF_OK) return r;
+    for (int i = 0; i < nsh; i++) {   // (C)
+        const int64_t off = (p->mode == BF_SHARD_EMULATED) ? int64_t(i) * p->nloc() : 0;
+        int ci = cur[i];   // the receive array is the level-h output array of this shard
+        if ((r = run_steps(p, p->sh[i], st, ex + 1, st.size(), nullptr, ldf, Gc + off, ldg, nv, ci, true, ws[i], s)) !=
+            BF_OK)
+            return r;
     }
     return BF_OK;
 }
@@ -458,6 +529,11 @@ bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, in
         }
         size_t ex = 0;
         while (st[ex].kind != Step::EXCHANGE) ex++;
+        if (p->exchange_peer && ws0 == p->sh[0].ws && ex >= 2 && st[ex - 1].kind != Step::S0) {
+            bf_status_t r = apply_chunk_peer(p, st, ex, ws, Fc, ldf, Gc, ldg, nv, s);
+            if (r != BF_OK) return r;
+            continue;
+        }
         // rows of shard i: emulated plans take the full F/G (shard i at row offset i N/G), NCCL plans the
         // local rows
         int cur = 0;
@@ -896,12 +972,80 @@ bf_status_t bf_debug_band_trace(int64_t* out, int32_t n)
     return e == cudaSuccess ? BF_OK : cuda_fail(e, "band trace");
 }
 
+namespace {
+// Fused-exchange destinations: each shard's workspace base.  Emulated shards share the device; for one
+// shard per GPU the plans exchange CUDA IPC handles of their workspaces (NCCL send/recv of the 64-byte
+// handles) and map the peers' workspaces (NVLink peer access).  Collective for NCCL plans.
+bf_status_t setup_peer_exchange(bf_plan_s* p)
+{
+    DeviceGuard g(p->device);
+    if (p->mode == BF_SHARD_EMULATED) {
+        for (int i = 0; i < p->world; i++) p->peer_ws[i] = p->sh[i].ws;
+        return BF_OK;
+    }
+    if (p->peer_ws[p->rank]) return BF_OK;   // already mapped
+    cudaError_t e;
+    if (!p->bar_buf && (e = cudaMalloc(&p->bar_buf, 2 * size_t(p->world))) != cudaSuccess) return cuda_fail(e, "barrier");
+    cudaMemset(p->bar_buf, 0, 2 * size_t(p->world));
+    if (p->world == 1) {
+        p->peer_ws[0] = p->sh[0].ws;
+        return BF_OK;
+    }
+    std::vector<cudaIpcMemHandle_t> hs(p->world);
+    if ((e = cudaIpcGetMemHandle(&hs[p->rank], p->sh[0].ws)) != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    char* hb = nullptr;
+    const size_t hsz = sizeof(cudaIpcMemHandle_t);
+    if ((e = cudaMalloc(&hb, hsz * p->world)) != cudaSuccess) return cuda_fail(e, "handle buffer");
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaMemcpyAsync(hb + hsz * p->rank, &hs[p->rank], hsz, cudaMemcpyHostToDevice, s);
+    Nccl& n = nccl();
+    ncclResult_t r = n.GroupStart();
+    for (int peer = 0; peer < p->world && !r; peer++) {
+        if (peer == p->rank) continue;
+        if ((r = n.Send(hb + hsz * p->rank, hsz, kNcclUint8, peer, p->comm, s))) break;
+        r = n.Recv(hb + hsz * peer, hsz, kNcclUint8, peer, p->comm, s);
+    }
+    ncclResult_t r2 = n.GroupEnd();
+    cudaMemcpyAsync(hs.data(), hb, hsz * p->world, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    cudaFree(hb);
+    if (r || r2) return nccl_fail(r ? r : r2, "IPC handle exchange");
+    if (e != cudaSuccess) return cuda_fail(e, "IPC handle exchange");
+    for (int d = 0; d < p->world; d++) {
+        if (d == p->rank) {
+            p->peer_ws[d] = p->sh[0].ws;
+            continue;
+        }
+        void* ptr = nullptr;
+        if ((e = cudaIpcOpenMemHandle(&ptr, hs[d], cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess)
+            return cuda_fail(e, "cudaIpcOpenMemHandle");
+        p->peer_ws[d] = static_cast<float2*>(ptr);
+        p->peer_ipc[d] = true;
+    }
+    return BF_OK;
+}
+}  // namespace
+
 bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
     if (option == BF_OPT_TENSOR_CORES) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_TENSOR_CORES takes 0 or 1");
         p->tensor_cores = value != 0;
+        return BF_OK;
+    }
+    if (option == BF_OPT_EXCHANGE) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_EXCHANGE takes 0 or 1");
+        if (value == 1) {
+            if (p->mode == BF_SHARD_NONE) return fail(BF_ERR_NOT_SUPPORTED, "the fused exchange needs a sharded plan");
+            if (p->world > bfs::kMaxShards) return fail(BF_ERR_NOT_SUPPORTED, "more than %d shards", bfs::kMaxShards);
+            if (p->d.h == p->d.l0) return fail(BF_ERR_NOT_SUPPORTED, "no transfer level produces level h (h == l0)");
+            bf_status_t st = setup_peer_exchange(p);
+            if (st != BF_OK) return st;
+        }
+        p->exchange_peer = value != 0;
         return BF_OK;
     }
     if (option == BF_OPT_BAND_TRACE_J0) {

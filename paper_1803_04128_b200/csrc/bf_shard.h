@@ -13,6 +13,7 @@
 // source q) as [q][a' < 2^(h-g)][b_l < 2^(h-g)], b = q 2^(h-g) + b_l.
 #pragma once
 #include <cstdint>
+#include <cuda_runtime.h>
 
 #if defined(__CUDACC__)
 #define BF_HD __host__ __device__ __forceinline__
@@ -40,5 +41,27 @@ BF_HD int64_t first_half_global(int64_t loc, int LN, int l, int g, int q)
 
 // Global pair index of second-half local pair `loc` of rank q at level l.
 BF_HD int64_t second_half_global(int64_t loc, int LN, int g, int q) { return (int64_t(q) << (LN - g)) + loc; }
+
+// Fused exchange (peer stores): the launch that produces level h writes each output pair straight into
+// its destination shard's receive array instead of its own send buffer.  Local first-half pair p goes to
+// shard d = p >> lb (blocks of 2^lb pairs) at receive position src 2^lb + (p mod 2^lb) (the layout
+// recv_index reads).  dst[d] are device pointers (same device for emulated shards, CUDA-IPC-mapped peer
+// memory over NVLink for one shard per GPU).
+constexpr int kMaxShards = 16;
+struct PeerOut {
+    float2* dst[kMaxShards];
+    int lb;    // log2 pairs per destination block
+    int src;   // this shard
+    int on;    // 0: ordinary output array
+};
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ float2* pair_out(float2* out, const PeerOut& po, int64_t p, int R, int nv)
+{
+    if (!po.on) return out + p * R * int64_t(nv);
+    const int64_t d = p >> po.lb, off = (p & ((int64_t(1) << po.lb) - 1)) + (int64_t(po.src) << po.lb);
+    return po.dst[d] + off * R * int64_t(nv);
+}
+#endif
 
 }  // namespace bfs

@@ -728,7 +728,7 @@ struct BandTC {
 template <int R>
 __global__ void __launch_bounds__(384, 1)
     band_tc_kernel(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ W1,
-                   const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg)
+                   const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg, const bfs::PeerOut po)
 {
     using C = BandTC<R>;
     extern __shared__ __align__(128) uint8_t sm_band[];
@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                     for (int e = 0; e < 2; e++) {
                         const int64_t p = (((a0 << 2) + 2 * u + e) << shg) + bq;
-                        float2* o = out + p * R * int64_t(nv) + vg;
+                        float2* o = bfs::pair_out(out, po, p, R, nv) + vg;
 #pragma unroll
                         for (int t = 0; t < R; t++)
                             o[int64_t(t) * nv] = make_float2(d[u][e * C::SC + 2 * t], d[u][e * C::SC + 2 * t + 1]);
@@ -1001,7 +1001,7 @@ struct Band2P {
 template <int R>
 __global__ void __launch_bounds__(512, 1)
     band_tc2p_kernel(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ W1,
-                     const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg)
+                     const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg, const bfs::PeerOut po)
 {
     using C = BandTC<R>;
     using Q = Band2P<R>;
@@ -1268,7 +1268,7 @@ __global__ void __launch_bounds__(512, 1)
 
 template <int R>
 static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                              cudaStream_t s, int rh, int rhg)
+                              cudaStream_t s, int rh, int rhg, const bfs::PeerOut& po)
 {
     using C = BandTC<R>;
     const int64_t groups = d.N >> 2;
@@ -1278,14 +1278,14 @@ static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, floa
             auto kern = band_tc2p_kernel<R>;
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
             if (e != cudaSuccess) return e;
-            kern<<<grid, 512, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg);
+            kern<<<grid, 512, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
             return cudaGetLastError();
         }
     }
     auto kern = band_tc_kernel<R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
-    kern<<<grid, 384, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg);
+    kern<<<grid, 384, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
     return cudaGetLastError();
 }
 
@@ -1301,13 +1301,14 @@ bool band_tc_supported(const Dims& d, int nv)
 }
 
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh, int rhg)
+                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po)
 {
+    const bfs::PeerOut pz = po ? *po : bfs::PeerOut{};
     switch (d.R) {
-    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg);
-    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg);
-    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg);
-    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg);
+    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg, pz);
+    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg, pz);
+    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg, pz);
+    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg, pz);
     default: return cudaErrorInvalidValue;
     }
 }

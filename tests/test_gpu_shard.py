@@ -91,3 +91,46 @@ def test_cfg5_index_sharded_8_emulated():
     assert np.array_equal(G, ref)
     R = oracle.bf_apply(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank, F[:, [5]])
     assert oracle.rel_l2(G[:, 5].astype(np.complex128), R[:, 0]) <= 1e-5
+
+
+@pytest.mark.parametrize("kernel,amp,LN,l0,r,nrhs,chunk,worlds", CASES)
+def test_fused_exchange_equals_copy_exchange(kernel, amp, LN, l0, r, nrhs, chunk, worlds):
+    """BF_OPT_EXCHANGE = 1: the launch producing level h stores every output pair straight into its
+    destination shard's receive array (no separate exchange step).  Same arithmetic, so the result equals
+    the copy-exchange (and hence the unsharded) result bitwise."""
+    k = bf.fio(kernel, amp, LN, l0, r)
+    F = W.rhs(1 << LN, nrhs, 400 + LN)
+    ref = _apply(bf.Plan.build_fio(k, max_nrhs_chunk=chunk), F)
+    for world in worlds:
+        plan = bf.Plan.build_fio_emulated(k, world, max_nrhs_chunk=chunk)
+        plan.set_option(bf.BF_OPT_EXCHANGE, 1)
+        plan.set_timing(True)
+        G = _apply(plan, F)
+        t = plan.timing()
+        plan.destroy()
+        assert t["exchange"][1] == 0, t                      # no separate exchange launch
+        assert np.array_equal(G, ref), f"world={world}"
+
+
+def test_fused_exchange_option_validation():
+    k = bf.fio(W.K_FIO, W.A_CFG1, 12, 4, 10)
+    plan = bf.Plan.build_fio(k, max_nrhs_chunk=2)
+    with pytest.raises(bf.BFError):
+        plan.set_option(bf.BF_OPT_EXCHANGE, 1)               # not a sharded plan
+    plan.destroy()
+    plan = bf.Plan.build_fio_emulated(bf.fio(W.K_FIO, W.A_CFG1, 12, 4, 10), 2, max_nrhs_chunk=1)
+    with pytest.raises(bf.BFError):
+        plan.set_option(bf.BF_OPT_EXCHANGE, 2)                # not a mode
+    plan.set_option(bf.BF_OPT_EXCHANGE, 1)
+    plan.set_option(bf.BF_OPT_EXCHANGE, 0)
+    plan.destroy()
+
+
+def test_nccl_world1_fused_exchange():
+    k = bf.fio(W.K_FIO, W.A_CFG1, 14, 5, 10)
+    F = W.rhs(1 << 14, 6, 5)
+    ref = _apply(bf.Plan.build_fio(k, max_nrhs_chunk=6), F)
+    plan = bf.Plan.build_fio_sharded(k, 0, 1, bf.nccl_unique_id(), max_nrhs_chunk=6)
+    plan.set_option(bf.BF_OPT_EXCHANGE, 1)
+    assert np.array_equal(_apply(plan, F), ref)
+    plan.destroy()
