@@ -187,7 +187,8 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        0: every stage runs the FP32 FFMA (SIMT) kernels.
  * Returns BF_ERR_INVALID_ARG for an unknown option or value. */
 #define BF_OPT_TENSOR_CORES 1
-/*   BF_OPT_BAND_PIPELINES 1 (default): the tensor-core band kernel runs one job at a time per SM;
+/*   BF_OPT_BAND_PIPELINES 1 (default): the level-by-level tensor-core band kernel (BF_OPT_BAND_COMPOSE = 0)
+ *                        runs one job at a time per SM;
  *                        2: jobs alternate between two TMEM pipelines where TMEM allows (r <= 10; measured
  *                        slower at cfg4).  Process-wide tuning knob. */
 #define BF_OPT_BAND_PIPELINES 2
@@ -203,6 +204,11 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        Not available when h == l0 or with a caller workspace (bf_apply_ex), where the
  *                        separate exchange is used. */
 #define BF_OPT_EXCHANGE 4
+/*   BF_OPT_BAND_COMPOSE  1 (default): the tensor-core band applies its two transfer levels as one composed
+ *                        4 x 4 block operator per group of 4 pairs (C = W_{l+1} W_l per block path, formed
+ *                        in FP32 on chip; same MAC count, one accumulation chain per tile);
+ *                        0: the level-by-level band kernels (selected by BF_OPT_BAND_PIPELINES). */
+#define BF_OPT_BAND_COMPOSE 5
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band

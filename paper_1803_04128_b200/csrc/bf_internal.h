@@ -55,7 +55,8 @@ cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, flo
 // Band of 2 transfer levels on the tensor cores (bf_tc.cu): same contract as launch_band with K = 2.
 bool band_tc_supported(const Dims& d, int nv);
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr);
+                           cudaStream_t s, int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr,
+                           bool compose = true);
 
 // Diagnostic: SM-clock timeline of the last band_tc launch (CTA 0, first 64 jobs x 12 events).
 cudaError_t band_trace(long long* out, int n);

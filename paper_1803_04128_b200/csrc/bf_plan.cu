@@ -153,6 +153,7 @@ struct bf_plan_s {
     float2* dG = nullptr;
     cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the pipelined bf_apply_host
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
+    bool band_compose = true;  // BF_OPT_BAND_COMPOSE
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -425,7 +426,7 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                 const float2* W[2] = {sh.xfer[stp.l_first - p->d.l0 - 1],
                                       stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
                 if (stp.K == 2 && p->tensor_cores && bfk::band_tc_supported(dl, nv))
-                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po);
+                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po, p->band_compose);
                 return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
             }
             case Step::SL:
@@ -1046,6 +1047,11 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
             if (st != BF_OK) return st;
         }
         p->exchange_peer = value != 0;
+        return BF_OK;
+    }
+    if (option == BF_OPT_BAND_COMPOSE) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_COMPOSE takes 0 or 1");
+        p->band_compose = value != 0;
         return BF_OK;
     }
     if (option == BF_OPT_BAND_TRACE_J0) {

@@ -1266,13 +1266,272 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
+// =============================================================================================
+// Composed two-level band (the default tensor-core band).  The two transfer levels of a band map a
+// group of 4 input pairs to 4 output pairs, and each output pair reaches each input pair through
+// exactly one pair of the middle level (eqn:2 P:748-752 / eqn:3 P:780-785 applied twice), so the band
+// is ONE dense 4 x 4 block operator per group,
+//     C[o][i] = W2[o][.., s'] W1[(s', u')][.., s]       (o = 2u' + e', i = 2s' + s, r x r complex blocks)
+// with the same 16 r^2 complex MACs per vector and group as the two levels applied one after the other.
+// The weight warps form C per group from the two levels' compact blocks (FP32; 16 r^3 complex MACs per
+// group, reused by every vector tile of the group) and write it real-embedded and split hi/lo as one
+// K = N = 8r B tile; per job the tensor pipe then runs a single accumulation chain (3 passes x r K-steps,
+// N = 8r) and the level-1 drain / re-split of band_tc_kernel disappears.
+// Warps: 0-3 split the raw rows into A (TMEM), 4-11 epilogue (lane quadrant warp % 4, output half
+// (warp - 4) / 4), 12 loader, 13 MMA issuer, 14-15 weights (compose one group ahead).
+// =============================================================================================
+template <int R>
+struct BandCmp {
+    static constexpr int P = 4;
+    static constexpr int SC = 2 * R;                                  // real columns of one pair slot
+    static constexpr int KB = P * SC;                                 // MMA K = N = 8r
+    static constexpr int NB = KB;
+    static constexpr int ACOLS = 2 * KB;                              // A buffer: hi at +0, lo at +KB
+    static constexpr int NABUF = (2 * ACOLS + 2 * NB <= 512) ? 2 : 1;
+    static constexpr int NDBUF = (NABUF * ACOLS + 2 * NB <= 512) ? 2 : 1;
+    static constexpr int D_OFF = NABUF * ACOLS;
+    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + NDBUF * NB>();
+    static constexpr uint32_t RAW = uint32_t(P) * R * 128 * 8;       // raw rows of one vector tile
+    static constexpr uint32_t BLK = 2 * R * R;                        // complex entries of one compact block
+    static constexpr uint32_t WST = 2 * P * BLK * 8;                  // staged compact blocks, both levels
+    static constexpr uint32_t WT = uint32_t(NB) * KB * 4;             // one B tile (hi or lo)
+    static constexpr uint32_t WSET = 2 * WT;
+    static constexpr uint32_t OFF_WST = 2 * RAW;                      // two staging buffers (prefetch)
+    static constexpr uint32_t OFF_W = OFF_WST + 2 * WST;
+    static constexpr int NWBUF = (size_t(OFF_W) + 2 * size_t(WSET) <= 232448 - 1024) ? 2 : 1;
+    static constexpr size_t SMEM = size_t(OFF_W) + NWBUF * size_t(WSET);
+    static constexpr int ITEMS = P * P * R;                           // (o, i, t') compose items
+    static_assert(KB % 16 == 0 && D_OFF + NDBUF * NB <= 512 && OFF_W % 128 == 0 && WT % 128 == 0 &&
+                      SMEM <= 232448 - 1024, "composed band shape");
+};
+
+template <int R>
+__global__ void __launch_bounds__(512, 1)
+    band_cmp_kernel(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ W1,
+                    const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg, const bfs::PeerOut po)
+{
+    using C = BandCmp<R>;
+    extern __shared__ __align__(128) uint8_t sm_cmp[];
+    __shared__ uint64_t raw_full[2], raw_empty[2], a_ready[2], a_free[2], d_full[2], d_free[2], w_full[2], w_free[2];
+    __shared__ uint64_t wst_full[2];
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t N = int64_t(1) << LN;
+    const int lin = l_first - 1, shg = LN - lin - 2;
+    const int64_t ngroups = N >> 2;
+    const int nvt = (nv + 127) / 128;
+    const int nit = int((ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const int njobs = nit * nvt;
+
+    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&raw_full[i], 1);
+            tc::mbar_init(&raw_empty[i], 128);
+            tc::mbar_init(&a_ready[i], 128);
+            tc::mbar_init(&a_free[i], 1);
+            tc::mbar_init(&d_full[i], 1);
+            tc::mbar_init(&d_free[i], 256);
+            tc::mbar_init(&w_full[i], 64);
+            tc::mbar_init(&w_free[i], 1);
+            tc::mbar_init(&wst_full[i], 1);
+        }
+        tc::mbar_fence_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base;
+
+    if (warp < 4) {
+        // ---- split: raw rows -> A buffer (TMEM), lane = vector ----
+        const uint32_t lb = uint32_t(warp * 32) << 16;
+        for (int J = 0; J < njobs; J++) {
+            const int e = J & 1;
+            tc::mbar_wait(&raw_full[e], uint32_t(J >> 1) & 1);
+            const int ab = J % C::NABUF, use = J / C::NABUF;
+            if (use > 0) tc::mbar_wait(&a_free[ab], uint32_t(use - 1) & 1);
+            tc::fence_after_sync();
+            const float2* rd = reinterpret_cast<const float2*>(sm_cmp + e * C::RAW);
+#pragma unroll 1
+            for (int s = 0; s < C::P; s++) {
+                float hi[C::SC], lo[C::SC];
+#pragma unroll
+                for (int t = 0; t < R; t++) {
+                    const float2 x = rd[(s * R + t) * 128 + tid];
+                    tc::split(x.x, hi[2 * t], lo[2 * t]);
+                    tc::split(x.y, hi[2 * t + 1], lo[2 * t + 1]);
+                }
+                const uint32_t ta = tmem + lb + uint32_t(ab * C::ACOLS + s * C::SC);
+                tc::tmem_st_cols<C::SC>(ta, hi);
+                tc::tmem_st_cols<C::SC>(ta + C::KB, lo);
+            }
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&raw_empty[e]);
+            tc::mbar_arrive(&a_ready[ab]);
+        }
+    } else if (warp < 12) {
+        // ---- epilogue: drain half of the accumulator row (2 output pairs) and store it ----
+        const int q = warp & 3, hf = (warp - 4) >> 2;
+        const int v = q * 32 + lane;
+        const uint32_t lb = uint32_t(q * 32) << 16;
+        for (int J = 0; J < njobs; J++) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+            const int db = J % C::NDBUF;
+            tc::mbar_wait(&d_full[db], uint32_t(J / C::NDBUF) & 1);
+            tc::fence_after_sync();
+            float d[2 * C::SC];
+            tc::tmem_ld_cols<2 * C::SC>(tmem + lb + uint32_t(C::D_OFF + db * C::NB + hf * 2 * C::SC), d);
+            tc::tmem_wait_ld();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&d_free[db]);
+            const int vg = vt * 128 + v;
+            if (vg < nv) {
+                const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+#pragma unroll
+                for (int oo = 0; oo < 2; oo++) {
+                    const int64_t p = (((a0 << 2) + 2 * hf + oo) << shg) + bq;
+                    float2* o = bfs::pair_out(out, po, p, R, nv) + vg;
+#pragma unroll
+                    for (int t = 0; t < R; t++)
+                        o[int64_t(t) * nv] = make_float2(d[oo * C::SC + 2 * t], d[oo * C::SC + 2 * t + 1]);
+                }
+            }
+        }
+    } else if (warp == 12) {
+        // ---- loader: the group's 4 r raw coefficient rows of one vector tile (1-D bulk copies) ----
+        if (lane == 0) {
+            for (int J = 0; J < njobs; J++) {
+                const int it = int(unsigned(J) / unsigned(nvt));
+                const int vt = J - it * nvt;
+                const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+                const int e = J & 1;
+                if (J >= 2) tc::mbar_wait(&raw_empty[e], uint32_t((J >> 1) - 1) & 1);
+                const int v0 = vt * 128, vw = min(128, nv - v0);
+                const uint32_t row_bytes = uint32_t(vw) * 8;
+                tc::mbar_arrive_expect_tx(&raw_full[e], C::P * R * row_bytes);
+                const int64_t pin = rh ? bfs::recv_index(g * C::P, rh, rhg) : g * C::P;   // P pairs contiguous
+                uint8_t* dst = sm_cmp + e * C::RAW;
+                for (int row = 0; row < C::P * R; row++)
+                    tc::bulk_g2s(dst + row * 128 * 8, in + (pin * R + row) * int64_t(nv) + v0, row_bytes, &raw_full[e]);
+            }
+        }
+    } else if (warp == 13) {
+        // ---- MMA issuer (whole warp, one elected lane issues): one chain of 3 x (8r / 8) MMAs per job ----
+        constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
+        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
+        const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_cmp + C::OFF_W), LBO_B);
+        for (int J = 0; J < njobs; J++) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int wb = it % C::NWBUF, ab = J % C::NABUF, db = J % C::NDBUF;
+            if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
+            tc::mbar_wait(&a_ready[ab], uint32_t(J / C::NABUF) & 1);
+            if (J >= C::NDBUF) tc::mbar_wait(&d_free[db], uint32_t(J / C::NDBUF - 1) & 1);
+            tc::fence_after_sync();
+            const uint32_t d = tmem + uint32_t(C::D_OFF + db * C::NB);
+            const uint32_t ahi = tmem + uint32_t(ab * C::ACOLS);
+            const uint64_t bhi = tc::desc_add(dW, wb * C::WSET);
+#pragma unroll
+            for (int qq = 0; qq < 3; qq++) {
+                const int pass = kPassOrder[qq];
+                const uint32_t a = ahi + (pass == 1 ? C::KB : 0);
+                const uint64_t b = pass == 2 ? tc::desc_add(bhi, C::WT) : bhi;
+#pragma unroll
+                for (int ks = 0; ks < C::KB / 8; ks++)
+                    tc::mma_tf32_ts_warp(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc, (qq | ks) ? 1u : 0u);
+            }
+            tc::commit_warp(&d_full[db]);
+            tc::commit_warp(&a_free[ab]);
+            if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
+            __syncwarp();
+        }
+    } else {
+        // ---- weights (warps 14-15): stage both levels' compact blocks (bulk copies, one group ahead),
+        //      compose, embed + split into the B tile ----
+        const int wt = tid - 448;
+        // block (m, u, e) of group g: level 1 (m = 0) pair p1(u, e), level 2 (m = 1) pair p2(u, e)
+        auto stage_group = [&](int it, int sb) {
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+            uint8_t* dst = sm_cmp + C::OFF_WST + sb * C::WST;
+            tc::mbar_arrive_expect_tx(&wst_full[sb], C::WST);
+            for (int b = 0; b < 8; b++) {
+                const int m = b >> 2, u = (b >> 1) & 1, e = b & 1;
+                const int64_t p = m == 0 ? ((((a0 << 1) + e) << (LN - lin - 1)) + (bq << 1) + u)
+                                         : ((((a0 << 2) + 2 * u + e) << shg) + bq);
+                tc::bulk_g2s(dst + b * C::BLK * 8, (m == 0 ? W1 : W2) + p * C::BLK, C::BLK * 8, &wst_full[sb]);
+            }
+        };
+        if (wt == 0 && nit > 0) stage_group(0, 0);
+        for (int it = 0; it < nit; it++) {
+            const int wb = it % C::NWBUF, sb = it & 1;
+            if (wt == 0 && it + 1 < nit) stage_group(it + 1, sb ^ 1);   // its buffer was released by the bar.sync
+            tc::mbar_wait(&wst_full[sb], uint32_t(it >> 1) & 1);
+            const float2* st = reinterpret_cast<const float2*>(sm_cmp + C::OFF_WST + sb * C::WST);
+            if (it >= C::NWBUF) tc::mbar_wait(&w_free[wb], uint32_t(it / C::NWBUF - 1) & 1);
+            uint8_t* th = sm_cmp + C::OFF_W + wb * C::WSET;
+            uint8_t* tl = th + C::WT;
+            for (int item = wt; item < C::ITEMS; item += 64) {
+                const int tp = item % R, oi = item / R, o = oi >> 2, i = oi & 3;
+                const int up = o >> 1, sp = i >> 1, s = i & 1;
+                const float2* L2 = st + (4 + o) * C::BLK + sp * R * R + tp;   // W2[p2(o)][(s' R + j') R + t']
+                const float2* L1 = st + (sp * 2 + up) * C::BLK + s * R * R;   // W1[p1(s', u')][(s R + j) R + j']
+                float2 w2[R];
+#pragma unroll
+                for (int jp = 0; jp < R; jp++) w2[jp] = L2[jp * R];
+#pragma unroll 2
+                for (int j = 0; j < R; j++) {
+                    float2 c = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int jp = 0; jp < R; jp++) {
+                        const float2 w1 = L1[j * R + jp];
+                        c.x = fmaf(w2[jp].x, w1.x, fmaf(-w2[jp].y, w1.y, c.x));
+                        c.y = fmaf(w2[jp].x, w1.y, fmaf(w2[jp].y, w1.x, c.y));
+                    }
+                    float hr, lr, hi_, li;
+                    tc::split(c.x, hr, lr);
+                    tc::split(c.y, hi_, li);
+                    const int n = o * C::SC + 2 * tp, k = i * C::SC + 2 * j;
+                    const uint32_t o0 = tc::kmaj_off(n, k, C::NB), o1 = tc::kmaj_off(n + 1, k, C::NB);
+                    *reinterpret_cast<float2*>(th + o0) = make_float2(hr, -hi_);
+                    *reinterpret_cast<float2*>(tl + o0) = make_float2(lr, -li);
+                    *reinterpret_cast<float2*>(th + o1) = make_float2(hi_, hr);
+                    *reinterpret_cast<float2*>(tl + o1) = make_float2(li, lr);
+                }
+            }
+            tc::fence_proxy_async();
+            tc::mbar_arrive(&w_full[wb]);
+            asm volatile("bar.sync 1, 64;" ::: "memory");   // staging buffer sb free for group it + 2
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+    }
+}
+
 template <int R>
 static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                              cudaStream_t s, int rh, int rhg, const bfs::PeerOut& po)
+                              cudaStream_t s, int rh, int rhg, const bfs::PeerOut& po, bool compose)
 {
     using C = BandTC<R>;
     const int64_t groups = d.N >> 2;
     const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
+    if (compose) {
+        using CC = BandCmp<R>;
+        auto kern = band_cmp_kernel<R>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CC::SMEM));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, 512, CC::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
+        return cudaGetLastError();
+    }
     if constexpr (Band2P<R>::FITS) {
         if (!g_band_single_pipeline) {
             auto kern = band_tc2p_kernel<R>;
@@ -1301,14 +1560,14 @@ bool band_tc_supported(const Dims& d, int nv)
 }
 
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po)
+                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, bool compose)
 {
     const bfs::PeerOut pz = po ? *po : bfs::PeerOut{};
     switch (d.R) {
-    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg, pz);
-    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg, pz);
-    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg, pz);
-    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg, pz);
+    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg, pz, compose);
+    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg, pz, compose);
+    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg, pz, compose);
+    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg, pz, compose);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -145,6 +145,7 @@ def test_tc_band_two_pipeline_variant():
     LN, l0, r, nrhs = 14, 5, 10, 64          # two two-level bands (levels 6..9), nv = 128
     F = W.rhs(1 << LN, nrhs, 31)
     plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    plan.set_option(bf.BF_OPT_BAND_COMPOSE, 0)       # the level-by-level kernels
     with pytest.raises(bf.BFError):
         plan.set_option(bf.BF_OPT_BAND_PIPELINES, 3)
     G1 = _apply(plan, F)
@@ -157,3 +158,25 @@ def test_tc_band_two_pipeline_variant():
     assert np.array_equal(G1, G2)
     R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, :3])
     assert np.all(oracle.rel_l2(G2[:, :3].astype(np.complex128), R, axis=0) <= PARITY)
+
+
+@pytest.mark.parametrize("r,l0,LN,nrhs", [(6, 6, 14, 64), (8, 5, 14, 96), (10, 6, 16, 256), (12, 5, 14, 70)])
+def test_tc_band_composed(r, l0, LN, nrhs):
+    """Default band (BF_OPT_BAND_COMPOSE = 1): both levels of a band as one composed 4 x 4 block operator
+    per group, formed in FP32 on chip.  Checked against the oracle (which applies the levels one after
+    the other in FP64) and against the level-by-level tensor-core band (same algebra, other rounding)."""
+    F = W.rhs(1 << LN, nrhs, 40 + r)
+    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    assert any(k.startswith("xfer") for k in plan.info()["tc_classes"])
+    Gc = _apply(plan, F)
+    plan.set_option(bf.BF_OPT_BAND_COMPOSE, 0)
+    Gl = _apply(plan, F)
+    with pytest.raises(bf.BFError):
+        plan.set_option(bf.BF_OPT_BAND_COMPOSE, 2)
+    plan.destroy()
+    cols = [0, nrhs // 2, nrhs - 1]
+    R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, cols])
+    assert np.all(oracle.rel_l2(Gc[:, cols].astype(np.complex128), R, axis=0) <= PARITY)
+    d = oracle.rel_l2(Gc.astype(np.complex128), Gl.astype(np.complex128), axis=0)
+    assert np.all(d <= PATHS_AGREE), d.max()
+    assert not np.array_equal(Gc, Gl)                 # the composed kernel really ran

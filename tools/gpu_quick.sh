@@ -1,7 +1,7 @@
 # quick perf iteration: TC parity + band timeline + bench (no full suite)
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_tc.py -x -q > gpurun_out/pytest_tc.log 2>&1; PT=$?; echo "pytest_tc=$PT"; tail -2 gpurun_out/pytest_tc.log
-timeout 300 python tools/band_trace.py 18 > gpurun_out/trace.log 2>&1; echo "trace=$?"; sed -n '1p;22,30p;$p' gpurun_out/trace.log
+true
 timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench.log 2>&1; echo "bench=$?"
 tail -1 gpurun_out/bench.log | python -c "
 import json,sys
