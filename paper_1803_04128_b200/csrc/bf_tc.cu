@@ -21,7 +21,9 @@
 // versus 3.7e-7 when the chain is cut every 12 MMAs and the partial sums are added in
 // FP32 registers).  Hence N = 128 tiles, accumulation chains of <= 24 MMAs (at most 8 of them
 // the large Ahi Bhi products, issued last) and FP32 register sums across chains here.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <cstdint>
 
 #include "bf_internal.h"
@@ -58,6 +60,30 @@ __device__ __forceinline__ float embed(float2 w, int cp, int c)
 }
 
 }  // namespace
+
+// Tensor map of a coefficient array viewed as a 2-D FP32 tensor [rows][2 nv] (row = (pair, t), nv vectors of
+// 8 bytes), box = 2 * 128 floats x box_rows rows: one TMA request moves a job's rows of one vector tile.
+// The driver entry point is resolved once through the runtime (the library links no libcuda).
+static cudaError_t make_rows_tmap(CUtensorMap* m, const float2* base, int64_t rows, int nv, int box_rows)
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {cuuint64_t(2 * nv), cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {cuuint64_t(nv) * 8};
+    const cuuint32_t box[2] = {256, cuuint32_t(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 
 // =============================================================================================
 // Expanded leaf weights (plan finalization)
@@ -444,7 +470,7 @@ struct SLTC {
 
 template <int R, int N0, int NA, int KP>
 __global__ void __launch_bounds__(448, 1)
-    sl_tc_kernel(const float2* __restrict__ in, const float* __restrict__ Ux, const float2* __restrict__ ampa,
+    sl_tc_kernel(const __grid_constant__ CUtensorMap tin, const float* __restrict__ Ux, const float2* __restrict__ ampa,
                  float2* __restrict__ G, int64_t ldg, int LN, int nv, int nvt)
 {
     using C = SLTC<R, N0, NA, KP>;
@@ -492,18 +518,17 @@ __global__ void __launch_bounds__(448, 1)
                 const int jl = gch / C::NCH, ch = gch - jl * C::NCH;
                 const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
                 const int64_t a = job / unsigned(nvt);
-                const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
+                const int v0 = int(job % unsigned(nvt)) * 128;
                 const int e = gch % C::NR, use = gch / C::NR;
                 if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
                 tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
                 tc::bulk_g2s(opB(e, 0), Ux + (a * C::NCH + ch) * 2 * (C::BT / 4), 2 * C::BT, &b_full[e]);
                 if (use > 0) tc::mbar_wait(&raw_empty[e], (use - 1) & 1);
-                const uint32_t row_bytes = uint32_t(vw) * 8;
-                tc::mbar_arrive_expect_tx(&raw_full[e], KP * R * row_bytes);
+                // the chunk's KP R coefficient rows of this vector tile: one 2-D tensor copy (whole box, a
+                // ragged tile zero-filled); per-row 1-D copies measured ~85 clk each to issue
+                tc::mbar_arrive_expect_tx(&raw_full[e], C::RAW);
                 const int64_t p0 = a * N0 + int64_t(ch) * KP;
-                for (int row = 0; row < KP * R; row++)
-                    tc::bulk_g2s(raw(e) + row * 128 * 8, in + (p0 * R + row) * int64_t(nv) + v0, row_bytes,
-                                 &raw_full[e]);
+                tc::tma_load_2d(raw(e), &tin, 2 * v0, int(p0 * R), &raw_full[e]);
             }
         }
     } else if (warp == 13) {
@@ -638,7 +663,10 @@ static cudaError_t sl_tc_go(const Dims& d, const float2* in, const float* Ux, co
     const int nvt = (nv + 127) / 128;
     const int64_t jobs = (d.N / N0) * nvt;
     const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
-    kern<<<grid, 448, C::SMEM, s>>>(in, Ux, ampa, G, ldg, d.LN, nv, nvt);
+    CUtensorMap tin;
+    e = make_rows_tmap(&tin, in, d.N * R, nv, KP * R);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 448, C::SMEM, s>>>(tin, Ux, ampa, G, ldg, d.LN, nv, nvt);
     return cudaGetLastError();
 }
 
@@ -1291,28 +1319,37 @@ struct BandCmp {
     static constexpr int NDBUF = (NABUF * ACOLS + 2 * NB <= 512) ? 2 : 1;
     static constexpr int D_OFF = NABUF * ACOLS;
     static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + NDBUF * NB>();
-    static constexpr uint32_t RAW = uint32_t(P) * R * 128 * 8;       // raw rows of one vector tile
+    static constexpr uint32_t SLOT = uint32_t(R) * 128 * 8;          // raw rows of one pair, one vector tile
     static constexpr uint32_t BLK = 2 * R * R;                        // complex entries of one compact block
     static constexpr uint32_t WST = 2 * P * BLK * 8;                  // staged compact blocks, both levels
     static constexpr uint32_t WT = uint32_t(NB) * KB * 4;             // one B tile (hi or lo)
     static constexpr uint32_t WSET = 2 * WT;
-    static constexpr uint32_t OFF_WST = 2 * RAW;                      // two staging buffers (prefetch)
+    static constexpr size_t LIM = 232448 - 1024;
+    static constexpr int NWBUF = (8 * size_t(SLOT) + 2 * size_t(WST) + 2 * size_t(WSET) <= LIM) ? 2 : 1;
+    // raw ring of single-pair slots (freed one pair at a time, so more bytes stay in flight)
+    static constexpr int NQ_FIT = int((LIM - 2 * size_t(WST) - NWBUF * size_t(WSET)) / SLOT);
+#ifdef BF_BAND_NQ
+    static constexpr int NQ = NQ_FIT > BF_BAND_NQ ? BF_BAND_NQ : NQ_FIT;
+#else
+    static constexpr int NQ = NQ_FIT > 16 ? 16 : NQ_FIT;
+#endif
+    static constexpr uint32_t OFF_WST = uint32_t(NQ) * SLOT;          // two staging buffers (prefetch)
     static constexpr uint32_t OFF_W = OFF_WST + 2 * WST;
-    static constexpr int NWBUF = (size_t(OFF_W) + 2 * size_t(WSET) <= 232448 - 1024) ? 2 : 1;
     static constexpr size_t SMEM = size_t(OFF_W) + NWBUF * size_t(WSET);
-    static constexpr int ITEMS = P * P * R;                           // (o, i, t') compose items
-    static_assert(KB % 16 == 0 && D_OFF + NDBUF * NB <= 512 && OFF_W % 128 == 0 && WT % 128 == 0 &&
-                      SMEM <= 232448 - 1024, "composed band shape");
+    static constexpr int ITEMS = P * P * R * 2;                       // (o, i, t', j half) compose items
+    static_assert(KB % 16 == 0 && D_OFF + NDBUF * NB <= 512 && OFF_W % 128 == 0 && WT % 128 == 0 && NQ >= 8 &&
+                      SMEM <= LIM, "composed band shape");
 };
 
 template <int R>
 __global__ void __launch_bounds__(512, 1)
-    band_cmp_kernel(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ W1,
+    band_cmp_kernel(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ W1,
                     const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg, const bfs::PeerOut po)
 {
     using C = BandCmp<R>;
     extern __shared__ __align__(128) uint8_t sm_cmp[];
-    __shared__ uint64_t raw_full[2], raw_empty[2], a_ready[2], a_free[2], d_full[2], d_free[2], w_full[2], w_free[2];
+    __shared__ uint64_t slot_full[16], slot_empty[16];
+    __shared__ uint64_t a_ready[2], a_free[2], d_full[2], d_free[2], w_full[2], w_free[2];
     __shared__ uint64_t wst_full[2];
     __shared__ uint32_t tmem_base;
 
@@ -1326,9 +1363,11 @@ __global__ void __launch_bounds__(512, 1)
 
     if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
     if (tid == 0) {
+        for (int i = 0; i < C::NQ; i++) {
+            tc::mbar_init(&slot_full[i], 1);
+            tc::mbar_init(&slot_empty[i], 128);
+        }
         for (int i = 0; i < 2; i++) {
-            tc::mbar_init(&raw_full[i], 1);
-            tc::mbar_init(&raw_empty[i], 128);
             tc::mbar_init(&a_ready[i], 128);
             tc::mbar_init(&a_free[i], 1);
             tc::mbar_init(&d_full[i], 1);
@@ -1348,28 +1387,31 @@ __global__ void __launch_bounds__(512, 1)
         // ---- split: raw rows -> A buffer (TMEM), lane = vector ----
         const uint32_t lb = uint32_t(warp * 32) << 16;
         for (int J = 0; J < njobs; J++) {
-            const int e = J & 1;
-            tc::mbar_wait(&raw_full[e], uint32_t(J >> 1) & 1);
             const int ab = J % C::NABUF, use = J / C::NABUF;
             if (use > 0) tc::mbar_wait(&a_free[ab], uint32_t(use - 1) & 1);
             tc::fence_after_sync();
-            const float2* rd = reinterpret_cast<const float2*>(sm_cmp + e * C::RAW);
+            if (tid == 0) btrace(J, 1);
 #pragma unroll 1
             for (int s = 0; s < C::P; s++) {
+                const int k = J * C::P + s, q = k % C::NQ;
+                tc::mbar_wait(&slot_full[q], uint32_t(k / C::NQ) & 1);
+                if (tid == 0 && s == 0) btrace(J, 0);
+                const float2* rd = reinterpret_cast<const float2*>(sm_cmp + q * C::SLOT);
                 float hi[C::SC], lo[C::SC];
 #pragma unroll
                 for (int t = 0; t < R; t++) {
-                    const float2 x = rd[(s * R + t) * 128 + tid];
+                    const float2 x = rd[t * 128 + tid];
                     tc::split(x.x, hi[2 * t], lo[2 * t]);
                     tc::split(x.y, hi[2 * t + 1], lo[2 * t + 1]);
                 }
+                tc::mbar_arrive(&slot_empty[q]);   // the slot's values are in registers
                 const uint32_t ta = tmem + lb + uint32_t(ab * C::ACOLS + s * C::SC);
                 tc::tmem_st_cols<C::SC>(ta, hi);
                 tc::tmem_st_cols<C::SC>(ta + C::KB, lo);
             }
             tc::tmem_wait_st();
             tc::fence_before_sync();
-            tc::mbar_arrive(&raw_empty[e]);
+            if (tid == 0) btrace(J, 2);
             tc::mbar_arrive(&a_ready[ab]);
         }
     } else if (warp < 12) {
@@ -1384,6 +1426,7 @@ __global__ void __launch_bounds__(512, 1)
             const int db = J % C::NDBUF;
             tc::mbar_wait(&d_full[db], uint32_t(J / C::NDBUF) & 1);
             tc::fence_after_sync();
+            if (tid == 128) btrace(J, 5);
             float d[2 * C::SC];
             tc::tmem_ld_cols<2 * C::SC>(tmem + lb + uint32_t(C::D_OFF + db * C::NB + hf * 2 * C::SC), d);
             tc::tmem_wait_ld();
@@ -1401,24 +1444,27 @@ __global__ void __launch_bounds__(512, 1)
                         o[int64_t(t) * nv] = make_float2(d[oo * C::SC + 2 * t], d[oo * C::SC + 2 * t + 1]);
                 }
             }
+            if (tid == 128) btrace(J, 6);
         }
     } else if (warp == 12) {
-        // ---- loader: the group's 4 r raw coefficient rows of one vector tile (1-D bulk copies) ----
-        if (lane == 0) {
-            for (int J = 0; J < njobs; J++) {
-                const int it = int(unsigned(J) / unsigned(nvt));
-                const int vt = J - it * nvt;
-                const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
-                const int e = J & 1;
-                if (J >= 2) tc::mbar_wait(&raw_empty[e], uint32_t((J >> 1) - 1) & 1);
-                const int v0 = vt * 128, vw = min(128, nv - v0);
-                const uint32_t row_bytes = uint32_t(vw) * 8;
-                tc::mbar_arrive_expect_tx(&raw_full[e], C::P * R * row_bytes);
-                const int64_t pin = rh ? bfs::recv_index(g * C::P, rh, rhg) : g * C::P;   // P pairs contiguous
-                uint8_t* dst = sm_cmp + e * C::RAW;
-                for (int row = 0; row < C::P * R; row++)
-                    tc::bulk_g2s(dst + row * 128 * 8, in + (pin * R + row) * int64_t(nv) + v0, row_bytes, &raw_full[e]);
+        // ---- loader: the group's 4 r raw coefficient rows of one vector tile, one 2-D tensor copy per pair
+        //      (40 separate 1-KB bulk copies measured ~85 clk each to issue: the loader was the bottleneck) ----
+        for (int J = 0; J < njobs; J++) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+            const int64_t pin = rh ? bfs::recv_index(g * C::P, rh, rhg) : g * C::P;   // P pairs contiguous
+            for (int s = 0; s < C::P; s++) {
+                const int k = J * C::P + s, q = k % C::NQ;
+                if (k >= C::NQ) tc::mbar_wait(&slot_empty[q], uint32_t(k / C::NQ - 1) & 1);
+                if (lane == 0) {
+                    if (s == 0) btrace(J, 7);
+                    tc::mbar_arrive_expect_tx(&slot_full[q], C::SLOT);   // whole box (ragged tile: zero fill)
+                    tc::tma_load_2d(sm_cmp + q * C::SLOT, &tin, 2 * vt * 128, int((pin + s) * R), &slot_full[q]);
+                }
+                __syncwarp();
             }
+            if (lane == 0) btrace(J, 8);
         }
     } else if (warp == 13) {
         // ---- MMA issuer (whole warp, one elected lane issues): one chain of 3 x (8r / 8) MMAs per job ----
@@ -1430,9 +1476,11 @@ __global__ void __launch_bounds__(512, 1)
             const int vt = J - it * nvt;
             const int wb = it % C::NWBUF, ab = J % C::NABUF, db = J % C::NDBUF;
             if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
+            if (lane == 0) btrace(J, 11);
             tc::mbar_wait(&a_ready[ab], uint32_t(J / C::NABUF) & 1);
             if (J >= C::NDBUF) tc::mbar_wait(&d_free[db], uint32_t(J / C::NDBUF - 1) & 1);
             tc::fence_after_sync();
+            if (lane == 0) btrace(J, 3);
             const uint32_t d = tmem + uint32_t(C::D_OFF + db * C::NB);
             const uint32_t ahi = tmem + uint32_t(ab * C::ACOLS);
             const uint64_t bhi = tc::desc_add(dW, wb * C::WSET);
@@ -1449,6 +1497,7 @@ __global__ void __launch_bounds__(512, 1)
             tc::commit_warp(&a_free[ab]);
             if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
             __syncwarp();
+            if (lane == 0) btrace(J, 4);
         }
     } else {
         // ---- weights (warps 14-15): stage both levels' compact blocks (bulk copies, one group ahead),
@@ -1474,28 +1523,44 @@ __global__ void __launch_bounds__(512, 1)
             tc::mbar_wait(&wst_full[sb], uint32_t(it >> 1) & 1);
             const float2* st = reinterpret_cast<const float2*>(sm_cmp + C::OFF_WST + sb * C::WST);
             if (it >= C::NWBUF) tc::mbar_wait(&w_free[wb], uint32_t(it / C::NWBUF - 1) & 1);
+            if (wt == 0) btrace(int64_t(it) * nvt, 9);
             uint8_t* th = sm_cmp + C::OFF_W + wb * C::WSET;
             uint8_t* tl = th + C::WT;
+            // item = (o, i, t', half of j): R / 2 independent complex accumulators per thread (ILP), the
+            // L1 row pairs (j, j'), (j, j' + 1) as one 16-byte load
+            constexpr int H = R / 2;
+#pragma unroll 1
             for (int item = wt; item < C::ITEMS; item += 64) {
-                const int tp = item % R, oi = item / R, o = oi >> 2, i = oi & 3;
+                const int jh = item & 1, r2 = item >> 1;
+                const int tp = r2 % R, oi = r2 / R, o = oi >> 2, i = oi & 3;
                 const int up = o >> 1, sp = i >> 1, s = i & 1;
-                const float2* L2 = st + (4 + o) * C::BLK + sp * R * R + tp;   // W2[p2(o)][(s' R + j') R + t']
-                const float2* L1 = st + (sp * 2 + up) * C::BLK + s * R * R;   // W1[p1(s', u')][(s R + j) R + j']
-                float2 w2[R];
+                const float2* L2 = st + (4 + o) * C::BLK + sp * R * R + tp;              // W2[p2(o)][(s' R + j') R + t']
+                const float2* L1 = st + (sp * 2 + up) * C::BLK + s * R * R + jh * H * R;   // W1[p1(s', u')][(s R + j) R + j']
+                float2 c[H];
 #pragma unroll
-                for (int jp = 0; jp < R; jp++) w2[jp] = L2[jp * R];
-#pragma unroll 2
-                for (int j = 0; j < R; j++) {
-                    float2 c = make_float2(0.f, 0.f);
+                for (int jj = 0; jj < H; jj++) c[jj] = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int jp = 0; jp < R; jp++) {
-                        const float2 w1 = L1[j * R + jp];
-                        c.x = fmaf(w2[jp].x, w1.x, fmaf(-w2[jp].y, w1.y, c.x));
-                        c.y = fmaf(w2[jp].x, w1.y, fmaf(w2[jp].y, w1.x, c.y));
+                for (int jp = 0; jp < R; jp += 2) {
+                    const float2 wa = L2[jp * R], wb = L2[(jp + 1) * R];
+#pragma unroll
+                    for (int jj = 0; jj < H; jj++) {
+                        const float4 w1 = *reinterpret_cast<const float4*>(L1 + jj * R + jp);
+                        c[jj].x = fmaf(wa.x, w1.x, c[jj].x);
+                        c[jj].y = fmaf(wa.x, w1.y, c[jj].y);
+                        c[jj].x = fmaf(-wa.y, w1.y, c[jj].x);
+                        c[jj].y = fmaf(wa.y, w1.x, c[jj].y);
+                        c[jj].x = fmaf(wb.x, w1.z, c[jj].x);
+                        c[jj].y = fmaf(wb.x, w1.w, c[jj].y);
+                        c[jj].x = fmaf(-wb.y, w1.w, c[jj].x);
+                        c[jj].y = fmaf(wb.y, w1.z, c[jj].y);
                     }
+                }
+#pragma unroll
+                for (int jj = 0; jj < H; jj++) {
+                    const int j = jh * H + jj;
                     float hr, lr, hi_, li;
-                    tc::split(c.x, hr, lr);
-                    tc::split(c.y, hi_, li);
+                    tc::split(c[jj].x, hr, lr);
+                    tc::split(c[jj].y, hi_, li);
                     const int n = o * C::SC + 2 * tp, k = i * C::SC + 2 * j;
                     const uint32_t o0 = tc::kmaj_off(n, k, C::NB), o1 = tc::kmaj_off(n + 1, k, C::NB);
                     *reinterpret_cast<float2*>(th + o0) = make_float2(hr, -hi_);
@@ -1505,6 +1570,7 @@ __global__ void __launch_bounds__(512, 1)
                 }
             }
             tc::fence_proxy_async();
+            if (wt == 0) btrace(int64_t(it) * nvt, 10);
             tc::mbar_arrive(&w_full[wb]);
             asm volatile("bar.sync 1, 64;" ::: "memory");   // staging buffer sb free for group it + 2
         }
@@ -1529,7 +1595,10 @@ static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, floa
         auto kern = band_cmp_kernel<R>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CC::SMEM));
         if (e != cudaSuccess) return e;
-        kern<<<grid, 512, CC::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
+        CUtensorMap tin;
+        e = make_rows_tmap(&tin, in, d.N * R, nv, R);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, 512, CC::SMEM, s>>>(tin, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
         return cudaGetLastError();
     }
     if constexpr (Band2P<R>::FITS) {

@@ -264,6 +264,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// 2-D tiled tensor copy global -> shared (TMA engine, tensor map built on the host), completion counted in
+// bytes on `bar` (the whole box, out-of-bounds elements zero-filled).  c0 = innermost coordinate.
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
 // one lane of the (fully converged) warp
 __device__ __forceinline__ bool elect_one()
 {
