@@ -25,7 +25,8 @@ plan.apply(F, G, w.nrhs)
 torch.cuda.synchronize()
 print("kernel ms:", {k: round(v[0], 3) for k, v in plan.timing().items() if v[1]})
 plan.set_timing(False)
-plan.apply(F, G, w.nrhs)
+for _ in range(int(os.environ.get("BT_WARM", "1"))):   # BT_WARM > 1: trace inside a sustained (power-capped) run
+    plan.apply(F, G, w.nrhs)
 torch.cuda.synchronize()
 T = bf.debug_band_trace()   # the last band launch of the apply (second half)
 if mode:
