@@ -1337,6 +1337,11 @@ struct BandCmp {
     static constexpr uint32_t OFF_W = OFF_WST + 2 * WST;
     static constexpr size_t SMEM = size_t(OFF_W) + NWBUF * size_t(WSET);
     static constexpr int ITEMS = P * P * R * 2;                       // (o, i, t', j half) compose items
+#ifdef BF_BAND_SPLIT4
+    static constexpr int NSPLIT = 4;                                  // split warps (the rest of 0-11: epilogue)
+#else
+    static constexpr int NSPLIT = 8;
+#endif
     static_assert(KB % 16 == 0 && D_OFF + NDBUF * NB <= 512 && OFF_W % 128 == 0 && WT % 128 == 0 && NQ >= 8 &&
                       SMEM <= LIM, "composed band shape");
 };
@@ -1368,10 +1373,10 @@ __global__ void __launch_bounds__(512, 1)
             tc::mbar_init(&slot_empty[i], 128);
         }
         for (int i = 0; i < 2; i++) {
-            tc::mbar_init(&a_ready[i], 128);
+            tc::mbar_init(&a_ready[i], 32 * C::NSPLIT);
             tc::mbar_init(&a_free[i], 1);
             tc::mbar_init(&d_full[i], 1);
-            tc::mbar_init(&d_free[i], 256);
+            tc::mbar_init(&d_free[i], 32 * (12 - C::NSPLIT));
             tc::mbar_init(&w_full[i], 64);
             tc::mbar_init(&w_free[i], 1);
             tc::mbar_init(&wst_full[i], 1);
@@ -1383,16 +1388,20 @@ __global__ void __launch_bounds__(512, 1)
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base;
 
-    if (warp < 4) {
-        // ---- split: raw rows -> A buffer (TMEM), lane = vector ----
-        const uint32_t lb = uint32_t(warp * 32) << 16;
+    if (warp < C::NSPLIT) {
+        // ---- split: raw rows -> A buffer (TMEM), lane = vector; with 8 split warps each lane quadrant has two
+        //      warps, one per half of the group's 4 pair slots ----
+        const int qd = warp & 3, hs = warp >> 2;
+        const int v = qd * 32 + lane;
+        constexpr int SPW = C::P * 4 / C::NSPLIT;   // pair slots per split warp
+        const uint32_t lb = uint32_t(qd * 32) << 16;
         for (int J = 0; J < njobs; J++) {
             const int ab = J % C::NABUF, use = J / C::NABUF;
             if (use > 0) tc::mbar_wait(&a_free[ab], uint32_t(use - 1) & 1);
             tc::fence_after_sync();
             if (tid == 0) btrace(J, 1);
 #pragma unroll 1
-            for (int s = 0; s < C::P; s++) {
+            for (int s = hs * SPW; s < (hs + 1) * SPW; s++) {
                 const int k = J * C::P + s, q = k % C::NQ;
                 tc::mbar_wait(&slot_full[q], uint32_t(k / C::NQ) & 1);
                 if (tid == 0 && s == 0) btrace(J, 0);
@@ -1400,14 +1409,20 @@ __global__ void __launch_bounds__(512, 1)
                 float hi[C::SC], lo[C::SC];
 #pragma unroll
                 for (int t = 0; t < R; t++) {
-                    const float2 x = rd[t * 128 + tid];
+                    const float2 x = rd[t * 128 + v];
+#ifdef BF_EXP_NO_SPLIT
+                    hi[2 * t] = x.x; lo[2 * t] = 0.f; hi[2 * t + 1] = x.y; lo[2 * t + 1] = 0.f;
+#else
                     tc::split(x.x, hi[2 * t], lo[2 * t]);
                     tc::split(x.y, hi[2 * t + 1], lo[2 * t + 1]);
+#endif
                 }
                 tc::mbar_arrive(&slot_empty[q]);   // the slot's values are in registers
                 const uint32_t ta = tmem + lb + uint32_t(ab * C::ACOLS + s * C::SC);
+#ifndef BF_EXP_NO_TMEM_ST
                 tc::tmem_st_cols<C::SC>(ta, hi);
                 tc::tmem_st_cols<C::SC>(ta + C::KB, lo);
+#endif
             }
             tc::tmem_wait_st();
             tc::fence_before_sync();
@@ -1415,8 +1430,10 @@ __global__ void __launch_bounds__(512, 1)
             tc::mbar_arrive(&a_ready[ab]);
         }
     } else if (warp < 12) {
-        // ---- epilogue: drain half of the accumulator row (2 output pairs) and store it ----
-        const int q = warp & 3, hf = (warp - 4) >> 2;
+        // ---- epilogue: drain the accumulator row in halves of 2 output pairs and store them (8 epilogue warps:
+        //      one half each; 4 warps: both halves) ----
+        constexpr int HPW = 8 / (12 - C::NSPLIT);
+        const int q = warp & 3, hf0 = ((warp - C::NSPLIT) >> 2) * HPW;
         const int v = q * 32 + lane;
         const uint32_t lb = uint32_t(q * 32) << 16;
         for (int J = 0; J < njobs; J++) {
@@ -1426,25 +1443,35 @@ __global__ void __launch_bounds__(512, 1)
             const int db = J % C::NDBUF;
             tc::mbar_wait(&d_full[db], uint32_t(J / C::NDBUF) & 1);
             tc::fence_after_sync();
-            if (tid == 128) btrace(J, 5);
-            float d[2 * C::SC];
-            tc::tmem_ld_cols<2 * C::SC>(tmem + lb + uint32_t(C::D_OFF + db * C::NB + hf * 2 * C::SC), d);
-            tc::tmem_wait_ld();
-            tc::fence_before_sync();
-            tc::mbar_arrive(&d_free[db]);
+            if (warp == C::NSPLIT && lane == 0) btrace(J, 5);
             const int vg = vt * 128 + v;
-            if (vg < nv) {
-                const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+#pragma unroll 1
+            for (int h = 0; h < HPW; h++) {
+                const int hf = hf0 + h;
+                float d[2 * C::SC];
+                tc::tmem_ld_cols<2 * C::SC>(tmem + lb + uint32_t(C::D_OFF + db * C::NB + hf * 2 * C::SC), d);
+                tc::tmem_wait_ld();
+                if (h == HPW - 1) {
+                    tc::fence_before_sync();
+                    tc::mbar_arrive(&d_free[db]);
+                }
+#ifdef BF_EXP_NO_STORE
+                if (vg < 0) {
+#else
+                if (vg < nv) {
+#endif
 #pragma unroll
-                for (int oo = 0; oo < 2; oo++) {
-                    const int64_t p = (((a0 << 2) + 2 * hf + oo) << shg) + bq;
-                    float2* o = bfs::pair_out(out, po, p, R, nv) + vg;
+                    for (int oo = 0; oo < 2; oo++) {
+                        const int64_t p = (((a0 << 2) + 2 * hf + oo) << shg) + bq;
+                        float2* o = bfs::pair_out(out, po, p, R, nv) + vg;
 #pragma unroll
-                    for (int t = 0; t < R; t++)
-                        o[int64_t(t) * nv] = make_float2(d[oo * C::SC + 2 * t], d[oo * C::SC + 2 * t + 1]);
+                        for (int t = 0; t < R; t++)
+                            o[int64_t(t) * nv] = make_float2(d[oo * C::SC + 2 * t], d[oo * C::SC + 2 * t + 1]);
+                    }
                 }
             }
-            if (tid == 128) btrace(J, 6);
+            if (warp == C::NSPLIT && lane == 0) btrace(J, 6);
         }
     } else if (warp == 12) {
         // ---- loader: the group's 4 r raw coefficient rows of one vector tile, one 2-D tensor copy per pair
@@ -1530,7 +1557,11 @@ __global__ void __launch_bounds__(512, 1)
             // L1 row pairs (j, j'), (j, j' + 1) as one 16-byte load
             constexpr int H = R / 2;
 #pragma unroll 1
+#ifdef BF_EXP_NO_COMPOSE
+            for (int item = wt; item < 0; item += 64) {
+#else
             for (int item = wt; item < C::ITEMS; item += 64) {
+#endif
                 const int jh = item & 1, r2 = item >> 1;
                 const int tp = r2 % R, oi = r2 / R, o = oi >> 2, i = oi & 3;
                 const int up = o >> 1, sp = i >> 1, s = i & 1;
