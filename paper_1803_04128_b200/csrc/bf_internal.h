@@ -31,6 +31,11 @@ int64_t leafx_floats(const Dims& d);
 cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U, float* V0x, float* Ux, cudaStream_t s);
 // S0 on the tensor cores: same contract as launch_s0, weights from V0x.
 bool s0_tc_supported(const Dims& d, int nv, int64_t ldf);
+// S0 with FP16 split passes (bf_tc.cu): image of leafx_floats(d) halves + leafh_rows(d) biased row exponents
+int64_t leafh_rows(const Dims& d);
+cudaError_t expand_s0_h16(const Dims& d, const float2* V0, void* V0h, void* V0e, cudaStream_t s);
+cudaError_t launch_s0_h16(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const void* V0h,
+                          const void* V0e, float2* out, int nv, cudaStream_t s);
 cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x, float2* out,
                          int nv, cudaStream_t s);
 

@@ -129,6 +129,8 @@ struct Shard {
     std::vector<float2*> xfer;
     float* v0x = nullptr;      // tensor-core image of V0 / U (bf_tc.cu), built at finalize when used
     float* ux = nullptr;
+    void* v0h = nullptr;       // FP16 S0 image (BF_OPT_LEAF_F16), instead of v0x, and its row scales
+    void* v0s = nullptr;       // biased exponents (one byte per complex output row) of the FP16 image
     float2* ws = nullptr;      // two coefficient arrays of (N/G) R nv_max
 };
 
@@ -154,6 +156,7 @@ struct bf_plan_s {
     cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the pipelined bf_apply_host
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
     bool band_compose = true;  // BF_OPT_BAND_COMPOSE
+    bool leaf_f16 = true;      // BF_OPT_LEAF_F16
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -270,6 +273,8 @@ void free_plan(bf_plan_s* p)
         cudaFree(s.sw);
         cudaFree(s.v0x);
         cudaFree(s.ux);
+        cudaFree(s.v0h);
+        cudaFree(s.v0s);
         cudaFree(s.u);
         for (auto x : s.xfer) cudaFree(x);
         cudaFree(s.ws);
@@ -417,6 +422,8 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
         cudaError_t e = timed(p, stp.cls, s, [&]() -> cudaError_t {
             switch (stp.kind) {
             case Step::S0:
+                if (p->tensor_cores && sh.v0h && bfk::s0_tc_supported(dl, nv, ldf))
+                    return bfk::launch_s0_h16(dl, F, ldf, sh.amp_b, sh.v0h, sh.v0s, in, nv, s);
                 if (p->tensor_cores && sh.v0x && bfk::s0_tc_supported(dl, nv, ldf))
                     return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s);
                 return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
@@ -727,6 +734,43 @@ bf_status_t bf_plan_upload(bf_plan_t p, int32_t stage, int64_t block_begin, int6
     return BF_OK;
 }
 
+namespace {
+// The tensor-core image of V0 in the format BF_OPT_LEAF_F16 selects (the other one is freed): FP16 hi/lo
+// tiles + per-row scales (s0_h16_kernel), or TF32 hi/lo tiles (s0_tc_kernel).  Without memory for it the
+// SIMT S0 serves the plan.
+bf_status_t build_s0_image(bf_plan_s* p, Shard& s)
+{
+    const bfk::Dims dl = p->local();
+    cudaFree(s.v0x);
+    cudaFree(s.v0h);
+    cudaFree(s.v0s);
+    s.v0x = nullptr;
+    s.v0h = nullptr;
+    s.v0s = nullptr;
+    cudaError_t e;
+    if (p->leaf_f16) {
+        if (cudaMalloc(&s.v0h, size_t(bfk::leafx_floats(dl)) * 2) != cudaSuccess ||
+            cudaMalloc(&s.v0s, size_t(bfk::leafh_rows(dl))) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(s.v0h);
+            cudaFree(s.v0s);
+            s.v0h = nullptr;
+            s.v0s = nullptr;
+            return BF_OK;
+        }
+        e = bfk::expand_s0_h16(dl, s.v0, s.v0h, s.v0s, 0);
+    } else {
+        if (cudaMalloc(&s.v0x, size_t(bfk::leafx_floats(dl)) * sizeof(float)) != cudaSuccess) {
+            cudaGetLastError();
+            s.v0x = nullptr;
+            return BF_OK;
+        }
+        e = bfk::expand_leaf_weights(dl, s.v0, nullptr, s.v0x, nullptr, 0);
+    }
+    return e == cudaSuccess ? BF_OK : cuda_fail(e, "S0 weight image");
+}
+}  // namespace
+
 bf_status_t bf_plan_finalize(bf_plan_t p)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
@@ -760,15 +804,14 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
     if (p->tensor_cores && bfk::leaf_tc_shape(dl) && p->max_chunk * p->d.n_amp >= 64) {
         const size_t bytes = size_t(bfk::leafx_floats(dl)) * sizeof(float);
         for (Shard& s : p->sh) {
-            if (cudaMalloc(&s.v0x, bytes) != cudaSuccess || cudaMalloc(&s.ux, bytes) != cudaSuccess) {
+            if (cudaMalloc(&s.ux, bytes) != cudaSuccess) {
                 cudaGetLastError();   // not enough device memory: the SIMT leaf kernels serve this plan
-                cudaFree(s.v0x);
-                cudaFree(s.ux);
-                s.v0x = s.ux = nullptr;
+                s.ux = nullptr;
                 continue;
             }
-            e = bfk::expand_leaf_weights(dl, s.v0, s.u, s.v0x, s.ux, 0);
+            e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
             if (e != cudaSuccess) return cuda_fail(e, "leaf weight expansion");
+            if (bf_status_t st = build_s0_image(p, s); st != BF_OK) return st;
         }
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e, "leaf weight expansion");
@@ -936,13 +979,18 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
                                     int64_t(nx) * n * 2 * r * r);
     info->workspace_bytes = nsh * int64_t(p->ws_bytes);
     info->tc_weight_bytes = 0;
-    for (const Shard& s : p->sh)
-        if (s.v0x) info->tc_weight_bytes += 2 * bfk::leafx_floats(p->local()) * int64_t(sizeof(float));
+    for (const Shard& s : p->sh) {
+        const int64_t lx = bfk::leafx_floats(p->local());
+        if (s.v0x) info->tc_weight_bytes += lx * int64_t(sizeof(float));
+        if (s.ux) info->tc_weight_bytes += lx * int64_t(sizeof(float));
+        if (s.v0h) info->tc_weight_bytes += lx * 2 + bfk::leafh_rows(p->local());
+    }
     {
         const bfk::Dims dl = p->local();
         const int nvf = int(p->max_chunk * p->d.n_amp);
         int mask = 0;
-        if (p->tensor_cores && p->sh[0].v0x && bfk::s0_tc_supported(dl, nvf, dl.N)) mask |= 1 << bfk::KC_S0;
+        if (p->tensor_cores && (p->sh[0].v0x || p->sh[0].v0h) && bfk::s0_tc_supported(dl, nvf, dl.N))
+            mask |= 1 << bfk::KC_S0;
         if (p->tensor_cores && p->sh[0].ux && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
         if (p->tensor_cores && bfk::band_supported(dl.R, nvf) && bfk::band_tc_supported(dl, nvf))
             for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE))
@@ -1048,6 +1096,20 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
         }
         p->exchange_peer = value != 0;
         return BF_OK;
+    }
+    if (option == BF_OPT_LEAF_F16) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_LEAF_F16 takes 0 or 1");
+        if (p->leaf_f16 == (value != 0)) return BF_OK;
+        p->leaf_f16 = value != 0;
+        if (!p->finalized) return BF_OK;
+        DeviceGuard g(p->device);
+        cudaError_t e = cudaDeviceSynchronize();   // no apply may still read the old image
+        if (e != cudaSuccess) return cuda_fail(e, "leaf image switch");
+        for (Shard& s : p->sh)
+            if (s.v0x || s.v0h)
+                if (bf_status_t st = build_s0_image(p, s); st != BF_OK) return st;
+        e = cudaDeviceSynchronize();
+        return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf image switch");
     }
     if (option == BF_OPT_BAND_COMPOSE) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_COMPOSE takes 0 or 1");

@@ -157,10 +157,12 @@ cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U
 {
     if (!leaf_tc_shape(d)) return cudaErrorInvalidValue;
     const unsigned grid = 148 * 16;
-    expand_s0_kernel<<<grid, 256, 0, s>>>(V0, V0x, d.LN, d.l0, d.R);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    expand_sl_kernel<<<grid, 256, 0, s>>>(U, Ux, d.LN, d.l0, d.R, sl_kp(d.R));
+    if (V0x) {
+        expand_s0_kernel<<<grid, 256, 0, s>>>(V0, V0x, d.LN, d.l0, d.R);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (Ux) expand_sl_kernel<<<grid, 256, 0, s>>>(U, Ux, d.LN, d.l0, d.R, sl_kp(d.R));
     return cudaGetLastError();
 }
 
@@ -252,23 +254,11 @@ __global__ void __launch_bounds__(448, 1)
     const uint32_t tmem = tmem_base;
 
     if (warp == 4) {
-        // ---- loader: per job the F staging tile, and the weight ring (all jobs, in order) ----
+        // ---- loader: per job the F staging tile, and the weight ring (all jobs, in order).  The next job's F
+        //      tile is issued a few weight tiles into the current job (as soon as the split has released the
+        //      staging tile), so its latency hides behind the current job's MMAs ----
         if (lane == 0) {
-            int64_t it = 0;   // weight tiles issued
-            const int64_t total_it = njobs * C::NCH * C::KS;
-            auto issue_weights = [&](int64_t upto) {
-                for (; it < upto && it < total_it; it++) {
-                    const int st = int(it % C::NSTAGE);
-                    if (it >= C::NSTAGE) tc::mbar_wait(&empty[st], uint32_t(it / C::NSTAGE - 1) & 1);
-                    const int64_t jl = it / (C::NCH * C::KS);   // local job
-                    const int64_t b = unsigned(blockIdx.x + jl * gridDim.x) / unsigned(nvt);
-                    const int64_t w = it % (C::NCH * C::KS);
-                    tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
-                    tc::bulk_g2s(ring + st * C::STAGE, V0x + (b * (C::NCH * C::KS) + w) * 2 * S0X_TILE_FLOATS,
-                                 C::STAGE, &full[st]);
-                }
-            };
-            for (int64_t jl = 0; jl < njobs; jl++) {
+            auto issue_f = [&](int64_t jl) {
                 const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
                 const int64_t b = job / unsigned(nvt);
                 const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
@@ -278,7 +268,20 @@ __global__ void __launch_bounds__(448, 1)
                 for (int cl = 0; cl < cw; cl++)
                     tc::bulk_g2s(Fs + cl * C::FS, F + b * N0 + int64_t(c0 + cl) * ldf, N0 * 8, &f_full);
                 for (int k = 0; k < n_amp; k++) tc::bulk_g2s(Bk + k * N0, ampb + k * N + b * N0, N0 * 8, &f_full);
-                issue_weights((jl + 1) * C::NCH * C::KS);   // this job's weight tiles (bounded by the ring)
+            };
+            constexpr int WPJ = C::NCH * C::KS;                       // weight tiles per job
+            constexpr int F_AT = C::NSTAGE < WPJ - 1 ? C::NSTAGE : WPJ - 1;
+            if (njobs > 0) issue_f(0);
+            int64_t it = 0;
+            for (int64_t jl = 0; jl < njobs; jl++) {
+                const int64_t b = unsigned(blockIdx.x + jl * gridDim.x) / unsigned(nvt);
+                for (int w = 0; w < WPJ; w++, it++) {
+                    const int st = int(it % C::NSTAGE);
+                    if (it >= C::NSTAGE) tc::mbar_wait(&empty[st], uint32_t(it / C::NSTAGE - 1) & 1);
+                    tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
+                    tc::bulk_g2s(ring + st * C::STAGE, V0x + (b * WPJ + w) * 2 * S0X_TILE_FLOATS, C::STAGE, &full[st]);
+                    if (w == F_AT && jl + 1 < njobs) issue_f(jl + 1);
+                }
             }
         }
     } else if (warp < 4) {
@@ -357,19 +360,25 @@ __global__ void __launch_bounds__(448, 1)
             __syncwarp();
         }
     } else {
-        // ---- epilogue (warps 6-13): lane quarter warp % 4 = vectors, column half (warp - 6) / 4 ----
+        // ---- epilogue (warps 6-13): lane quarter warp % 4 = vectors, column half (warp - 6) / 4; output rows
+        //      advance incrementally (t, then pair a at stride nleaf R nv) ----
         const int q4 = warp & 3, cbase = ((warp - 6) >> 2) * 64;
+        const int64_t strideA = nleaf * R * int64_t(nv), jumpA = strideA - int64_t(R) * nv;
         int64_t gc = 0;
         for (int64_t jl = 0; jl < njobs; jl++) {
             const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
             const int64_t b = job / unsigned(nvt);
             const int vg = int(job % unsigned(nvt)) * 128 + q4 * 32 + lane;
+            float2* const obase = out + b * R * int64_t(nv) + vg;
             for (int nc = 0; nc < C::NCH; nc++, gc++) {
                 const int slot = int(gc & 1);
                 tc::mbar_wait(&dfull[slot], uint32_t(gc >> 1) & 1);
                 tc::fence_after_sync();
                 const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * S0X_NC + cbase);
-#pragma unroll 1
+                const int q0 = (nc * S0X_NC + cbase) >> 1;
+                int t = q0 % R;
+                float2* o = obase + int64_t(q0 / R) * strideA + int64_t(t) * nv;
+#pragma unroll
                 for (int c0 = 0; c0 < 64; c0 += 32) {
                     float x[32];
                     tc::tmem_ld16(taddr + c0, x);
@@ -379,12 +388,13 @@ __global__ void __launch_bounds__(448, 1)
                         tc::fence_before_sync();
                         tc::mbar_arrive(&dempty[slot]);
                     }
-                    if (vg < nv) {
 #pragma unroll
-                        for (int i = 0; i < 16; i++) {
-                            const int q = (nc * S0X_NC + cbase + c0) / 2 + i;   // complex output index a R + t
-                            const int a = q / R, t = q - a * R;
-                            out[((int64_t(a) * nleaf + b) * R + t) * nv + vg] = make_float2(x[2 * i], x[2 * i + 1]);
+                    for (int i = 0; i < 16; i++) {
+                        if (vg < nv) *o = make_float2(x[2 * i], x[2 * i + 1]);
+                        o += nv;
+                        if (++t == R) {
+                            t = 0;
+                            o += jumpA;
                         }
                     }
                 }
@@ -429,6 +439,361 @@ cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const floa
     return cudaErrorInvalidValue;
 }
 
+
+// =============================================================================================
+// S0 in FP16 passes (BF_OPT_LEAF_F16 = 1, the default).  Same job structure as s0_tc_kernel, but every
+// operand is split into FP16 hi + lo after a power-of-two scaling that brings each A row (one vector's
+// b_k F values of the leaf) and each B row (one output coefficient's V0 row) to max |x| in [0.5, 1):
+// hi = fp16(x), lo = fp16(x - hi), and D = Ahi Bhi + Alo Bhi + Ahi Blo accumulates in FP32 with
+// kind::f16 MMAs (K = 16 per instruction: twice the MAC rate of kind::tf32, tools/tc_probe_f16.cu).
+// The hi parts carry 11 significant bits like TF32, and the scaling keeps every value of interest in
+// FP16's normal range, so the product error matches the 3xTF32 split (measured model in the probe);
+// values below 2^-14 of their row's maximum go subnormal with an absolute error <= 2^-25 of that
+// maximum.  The epilogue multiplies by 2^{e_v} 2^{f_n}.  The weight image is half the bytes of the TF32
+// image (plus one FP32 scale per row).
+// =============================================================================================
+constexpr uint32_t S0H_TILE = uint32_t(S0X_NC) * S0X_KC * 2;   // one 128 x 32 FP16 tile (8 KB)
+
+int64_t leafh_rows(const Dims& d) { return d.N * int64_t(d.R); }   // biased exponents, one per complex output row
+
+__global__ void expand_s0_h16_kernel(const float2* __restrict__ V0, __half* __restrict__ X, uint8_t* __restrict__ S,
+                                     int LN, int l0, int R)
+{
+    const int n0 = 1 << l0;
+    const int64_t nleaf = (int64_t(1) << LN) >> l0;
+    const int rows = n0 * 2 * R, K = 2 * n0, cq = n0 * R;
+    const int nch = rows / S0X_NC, kch = K / S0X_KC;
+    const int64_t total = nleaf * cq;
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = g / cq;
+        const int q = int(g - b * cq);                 // complex output row q = a R + t: real rows 2q, 2q + 1
+        const int a = q / R, t = q - a * R;
+        const float2* w = V0 + (int64_t(a) * nleaf + b) * (n0 * R) + t;   // w[j R]
+        float mx = 0.f;
+        for (int j = 0; j < n0; j++) mx = fmaxf(mx, fmaxf(fabsf(w[j * R].x), fabsf(w[j * R].y)));
+        int e = 0;
+        frexpf(mx, &e);                                // mx 2^-e in [0.5, 1)
+        e = max(-126, min(126, e));
+        S[b * cq + q] = uint8_t(e + 127);              // biased: the epilogue multiplies by 2^e
+        for (int cp = 0; cp < 2; cp++) {
+            const int n = 2 * q + cp, nc = n / S0X_NC;
+            for (int k = 0; k < K; k++) {
+                const float x = ldexpf(embed(w[(k >> 1) * R], cp, k & 1), -e);
+                float hi, lo;
+                tc::split_h(x, hi, lo);
+                const int kc = k / S0X_KC;
+                __half* tile = X + ((b * nch + nc) * kch + kc) * 2 * int64_t(S0X_NC * S0X_KC);
+                const uint32_t off = tc::kmaj_off16(n % S0X_NC, k % S0X_KC, S0X_NC) / 2;
+                tile[off] = __float2half_rn(hi);
+                tile[S0X_NC * S0X_KC + off] = __float2half_rn(lo);
+            }
+        }
+    }
+}
+
+template <int R, int N0>
+struct S0H {
+    static constexpr int K = 2 * N0;
+    static constexpr int KS = K / S0X_KC;
+    static constexpr int NCH = N0 * 2 * R / S0X_NC;
+    static constexpr int NSTAGE = 2 * KS;                  // weight ring depth (16 KB stages)
+    static constexpr uint32_t STAGE = 2 * S0H_TILE;        // hi + lo
+    static constexpr int FS = N0 + 2;                      // padded staging rows (16-byte aligned, bank spread)
+    static constexpr uint32_t FBYTES = 128u * FS * 8;
+    static constexpr uint32_t OFF_F = NSTAGE * STAGE, OFF_BK = OFF_F + FBYTES, OFF_E = OFF_BK + 4 * N0 * 8;
+    static constexpr size_t SMEM = size_t(OFF_E) + 4 * 128 * 4;
+    static constexpr int A_COLS = K / 2;                   // packed FP16 pairs: hi at +0, lo at +A_COLS
+    static constexpr int A_BUF = 2 * A_COLS;               // two A buffers (the split fills job j + 1 while
+    static constexpr int D_OFF = 2 * A_BUF;                //   the tensor pipe runs job j)
+    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * S0X_NC>();
+    static_assert((N0 * 2 * R) % S0X_NC == 0 && KS >= 2, "tiling");
+    static_assert(SMEM <= 232448 - 1024 && D_OFF + 2 * S0X_NC <= 512, "budget");
+};
+
+template <int R, int N0>
+__global__ void __launch_bounds__(448, 1)
+    s0_h16_kernel(const float2* __restrict__ F, int64_t ldf, const float2* __restrict__ ampb,
+                  const __half* __restrict__ V0h, const uint8_t* __restrict__ V0s, float2* __restrict__ out, int LN,
+                  int n_amp, int nv, int nvt)
+{
+    using C = S0H<R, N0>;
+    extern __shared__ __align__(128) uint8_t sm_s0h[];
+    uint8_t* ring = sm_s0h;
+    float2* Fs = reinterpret_cast<float2*>(sm_s0h + C::OFF_F);    // [column][FS]
+    float2* Bk = reinterpret_cast<float2*>(sm_s0h + C::OFF_BK);   // [k][N0] b_k(x)
+    float* Es = reinterpret_cast<float*>(sm_s0h + C::OFF_E);       // [job % 4][128] 2^{e_v}
+    __shared__ uint64_t full[C::NSTAGE], empty[C::NSTAGE], dfull[2], dempty[2], f_full, f_empty, a_full[2], a_free[2];
+    __shared__ uint64_t e_full[4], e_empty[4];
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t N = int64_t(1) << LN;
+    const int64_t nleaf = N / N0;
+    const int64_t njobs_all = nleaf * nvt;
+    const int64_t njobs = (njobs_all - blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < C::NSTAGE; i++) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&dfull[i], 1);
+            tc::mbar_init(&dempty[i], 256);
+        }
+        for (int i = 0; i < 4; i++) {
+            tc::mbar_init(&e_full[i], 128);
+            tc::mbar_init(&e_empty[i], 256);
+        }
+        tc::mbar_init(&f_full, 1);
+        tc::mbar_init(&f_empty, 128);
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&a_full[i], 128);
+            tc::mbar_init(&a_free[i], 1);
+        }
+        tc::mbar_fence_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 4) {
+        // ---- loader: per job the F staging tile, and the weight ring (all jobs, in order).  The next job's F
+        //      tile is issued a few weight tiles into the current job (as soon as the split has released the
+        //      staging tile), so its latency hides behind the current job's MMAs ----
+        if (lane == 0) {
+            auto issue_f = [&](int64_t jl) {
+                const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
+                const int64_t b = job / unsigned(nvt);
+                const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
+                const int c0 = v0 / n_amp, cw = (vw + n_amp - 1) / n_amp;
+                if (jl > 0) tc::mbar_wait(&f_empty, uint32_t(jl - 1) & 1);
+                tc::mbar_arrive_expect_tx(&f_full, uint32_t(cw) * N0 * 8 + uint32_t(n_amp) * N0 * 8);
+                for (int cl = 0; cl < cw; cl++)
+                    tc::bulk_g2s(Fs + cl * C::FS, F + b * N0 + int64_t(c0 + cl) * ldf, N0 * 8, &f_full);
+                for (int k = 0; k < n_amp; k++) tc::bulk_g2s(Bk + k * N0, ampb + k * N + b * N0, N0 * 8, &f_full);
+            };
+            constexpr int WPJ = C::NCH * C::KS;                       // weight tiles per job
+            constexpr int F_AT = C::NSTAGE < WPJ - 1 ? C::NSTAGE : WPJ - 1;
+            if (njobs > 0) issue_f(0);
+            int64_t it = 0;
+            for (int64_t jl = 0; jl < njobs; jl++) {
+                const int64_t b = unsigned(blockIdx.x + jl * gridDim.x) / unsigned(nvt);
+                for (int w = 0; w < WPJ; w++, it++) {
+                    const int st = int(it % C::NSTAGE);
+                    if (it >= C::NSTAGE) tc::mbar_wait(&empty[st], uint32_t(it / C::NSTAGE - 1) & 1);
+                    tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
+                    tc::bulk_g2s(ring + st * C::STAGE, V0h + (b * WPJ + w) * 2 * (S0X_NC * S0X_KC), C::STAGE, &full[st]);
+                    if (w == F_AT && jl + 1 < njobs) issue_f(jl + 1);
+                }
+            }
+        }
+    } else if (warp < 4) {
+        // ---- A = Y^T scaled by 2^{-e_v}, FP16 hi / lo packed into TMEM; thread = vector ----
+        const int v = tid;
+        const uint32_t lb = uint32_t(warp * 32) << 16;
+        for (int64_t jl = 0; jl < njobs; jl++) {
+            const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
+            const int v0 = int(job % unsigned(nvt)) * 128, vg = v0 + v;
+            const int c0 = v0 / n_amp;
+            const int eb = int(jl & 3), ab = int(jl & 1);
+            tc::mbar_wait(&f_full, uint32_t(jl & 1));
+            if (jl >= 2) tc::mbar_wait(&a_free[ab], uint32_t((jl >> 1) - 1) & 1);
+            if (jl >= 4) tc::mbar_wait(&e_empty[eb], uint32_t((jl >> 2) - 1) & 1);
+            tc::fence_after_sync();
+            const bool ok = vg < nv;
+            const int cl = ok ? vg / n_amp - c0 : 0, k = ok ? vg % n_amp : 0;
+            const float2* fc = Fs + cl * C::FS;
+            const float2* bk = Bk + k * N0;
+            float mx = 0.f;
+#pragma unroll 4
+            for (int j = 0; j < N0; j += 2) {
+                const float4 f = *reinterpret_cast<const float4*>(fc + j);
+                const float4 a = *reinterpret_cast<const float4*>(bk + j);
+                const float2 y0 = cmul_tc(make_float2(a.x, a.y), make_float2(f.x, f.y));
+                const float2 y1 = cmul_tc(make_float2(a.z, a.w), make_float2(f.z, f.w));
+                mx = fmaxf(mx, fmaxf(fmaxf(fabsf(y0.x), fabsf(y0.y)), fmaxf(fabsf(y1.x), fabsf(y1.y))));
+            }
+            int e = 0;
+            frexpf(ok ? mx : 0.f, &e);
+            e = max(-126, min(126, e));
+            const float sc = ldexpf(1.f, -e);
+            Es[eb * 128 + v] = ldexpf(1.f, e);
+            tc::mbar_arrive(&e_full[eb]);
+#pragma unroll 1
+            for (int j0 = 0; j0 < N0; j0 += 8) {
+                float hi[8], lo[8];
+#pragma unroll
+                for (int jj = 0; jj < 8; jj += 2) {
+                    const float4 f = *reinterpret_cast<const float4*>(fc + j0 + jj);
+                    const float4 a = *reinterpret_cast<const float4*>(bk + j0 + jj);
+                    float2 y[2] = {cmul_tc(make_float2(a.x, a.y), make_float2(f.x, f.y)),
+                                   cmul_tc(make_float2(a.z, a.w), make_float2(f.z, f.w))};
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        if (!ok) y[h] = make_float2(0.f, 0.f);
+                        float hr, lr, hm, lm;
+                        tc::split_h(y[h].x * sc, hr, lr);
+                        tc::split_h(y[h].y * sc, hm, lm);
+                        hi[jj + h] = tc::pack_h2(hr, hm);   // column j = (re, im) of complex j: K index 2j, 2j + 1
+                        lo[jj + h] = tc::pack_h2(lr, lm);
+                    }
+                }
+                tc::tmem_st8(tmem + lb + uint32_t(ab * C::A_BUF + j0), hi);
+                tc::tmem_st8(tmem + lb + uint32_t(ab * C::A_BUF + C::A_COLS + j0), lo);
+            }
+            tc::fence_before_sync();
+            tc::mbar_arrive(&f_empty);
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&a_full[ab]);
+        }
+    } else if (warp == 5) {
+        // ---- MMA issuer: per 32-wide K tile 3 passes x 2 kind::f16 MMAs (K = 16) ----
+        constexpr uint32_t idesc = tc::idesc_f16(128, S0X_NC);
+        constexpr uint32_t LBO_B = (S0X_NC / 8) * 128;
+        const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(ring), LBO_B);
+        int64_t gc = 0;
+        for (int64_t jl = 0; jl < njobs; jl++) {
+            const int ab = int(jl & 1);
+            tc::mbar_wait(&a_full[ab], uint32_t(jl >> 1) & 1);
+            tc::fence_after_sync();
+            for (int nc = 0; nc < C::NCH; nc++, gc++) {
+                const int slot = int(gc & 1);
+                if (gc >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gc >> 1) - 1) & 1);
+                const int64_t it0 = gc * C::KS;
+                const uint32_t d = tmem + uint32_t(C::D_OFF + slot * S0X_NC);
+                for (int ks = 0; ks < C::KS; ks++) {
+                    const int st = int((it0 + ks) % C::NSTAGE);
+                    tc::mbar_wait(&full[st], uint32_t((it0 + ks) / C::NSTAGE) & 1);
+                    tc::fence_after_sync();
+#pragma unroll
+                    for (int q = 0; q < 3; q++) {
+                        const int pass = kPassOrder[q];
+                        const uint64_t b = tc::desc_add(dB0, st * C::STAGE + (pass == 2 ? S0H_TILE : 0));
+                        const uint32_t a = tmem + uint32_t(ab * C::A_BUF + (pass == 1 ? C::A_COLS : 0) + ks * (S0X_KC / 2));
+#pragma unroll
+                        for (int kk = 0; kk < S0X_KC / 16; kk++)
+                            tc::mma_f16_ts_warp(d, a + kk * 8, tc::desc_add(b, kk * 2 * LBO_B), idesc,
+                                                (q | ks | kk) ? 1u : 0u);
+                    }
+                    tc::commit_warp(&empty[st]);
+                }
+                tc::commit_warp(&dfull[slot]);
+                __syncwarp();
+            }
+            tc::commit_warp(&a_free[ab]);
+            __syncwarp();
+        }
+    } else {
+        // ---- epilogue (warps 6-13): lane quarter warp % 4 = vectors, column half (warp - 6) / 4.  Output rows
+        //      advance incrementally (t, then pair a at stride nleaf R nv); 2^{e_v + e_q} per complex row ----
+        const int q4 = warp & 3, cbase = ((warp - 6) >> 2) * 64;
+        constexpr int CQ = N0 * R;                                // complex output rows per leaf
+        const int64_t strideA = nleaf * R * int64_t(nv), jumpA = strideA - int64_t(R) * nv;
+        int64_t gc = 0;
+        for (int64_t jl = 0; jl < njobs; jl++) {
+            const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
+            const int64_t b = job / unsigned(nvt);
+            const int vg = int(job % unsigned(nvt)) * 128 + q4 * 32 + lane;
+            const int eb = int(jl & 3);
+            tc::mbar_wait(&e_full[eb], uint32_t(jl >> 2) & 1);
+            const float sv = Es[eb * 128 + q4 * 32 + lane];
+            tc::mbar_arrive(&e_empty[eb]);
+            const uint8_t* Sb = V0s + b * CQ + (cbase >> 1);
+            float2* const obase = out + b * R * int64_t(nv) + vg;
+            uint4 ex[2];   // the biased exponents of this thread's 32 complex rows of the chunk (one chunk ahead)
+            ex[0] = __ldg(reinterpret_cast<const uint4*>(Sb));
+            ex[1] = __ldg(reinterpret_cast<const uint4*>(Sb) + 1);
+            for (int nc = 0; nc < C::NCH; nc++, gc++) {
+                const int slot = int(gc & 1);
+                uint4 exn[2] = {ex[0], ex[1]};
+                if (nc + 1 < C::NCH) {
+                    exn[0] = __ldg(reinterpret_cast<const uint4*>(Sb + (nc + 1) * (S0X_NC / 2)));
+                    exn[1] = __ldg(reinterpret_cast<const uint4*>(Sb + (nc + 1) * (S0X_NC / 2)) + 1);
+                }
+                tc::mbar_wait(&dfull[slot], uint32_t(gc >> 1) & 1);
+                tc::fence_after_sync();
+                const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * S0X_NC + cbase);
+                const int q0 = (nc * S0X_NC + cbase) >> 1;
+                int t = q0 % R;
+                float2* o = obase + int64_t(q0 / R) * strideA + int64_t(t) * nv;
+#pragma unroll
+                for (int c0 = 0; c0 < 64; c0 += 32) {
+                    float x[32];
+                    tc::tmem_ld16(taddr + c0, x);
+                    tc::tmem_ld16(taddr + c0 + 16, x + 16);
+                    tc::tmem_wait_ld();
+                    if (c0 == 32) {
+                        tc::fence_before_sync();
+                        tc::mbar_arrive(&dempty[slot]);
+                    }
+                    const uint32_t* ew = reinterpret_cast<const uint32_t*>(&ex[c0 >> 5]);
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const uint32_t be = (ew[i >> 2] >> (8 * (i & 3))) & 0xffu;
+                        const float s2 = sv * __uint_as_float(be << 23);
+                        if (vg < nv) *o = make_float2(x[2 * i] * s2, x[2 * i + 1] * s2);
+                        o += nv;
+                        if (++t == R) {
+                            t = 0;
+                            o += jumpA;
+                        }
+                    }
+                }
+                ex[0] = exn[0];
+                ex[1] = exn[1];
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+    }
+}
+
+template <int R, int N0>
+static cudaError_t s0_h16_go(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const __half* V0h,
+                             const uint8_t* V0s, float2* out, int nv, cudaStream_t s)
+{
+    using C = S0H<R, N0>;
+    auto kern = s0_h16_kernel<R, N0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    const int nvt = (nv + 127) / 128;
+    const int64_t jobs = (d.N / N0) * nvt;
+    const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
+    kern<<<grid, 448, C::SMEM, s>>>(F, ldf, ampb, V0h, V0s, out, d.LN, d.n_amp, nv, nvt);
+    return cudaGetLastError();
+}
+
+cudaError_t expand_s0_h16(const Dims& d, const float2* V0, void* V0h, void* V0s, cudaStream_t s)
+{
+    if (!leaf_tc_shape(d)) return cudaErrorInvalidValue;
+    expand_s0_h16_kernel<<<148 * 16, 128, 0, s>>>(V0, static_cast<__half*>(V0h), static_cast<uint8_t*>(V0s), d.LN,
+                                                  d.l0, d.R);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_s0_h16(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const void* V0h,
+                          const void* V0s, float2* out, int nv, cudaStream_t s)
+{
+    const int n0 = 1 << d.l0;
+    const __half* X = static_cast<const __half*>(V0h);
+    const uint8_t* E8 = static_cast<const uint8_t*>(V0s);
+#define S0H_CASE(RR)                                                                                       \
+    if (d.R == RR)                                                                                         \
+        return n0 == 64 ? s0_h16_go<RR, 64>(d, F, ldf, ampb, X, E8, out, nv, s)                            \
+                        : s0_h16_go<RR, 32>(d, F, ldf, ampb, X, E8, out, nv, s);
+    S0H_CASE(6) S0H_CASE(8) S0H_CASE(10) S0H_CASE(12) S0H_CASE(16)
+#undef S0H_CASE
+    return cudaErrorInvalidValue;
+}
+
 // =============================================================================================
 // SL (eqn:bf3 P:791-797, amplitude post-scale and sum over k eqn:tg P:24-28) on the tensor cores,
 // persistent.  A job = one T_X leaf a x one tile of 128 vectors (vector tile fastest).
@@ -450,7 +815,11 @@ struct SLTC {
     static constexpr int NB = 2 * N0;
     static constexpr int KC = KP * 2 * R;
     static constexpr int NCH = N0 / KP;
+#ifdef BF_SL_SEG
+    static constexpr int SEG = BF_SL_SEG;                        // chunks per accumulation segment
+#else
     static constexpr int SEG = 2;                                // chunks per accumulation segment
+#endif
     static constexpr int NSEG = (NCH + SEG - 1) / SEG;
     static constexpr uint32_t RAW = uint32_t(KP) * R * 128 * 8;
     static constexpr uint32_t BT = uint32_t(NB) * KC * 4;   // one of hi / lo

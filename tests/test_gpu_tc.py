@@ -180,3 +180,44 @@ def test_tc_band_composed(r, l0, LN, nrhs):
     d = oracle.rel_l2(Gc.astype(np.complex128), Gl.astype(np.complex128), axis=0)
     assert np.all(d <= PATHS_AGREE), d.max()
     assert not np.array_equal(Gc, Gl)                 # the composed kernel really ran
+
+
+@pytest.mark.parametrize("kernel,amp,LN,l0,r,nrhs", [(W.K_FIO, W.A_CFG1, 14, 6, 10, 128),
+                                                     (W.K_FIO_JUMP, W.A_CFG3, 12, 5, 16, 32),
+                                                     (W.K_DFT, W.A_ONE, 12, 6, 6, 70)])
+def test_tc_leaf_f16_vs_tf32(kernel, amp, LN, l0, r, nrhs):
+    """BF_OPT_LEAF_F16 (default 1): S0 in FP16 split passes with per-row power-of-two scaling; 0: 3xTF32.
+    Both meet the oracle bar and agree with each other like the two FP32-accurate paths do."""
+    F = W.rhs(1 << LN, nrhs, 60 + r)
+    plan = bf.Plan.build_fio(bf.fio(kernel, amp, LN, l0, r), max_nrhs_chunk=nrhs)
+    assert "s0" in plan.info()["tc_classes"]
+    bytes_f16 = plan.info()["tc_weight_bytes"]
+    G16 = _apply(plan, F)
+    plan.set_option(bf.BF_OPT_LEAF_F16, 0)
+    assert "s0" in plan.info()["tc_classes"] and plan.info()["tc_weight_bytes"] > bytes_f16
+    G32 = _apply(plan, F)
+    with pytest.raises(bf.BFError):
+        plan.set_option(bf.BF_OPT_LEAF_F16, 2)
+    plan.destroy()
+    cols = [0, nrhs - 1]
+    R = oracle.bf_apply(kernel, amp, LN, l0, r, F[:, cols])
+    for G in (G16, G32):
+        assert np.all(oracle.rel_l2(G[:, cols].astype(np.complex128), R, axis=0) <= PARITY)
+    d = oracle.rel_l2(G16.astype(np.complex128), G32.astype(np.complex128), axis=0)
+    assert np.all(d <= PATHS_AGREE), d.max()
+    assert not np.array_equal(G16, G32)
+
+
+def test_tc_scale_equivariance():
+    """The FP16 S0 scales every vector by a power of two chosen from its own values, so the whole
+    tensor-core path is exactly homogeneous under power-of-two scaling of F (no overflow at 2^60, no
+    precision loss at 2^-60): G(2^k F) == 2^k G(F) bitwise."""
+    LN, l0, r, nrhs = 12, 6, 10, 64
+    F = W.rhs(1 << LN, nrhs, 9)
+    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    G = _apply(plan, F)
+    for k in (60, -60):
+        Gk = _apply(plan, np.asfortranarray(F * np.float32(2.0 ** k)).astype(np.complex64))
+        assert np.all(np.isfinite(Gk))
+        assert np.array_equal(Gk, (G * np.float32(2.0 ** k)).astype(np.complex64)), k
+    plan.destroy()
