@@ -36,6 +36,12 @@ int64_t leafh_rows(const Dims& d);
 cudaError_t expand_s0_h16(const Dims& d, const float2* V0, void* V0h, void* V0e, cudaStream_t s);
 cudaError_t launch_s0_h16(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const void* V0h,
                           const void* V0e, float2* out, int nv, cudaStream_t s);
+// SL with FP16 split passes: image of leafx_floats(d) halves + leafu_rows(d) biased exponents
+int64_t leafu_rows(const Dims& d);
+bool sl_h16_shape(const Dims& d);   // the FP16 SL fits this shape (else the 3xTF32 SL)
+cudaError_t expand_sl_h16(const Dims& d, const float2* U, void* Uh, void* Ue, cudaStream_t s);
+cudaError_t launch_sl_h16(const Dims& d, const float2* in, const void* Uh, const void* Ue, const float2* ampa,
+                          float2* G, int64_t ldg, int nv, cudaStream_t s);
 cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x, float2* out,
                          int nv, cudaStream_t s);
 

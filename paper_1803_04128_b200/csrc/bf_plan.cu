@@ -131,6 +131,8 @@ struct Shard {
     float* ux = nullptr;
     void* v0h = nullptr;       // FP16 S0 image (BF_OPT_LEAF_F16), instead of v0x, and its row scales
     void* v0s = nullptr;       // biased exponents (one byte per complex output row) of the FP16 image
+    void* uh = nullptr;        // FP16 SL image (BF_OPT_LEAF_F16, shapes where it fits), instead of ux
+    void* ue = nullptr;
     float2* ws = nullptr;      // two coefficient arrays of (N/G) R nv_max
 };
 
@@ -275,6 +277,8 @@ void free_plan(bf_plan_s* p)
         cudaFree(s.ux);
         cudaFree(s.v0h);
         cudaFree(s.v0s);
+        cudaFree(s.uh);
+        cudaFree(s.ue);
         cudaFree(s.u);
         for (auto x : s.xfer) cudaFree(x);
         cudaFree(s.ws);
@@ -437,6 +441,8 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                 return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
             }
             case Step::SL:
+                if (p->tensor_cores && sh.uh && bfk::sl_tc_supported(dl, nv))
+                    return bfk::launch_sl_h16(dl, in, sh.uh, sh.ue, sh.amp_a, G, ldg, nv, s);
                 if (p->tensor_cores && sh.ux && bfk::sl_tc_supported(dl, nv))
                     return bfk::launch_sl_tc(dl, in, sh.ux, sh.amp_a, G, ldg, nv, s);
                 return bfk::launch_sl(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
@@ -735,39 +741,49 @@ bf_status_t bf_plan_upload(bf_plan_t p, int32_t stage, int64_t block_begin, int6
 }
 
 namespace {
-// The tensor-core image of V0 in the format BF_OPT_LEAF_F16 selects (the other one is freed): FP16 hi/lo
-// tiles + per-row scales (s0_h16_kernel), or TF32 hi/lo tiles (s0_tc_kernel).  Without memory for it the
-// SIMT S0 serves the plan.
-bf_status_t build_s0_image(bf_plan_s* p, Shard& s)
+// The tensor-core leaf images in the format BF_OPT_LEAF_F16 selects (the other format is freed): FP16
+// hi/lo tiles + per-row exponents (s0_h16_kernel, sl_h16_kernel where the shape fits), or TF32 hi/lo
+// tiles (s0_tc_kernel, sl_tc_kernel).  Without memory for an image the SIMT kernel serves that stage.
+bf_status_t build_leaf_images(bf_plan_s* p, Shard& s)
 {
     const bfk::Dims dl = p->local();
-    cudaFree(s.v0x);
-    cudaFree(s.v0h);
-    cudaFree(s.v0s);
-    s.v0x = nullptr;
-    s.v0h = nullptr;
-    s.v0s = nullptr;
-    cudaError_t e;
-    if (p->leaf_f16) {
-        if (cudaMalloc(&s.v0h, size_t(bfk::leafx_floats(dl)) * 2) != cudaSuccess ||
-            cudaMalloc(&s.v0s, size_t(bfk::leafh_rows(dl))) != cudaSuccess) {
-            cudaGetLastError();
-            cudaFree(s.v0h);
-            cudaFree(s.v0s);
-            s.v0h = nullptr;
-            s.v0s = nullptr;
-            return BF_OK;
-        }
-        e = bfk::expand_s0_h16(dl, s.v0, s.v0h, s.v0s, 0);
-    } else {
-        if (cudaMalloc(&s.v0x, size_t(bfk::leafx_floats(dl)) * sizeof(float)) != cudaSuccess) {
-            cudaGetLastError();
-            s.v0x = nullptr;
-            return BF_OK;
-        }
-        e = bfk::expand_leaf_weights(dl, s.v0, nullptr, s.v0x, nullptr, 0);
+    void** all[] = {reinterpret_cast<void**>(&s.v0x), &s.v0h, &s.v0s, reinterpret_cast<void**>(&s.ux), &s.uh, &s.ue};
+    for (void** x : all) {
+        cudaFree(*x);
+        *x = nullptr;
     }
-    return e == cudaSuccess ? BF_OK : cuda_fail(e, "S0 weight image");
+    const size_t lx = size_t(bfk::leafx_floats(dl));
+    auto alloc = [](void** x, size_t bytes) {
+        if (cudaMalloc(x, bytes) == cudaSuccess) return true;
+        cudaGetLastError();
+        *x = nullptr;
+        return false;
+    };
+    cudaError_t e = cudaSuccess;
+    if (p->leaf_f16) {
+        if (alloc(&s.v0h, lx * 2) && alloc(&s.v0s, size_t(bfk::leafh_rows(dl))))
+            e = bfk::expand_s0_h16(dl, s.v0, s.v0h, s.v0s, 0);
+        else {
+            cudaFree(s.v0h);
+            s.v0h = nullptr;
+        }
+        if (e == cudaSuccess && bfk::sl_h16_shape(dl)) {
+            if (alloc(&s.uh, lx * 2) && alloc(&s.ue, size_t(bfk::leafu_rows(dl))))
+                e = bfk::expand_sl_h16(dl, s.u, s.uh, s.ue, 0);
+            else {
+                cudaFree(s.uh);
+                s.uh = nullptr;
+            }
+        } else if (e == cudaSuccess && alloc(reinterpret_cast<void**>(&s.ux), lx * sizeof(float))) {
+            e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
+        }
+    } else {
+        if (alloc(reinterpret_cast<void**>(&s.v0x), lx * sizeof(float)))
+            e = bfk::expand_leaf_weights(dl, s.v0, s.u, s.v0x, nullptr, 0);
+        if (e == cudaSuccess && alloc(reinterpret_cast<void**>(&s.ux), lx * sizeof(float)))
+            e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
+    }
+    return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf weight images");
 }
 }  // namespace
 
@@ -802,17 +818,8 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
     // tensor-core leaf weights: only when a chunk can be a dense contraction (nv >= 64 vectors)
     const bfk::Dims dl = p->local();
     if (p->tensor_cores && bfk::leaf_tc_shape(dl) && p->max_chunk * p->d.n_amp >= 64) {
-        const size_t bytes = size_t(bfk::leafx_floats(dl)) * sizeof(float);
-        for (Shard& s : p->sh) {
-            if (cudaMalloc(&s.ux, bytes) != cudaSuccess) {
-                cudaGetLastError();   // not enough device memory: the SIMT leaf kernels serve this plan
-                s.ux = nullptr;
-                continue;
-            }
-            e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
-            if (e != cudaSuccess) return cuda_fail(e, "leaf weight expansion");
-            if (bf_status_t st = build_s0_image(p, s); st != BF_OK) return st;
-        }
+        for (Shard& s : p->sh)
+            if (bf_status_t st = build_leaf_images(p, s); st != BF_OK) return st;
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e, "leaf weight expansion");
     }
@@ -984,6 +991,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
         if (s.v0x) info->tc_weight_bytes += lx * int64_t(sizeof(float));
         if (s.ux) info->tc_weight_bytes += lx * int64_t(sizeof(float));
         if (s.v0h) info->tc_weight_bytes += lx * 2 + bfk::leafh_rows(p->local());
+        if (s.uh) info->tc_weight_bytes += lx * 2 + bfk::leafu_rows(p->local());
     }
     {
         const bfk::Dims dl = p->local();
@@ -991,7 +999,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
         int mask = 0;
         if (p->tensor_cores && (p->sh[0].v0x || p->sh[0].v0h) && bfk::s0_tc_supported(dl, nvf, dl.N))
             mask |= 1 << bfk::KC_S0;
-        if (p->tensor_cores && p->sh[0].ux && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
+        if (p->tensor_cores && (p->sh[0].ux || p->sh[0].uh) && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
         if (p->tensor_cores && bfk::band_supported(dl.R, nvf) && bfk::band_tc_supported(dl, nvf))
             for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE))
                 if (stp.kind == Step::BAND && stp.K == 2) mask |= 1 << stp.cls;
@@ -1106,8 +1114,8 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
         cudaError_t e = cudaDeviceSynchronize();   // no apply may still read the old image
         if (e != cudaSuccess) return cuda_fail(e, "leaf image switch");
         for (Shard& s : p->sh)
-            if (s.v0x || s.v0h)
-                if (bf_status_t st = build_s0_image(p, s); st != BF_OK) return st;
+            if (s.v0x || s.v0h || s.ux || s.uh)
+                if (bf_status_t st = build_leaf_images(p, s); st != BF_OK) return st;
         e = cudaDeviceSynchronize();
         return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf image switch");
     }

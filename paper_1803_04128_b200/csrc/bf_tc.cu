@@ -634,11 +634,8 @@ __global__ void __launch_bounds__(448, 1)
 #pragma unroll
                     for (int h = 0; h < 2; h++) {
                         if (!ok) y[h] = make_float2(0.f, 0.f);
-                        float hr, lr, hm, lm;
-                        tc::split_h(y[h].x * sc, hr, lr);
-                        tc::split_h(y[h].y * sc, hm, lm);
-                        hi[jj + h] = tc::pack_h2(hr, hm);   // column j = (re, im) of complex j: K index 2j, 2j + 1
-                        lo[jj + h] = tc::pack_h2(lr, lm);
+                        // column j = (re, im) of complex j: K index 2j, 2j + 1
+                        tc::split_h2(y[h].x * sc, y[h].y * sc, hi[jj + h], lo[jj + h]);
                     }
                 }
                 tc::tmem_st8(tmem + lb + uint32_t(ab * C::A_BUF + j0), hi);
@@ -1054,6 +1051,345 @@ cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const
     SLTC_NA(6, 64, 2) SLTC_NA(8, 64, 2) SLTC_NA(10, 64, 2) SLTC_NA(12, 64, 1) SLTC_NA(16, 64, 1)
     SLTC_NA(6, 32, 2) SLTC_NA(8, 32, 2) SLTC_NA(10, 32, 2) SLTC_NA(12, 32, 1) SLTC_NA(16, 32, 1)
 #undef SLTC_NA
+    return cudaErrorInvalidValue;
+}
+
+// =============================================================================================
+// SL in FP16 split passes (BF_OPT_LEAF_F16 = 1, the default): the structure of sl_tc_kernel with
+// kind::f16 MMAs (K = 16).  Every K chunk (KP pairs of the leaf, KC = KP 2r, a multiple of 16) is its own
+// accumulation segment: the split scales each vector's chunk by 2^{-e_vc} (max |x| in [0.5, 1)) before
+// the FP16 hi / lo split, and the drain adds 2^{e_vc} D_c into the FP32 register sums; the image rows
+// (output point j, re / im) are scaled to max |x| in [0.5, 1) with the exponent applied with a_k at the
+// end of the job.  Half the Ux image bytes, half the tensor time of the 3xTF32 SL.
+// =============================================================================================
+static int sl_kp_h(int R) { return (R == 12) ? 2 : (R == 16 ? 2 : 4); }   // KC = KP 2r multiple of 16
+
+int64_t leafu_rows(const Dims& d) { return d.N; }   // biased exponents of the SL image: one per output point
+
+__global__ void expand_sl_h16_kernel(const float2* __restrict__ U, __half* __restrict__ X, uint8_t* __restrict__ S,
+                                     int LN, int l0, int R, int KP)
+{
+    const int n0 = 1 << l0;
+    const int64_t nleaf = (int64_t(1) << LN) >> l0;
+    const int rows = 2 * n0, K = n0 * 2 * R, KC = KP * 2 * R;
+    const int nch = n0 / KP;
+    const int64_t tile = int64_t(rows) * KC;
+    const int64_t total = nleaf * n0;
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t a = g / n0;
+        const int j = int(g - a * n0);
+        const float2* w = U + (a * n0) * (n0 * R) + j;   // element (b, t): w[b n0 R + t n0]
+        float mx = 0.f;
+        for (int b = 0; b < n0; b++)
+            for (int t = 0; t < R; t++) {
+                const float2 x = w[(int64_t(b) * R + t) * n0];
+                mx = fmaxf(mx, fmaxf(fabsf(x.x), fabsf(x.y)));
+            }
+        int e = 0;
+        frexpf(mx, &e);
+        e = max(-126, min(126, e));
+        S[a * n0 + j] = uint8_t(e + 127);
+        for (int cp = 0; cp < 2; cp++) {
+            const int n = 2 * j + cp;
+            for (int k = 0; k < K; k++) {
+                const int b = k / (2 * R), t = (k / 2) % R, c = k & 1;
+                const float x = ldexpf(embed(w[(int64_t(b) * R + t) * n0], cp, c), -e);
+                float hi, lo;
+                tc::split_h(x, hi, lo);
+                const int ch = b / KP, kk = k - ch * KC;
+                __half* tl = X + ((a * nch + ch) * 2) * tile;
+                const uint32_t off = tc::kmaj_off16(n, kk, rows) / 2;
+                tl[off] = __float2half_rn(hi);
+                tl[tile + off] = __float2half_rn(lo);
+            }
+        }
+    }
+}
+
+template <int R, int N0, int NA, int KP>
+struct SLH {
+    static constexpr int NB = 2 * N0;
+    static constexpr int KC = KP * 2 * R;
+    static constexpr int NCH = N0 / KP;
+    static constexpr uint32_t RAW = uint32_t(KP) * R * 128 * 8;
+    static constexpr uint32_t BT = uint32_t(NB) * KC * 2;          // one of hi / lo (FP16)
+    static constexpr uint32_t GS_STRIDE = N0 + 1;
+    static constexpr uint32_t GS_BYTES = uint32_t(128 / NA) * GS_STRIDE * 8;
+    static constexpr uint32_t AS_BYTES = uint32_t(NA) * N0 * 8;
+    static constexpr uint32_t ES_BYTES = 4 * 128 * 4;
+    static constexpr size_t LIM = 232448 - 1024;
+    static constexpr int NR_FIT = int((LIM - GS_BYTES - AS_BYTES - ES_BYTES) / (RAW + 2 * BT));
+    static constexpr int NR = NR_FIT > 4 ? 4 : (NR_FIT < 2 ? 2 : NR_FIT);   // ring depth
+    static constexpr uint32_t OFF_B = NR * RAW, OFF_GS = OFF_B + 2 * NR * BT, OFF_AS = OFF_GS + GS_BYTES;
+    static constexpr uint32_t OFF_ES = OFF_AS + AS_BYTES;
+    static constexpr size_t SMEM = size_t(OFF_ES) + ES_BYTES;
+    static constexpr int A_COLS = KC;                                   // hi KC/2 packed columns, then lo
+    static constexpr int D_OFF = 2 * A_COLS;
+    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * NB>();
+    // shapes that fit (otherwise the plan keeps the 3xTF32 SL): whole kind::f16 K steps, a ring of >= 2
+    static constexpr bool OK = KC % 16 == 0 && NR_FIT >= 2 && D_OFF + 2 * NB <= 512 && SMEM <= LIM;
+};
+
+template <int R, int N0, int NA, int KP>
+__global__ void __launch_bounds__(448, 1)
+    sl_h16_kernel(const __grid_constant__ CUtensorMap tin, const __half* __restrict__ Uh,
+                  const uint8_t* __restrict__ Ue, const float2* __restrict__ ampa, float2* __restrict__ G, int64_t ldg,
+                  int LN, int nv, int nvt)
+{
+    using C = SLH<R, N0, NA, KP>;
+    extern __shared__ __align__(128) uint8_t sm_slh[];
+    auto raw = [&](int e) { return sm_slh + e * C::RAW; };
+    auto opB = [&](int e, int lo) { return sm_slh + C::OFF_B + (2 * e + lo) * C::BT; };
+    float2* Gs = reinterpret_cast<float2*>(sm_slh + C::OFF_GS);   // [128/NA][GS_STRIDE]
+    float2* As = reinterpret_cast<float2*>(sm_slh + C::OFF_AS);   // [NA][N0] a_k(x) of the current job
+    float* Es = reinterpret_cast<float*>(sm_slh + C::OFF_ES);      // [chunk % 4][128] 2^{e_vc}
+    __shared__ uint64_t raw_full[C::NR], raw_empty[C::NR], b_full[C::NR], b_empty[C::NR], a_full[2], a_empty[2],
+        dfull[2], dempty[2], e_full[4], e_empty[4];
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t N = int64_t(1) << LN;
+    const int64_t njobs_all = (N / N0) * nvt;
+    const int njobs = int((njobs_all - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const int nch_all = njobs * C::NCH;
+
+    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < C::NR; i++) {
+            tc::mbar_init(&raw_full[i], 1);
+            tc::mbar_init(&raw_empty[i], 128);
+            tc::mbar_init(&b_full[i], 1);
+            tc::mbar_init(&b_empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&a_full[i], 128);
+            tc::mbar_init(&a_empty[i], 1);
+            tc::mbar_init(&dfull[i], 1);
+            tc::mbar_init(&dempty[i], 256);
+        }
+        for (int i = 0; i < 4; i++) {
+            tc::mbar_init(&e_full[i], 128);
+            tc::mbar_init(&e_empty[i], 256);
+        }
+        tc::mbar_fence_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 12) {
+        // ---- loader: the chunk stream of all this CTA's jobs (Ux tiles: bulk copy; delta rows: 2-D TMA) ----
+        if (lane == 0) {
+            for (int gch = 0; gch < nch_all; gch++) {
+                const int jl = gch / C::NCH, ch = gch - jl * C::NCH;
+                const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
+                const int64_t a = job / unsigned(nvt);
+                const int v0 = int(job % unsigned(nvt)) * 128;
+                const int e = gch % C::NR, use = gch / C::NR;
+                if (use > 0) tc::mbar_wait(&raw_empty[e], (use - 1) & 1);
+                tc::mbar_arrive_expect_tx(&raw_full[e], C::RAW);
+                const int64_t p0 = a * N0 + int64_t(ch) * KP;
+                tc::tma_load_2d(raw(e), &tin, 2 * v0, int(p0 * R), &raw_full[e]);
+                if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
+                tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
+                tc::bulk_g2s(opB(e, 0), Uh + (a * C::NCH + ch) * 2 * (C::BT / 2), 2 * C::BT, &b_full[e]);
+            }
+        }
+    } else if (warp == 13) {
+        // ---- MMA issuer: one accumulation segment per chunk, 3 passes x KC/16 kind::f16 MMAs ----
+        constexpr uint32_t idesc = tc::idesc_f16(128, C::NB);
+        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
+        const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(opB(0, 0)), LBO_B);
+        for (int gch = 0; gch < nch_all; gch++) {
+            const int e = gch % C::NR, sa = gch & 1, slot = gch & 1;
+            if (gch >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gch >> 1) - 1) & 1);
+            tc::mbar_wait(&a_full[sa], uint32_t(gch >> 1) & 1);
+            tc::mbar_wait(&b_full[e], uint32_t(gch / C::NR) & 1);
+            tc::fence_after_sync();
+            const uint32_t d = tmem + uint32_t(C::D_OFF + slot * C::NB);
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                const int pass = kPassOrder[q];
+                const uint32_t aa = tmem + uint32_t(sa * C::A_COLS + (pass == 1 ? C::KC / 2 : 0));
+                const uint64_t bb = tc::desc_add(dB0, (2 * e + (pass == 2)) * C::BT);
+#pragma unroll
+                for (int ks = 0; ks < C::KC / 16; ks++)
+                    tc::mma_f16_ts_warp(d, aa + ks * 8, tc::desc_add(bb, ks * 2 * LBO_B), idesc, (q | ks) ? 1u : 0u);
+            }
+            tc::commit_warp(&a_empty[sa]);
+            tc::commit_warp(&b_empty[e]);
+            tc::commit_warp(&dfull[slot]);
+            __syncwarp();
+        }
+    } else if (warp < 4) {
+        // ---- split: raw delta rows of a chunk, scaled by 2^{-e_vc}, FP16 hi / lo packed into TMEM ----
+        const int v = tid;
+        const uint32_t lb = uint32_t(warp * 32) << 16;
+        for (int gch = 0; gch < nch_all; gch++) {
+            const int e = gch % C::NR, sa = gch & 1, eb = gch & 3;
+            tc::mbar_wait(&raw_full[e], uint32_t(gch / C::NR) & 1);
+            if (gch >= 2) tc::mbar_wait(&a_empty[sa], uint32_t((gch >> 1) - 1) & 1);
+            if (gch >= 4) tc::mbar_wait(&e_empty[eb], uint32_t((gch >> 2) - 1) & 1);
+            tc::fence_after_sync();
+            const float2* rd = reinterpret_cast<const float2*>(raw(e));   // [KP R][128]
+            float mx = 0.f;
+#pragma unroll
+            for (int row = 0; row < KP * R; row++) {
+                const float2 x = rd[row * 128 + v];
+                mx = fmaxf(mx, fmaxf(fabsf(x.x), fabsf(x.y)));
+            }
+            int ex = 0;
+            frexpf(mx, &ex);
+            ex = max(-126, min(126, ex));
+            const float sc = ldexpf(1.f, -ex);
+            Es[eb * 128 + v] = ldexpf(1.f, ex);
+            tc::mbar_arrive(&e_full[eb]);
+            float hi[C::KC / 2], lo[C::KC / 2];   // packed column (pl, t) = pl R + t: (re, im)
+#pragma unroll
+            for (int row = 0; row < KP * R; row++) {
+                const float2 x = rd[row * 128 + v];
+                tc::split_h2(x.x * sc, x.y * sc, hi[row], lo[row]);
+            }
+            tc::fence_before_sync();
+            tc::mbar_arrive(&raw_empty[e]);
+            const uint32_t ta = tmem + lb + uint32_t(sa * C::A_COLS);
+            tc::tmem_st_cols<C::KC / 2>(ta, hi);
+            tc::tmem_st_cols<C::KC / 2>(ta + C::KC / 2, lo);
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&a_full[sa]);
+        }
+    } else {
+        // ---- drain + epilogue (warps 4-11): lane quarter warp % 4 = vectors, column half (warp - 4) / 4 ----
+        constexpr int HC = C::NB / 2;   // columns per drain thread (j in a half of the leaf)
+        const int q4 = warp & 3, half = (warp - 4) >> 2, vl = q4 * 32 + lane, dt = (warp - 4) * 32 + lane;
+        const int k = vl % NA, cl = vl / NA;
+        int gch = 0;
+        for (int jl = 0; jl < njobs; jl++) {
+            const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
+            const int64_t a = job / unsigned(nvt);
+            const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
+            // this thread's output points j = half HC/2 .. + HC/2: their image row exponents (read now, used at
+            // the end of the job)
+            uint32_t rexp[HC / 8];
+#pragma unroll
+            for (int u = 0; u < HC / 8; u++)
+                rexp[u] = __ldg(reinterpret_cast<const uint32_t*>(Ue + a * N0 + half * (HC / 2)) + u);
+            float sum[HC];
+#pragma unroll
+            for (int i = 0; i < HC; i++) sum[i] = 0.f;
+            for (int ch = 0; ch < C::NCH; ch++, gch++) {
+                const int slot = gch & 1, eb = gch & 3;
+                tc::mbar_wait(&e_full[eb], uint32_t(gch >> 2) & 1);
+                const float sv = Es[eb * 128 + vl];
+                tc::mbar_arrive(&e_empty[eb]);
+                tc::mbar_wait(&dfull[slot], uint32_t(gch >> 1) & 1);
+                tc::fence_after_sync();
+                const uint32_t taddr =
+                    tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * C::NB + half * HC);
+#pragma unroll
+                for (int c0 = 0; c0 < HC; c0 += 32) {
+                    float x[32];
+                    tc::tmem_ld_cols<(HC < 32 ? HC : 32)>(taddr + c0, x);
+                    tc::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < (HC < 32 ? HC : 32); i++) sum[c0 + i] = fmaf(x[i], sv, sum[c0 + i]);
+                }
+                tc::fence_before_sync();
+                tc::mbar_arrive(&dempty[slot]);
+            }
+            // epilogue of the job: 2^{e_j} a_k(x) (staged per job), sum over k, G transposed through Gs
+            asm volatile("bar.sync 1, 256;" ::: "memory");   // the previous job's copy-out is done with Gs / As
+            for (int i = dt; i < NA * N0; i += 256) As[i] = __ldg(ampa + (i / N0) * N + a * N0 + (i % N0));
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll
+            for (int jj = 0; jj < HC / 2; jj++) {
+                const int j = half * (HC / 2) + jj;
+                const uint32_t be = (rexp[jj >> 2] >> (8 * (jj & 3))) & 0xffu;
+                const float sj = __uint_as_float(be << 23);
+                float2 g = cmul_tc(As[k * N0 + j], make_float2(sum[2 * jj] * sj, sum[2 * jj + 1] * sj));
+#pragma unroll
+                for (int m = 1; m < NA; m <<= 1) {
+                    g.x += __shfl_xor_sync(0xffffffffu, g.x, m);
+                    g.y += __shfl_xor_sync(0xffffffffu, g.y, m);
+                }
+                if ((j % NA) == k) Gs[cl * C::GS_STRIDE + j] = g;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            const int c0 = v0 / NA, cw = vw / NA;
+            for (int idx = dt; idx < cw * N0; idx += 256) {
+                const int cc = idx / N0, j = idx % N0;
+                G[a * N0 + j + int64_t(c0 + cc) * ldg] = Gs[cc * C::GS_STRIDE + j];
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+    }
+}
+
+template <int R, int N0, int NA, int KP>
+static cudaError_t sl_h16_go(const Dims& d, const float2* in, const __half* Uh, const uint8_t* Ue, const float2* ampa,
+                             float2* G, int64_t ldg, int nv, cudaStream_t s)
+{
+    using C = SLH<R, N0, NA, KP>;
+    if constexpr (!C::OK) {
+        return cudaErrorInvalidValue;
+    } else {
+    auto kern = sl_h16_kernel<R, N0, NA, KP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    const int nvt = (nv + 127) / 128;
+    const int64_t jobs = (d.N / N0) * nvt;
+    const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
+    CUtensorMap tin;
+    e = make_rows_tmap(&tin, in, d.N * R, nv, KP * R);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 448, C::SMEM, s>>>(tin, Uh, Ue, ampa, G, ldg, d.LN, nv, nvt);
+    return cudaGetLastError();
+    }
+}
+
+bool sl_h16_shape(const Dims& d)
+{
+    const int n0 = 1 << d.l0;
+#define SLH_OK(RR, N0_, KP_)                                                                     \
+    if (d.R == RR && n0 == N0_)                                                                  \
+        return d.n_amp == 1 ? SLH<RR, N0_, 1, KP_>::OK                                           \
+                            : (d.n_amp == 2 ? SLH<RR, N0_, 2, KP_>::OK : (d.n_amp == 4 && SLH<RR, N0_, 4, KP_>::OK));
+    SLH_OK(6, 64, 4) SLH_OK(8, 64, 4) SLH_OK(10, 64, 4) SLH_OK(12, 64, 2) SLH_OK(16, 64, 2)
+    SLH_OK(6, 32, 4) SLH_OK(8, 32, 4) SLH_OK(10, 32, 4) SLH_OK(12, 32, 2) SLH_OK(16, 32, 2)
+#undef SLH_OK
+    return false;
+}
+
+cudaError_t expand_sl_h16(const Dims& d, const float2* U, void* Uh, void* Ue, cudaStream_t s)
+{
+    if (!leaf_tc_shape(d)) return cudaErrorInvalidValue;
+    expand_sl_h16_kernel<<<148 * 16, 128, 0, s>>>(U, static_cast<__half*>(Uh), static_cast<uint8_t*>(Ue), d.LN, d.l0,
+                                                  d.R, sl_kp_h(d.R));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sl_h16(const Dims& d, const float2* in, const void* Uh, const void* Ue, const float2* ampa,
+                          float2* G, int64_t ldg, int nv, cudaStream_t s)
+{
+    const int n0 = 1 << d.l0;
+    const __half* X = static_cast<const __half*>(Uh);
+    const uint8_t* E8 = static_cast<const uint8_t*>(Ue);
+#define SLH_NA(RR, N0_, KP_)                                                                        \
+    if (d.R == RR && n0 == N0_) {                                                                   \
+        if (d.n_amp == 1) return sl_h16_go<RR, N0_, 1, KP_>(d, in, X, E8, ampa, G, ldg, nv, s);    \
+        if (d.n_amp == 2) return sl_h16_go<RR, N0_, 2, KP_>(d, in, X, E8, ampa, G, ldg, nv, s);    \
+        if (d.n_amp == 4) return sl_h16_go<RR, N0_, 4, KP_>(d, in, X, E8, ampa, G, ldg, nv, s);    \
+    }
+    SLH_NA(6, 64, 4) SLH_NA(8, 64, 4) SLH_NA(10, 64, 4) SLH_NA(12, 64, 2) SLH_NA(16, 64, 2)
+    SLH_NA(6, 32, 4) SLH_NA(8, 32, 4) SLH_NA(10, 32, 4) SLH_NA(12, 32, 2) SLH_NA(16, 32, 2)
+#undef SLH_NA
     return cudaErrorInvalidValue;
 }
 

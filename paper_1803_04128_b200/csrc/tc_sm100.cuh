@@ -79,6 +79,16 @@ __device__ __forceinline__ float pack_h2(float lo_elem, float hi_elem)
                        (uint32_t(__half_as_ushort(__float2half_rn(hi_elem))) << 16);
     return __uint_as_float(u);
 }
+// FP16 split of a complex value (re, im), already scaled: hi = fp16 pair, lo = fp16 pair of the residuals,
+// both packed (re in the low half: K index 2j, im: 2j + 1) -- one pack conversion per part
+__device__ __forceinline__ void split_h2(float re, float im, float& hi, float& lo)
+{
+    const __half2 h = __floats2half2_rn(re, im);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(re - hf.x, im - hf.y);
+    hi = __uint_as_float(*reinterpret_cast<const uint32_t*>(&h));
+    lo = __uint_as_float(*reinterpret_cast<const uint32_t*>(&l));
+}
 // FP16 split of x (|x| <= 1 after the caller's power-of-two scaling): hi = fp16(x), lo = fp16(x - hi)
 __device__ __forceinline__ void split_h(float x, float& hi, float& lo)
 {

@@ -186,15 +186,16 @@ def test_tc_band_composed(r, l0, LN, nrhs):
                                                      (W.K_FIO_JUMP, W.A_CFG3, 12, 5, 16, 32),
                                                      (W.K_DFT, W.A_ONE, 12, 6, 6, 70)])
 def test_tc_leaf_f16_vs_tf32(kernel, amp, LN, l0, r, nrhs):
-    """BF_OPT_LEAF_F16 (default 1): S0 in FP16 split passes with per-row power-of-two scaling; 0: 3xTF32.
-    Both meet the oracle bar and agree with each other like the two FP32-accurate paths do."""
+    """BF_OPT_LEAF_F16 (default 1): S0 and SL in FP16 split passes with per-row / per-chunk power-of-two
+    scaling; 0: 3xTF32.  Both meet the oracle bar and agree with each other like the two FP32-accurate
+    paths do."""
     F = W.rhs(1 << LN, nrhs, 60 + r)
     plan = bf.Plan.build_fio(bf.fio(kernel, amp, LN, l0, r), max_nrhs_chunk=nrhs)
-    assert "s0" in plan.info()["tc_classes"]
+    assert {"s0", "sl"} <= set(plan.info()["tc_classes"])
     bytes_f16 = plan.info()["tc_weight_bytes"]
     G16 = _apply(plan, F)
     plan.set_option(bf.BF_OPT_LEAF_F16, 0)
-    assert "s0" in plan.info()["tc_classes"] and plan.info()["tc_weight_bytes"] > bytes_f16
+    assert {"s0", "sl"} <= set(plan.info()["tc_classes"]) and plan.info()["tc_weight_bytes"] > bytes_f16
     G32 = _apply(plan, F)
     with pytest.raises(bf.BFError):
         plan.set_option(bf.BF_OPT_LEAF_F16, 2)
