@@ -37,9 +37,9 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
 def _peaks():
-    """HBM GB/s and the TF32 tensor peak (TFLOP/s) with their sources.  TF32 = the measured sustained
-    cuBLAS bf16 rate x the guide's nominal tf32/bf16 ratio (1.1 / 2.25): the kernels run inside a
-    ~100 ms step under the power cap (B200_PROFILING.md)."""
+    """HBM GB/s, the TF32 tensor peak (TFLOP/s) and the FP16 one with their sources.  FP16 = the measured
+    sustained cuBLAS bf16 rate (same dense rate for fp16); TF32 = that x the guide's nominal tf32/bf16
+    ratio (1.1 / 2.25): the kernels run inside a ~100 ms step under the power cap (B200_PROFILING.md)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
@@ -49,7 +49,7 @@ def _peaks():
     except Exception:
         hbm, src = 6650.0, "fallback"
         bf16, tsrc = 1400.0, "fallback sustained bf16 1.4 PF x 1.1/2.25"
-    return hbm, src, bf16 * 1.1 / 2.25, tsrc
+    return hbm, src, bf16 * 1.1 / 2.25, tsrc, bf16
 
 
 class ClockSampler:
@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exchange", choices=["copy", "fused"], default="copy",
                     help="index-shard exchange: NCCL send/recv step, or peer stores from the level-h launch")
+    ap.add_argument("--leaf-tf32", action="store_true",
+                    help="leaf stages in 3xTF32 instead of FP16 split passes (BF_OPT_LEAF_F16 = 0)")
     ap.add_argument("--band-pipelines", type=int, default=None, choices=[1, 2],
                     help="tensor-core band variant (tuning; default: the library's)")
     args = ap.parse_args()
@@ -244,6 +246,8 @@ def main():
     t_build = time.perf_counter() - t0
     if args.band_pipelines:
         plan.set_option(bf.BF_OPT_BAND_PIPELINES, args.band_pipelines)
+    if args.leaf_tf32:
+        plan.set_option(bf.BF_OPT_LEAF_F16, 0)
     info = plan.info()
     Fd = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()
     Gd = torch.empty_like(Fd)
@@ -278,18 +282,22 @@ def main():
     value = w.n * w.nrhs * jobs / (ms / 1e3)
 
     # ---- roofline of the dominant kernel class ----
-    hbm, hbm_src, tf32, tf32_src = _peaks()
+    hbm, hbm_src, tf32, tf32_src, f16 = _peaks()
     wl = w.with_(log2n=w.log2n - (world.bit_length() - 1)) if args.index_shard else w   # this rank's share
     model = stage_model(wl, min(chunk, w.nrhs) * w.n_amp, info)
     # the level-h exchange moves (G-1)/G of the local coefficients out and as much in
     model["exchange"] = (0, 2 * 8 * wl.n * w.rank * min(chunk, w.nrhs) * w.n_amp * (world - 1) // world)
     tc_classes = set(info["tc_classes"])
+    f16_classes = set(info["f16_classes"])
+
+    def tpeak(k):
+        return f16 if k in f16_classes else tf32
 
     def times(k):
         """(compute seconds, hbm seconds) of one launch of class k at its peaks.  Tensor-core classes
-        issue 3 TF32 products per FP32-accurate product (3xTF32)."""
+        issue 3 split products per FP32-accurate product (3xTF32, or 3 FP16 passes at the fp16 rate)."""
         f, b = model[k]
-        tcomp = 3 * f / (tf32 * 1e12) if k in tc_classes else f / (FP32_PEAK_TFLOPS * 1e12)
+        tcomp = 3 * f / (tpeak(k) * 1e12) if k in tc_classes else f / (FP32_PEAK_TFLOPS * 1e12)
         return tcomp, b / (hbm * 1e9)
 
     dom = max((k for k in ktimes if k != "exchange"), key=lambda k: ktimes[k][0])   # largest share of the step
@@ -301,8 +309,10 @@ def main():
         roof = {"bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm, "unit": "GB/s",
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
     elif dom in tc_classes:
-        roof = {"bound": "tensor", "achieved": 3 * flops / avg_s / 1e12, "peak": tf32, "unit": "TFLOP/s",
-                "peak_source": tf32_src + "; achieved counts the 3 TF32 passes of each algorithmic FP32 flop"}
+        fp16 = dom in f16_classes
+        roof = {"bound": "tensor", "achieved": 3 * flops / avg_s / 1e12, "peak": tpeak(dom), "unit": "TFLOP/s",
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (fp16 dense rate = bf16)" if fp16 else tf32_src)
+                + "; achieved counts the 3 split passes of each algorithmic FP32 flop"}
     else:
         roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "peak_source": "FP32 FFMA from unit counts: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 5)"}
@@ -348,7 +358,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if args.index_shard else "weak",
             "vs_baseline": None,
-            "dtype": "c64 (3xTF32 tcgen05 and FP32 FFMA, FP32 accumulation)" if tc_classes else "c64 (fp32 FFMA)",
+            "dtype": ("c64: tcgen05 split products with FP32 accumulation (" +
+                      ", ".join(f"{k} {'3xFP16' if k in f16_classes else '3xTF32'}" for k in sorted(tc_classes)) + ")")
+                     if tc_classes else "c64 (fp32 FFMA)",
             "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel; factors from the host builder)",
             "config": {"workload": args.config, "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
                        "nrhs_per_gpu": w.nrhs if not args.index_shard else w.nrhs,

@@ -121,6 +121,8 @@ typedef struct {
     int64_t tc_weight_bytes;     /* device bytes of the tensor-core leaf weight images (0 if not built) */
     int32_t tc_class_mask;       /* bit c set: kernel class c (bf_plan_timing numbering) runs on the tensor
                                     cores for a full chunk of max_nrhs_chunk columns */
+    int32_t f16_class_mask;      /* subset of tc_class_mask whose split products are kind::f16 MMAs
+                                    (BF_OPT_LEAF_F16); the others are kind::tf32 */
 } bf_plan_info_t;
 
 /* index sharding modes */

@@ -61,7 +61,7 @@ class bf_plan_info_t(ctypes.Structure):
                 ("device", ctypes.c_int32), ("class_launches", ctypes.c_int32 * 6),
                 ("class_levels", ctypes.c_int32 * 6), ("world", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
                 ("sharding", ctypes.c_int32), ("rows_local", ctypes.c_int64), ("tc_weight_bytes", ctypes.c_int64),
-                ("tc_class_mask", ctypes.c_int32)]
+                ("tc_class_mask", ctypes.c_int32), ("f16_class_mask", ctypes.c_int32)]
 
 
 class bf_fio_t(ctypes.Structure):
@@ -260,6 +260,7 @@ class Plan:
         out["class_launches"] = dict(zip(KCLASS_NAMES, list(i.class_launches)))
         out["class_levels"] = dict(zip(KCLASS_NAMES, list(i.class_levels)))
         out["tc_classes"] = [n for c, n in enumerate(KCLASS_NAMES) if i.tc_class_mask >> c & 1]
+        out["f16_classes"] = [n for c, n in enumerate(KCLASS_NAMES) if i.f16_class_mask >> c & 1]
         return out
 
     def workspace_bytes(self, nrhs_chunk: int) -> int:

@@ -1004,6 +1004,10 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
             for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE))
                 if (stp.kind == Step::BAND && stp.K == 2) mask |= 1 << stp.cls;
         info->tc_class_mask = mask;
+        int fmask = 0;
+        if ((mask >> bfk::KC_S0 & 1) && p->sh[0].v0h) fmask |= 1 << bfk::KC_S0;
+        if ((mask >> bfk::KC_SL & 1) && p->sh[0].uh) fmask |= 1 << bfk::KC_SL;
+        info->f16_class_mask = fmask;
     }
     const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp), p->mode != BF_SHARD_NONE);
     info->launches_per_chunk = 0;
