@@ -13,9 +13,9 @@ tail -c 1500 gpurun_out/bench_ref.log
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu_launch=$?"
 CMD2="python bench.py --log2n 16 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"s0_tc|s0_h16|band_tc|band_cmp|sl_tc|sl_h16" -s 6 -c 6 -o gpurun_out/prof_full $CMD2 > gpurun_out/ncu_full.log 2>&1; echo "ncu_full=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"^(s0_tc|s0_h16|band_tc|band_cmp|sl_tc|sl_h16)" -s 6 -c 6 -o gpurun_out/prof_full $CMD2 > gpurun_out/ncu_full.log 2>&1; echo "ncu_full=$?"
 tail -5 gpurun_out/ncu_full.log
 # DRAM traffic per TC kernel at full size (single-pass metrics)
 CMD3="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-  -k regex:"s0_tc|s0_h16|band_tc|band_cmp|sl_tc|sl_h16" -s 6 -c 6 --csv --log-file gpurun_out/traffic.csv $CMD3 > gpurun_out/ncu_traffic.log 2>&1; echo "ncu_traffic=$?"
+  -k regex:"^(s0_tc|s0_h16|band_tc|band_cmp|sl_tc|sl_h16)" -s 6 -c 6 --csv --log-file gpurun_out/traffic.csv $CMD3 > gpurun_out/ncu_traffic.log 2>&1; echo "ncu_traffic=$?"

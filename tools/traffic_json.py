@@ -17,9 +17,21 @@ for r in rows:
     launches.setdefault(r["ID"], {"kernel": r["Kernel Name"]})[r["Metric Name"]] = float(r["Metric Value"])
 seq = list(launches.values())
 assert len(seq) == 6, [s["kernel"][:40] for s in seq]
-classes = ["s0", "xfer_first_half", "xfer_first_half", "xfer_switch", "xfer_second_half", "xfer_second_half"]
-# schedule order at cfg4 (l0 = 6, h = 10, D = 14): S0, bands (7,8), (9,10 + switch), (11,12), (13,14), SL
-classes = ["s0", "xfer_first_half", "xfer_switch", "xfer_second_half", "xfer_second_half", "sl"]
+# classes by name: the leaf kernels by their names; the bands of an apply follow its S0 in schedule order
+# (cfg4: levels (7,8), (9,10 + switch), (11,12), (13,14)); bands before the S0 end the previous apply
+names = [s["kernel"] for s in seq]
+i0 = next(i for i, n in enumerate(names) if " s0_" in n or n.startswith("void s0_"))
+band_order = ["xfer_first_half", "xfer_switch", "xfer_second_half", "xfer_second_half"]
+classes, nb = [], 0
+for i, n in enumerate(names):
+    if "s0_" in n:
+        classes.append("s0")
+    elif "sl_" in n:
+        classes.append("sl")
+    elif i > i0:
+        classes.append(band_order[nb]); nb += 1
+    else:
+        classes.append("xfer_second_half")
 out = {"what": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --metrics (single pass, --clock-control "
                "none), tools/gpu_full.sh: `python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e` (cfg4, "
                "N=2^20, 256 RHS)",
