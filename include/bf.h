@@ -217,6 +217,10 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        DESIGN.md 5); its weight image is half the bytes.  0: the 3xTF32 S0.  Switching
  *                        after creation rebuilds the S0 image (synchronous). */
 #define BF_OPT_LEAF_F16 6
+/*   BF_OPT_BAND_F16      0 (default) / 1: the composed tensor-core band in FP16 split passes (per-vector and
+ *                        per-group power-of-two scaling, kind::f16 MMAs) instead of 3xTF32.  Process-wide
+ *                        tuning knob. */
+#define BF_OPT_BAND_F16 7
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band

@@ -72,6 +72,7 @@ cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2*
 // Diagnostic: SM-clock timeline of the last band_tc launch (CTA 0, first 64 jobs x 12 events).
 cudaError_t band_trace(long long* out, int n);
 void band_set_single_pipeline(int v);
+void band_set_f16(int v);
 void band_trace_window(int j0);
 
 // Plan finalization: W[p] <- Sw[p] W[p] for npairs blocks (W column-major R x cols, Sw R x R).

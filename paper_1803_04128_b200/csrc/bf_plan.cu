@@ -1123,6 +1123,11 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
         e = cudaDeviceSynchronize();
         return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf image switch");
     }
+    if (option == BF_OPT_BAND_F16) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_F16 takes 0 or 1");
+        bfk::band_set_f16(int(value));
+        return BF_OK;
+    }
     if (option == BF_OPT_BAND_COMPOSE) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_COMPOSE takes 0 or 1");
         p->band_compose = value != 0;

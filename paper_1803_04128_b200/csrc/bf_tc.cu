@@ -1399,6 +1399,9 @@ cudaError_t launch_sl_h16(const Dims& d, const float2* in, const void* Uh, const
 // the split) slows the tensor pipe on others, and the launch is 1.4x slower overall.
 static int g_band_single_pipeline = 1;
 void band_set_single_pipeline(int v) { g_band_single_pipeline = v; }
+// FP16 split passes in the composed band (experiment knob until measured; process-wide like the above)
+static int g_band_f16 = 0;
+void band_set_f16(int v) { g_band_f16 = v; }
 
 // ---- timeline trace of the band kernel (diagnostic; CTA 0, first BT_JOBS jobs, SM clock) ----
 constexpr int BT_JOBS = 64, BT_EV = 12;
@@ -2319,6 +2322,337 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
+// =============================================================================================
+// Composed band in FP16 split passes (BF_OPT_BAND_F16 = 1).  Same job structure as band_cmp_kernel; the
+// A operand of a job (4 pairs x r coefficients of one vector) is scaled by 2^{-e_v} with e_v from its max
+// (the two split warps of a lane quadrant exchange their halves' maxima through shared memory), the
+// composed block operator C of a group by 2^{-e_g} (its max), both split into FP16 hi + lo and multiplied
+// with kind::f16 MMAs (K = 16): half the MMAs, half the TMEM stores and half the B bytes of the 3xTF32
+// band.  The epilogue multiplies by 2^{e_v + e_g}.
+// =============================================================================================
+template <int R>
+struct BandH {
+    using B = BandCmp<R>;
+    static constexpr int P = 4, SC = 2 * R, KB = P * SC, NB = KB;
+    static constexpr int ACOLS = KB;                                  // hi KB/2 packed columns, then lo
+    static constexpr int NABUF = 2, NDBUF = 2;
+    static constexpr int D_OFF = NABUF * ACOLS;
+    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + NDBUF * NB>();
+    static constexpr uint32_t SLOT = B::SLOT, BLK = B::BLK, WST = B::WST;
+    static constexpr uint32_t WT = uint32_t(NB) * KB * 2;             // one FP16 B tile (hi or lo)
+    static constexpr uint32_t WSET = 2 * WT;
+    static constexpr uint32_t CST = uint32_t(P) * P * R * R * 8;      // the composed C (FP32 complex)
+    static constexpr uint32_t XCH = 2 * 2 * 128 * 4 + 4 * 128 * 4 + 4 * 4;   // maxima exchange, e_v ring, e_g ring
+    static constexpr size_t LIM = 232448 - 1024;
+    static constexpr int NQ_FIT = int((LIM - 2 * size_t(WST) - CST - 2 * size_t(WSET) - XCH) / SLOT);
+    static constexpr int NQ = NQ_FIT > 16 ? 16 : NQ_FIT;
+    static constexpr uint32_t OFF_WST = uint32_t(NQ) * SLOT;
+    static constexpr uint32_t OFF_CST = OFF_WST + 2 * WST;
+    static constexpr uint32_t OFF_W = OFF_CST + CST;
+    static constexpr uint32_t OFF_X = OFF_W + 2 * WSET;
+    static constexpr size_t SMEM = size_t(OFF_X) + XCH;
+    static constexpr int ITEMS = P * P * R * 2;
+    static_assert(KB % 16 == 0 && D_OFF + NDBUF * NB <= 512 && OFF_W % 128 == 0 && WT % 128 == 0 && NQ >= 6 &&
+                      SMEM <= LIM, "FP16 band shape");
+};
+
+template <int R>
+__global__ void __launch_bounds__(512, 1)
+    band_h16_kernel(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ W1,
+                    const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg, const bfs::PeerOut po)
+{
+    using C = BandH<R>;
+    extern __shared__ __align__(128) uint8_t sm_bh[];
+    __shared__ uint64_t slot_full[16], slot_empty[16];
+    __shared__ uint64_t a_ready[2], a_free[2], d_full[2], d_free[2], w_full[2], w_free[2], wst_full[2];
+    __shared__ uint64_t e_full[4], e_empty[4], g_full[4], g_empty[4];
+    __shared__ float red[2];
+    __shared__ uint32_t tmem_base;
+    float* Mx = reinterpret_cast<float*>(sm_bh + C::OFF_X);           // [J & 1][half][128] split maxima
+    float* Ev = Mx + 2 * 2 * 128;                                      // [J & 3][128] 2^{e_v}
+    float* Eg = Ev + 4 * 128;                                          // [group & 3] 2^{e_g}
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t N = int64_t(1) << LN;
+    const int lin = l_first - 1, shg = LN - lin - 2;
+    const int64_t ngroups = N >> 2;
+    const int nvt = (nv + 127) / 128;
+    const int nit = int((ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const int njobs = nit * nvt;
+
+    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < C::NQ; i++) {
+            tc::mbar_init(&slot_full[i], 1);
+            tc::mbar_init(&slot_empty[i], 128);
+        }
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&a_ready[i], 256);
+            tc::mbar_init(&a_free[i], 1);
+            tc::mbar_init(&d_full[i], 1);
+            tc::mbar_init(&d_free[i], 128);
+            tc::mbar_init(&w_full[i], 64);
+            tc::mbar_init(&w_free[i], 1);
+            tc::mbar_init(&wst_full[i], 1);
+        }
+        for (int i = 0; i < 4; i++) {
+            tc::mbar_init(&e_full[i], 128);
+            tc::mbar_init(&e_empty[i], 128);
+            tc::mbar_init(&g_full[i], 64);
+            tc::mbar_init(&g_empty[i], 128);
+        }
+        tc::mbar_fence_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base;
+
+    if (warp < 8) {
+        // ---- split (two warps per lane quadrant, one per half of the group's 4 pair slots) ----
+        const int qd = warp & 3, hs = warp >> 2;
+        const int v = qd * 32 + lane;
+        const uint32_t lb = uint32_t(qd * 32) << 16;
+        for (int J = 0; J < njobs; J++) {
+            const int ab = J & 1, use = J >> 1, eb = J & 3;
+            if (use > 0) tc::mbar_wait(&a_free[ab], uint32_t(use - 1) & 1);
+            if (hs == 0 && J >= 4) tc::mbar_wait(&e_empty[eb], uint32_t((J >> 2) - 1) & 1);
+            tc::fence_after_sync();
+            float mx = 0.f;
+#pragma unroll 1
+            for (int s = 2 * hs; s < 2 * hs + 2; s++) {
+                const int k = J * C::P + s, q = k % C::NQ;
+                tc::mbar_wait(&slot_full[q], uint32_t(k / C::NQ) & 1);
+                const float2* rd = reinterpret_cast<const float2*>(sm_bh + q * C::SLOT);
+#pragma unroll
+                for (int t = 0; t < R; t++) {
+                    const float2 x = rd[t * 128 + v];
+                    mx = fmaxf(mx, fmaxf(fabsf(x.x), fabsf(x.y)));
+                }
+            }
+            Mx[(ab * 2 + hs) * 128 + v] = mx;
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + qd) : "memory");   // the two warps of this quadrant
+            mx = fmaxf(mx, Mx[(ab * 2 + (hs ^ 1)) * 128 + v]);
+            int e = 0;
+            frexpf(mx, &e);
+            e = max(-126, min(126, e));
+            const float sc = ldexpf(1.f, -e);
+            if (hs == 0) {
+                Ev[eb * 128 + v] = ldexpf(1.f, e);
+                tc::mbar_arrive(&e_full[eb]);
+            }
+            float hi[2 * R], lo[2 * R];   // this half's two pair slots, packed (re, im) columns
+#pragma unroll
+            for (int s2 = 0; s2 < 2; s2++) {
+                const int k = J * C::P + 2 * hs + s2, q = k % C::NQ;
+                const float2* rd = reinterpret_cast<const float2*>(sm_bh + q * C::SLOT);
+#pragma unroll
+                for (int t = 0; t < R; t++) {
+                    const float2 x = rd[t * 128 + v];
+                    tc::split_h2(x.x * sc, x.y * sc, hi[s2 * R + t], lo[s2 * R + t]);
+                }
+                tc::mbar_arrive(&slot_empty[q]);
+            }
+            const uint32_t ta = tmem + lb + uint32_t(ab * C::ACOLS + 2 * hs * R);
+            tc::tmem_st_cols<2 * R>(ta, hi);
+            tc::tmem_st_cols<2 * R>(ta + C::KB / 2, lo);
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&a_ready[ab]);
+        }
+    } else if (warp < 12) {
+        // ---- epilogue (4 warps): drain the accumulator row in halves, scale by 2^{e_v + e_g}, store ----
+        const int q = warp & 3;
+        const int v = q * 32 + lane;
+        const uint32_t lb = uint32_t(q * 32) << 16;
+        float sg = 1.f;
+        for (int J = 0; J < njobs; J++) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+            const int db = J & 1, eb = J & 3;
+            if (vt == 0) {
+                tc::mbar_wait(&g_full[it & 3], uint32_t(it >> 2) & 1);
+                sg = Eg[it & 3];
+                tc::mbar_arrive(&g_empty[it & 3]);
+            }
+            tc::mbar_wait(&e_full[eb], uint32_t(J >> 2) & 1);
+            const float s2 = Ev[eb * 128 + v] * sg;
+            tc::mbar_arrive(&e_empty[eb]);
+            tc::mbar_wait(&d_full[db], uint32_t(J >> 1) & 1);
+            tc::fence_after_sync();
+            const int vg = vt * 128 + v;
+            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+#pragma unroll 1
+            for (int hf = 0; hf < 2; hf++) {
+                float d[2 * C::SC];
+                tc::tmem_ld_cols<2 * C::SC>(tmem + lb + uint32_t(C::D_OFF + db * C::NB + hf * 2 * C::SC), d);
+                tc::tmem_wait_ld();
+                if (hf == 1) {
+                    tc::fence_before_sync();
+                    tc::mbar_arrive(&d_free[db]);
+                }
+                if (vg < nv) {
+#pragma unroll
+                    for (int oo = 0; oo < 2; oo++) {
+                        const int64_t p = (((a0 << 2) + 2 * hf + oo) << shg) + bq;
+                        float2* o = bfs::pair_out(out, po, p, R, nv) + vg;
+#pragma unroll
+                        for (int t = 0; t < R; t++)
+                            o[int64_t(t) * nv] =
+                                make_float2(d[oo * C::SC + 2 * t] * s2, d[oo * C::SC + 2 * t + 1] * s2);
+                    }
+                }
+            }
+        }
+    } else if (warp == 12) {
+        // ---- loader: one 2-D tensor copy per pair slot ----
+        for (int J = 0; J < njobs; J++) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+            const int64_t pin = rh ? bfs::recv_index(g * C::P, rh, rhg) : g * C::P;
+            for (int s = 0; s < C::P; s++) {
+                const int k = J * C::P + s, q = k % C::NQ;
+                if (k >= C::NQ) tc::mbar_wait(&slot_empty[q], uint32_t(k / C::NQ - 1) & 1);
+                if (lane == 0) {
+                    tc::mbar_arrive_expect_tx(&slot_full[q], C::SLOT);
+                    tc::tma_load_2d(sm_bh + q * C::SLOT, &tin, 2 * vt * 128, int((pin + s) * R), &slot_full[q]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 13) {
+        // ---- MMA issuer: one chain of 3 x (8r / 16) kind::f16 MMAs per job ----
+        constexpr uint32_t idesc = tc::idesc_f16(128, C::NB);
+        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
+        const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_bh + C::OFF_W), LBO_B);
+        for (int J = 0; J < njobs; J++) {
+            const int it = int(unsigned(J) / unsigned(nvt));
+            const int vt = J - it * nvt;
+            const int wb = it & 1, ab = J & 1, db = J & 1;
+            if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it >> 1) & 1);
+            tc::mbar_wait(&a_ready[ab], uint32_t(J >> 1) & 1);
+            if (J >= 2) tc::mbar_wait(&d_free[db], uint32_t((J >> 1) - 1) & 1);
+            tc::fence_after_sync();
+            const uint32_t d = tmem + uint32_t(C::D_OFF + db * C::NB);
+            const uint32_t ahi = tmem + uint32_t(ab * C::ACOLS);
+            const uint64_t bhi = tc::desc_add(dW, wb * C::WSET);
+#pragma unroll
+            for (int qq = 0; qq < 3; qq++) {
+                const int pass = kPassOrder[qq];
+                const uint32_t a = ahi + (pass == 1 ? C::KB / 2 : 0);
+                const uint64_t b = pass == 2 ? tc::desc_add(bhi, C::WT) : bhi;
+#pragma unroll
+                for (int ks = 0; ks < C::KB / 16; ks++)
+                    tc::mma_f16_ts_warp(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc, (qq | ks) ? 1u : 0u);
+            }
+            tc::commit_warp(&d_full[db]);
+            tc::commit_warp(&a_free[ab]);
+            if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
+            __syncwarp();
+        }
+    } else {
+        // ---- weights (warps 14-15): stage compact blocks (bulk, one group ahead), compose C in FP32 into
+        //      shared memory, take the group max, write the scaled FP16 hi / lo B tile ----
+        const int wt = tid - 448;
+        auto stage_group = [&](int it, int sb) {
+            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
+            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+            uint8_t* dst = sm_bh + C::OFF_WST + sb * C::WST;
+            tc::mbar_arrive_expect_tx(&wst_full[sb], C::WST);
+            for (int b = 0; b < 8; b++) {
+                const int m = b >> 2, u = (b >> 1) & 1, e = b & 1;
+                const int64_t p = m == 0 ? ((((a0 << 1) + e) << (LN - lin - 1)) + (bq << 1) + u)
+                                         : ((((a0 << 2) + 2 * u + e) << shg) + bq);
+                tc::bulk_g2s(dst + b * C::BLK * 8, (m == 0 ? W1 : W2) + p * C::BLK, C::BLK * 8, &wst_full[sb]);
+            }
+        };
+        float2* Cs = reinterpret_cast<float2*>(sm_bh + C::OFF_CST);   // [o][t'][i][j]
+        if (wt == 0 && nit > 0) stage_group(0, 0);
+        for (int it = 0; it < nit; it++) {
+            const int wb = it & 1, sb = it & 1, gb = it & 3;
+            if (wt == 0 && it + 1 < nit) stage_group(it + 1, sb ^ 1);
+            tc::mbar_wait(&wst_full[sb], uint32_t(it >> 1) & 1);
+            const float2* st = reinterpret_cast<const float2*>(sm_bh + C::OFF_WST + sb * C::WST);
+            constexpr int H = R / 2;
+            float mx = 0.f;
+#pragma unroll 1
+            for (int item = wt; item < C::ITEMS; item += 64) {
+                const int jh = item & 1, r2 = item >> 1;
+                const int tp = r2 % R, oi = r2 / R, o = oi >> 2, i = oi & 3;
+                const int up = o >> 1, sp = i >> 1, s = i & 1;
+                const float2* L2 = st + (4 + o) * C::BLK + sp * R * R + tp;
+                const float2* L1 = st + (sp * 2 + up) * C::BLK + s * R * R + jh * H * R;
+                float2 c[H];
+#pragma unroll
+                for (int jj = 0; jj < H; jj++) c[jj] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int jp = 0; jp < R; jp += 2) {
+                    const float2 wa = L2[jp * R], wb2 = L2[(jp + 1) * R];
+#pragma unroll
+                    for (int jj = 0; jj < H; jj++) {
+                        const float4 w1 = *reinterpret_cast<const float4*>(L1 + jj * R + jp);
+                        c[jj].x = fmaf(wa.x, w1.x, c[jj].x);
+                        c[jj].y = fmaf(wa.x, w1.y, c[jj].y);
+                        c[jj].x = fmaf(-wa.y, w1.y, c[jj].x);
+                        c[jj].y = fmaf(wa.y, w1.x, c[jj].y);
+                        c[jj].x = fmaf(wb2.x, w1.z, c[jj].x);
+                        c[jj].y = fmaf(wb2.x, w1.w, c[jj].y);
+                        c[jj].x = fmaf(-wb2.y, w1.w, c[jj].x);
+                        c[jj].y = fmaf(wb2.y, w1.z, c[jj].y);
+                    }
+                }
+#pragma unroll
+                for (int jj = 0; jj < H; jj++) {
+                    Cs[((o * R + tp) * 4 + i) * R + jh * H + jj] = c[jj];
+                    mx = fmaxf(mx, fmaxf(fabsf(c[jj].x), fabsf(c[jj].y)));
+                }
+            }
+            // group max over the 64 weight threads
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+            if (lane == 0) red[wt >> 5] = mx;
+            asm volatile("bar.sync 1, 64;" ::: "memory");   // C and the two warp maxima are in shared memory
+            mx = fmaxf(red[0], red[1]);
+            int e = 0;
+            frexpf(mx, &e);
+            e = max(-126, min(126, e));
+            const float sc = ldexpf(1.f, -e);
+            if (it >= 2) tc::mbar_wait(&w_free[wb], uint32_t((it >> 1) - 1) & 1);
+            uint8_t* th = sm_bh + C::OFF_W + wb * C::WSET;
+            uint8_t* tl = th + C::WT;
+            // real embedding of C[o][t'][i][j] at rows n = o 2r + 2t' (+1), K columns k = i 2r + 2j (+1)
+            for (int idx = wt; idx < C::P * R * C::P * R; idx += 64) {
+                const int orow = idx / (C::P * R), icol = idx - orow * (C::P * R);   // (o, t'), (i, j)
+                const int o = orow / R, tp = orow - o * R, i = icol / R, j = icol - i * R;
+                const float2 cv = Cs[((o * R + tp) * 4 + i) * R + j];
+                float hr, hm, lr, lm;   // packed halves: (re, -im) for row n, (im, re) for row n + 1
+                tc::split_h2(cv.x * sc, -cv.y * sc, hr, lr);
+                tc::split_h2(cv.y * sc, cv.x * sc, hm, lm);
+                const int n = o * C::SC + 2 * tp, k = i * C::SC + 2 * j;
+                const uint32_t o0 = tc::kmaj_off16(n, k, C::NB), o1 = tc::kmaj_off16(n + 1, k, C::NB);
+                *reinterpret_cast<float*>(th + o0) = hr;
+                *reinterpret_cast<float*>(tl + o0) = lr;
+                *reinterpret_cast<float*>(th + o1) = hm;
+                *reinterpret_cast<float*>(tl + o1) = lm;
+            }
+            tc::fence_proxy_async();
+            tc::mbar_arrive(&w_full[wb]);
+            if (it >= 4) tc::mbar_wait(&g_empty[gb], uint32_t((it >> 2) - 1) & 1);
+            if (wt == 0) Eg[gb] = ldexpf(1.f, e);
+            tc::mbar_arrive(&g_full[gb]);
+            asm volatile("bar.sync 1, 64;" ::: "memory");   // staging buffer sb and Cs free for the next group
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+    }
+}
+
 template <int R>
 static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
                               cudaStream_t s, int rh, int rhg, const bfs::PeerOut& po, bool compose)
@@ -2326,6 +2660,17 @@ static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, floa
     using C = BandTC<R>;
     const int64_t groups = d.N >> 2;
     const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
+    if (compose && g_band_f16) {
+        using CH = BandH<R>;
+        auto kern = band_h16_kernel<R>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CH::SMEM));
+        if (e != cudaSuccess) return e;
+        CUtensorMap tin;
+        e = make_rows_tmap(&tin, in, d.N * R, nv, R);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, 512, CH::SMEM, s>>>(tin, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
+        return cudaGetLastError();
+    }
     if (compose) {
         using CC = BandCmp<R>;
         auto kern = band_cmp_kernel<R>;

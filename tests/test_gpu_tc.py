@@ -222,3 +222,27 @@ def test_tc_scale_equivariance():
         assert np.all(np.isfinite(Gk))
         assert np.array_equal(Gk, (G * np.float32(2.0 ** k)).astype(np.complex64)), k
     plan.destroy()
+
+
+@pytest.mark.parametrize("r,l0,LN,nrhs", [(6, 6, 14, 64), (8, 5, 14, 96), (10, 6, 16, 256), (12, 5, 14, 70)])
+def test_tc_band_f16(r, l0, LN, nrhs):
+    """BF_OPT_BAND_F16 = 1 (process-wide knob): the composed band in FP16 split passes with per-vector and
+    per-group power-of-two scaling.  Oracle bar, agreement with the 3xTF32 band, exact 2^k homogeneity."""
+    F = W.rhs(1 << LN, nrhs, 70 + r)
+    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    assert any(k.startswith("xfer") for k in plan.info()["tc_classes"])
+    G32 = _apply(plan, F)
+    plan.set_option(bf.BF_OPT_BAND_F16, 1)
+    try:
+        G16 = _apply(plan, F)
+        Gk = _apply(plan, np.asfortranarray(F * np.float32(2.0 ** -40)).astype(np.complex64))
+    finally:
+        plan.set_option(bf.BF_OPT_BAND_F16, 0)
+    plan.destroy()
+    cols = [0, nrhs - 1]
+    R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, cols])
+    assert np.all(oracle.rel_l2(G16[:, cols].astype(np.complex128), R, axis=0) <= PARITY)
+    d = oracle.rel_l2(G16.astype(np.complex128), G32.astype(np.complex128), axis=0)
+    assert np.all(d <= PATHS_AGREE), d.max()
+    assert not np.array_equal(G16, G32)
+    assert np.array_equal(Gk, (G16 * np.float32(2.0 ** -40)).astype(np.complex64))
