@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exchange", choices=["copy", "fused"], default="copy",
                     help="index-shard exchange: NCCL send/recv step, or peer stores from the level-h launch")
+    ap.add_argument("--host-pieces", type=int, default=None,
+                    help="bf_apply_host pipeline pieces per chunk (BF_OPT_HOST_PIECES; e2e only)")
     ap.add_argument("--band-f16", action="store_true",
                     help="composed band in FP16 split passes (BF_OPT_BAND_F16 = 1)")
     ap.add_argument("--leaf-tf32", action="store_true",
@@ -252,6 +254,8 @@ def main():
         plan.set_option(bf.BF_OPT_LEAF_F16, 0)
     if args.band_f16:
         plan.set_option(bf.BF_OPT_BAND_F16, 1)
+    if args.host_pieces:
+        plan.set_option(bf.BF_OPT_HOST_PIECES, args.host_pieces)
     info = plan.info()
     Fd = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()
     Gd = torch.empty_like(Fd)

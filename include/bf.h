@@ -221,6 +221,9 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        per-group power-of-two scaling, kind::f16 MMAs) instead of 3xTF32.  Process-wide
  *                        tuning knob. */
 #define BF_OPT_BAND_F16 7
+/*   BF_OPT_HOST_PIECES   2 (default), 1..16: bf_apply_host splits each chunk into this many pieces whose
+ *                        host<->device copies overlap the apply of the neighbouring pieces. */
+#define BF_OPT_HOST_PIECES 8
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band

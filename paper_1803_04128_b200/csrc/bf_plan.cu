@@ -159,6 +159,7 @@ struct bf_plan_s {
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
     bool band_compose = true;  // BF_OPT_BAND_COMPOSE
     bool leaf_f16 = true;      // BF_OPT_LEAF_F16
+    int host_pieces = 2;       // BF_OPT_HOST_PIECES: bf_apply_host pipeline pieces per chunk
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -918,11 +919,13 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
                     (e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking)) != cudaSuccess))
         return cuda_fail(e, "copy streams");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // Pipeline over pieces of half a chunk (ping-pong halves of the staging buffers): the host->device
-    // copy of piece i+1 and the device->host copy of piece i-1 run on their own streams while piece i is
-    // applied on `stream` (PCIe is full duplex).  Hazards are ordered with events: a staging half is
-    // refilled only after the apply that read it, and rewritten only after the copy-out that read it.
-    const int64_t piece = chunk >= 2 ? (chunk + 1) / 2 : chunk;
+    // Pipeline over pieces of 1/NP of a chunk (NP = BF_OPT_HOST_PIECES, a ring of NP parts of the staging
+    // buffers): the host->device copy of piece i+1 and the device->host copy of piece i-1 run on their own
+    // streams while piece i is applied on `stream` (PCIe is full duplex).  Hazards are ordered with events:
+    // a staging part is refilled only after the apply that read it, and rewritten only after the copy-out
+    // that read it.
+    const int NP = int(std::min<int64_t>(p->host_pieces, chunk));
+    const int64_t piece = (chunk + NP - 1) / NP;
     const int64_t npieces = (nrhs + piece - 1) / piece;
     std::vector<cudaEvent_t> ev(3 * size_t(npieces), nullptr);   // [h2d done, apply done, d2h done] per piece
     for (auto& x : ev)
@@ -937,19 +940,19 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
     }
     st = BF_OK;
     for (int64_t i = 0; i < npieces && st == BF_OK; i++) {
-        const int64_t c0 = i * piece, nc = std::min(piece, nrhs - c0), buf = i & 1;
+        const int64_t c0 = i * piece, nc = std::min(piece, nrhs - c0), buf = i % NP;
         const size_t bytes = size_t(rows * nc) * sizeof(float2);
         float2* dF = p->dF + buf * piece * rows;
         float2* dG = p->dG + buf * piece * rows;
         cudaEvent_t* E = &ev[3 * size_t(i)];
-        if (i >= 2) cudaStreamWaitEvent(p->h2d, ev[3 * size_t(i - 2) + 1], 0);
+        if (i >= NP) cudaStreamWaitEvent(p->h2d, ev[3 * size_t(i - NP) + 1], 0);
         if ((e = cudaMemcpyAsync(dF, F_host + c0 * rows, bytes, cudaMemcpyHostToDevice, p->h2d)) != cudaSuccess) {
             st = cuda_fail(e, "H2D");
             break;
         }
         cudaEventRecord(E[0], p->h2d);
         cudaStreamWaitEvent(s, E[0], 0);
-        if (i >= 2) cudaStreamWaitEvent(s, ev[3 * size_t(i - 2) + 2], 0);
+        if (i >= NP) cudaStreamWaitEvent(s, ev[3 * size_t(i - NP) + 2], 0);
         if ((st = apply_impl(p, dF, rows, dG, rows, nc, p->sh[0].ws, s)) != BF_OK) break;
         cudaEventRecord(E[1], s);
         cudaStreamWaitEvent(p->d2h, E[1], 0);
@@ -1122,6 +1125,11 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
                 if (bf_status_t st = build_leaf_images(p, s); st != BF_OK) return st;
         e = cudaDeviceSynchronize();
         return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf image switch");
+    }
+    if (option == BF_OPT_HOST_PIECES) {
+        if (value < 1 || value > 16) return fail(BF_ERR_INVALID_ARG, "BF_OPT_HOST_PIECES takes 1..16");
+        p->host_pieces = int(value);
+        return BF_OK;
     }
     if (option == BF_OPT_BAND_F16) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_F16 takes 0 or 1");
