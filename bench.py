@@ -194,8 +194,8 @@ def main():
                     help="bf_apply_host pipeline pieces per chunk (BF_OPT_HOST_PIECES; e2e only)")
     ap.add_argument("--band-f16", action="store_true",
                     help="composed band in FP16 split passes (BF_OPT_BAND_F16 = 1)")
-    ap.add_argument("--leaf-tf32", action="store_true",
-                    help="leaf stages in 3xTF32 instead of FP16 split passes (BF_OPT_LEAF_F16 = 0)")
+    ap.add_argument("--leaf-f16", action="store_true",
+                    help="leaf stages in FP16 split passes instead of 3xTF32 (BF_OPT_LEAF_F16 = 1, opt-in)")
     ap.add_argument("--band-pipelines", type=int, default=None, choices=[1, 2],
                     help="tensor-core band variant (tuning; default: the library's)")
     args = ap.parse_args()
@@ -250,8 +250,8 @@ def main():
     t_build = time.perf_counter() - t0
     if args.band_pipelines:
         plan.set_option(bf.BF_OPT_BAND_PIPELINES, args.band_pipelines)
-    if args.leaf_tf32:
-        plan.set_option(bf.BF_OPT_LEAF_F16, 0)
+    if args.leaf_f16:
+        plan.set_option(bf.BF_OPT_LEAF_F16, 1)
     if args.band_f16:
         plan.set_option(bf.BF_OPT_BAND_F16, 1)
     if args.host_pieces:

@@ -211,11 +211,12 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        in FP32 on chip; same MAC count, one accumulation chain per tile);
  *                        0: the level-by-level band kernels (selected by BF_OPT_BAND_PIPELINES). */
 #define BF_OPT_BAND_COMPOSE 5
-/*   BF_OPT_LEAF_F16      1 (default): the tensor-core S0 splits its operands into FP16 hi + lo after
- *                        power-of-two scaling of every operand row to max |x| in [0.5, 1) and runs the 3
- *                        split products as kind::f16 MMAs (twice the kind::tf32 rate, same 11-bit hi parts;
- *                        DESIGN.md 5); its weight image is half the bytes.  0: the 3xTF32 S0.  Switching
- *                        after creation rebuilds the S0 image (synchronous). */
+/*   BF_OPT_LEAF_F16      0 (default): the tensor-core leaf stages S0 / SL in 3xTF32.  1 (opt-in): they split
+ *                        their operands into FP16 hi + lo after power-of-two scaling of every operand row to
+ *                        max |x| in [0.5, 1) and run the 3 split products as kind::f16 MMAs (twice the
+ *                        kind::tf32 rate, same 11-bit hi parts, measured error no larger; DESIGN.md 5 and
+ *                        reading R17); the weight images are half the bytes.  Switching after creation
+ *                        rebuilds the leaf images (synchronous). */
 #define BF_OPT_LEAF_F16 6
 /*   BF_OPT_BAND_F16      0 (default) / 1: the composed tensor-core band in FP16 split passes (per-vector and
  *                        per-group power-of-two scaling, kind::f16 MMAs) instead of 3xTF32.  Process-wide

@@ -158,7 +158,7 @@ struct bf_plan_s {
     cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the pipelined bf_apply_host
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
     bool band_compose = true;  // BF_OPT_BAND_COMPOSE
-    bool leaf_f16 = true;      // BF_OPT_LEAF_F16
+    bool leaf_f16 = false;     // BF_OPT_LEAF_F16 (opt-in: the north_star names 3xTF32 or FP64)
     int host_pieces = 2;       // BF_OPT_HOST_PIECES: bf_apply_host pipeline pieces per chunk
     // timing
     bool timing = false;

@@ -186,12 +186,14 @@ def test_tc_band_composed(r, l0, LN, nrhs):
                                                      (W.K_FIO_JUMP, W.A_CFG3, 12, 5, 16, 32),
                                                      (W.K_DFT, W.A_ONE, 12, 6, 6, 70)])
 def test_tc_leaf_f16_vs_tf32(kernel, amp, LN, l0, r, nrhs):
-    """BF_OPT_LEAF_F16 (default 1): S0 and SL in FP16 split passes with per-row / per-chunk power-of-two
-    scaling; 0: 3xTF32.  Both meet the oracle bar and agree with each other like the two FP32-accurate
-    paths do."""
+    """BF_OPT_LEAF_F16 = 1 (opt-in): S0 and SL in FP16 split passes with per-row / per-chunk power-of-two
+    scaling; 0 (default): 3xTF32.  Both meet the oracle bar and agree with each other like the two
+    FP32-accurate paths do."""
     F = W.rhs(1 << LN, nrhs, 60 + r)
     plan = bf.Plan.build_fio(bf.fio(kernel, amp, LN, l0, r), max_nrhs_chunk=nrhs)
-    assert {"s0", "sl"} <= set(plan.info()["tc_classes"])
+    assert plan.info()["f16_classes"] == []
+    plan.set_option(bf.BF_OPT_LEAF_F16, 1)
+    assert {"s0", "sl"} <= set(plan.info()["tc_classes"]) and set(plan.info()["f16_classes"]) == {"s0", "sl"}
     bytes_f16 = plan.info()["tc_weight_bytes"]
     G16 = _apply(plan, F)
     plan.set_option(bf.BF_OPT_LEAF_F16, 0)
@@ -209,13 +211,15 @@ def test_tc_leaf_f16_vs_tf32(kernel, amp, LN, l0, r, nrhs):
     assert not np.array_equal(G16, G32)
 
 
-def test_tc_scale_equivariance():
-    """The FP16 S0 scales every vector by a power of two chosen from its own values, so the whole
-    tensor-core path is exactly homogeneous under power-of-two scaling of F (no overflow at 2^60, no
-    precision loss at 2^-60): G(2^k F) == 2^k G(F) bitwise."""
+@pytest.mark.parametrize("leaf_f16", [0, 1])
+def test_tc_scale_equivariance(leaf_f16):
+    """Both leaf precisions are exactly homogeneous under power-of-two scaling of F: 3xTF32 because every
+    rounding commutes with 2^k, the FP16 passes because they scale each vector by a power of two chosen from
+    its own values (no overflow at 2^60, no precision loss at 2^-60): G(2^k F) == 2^k G(F) bitwise."""
     LN, l0, r, nrhs = 12, 6, 10, 64
     F = W.rhs(1 << LN, nrhs, 9)
     plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    plan.set_option(bf.BF_OPT_LEAF_F16, leaf_f16)
     G = _apply(plan, F)
     for k in (60, -60):
         Gk = _apply(plan, np.asfortranarray(F * np.float32(2.0 ** k)).astype(np.complex64))
