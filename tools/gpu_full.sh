@@ -19,3 +19,5 @@ tail -5 gpurun_out/ncu_full.log
 CMD3="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
   -k regex:"^(s0_tc|s0_h16|band_tc|band_cmp|sl_tc|sl_h16)" -s 6 -c 6 --csv --log-file gpurun_out/traffic.csv $CMD3 > gpurun_out/ncu_traffic.log 2>&1; echo "ncu_traffic=$?"
+# opt-in FP16 leaf passes (BF_OPT_LEAF_F16 = 1) for comparison
+timeout 900 python bench.py --leaf-f16 --no-cpu-baseline > gpurun_out/bench_leaf_f16.log 2>&1; echo "bench_f16=$?"
