@@ -223,7 +223,9 @@ __global__ void __launch_bounds__(448, 1)
     uint8_t* ring = sm_s0tc;
     float2* Fs = reinterpret_cast<float2*>(sm_s0tc + C::OFF_F);    // [column][FS]
     float2* Bk = reinterpret_cast<float2*>(sm_s0tc + C::OFF_BK);   // [k][N0] b_k(x)
-    __shared__ uint64_t full[C::NSTAGE], empty[C::NSTAGE], dfull[2], dempty[2], f_full, f_empty, a_full, a_free;
+    // A is built and released per 32-wide K tile (a_full / a_free per tile): the next job's split of tile kt
+    // overlaps the current job's last chunk on tiles > kt (a single A buffer fills TMEM with the accumulators)
+    __shared__ uint64_t full[C::NSTAGE], empty[C::NSTAGE], dfull[2], dempty[2], f_full, f_empty, a_full[4], a_free[4];
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -244,8 +246,10 @@ __global__ void __launch_bounds__(448, 1)
         }
         tc::mbar_init(&f_full, 1);
         tc::mbar_init(&f_empty, 128);
-        tc::mbar_init(&a_full, 128);
-        tc::mbar_init(&a_free, 1);
+        for (int i = 0; i < C::KS; i++) {
+            tc::mbar_init(&a_full[i], 128);
+            tc::mbar_init(&a_free[i], 1);
+        }
         tc::mbar_fence_init();
     }
     tc::fence_before_sync();
@@ -293,14 +297,17 @@ __global__ void __launch_bounds__(448, 1)
             const int v0 = int(job % unsigned(nvt)) * 128, vg = v0 + v;
             const int c0 = v0 / n_amp;
             tc::mbar_wait(&f_full, uint32_t(jl & 1));
-            if (jl > 0) tc::mbar_wait(&a_free, uint32_t(jl - 1) & 1);
-            tc::fence_after_sync();
             const bool ok = vg < nv;
             const int cl = ok ? vg / n_amp - c0 : 0, k = ok ? vg % n_amp : 0;
             const float2* fc = Fs + cl * C::FS;
             const float2* bk = Bk + k * N0;
 #pragma unroll 1
             for (int j0 = 0; j0 < N0; j0 += 8) {
+                const int kt = j0 / (S0X_KC / 2);   // 32-wide K tile = 16 complex j
+                if ((j0 % (S0X_KC / 2)) == 0) {
+                    if (jl > 0) tc::mbar_wait(&a_free[kt], uint32_t(jl - 1) & 1);
+                    tc::fence_after_sync();
+                }
                 float hi[16], lo[16];
 #pragma unroll
                 for (int jj = 0; jj < 8; jj += 2) {
@@ -316,12 +323,13 @@ __global__ void __launch_bounds__(448, 1)
                 }
                 tc::tmem_st16(tmem + lb + uint32_t(2 * j0), hi);
                 tc::tmem_st16(tmem + lb + uint32_t(C::A_COLS + 2 * j0), lo);
+                if ((j0 + 8) % (S0X_KC / 2) == 0) {
+                    tc::tmem_wait_st();
+                    tc::fence_before_sync();
+                    tc::mbar_arrive(&a_full[kt]);
+                }
             }
-            tc::fence_before_sync();
             tc::mbar_arrive(&f_empty);   // the staging tile may be refilled for the next job
-            tc::tmem_wait_st();
-            tc::fence_before_sync();
-            tc::mbar_arrive(&a_full);
         }
     } else if (warp == 5) {
         // ---- MMA issuer (whole warp, one elected lane issues) ----
@@ -330,8 +338,6 @@ __global__ void __launch_bounds__(448, 1)
         const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(ring), LBO_B);
         int64_t gc = 0;   // global chunk counter (accumulator slots alternate across jobs)
         for (int64_t jl = 0; jl < njobs; jl++) {
-            tc::mbar_wait(&a_full, uint32_t(jl & 1));
-            tc::fence_after_sync();
             for (int nc = 0; nc < C::NCH; nc++, gc++) {
                 const int slot = int(gc & 1);
                 if (gc >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gc >> 1) - 1) & 1);
@@ -339,6 +345,7 @@ __global__ void __launch_bounds__(448, 1)
                 const uint32_t d = tmem + uint32_t(C::D_OFF + slot * S0X_NC);
                 for (int ks = 0; ks < C::KS; ks++) {
                     const int st = int((it0 + ks) % C::NSTAGE);
+                    if (nc == 0) tc::mbar_wait(&a_full[ks], uint32_t(jl & 1));
                     tc::mbar_wait(&full[st], uint32_t((it0 + ks) / C::NSTAGE) & 1);
                     tc::fence_after_sync();
 #pragma unroll
@@ -352,12 +359,11 @@ __global__ void __launch_bounds__(448, 1)
                                                  (q | ks | kk) ? 1u : 0u);
                     }
                     tc::commit_warp(&empty[st]);   // the tile is free once its 3 passes are done
+                    if (nc == C::NCH - 1) tc::commit_warp(&a_free[ks]);   // A tile ks: last use in this job
                 }
                 tc::commit_warp(&dfull[slot]);
                 __syncwarp();
             }
-            tc::commit_warp(&a_free);
-            __syncwarp();
         }
     } else {
         // ---- epilogue (warps 6-13): lane quarter warp % 4 = vectors, column half (warp - 6) / 4; output rows
