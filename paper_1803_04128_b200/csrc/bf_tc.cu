@@ -829,15 +829,18 @@ struct SLTC {
     static constexpr uint32_t GS_STRIDE = N0 + 1;
     static constexpr uint32_t GS_BYTES = uint32_t(128 / NA) * GS_STRIDE * 8;
     static constexpr uint32_t AS_BYTES = uint32_t(NA) * N0 * 8;
-    static constexpr int NR = (3 * (RAW + 2 * BT) + GS_BYTES + AS_BYTES <= 232448 - 1024) ? 3 : 2;   // ring depth
-    static constexpr uint32_t OFF_B = NR * RAW, OFF_GS = OFF_B + 2 * NR * BT, OFF_AS = OFF_GS + GS_BYTES;
+    // separate rings: the coefficient rows come from DRAM (deep ring), the Ux tiles mostly from L2 (2 deep)
+    static constexpr int NB_R = 2;                                   // Ux ring depth
+    static constexpr int NR_FIT = int((232448 - 1024 - GS_BYTES - AS_BYTES - NB_R * 2 * BT) / RAW);
+    static constexpr int NR = NR_FIT > 8 ? 8 : NR_FIT;               // raw ring depth
+    static constexpr uint32_t OFF_B = NR * RAW, OFF_GS = OFF_B + 2 * NB_R * BT, OFF_AS = OFF_GS + GS_BYTES;
     static constexpr size_t SMEM = size_t(OFF_AS) + AS_BYTES;
     // TMEM: two A stages (hi KC columns, then lo KC columns) and two accumulators of NB columns
     static constexpr int A_COLS = 2 * KC, D_OFF = 2 * A_COLS;
     static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * NB>();
     static_assert(KC % 8 == 0, "K chunk must be whole MMA K steps");
     static_assert(D_OFF + 2 * NB <= 512, "TMEM budget");
-    static_assert(SMEM <= 232448 - 1024, "shared memory budget");
+    static_assert(SMEM <= 232448 - 1024 && NR >= 2, "shared memory budget");
 };
 
 template <int R, int N0, int NA, int KP>
@@ -851,7 +854,7 @@ __global__ void __launch_bounds__(448, 1)
     auto opB = [&](int e, int lo) { return sm_sltc + C::OFF_B + (2 * e + lo) * C::BT; };
     float2* Gs = reinterpret_cast<float2*>(sm_sltc + C::OFF_GS);   // [128/NA][GS_STRIDE]
     float2* As = reinterpret_cast<float2*>(sm_sltc + C::OFF_AS);   // [NA][N0] a_k(x) of the current job
-    __shared__ uint64_t raw_full[C::NR], raw_empty[C::NR], b_full[C::NR], b_empty[C::NR], a_full[2], a_empty[2],
+    __shared__ uint64_t raw_full[C::NR], raw_empty[C::NR], b_full[C::NB_R], b_empty[C::NB_R], a_full[2], a_empty[2],
         dfull[2], dempty[2];
     __shared__ uint32_t tmem_base;
     constexpr int TMEM_COLS = C::TMEM_COLS;
@@ -867,6 +870,8 @@ __global__ void __launch_bounds__(448, 1)
         for (int i = 0; i < C::NR; i++) {
             tc::mbar_init(&raw_full[i], 1);
             tc::mbar_init(&raw_empty[i], 128);
+        }
+        for (int i = 0; i < C::NB_R; i++) {
             tc::mbar_init(&b_full[i], 1);
             tc::mbar_init(&b_empty[i], 1);
         }
@@ -884,7 +889,8 @@ __global__ void __launch_bounds__(448, 1)
     const uint32_t tmem = tmem_base;
 
     if (warp == 12) {
-        // ---- loader: the chunk stream of all this CTA's jobs ----
+        // ---- loaders: lane 0 streams the coefficient rows (2-D TMA, deep ring), lane 1 the Ux tiles (bulk
+        //      copies, 2-deep ring); the two streams only meet in the MMA ----
         if (lane == 0) {
             for (int gch = 0; gch < nch_all; gch++) {
                 const int jl = gch / C::NCH, ch = gch - jl * C::NCH;
@@ -892,15 +898,22 @@ __global__ void __launch_bounds__(448, 1)
                 const int64_t a = job / unsigned(nvt);
                 const int v0 = int(job % unsigned(nvt)) * 128;
                 const int e = gch % C::NR, use = gch / C::NR;
-                if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
-                tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
-                tc::bulk_g2s(opB(e, 0), Ux + (a * C::NCH + ch) * 2 * (C::BT / 4), 2 * C::BT, &b_full[e]);
                 if (use > 0) tc::mbar_wait(&raw_empty[e], (use - 1) & 1);
                 // the chunk's KP R coefficient rows of this vector tile: one 2-D tensor copy (whole box, a
                 // ragged tile zero-filled); per-row 1-D copies measured ~85 clk each to issue
                 tc::mbar_arrive_expect_tx(&raw_full[e], C::RAW);
                 const int64_t p0 = a * N0 + int64_t(ch) * KP;
                 tc::tma_load_2d(raw(e), &tin, 2 * v0, int(p0 * R), &raw_full[e]);
+            }
+        } else if (lane == 1) {
+            for (int gch = 0; gch < nch_all; gch++) {
+                const int jl = gch / C::NCH, ch = gch - jl * C::NCH;
+                const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
+                const int64_t a = job / unsigned(nvt);
+                const int e = gch % C::NB_R, use = gch / C::NB_R;
+                if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
+                tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
+                tc::bulk_g2s(opB(e, 0), Ux + (a * C::NCH + ch) * 2 * (C::BT / 4), 2 * C::BT, &b_full[e]);
             }
         }
     } else if (warp == 13) {
@@ -911,11 +924,11 @@ __global__ void __launch_bounds__(448, 1)
         int gseg = 0;   // accumulation segments issued (slots alternate across jobs)
         for (int gch = 0; gch < nch_all; gch++) {
             const int ch = gch % C::NCH;
-            const int e = gch % C::NR, sa = gch & 1, slot = gseg & 1, first = (ch % C::SEG) == 0;
+            const int e = gch % C::NB_R, sa = gch & 1, slot = gseg & 1, first = (ch % C::SEG) == 0;
             const bool last = (ch % C::SEG) == C::SEG - 1 || ch == C::NCH - 1;
             if (first && gseg >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gseg >> 1) - 1) & 1);
             tc::mbar_wait(&a_full[sa], uint32_t(gch >> 1) & 1);
-            tc::mbar_wait(&b_full[e], uint32_t(gch / C::NR) & 1);
+            tc::mbar_wait(&b_full[e], uint32_t(gch / C::NB_R) & 1);
             tc::fence_after_sync();
             const uint32_t d = tmem + uint32_t(C::D_OFF + slot * C::NB);
 #pragma unroll
