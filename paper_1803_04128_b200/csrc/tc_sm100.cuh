@@ -18,11 +18,13 @@ namespace tc {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 
 // ---- 3xTF32 split ---------------------------------------------------------------------------
+// Round to the nearest tf32, ties away from zero (= cvt.rna.tf32.f32 for every finite x): add half of the
+// dropped 13-bit field to the sign-magnitude bit pattern, then clear the field.  Two integer instructions;
+// cvt.rna.tf32.f32 itself is emulated on sm_100a with five (IADD, LOP3, FSETP, SEL for NaN/Inf handling,
+// measured in the band's SASS), which made the split the band's largest instruction stream.
 __device__ __forceinline__ float tf32_rna(float x)
 {
-    uint32_t h;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-    return __uint_as_float(h);
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 __device__ __forceinline__ void split(float x, float& hi, float& lo)
 {
