@@ -830,7 +830,7 @@ struct SLTC {
     static constexpr uint32_t GS_BYTES = uint32_t(128 / NA) * GS_STRIDE * 8;
     static constexpr uint32_t AS_BYTES = uint32_t(NA) * N0 * 8;
     // separate rings: the coefficient rows come from DRAM (deep ring), the Ux tiles mostly from L2 (2 deep)
-    static constexpr int NB_R = 2;                                   // Ux ring depth
+    static constexpr int NB_R = 3;                                   // Ux ring depth
     static constexpr int NR_FIT = int((232448 - 1024 - GS_BYTES - AS_BYTES - NB_R * 2 * BT) / RAW);
     static constexpr int NR = NR_FIT > 8 ? 8 : NR_FIT;               // raw ring depth
     static constexpr uint32_t OFF_B = NR * RAW, OFF_GS = OFF_B + 2 * NB_R * BT, OFF_AS = OFF_GS + GS_BYTES;
