@@ -2528,14 +2528,29 @@ __global__ void __launch_bounds__(512, 1)
                     tc::mbar_arrive(&d_free[db]);
                 }
                 if (vg < nv) {
+                    if (!po.on) {
+                        const int64_t p = (((a0 << 2) + 2 * hf) << shg) + bq;
+                        float2* o = out + p * R * int64_t(nv) + vg;
+                        const int64_t pstep = (int64_t(1) << shg) * R * int64_t(nv) - int64_t(R) * nv;
 #pragma unroll
-                    for (int oo = 0; oo < 2; oo++) {
-                        const int64_t p = (((a0 << 2) + 2 * hf + oo) << shg) + bq;
-                        float2* o = bfs::pair_out(out, po, p, R, nv) + vg;
+                        for (int oo = 0; oo < 2; oo++) {
 #pragma unroll
-                        for (int t = 0; t < R; t++)
-                            o[int64_t(t) * nv] =
-                                make_float2(d[oo * C::SC + 2 * t] * s2, d[oo * C::SC + 2 * t + 1] * s2);
+                            for (int t = 0; t < R; t++) {
+                                *o = make_float2(d[oo * C::SC + 2 * t] * s2, d[oo * C::SC + 2 * t + 1] * s2);
+                                o += nv;
+                            }
+                            o += pstep;
+                        }
+                    } else {
+#pragma unroll
+                        for (int oo = 0; oo < 2; oo++) {
+                            const int64_t p = (((a0 << 2) + 2 * hf + oo) << shg) + bq;
+                            float2* o = bfs::pair_out(out, po, p, R, nv) + vg;
+#pragma unroll
+                            for (int t = 0; t < R; t++)
+                                o[int64_t(t) * nv] =
+                                    make_float2(d[oo * C::SC + 2 * t] * s2, d[oo * C::SC + 2 * t + 1] * s2);
+                        }
                     }
                 }
             }
