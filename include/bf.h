@@ -192,7 +192,7 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
 /*   BF_OPT_BAND_PIPELINES 1 (default): the level-by-level tensor-core band kernel (BF_OPT_BAND_COMPOSE = 0)
  *                        runs one job at a time per SM;
  *                        2: jobs alternate between two TMEM pipelines where TMEM allows (r <= 10; measured
- *                        slower at cfg4).  Process-wide tuning knob. */
+ *                        slower at cfg4). */
 #define BF_OPT_BAND_PIPELINES 2
 /*   BF_OPT_BAND_TRACE_J0 (diagnostic): enables the band timeline trace of bf_debug_band_trace for CTA
  *                        value >> 16, jobs from value & 65535 (off by default). */
@@ -219,8 +219,8 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        rebuilds the leaf images (synchronous). */
 #define BF_OPT_LEAF_F16 6
 /*   BF_OPT_BAND_F16      0 (default) / 1: the composed tensor-core band in FP16 split passes (per-vector and
- *                        per-group power-of-two scaling, kind::f16 MMAs) instead of 3xTF32.  Process-wide
- *                        tuning knob. */
+ *                        per-group power-of-two scaling, kind::f16 MMAs) instead of 3xTF32 (measured slower
+ *                        in the power-capped step). */
 #define BF_OPT_BAND_F16 7
 /*   BF_OPT_HOST_PIECES   2 (default), 1..16: bf_apply_host splits each chunk into this many pieces whose
  *                        host<->device copies overlap the apply of the neighbouring pieces. */

@@ -65,14 +65,17 @@ cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, flo
 
 // Band of 2 transfer levels on the tensor cores (bf_tc.cu): same contract as launch_band with K = 2.
 bool band_tc_supported(const Dims& d, int nv);
+// which tensor-core band kernel runs (per plan: BF_OPT_BAND_COMPOSE, BF_OPT_BAND_F16, BF_OPT_BAND_PIPELINES)
+struct BandVariant {
+    bool compose = true;         // the composed two-level operator (band_cmp_kernel / band_h16_kernel)
+    bool f16 = false;            // composed band in FP16 split passes
+    bool two_pipelines = false;  // level-by-level band with two TMEM pipelines (r <= 10)
+};
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr,
-                           bool compose = true);
+                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, const BandVariant& bv);
 
 // Diagnostic: SM-clock timeline of the last band_tc launch (CTA 0, first 64 jobs x 12 events).
 cudaError_t band_trace(long long* out, int n);
-void band_set_single_pipeline(int v);
-void band_set_f16(int v);
 void band_trace_window(int j0);
 
 // Plan finalization: W[p] <- Sw[p] W[p] for npairs blocks (W column-major R x cols, Sw R x R).

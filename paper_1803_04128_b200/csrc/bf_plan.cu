@@ -157,7 +157,7 @@ struct bf_plan_s {
     float2* dG = nullptr;
     cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the pipelined bf_apply_host
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
-    bool band_compose = true;  // BF_OPT_BAND_COMPOSE
+    bfk::BandVariant band;     // BF_OPT_BAND_COMPOSE / BF_OPT_BAND_F16 / BF_OPT_BAND_PIPELINES
     bool leaf_f16 = false;     // BF_OPT_LEAF_F16 (opt-in: the north_star names 3xTF32 or FP64)
     int host_pieces = 2;       // BF_OPT_HOST_PIECES: bf_apply_host pipeline pieces per chunk
     // timing
@@ -438,7 +438,7 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                 const float2* W[2] = {sh.xfer[stp.l_first - p->d.l0 - 1],
                                       stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
                 if (stp.K == 2 && p->tensor_cores && bfk::band_tc_supported(dl, nv))
-                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po, p->band_compose);
+                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po, p->band);
                 return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
             }
             case Step::SL:
@@ -1133,12 +1133,12 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
     }
     if (option == BF_OPT_BAND_F16) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_F16 takes 0 or 1");
-        bfk::band_set_f16(int(value));
+        p->band.f16 = value != 0;
         return BF_OK;
     }
     if (option == BF_OPT_BAND_COMPOSE) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_COMPOSE takes 0 or 1");
-        p->band_compose = value != 0;
+        p->band.compose = value != 0;
         return BF_OK;
     }
     if (option == BF_OPT_BAND_TRACE_J0) {
@@ -1147,7 +1147,7 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
     }
     if (option == BF_OPT_BAND_PIPELINES) {
         if (value != 1 && value != 2) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_PIPELINES takes 1 or 2");
-        bfk::band_set_single_pipeline(value == 1);
+        p->band.two_pipelines = value == 2;
         return BF_OK;
     }
     return fail(BF_ERR_INVALID_ARG, "unknown plan option");

@@ -1416,11 +1416,8 @@ cudaError_t launch_sl_h16(const Dims& d, const float2* in, const void* Uh, const
 // they fit.  Measured at cfg4 (tools/band_trace.py, profiles/r1_band_variants.txt): the two-pipeline kernel
 // halves the per-job cycle count on some SMs, but its concurrent tcgen05.st/ld traffic (two epilogues plus
 // the split) slows the tensor pipe on others, and the launch is 1.4x slower overall.
-static int g_band_single_pipeline = 1;
-void band_set_single_pipeline(int v) { g_band_single_pipeline = v; }
-// FP16 split passes in the composed band (experiment knob until measured; process-wide like the above)
-static int g_band_f16 = 0;
-void band_set_f16(int v) { g_band_f16 = v; }
+
+
 
 // ---- timeline trace of the band kernel (diagnostic; CTA 0, first BT_JOBS jobs, SM clock) ----
 constexpr int BT_JOBS = 64, BT_EV = 12;
@@ -2705,12 +2702,13 @@ __global__ void __launch_bounds__(512, 1)
 
 template <int R>
 static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                              cudaStream_t s, int rh, int rhg, const bfs::PeerOut& po, bool compose)
+                              cudaStream_t s, int rh, int rhg, const bfs::PeerOut& po, const BandVariant& bv)
 {
+    const bool compose = bv.compose;
     using C = BandTC<R>;
     const int64_t groups = d.N >> 2;
     const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
-    if (compose && g_band_f16) {
+    if (compose && bv.f16) {
         using CH = BandH<R>;
         auto kern = band_h16_kernel<R>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CH::SMEM));
@@ -2733,7 +2731,7 @@ static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, floa
         return cudaGetLastError();
     }
     if constexpr (Band2P<R>::FITS) {
-        if (!g_band_single_pipeline) {
+        if (bv.two_pipelines) {
             auto kern = band_tc2p_kernel<R>;
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
             if (e != cudaSuccess) return e;
@@ -2760,14 +2758,14 @@ bool band_tc_supported(const Dims& d, int nv)
 }
 
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, bool compose)
+                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, const BandVariant& bv)
 {
     const bfs::PeerOut pz = po ? *po : bfs::PeerOut{};
     switch (d.R) {
-    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg, pz, compose);
-    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg, pz, compose);
-    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg, pz, compose);
-    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg, pz, compose);
+    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv);
+    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv);
+    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv);
+    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv);
     default: return cudaErrorInvalidValue;
     }
 }

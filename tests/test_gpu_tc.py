@@ -230,7 +230,7 @@ def test_tc_scale_equivariance(leaf_f16):
 
 @pytest.mark.parametrize("r,l0,LN,nrhs", [(6, 6, 14, 64), (8, 5, 14, 96), (10, 6, 16, 256), (12, 5, 14, 70)])
 def test_tc_band_f16(r, l0, LN, nrhs):
-    """BF_OPT_BAND_F16 = 1 (process-wide knob): the composed band in FP16 split passes with per-vector and
+    """BF_OPT_BAND_F16 = 1 (per plan): the composed band in FP16 split passes with per-vector and
     per-group power-of-two scaling.  Oracle bar, agreement with the 3xTF32 band, exact 2^k homogeneity."""
     F = W.rhs(1 << LN, nrhs, 70 + r)
     plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
