@@ -48,7 +48,8 @@ cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const floa
 // SL on the tensor cores: same contract as launch_sl, weights from Ux.
 bool sl_tc_supported(const Dims& d, int nv);
 cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const float2* ampa, float2* G, int64_t ldg,
-                         int nv, cudaStream_t s);
+                         int nv, cudaStream_t s,
+                         bool multicast = true);
 
 // Transfer level l (eqn:2 / eqn:3): out[p](t) = sum_{c,s} W[p](t, c r + s) in[(a>>1) 2^(LN-l+1) + 2b + c](s)
 // (at l == h the switch is already folded into W).

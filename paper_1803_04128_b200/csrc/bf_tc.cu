@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <algorithm>
 #include <cstdint>
 
 #include "bf_internal.h"
@@ -843,7 +844,10 @@ struct SLTC {
     static_assert(SMEM <= 232448 - 1024 && NR >= 2, "shared memory budget");
 };
 
-template <int R, int N0, int NA, int KP>
+// CL = 2: launched as clusters of two CTAs that work on the two halves of a leaf's vector tiles at the same
+// time; each CTA bulk-copies half of every Ux stage and multicasts it to both (half the L2 -> SM traffic of
+// the 1.3 MB-per-job Ux stream), and a stage is refilled only after both CTAs' MMAs released it.
+template <int R, int N0, int NA, int KP, int CL>
 __global__ void __launch_bounds__(448, 1)
     sl_tc_kernel(const __grid_constant__ CUtensorMap tin, const float* __restrict__ Ux, const float2* __restrict__ ampa,
                  float2* __restrict__ G, int64_t ldg, int LN, int nv, int nvt)
@@ -861,8 +865,18 @@ __global__ void __launch_bounds__(448, 1)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t N = int64_t(1) << LN;
-    const int64_t njobs_all = (N / N0) * nvt;
-    const int njobs = int((njobs_all - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    // job jl of this CTA -> (leaf a, first vector v0)
+    const int cr = CL == 2 ? int(blockIdx.x & 1) : 0;
+    const int64_t cid = CL == 2 ? int64_t(blockIdx.x >> 1) : int64_t(blockIdx.x);
+    const int64_t ncl = CL == 2 ? int64_t(gridDim.x >> 1) : int64_t(gridDim.x);
+    const int per = CL == 2 ? nvt / 2 : nvt;                 // units per leaf: vector tiles or tile pairs
+    const int64_t units = (N / N0) * per;
+    const int njobs = int((units - cid + ncl - 1) / ncl);
+    auto job_of = [&](int jl, int64_t& a, int& v0) {
+        const int64_t u = cid + int64_t(jl) * ncl;
+        a = u / per;
+        v0 = (CL == 2 ? int(u % per) * 2 + cr : int(u % per)) * 128;
+    };
     const int nch_all = njobs * C::NCH;
 
     if (warp == 0) tc::tmem_alloc<TMEM_COLS>(&tmem_base);
@@ -873,7 +887,7 @@ __global__ void __launch_bounds__(448, 1)
         }
         for (int i = 0; i < C::NB_R; i++) {
             tc::mbar_init(&b_full[i], 1);
-            tc::mbar_init(&b_empty[i], 1);
+            tc::mbar_init(&b_empty[i], CL);   // released by the MMA commit of every CTA of the cluster
         }
         for (int i = 0; i < 2; i++) {
             tc::mbar_init(&a_full[i], 128);
@@ -885,6 +899,7 @@ __global__ void __launch_bounds__(448, 1)
     }
     tc::fence_before_sync();
     __syncthreads();
+    if constexpr (CL == 2) tc::cluster_sync();   // both CTAs' barriers exist before any multicast
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base;
 
@@ -894,9 +909,9 @@ __global__ void __launch_bounds__(448, 1)
         if (lane == 0) {
             for (int gch = 0; gch < nch_all; gch++) {
                 const int jl = gch / C::NCH, ch = gch - jl * C::NCH;
-                const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
-                const int64_t a = job / unsigned(nvt);
-                const int v0 = int(job % unsigned(nvt)) * 128;
+                int64_t a;
+                int v0;
+                job_of(jl, a, v0);
                 const int e = gch % C::NR, use = gch / C::NR;
                 if (use > 0) tc::mbar_wait(&raw_empty[e], (use - 1) & 1);
                 // the chunk's KP R coefficient rows of this vector tile: one 2-D tensor copy (whole box, a
@@ -908,12 +923,17 @@ __global__ void __launch_bounds__(448, 1)
         } else if (lane == 1) {
             for (int gch = 0; gch < nch_all; gch++) {
                 const int jl = gch / C::NCH, ch = gch - jl * C::NCH;
-                const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
-                const int64_t a = job / unsigned(nvt);
+                int64_t a;
+                int v0;
+                job_of(jl, a, v0);
                 const int e = gch % C::NB_R, use = gch / C::NB_R;
                 if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
-                tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
-                tc::bulk_g2s(opB(e, 0), Ux + (a * C::NCH + ch) * 2 * (C::BT / 4), 2 * C::BT, &b_full[e]);
+                tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);   // both halves land here
+                const float* src = Ux + (a * C::NCH + ch) * 2 * (C::BT / 4);
+                if constexpr (CL == 2)
+                    tc::bulk_g2s_mc(opB(e, cr), src + cr * (C::BT / 4), C::BT, &b_full[e], uint16_t(3));
+                else
+                    tc::bulk_g2s(opB(e, 0), src, 2 * C::BT, &b_full[e]);
             }
         }
     } else if (warp == 13) {
@@ -942,7 +962,10 @@ __global__ void __launch_bounds__(448, 1)
                                          (first && q == 0 && ks == 0) ? 0u : 1u);
             }
             tc::commit_warp(&a_empty[sa]);
-            tc::commit_warp(&b_empty[e]);
+            if constexpr (CL == 2)
+                tc::commit_mc_warp(&b_empty[e], uint16_t(3));
+            else
+                tc::commit_warp(&b_empty[e]);
             if (last) {
                 tc::commit_warp(&dfull[slot]);
                 gseg++;
@@ -982,9 +1005,10 @@ __global__ void __launch_bounds__(448, 1)
         const int k = vl % NA, cl = vl / NA;
         int gseg = 0;
         for (int jl = 0; jl < njobs; jl++) {
-            const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
-            const int64_t a = job / unsigned(nvt);
-            const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
+            int64_t a;
+            int v0;
+            job_of(jl, a, v0);
+            const int vw = min(128, nv - v0);
             float sum[HC];
 #pragma unroll
             for (int i = 0; i < HC; i++) sum[i] = 0.f;
@@ -1031,6 +1055,7 @@ __global__ void __launch_bounds__(448, 1)
     }
     tc::fence_before_sync();
     __syncthreads();
+    if constexpr (CL == 2) tc::cluster_sync();   // no CTA leaves while its partner may still multicast into it
     if (warp == 0) {
         tc::fence_after_sync();
         tc::tmem_dealloc<TMEM_COLS>(tmem);
@@ -1039,18 +1064,39 @@ __global__ void __launch_bounds__(448, 1)
 
 template <int R, int N0, int NA, int KP>
 static cudaError_t sl_tc_go(const Dims& d, const float2* in, const float* Ux, const float2* ampa, float2* G, int64_t ldg,
-                            int nv, cudaStream_t s)
+                            int nv, cudaStream_t s, bool multicast)
 {
     using C = SLTC<R, N0, NA, KP>;
-    auto kern = sl_tc_kernel<R, N0, NA, KP>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    if (e != cudaSuccess) return e;
     const int nvt = (nv + 127) / 128;
-    const int64_t jobs = (d.N / N0) * nvt;
-    const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
     CUtensorMap tin;
-    e = make_rows_tmap(&tin, in, d.N * R, nv, KP * R);
+    cudaError_t e = make_rows_tmap(&tin, in, d.N * R, nv, KP * R);
     if (e != cudaSuccess) return e;
+    const int64_t leaves = d.N / N0;
+    if (multicast && nvt % 2 == 0 && sm_count() >= 2) {
+        auto kern = sl_tc_kernel<R, N0, NA, KP, 2>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+        if (e != cudaSuccess) return e;
+        const int64_t pairs = leaves * (nvt / 2);
+        const int64_t ncl = std::min<int64_t>(pairs, sm_count() / 2);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(2 * ncl));
+        cfg.blockDim = dim3(448);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, tin, Ux, ampa, G, ldg, d.LN, nv, nvt);
+    }
+    auto kern = sl_tc_kernel<R, N0, NA, KP, 1>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    const int64_t jobs = leaves * nvt;
+    const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
     kern<<<grid, 448, C::SMEM, s>>>(tin, Ux, ampa, G, ldg, d.LN, nv, nvt);
     return cudaGetLastError();
 }
@@ -1058,14 +1104,14 @@ static cudaError_t sl_tc_go(const Dims& d, const float2* in, const float* Ux, co
 bool sl_tc_supported(const Dims& d, int nv) { return leaf_tc_shape(d) && nv >= 64 && nv % 2 == 0; }
 
 cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const float2* ampa, float2* G, int64_t ldg,
-                         int nv, cudaStream_t s)
+                         int nv, cudaStream_t s, bool multicast)
 {
     const int n0 = 1 << d.l0;
 #define SLTC_NA(RR, N0_, KP_)                                                                 \
     if (d.R == RR && n0 == N0_) {                                                             \
-        if (d.n_amp == 1) return sl_tc_go<RR, N0_, 1, KP_>(d, in, Ux, ampa, G, ldg, nv, s);  \
-        if (d.n_amp == 2) return sl_tc_go<RR, N0_, 2, KP_>(d, in, Ux, ampa, G, ldg, nv, s);  \
-        if (d.n_amp == 4) return sl_tc_go<RR, N0_, 4, KP_>(d, in, Ux, ampa, G, ldg, nv, s);  \
+        if (d.n_amp == 1) return sl_tc_go<RR, N0_, 1, KP_>(d, in, Ux, ampa, G, ldg, nv, s, multicast);  \
+        if (d.n_amp == 2) return sl_tc_go<RR, N0_, 2, KP_>(d, in, Ux, ampa, G, ldg, nv, s, multicast);  \
+        if (d.n_amp == 4) return sl_tc_go<RR, N0_, 4, KP_>(d, in, Ux, ampa, G, ldg, nv, s, multicast);  \
     }
     SLTC_NA(6, 64, 2) SLTC_NA(8, 64, 2) SLTC_NA(10, 64, 2) SLTC_NA(12, 64, 1) SLTC_NA(16, 64, 1)
     SLTC_NA(6, 32, 2) SLTC_NA(8, 32, 2) SLTC_NA(10, 32, 2) SLTC_NA(12, 32, 1) SLTC_NA(16, 32, 1)
