@@ -236,7 +236,10 @@ bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
  * values; 0 = not recorded) -- into out[0 .. n).  Synchronous. */
 bf_status_t bf_debug_band_trace(int64_t *out, int32_t n);
 
-/* Wait for the plan's outstanding work, then free everything it owns. */
+/* Wait for the plan's outstanding work (the last bf_apply enqueued outside a CUDA-graph capture; replays of a
+ * graph that captured bf_apply must be synchronized by the caller), then free everything it owns.
+ * bf_apply / bf_apply_ex only enqueue work (no allocation, no host synchronization), so they can be captured
+ * into a CUDA graph (tests/test_gpu_tc.py::test_cuda_graph_capture). */
 bf_status_t bf_plan_destroy(bf_plan_t plan);
 
 /* ---- index-sharded plans: one long vector split by index over world = 2^g ranks ----

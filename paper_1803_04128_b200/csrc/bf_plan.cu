@@ -574,7 +574,11 @@ bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, in
             if (r != BF_OK) return r;
         }
     }
-    cudaEventRecord(p->done, s);
+    // completion marker for bf_plan_destroy; not recorded while the stream is being captured into a CUDA
+    // graph (the replays are the caller's to synchronize before destroying the plan)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone)
+        cudaEventRecord(p->done, s);
     return BF_OK;
 }
 

@@ -269,3 +269,38 @@ def test_tc_sl_multicast(LN, nrhs):
     assert np.array_equal(Gm, G1)
     R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, [0, nrhs - 1]])
     assert np.all(oracle.rel_l2(Gm[:, [0, nrhs - 1]].astype(np.complex128), R, axis=0) <= PARITY)
+
+
+@pytest.mark.parametrize("nrhs", [128, 8])
+def test_cuda_graph_capture(nrhs):
+    """bf_apply only enqueues (no allocation, no host synchronization), so it can be captured
+    into a CUDA graph; replays equal the eager apply bitwise, also after the input buffer is refilled.
+    nrhs = 128 runs the tensor-core kernels (incl. the cluster-launched SL), nrhs = 8 the SIMT ones."""
+    LN, l0, r = 14, 6, 10
+    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    F1 = torch.from_numpy(np.ascontiguousarray(W.rhs(1 << LN, nrhs, 5).T)).cuda()
+    F2 = torch.from_numpy(np.ascontiguousarray(W.rhs(1 << LN, nrhs, 6).T)).cuda()
+    ref1, ref2 = torch.empty_like(F1), torch.empty_like(F1)
+    plan.apply(F1, ref1, nrhs)
+    plan.apply(F2, ref2, nrhs)
+    torch.cuda.synchronize()
+    Fin, Gout = F1.clone(), torch.empty_like(F1)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.apply(Fin, Gout, nrhs)      # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.apply(Fin, Gout, nrhs)
+    Gout.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(Gout, ref1)
+    Fin.copy_(F2)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(Gout, ref2)
+    del g
+    plan.destroy()
