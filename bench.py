@@ -192,8 +192,8 @@ def main():
                     help="index-shard exchange: NCCL send/recv step, or peer stores from the level-h launch")
     ap.add_argument("--host-pieces", type=int, default=None,
                     help="bf_apply_host pipeline pieces per chunk (BF_OPT_HOST_PIECES; e2e only)")
-    ap.add_argument("--no-sl-multicast", action="store_true",
-                    help="TF32 SL without the 2-CTA cluster Ux multicast (BF_OPT_SL_MULTICAST = 0)")
+    ap.add_argument("--no-leaf-multicast", action="store_true",
+                    help="TF32 SL without the 2-CTA cluster Ux multicast (BF_OPT_LEAF_MULTICAST = 0)")
     ap.add_argument("--band-f16", action="store_true",
                     help="composed band in FP16 split passes (BF_OPT_BAND_F16 = 1)")
     ap.add_argument("--leaf-f16", action="store_true",
@@ -256,8 +256,8 @@ def main():
         plan.set_option(bf.BF_OPT_LEAF_F16, 1)
     if args.band_f16:
         plan.set_option(bf.BF_OPT_BAND_F16, 1)
-    if args.no_sl_multicast:
-        plan.set_option(bf.BF_OPT_SL_MULTICAST, 0)
+    if args.no_leaf_multicast:
+        plan.set_option(bf.BF_OPT_LEAF_MULTICAST, 0)
     if args.host_pieces:
         plan.set_option(bf.BF_OPT_HOST_PIECES, args.host_pieces)
     info = plan.info()

@@ -225,10 +225,11 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
 /*   BF_OPT_HOST_PIECES   2 (default), 1..16: bf_apply_host splits each chunk into this many pieces whose
  *                        host<->device copies overlap the apply of the neighbouring pieces. */
 #define BF_OPT_HOST_PIECES 8
-/*   BF_OPT_SL_MULTICAST  1 (default): the 3xTF32 SL runs as clusters of two CTAs working on the two halves of
- *                        a leaf's vector tiles, each loading half of every Ux tile and multicasting it to both
- *                        (needs an even number of 128-vector tiles per chunk; else one CTA per tile); 0: off. */
-#define BF_OPT_SL_MULTICAST 9
+/*   BF_OPT_LEAF_MULTICAST 1 (default): the 3xTF32 leaf stages S0 and SL run as clusters of two CTAs working
+ *                        on the two halves of a leaf's vector tiles, each loading half of every weight-image
+ *                        tile (V0x / Ux) and multicasting it to both (needs an even number of 128-vector tiles
+ *                        per chunk; else one CTA per tile); 0: off. */
+#define BF_OPT_LEAF_MULTICAST 9
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band

@@ -43,7 +43,8 @@ cudaError_t expand_sl_h16(const Dims& d, const float2* U, void* Uh, void* Ue, cu
 cudaError_t launch_sl_h16(const Dims& d, const float2* in, const void* Uh, const void* Ue, const float2* ampa,
                           float2* G, int64_t ldg, int nv, cudaStream_t s);
 cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x, float2* out,
-                         int nv, cudaStream_t s);
+                         int nv, cudaStream_t s,
+                         bool multicast = true);
 
 // SL on the tensor cores: same contract as launch_sl, weights from Ux.
 bool sl_tc_supported(const Dims& d, int nv);

@@ -160,7 +160,7 @@ struct bf_plan_s {
     bfk::BandVariant band;     // BF_OPT_BAND_COMPOSE / BF_OPT_BAND_F16 / BF_OPT_BAND_PIPELINES
     bool leaf_f16 = false;     // BF_OPT_LEAF_F16 (opt-in: the north_star names 3xTF32 or FP64)
     int host_pieces = 2;       // BF_OPT_HOST_PIECES: bf_apply_host pipeline pieces per chunk
-    bool sl_multicast = true;  // BF_OPT_SL_MULTICAST: TF32 SL as 2-CTA clusters sharing the Ux stream
+    bool leaf_multicast = true;  // BF_OPT_LEAF_MULTICAST: TF32 S0 / SL as 2-CTA clusters sharing the weight stream
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -431,7 +431,7 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                 if (p->tensor_cores && sh.v0h && bfk::s0_tc_supported(dl, nv, ldf))
                     return bfk::launch_s0_h16(dl, F, ldf, sh.amp_b, sh.v0h, sh.v0s, in, nv, s);
                 if (p->tensor_cores && sh.v0x && bfk::s0_tc_supported(dl, nv, ldf))
-                    return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s);
+                    return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s, p->leaf_multicast);
                 return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
             case Step::XFER:
                 return bfk::launch_xfer(dl, lk, in, out, sh.xfer[stp.l_first - p->d.l0 - 1], nv, s, rh, rhg, po);
@@ -446,7 +446,7 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                 if (p->tensor_cores && sh.uh && bfk::sl_tc_supported(dl, nv))
                     return bfk::launch_sl_h16(dl, in, sh.uh, sh.ue, sh.amp_a, G, ldg, nv, s);
                 if (p->tensor_cores && sh.ux && bfk::sl_tc_supported(dl, nv))
-                    return bfk::launch_sl_tc(dl, in, sh.ux, sh.amp_a, G, ldg, nv, s, p->sl_multicast);
+                    return bfk::launch_sl_tc(dl, in, sh.ux, sh.amp_a, G, ldg, nv, s, p->leaf_multicast);
                 return bfk::launch_sl(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
             default: return cudaErrorInvalidValue;
             }
@@ -1131,9 +1131,9 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
         e = cudaDeviceSynchronize();
         return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf image switch");
     }
-    if (option == BF_OPT_SL_MULTICAST) {
-        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_SL_MULTICAST takes 0 or 1");
-        p->sl_multicast = value != 0;
+    if (option == BF_OPT_LEAF_MULTICAST) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_LEAF_MULTICAST takes 0 or 1");
+        p->leaf_multicast = value != 0;
         return BF_OK;
     }
     if (option == BF_OPT_HOST_PIECES) {

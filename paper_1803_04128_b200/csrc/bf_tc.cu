@@ -214,7 +214,10 @@ struct S0TC {
     static_assert(SMEM <= 232448 - 1024 && D_OFF + 2 * S0X_NC <= 512, "budget");
 };
 
-template <int R, int N0>
+// CL = 2: clusters of two CTAs on the two halves of a leaf's vector tiles at the same time; each CTA bulk-copies
+// one of the two 16 KB tiles (hi or lo) of every V0x stage and multicasts it to both (half the L2 -> SM
+// traffic of the 1.3 MB-per-job weight stream); cluster-multicast MMA commits release a stage in both CTAs.
+template <int R, int N0, int CL>
 __global__ void __launch_bounds__(448, 1)
     s0_tc_kernel(const float2* __restrict__ F, int64_t ldf, const float2* __restrict__ ampb,
                  const float* __restrict__ V0x, float2* __restrict__ out, int LN, int n_amp, int nv, int nvt)
@@ -232,14 +235,22 @@ __global__ void __launch_bounds__(448, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t N = int64_t(1) << LN;
     const int64_t nleaf = N / N0;
-    const int64_t njobs_all = nleaf * nvt;
-    const int64_t njobs = (njobs_all - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int cr = CL == 2 ? int(blockIdx.x & 1) : 0;
+    const int64_t cid = CL == 2 ? int64_t(blockIdx.x >> 1) : int64_t(blockIdx.x);
+    const int64_t ncl = CL == 2 ? int64_t(gridDim.x >> 1) : int64_t(gridDim.x);
+    const int per = CL == 2 ? nvt / 2 : nvt;
+    const int64_t njobs = (nleaf * per - cid + ncl - 1) / ncl;
+    auto job_of = [&](int64_t jl, int64_t& b, int& v0) {   // job jl of this CTA -> (leaf b, first vector v0)
+        const int64_t u = cid + jl * ncl;
+        b = u / per;
+        v0 = (CL == 2 ? int(u % per) * 2 + cr : int(u % per)) * 128;
+    };
 
     if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
     if (tid == 0) {
         for (int i = 0; i < C::NSTAGE; i++) {
             tc::mbar_init(&full[i], 1);
-            tc::mbar_init(&empty[i], 1);
+            tc::mbar_init(&empty[i], CL);
         }
         for (int i = 0; i < 2; i++) {
             tc::mbar_init(&dfull[i], 1);
@@ -255,6 +266,7 @@ __global__ void __launch_bounds__(448, 1)
     }
     tc::fence_before_sync();
     __syncthreads();
+    if constexpr (CL == 2) tc::cluster_sync();
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base;
 
@@ -264,9 +276,10 @@ __global__ void __launch_bounds__(448, 1)
         //      staging tile), so its latency hides behind the current job's MMAs ----
         if (lane == 0) {
             auto issue_f = [&](int64_t jl) {
-                const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
-                const int64_t b = job / unsigned(nvt);
-                const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
+                int64_t b;
+                int v0;
+                job_of(jl, b, v0);
+                const int vw = min(128, nv - v0);
                 const int c0 = v0 / n_amp, cw = (vw + n_amp - 1) / n_amp;
                 if (jl > 0) tc::mbar_wait(&f_empty, uint32_t(jl - 1) & 1);
                 tc::mbar_arrive_expect_tx(&f_full, uint32_t(cw) * N0 * 8 + uint32_t(n_amp) * N0 * 8);
@@ -279,12 +292,19 @@ __global__ void __launch_bounds__(448, 1)
             if (njobs > 0) issue_f(0);
             int64_t it = 0;
             for (int64_t jl = 0; jl < njobs; jl++) {
-                const int64_t b = unsigned(blockIdx.x + jl * gridDim.x) / unsigned(nvt);
+                int64_t b;
+                int v0j;
+                job_of(jl, b, v0j);
                 for (int w = 0; w < WPJ; w++, it++) {
                     const int st = int(it % C::NSTAGE);
                     if (it >= C::NSTAGE) tc::mbar_wait(&empty[st], uint32_t(it / C::NSTAGE - 1) & 1);
-                    tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
-                    tc::bulk_g2s(ring + st * C::STAGE, V0x + (b * WPJ + w) * 2 * S0X_TILE_FLOATS, C::STAGE, &full[st]);
+                    tc::mbar_arrive_expect_tx(&full[st], C::STAGE);   // both tiles land here
+                    const float* src = V0x + (b * WPJ + w) * 2 * S0X_TILE_FLOATS;
+                    if constexpr (CL == 2)
+                        tc::bulk_g2s_mc(ring + st * C::STAGE + cr * C::TILE, src + cr * S0X_TILE_FLOATS, C::TILE,
+                                        &full[st], uint16_t(3));
+                    else
+                        tc::bulk_g2s(ring + st * C::STAGE, src, C::STAGE, &full[st]);
                     if (w == F_AT && jl + 1 < njobs) issue_f(jl + 1);
                 }
             }
@@ -294,8 +314,10 @@ __global__ void __launch_bounds__(448, 1)
         const int v = tid;
         const uint32_t lb = uint32_t(warp * 32) << 16;
         for (int64_t jl = 0; jl < njobs; jl++) {
-            const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
-            const int v0 = int(job % unsigned(nvt)) * 128, vg = v0 + v;
+            int64_t bj;
+            int v0;
+            job_of(jl, bj, v0);
+            const int vg = v0 + v;
             const int c0 = v0 / n_amp;
             tc::mbar_wait(&f_full, uint32_t(jl & 1));
             const bool ok = vg < nv;
@@ -359,7 +381,10 @@ __global__ void __launch_bounds__(448, 1)
                             tc::mma_tf32_ts_warp(d, a + kk * 8, tc::desc_add(b, kk * 2 * LBO_B), idesc,
                                                  (q | ks | kk) ? 1u : 0u);
                     }
-                    tc::commit_warp(&empty[st]);   // the tile is free once its 3 passes are done
+                    if constexpr (CL == 2)
+                        tc::commit_mc_warp(&empty[st], uint16_t(3));   // free in both CTAs of the cluster
+                    else
+                        tc::commit_warp(&empty[st]);   // the tile is free once its 3 passes are done
                     if (nc == C::NCH - 1) tc::commit_warp(&a_free[ks]);   // A tile ks: last use in this job
                 }
                 tc::commit_warp(&dfull[slot]);
@@ -373,9 +398,10 @@ __global__ void __launch_bounds__(448, 1)
         const int64_t strideA = nleaf * R * int64_t(nv), jumpA = strideA - int64_t(R) * nv;
         int64_t gc = 0;
         for (int64_t jl = 0; jl < njobs; jl++) {
-            const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
-            const int64_t b = job / unsigned(nvt);
-            const int vg = int(job % unsigned(nvt)) * 128 + q4 * 32 + lane;
+            int64_t b;
+            int v0;
+            job_of(jl, b, v0);
+            const int vg = v0 + q4 * 32 + lane;
             float2* const obase = out + b * R * int64_t(nv) + vg;
             for (int nc = 0; nc < C::NCH; nc++, gc++) {
                 const int slot = int(gc & 1);
@@ -410,6 +436,7 @@ __global__ void __launch_bounds__(448, 1)
     }
     tc::fence_before_sync();
     __syncthreads();
+    if constexpr (CL == 2) tc::cluster_sync();
     if (warp == 0) {
         tc::fence_after_sync();
         tc::tmem_dealloc<C::TMEM_COLS>(tmem);
@@ -418,14 +445,35 @@ __global__ void __launch_bounds__(448, 1)
 
 template <int R, int N0>
 static cudaError_t s0_tc_go(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x,
-                            float2* out, int nv, cudaStream_t s)
+                            float2* out, int nv, cudaStream_t s, bool multicast)
 {
     using C = S0TC<R, N0>;
-    auto kern = s0_tc_kernel<R, N0>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    if (e != cudaSuccess) return e;
     const int nvt = (nv + 127) / 128;
-    const int64_t jobs = (d.N / N0) * nvt;
+    const int64_t leaves = d.N / N0;
+    cudaError_t e;
+    if (multicast && nvt % 2 == 0 && sm_count() >= 2) {
+        auto kern = s0_tc_kernel<R, N0, 2>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+        if (e != cudaSuccess) return e;
+        const int64_t ncl = std::min<int64_t>(leaves * (nvt / 2), sm_count() / 2);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(2 * ncl));
+        cfg.blockDim = dim3(448);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, F, ldf, ampb, V0x, out, d.LN, d.n_amp, nv, nvt);
+    }
+    auto kern = s0_tc_kernel<R, N0, 1>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    const int64_t jobs = leaves * nvt;
     const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
     kern<<<grid, 448, C::SMEM, s>>>(F, ldf, ampb, V0x, out, d.LN, d.n_amp, nv, nvt);
     return cudaGetLastError();
@@ -434,13 +482,13 @@ static cudaError_t s0_tc_go(const Dims& d, const float2* F, int64_t ldf, const f
 bool s0_tc_supported(const Dims& d, int nv, int64_t ldf) { return leaf_tc_shape(d) && nv >= 64 && (ldf % 2) == 0; }
 
 cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x, float2* out,
-                         int nv, cudaStream_t s)
+                         int nv, cudaStream_t s, bool multicast)
 {
     const int n0 = 1 << d.l0;
 #define S0TC_CASE(RR)                                                                                      \
     if (d.R == RR)                                                                                         \
-        return n0 == 64 ? s0_tc_go<RR, 64>(d, F, ldf, ampb, V0x, out, nv, s)                               \
-                        : s0_tc_go<RR, 32>(d, F, ldf, ampb, V0x, out, nv, s);
+        return n0 == 64 ? s0_tc_go<RR, 64>(d, F, ldf, ampb, V0x, out, nv, s, multicast)                               \
+                        : s0_tc_go<RR, 32>(d, F, ldf, ampb, V0x, out, nv, s, multicast);
     S0TC_CASE(6) S0TC_CASE(8) S0TC_CASE(10) S0TC_CASE(12) S0TC_CASE(16)
 #undef S0TC_CASE
     return cudaErrorInvalidValue;

@@ -253,17 +253,17 @@ def test_tc_band_f16(r, l0, LN, nrhs):
 
 
 @pytest.mark.parametrize("LN,nrhs", [(14, 128), (14, 100), (12, 192), (16, 256)])
-def test_tc_sl_multicast(LN, nrhs):
-    """BF_OPT_SL_MULTICAST (default 1): the 3xTF32 SL as 2-CTA clusters that each bulk-copy half of every
-    Ux tile and multicast it to both.  Same arithmetic per vector as the one-CTA kernel, so the result is
+def test_tc_leaf_multicast(LN, nrhs):
+    """BF_OPT_LEAF_MULTICAST (default 1): the 3xTF32 S0 and SL as 2-CTA clusters that each bulk-copy half of
+    every weight-image tile and multicast it to both.  Same arithmetic per vector as the one-CTA kernel, so the result is
     bitwise equal (even vector-tile counts use the clusters: nv = 256, 200 (ragged), 512; nv = 384 falls
     back to one CTA per tile)."""
     l0, r = 6, 10
     F = W.rhs(1 << LN, nrhs, 80 + LN)
     plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
-    assert "sl" in plan.info()["tc_classes"]
+    assert {"s0", "sl"} <= set(plan.info()["tc_classes"])
     Gm = _apply(plan, F)
-    plan.set_option(bf.BF_OPT_SL_MULTICAST, 0)
+    plan.set_option(bf.BF_OPT_LEAF_MULTICAST, 0)
     G1 = _apply(plan, F)
     plan.destroy()
     assert np.array_equal(Gm, G1)
