@@ -222,8 +222,11 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        per-group power-of-two scaling, kind::f16 MMAs) instead of 3xTF32 (measured slower
  *                        in the power-capped step). */
 #define BF_OPT_BAND_F16 7
-/*   BF_OPT_HOST_PIECES   2 (default), 1..16: bf_apply_host splits each chunk into this many pieces whose
- *                        host<->device copies overlap the apply of the neighbouring pieces. */
+/*   BF_OPT_HOST_PIECES   2 (default), 1..16: bf_apply_host splits each chunk into this many equal pieces whose
+ *                        host<->device copies overlap the apply of the neighbouring pieces; 3 = tapered
+ *                        pieces of 1/4, 1/2, 1/4 of a chunk (measured at cfg4: 2 pieces 137.5 ms, tapered
+ *                        140 ms, 4 pieces 145 ms: smaller pieces re-read the factors and fall below the
+ *                        tensor-core tiles). */
 #define BF_OPT_HOST_PIECES 8
 /*   BF_OPT_LEAF_MULTICAST 1 (default): the 3xTF32 leaf stages S0 and SL run as clusters of two CTAs working
  *                        on the two halves of a leaf's vector tiles, each loading half of every weight-image

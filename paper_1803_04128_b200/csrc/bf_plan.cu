@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/bf.h"
@@ -924,14 +925,34 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
                     (e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking)) != cudaSuccess))
         return cuda_fail(e, "copy streams");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // Pipeline over pieces of 1/NP of a chunk (NP = BF_OPT_HOST_PIECES, a ring of NP parts of the staging
-    // buffers): the host->device copy of piece i+1 and the device->host copy of piece i-1 run on their own
-    // streams while piece i is applied on `stream` (PCIe is full duplex).  Hazards are ordered with events:
-    // a staging part is refilled only after the apply that read it, and rewritten only after the copy-out
-    // that read it.
-    const int NP = int(std::min<int64_t>(p->host_pieces, chunk));
-    const int64_t piece = (chunk + NP - 1) / NP;
-    const int64_t npieces = (nrhs + piece - 1) / piece;
+    // Pipeline over pieces (BF_OPT_HOST_PIECES = NP): the host->device copy of piece i+1 and the
+    // device->host copy of piece i-1 run on their own streams while piece i is applied on `stream` (PCIe is
+    // full duplex).  NP = 3 ("tapered"): per chunk-sized span, pieces of 1/4, 1/2, 1/4 -- only the small
+    // first and last pieces' copies are exposed; otherwise NP equal pieces.  Staging parts form a ring of
+    // NB parts; hazards are ordered with events: a part is refilled only after the apply that read it, and
+    // rewritten only after the copy-out that read it.
+    std::vector<std::pair<int64_t, int64_t>> pcs;   // (first column, columns)
+    int NB;
+    int64_t part;
+    if (p->host_pieces == 3 && chunk >= 4) {
+        NB = 2;
+        part = (chunk + 1) / 2;
+        for (int64_t c = 0; c < nrhs; c += chunk) {
+            const int64_t span = std::min(chunk, nrhs - c), q = span / 4;
+            if (q == 0) {
+                pcs.push_back({c, span});
+                continue;
+            }
+            pcs.push_back({c, q});
+            pcs.push_back({c + q, span - 2 * q});
+            pcs.push_back({c + span - q, q});
+        }
+    } else {
+        NB = int(std::min<int64_t>(std::max(p->host_pieces, 1), chunk));
+        part = (chunk + NB - 1) / NB;
+        for (int64_t c = 0; c < nrhs; c += part) pcs.push_back({c, std::min(part, nrhs - c)});
+    }
+    const int64_t npieces = int64_t(pcs.size());
     std::vector<cudaEvent_t> ev(3 * size_t(npieces), nullptr);   // [h2d done, apply done, d2h done] per piece
     for (auto& x : ev)
         if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) break;
@@ -945,19 +966,19 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
     }
     st = BF_OK;
     for (int64_t i = 0; i < npieces && st == BF_OK; i++) {
-        const int64_t c0 = i * piece, nc = std::min(piece, nrhs - c0), buf = i % NP;
+        const int64_t c0 = pcs[size_t(i)].first, nc = pcs[size_t(i)].second, buf = i % NB;
         const size_t bytes = size_t(rows * nc) * sizeof(float2);
-        float2* dF = p->dF + buf * piece * rows;
-        float2* dG = p->dG + buf * piece * rows;
+        float2* dF = p->dF + buf * part * rows;
+        float2* dG = p->dG + buf * part * rows;
         cudaEvent_t* E = &ev[3 * size_t(i)];
-        if (i >= NP) cudaStreamWaitEvent(p->h2d, ev[3 * size_t(i - NP) + 1], 0);
+        if (i >= NB) cudaStreamWaitEvent(p->h2d, ev[3 * size_t(i - NB) + 1], 0);
         if ((e = cudaMemcpyAsync(dF, F_host + c0 * rows, bytes, cudaMemcpyHostToDevice, p->h2d)) != cudaSuccess) {
             st = cuda_fail(e, "H2D");
             break;
         }
         cudaEventRecord(E[0], p->h2d);
         cudaStreamWaitEvent(s, E[0], 0);
-        if (i >= NP) cudaStreamWaitEvent(s, ev[3 * size_t(i - NP) + 2], 0);
+        if (i >= NB) cudaStreamWaitEvent(s, ev[3 * size_t(i - NB) + 2], 0);
         if ((st = apply_impl(p, dF, rows, dG, rows, nc, p->sh[0].ws, s)) != BF_OK) break;
         cudaEventRecord(E[1], s);
         cudaStreamWaitEvent(p->d2h, E[1], 0);
