@@ -15,6 +15,7 @@ Prints ONE JSON line on rank 0.  See DESIGN.md section 7 for every field.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -206,10 +207,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
-    if local_world > 1 and "OMP_NUM_THREADS" not in os.environ:
-        # the untimed host factor builder is OpenMP: share the host cores between the ranks of this node
-        # (must be set before the library / OpenMP runtime is loaded)
-        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_world))
+    # Host OpenMP threads (the untimed factor builder; the oracle of the reference arm).  torchrun exports
+    # OMP_NUM_THREADS=1 to every rank by default, which would make the builder and the reference arm
+    # single-threaded: replace that default.  GPU arm: share the node's cores between its ranks; reference
+    # arm: rank 0 works alone and takes all of them.  Set before our libraries load libgomp, and also
+    # through omp_set_num_threads in case it is already initialized.
+    torchrun_default = os.environ.get("OMP_NUM_THREADS") == "1" and "TORCHELASTIC_RUN_ID" in os.environ
+    if torchrun_default or (local_world > 1 and "OMP_NUM_THREADS" not in os.environ):
+        ncores = os.cpu_count() or 1
+        nthr = ncores if args.impl == "reference" else max(1, ncores // local_world)
+        os.environ["OMP_NUM_THREADS"] = str(nthr)
+        try:
+            ctypes.CDLL("libgomp.so.1").omp_set_num_threads(ctypes.c_int(nthr))
+        except OSError:
+            pass
     w = W.CONFIGS[args.config]
     if args.nrhs:
         w = w.with_(nrhs=args.nrhs)
