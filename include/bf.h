@@ -158,7 +158,8 @@ bf_status_t bf_plan_finalize(bf_plan_t plan);
 bf_status_t bf_apply(bf_plan_t plan, const bf_c64 *F, bf_c64 *G, int64_t nrhs, void *stream);
 
 /* As bf_apply with leading dimensions (ldf, ldg >= N, even) and an optional
- * caller workspace (device, 16-byte aligned, >= bf_workspace_bytes(plan, chunk)). */
+ * caller workspace (device, 16-byte aligned, >= bf_workspace_bytes(plan, chunk)).
+ * F or G not 16-byte aligned, or an odd ldf / ldg: BF_ERR_ALIGNMENT. */
 bf_status_t bf_apply_ex(bf_plan_t plan, const bf_c64 *F, int64_t ldf, bf_c64 *G, int64_t ldg, int64_t nrhs,
                         void *workspace, size_t workspace_bytes, void *stream);
 
@@ -203,8 +204,8 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        destination shard's receive array (peer memory over NVLink via CUDA IPC for one
  *                        shard per GPU; the same device for emulated shards), ordered by stream-ordered
  *                        barriers.  Enabling it is collective for NCCL plans (every rank must call it).
- *                        Not available when h == l0 or with a caller workspace (bf_apply_ex), where the
- *                        separate exchange is used. */
+ *                        Not available when h == l0 (BF_ERR_NOT_SUPPORTED).  While it is on, bf_apply_ex with a
+ *                        caller workspace returns BF_ERR_NOT_SUPPORTED (the peers store into the plan workspace). */
 #define BF_OPT_EXCHANGE 4
 /*   BF_OPT_BAND_COMPOSE  1 (default): the tensor-core band applies its two transfer levels as one composed
  *                        4 x 4 block operator per group of 4 pairs (C = W_{l+1} W_l per block path, formed

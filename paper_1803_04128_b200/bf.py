@@ -81,6 +81,19 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        if "BF_NCCL_LIB" not in os.environ:
+            # index-sharded plans dlopen NCCL on first use: point them at the NCCL torch.distributed uses
+            # (the nvidia-nccl wheel), not whichever libnccl.so.2 the loader finds first
+            import importlib.util
+            try:
+                spec = importlib.util.find_spec("nvidia.nccl")
+            except (ImportError, ValueError):
+                spec = None
+            for d in (spec.submodule_search_locations or []) if spec else []:
+                cand = os.path.join(d, "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["BF_NCCL_LIB"] = cand
+                    break
         L = ctypes.CDLL(LIB_PATH)
         vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
         P = ctypes.POINTER

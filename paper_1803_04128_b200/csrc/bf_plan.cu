@@ -86,8 +86,8 @@ Nccl& nccl()
     static bool tried = false;
     if (tried) return n;
     tried = true;
-    const char* cands[] = {getenv("BF_NCCL_LIB"), "libnccl.so.2", "libnccl.so",
-                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    // BF_NCCL_LIB (the Python binding points it at the NCCL torch loaded), else the standard sonames
+    const char* cands[] = {getenv("BF_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
     void* h = nullptr;
     for (const char* c : cands)
         if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
@@ -150,12 +150,14 @@ struct bf_plan_s {
     float2* peer_ws[bfs::kMaxShards] = {};   // workspace base of every shard (IPC-mapped for NCCL plans)
     bool peer_ipc[bfs::kMaxShards] = {};     // opened with cudaIpcOpenMemHandle (closed at destroy)
     char* bar_buf = nullptr;                 // 2 x world bytes for the stream-ordered NCCL barrier
-    std::vector<std::vector<int64_t>> uploaded;   // [shard][stage slot]
+    // [shard][stage slot]: block ranges [begin, end) uploaded so far (finalize checks their union covers the stage)
+    std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>> uploaded;
     bool finalized = false;
     size_t ws_bytes = 0;       // per shard
     // end-to-end staging (lazily allocated by bf_apply_host)
     float2* dF = nullptr;
     float2* dG = nullptr;
+    int64_t staging_elems = 0;   // complex elements of dF / dG each
     cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the pipelined bf_apply_host
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
     bfk::BandVariant band;     // BF_OPT_BAND_COMPOSE / BF_OPT_BAND_F16 / BF_OPT_BAND_PIPELINES
@@ -615,7 +617,7 @@ bf_status_t alloc_plan(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk
     const int nsh = (mode == BF_SHARD_EMULATED) ? world : 1;
     p->sh.resize(nsh);
     const int nx = p->d.D - p->d.l0;
-    p->uploaded.assign(nsh, std::vector<int64_t>(5 + nx, 0));
+    p->uploaded.assign(nsh, std::vector<std::vector<std::pair<int64_t, int64_t>>>(5 + nx));
     const int64_t n = p->nloc(), r = p->d.R, n0 = int64_t(1) << p->d.l0;
     const int64_t nv = max_nrhs_chunk * p->d.n_amp;
     p->ws_bytes = size_t(2) * size_t(n * r) * size_t(nv) * sizeof(float2);
@@ -660,7 +662,7 @@ bf_status_t bfp_stage_dst(bf_plan_t p, int shard, int32_t stage, int64_t begin, 
         return fail(BF_ERR_INVALID_ARG, "block range [%lld,%lld) out of [0,%lld)", (long long)begin,
                     (long long)(begin + count), (long long)stage_blocks(p, stage));
     *dst = stage_base(p->sh[shard], stage) + begin * stage_elems(p, stage);
-    p->uploaded[shard][slot] += count;
+    if (count > 0) p->uploaded[shard][slot].push_back({begin, begin + count});
     return BF_OK;
 }
 
@@ -802,9 +804,18 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
     for (size_t i = 0; i < p->sh.size(); i++)
         for (int slot = 0; slot < 5 + nx; slot++) {
             const int stage = slot < 5 ? slot : BF_STAGE_XFER0 + (slot - 5);
-            if (p->uploaded[i][slot] < stage_blocks(p, stage))
-                return fail(BF_ERR_STATE, "shard %zu stage %d: %lld of %lld blocks uploaded", i, stage,
-                            (long long)p->uploaded[i][slot], (long long)stage_blocks(p, stage));
+            // union of the uploaded ranges: the first block not covered (overlapping or repeated uploads of
+            // one range do not count twice)
+            auto rs = p->uploaded[i][slot];
+            std::sort(rs.begin(), rs.end());
+            int64_t covered = 0;
+            for (const auto& r : rs) {
+                if (r.first > covered) break;
+                covered = std::max(covered, r.second);
+            }
+            if (covered < stage_blocks(p, stage))
+                return fail(BF_ERR_STATE, "shard %zu stage %d: block %lld of %lld not uploaded", i, stage,
+                            (long long)covered, (long long)stage_blocks(p, stage));
         }
     DeviceGuard g(p->device);
     // fold the switch into the factor that produces level h: XFER_h, or V0 when h == l0 (no transfer level
@@ -881,11 +892,17 @@ bf_status_t bf_apply_ex(bf_plan_t p, const bf_c64* F, int64_t ldf, bf_c64* G, in
     if (ldf < rows || ldg < rows)
         return fail(BF_ERR_ALIGNMENT, "ldf=%lld / ldg=%lld < rows=%lld", (long long)ldf, (long long)ldg,
                     (long long)rows);
-    if ((reinterpret_cast<uintptr_t>(F) | reinterpret_cast<uintptr_t>(G)) % 8)
-        return fail(BF_ERR_ALIGNMENT, "F/G not 8-byte aligned");
+    // 16-byte aligned columns (the tensor-core S0 bulk-copies F columns; cp.async.bulk needs a 16-B source)
+    if ((reinterpret_cast<uintptr_t>(F) | reinterpret_cast<uintptr_t>(G)) % 16)
+        return fail(BF_ERR_ALIGNMENT, "F/G not 16-byte aligned");
+    if ((ldf | ldg) & 1) return fail(BF_ERR_ALIGNMENT, "ldf=%lld / ldg=%lld not even", (long long)ldf, (long long)ldg);
     float2* ws = p->sh[0].ws;
     if (workspace) {
         if (p->mode == BF_SHARD_EMULATED) return fail(BF_ERR_NOT_SUPPORTED, "emulated plans use their own workspace");
+        // the fused exchange stores into the peers' plan workspaces (IPC-mapped): every rank must use its plan
+        // workspace, else the ranks would run different exchange protocols and hang
+        if (p->exchange_peer)
+            return fail(BF_ERR_NOT_SUPPORTED, "a caller workspace cannot be used with the fused exchange (BF_OPT_EXCHANGE = 1)");
         if (reinterpret_cast<uintptr_t>(workspace) % 16) return fail(BF_ERR_ALIGNMENT, "workspace not 16-byte aligned");
         if (workspace_bytes < bf_workspace_bytes(p, std::min(nrhs, p->max_chunk)))
             return fail(BF_ERR_INVALID_ARG, "workspace of %zu B < %zu B", workspace_bytes,
@@ -918,8 +935,6 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
     DeviceGuard g(p->device);
     const int64_t rows = (p->mode == BF_SHARD_NCCL) ? p->nloc() : p->d.N, chunk = p->max_chunk;
     bf_status_t st;
-    if (!p->dF && ((st = dalloc(&p->dF, rows * chunk, "e2e F")) || (st = dalloc(&p->dG, rows * chunk, "e2e G"))))
-        return st;
     cudaError_t e;
     if (!p->h2d && ((e = cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
                     (e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking)) != cudaSuccess))
@@ -953,6 +968,17 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
         for (int64_t c = 0; c < nrhs; c += part) pcs.push_back({c, std::min(part, nrhs - c)});
     }
     const int64_t npieces = int64_t(pcs.size());
+    // staging ring: NB slots of the largest piece (the pieces of one span are not all equal)
+    for (const auto& pc : pcs) part = std::max(part, pc.second);
+    const int64_t need = rows * NB * part;
+    if (p->staging_elems < need) {
+        cudaFree(p->dF);
+        cudaFree(p->dG);
+        p->dF = p->dG = nullptr;
+        p->staging_elems = 0;
+        if ((st = dalloc(&p->dF, need, "e2e F")) || (st = dalloc(&p->dG, need, "e2e G"))) return st;
+        p->staging_elems = need;
+    }
     std::vector<cudaEvent_t> ev(3 * size_t(npieces), nullptr);   // [h2d done, apply done, d2h done] per piece
     for (auto& x : ev)
         if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) break;

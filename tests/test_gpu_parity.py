@@ -255,3 +255,75 @@ def test_timing_counts_launches():
     assert n == 2 * info["launches_per_chunk"]      # 2 chunks
     assert all(v[0] >= 0 for v in t.values())
     plan.set_timing(False)
+
+
+@pytest.mark.parametrize("chunk", [5, 7, 9])
+@pytest.mark.parametrize("pieces", [2, 3, 4])
+def test_apply_host_piece_layouts(chunk, pieces):
+    """bf_apply_host's staging ring holds the largest piece of every layout (odd chunks, tapered pieces)."""
+    plan = _small_plan(nrhs_chunk=chunk)
+    plan.set_option(bf.BF_OPT_HOST_PIECES, pieces)
+    N, nrhs = 1 << 12, 2 * chunk + 3
+    F = W.rhs(N, nrhs, 20 + chunk)
+    ref = gpu_apply(plan, F)
+    Fh = torch.from_numpy(np.ascontiguousarray(F.T)).pin_memory()
+    Gh = torch.empty_like(Fh).pin_memory()
+    plan.apply_host(Fh, Gh, nrhs)
+    assert np.array_equal(np.asfortranarray(Gh.numpy().T), ref)
+
+
+def test_alignment_rejected():
+    """F/G must be 16-byte aligned and ld even (bf.h): a view offset by one complex64 is refused with
+    BF_ERR_ALIGNMENT instead of faulting the bulk copies of the tensor-core S0."""
+    plan = _small_plan()
+    N = 1 << 12
+    buf = torch.zeros(2 * N + 1, dtype=torch.complex64, device="cuda")
+    G = torch.zeros(2 * N, dtype=torch.complex64, device="cuda")
+    with pytest.raises(bf.BFError) as e:
+        plan.apply(buf[1:], G, 2)
+    assert e.value.status == 3
+    Fp = torch.zeros(2 * (N + 1), dtype=torch.complex64, device="cuda")
+    with pytest.raises(bf.BFError) as e:
+        plan.apply_ex(Fp, N + 1, torch.zeros_like(Fp), N + 1, 2)
+    assert e.value.status == 3
+    plan.apply(buf[2:], G, 2)                                   # 16-byte aligned view: fine
+    torch.cuda.synchronize()
+
+
+def test_upload_coverage():
+    """finalize needs every block of every stage: repeating one range does not make up for a missing one."""
+    import ctypes
+    LN, l0, r = 10, 4, 12
+    N = 1 << LN
+    a, b, v0, xf, sw, u = _host_factors(W.K_FIO, W.A_CFG1, LN, l0, r)
+    L = bf.lib()
+
+    def alloc():
+        d = bf.bf_desc_t(bf.BF_ABI_VERSION, LN, l0, r, a.shape[0], bf.BF_MEM_HOST)
+        h = ctypes.c_void_p()
+        assert L.bf_plan_alloc(ctypes.byref(d), 0, 1, ctypes.byref(h)) == 0
+        return h
+
+    def up(h, stage, arr, b0, n):
+        assert L.bf_plan_upload(h, stage, b0, n, arr[b0:].ctypes.data, bf.BF_MEM_HOST) == 0
+
+    for overlap in (True, False):
+        h = alloc()
+        up(h, bf.BF_STAGE_AMP_A, a, 0, a.shape[0])
+        up(h, bf.BF_STAGE_AMP_B, b, 0, b.shape[0])
+        up(h, bf.BF_STAGE_SW, sw, 0, N)
+        up(h, bf.BF_STAGE_U, u, 0, N)
+        for i, x in enumerate(xf):
+            up(h, bf.BF_STAGE_XFER0 + i, x, 0, N)
+        up(h, bf.BF_STAGE_V0, v0, 0, N // 2)
+        if overlap:
+            up(h, bf.BF_STAGE_V0, v0, 0, N // 2)                 # the same half twice: N blocks counted
+            assert L.bf_plan_finalize(h) == 8                    # BF_ERR_STATE
+            up(h, bf.BF_STAGE_V0, v0, N // 4, 3 * N // 4)        # overlapping ranges that cover the rest
+        else:
+            up(h, bf.BF_STAGE_V0, v0, N // 2, N // 2)
+        assert L.bf_plan_finalize(h) == 0
+        p = bf.Plan(h.value)
+        ref = bf.Plan.from_arrays(LN, l0, r, a, b, v0, xf, sw, u, max_nrhs_chunk=1)
+        F = W.rhs(N, 1, 3)
+        assert np.array_equal(gpu_apply(p, F), gpu_apply(ref, F))

@@ -133,4 +133,10 @@ def test_nccl_world1_fused_exchange():
     plan = bf.Plan.build_fio_sharded(k, 0, 1, bf.nccl_unique_id(), max_nrhs_chunk=6)
     plan.set_option(bf.BF_OPT_EXCHANGE, 1)
     assert np.array_equal(_apply(plan, F), ref)
+    # a caller workspace would silently switch this rank to the other exchange protocol: refused
+    Ft = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()
+    ws = torch.empty(plan.workspace_bytes(6) // 8, dtype=torch.complex64, device="cuda")
+    with pytest.raises(bf.BFError) as e:
+        plan.apply_ex(Ft, 1 << 14, torch.empty_like(Ft), 1 << 14, 6, workspace=ws, workspace_bytes=plan.workspace_bytes(6))
+    assert e.value.status == 7
     plan.destroy()
