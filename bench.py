@@ -5,8 +5,10 @@
 One step = one bf_apply of the whole hot path (S0, all transfer levels with the
 switch, SL) over one batch of 256 complex64 RHS of BASELINE config 4 (N = 2^20,
 leaf 64, r = 10, 2 amplitude terms), inputs resident in HBM.  Multi-GPU: one
-process per GPU (torchrun), RHS-sharded with no collective on the data path:
-every rank applies the replicated plan to its own 256 columns (weak scaling).
+process per GPU (torchrun; `--gpus N` without torchrun launches it), RHS-sharded
+as config 4 says: rank q applies the replicated plan to columns
+[q 256/N, (q+1) 256/N) of the one seeded batch, no collective on the data path
+(strong scaling; value = N.256 / max-over-ranks time).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -134,6 +136,24 @@ def stage_model(w, nvec, info):
     return out
 
 
+def rhs_columns(nrhs: int, world: int, rank: int):
+    """Columns [c0, c1) of the global RHS batch that rank `rank` of `world` applies (contiguous,
+    balanced; the RHS are independent units, so the ranks' results concatenate to the 1-GPU result)."""
+    return rank * nrhs // world, (rank + 1) * nrhs // world
+
+
+def _self_launch(args) -> int:
+    """`--gpus N` (N > 1) outside torchrun: start N ranks on this node with torch.distributed.run (127.0.0.1)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def cpu_oracle_sample(w):
     """The oracle as it stands on the host cores: cfg4's full-N butterfly for ONE RHS column
     (its 2 amplitude vectors), blocks generated on the fly in FP64."""
@@ -165,7 +185,7 @@ def run_reference(args, w, rank, world):
               f"FP64 CPU oracle with on-the-fly blocks")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussian RHS, closed-form kernel)",
         "config": {"workload": "cfg4", "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
                    "nrhs_per_step": 1},
@@ -182,7 +202,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--nrhs", type=int, default=None, help="RHS per rank (default: the config's)")
+    ap.add_argument("--nrhs", type=int, default=None, help="global RHS batch (default: the config's), split over the ranks")
     ap.add_argument("--chunk", type=int, default=None, help="max_nrhs_chunk (default: all RHS in one chunk)")
     ap.add_argument("--log2n", type=int, default=None, help="override N (profiling of a smaller instance only)")
     ap.add_argument("--index-shard", action="store_true",
@@ -203,8 +223,12 @@ def main():
                     help="tensor-core band variant (tuning; default: the library's)")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ and args.gpus != 1:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     # Host OpenMP threads (the untimed factor builder; the oracle of the reference arm).  torchrun exports
@@ -243,7 +267,12 @@ def main():
         if world > 1:
             dist.barrier()
 
-    chunk = args.chunk or w.nrhs
+    if args.index_shard:
+        c0, c1 = 0, w.nrhs   # every rank holds all columns, a 1/G slice of the rows
+    else:
+        c0, c1 = rhs_columns(w.nrhs, world, rank)
+    nloc = c1 - c0   # columns this rank applies per step
+    chunk = args.chunk or nloc
     t0 = time.perf_counter()
     if args.index_shard:
         # one batch split by index: rank q owns xi-rows and x-rows [q N/G, (q+1) N/G) (strong scaling)
@@ -258,8 +287,8 @@ def main():
         F = np.asfortranarray(F[rank * rows:(rank + 1) * rows])
     else:
         plan = bf.Plan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=chunk)
-        # this rank's RHS: columns [rank*nrhs, (rank+1)*nrhs) of the seeded global batch (weak scaling)
-        F = W.rhs(w.n, w.nrhs, w.seed + 1000 * rank)
+        # this rank's RHS: columns [c0, c1) of the one seeded global batch (strong scaling)
+        F = W.rhs(w.n, w.nrhs, w.seed) if world == 1 else W.rhs(w.n, w.nrhs, w.seed, cols=range(c0, c1))
     t_build = time.perf_counter() - t0
     if args.band_pipelines:
         plan.set_option(bf.BF_OPT_BAND_PIPELINES, args.band_pipelines)
@@ -277,7 +306,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     for _ in range(args.warmup):
-        plan.apply(Fd, Gd, w.nrhs, stream)
+        plan.apply(Fd, Gd, nloc, stream)
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, device-timed with CUDA events on the launching stream ----
@@ -288,7 +317,7 @@ def main():
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            plan.apply(Fd, Gd, w.nrhs, stream)
+            plan.apply(Fd, Gd, nloc, stream)
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -299,17 +328,16 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    chunks = -(-w.nrhs // chunk)
+    chunks = -(-nloc // chunk)
     launches = info["launches_per_chunk"] * chunks * args.steps
-    jobs = 1 if args.index_shard else world   # batches processed by the whole job per step
-    value = w.n * w.nrhs * jobs / (ms / 1e3)
+    value = w.n * w.nrhs / (ms / 1e3)   # the whole batch of w.nrhs columns per step, all ranks together
 
     # ---- roofline of the dominant kernel class ----
     hbm, hbm_src, tf32, tf32_src, f16 = _peaks()
     wl = w.with_(log2n=w.log2n - (world.bit_length() - 1)) if args.index_shard else w   # this rank's share
-    model = stage_model(wl, min(chunk, w.nrhs) * w.n_amp, info)
+    model = stage_model(wl, min(chunk, nloc) * w.n_amp, info)
     # the level-h exchange moves (G-1)/G of the local coefficients out and as much in
-    model["exchange"] = (0, 2 * 8 * wl.n * w.rank * min(chunk, w.nrhs) * w.n_amp * (world - 1) // world)
+    model["exchange"] = (0, 2 * 8 * wl.n * w.rank * min(chunk, nloc) * w.n_amp * (world - 1) // world)
     tc_classes = set(info["tc_classes"])
     f16_classes = set(info["f16_classes"])
 
@@ -349,26 +377,26 @@ def main():
     tot_f = sum(model[k][0] * ktimes[k][1] for k in model) / args.steps
     lbl = sum(max(times(k)) * ktimes[k][1] for k in model if k != "exchange") / args.steps
     comp = sum(times(k)[0] * ktimes[k][1] for k in model if k != "exchange") / args.steps
-    fused = max(comp, (16 * wl.n * w.nrhs + info["factor_bytes"]) / (hbm * 1e9))
+    fused = max(comp, (16 * wl.n * nloc + info["factor_bytes"]) / (hbm * 1e9))
 
     # ---- end to end: host buffers through the C ABI (bf_apply_host), copies inside the timed region ----
     e2e = None
     if not args.no_e2e:
         Fh = torch.from_numpy(np.ascontiguousarray(F.T)).pin_memory()
         Gh = torch.empty_like(Fh).pin_memory()
-        plan.apply_host(Fh, Gh, w.nrhs, stream)    # warm-up (allocates the staging buffers once)
+        plan.apply_host(Fh, Gh, nloc, stream)    # warm-up (allocates the staging buffers once)
         ne = max(1, min(args.steps, 3))
         barrier()
         t0 = time.perf_counter()
         for _ in range(ne):
-            plan.apply_host(Fh, Gh, w.nrhs, stream)   # synchronizes: the result is on the host
+            plan.apply_host(Fh, Gh, nloc, stream)   # synchronizes: the result is on the host
         te = (time.perf_counter() - t0) / ne
         if world > 1:
             t = torch.tensor([te], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         nb = Fd.numel() * 8
-        e2e = {"value": w.n * w.nrhs * jobs / te, "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+        e2e = {"value": w.n * w.nrhs / te, "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
                "ms_per_step": te * 1e3, "steps": ne}
 
     cpu = None
@@ -379,19 +407,19 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if args.index_shard else "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": ("c64: tcgen05 split products with FP32 accumulation (" +
                       ", ".join(f"{k} {'3xFP16' if k in f16_classes else '3xTF32'}" for k in sorted(tc_classes)) + ")")
                      if tc_classes else "c64 (fp32 FFMA)",
             "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel; factors from the host builder)",
             "config": {"workload": args.config, "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
-                       "nrhs_per_gpu": w.nrhs if not args.index_shard else w.nrhs,
-                       "global_batch": w.nrhs * jobs, "max_nrhs_chunk": chunk,
+                       "nrhs_per_gpu": nloc, "global_batch": w.nrhs, "max_nrhs_chunk": chunk,
                        "parallelism": (f"index-sharded x{world} (level-h exchange: "
                                        + ("peer stores from the level-h launch)" if args.exchange == "fused"
                                           else "NCCL all-to-all)") if args.index_shard
-                                       else f"rhs-sharded x{world} (no collective)"),
+                                       else f"rhs-sharded x{world}: rank q applies columns [q {w.nrhs}/{world}, "
+                                            f"(q+1) {w.nrhs}/{world}) (no collective)"),
                        "l2": "no flush: the working set (F 2.1 GB, coefficients 43 GB/level, factors 25 GB) "
                              "exceeds the 126 MB L2",
                        "tensor_core_classes": info["tc_classes"], "tc_weight_bytes": info["tc_weight_bytes"]},

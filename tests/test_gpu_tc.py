@@ -313,3 +313,31 @@ def test_cuda_graph_capture(nrhs):
     assert torch.equal(Gout, ref2)
     del g
     plan.destroy()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_rhs_shards_concatenate_to_one_gpu(world):
+    """bench.py's RHS sharding: each rank applies columns [q nrhs/G, (q+1) nrhs/G) with its own
+    replicated plan; the blocks concatenate to the one-GPU result.  Bitwise while every shard takes the same
+    kernels as the full batch (each vector's reduction order does not depend on the batch); a shard whose
+    vector count falls to another kernel class agrees within the paths' FP32 agreement."""
+    import bench
+    k = bf.fio(W.K_FIO, W.A_CFG1, 14, 6, 10)   # cfg4's shape at N = 2^14
+    nrhs = 256
+    F = W.rhs(1 << 14, nrhs, 3)
+    full = bf.Plan.build_fio(k, max_nrhs_chunk=nrhs)
+    ref, tc_full = _apply(full, F), set(full.info()["tc_classes"])
+    full.destroy()
+    blocks, same = [], True
+    for q in range(world):
+        c0, c1 = bench.rhs_columns(nrhs, world, q)
+        p = bf.Plan.build_fio(k, max_nrhs_chunk=c1 - c0)
+        same &= set(p.info()["tc_classes"]) == tc_full
+        blocks.append(_apply(p, np.asfortranarray(F[:, c0:c1])))
+        p.destroy()
+    G = np.concatenate(blocks, axis=1)
+    if same:
+        assert np.array_equal(G, ref)
+    else:
+        err = oracle.rel_l2(G.astype(np.complex128), ref.astype(np.complex128), axis=0)
+        assert np.all(err <= PATHS_AGREE), err.max()
