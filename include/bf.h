@@ -234,6 +234,11 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        tile (V0x / Ux) and multicasting it to both (needs an even number of 128-vector tiles
  *                        per chunk; else one CTA per tile); 0: off. */
 #define BF_OPT_LEAF_MULTICAST 9
+/*   BF_OPT_SMALL_BAND    1 (default): transfer levels of chunks with 8 <= nv < 128 vectors (nv % 8 == 0) run two
+ *                        levels per launch in the persistent small-batch band kernel (bulk-copy-fed ring of 4-pair
+ *                        jobs, one job per warp); 0: one level per launch (xfer kernel).
+ *                        Both compute every output with the same FP32 operation order (bitwise equal). */
+#define BF_OPT_SMALL_BAND 10
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band

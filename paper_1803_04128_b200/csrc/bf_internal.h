@@ -65,6 +65,12 @@ bool band_supported(int R, int nv);
 cudaError_t launch_band(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W, int nv,
                         cudaStream_t s, int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr);
 
+// Band of K (1 or 2) transfer levels for small vector batches (bf_small.cu: 8 <= nv < 128, nv % 8 == 0):
+// persistent, bulk-copy-fed, one 4-pair job per warp; same contract as launch_band.
+bool band_sv_supported(const Dims& d, int nv);
+cudaError_t launch_band_sv(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W,
+                           int nv, cudaStream_t s, int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr);
+
 // Band of 2 transfer levels on the tensor cores (bf_tc.cu): same contract as launch_band with K = 2.
 bool band_tc_supported(const Dims& d, int nv);
 // which tensor-core band kernel runs (per plan: BF_OPT_BAND_COMPOSE, BF_OPT_BAND_F16, BF_OPT_BAND_PIPELINES)

@@ -33,7 +33,7 @@ def _apply(plan, F):
 
 CASES = [
     # kernel, amp, LN, l0, r, nrhs, chunk, worlds
-    (W.K_FIO, W.A_CFG1, 16, 6, 10, 8, 8, (2, 4, 8)),        # cfg5's shape at reduced N: per-level kernels
+    (W.K_FIO, W.A_CFG1, 16, 6, 10, 8, 8, (2, 4, 8)),        # cfg5 shape at reduced N: small-batch bands (nv 16)
     (W.K_FIO, W.A_CFG1, 14, 5, 10, 70, 70, (2, 4)),         # bands, odd first half (levels 6,7 | exchange)
     (W.K_FIO_JUMP, W.A_CFG3, 16, 5, 8, 33, 20, (2, 8)),     # n_amp 4, ragged chunks (80 + 52 vectors)
 ]

@@ -44,6 +44,10 @@ def summarize(report):
             if key in hdr:
                 i = hdr.index(key)
                 print(f"  {name:16s} {r[i]:>16s} {units[i]}")
+        # tensor-pipe utilisation (tcgen05 kernels): every sm__pipe_tensor* / *tmem* percentage the report has
+        for i, h in enumerate(hdr):
+            if ("pipe_tensor" in h or "tmem" in h.lower() or "pipe_uniform" in h) and "pct" in h and r[i]:
+                print(f"  {h[:70]:70s} {r[i]:>10s}")
         vals = sorted(((float(r[i] or 0), hdr[i]) for i in stall), reverse=True)[:6]
         tot = sum(float(r[i] or 0) for i in stall)
         print("  stalls (warps per issue):", ", ".join(
