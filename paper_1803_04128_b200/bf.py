@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbfapply.so")
+LIB_PATH = os.environ.get("BF_LIB") or os.path.join(HERE, "libbfapply.so")   # BF_LIB: tuning variants only
 
 BF_ABI_VERSION = 1
 BF_MEM_HOST, BF_MEM_DEVICE = 0, 1

@@ -37,24 +37,31 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Build libbfapply.so (or, with `out`, a tuning variant at that path from a separate build directory)."""
+    global LIB, BUILD_DIR
+    if out:
+        LIB, BUILD_DIR = out, out + ".build"
     stamp = os.path.join(BUILD_DIR, "digest")
     dig = _digest()
     if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == dig:
         return LIB
     os.makedirs(BUILD_DIR, exist_ok=True)
-    objs = []
+    jobs = []
     for src in CU_SOURCES:
         obj = os.path.join(BUILD_DIR, src + ".o")
         cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
-        _run(cmd, os.path.join(BUILD_DIR, src + ".ptxas.log"), verbose)
-        objs.append(obj)
+        jobs.append((cmd, os.path.join(BUILD_DIR, src + ".ptxas.log"), obj))
     for src in CXX_SOURCES:
         obj = os.path.join(BUILD_DIR, src + ".o")
         cmd = ["g++", *CXX_FLAGS, "-I", INCLUDE, "-I", "/usr/local/cuda/include", "-c", os.path.join(CSRC, src),
                "-o", obj]
-        _run(cmd, None, verbose)
-        objs.append(obj)
+        jobs.append((cmd, None, obj))
+    from concurrent.futures import ThreadPoolExecutor   # the translation units compile independently
+    with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        for f in [ex.submit(_run, c, log, verbose) for c, log, _ in jobs]:
+            f.result()
+    objs = [o for _, _, o in jobs]
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp"]
     _run(cmd, None, verbose)

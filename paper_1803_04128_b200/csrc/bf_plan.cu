@@ -1058,7 +1058,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
         if (p->tensor_cores && (p->sh[0].v0x || p->sh[0].v0h) && bfk::s0_tc_supported(dl, nvf, dl.N))
             mask |= 1 << bfk::KC_S0;
         if (p->tensor_cores && (p->sh[0].ux || p->sh[0].uh) && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
-        if (p->tensor_cores && bfk::band_supported(dl.R, nvf) && bfk::band_tc_supported(dl, nvf))
+        if (p->tensor_cores && bfk::band_tc_supported(dl, nvf))
             for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE, p->small_band))
                 if (stp.kind == Step::BAND && stp.K == 2) mask |= 1 << stp.cls;
         info->tc_class_mask = mask;

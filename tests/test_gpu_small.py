@@ -59,8 +59,7 @@ def test_small_band_parity(kernel, amp, LN, l0, r, nrhs, cols):
     info = plan.info()
     nx = LN - 2 * l0
     launches = sum(info["class_launches"][k] for k in ("xfer_first_half", "xfer_switch", "xfer_second_half"))
-    half1 = LN // 2 - l0
-    assert launches == (half1 + 1) // 2 + (nx - half1 + 1) // 2, info["class_launches"]   # bands of 2
+    assert launches == (nx + 1) // 2, info["class_launches"]   # bands of 2 (unsharded: across h too)
     G = _apply(plan, F)
     plan.set_option(bf.BF_OPT_SMALL_BAND, 0)
     G1 = _apply(plan, F)

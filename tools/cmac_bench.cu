@@ -24,6 +24,32 @@ __global__ void ffma_peak(float* out, int iters)
     if (s == 1234.5f) out[0] = s;
 }
 
+// the same with packed FP32 pairs (sm_100a FFMA2): 8 independent chains of 2-wide FMAs
+__global__ void ffma2_peak(float* out, int iters)
+{
+    unsigned long long a[8];
+    for (int i = 0; i < 8; i++) {
+        const float lo = threadIdx.x * 1e-7f + i, hi = lo + 0.5f;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(a[i]) : "f"(lo), "f"(hi));
+    }
+    unsigned long long b, c;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(0.999999f));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(1e-7f));
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+#pragma unroll
+            for (int i = 0; i < 8; i++) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[i]) : "l"(b), "l"(c));
+    }
+    float s = 0;
+    for (int i = 0; i < 8; i++) {
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a[i]));
+        s += lo + hi;
+    }
+    if (s == 1234.5f) out[0] = s;
+}
+
 __device__ __forceinline__ void cmac(float2& acc, float2 w, float2 v)
 {
     acc.x = fmaf(w.x, v.x, acc.x);
@@ -136,7 +162,7 @@ static void run(const char* name, K kern, int blocks, int threads, int iters, do
     cudaEventElapsedTime(&ms, a, b);
     const double fl = double(blocks) * threads * iters * flops_per_thread_iter;
     int clk = 0;
-    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);   // kHz
     printf("%-16s %8.3f ms  %7.2f TFLOP/s  (%.1f%% of 148x128x2x%.3f GHz)\n", name, ms, fl / ms / 1e9,
            100.0 * fl / ms / 1e9 / (148 * 128 * 2 * clk * 1e-6), clk * 1e-6);
     cudaFree(out);
@@ -146,6 +172,12 @@ int main()
 {
     const int blocks = 148 * 8;
     run("ffma_peak", ffma_peak, blocks, 256, 20000, 16.0 * 8 * 2);
+    run("ffma2_peak", ffma2_peak, blocks, 256, 20000, 16.0 * 8 * 4);
+    // low occupancy: 8 warps per SM (2 per sub-partition), as the persistent small-batch band runs
+    run("ffma_8w", ffma_peak, 148, 256, 20000, 16.0 * 8 * 2);
+    run("ffma2_8w", ffma2_peak, 148, 256, 20000, 16.0 * 8 * 4);
+    run("ffma_4w", ffma_peak, 148, 128, 20000, 16.0 * 8 * 2);
+    run("ffma2_4w", ffma2_peak, 148, 128, 20000, 16.0 * 8 * 4);
     run("cmac_inter<10>", cmac_inter<10>, 148 * 2 * 8, 256, 400, 64.0 * 10 * 4 * 8);
     run("cmac_planar<10>", cmac_planar<10>, 148 * 2 * 8, 256, 400, 64.0 * 10 * 4 * 8);
     run("cmac_inter<8>", cmac_inter<8>, 148 * 2 * 8, 256, 400, 64.0 * 8 * 4 * 8);
