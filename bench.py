@@ -220,8 +220,8 @@ def main():
     ap.add_argument("--leaf-f16", action="store_true",
                     help="leaf stages in FP16 split passes instead of 3xTF32 (BF_OPT_LEAF_F16 = 1, opt-in)")
     ap.add_argument("--no-tc", action="store_true", help="every stage on the FP32 kernels (BF_OPT_TENSOR_CORES = 0)")
-    ap.add_argument("--no-small-band", action="store_true",
-                    help="small vector batches: one transfer level per launch (BF_OPT_SMALL_BAND = 0)")
+    ap.add_argument("--no-small-batch", action="store_true",
+                    help="small vector batches: one transfer level per launch (BF_OPT_SMALL_BATCH = 0)")
     ap.add_argument("--band-pipelines", type=int, default=None, choices=[1, 2],
                     help="tensor-core band variant (tuning; default: the library's)")
     args = ap.parse_args()
@@ -295,8 +295,8 @@ def main():
     t_build = time.perf_counter() - t0
     if args.no_tc:
         plan.set_tensor_cores(False)
-    if args.no_small_band:
-        plan.set_option(bf.BF_OPT_SMALL_BAND, 0)
+    if args.no_small_batch:
+        plan.set_option(bf.BF_OPT_SMALL_BATCH, 0)
     if args.band_pipelines:
         plan.set_option(bf.BF_OPT_BAND_PIPELINES, args.band_pipelines)
     if args.leaf_f16:

@@ -234,11 +234,13 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        tile (V0x / Ux) and multicasting it to both (needs an even number of 128-vector tiles
  *                        per chunk; else one CTA per tile); 0: off. */
 #define BF_OPT_LEAF_MULTICAST 9
-/*   BF_OPT_SMALL_BAND    1 (default): transfer levels of chunks with 8 <= nv < 128 vectors (nv % 8 == 0) run two
- *                        levels per launch in the persistent small-batch band kernel (bulk-copy-fed ring of 4-pair
- *                        jobs, one job per warp); 0: one level per launch (xfer kernel).
- *                        Both compute every output with the same FP32 operation order (bitwise equal). */
-#define BF_OPT_SMALL_BAND 10
+/*   BF_OPT_SMALL_BATCH   1 (default): chunks of few vectors (nv % 8 == 0) run the persistent small-batch kernels
+ *                        (bf_small.cu: a producer warp bulk-copies weight blocks into a shared-memory ring, one job
+ *                        per consumer warp): transfer levels two per launch for 8 <= nv < 128,
+ *                        S0 for nv <= 56, SL for nv in {8, 16, 32}; 0: the FP32 kernels of bf_kernels.cu (one
+ *                        transfer level per launch).  Both compute every output with the same FP32 operation order
+ *                        (bitwise equal). */
+#define BF_OPT_SMALL_BATCH 10
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band

@@ -71,6 +71,14 @@ bool band_sv_supported(const Dims& d, int nv);
 cudaError_t launch_band_sv(const Dims& d, int l_first, int K, const float2* in, float2* out, const float2* const* W,
                            int nv, cudaStream_t s, int rh = 0, int rhg = 0, const bfs::PeerOut* po = nullptr);
 
+// S0 / SL for small vector batches (bf_small.cu): same contracts as launch_s0 / launch_sl.
+bool s0_sv_supported(const Dims& d, int nv);
+cudaError_t launch_s0_sv(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float2* V0,
+                         float2* out, int nv, cudaStream_t s);
+bool sl_sv_supported(const Dims& d, int nv);
+cudaError_t launch_sl_sv(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,
+                         int nv, cudaStream_t s);
+
 // Band of 2 transfer levels on the tensor cores (bf_tc.cu): same contract as launch_band with K = 2.
 bool band_tc_supported(const Dims& d, int nv);
 // which tensor-core band kernel runs (per plan: BF_OPT_BAND_COMPOSE, BF_OPT_BAND_F16, BF_OPT_BAND_PIPELINES)

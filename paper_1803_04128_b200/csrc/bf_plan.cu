@@ -164,7 +164,7 @@ struct bf_plan_s {
     bool leaf_f16 = false;     // BF_OPT_LEAF_F16 (opt-in: the north_star names 3xTF32 or FP64)
     int host_pieces = 2;       // BF_OPT_HOST_PIECES: bf_apply_host pipeline pieces per chunk
     bool leaf_multicast = true;  // BF_OPT_LEAF_MULTICAST: TF32 S0 / SL as 2-CTA clusters sharing the weight stream
-    bool small_band = true;      // BF_OPT_SMALL_BAND: fused bands for small vector batches (bf_small.cu)
+    bool small_batch = true;      // BF_OPT_SMALL_BATCH: fused bands for small vector batches (bf_small.cu)
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -359,11 +359,11 @@ void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool
 // when the band kernel supports the shape, the switch applied inside the launch that produces level h),
 // SL.  With no transfer level (h == l0) the switch runs alone after S0.  Sharded: the bands stop at h,
 // the exchange follows, then the second half.
-std::vector<Step> schedule(const bfk::Dims& d, int nv, bool sharded, bool small_band)
+std::vector<Step> schedule(const bfk::Dims& d, int nv, bool sharded, bool small_batch)
 {
     std::vector<Step> st;
     st.push_back({Step::S0, 0, 1, bfk::KC_S0, 0});
-    const bool band = bfk::band_supported(d.R, nv) || (small_band && bfk::band_sv_supported(d, nv));
+    const bool band = bfk::band_supported(d.R, nv) || (small_batch && bfk::band_sv_supported(d, nv));
     if (!sharded) {
         push_levels(st, d, d.l0 + 1, d.D, band);
     } else {
@@ -436,6 +436,8 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                     return bfk::launch_s0_h16(dl, F, ldf, sh.amp_b, sh.v0h, sh.v0s, in, nv, s);
                 if (p->tensor_cores && sh.v0x && bfk::s0_tc_supported(dl, nv, ldf))
                     return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s, p->leaf_multicast);
+                if (p->small_batch && nv < 64 && bfk::s0_sv_supported(dl, nv))
+                    return bfk::launch_s0_sv(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
                 return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
             case Step::XFER:
                 return bfk::launch_xfer(dl, lk, in, out, sh.xfer[stp.l_first - p->d.l0 - 1], nv, s, rh, rhg, po);
@@ -444,7 +446,7 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                                       stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
                 if (stp.K == 2 && p->tensor_cores && bfk::band_tc_supported(dl, nv))
                     return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po, p->band);
-                if (p->small_band && bfk::band_sv_supported(dl, nv))
+                if (p->small_batch && bfk::band_sv_supported(dl, nv))
                     return bfk::launch_band_sv(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
                 return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
             }
@@ -453,11 +455,19 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                     return bfk::launch_sl_h16(dl, in, sh.uh, sh.ue, sh.amp_a, G, ldg, nv, s);
                 if (p->tensor_cores && sh.ux && bfk::sl_tc_supported(dl, nv))
                     return bfk::launch_sl_tc(dl, in, sh.ux, sh.amp_a, G, ldg, nv, s, p->leaf_multicast);
+                if (p->small_batch && bfk::sl_sv_supported(dl, nv))
+                    return bfk::launch_sl_sv(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
                 return bfk::launch_sl(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
             default: return cudaErrorInvalidValue;
             }
         });
-        if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+        if (e != cudaSuccess) {
+            static const char* kinds[] = {"S0", "transfer", "band", "SL", "exchange"};
+            char what[96];
+            snprintf(what, sizeof what, "kernel launch (%s, level %d, K %d, nv %d)", kinds[stp.kind], stp.l_first, stp.K,
+                     nv);
+            return cuda_fail(e, what);
+        }
         if (stp.kind == Step::XFER || stp.kind == Step::BAND) {
             cur = 1 - cur;
             remap = false;
@@ -540,7 +550,7 @@ bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, in
     for (int64_t c0 = 0; c0 < nrhs; c0 += chunk) {
         const int64_t nc = std::min(chunk, nrhs - c0);
         const int nv = int(nc * p->d.n_amp);
-        const auto st = schedule(p->d, nv, sharded, p->small_band);
+        const auto st = schedule(p->d, nv, sharded, p->small_batch);
         const float2* Fc = F + c0 * ldf;
         float2* Gc = G + c0 * ldg;
         if (!sharded) {
@@ -1059,7 +1069,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
             mask |= 1 << bfk::KC_S0;
         if (p->tensor_cores && (p->sh[0].ux || p->sh[0].uh) && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
         if (p->tensor_cores && bfk::band_tc_supported(dl, nvf))
-            for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE, p->small_band))
+            for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE, p->small_batch))
                 if (stp.kind == Step::BAND && stp.K == 2) mask |= 1 << stp.cls;
         info->tc_class_mask = mask;
         int fmask = 0;
@@ -1067,7 +1077,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
         if ((mask >> bfk::KC_SL & 1) && p->sh[0].uh) fmask |= 1 << bfk::KC_SL;
         info->f16_class_mask = fmask;
     }
-    const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp), p->mode != BF_SHARD_NONE, p->small_band);
+    const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp), p->mode != BF_SHARD_NONE, p->small_batch);
     info->launches_per_chunk = 0;
     for (int i = 0; i < BF_NUM_KCLASS; i++) info->class_launches[i] = info->class_levels[i] = 0;
     for (const auto& x : st) {
@@ -1186,9 +1196,9 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
         p->leaf_multicast = value != 0;
         return BF_OK;
     }
-    if (option == BF_OPT_SMALL_BAND) {
-        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_SMALL_BAND takes 0 or 1");
-        p->small_band = value != 0;
+    if (option == BF_OPT_SMALL_BATCH) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_SMALL_BATCH takes 0 or 1");
+        p->small_batch = value != 0;
         return BF_OK;
     }
     if (option == BF_OPT_HOST_PIECES) {

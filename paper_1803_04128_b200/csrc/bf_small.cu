@@ -24,6 +24,7 @@
 // nv > 8 VPL: the warp sweeps the vectors in passes of 8 VPL (weights re-read from shared memory).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "bf_internal.h"
@@ -139,6 +140,8 @@ __device__ __forceinline__ int64_t sv_pair(int64_t j, int m, int u, int e, int L
 }
 
 template <int R, int VPL, int K, int J>
+// (9-12 warps put 3 on some SM sub-partition, whose 16K registers then cap a thread at 168 registers; the
+// launch bounds let ptxas apply that cap)
 __global__ void __launch_bounds__(32 * (SV_MAX_CONSUMERS + 1), 1)
     band_sv_kernel(const float2* __restrict__ in, float2* __restrict__ out, const SvArgs args, int LN, int l_first,
                    int nv, int64_t nsuper, int S, int C)
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_CONSUMERS + 1), 1)
                 for (int c = 0; c < 2; c++) {
                     const float2* xs = X + (c ? in1 : in0) * R * nv + vb;
                     const float2* wc = Wb + c * R * R;
-#pragma unroll
+#pragma unroll(K == 2 ? R : 2)   // K = 1: full unrolling let the compiler hoist every weight load (spills)
                     for (int sr = 0; sr < R; sr++) {
                         float2 x[VPL], w[R];
                         ld_vec<VPL>(x, xs + sr * nv);
@@ -274,14 +277,9 @@ int env_int(const char* name)
     return e ? atoi(e) : 0;
 }
 
-// vectors per lane: 2 (R x 2 register tile, passes of 16 vectors) unless nv is not a multiple of 16
-int sv_vpl(int nv)
-{
-    static const int v_env = env_int("BF_SV_VPL");   // tuning experiments
-    if (v_env == 4 && nv % 32 == 0) return 4;
-    if (v_env == 1) return 1;
-    return nv % 16 == 0 ? 2 : 1;
-}
+// vectors per lane: 2 (R x 2 register tile, passes of 16 vectors) unless nv is not a multiple of 16 (R x 4 tiles
+// measured no faster at nv = 32 and spill at r >= 12 under the 168-register cap)
+int sv_vpl(int nv) { return nv % 16 == 0 ? 2 : 1; }
 
 // Super-job size J, ring depth S and consumer warps C for one CTA per SM.  J = 2 where 6+ slots fit (fewer,
 // larger bulk copies), else J = 1.  C = min(8, J (S - 2)) rounded to a multiple of J: two slots of prefetch
@@ -355,11 +353,319 @@ cudaError_t sv_vpl_go(const Dims& d, int l_first, const float2* in, float2* out,
     return J == 2 ? sv_go<R, VV, K, 2>(d, l_first, in, out, W, nv, S, C, st, rh, rhg, po)        \
                   : sv_go<R, VV, K, 1>(d, l_first, in, out, W, nv, S, C, st, rh, rhg, po);
     switch (sv_vpl(nv)) {
-    case 4: SV_J(4)
     case 2: SV_J(2)
     default: SV_J(1)
     }
 #undef SV_J
+}
+
+// =====================================================================================================
+// Leaf stages for small vector batches (8 <= nv <= 64 / 32): the same structure as the band -- a producer warp
+// bulk-copies the weight blocks into a ring, consumer warps hold fixed R x VPL (S0) or JPL x VPL (SL)
+// register tiles and run packed FFMA2 complex MACs in the FP32 order of s0_kernel / sl_kernel (bitwise
+// equal results).
+// =====================================================================================================
+
+// cmul of bf_kernels.cu (the amplitude pre-scale b_k(x) F[x, c], same rounding)
+__device__ __forceinline__ float2 cmul_sv(const float2 a, const float2 b)
+{
+    return make_float2(fmaf(a.x, b.x, -(a.y * b.y)), fmaf(a.x, b.y, a.y * b.x));
+}
+
+__host__ __device__ constexpr int pad32(int bytes) { return bytes + ((32 - bytes % 128) % 128 + 128) % 128; }
+
+// S0 (eqn:1 P:698-702, eqn:tg P:24-28): out[p = a N/n0 + b][t][v] = sum_j V0[p](t, j) y_b[j][v],
+// y_b[j][v] = b_k(x) F[x, c], x = b n0 + j, v = c n_amp + k.
+// A job is (leaf b, group g of 4 consecutive a): the 4 blocks V0[(4g + al) N/n0 + b] (4 bulk copies, bank-
+// staggered), one job per consumer warp, lane = (al = lane / 8, vl = lane % 8) x R rows x VPL vectors.
+// Warp 1 builds y_b (double-buffered by leaf) from F and b_k with ordinary loads.
+template <int R, int VPL>
+__global__ void __launch_bounds__(32 * (SV_MAX_CONSUMERS + 2), 1)
+    s0_sv_kernel(const float2* __restrict__ F, int64_t ldf, const float2* __restrict__ ampb,
+                 const float2* __restrict__ V0, float2* __restrict__ out, int LN, int l0, int n_amp, int nv, int S,
+                 int C)
+{
+    extern __shared__ __align__(128) unsigned char sv_smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sv_smem);
+    uint64_t* empty = full + S;
+    uint64_t* yfull = empty + S;
+    uint64_t* yempty = yfull + 2;
+    const int n0 = 1 << l0, G = n0 / 4;
+    const int64_t N = int64_t(1) << LN, nleaf = N >> l0;
+    float2* Y = reinterpret_cast<float2*>(sv_smem + SV_HDR);   // [2][n0][nv]
+    unsigned char* slots = sv_smem + SV_HDR + 2 * n0 * nv * 8;
+    const int BLK = R * n0 * 8, WB = pad32(BLK), SB = (4 * WB + 127) / 128 * 128;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int q = 0; q < 2; q++) {
+            tc::mbar_init(&yfull[q], 1);
+            tc::mbar_init(&yempty[q], G);
+        }
+        tc::mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == 0) {   // ---- weight producer: job i = k G + g (k-th leaf of this CTA) -> slot i % S
+        for (int64_t i = 0;; i++) {
+            const int64_t k = i / G, b = blockIdx.x + k * gridDim.x;
+            const int g = int(i % G);
+            if (b >= nleaf) break;
+            const int s = int(i % S);
+            if (i >= S) tc::mbar_wait(&empty[s], uint32_t((i / S - 1) & 1));
+            if (lane == 0) tc::mbar_arrive_expect_tx(&full[s], uint32_t(4 * BLK));
+            __syncwarp();
+            if (lane < 4)
+                tc::bulk_g2s(slots + size_t(s) * SB + lane * WB, V0 + ((4 * g + lane) * nleaf + b) * int64_t(R) * n0,
+                             uint32_t(BLK), &full[s]);
+        }
+        return;
+    }
+    if (warp == 1) {   // ---- y builder: y_b for the k-th leaf into buffer k % 2
+        const int nrhs = nv / n_amp;
+        for (int64_t k = 0;; k++) {
+            const int64_t b = blockIdx.x + k * gridDim.x;
+            if (b >= nleaf) break;
+            const int yb = int(k & 1);
+            if (k >= 2) tc::mbar_wait(&yempty[yb], uint32_t(((k >> 1) - 1) & 1));
+            float2* Yb = Y + yb * n0 * nv;
+            for (int e = lane; e < n0 * nrhs; e += 32) {
+                const int j = e % n0, c = e / n0;
+                const int64_t x = b * n0 + j;
+                const float2 f = __ldg(F + x + c * ldf);
+                for (int kk = 0; kk < n_amp; kk++) Yb[j * nv + c * n_amp + kk] = cmul_sv(__ldg(ampb + kk * N + x), f);
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&yfull[yb]);
+        }
+        return;
+    }
+    // ---- consumers
+    const int al = lane >> 3, vl = lane & 7;
+    const int passes = nv / (8 * VPL);
+    for (int64_t i = warp - 2;; i += C) {
+        const int64_t k = i / G, b = blockIdx.x + k * gridDim.x;
+        const int g = int(i % G);
+        if (b >= nleaf) break;
+        const int yb = int(k & 1), s = int(i % S);
+        tc::mbar_wait(&yfull[yb], uint32_t((k >> 1) & 1));
+        tc::mbar_wait(&full[s], uint32_t((i / S) & 1));
+        const float2* Wb = reinterpret_cast<const float2*>(slots + size_t(s) * SB + al * WB);
+        const float2* Yb = Y + yb * n0 * nv;
+        const int64_t p = (4 * g + al) * nleaf + b;
+#pragma unroll 1
+        for (int ps = 0; ps < passes; ps++) {
+            const int vb = ps * 8 * VPL + vl * VPL;
+            unsigned long long acc[R][VPL];
+#pragma unroll
+            for (int t = 0; t < R; t++)
+#pragma unroll
+                for (int q = 0; q < VPL; q++) acc[t][q] = 0ull;
+#pragma unroll 4
+            for (int j = 0; j < n0; j++) {
+                float2 x[VPL], w[R];
+                ld_vec<VPL>(x, Yb + j * nv + vb);
+                ld_vec<R>(w, Wb + j * R);
+                unsigned long long xp[VPL], ixp[VPL];
+#pragma unroll
+                for (int q = 0; q < VPL; q++) {
+                    xp[q] = pk2(x[q].x, x[q].y);
+                    ixp[q] = pk2(-x[q].y, x[q].x);
+                }
+#pragma unroll
+                for (int t = 0; t < R; t++)
+#pragma unroll
+                    for (int q = 0; q < VPL; q++) cmac2(acc[t][q], w[t].x, w[t].y, xp[q], ixp[q]);
+            }
+            float2* o = out + p * R * int64_t(nv) + vb;
+#pragma unroll
+            for (int t = 0; t < R; t++) {
+                float2 ov[VPL];
+#pragma unroll
+                for (int q = 0; q < VPL; q++) asm("mov.b64 {%0, %1}, %2;" : "=f"(ov[q].x), "=f"(ov[q].y) : "l"(acc[t][q]));
+                st_vec<VPL>(o + t * nv, ov);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            tc::mbar_arrive(&empty[s]);
+            tc::mbar_arrive(&yempty[yb]);
+        }
+    }
+}
+
+// SL (eqn:bf3 P:791-797 + eqn:tg P:24-28): G[x, c] = sum_k a_k(x) sum_{b < n0} sum_t U[a n0 + b](j, t)
+// delta[a n0 + b](t)[c n_amp + k], x = a n0 + j.  A consumer warp owns whole T_X leaves a (the reduction over
+// b stays in registers); the producer streams each leaf's pairs in chunks of 2 (coefficients and U blocks,
+// one bulk copy each) through a ring shared by the consumers in round-robin order.  Lane = (j group q < 4,
+// v group vl < 8): rows j = 2 (4 m + q) + {0, 1} (m < n0 / 8: the 4 groups of one load are 4 consecutive
+// 16-byte chunks -- conflict-free) x VPL = nv / 8 vectors (whole RHS columns: VPL % n_amp == 0).
+constexpr int SL_SV_B = 2;   // pairs per chunk
+
+template <int R, int VPL, int NA, int N0>
+// (9-12 warps put 3 on some SM sub-partition, whose 16K registers then cap a thread at 168 registers; the
+// launch bounds let ptxas apply that cap)
+__global__ void __launch_bounds__(32 * (SV_MAX_CONSUMERS + 1), 1)
+    sl_sv_kernel(const float2* __restrict__ in, const float2* __restrict__ U, const float2* __restrict__ ampa,
+                 float2* __restrict__ G, int64_t ldg, int LN, int S, int C)
+{
+    constexpr int nv = 8 * VPL, JPL = N0 / 4, NCH = N0 / SL_SV_B;
+    constexpr int DB = SL_SV_B * R * nv * 8, UB = SL_SV_B * N0 * R * 8, SB = (DB + UB + 127) / 128 * 128;
+    extern __shared__ __align__(128) unsigned char sv_smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sv_smem);
+    uint64_t* empty = full + S;
+    unsigned char* slots = sv_smem + SV_HDR;
+    const int64_t N = int64_t(1) << LN, nleaf = N / N0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // leaves of this CTA: a = blockIdx.x + m gridDim.x, m < Lc; round r has A_r = min(C, Lc - r C) consumers
+    const int64_t Lc = (nleaf - blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == 0) {   // ---- producer: round r, chunk n, consumer w' -> ring index i
+        int64_t i = 0;
+        for (int64_t r = 0; r * C < Lc; r++) {
+            const int A = int(Lc - r * C < C ? Lc - r * C : C);
+            for (int n = 0; n < NCH; n++)
+                for (int wq = 0; wq < A; wq++, i++) {
+                    const int64_t a = blockIdx.x + (r * C + wq) * gridDim.x;
+                    const int s = int(i % S);
+                    if (i >= S) tc::mbar_wait(&empty[s], uint32_t((i / S - 1) & 1));
+                    if (lane == 0) {
+                        const int64_t p0 = a * N0 + n * SL_SV_B;
+                        tc::mbar_arrive_expect_tx(&full[s], uint32_t(DB + UB));
+                        tc::bulk_g2s(slots + size_t(s) * SB, in + p0 * R * nv, uint32_t(DB), &full[s]);
+                        tc::bulk_g2s(slots + size_t(s) * SB + DB, U + p0 * R * N0, uint32_t(UB), &full[s]);
+                    }
+                    __syncwarp();
+                }
+        }
+        return;
+    }
+    const int wq = warp - 1, q = lane >> 3, vl = lane & 7;
+    for (int64_t r = 0; r * C < Lc; r++) {
+        const int A = int(Lc - r * C < C ? Lc - r * C : C);
+        if (wq >= A) break;
+        const int64_t a = blockIdx.x + (r * C + wq) * gridDim.x;
+        unsigned long long acc[JPL][VPL];
+#pragma unroll
+        for (int jj = 0; jj < JPL; jj++)
+#pragma unroll
+            for (int v = 0; v < VPL; v++) acc[jj][v] = 0ull;
+        for (int n = 0; n < NCH; n++) {
+            const int64_t i = r * C * NCH + int64_t(n) * A + wq;
+            const int s = int(i % S);
+            tc::mbar_wait(&full[s], uint32_t((i / S) & 1));
+            const float2* D = reinterpret_cast<const float2*>(slots + size_t(s) * SB);
+            const float2* Ub = reinterpret_cast<const float2*>(slots + size_t(s) * SB + DB);
+#pragma unroll
+            for (int bb = 0; bb < SL_SV_B; bb++)
+#pragma unroll 2
+                for (int t = 0; t < R; t++) {
+                    float2 x[VPL], w[JPL];
+                    ld_vec<VPL>(x, D + (bb * R + t) * nv + vl * VPL);
+                    const float2* uc = Ub + (bb * R + t) * N0 + 2 * q;   // column t of block bb (n0 rows)
+#pragma unroll
+                    for (int m = 0; m < JPL / 2; m++) {
+                        const float4 u4 = *reinterpret_cast<const float4*>(uc + 8 * m);
+                        w[2 * m] = make_float2(u4.x, u4.y);
+                        w[2 * m + 1] = make_float2(u4.z, u4.w);
+                    }
+                    unsigned long long xp[VPL], ixp[VPL];
+#pragma unroll
+                    for (int v = 0; v < VPL; v++) {
+                        xp[v] = pk2(x[v].x, x[v].y);
+                        ixp[v] = pk2(-x[v].y, x[v].x);
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < JPL; jj++)
+#pragma unroll
+                        for (int v = 0; v < VPL; v++) cmac2(acc[jj][v], w[jj].x, w[jj].y, xp[v], ixp[v]);
+                }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&empty[s]);
+        }
+        // epilogue: g(x, c) = sum_k a_k(x) u_k(x) (cmac order of sl_kernel), c = (vl VPL) / NA + cc
+#pragma unroll
+        for (int jj = 0; jj < JPL; jj++) {
+            const int j = 2 * (4 * (jj >> 1) + q) + (jj & 1);
+            const int64_t x = a * N0 + j;
+            float2 ak[NA];
+#pragma unroll
+            for (int k = 0; k < NA; k++) ak[k] = __ldg(ampa + k * N + x);
+#pragma unroll
+            for (int cc = 0; cc < VPL / NA; cc++) {
+                float2 g = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < NA; k++) {
+                    float2 u;
+                    asm("mov.b64 {%0, %1}, %2;" : "=f"(u.x), "=f"(u.y) : "l"(acc[jj][cc * NA + k]));
+                    cmac(g, ak[k], u);
+                }
+                G[x + int64_t(vl * VPL / NA + cc) * ldg] = g;
+            }
+        }
+    }
+}
+
+template <int R, int VPL>
+cudaError_t s0_sv_go(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float2* V0, float2* out,
+                     int nv, cudaStream_t st)
+{
+    const int n0 = 1 << d.l0;
+    const int SB = (4 * pad32(R * n0 * 8) + 127) / 128 * 128;
+    const int ybytes = 2 * n0 * nv * 8;
+    int S = (SV_SMEM_LIMIT - SV_HDR - ybytes) / SB;
+    if (S < 3) return cudaErrorInvalidValue;
+    int C = S - 2 > SV_MAX_CONSUMERS ? SV_MAX_CONSUMERS : S - 2;
+    if (S > C + 4) S = C + 4;
+    const size_t shm = SV_HDR + ybytes + size_t(S) * SB;
+    auto kern = s0_sv_kernel<R, VPL>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+    if (e != cudaSuccess) return e;
+    const int64_t nleaf = d.N >> d.l0;
+    const int64_t grid = nleaf < num_sms() ? nleaf : num_sms();
+    kern<<<unsigned(grid), 32 * (C + 2), shm, st>>>(F, ldf, ampb, V0, out, d.LN, d.l0, d.n_amp, nv, S, C);
+    e = cudaGetLastError();
+    if (e != cudaSuccess && getenv("BF_DEBUG_LAUNCH")) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, kern);
+        fprintf(stderr, "s0_sv<%d,%d>: threads %d shm %zu grid %lld S %d C %d | regs %d maxthreads %d static smem %zu local %zu\n",
+                R, VPL, 32 * (C + 2), shm, (long long)grid, S, C, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+                fa.localSizeBytes);
+    }
+    return e;
+}
+
+template <int R, int VPL, int NA, int N0>
+cudaError_t sl_sv_go(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,
+                     cudaStream_t st)
+{
+    constexpr int nv = 8 * VPL;
+    constexpr int SB = (SL_SV_B * R * nv * 8 + SL_SV_B * N0 * R * 8 + 127) / 128 * 128;
+    int S = (SV_SMEM_LIMIT - SV_HDR) / SB;
+    int C = S - 2 > SV_MAX_CONSUMERS ? SV_MAX_CONSUMERS : S - 2;
+    if (C < 1) return cudaErrorInvalidValue;
+    if (S > 2 * C) S = 2 * C;
+    const size_t shm = SV_HDR + size_t(S) * SB;
+    auto kern = sl_sv_kernel<R, VPL, NA, N0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+    if (e != cudaSuccess) return e;
+    const int64_t nleaf = d.N / N0;
+    const int64_t grid = nleaf < num_sms() ? nleaf : num_sms();
+    kern<<<unsigned(grid), 32 * (C + 1), shm, st>>>(in, U, ampa, G, ldg, d.LN, S, C);
+    return cudaGetLastError();
 }
 
 }  // namespace
@@ -386,6 +692,69 @@ cudaError_t launch_band_sv(const Dims& d, int l_first, int K, const float2* in, 
     default: return cudaErrorInvalidValue;
     }
 #undef BF_SV_CASE
+}
+
+
+// S0 / SL for small vector batches: nv % 8 == 0, 8 <= nv <= 64 (S0) / 32 (SL), leaf 8..128 (S0) / 32, 64 (SL)
+bool s0_sv_supported(const Dims& d, int nv)
+{
+    const int n0 = 1 << d.l0;
+    if (!(d.R == 6 || d.R == 8 || d.R == 10 || d.R == 12 || d.R == 14 || d.R == 16)) return false;
+    if (nv < 8 || nv > 64 || nv % 8 || n0 < 8) return false;
+    const int SB = (4 * pad32(d.R * n0 * 8) + 127) / 128 * 128;
+    return (SV_SMEM_LIMIT - SV_HDR - 2 * n0 * nv * 8) / SB >= 3;
+}
+
+cudaError_t launch_s0_sv(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float2* V0,
+                         float2* out, int nv, cudaStream_t s)
+{
+    const bool v2 = nv % 16 == 0;
+#define S0SV_CASE(RR) \
+    case RR: return v2 ? s0_sv_go<RR, 2>(d, F, ldf, ampb, V0, out, nv, s) : s0_sv_go<RR, 1>(d, F, ldf, ampb, V0, out, nv, s);
+    switch (d.R) {
+        S0SV_CASE(6) S0SV_CASE(8) S0SV_CASE(10) S0SV_CASE(12) S0SV_CASE(14) S0SV_CASE(16)
+    default: return cudaErrorInvalidValue;
+    }
+#undef S0SV_CASE
+}
+
+bool sl_sv_supported(const Dims& d, int nv)
+{
+    const int n0 = 1 << d.l0;
+    if (!(d.R == 6 || d.R == 8 || d.R == 10 || d.R == 12 || d.R == 14 || d.R == 16)) return false;
+    if (!(nv == 8 || nv == 16 || nv == 32) || !(n0 == 32 || n0 == 64)) return false;
+    if (nv == 32 && n0 == 64) return false;   // 16 x 4 accumulator tile: spills under the 168-register cap
+    return (nv / 8) % d.n_amp == 0;
+}
+
+cudaError_t launch_sl_sv(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,
+                         int nv, cudaStream_t s)
+{
+    const int n0 = 1 << d.l0;
+#define SLSV_N0(RR, VV, NA)                                                                                \
+    if constexpr (VV == 4) return sl_sv_go<RR, VV, NA, 32>(d, in, U, ampa, G, ldg, s);                     \
+    else return n0 == 64 ? sl_sv_go<RR, VV, NA, 64>(d, in, U, ampa, G, ldg, s)                              \
+                         : sl_sv_go<RR, VV, NA, 32>(d, in, U, ampa, G, ldg, s);
+#define SLSV_V(RR)                                                              \
+    if (nv == 8) {                                                              \
+        SLSV_N0(RR, 1, 1)                                                       \
+    } else if (nv == 16) {                                                      \
+        if (d.n_amp == 2) { SLSV_N0(RR, 2, 2) } else { SLSV_N0(RR, 2, 1) }      \
+    } else {                                                                    \
+        if (d.n_amp == 4) { SLSV_N0(RR, 4, 4) }                                 \
+        else if (d.n_amp == 2) { SLSV_N0(RR, 4, 2) } else { SLSV_N0(RR, 4, 1) } \
+    }
+    switch (d.R) {
+    case 6: SLSV_V(6)
+    case 8: SLSV_V(8)
+    case 10: SLSV_V(10)
+    case 12: SLSV_V(12)
+    case 14: SLSV_V(14)
+    case 16: SLSV_V(16)
+    default: return cudaErrorInvalidValue;
+    }
+#undef SLSV_V
+#undef SLSV_N0
 }
 
 }  // namespace bfk

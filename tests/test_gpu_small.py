@@ -2,7 +2,7 @@
 path of cfg2 (nv = 32), cfg5 (nv = 16) and cfg4 sharded over 8 GPUs (nv = 64).
 
 Each case is checked (1) against the CPU oracle per RHS column at the north_star bar (relative l2 <= 1e-5),
-(2) bitwise against the same plan with the bands off (BF_OPT_SMALL_BAND = 0: one transfer level per launch,
+(2) bitwise against the same plan with the bands off (BF_OPT_SMALL_BATCH = 0: one transfer level per launch,
 xfer_kernel), which performs every complex MAC in the same FP32 order, and (3) for the launch count the
 plan reports (two levels per launch).
 """
@@ -51,7 +51,7 @@ SMALL = [
 
 
 @pytest.mark.parametrize("kernel,amp,LN,l0,r,nrhs,cols", SMALL)
-def test_small_band_parity(kernel, amp, LN, l0, r, nrhs, cols):
+def test_small_batch_parity(kernel, amp, LN, l0, r, nrhs, cols):
     N = 1 << LN
     F = W.rhs(N, nrhs, 600 + LN + r)
     plan = bf.Plan.build_fio(bf.fio(kernel, amp, LN, l0, r), max_nrhs_chunk=nrhs)
@@ -61,7 +61,7 @@ def test_small_band_parity(kernel, amp, LN, l0, r, nrhs, cols):
     launches = sum(info["class_launches"][k] for k in ("xfer_first_half", "xfer_switch", "xfer_second_half"))
     assert launches == (nx + 1) // 2, info["class_launches"]   # bands of 2 (unsharded: across h too)
     G = _apply(plan, F)
-    plan.set_option(bf.BF_OPT_SMALL_BAND, 0)
+    plan.set_option(bf.BF_OPT_SMALL_BATCH, 0)
     G1 = _apply(plan, F)
     plan.destroy()
     assert np.array_equal(G, G1), "small-batch band == one level per launch, bitwise"
@@ -71,7 +71,7 @@ def test_small_band_parity(kernel, amp, LN, l0, r, nrhs, cols):
     assert np.all(err <= PARITY), err
 
 
-def test_small_band_ragged_chunks_and_fallback():
+def test_small_batch_ragged_chunks_and_fallback():
     """chunks of 40 + 40 + 20 vectors (nrhs 50, chunk 20, n_amp 2): two band chunks and one chunk whose nv is not a
     multiple of 8 (per-level kernels); every column within the bar, batch-consistent with a 1-column apply."""
     k = bf.fio(W.K_FIO, W.A_CFG1, 14, 5, 10)
@@ -86,7 +86,7 @@ def test_small_band_ragged_chunks_and_fallback():
     assert np.array_equal(_apply(p1, np.asfortranarray(F[:, 20:24])), G[:, 20:24])
 
 
-def test_small_band_mutation():
+def test_small_batch_mutation():
     """A wrong block in any transfer level makes parity fail with the small-batch bands (the test can fail)."""
     LN, l0, r = 12, 4, 10
     N = 1 << LN
