@@ -40,9 +40,9 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
 def _peaks():
-    """HBM GB/s, the TF32 tensor peak (TFLOP/s) and the FP16 one with their sources.  FP16 = the measured
-    sustained cuBLAS bf16 rate (same dense rate for fp16); TF32 = that x the guide's nominal tf32/bf16
-    ratio (1.1 / 2.25): the kernels run inside a ~100 ms step under the power cap (B200_PROFILING.md)."""
+    """HBM GB/s and the TF32 tensor peak (TFLOP/s) with their sources.  TF32 = the measured sustained cuBLAS
+    bf16 rate x the guide's nominal tf32/bf16 ratio (1.1 / 2.25): the kernels run inside a ~100 ms step under
+    the power cap (B200_PROFILING.md)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
@@ -52,7 +52,7 @@ def _peaks():
     except Exception:
         hbm, src = 6650.0, "fallback"
         bf16, tsrc = 1400.0, "fallback sustained bf16 1.4 PF x 1.1/2.25"
-    return hbm, src, bf16 * 1.1 / 2.25, tsrc, bf16
+    return hbm, src, bf16 * 1.1 / 2.25, tsrc
 
 
 class ClockSampler:
@@ -215,15 +215,11 @@ def main():
                     help="bf_apply_host pipeline pieces per chunk (BF_OPT_HOST_PIECES; e2e only)")
     ap.add_argument("--no-leaf-multicast", action="store_true",
                     help="TF32 SL without the 2-CTA cluster Ux multicast (BF_OPT_LEAF_MULTICAST = 0)")
-    ap.add_argument("--band-f16", action="store_true",
-                    help="composed band in FP16 split passes (BF_OPT_BAND_F16 = 1)")
-    ap.add_argument("--leaf-f16", action="store_true",
-                    help="leaf stages in FP16 split passes instead of 3xTF32 (BF_OPT_LEAF_F16 = 1, opt-in)")
     ap.add_argument("--no-tc", action="store_true", help="every stage on the FP32 kernels (BF_OPT_TENSOR_CORES = 0)")
     ap.add_argument("--no-small-batch", action="store_true",
                     help="small vector batches: one transfer level per launch (BF_OPT_SMALL_BATCH = 0)")
-    ap.add_argument("--band-pipelines", type=int, default=None, choices=[1, 2],
-                    help="tensor-core band variant (tuning; default: the library's)")
+    ap.add_argument("--band-compose", type=int, default=None, choices=[0, 1],
+                    help="tensor-core band: composed two-level operator (1) or level by level (0) (BF_OPT_BAND_COMPOSE)")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -297,12 +293,8 @@ def main():
         plan.set_tensor_cores(False)
     if args.no_small_batch:
         plan.set_option(bf.BF_OPT_SMALL_BATCH, 0)
-    if args.band_pipelines:
-        plan.set_option(bf.BF_OPT_BAND_PIPELINES, args.band_pipelines)
-    if args.leaf_f16:
-        plan.set_option(bf.BF_OPT_LEAF_F16, 1)
-    if args.band_f16:
-        plan.set_option(bf.BF_OPT_BAND_F16, 1)
+    if args.band_compose is not None:
+        plan.set_option(bf.BF_OPT_BAND_COMPOSE, args.band_compose)
     if args.no_leaf_multicast:
         plan.set_option(bf.BF_OPT_LEAF_MULTICAST, 0)
     if args.host_pieces:
@@ -340,20 +332,19 @@ def main():
     value = w.n * w.nrhs / (ms / 1e3)   # the whole batch of w.nrhs columns per step, all ranks together
 
     # ---- roofline of the dominant kernel class ----
-    hbm, hbm_src, tf32, tf32_src, f16 = _peaks()
+    hbm, hbm_src, tf32, tf32_src = _peaks()
     wl = w.with_(log2n=w.log2n - (world.bit_length() - 1)) if args.index_shard else w   # this rank's share
     model = stage_model(wl, min(chunk, nloc) * w.n_amp, info)
     # the level-h exchange moves (G-1)/G of the local coefficients out and as much in
     model["exchange"] = (0, 2 * 8 * wl.n * w.rank * min(chunk, nloc) * w.n_amp * (world - 1) // world)
     tc_classes = set(info["tc_classes"])
-    f16_classes = set(info["f16_classes"])
 
     def tpeak(k):
-        return f16 if k in f16_classes else tf32
+        return tf32
 
     def times(k):
         """(compute seconds, hbm seconds) of one launch of class k at its peaks.  Tensor-core classes
-        issue 3 split products per FP32-accurate product (3xTF32, or 3 FP16 passes at the fp16 rate)."""
+        issue 3 split products per FP32-accurate product (3xTF32)."""
         f, b = model[k]
         tcomp = 3 * f / (tpeak(k) * 1e12) if k in tc_classes else f / (FP32_PEAK_TFLOPS * 1e12)
         return tcomp, b / (hbm * 1e9)
@@ -367,9 +358,8 @@ def main():
         roof = {"bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm, "unit": "GB/s",
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
     elif dom in tc_classes:
-        fp16 = dom in f16_classes
         roof = {"bound": "tensor", "achieved": 3 * flops / avg_s / 1e12, "peak": tpeak(dom), "unit": "TFLOP/s",
-                "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (fp16 dense rate = bf16)" if fp16 else tf32_src)
+                "peak_source": tf32_src
                 + "; achieved counts the 3 split passes of each algorithmic FP32 flop"}
     else:
         roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -417,7 +407,7 @@ def main():
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": ("c64: tcgen05 split products with FP32 accumulation (" +
-                      ", ".join(f"{k} {'3xFP16' if k in f16_classes else '3xTF32'}" for k in sorted(tc_classes)) + ")")
+                      ", ".join(f"{k} 3xTF32" for k in sorted(tc_classes)) + ")")
                      if tc_classes else "c64 (fp32 FFMA)",
             "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel; factors from the host builder)",
             "config": {"workload": args.config, "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,

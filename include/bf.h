@@ -120,9 +120,7 @@ typedef struct {
     int64_t rows_local;          /* rows of F and G bf_apply expects: N, or N/world for BF_SHARD_NCCL */
     int64_t tc_weight_bytes;     /* device bytes of the tensor-core leaf weight images (0 if not built) */
     int32_t tc_class_mask;       /* bit c set: kernel class c (bf_plan_timing numbering) runs on the tensor
-                                    cores for a full chunk of max_nrhs_chunk columns */
-    int32_t f16_class_mask;      /* subset of tc_class_mask whose split products are kind::f16 MMAs
-                                    (BF_OPT_LEAF_F16); the others are kind::tf32 */
+                                    cores (3xTF32) for a full chunk of max_nrhs_chunk columns */
 } bf_plan_info_t;
 
 /* index sharding modes */
@@ -190,14 +188,6 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        0: every stage runs the FP32 FFMA (SIMT) kernels.
  * Returns BF_ERR_INVALID_ARG for an unknown option or value. */
 #define BF_OPT_TENSOR_CORES 1
-/*   BF_OPT_BAND_PIPELINES 1 (default): the level-by-level tensor-core band kernel (BF_OPT_BAND_COMPOSE = 0)
- *                        runs one job at a time per SM;
- *                        2: jobs alternate between two TMEM pipelines where TMEM allows (r <= 10; measured
- *                        slower at cfg4). */
-#define BF_OPT_BAND_PIPELINES 2
-/*   BF_OPT_BAND_TRACE_J0 (diagnostic): enables the band timeline trace of bf_debug_band_trace for CTA
- *                        value >> 16, jobs from value & 65535 (off by default). */
-#define BF_OPT_BAND_TRACE_J0 3
 /*   BF_OPT_EXCHANGE (index-sharded plans): 0 (default) = the level-h exchange is a separate step (NCCL
  *                        grouped send/recv, or device copies between emulated shards); 1 = fused exchange:
  *                        the launch that produces level h stores each output pair directly into its
@@ -210,19 +200,8 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
 /*   BF_OPT_BAND_COMPOSE  1 (default): the tensor-core band applies its two transfer levels as one composed
  *                        4 x 4 block operator per group of 4 pairs (C = W_{l+1} W_l per block path, formed
  *                        in FP32 on chip; same MAC count, one accumulation chain per tile);
- *                        0: the level-by-level band kernels (selected by BF_OPT_BAND_PIPELINES). */
+ *                        0: the level-by-level band kernel (band_tc_kernel). */
 #define BF_OPT_BAND_COMPOSE 5
-/*   BF_OPT_LEAF_F16      0 (default): the tensor-core leaf stages S0 / SL in 3xTF32.  1 (opt-in): they split
- *                        their operands into FP16 hi + lo after power-of-two scaling of every operand row to
- *                        max |x| in [0.5, 1) and run the 3 split products as kind::f16 MMAs (twice the
- *                        kind::tf32 rate, same 11-bit hi parts, measured error no larger; DESIGN.md 5 and
- *                        reading R17); the weight images are half the bytes.  Switching after creation
- *                        rebuilds the leaf images (synchronous). */
-#define BF_OPT_LEAF_F16 6
-/*   BF_OPT_BAND_F16      0 (default) / 1: the composed tensor-core band in FP16 split passes (per-vector and
- *                        per-group power-of-two scaling, kind::f16 MMAs) instead of 3xTF32 (measured slower
- *                        in the power-capped step). */
-#define BF_OPT_BAND_F16 7
 /*   BF_OPT_HOST_PIECES   2 (default), 1..16: bf_apply_host splits each chunk into this many equal pieces whose
  *                        host<->device copies overlap the apply of the neighbouring pieces; 3 = tapered
  *                        pieces of 1/4, 1/2, 1/4 of a chunk (measured at cfg4: 2 pieces 137.5 ms, tapered
@@ -242,11 +221,6 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        (bitwise equal). */
 #define BF_OPT_SMALL_BATCH 10
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
-
-/* Diagnostic (performance work only): copies the SM-clock timeline that the last tensor-core band
- * launch on the current device recorded for CTA 0 -- its first 64 jobs x 12 event slots (clock64
- * values; 0 = not recorded) -- into out[0 .. n).  Synchronous. */
-bf_status_t bf_debug_band_trace(int64_t *out, int32_t n);
 
 /* Wait for the plan's outstanding work (the last bf_apply enqueued outside a CUDA-graph capture; replays of a
  * graph that captured bf_apply must be synchronized by the caller), then free everything it owns.

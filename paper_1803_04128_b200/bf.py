@@ -24,12 +24,8 @@ BF_NUM_KCLASS = 6
 KCLASS_NAMES = ("s0", "xfer_first_half", "xfer_switch", "xfer_second_half", "sl", "exchange")
 BF_SHARD_NONE, BF_SHARD_NCCL, BF_SHARD_EMULATED = 0, 1, 2
 BF_OPT_TENSOR_CORES = 1
-BF_OPT_BAND_PIPELINES = 2
-BF_OPT_BAND_TRACE_J0 = 3
 BF_OPT_EXCHANGE = 4
 BF_OPT_BAND_COMPOSE = 5
-BF_OPT_LEAF_F16 = 6
-BF_OPT_BAND_F16 = 7
 BF_OPT_HOST_PIECES = 8
 BF_OPT_LEAF_MULTICAST = 9
 BF_OPT_SMALL_BATCH = 10
@@ -38,7 +34,7 @@ STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALI
 
 # every symbol include/*.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finalize", "bf_apply", "bf_apply_ex",
-           "bf_apply_host", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing", "bf_plan_set_option", "bf_debug_band_trace",
+           "bf_apply_host", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing", "bf_plan_set_option",
            "bf_plan_destroy", "bf_last_error", "bf_abi_version", "bf_build_n_amp", "bf_build_amp", "bf_build_blocks",
            "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
            "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated")
@@ -65,7 +61,7 @@ class bf_plan_info_t(ctypes.Structure):
                 ("device", ctypes.c_int32), ("class_launches", ctypes.c_int32 * 6),
                 ("class_levels", ctypes.c_int32 * 6), ("world", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
                 ("sharding", ctypes.c_int32), ("rows_local", ctypes.c_int64), ("tc_weight_bytes", ctypes.c_int64),
-                ("tc_class_mask", ctypes.c_int32), ("f16_class_mask", ctypes.c_int32)]
+                ("tc_class_mask", ctypes.c_int32)]
 
 
 class bf_fio_t(ctypes.Structure):
@@ -110,7 +106,6 @@ def lib():
             "bf_plan_get_info": ([vp, P(bf_plan_info_t)], i32),
             "bf_plan_set_timing": ([vp, i32], i32),
             "bf_plan_set_option": ([vp, i32, ctypes.c_int64], i32),
-            "bf_debug_band_trace": ([vp, i32], i32),
             "bf_plan_timing": ([vp, P(ctypes.c_double), P(i64)], i32),
             "bf_plan_destroy": ([vp], i32),
             "bf_last_error": ([], ctypes.c_char_p),
@@ -171,13 +166,6 @@ def build_blocks(k: bf_fio_t, stage: int, begin: int, count: int) -> np.ndarray:
     out = np.zeros((count, e), np.complex64)
     _check(lib().bf_build_blocks(ctypes.byref(k), stage, begin, count, out.ctypes.data))
     return out
-
-
-def debug_band_trace() -> np.ndarray:
-    """SM-clock timeline of the last tensor-core band launch (CTA 0): [64 jobs, 12 events] int64."""
-    out = np.zeros(64 * 12, np.int64)
-    _check(lib().bf_debug_band_trace(out.ctypes.data_as(ctypes.c_void_p), out.size))
-    return out.reshape(64, 12)
 
 
 def nccl_unique_id() -> bytes:
@@ -277,7 +265,6 @@ class Plan:
         out["class_launches"] = dict(zip(KCLASS_NAMES, list(i.class_launches)))
         out["class_levels"] = dict(zip(KCLASS_NAMES, list(i.class_levels)))
         out["tc_classes"] = [n for c, n in enumerate(KCLASS_NAMES) if i.tc_class_mask >> c & 1]
-        out["f16_classes"] = [n for c, n in enumerate(KCLASS_NAMES) if i.f16_class_mask >> c & 1]
         return out
 
     def workspace_bytes(self, nrhs_chunk: int) -> int:

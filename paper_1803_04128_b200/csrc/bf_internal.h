@@ -31,17 +31,6 @@ int64_t leafx_floats(const Dims& d);
 cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U, float* V0x, float* Ux, cudaStream_t s);
 // S0 on the tensor cores: same contract as launch_s0, weights from V0x.
 bool s0_tc_supported(const Dims& d, int nv, int64_t ldf);
-// S0 with FP16 split passes (bf_tc.cu): image of leafx_floats(d) halves + leafh_rows(d) biased row exponents
-int64_t leafh_rows(const Dims& d);
-cudaError_t expand_s0_h16(const Dims& d, const float2* V0, void* V0h, void* V0e, cudaStream_t s);
-cudaError_t launch_s0_h16(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const void* V0h,
-                          const void* V0e, float2* out, int nv, cudaStream_t s);
-// SL with FP16 split passes: image of leafx_floats(d) halves + leafu_rows(d) biased exponents
-int64_t leafu_rows(const Dims& d);
-bool sl_h16_shape(const Dims& d);   // the FP16 SL fits this shape (else the 3xTF32 SL)
-cudaError_t expand_sl_h16(const Dims& d, const float2* U, void* Uh, void* Ue, cudaStream_t s);
-cudaError_t launch_sl_h16(const Dims& d, const float2* in, const void* Uh, const void* Ue, const float2* ampa,
-                          float2* G, int64_t ldg, int nv, cudaStream_t s);
 cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x, float2* out,
                          int nv, cudaStream_t s,
                          bool multicast = true);
@@ -81,18 +70,13 @@ cudaError_t launch_sl_sv(const Dims& d, const float2* in, const float2* U, const
 
 // Band of 2 transfer levels on the tensor cores (bf_tc.cu): same contract as launch_band with K = 2.
 bool band_tc_supported(const Dims& d, int nv);
-// which tensor-core band kernel runs (per plan: BF_OPT_BAND_COMPOSE, BF_OPT_BAND_F16, BF_OPT_BAND_PIPELINES)
+// which tensor-core band kernel runs (per plan: BF_OPT_BAND_COMPOSE)
 struct BandVariant {
-    bool compose = true;         // the composed two-level operator (band_cmp_kernel / band_h16_kernel)
-    bool f16 = false;            // composed band in FP16 split passes
-    bool two_pipelines = false;  // level-by-level band with two TMEM pipelines (r <= 10)
+    bool compose = true;         // the composed two-level operator (band_cmp_kernel); else band_tc_kernel
 };
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
                            cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, const BandVariant& bv);
 
-// Diagnostic: SM-clock timeline of the last band_tc launch (CTA 0, first 64 jobs x 12 events).
-cudaError_t band_trace(long long* out, int n);
-void band_trace_window(int j0);
 
 // Plan finalization: W[p] <- Sw[p] W[p] for npairs blocks (W column-major R x cols, Sw R x R).
 cudaError_t launch_fold_switch(const float2* Sw, float2* W, int64_t npairs, int R, int cols, cudaStream_t s);

@@ -130,10 +130,6 @@ struct Shard {
     std::vector<float2*> xfer;
     float* v0x = nullptr;      // tensor-core image of V0 / U (bf_tc.cu), built at finalize when used
     float* ux = nullptr;
-    void* v0h = nullptr;       // FP16 S0 image (BF_OPT_LEAF_F16), instead of v0x, and its row scales
-    void* v0s = nullptr;       // biased exponents (one byte per complex output row) of the FP16 image
-    void* uh = nullptr;        // FP16 SL image (BF_OPT_LEAF_F16, shapes where it fits), instead of ux
-    void* ue = nullptr;
     float2* ws = nullptr;      // two coefficient arrays of (N/G) R nv_max
 };
 
@@ -160,8 +156,7 @@ struct bf_plan_s {
     int64_t staging_elems = 0;   // complex elements of dF / dG each
     cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the pipelined bf_apply_host
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
-    bfk::BandVariant band;     // BF_OPT_BAND_COMPOSE / BF_OPT_BAND_F16 / BF_OPT_BAND_PIPELINES
-    bool leaf_f16 = false;     // BF_OPT_LEAF_F16 (opt-in: the north_star names 3xTF32 or FP64)
+    bfk::BandVariant band;     // BF_OPT_BAND_COMPOSE
     int host_pieces = 2;       // BF_OPT_HOST_PIECES: bf_apply_host pipeline pieces per chunk
     bool leaf_multicast = true;  // BF_OPT_LEAF_MULTICAST: TF32 S0 / SL as 2-CTA clusters sharing the weight stream
     bool small_batch = true;      // BF_OPT_SMALL_BATCH: fused bands for small vector batches (bf_small.cu)
@@ -281,10 +276,6 @@ void free_plan(bf_plan_s* p)
         cudaFree(s.sw);
         cudaFree(s.v0x);
         cudaFree(s.ux);
-        cudaFree(s.v0h);
-        cudaFree(s.v0s);
-        cudaFree(s.uh);
-        cudaFree(s.ue);
         cudaFree(s.u);
         for (auto x : s.xfer) cudaFree(x);
         cudaFree(s.ws);
@@ -432,8 +423,6 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
         cudaError_t e = timed(p, stp.cls, s, [&]() -> cudaError_t {
             switch (stp.kind) {
             case Step::S0:
-                if (p->tensor_cores && sh.v0h && bfk::s0_tc_supported(dl, nv, ldf))
-                    return bfk::launch_s0_h16(dl, F, ldf, sh.amp_b, sh.v0h, sh.v0s, in, nv, s);
                 if (p->tensor_cores && sh.v0x && bfk::s0_tc_supported(dl, nv, ldf))
                     return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s, p->leaf_multicast);
                 if (p->small_batch && nv < 64 && bfk::s0_sv_supported(dl, nv))
@@ -451,8 +440,6 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                 return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
             }
             case Step::SL:
-                if (p->tensor_cores && sh.uh && bfk::sl_tc_supported(dl, nv))
-                    return bfk::launch_sl_h16(dl, in, sh.uh, sh.ue, sh.amp_a, G, ldg, nv, s);
                 if (p->tensor_cores && sh.ux && bfk::sl_tc_supported(dl, nv))
                     return bfk::launch_sl_tc(dl, in, sh.ux, sh.amp_a, G, ldg, nv, s, p->leaf_multicast);
                 if (p->small_batch && bfk::sl_sv_supported(dl, nv))
@@ -763,48 +750,22 @@ bf_status_t bf_plan_upload(bf_plan_t p, int32_t stage, int64_t block_begin, int6
 }
 
 namespace {
-// The tensor-core leaf images in the format BF_OPT_LEAF_F16 selects (the other format is freed): FP16
-// hi/lo tiles + per-row exponents (s0_h16_kernel, sl_h16_kernel where the shape fits), or TF32 hi/lo
-// tiles (s0_tc_kernel, sl_tc_kernel).  Without memory for an image the SIMT kernel serves that stage.
+// The tensor-core leaf images (s0_tc_kernel, sl_tc_kernel): TF32 hi/lo tiles, real-embedded.  Without memory
+// for an image the SIMT kernel serves that stage.
 bf_status_t build_leaf_images(bf_plan_s* p, Shard& s)
 {
     const bfk::Dims dl = p->local();
-    void** all[] = {reinterpret_cast<void**>(&s.v0x), &s.v0h, &s.v0s, reinterpret_cast<void**>(&s.ux), &s.uh, &s.ue};
-    for (void** x : all) {
-        cudaFree(*x);
-        *x = nullptr;
-    }
     const size_t lx = size_t(bfk::leafx_floats(dl));
-    auto alloc = [](void** x, size_t bytes) {
+    auto alloc = [](float** x, size_t bytes) {
         if (cudaMalloc(x, bytes) == cudaSuccess) return true;
         cudaGetLastError();
         *x = nullptr;
         return false;
     };
     cudaError_t e = cudaSuccess;
-    if (p->leaf_f16) {
-        if (alloc(&s.v0h, lx * 2) && alloc(&s.v0s, size_t(bfk::leafh_rows(dl))))
-            e = bfk::expand_s0_h16(dl, s.v0, s.v0h, s.v0s, 0);
-        else {
-            cudaFree(s.v0h);
-            s.v0h = nullptr;
-        }
-        if (e == cudaSuccess && bfk::sl_h16_shape(dl)) {
-            if (alloc(&s.uh, lx * 2) && alloc(&s.ue, size_t(bfk::leafu_rows(dl))))
-                e = bfk::expand_sl_h16(dl, s.u, s.uh, s.ue, 0);
-            else {
-                cudaFree(s.uh);
-                s.uh = nullptr;
-            }
-        } else if (e == cudaSuccess && alloc(reinterpret_cast<void**>(&s.ux), lx * sizeof(float))) {
-            e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
-        }
-    } else {
-        if (alloc(reinterpret_cast<void**>(&s.v0x), lx * sizeof(float)))
-            e = bfk::expand_leaf_weights(dl, s.v0, s.u, s.v0x, nullptr, 0);
-        if (e == cudaSuccess && alloc(reinterpret_cast<void**>(&s.ux), lx * sizeof(float)))
-            e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
-    }
+    if (!s.v0x && alloc(&s.v0x, lx * sizeof(float))) e = bfk::expand_leaf_weights(dl, s.v0, s.u, s.v0x, nullptr, 0);
+    if (e == cudaSuccess && !s.ux && alloc(&s.ux, lx * sizeof(float)))
+        e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
     return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf weight images");
 }
 }  // namespace
@@ -1058,24 +1019,18 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
         const int64_t lx = bfk::leafx_floats(p->local());
         if (s.v0x) info->tc_weight_bytes += lx * int64_t(sizeof(float));
         if (s.ux) info->tc_weight_bytes += lx * int64_t(sizeof(float));
-        if (s.v0h) info->tc_weight_bytes += lx * 2 + bfk::leafh_rows(p->local());
-        if (s.uh) info->tc_weight_bytes += lx * 2 + bfk::leafu_rows(p->local());
     }
     {
         const bfk::Dims dl = p->local();
         const int nvf = int(p->max_chunk * p->d.n_amp);
         int mask = 0;
-        if (p->tensor_cores && (p->sh[0].v0x || p->sh[0].v0h) && bfk::s0_tc_supported(dl, nvf, dl.N))
+        if (p->tensor_cores && p->sh[0].v0x && bfk::s0_tc_supported(dl, nvf, dl.N))
             mask |= 1 << bfk::KC_S0;
-        if (p->tensor_cores && (p->sh[0].ux || p->sh[0].uh) && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
+        if (p->tensor_cores && p->sh[0].ux && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
         if (p->tensor_cores && bfk::band_tc_supported(dl, nvf))
             for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE, p->small_batch))
                 if (stp.kind == Step::BAND && stp.K == 2) mask |= 1 << stp.cls;
         info->tc_class_mask = mask;
-        int fmask = 0;
-        if ((mask >> bfk::KC_S0 & 1) && p->sh[0].v0h) fmask |= 1 << bfk::KC_S0;
-        if ((mask >> bfk::KC_SL & 1) && p->sh[0].uh) fmask |= 1 << bfk::KC_SL;
-        info->f16_class_mask = fmask;
     }
     const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp), p->mode != BF_SHARD_NONE, p->small_batch);
     info->launches_per_chunk = 0;
@@ -1092,13 +1047,6 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     info->sharding = p->mode;
     info->rows_local = (p->mode == BF_SHARD_NCCL) ? n : p->d.N;
     return BF_OK;
-}
-
-bf_status_t bf_debug_band_trace(int64_t* out, int32_t n)
-{
-    if (!out || n < 0) return fail(BF_ERR_INVALID_ARG, "bad argument");
-    cudaError_t e = bfk::band_trace(reinterpret_cast<long long*>(out), n);
-    return e == cudaSuccess ? BF_OK : cuda_fail(e, "band trace");
 }
 
 namespace {
@@ -1177,20 +1125,6 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
         p->exchange_peer = value != 0;
         return BF_OK;
     }
-    if (option == BF_OPT_LEAF_F16) {
-        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_LEAF_F16 takes 0 or 1");
-        if (p->leaf_f16 == (value != 0)) return BF_OK;
-        p->leaf_f16 = value != 0;
-        if (!p->finalized) return BF_OK;
-        DeviceGuard g(p->device);
-        cudaError_t e = cudaDeviceSynchronize();   // no apply may still read the old image
-        if (e != cudaSuccess) return cuda_fail(e, "leaf image switch");
-        for (Shard& s : p->sh)
-            if (s.v0x || s.v0h || s.ux || s.uh)
-                if (bf_status_t st = build_leaf_images(p, s); st != BF_OK) return st;
-        e = cudaDeviceSynchronize();
-        return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf image switch");
-    }
     if (option == BF_OPT_LEAF_MULTICAST) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_LEAF_MULTICAST takes 0 or 1");
         p->leaf_multicast = value != 0;
@@ -1206,23 +1140,9 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
         p->host_pieces = int(value);
         return BF_OK;
     }
-    if (option == BF_OPT_BAND_F16) {
-        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_F16 takes 0 or 1");
-        p->band.f16 = value != 0;
-        return BF_OK;
-    }
     if (option == BF_OPT_BAND_COMPOSE) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_COMPOSE takes 0 or 1");
         p->band.compose = value != 0;
-        return BF_OK;
-    }
-    if (option == BF_OPT_BAND_TRACE_J0) {
-        bfk::band_trace_window(int(value));
-        return BF_OK;
-    }
-    if (option == BF_OPT_BAND_PIPELINES) {
-        if (value != 1 && value != 2) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_PIPELINES takes 1 or 2");
-        p->band.two_pipelines = value == 2;
         return BF_OK;
     }
     return fail(BF_ERR_INVALID_ARG, "unknown plan option");

@@ -496,357 +496,6 @@ cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const floa
 
 
 // =============================================================================================
-// S0 in FP16 passes (BF_OPT_LEAF_F16 = 1, the default).  Same job structure as s0_tc_kernel, but every
-// operand is split into FP16 hi + lo after a power-of-two scaling that brings each A row (one vector's
-// b_k F values of the leaf) and each B row (one output coefficient's V0 row) to max |x| in [0.5, 1):
-// hi = fp16(x), lo = fp16(x - hi), and D = Ahi Bhi + Alo Bhi + Ahi Blo accumulates in FP32 with
-// kind::f16 MMAs (K = 16 per instruction: twice the MAC rate of kind::tf32, tools/tc_probe_f16.cu).
-// The hi parts carry 11 significant bits like TF32, and the scaling keeps every value of interest in
-// FP16's normal range, so the product error matches the 3xTF32 split (measured model in the probe);
-// values below 2^-14 of their row's maximum go subnormal with an absolute error <= 2^-25 of that
-// maximum.  The epilogue multiplies by 2^{e_v} 2^{f_n}.  The weight image is half the bytes of the TF32
-// image (plus one FP32 scale per row).
-// =============================================================================================
-constexpr uint32_t S0H_TILE = uint32_t(S0X_NC) * S0X_KC * 2;   // one 128 x 32 FP16 tile (8 KB)
-
-int64_t leafh_rows(const Dims& d) { return d.N * int64_t(d.R); }   // biased exponents, one per complex output row
-
-__global__ void expand_s0_h16_kernel(const float2* __restrict__ V0, __half* __restrict__ X, uint8_t* __restrict__ S,
-                                     int LN, int l0, int R)
-{
-    const int n0 = 1 << l0;
-    const int64_t nleaf = (int64_t(1) << LN) >> l0;
-    const int rows = n0 * 2 * R, K = 2 * n0, cq = n0 * R;
-    const int nch = rows / S0X_NC, kch = K / S0X_KC;
-    const int64_t total = nleaf * cq;
-    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t b = g / cq;
-        const int q = int(g - b * cq);                 // complex output row q = a R + t: real rows 2q, 2q + 1
-        const int a = q / R, t = q - a * R;
-        const float2* w = V0 + (int64_t(a) * nleaf + b) * (n0 * R) + t;   // w[j R]
-        float mx = 0.f;
-        for (int j = 0; j < n0; j++) mx = fmaxf(mx, fmaxf(fabsf(w[j * R].x), fabsf(w[j * R].y)));
-        int e = 0;
-        frexpf(mx, &e);                                // mx 2^-e in [0.5, 1)
-        e = max(-126, min(126, e));
-        S[b * cq + q] = uint8_t(e + 127);              // biased: the epilogue multiplies by 2^e
-        for (int cp = 0; cp < 2; cp++) {
-            const int n = 2 * q + cp, nc = n / S0X_NC;
-            for (int k = 0; k < K; k++) {
-                const float x = ldexpf(embed(w[(k >> 1) * R], cp, k & 1), -e);
-                float hi, lo;
-                tc::split_h(x, hi, lo);
-                const int kc = k / S0X_KC;
-                __half* tile = X + ((b * nch + nc) * kch + kc) * 2 * int64_t(S0X_NC * S0X_KC);
-                const uint32_t off = tc::kmaj_off16(n % S0X_NC, k % S0X_KC, S0X_NC) / 2;
-                tile[off] = __float2half_rn(hi);
-                tile[S0X_NC * S0X_KC + off] = __float2half_rn(lo);
-            }
-        }
-    }
-}
-
-template <int R, int N0>
-struct S0H {
-    static constexpr int K = 2 * N0;
-    static constexpr int KS = K / S0X_KC;
-    static constexpr int NCH = N0 * 2 * R / S0X_NC;
-    static constexpr int NSTAGE = 2 * KS;                  // weight ring depth (16 KB stages)
-    static constexpr uint32_t STAGE = 2 * S0H_TILE;        // hi + lo
-    static constexpr int FS = N0 + 2;                      // padded staging rows (16-byte aligned, bank spread)
-    static constexpr uint32_t FBYTES = 128u * FS * 8;
-    static constexpr uint32_t OFF_F = NSTAGE * STAGE, OFF_BK = OFF_F + FBYTES, OFF_E = OFF_BK + 4 * N0 * 8;
-    static constexpr size_t SMEM = size_t(OFF_E) + 4 * 128 * 4;
-    static constexpr int A_COLS = K / 2;                   // packed FP16 pairs: hi at +0, lo at +A_COLS
-    static constexpr int A_BUF = 2 * A_COLS;               // two A buffers (the split fills job j + 1 while
-    static constexpr int D_OFF = 2 * A_BUF;                //   the tensor pipe runs job j)
-    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * S0X_NC>();
-    static_assert((N0 * 2 * R) % S0X_NC == 0 && KS >= 2, "tiling");
-    static_assert(SMEM <= 232448 - 1024 && D_OFF + 2 * S0X_NC <= 512, "budget");
-};
-
-template <int R, int N0>
-__global__ void __launch_bounds__(448, 1)
-    s0_h16_kernel(const float2* __restrict__ F, int64_t ldf, const float2* __restrict__ ampb,
-                  const __half* __restrict__ V0h, const uint8_t* __restrict__ V0s, float2* __restrict__ out, int LN,
-                  int n_amp, int nv, int nvt)
-{
-    using C = S0H<R, N0>;
-    extern __shared__ __align__(128) uint8_t sm_s0h[];
-    uint8_t* ring = sm_s0h;
-    float2* Fs = reinterpret_cast<float2*>(sm_s0h + C::OFF_F);    // [column][FS]
-    float2* Bk = reinterpret_cast<float2*>(sm_s0h + C::OFF_BK);   // [k][N0] b_k(x)
-    float* Es = reinterpret_cast<float*>(sm_s0h + C::OFF_E);       // [job % 4][128] 2^{e_v}
-    __shared__ uint64_t full[C::NSTAGE], empty[C::NSTAGE], dfull[2], dempty[2], f_full, f_empty, a_full[2], a_free[2];
-    __shared__ uint64_t e_full[4], e_empty[4];
-    __shared__ uint32_t tmem_base;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t N = int64_t(1) << LN;
-    const int64_t nleaf = N / N0;
-    const int64_t njobs_all = nleaf * nvt;
-    const int64_t njobs = (njobs_all - blockIdx.x + gridDim.x - 1) / gridDim.x;
-
-    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
-    if (tid == 0) {
-        for (int i = 0; i < C::NSTAGE; i++) {
-            tc::mbar_init(&full[i], 1);
-            tc::mbar_init(&empty[i], 1);
-        }
-        for (int i = 0; i < 2; i++) {
-            tc::mbar_init(&dfull[i], 1);
-            tc::mbar_init(&dempty[i], 256);
-        }
-        for (int i = 0; i < 4; i++) {
-            tc::mbar_init(&e_full[i], 128);
-            tc::mbar_init(&e_empty[i], 256);
-        }
-        tc::mbar_init(&f_full, 1);
-        tc::mbar_init(&f_empty, 128);
-        for (int i = 0; i < 2; i++) {
-            tc::mbar_init(&a_full[i], 128);
-            tc::mbar_init(&a_free[i], 1);
-        }
-        tc::mbar_fence_init();
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = tmem_base;
-
-    if (warp == 4) {
-        // ---- loader: per job the F staging tile, and the weight ring (all jobs, in order).  The next job's F
-        //      tile is issued a few weight tiles into the current job (as soon as the split has released the
-        //      staging tile), so its latency hides behind the current job's MMAs ----
-        if (lane == 0) {
-            auto issue_f = [&](int64_t jl) {
-                const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
-                const int64_t b = job / unsigned(nvt);
-                const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
-                const int c0 = v0 / n_amp, cw = (vw + n_amp - 1) / n_amp;
-                if (jl > 0) tc::mbar_wait(&f_empty, uint32_t(jl - 1) & 1);
-                tc::mbar_arrive_expect_tx(&f_full, uint32_t(cw) * N0 * 8 + uint32_t(n_amp) * N0 * 8);
-                for (int cl = 0; cl < cw; cl++)
-                    tc::bulk_g2s(Fs + cl * C::FS, F + b * N0 + int64_t(c0 + cl) * ldf, N0 * 8, &f_full);
-                for (int k = 0; k < n_amp; k++) tc::bulk_g2s(Bk + k * N0, ampb + k * N + b * N0, N0 * 8, &f_full);
-            };
-            constexpr int WPJ = C::NCH * C::KS;                       // weight tiles per job
-            constexpr int F_AT = C::NSTAGE < WPJ - 1 ? C::NSTAGE : WPJ - 1;
-            if (njobs > 0) issue_f(0);
-            int64_t it = 0;
-            for (int64_t jl = 0; jl < njobs; jl++) {
-                const int64_t b = unsigned(blockIdx.x + jl * gridDim.x) / unsigned(nvt);
-                for (int w = 0; w < WPJ; w++, it++) {
-                    const int st = int(it % C::NSTAGE);
-                    if (it >= C::NSTAGE) tc::mbar_wait(&empty[st], uint32_t(it / C::NSTAGE - 1) & 1);
-                    tc::mbar_arrive_expect_tx(&full[st], C::STAGE);
-                    tc::bulk_g2s(ring + st * C::STAGE, V0h + (b * WPJ + w) * 2 * (S0X_NC * S0X_KC), C::STAGE, &full[st]);
-                    if (w == F_AT && jl + 1 < njobs) issue_f(jl + 1);
-                }
-            }
-        }
-    } else if (warp < 4) {
-        // ---- A = Y^T scaled by 2^{-e_v}, FP16 hi / lo packed into TMEM; thread = vector ----
-        const int v = tid;
-        const uint32_t lb = uint32_t(warp * 32) << 16;
-        for (int64_t jl = 0; jl < njobs; jl++) {
-            const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
-            const int v0 = int(job % unsigned(nvt)) * 128, vg = v0 + v;
-            const int c0 = v0 / n_amp;
-            const int eb = int(jl & 3), ab = int(jl & 1);
-            tc::mbar_wait(&f_full, uint32_t(jl & 1));
-            if (jl >= 2) tc::mbar_wait(&a_free[ab], uint32_t((jl >> 1) - 1) & 1);
-            if (jl >= 4) tc::mbar_wait(&e_empty[eb], uint32_t((jl >> 2) - 1) & 1);
-            tc::fence_after_sync();
-            const bool ok = vg < nv;
-            const int cl = ok ? vg / n_amp - c0 : 0, k = ok ? vg % n_amp : 0;
-            const float2* fc = Fs + cl * C::FS;
-            const float2* bk = Bk + k * N0;
-            float mx = 0.f;
-#pragma unroll 4
-            for (int j = 0; j < N0; j += 2) {
-                const float4 f = *reinterpret_cast<const float4*>(fc + j);
-                const float4 a = *reinterpret_cast<const float4*>(bk + j);
-                const float2 y0 = cmul_tc(make_float2(a.x, a.y), make_float2(f.x, f.y));
-                const float2 y1 = cmul_tc(make_float2(a.z, a.w), make_float2(f.z, f.w));
-                mx = fmaxf(mx, fmaxf(fmaxf(fabsf(y0.x), fabsf(y0.y)), fmaxf(fabsf(y1.x), fabsf(y1.y))));
-            }
-            int e = 0;
-            frexpf(ok ? mx : 0.f, &e);
-            e = max(-126, min(126, e));
-            const float sc = ldexpf(1.f, -e);
-            Es[eb * 128 + v] = ldexpf(1.f, e);
-            tc::mbar_arrive(&e_full[eb]);
-#pragma unroll 1
-            for (int j0 = 0; j0 < N0; j0 += 8) {
-                float hi[8], lo[8];
-#pragma unroll
-                for (int jj = 0; jj < 8; jj += 2) {
-                    const float4 f = *reinterpret_cast<const float4*>(fc + j0 + jj);
-                    const float4 a = *reinterpret_cast<const float4*>(bk + j0 + jj);
-                    float2 y[2] = {cmul_tc(make_float2(a.x, a.y), make_float2(f.x, f.y)),
-                                   cmul_tc(make_float2(a.z, a.w), make_float2(f.z, f.w))};
-#pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        if (!ok) y[h] = make_float2(0.f, 0.f);
-                        // column j = (re, im) of complex j: K index 2j, 2j + 1
-                        tc::split_h2(y[h].x * sc, y[h].y * sc, hi[jj + h], lo[jj + h]);
-                    }
-                }
-                tc::tmem_st8(tmem + lb + uint32_t(ab * C::A_BUF + j0), hi);
-                tc::tmem_st8(tmem + lb + uint32_t(ab * C::A_BUF + C::A_COLS + j0), lo);
-            }
-            tc::fence_before_sync();
-            tc::mbar_arrive(&f_empty);
-            tc::tmem_wait_st();
-            tc::fence_before_sync();
-            tc::mbar_arrive(&a_full[ab]);
-        }
-    } else if (warp == 5) {
-        // ---- MMA issuer: per 32-wide K tile 3 passes x 2 kind::f16 MMAs (K = 16) ----
-        constexpr uint32_t idesc = tc::idesc_f16(128, S0X_NC);
-        constexpr uint32_t LBO_B = (S0X_NC / 8) * 128;
-        const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(ring), LBO_B);
-        int64_t gc = 0;
-        for (int64_t jl = 0; jl < njobs; jl++) {
-            const int ab = int(jl & 1);
-            tc::mbar_wait(&a_full[ab], uint32_t(jl >> 1) & 1);
-            tc::fence_after_sync();
-            for (int nc = 0; nc < C::NCH; nc++, gc++) {
-                const int slot = int(gc & 1);
-                if (gc >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gc >> 1) - 1) & 1);
-                const int64_t it0 = gc * C::KS;
-                const uint32_t d = tmem + uint32_t(C::D_OFF + slot * S0X_NC);
-                for (int ks = 0; ks < C::KS; ks++) {
-                    const int st = int((it0 + ks) % C::NSTAGE);
-                    tc::mbar_wait(&full[st], uint32_t((it0 + ks) / C::NSTAGE) & 1);
-                    tc::fence_after_sync();
-#pragma unroll
-                    for (int q = 0; q < 3; q++) {
-                        const int pass = kPassOrder[q];
-                        const uint64_t b = tc::desc_add(dB0, st * C::STAGE + (pass == 2 ? S0H_TILE : 0));
-                        const uint32_t a = tmem + uint32_t(ab * C::A_BUF + (pass == 1 ? C::A_COLS : 0) + ks * (S0X_KC / 2));
-#pragma unroll
-                        for (int kk = 0; kk < S0X_KC / 16; kk++)
-                            tc::mma_f16_ts_warp(d, a + kk * 8, tc::desc_add(b, kk * 2 * LBO_B), idesc,
-                                                (q | ks | kk) ? 1u : 0u);
-                    }
-                    tc::commit_warp(&empty[st]);
-                }
-                tc::commit_warp(&dfull[slot]);
-                __syncwarp();
-            }
-            tc::commit_warp(&a_free[ab]);
-            __syncwarp();
-        }
-    } else {
-        // ---- epilogue (warps 6-13): lane quarter warp % 4 = vectors, column half (warp - 6) / 4.  Output rows
-        //      advance incrementally (t, then pair a at stride nleaf R nv); 2^{e_v + e_q} per complex row ----
-        const int q4 = warp & 3, cbase = ((warp - 6) >> 2) * 64;
-        constexpr int CQ = N0 * R;                                // complex output rows per leaf
-        const int64_t strideA = nleaf * R * int64_t(nv), jumpA = strideA - int64_t(R) * nv;
-        int64_t gc = 0;
-        for (int64_t jl = 0; jl < njobs; jl++) {
-            const unsigned job = unsigned(blockIdx.x + jl * gridDim.x);
-            const int64_t b = job / unsigned(nvt);
-            const int vg = int(job % unsigned(nvt)) * 128 + q4 * 32 + lane;
-            const int eb = int(jl & 3);
-            tc::mbar_wait(&e_full[eb], uint32_t(jl >> 2) & 1);
-            const float sv = Es[eb * 128 + q4 * 32 + lane];
-            tc::mbar_arrive(&e_empty[eb]);
-            const uint8_t* Sb = V0s + b * CQ + (cbase >> 1);
-            float2* const obase = out + b * R * int64_t(nv) + vg;
-            uint4 ex[2];   // the biased exponents of this thread's 32 complex rows of the chunk (one chunk ahead)
-            ex[0] = __ldg(reinterpret_cast<const uint4*>(Sb));
-            ex[1] = __ldg(reinterpret_cast<const uint4*>(Sb) + 1);
-            for (int nc = 0; nc < C::NCH; nc++, gc++) {
-                const int slot = int(gc & 1);
-                uint4 exn[2] = {ex[0], ex[1]};
-                if (nc + 1 < C::NCH) {
-                    exn[0] = __ldg(reinterpret_cast<const uint4*>(Sb + (nc + 1) * (S0X_NC / 2)));
-                    exn[1] = __ldg(reinterpret_cast<const uint4*>(Sb + (nc + 1) * (S0X_NC / 2)) + 1);
-                }
-                tc::mbar_wait(&dfull[slot], uint32_t(gc >> 1) & 1);
-                tc::fence_after_sync();
-                const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * S0X_NC + cbase);
-                const int q0 = (nc * S0X_NC + cbase) >> 1;
-                int t = q0 % R;
-                float2* o = obase + int64_t(q0 / R) * strideA + int64_t(t) * nv;
-#pragma unroll
-                for (int c0 = 0; c0 < 64; c0 += 32) {
-                    float x[32];
-                    tc::tmem_ld16(taddr + c0, x);
-                    tc::tmem_ld16(taddr + c0 + 16, x + 16);
-                    tc::tmem_wait_ld();
-                    if (c0 == 32) {
-                        tc::fence_before_sync();
-                        tc::mbar_arrive(&dempty[slot]);
-                    }
-                    const uint32_t* ew = reinterpret_cast<const uint32_t*>(&ex[c0 >> 5]);
-#pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const uint32_t be = (ew[i >> 2] >> (8 * (i & 3))) & 0xffu;
-                        const float s2 = sv * __uint_as_float(be << 23);
-                        if (vg < nv) *o = make_float2(x[2 * i] * s2, x[2 * i + 1] * s2);
-                        o += nv;
-                        if (++t == R) {
-                            t = 0;
-                            o += jumpA;
-                        }
-                    }
-                }
-                ex[0] = exn[0];
-                ex[1] = exn[1];
-            }
-        }
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 0) {
-        tc::fence_after_sync();
-        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
-    }
-}
-
-template <int R, int N0>
-static cudaError_t s0_h16_go(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const __half* V0h,
-                             const uint8_t* V0s, float2* out, int nv, cudaStream_t s)
-{
-    using C = S0H<R, N0>;
-    auto kern = s0_h16_kernel<R, N0>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    if (e != cudaSuccess) return e;
-    const int nvt = (nv + 127) / 128;
-    const int64_t jobs = (d.N / N0) * nvt;
-    const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
-    kern<<<grid, 448, C::SMEM, s>>>(F, ldf, ampb, V0h, V0s, out, d.LN, d.n_amp, nv, nvt);
-    return cudaGetLastError();
-}
-
-cudaError_t expand_s0_h16(const Dims& d, const float2* V0, void* V0h, void* V0s, cudaStream_t s)
-{
-    if (!leaf_tc_shape(d)) return cudaErrorInvalidValue;
-    expand_s0_h16_kernel<<<148 * 16, 128, 0, s>>>(V0, static_cast<__half*>(V0h), static_cast<uint8_t*>(V0s), d.LN,
-                                                  d.l0, d.R);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_s0_h16(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const void* V0h,
-                          const void* V0s, float2* out, int nv, cudaStream_t s)
-{
-    const int n0 = 1 << d.l0;
-    const __half* X = static_cast<const __half*>(V0h);
-    const uint8_t* E8 = static_cast<const uint8_t*>(V0s);
-#define S0H_CASE(RR)                                                                                       \
-    if (d.R == RR)                                                                                         \
-        return n0 == 64 ? s0_h16_go<RR, 64>(d, F, ldf, ampb, X, E8, out, nv, s)                            \
-                        : s0_h16_go<RR, 32>(d, F, ldf, ampb, X, E8, out, nv, s);
-    S0H_CASE(6) S0H_CASE(8) S0H_CASE(10) S0H_CASE(12) S0H_CASE(16)
-#undef S0H_CASE
-    return cudaErrorInvalidValue;
-}
-
-// =============================================================================================
 // SL (eqn:bf3 P:791-797, amplitude post-scale and sum over k eqn:tg P:24-28) on the tensor cores,
 // persistent.  A job = one T_X leaf a x one tile of 128 vectors (vector tile fastest).
 // D[v][2j + c'] = sum over K = (b, t, c) of A[v][(b, t, c)] B[(j, c')][(b, t, c)], A = delta_D[a n0 + b][t][v]
@@ -1168,370 +817,6 @@ cudaError_t launch_sl_tc(const Dims& d, const float2* in, const float* Ux, const
 }
 
 // =============================================================================================
-// SL in FP16 split passes (BF_OPT_LEAF_F16 = 1, the default): the structure of sl_tc_kernel with
-// kind::f16 MMAs (K = 16).  Every K chunk (KP pairs of the leaf, KC = KP 2r, a multiple of 16) is its own
-// accumulation segment: the split scales each vector's chunk by 2^{-e_vc} (max |x| in [0.5, 1)) before
-// the FP16 hi / lo split, and the drain adds 2^{e_vc} D_c into the FP32 register sums; the image rows
-// (output point j, re / im) are scaled to max |x| in [0.5, 1) with the exponent applied with a_k at the
-// end of the job.  Half the Ux image bytes, half the tensor time of the 3xTF32 SL.
-// =============================================================================================
-static int sl_kp_h(int R) { return (R == 12) ? 2 : (R == 16 ? 2 : 4); }   // KC = KP 2r multiple of 16
-
-int64_t leafu_rows(const Dims& d) { return d.N; }   // biased exponents of the SL image: one per output point
-
-__global__ void expand_sl_h16_kernel(const float2* __restrict__ U, __half* __restrict__ X, uint8_t* __restrict__ S,
-                                     int LN, int l0, int R, int KP)
-{
-    const int n0 = 1 << l0;
-    const int64_t nleaf = (int64_t(1) << LN) >> l0;
-    const int rows = 2 * n0, K = n0 * 2 * R, KC = KP * 2 * R;
-    const int nch = n0 / KP;
-    const int64_t tile = int64_t(rows) * KC;
-    const int64_t total = nleaf * n0;
-    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t a = g / n0;
-        const int j = int(g - a * n0);
-        const float2* w = U + (a * n0) * (n0 * R) + j;   // element (b, t): w[b n0 R + t n0]
-        float mx = 0.f;
-        for (int b = 0; b < n0; b++)
-            for (int t = 0; t < R; t++) {
-                const float2 x = w[(int64_t(b) * R + t) * n0];
-                mx = fmaxf(mx, fmaxf(fabsf(x.x), fabsf(x.y)));
-            }
-        int e = 0;
-        frexpf(mx, &e);
-        e = max(-126, min(126, e));
-        S[a * n0 + j] = uint8_t(e + 127);
-        for (int cp = 0; cp < 2; cp++) {
-            const int n = 2 * j + cp;
-            for (int k = 0; k < K; k++) {
-                const int b = k / (2 * R), t = (k / 2) % R, c = k & 1;
-                const float x = ldexpf(embed(w[(int64_t(b) * R + t) * n0], cp, c), -e);
-                float hi, lo;
-                tc::split_h(x, hi, lo);
-                const int ch = b / KP, kk = k - ch * KC;
-                __half* tl = X + ((a * nch + ch) * 2) * tile;
-                const uint32_t off = tc::kmaj_off16(n, kk, rows) / 2;
-                tl[off] = __float2half_rn(hi);
-                tl[tile + off] = __float2half_rn(lo);
-            }
-        }
-    }
-}
-
-template <int R, int N0, int NA, int KP>
-struct SLH {
-    static constexpr int NB = 2 * N0;
-    static constexpr int KC = KP * 2 * R;
-    static constexpr int NCH = N0 / KP;
-    static constexpr uint32_t RAW = uint32_t(KP) * R * 128 * 8;
-    static constexpr uint32_t BT = uint32_t(NB) * KC * 2;          // one of hi / lo (FP16)
-    static constexpr uint32_t GS_STRIDE = N0 + 1;
-    static constexpr uint32_t GS_BYTES = uint32_t(128 / NA) * GS_STRIDE * 8;
-    static constexpr uint32_t AS_BYTES = uint32_t(NA) * N0 * 8;
-    static constexpr uint32_t ES_BYTES = 4 * 128 * 4;
-    static constexpr size_t LIM = 232448 - 1024;
-    static constexpr int NR_FIT = int((LIM - GS_BYTES - AS_BYTES - ES_BYTES) / (RAW + 2 * BT));
-    static constexpr int NR = NR_FIT > 4 ? 4 : (NR_FIT < 2 ? 2 : NR_FIT);   // ring depth
-    static constexpr uint32_t OFF_B = NR * RAW, OFF_GS = OFF_B + 2 * NR * BT, OFF_AS = OFF_GS + GS_BYTES;
-    static constexpr uint32_t OFF_ES = OFF_AS + AS_BYTES;
-    static constexpr size_t SMEM = size_t(OFF_ES) + ES_BYTES;
-    static constexpr int A_COLS = KC;                                   // hi KC/2 packed columns, then lo
-    static constexpr int D_OFF = 2 * A_COLS;
-    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * NB>();
-    // shapes that fit (otherwise the plan keeps the 3xTF32 SL): whole kind::f16 K steps, a ring of >= 2
-    static constexpr bool OK = KC % 16 == 0 && NR_FIT >= 2 && D_OFF + 2 * NB <= 512 && SMEM <= LIM;
-};
-
-template <int R, int N0, int NA, int KP>
-__global__ void __launch_bounds__(448, 1)
-    sl_h16_kernel(const __grid_constant__ CUtensorMap tin, const __half* __restrict__ Uh,
-                  const uint8_t* __restrict__ Ue, const float2* __restrict__ ampa, float2* __restrict__ G, int64_t ldg,
-                  int LN, int nv, int nvt)
-{
-    using C = SLH<R, N0, NA, KP>;
-    extern __shared__ __align__(128) uint8_t sm_slh[];
-    auto raw = [&](int e) { return sm_slh + e * C::RAW; };
-    auto opB = [&](int e, int lo) { return sm_slh + C::OFF_B + (2 * e + lo) * C::BT; };
-    float2* Gs = reinterpret_cast<float2*>(sm_slh + C::OFF_GS);   // [128/NA][GS_STRIDE]
-    float2* As = reinterpret_cast<float2*>(sm_slh + C::OFF_AS);   // [NA][N0] a_k(x) of the current job
-    float* Es = reinterpret_cast<float*>(sm_slh + C::OFF_ES);      // [chunk % 4][128] 2^{e_vc}
-    __shared__ uint64_t raw_full[C::NR], raw_empty[C::NR], b_full[C::NR], b_empty[C::NR], a_full[2], a_empty[2],
-        dfull[2], dempty[2], e_full[4], e_empty[4];
-    __shared__ uint32_t tmem_base;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t N = int64_t(1) << LN;
-    const int64_t njobs_all = (N / N0) * nvt;
-    const int njobs = int((njobs_all - blockIdx.x + gridDim.x - 1) / gridDim.x);
-    const int nch_all = njobs * C::NCH;
-
-    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
-    if (tid == 0) {
-        for (int i = 0; i < C::NR; i++) {
-            tc::mbar_init(&raw_full[i], 1);
-            tc::mbar_init(&raw_empty[i], 128);
-            tc::mbar_init(&b_full[i], 1);
-            tc::mbar_init(&b_empty[i], 1);
-        }
-        for (int i = 0; i < 2; i++) {
-            tc::mbar_init(&a_full[i], 128);
-            tc::mbar_init(&a_empty[i], 1);
-            tc::mbar_init(&dfull[i], 1);
-            tc::mbar_init(&dempty[i], 256);
-        }
-        for (int i = 0; i < 4; i++) {
-            tc::mbar_init(&e_full[i], 128);
-            tc::mbar_init(&e_empty[i], 256);
-        }
-        tc::mbar_fence_init();
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = tmem_base;
-
-    if (warp == 12) {
-        // ---- loader: the chunk stream of all this CTA's jobs (Ux tiles: bulk copy; delta rows: 2-D TMA) ----
-        if (lane == 0) {
-            for (int gch = 0; gch < nch_all; gch++) {
-                const int jl = gch / C::NCH, ch = gch - jl * C::NCH;
-                const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
-                const int64_t a = job / unsigned(nvt);
-                const int v0 = int(job % unsigned(nvt)) * 128;
-                const int e = gch % C::NR, use = gch / C::NR;
-                if (use > 0) tc::mbar_wait(&raw_empty[e], (use - 1) & 1);
-                tc::mbar_arrive_expect_tx(&raw_full[e], C::RAW);
-                const int64_t p0 = a * N0 + int64_t(ch) * KP;
-                tc::tma_load_2d(raw(e), &tin, 2 * v0, int(p0 * R), &raw_full[e]);
-                if (use > 0) tc::mbar_wait(&b_empty[e], (use - 1) & 1);
-                tc::mbar_arrive_expect_tx(&b_full[e], 2 * C::BT);
-                tc::bulk_g2s(opB(e, 0), Uh + (a * C::NCH + ch) * 2 * (C::BT / 2), 2 * C::BT, &b_full[e]);
-            }
-        }
-    } else if (warp == 13) {
-        // ---- MMA issuer: one accumulation segment per chunk, 3 passes x KC/16 kind::f16 MMAs ----
-        constexpr uint32_t idesc = tc::idesc_f16(128, C::NB);
-        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
-        const uint64_t dB0 = tc::desc_kmajor(tc::smem_u32(opB(0, 0)), LBO_B);
-        for (int gch = 0; gch < nch_all; gch++) {
-            const int e = gch % C::NR, sa = gch & 1, slot = gch & 1;
-            if (gch >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gch >> 1) - 1) & 1);
-            tc::mbar_wait(&a_full[sa], uint32_t(gch >> 1) & 1);
-            tc::mbar_wait(&b_full[e], uint32_t(gch / C::NR) & 1);
-            tc::fence_after_sync();
-            const uint32_t d = tmem + uint32_t(C::D_OFF + slot * C::NB);
-#pragma unroll
-            for (int q = 0; q < 3; q++) {
-                const int pass = kPassOrder[q];
-                const uint32_t aa = tmem + uint32_t(sa * C::A_COLS + (pass == 1 ? C::KC / 2 : 0));
-                const uint64_t bb = tc::desc_add(dB0, (2 * e + (pass == 2)) * C::BT);
-#pragma unroll
-                for (int ks = 0; ks < C::KC / 16; ks++)
-                    tc::mma_f16_ts_warp(d, aa + ks * 8, tc::desc_add(bb, ks * 2 * LBO_B), idesc, (q | ks) ? 1u : 0u);
-            }
-            tc::commit_warp(&a_empty[sa]);
-            tc::commit_warp(&b_empty[e]);
-            tc::commit_warp(&dfull[slot]);
-            __syncwarp();
-        }
-    } else if (warp < 4) {
-        // ---- split: raw delta rows of a chunk, scaled by 2^{-e_vc}, FP16 hi / lo packed into TMEM ----
-        const int v = tid;
-        const uint32_t lb = uint32_t(warp * 32) << 16;
-        for (int gch = 0; gch < nch_all; gch++) {
-            const int e = gch % C::NR, sa = gch & 1, eb = gch & 3;
-            tc::mbar_wait(&raw_full[e], uint32_t(gch / C::NR) & 1);
-            if (gch >= 2) tc::mbar_wait(&a_empty[sa], uint32_t((gch >> 1) - 1) & 1);
-            if (gch >= 4) tc::mbar_wait(&e_empty[eb], uint32_t((gch >> 2) - 1) & 1);
-            tc::fence_after_sync();
-            const float2* rd = reinterpret_cast<const float2*>(raw(e));   // [KP R][128]
-            float mx = 0.f;
-#pragma unroll
-            for (int row = 0; row < KP * R; row++) {
-                const float2 x = rd[row * 128 + v];
-                mx = fmaxf(mx, fmaxf(fabsf(x.x), fabsf(x.y)));
-            }
-            int ex = 0;
-            frexpf(mx, &ex);
-            ex = max(-126, min(126, ex));
-            const float sc = ldexpf(1.f, -ex);
-            Es[eb * 128 + v] = ldexpf(1.f, ex);
-            tc::mbar_arrive(&e_full[eb]);
-            float hi[C::KC / 2], lo[C::KC / 2];   // packed column (pl, t) = pl R + t: (re, im)
-#pragma unroll
-            for (int row = 0; row < KP * R; row++) {
-                const float2 x = rd[row * 128 + v];
-                tc::split_h2(x.x * sc, x.y * sc, hi[row], lo[row]);
-            }
-            tc::fence_before_sync();
-            tc::mbar_arrive(&raw_empty[e]);
-            const uint32_t ta = tmem + lb + uint32_t(sa * C::A_COLS);
-            tc::tmem_st_cols<C::KC / 2>(ta, hi);
-            tc::tmem_st_cols<C::KC / 2>(ta + C::KC / 2, lo);
-            tc::tmem_wait_st();
-            tc::fence_before_sync();
-            tc::mbar_arrive(&a_full[sa]);
-        }
-    } else {
-        // ---- drain + epilogue (warps 4-11): lane quarter warp % 4 = vectors, column half (warp - 4) / 4 ----
-        constexpr int HC = C::NB / 2;   // columns per drain thread (j in a half of the leaf)
-        const int q4 = warp & 3, half = (warp - 4) >> 2, vl = q4 * 32 + lane, dt = (warp - 4) * 32 + lane;
-        const int k = vl % NA, cl = vl / NA;
-        int gch = 0;
-        for (int jl = 0; jl < njobs; jl++) {
-            const unsigned job = unsigned(blockIdx.x + int64_t(jl) * gridDim.x);
-            const int64_t a = job / unsigned(nvt);
-            const int v0 = int(job % unsigned(nvt)) * 128, vw = min(128, nv - v0);
-            // this thread's output points j = half HC/2 .. + HC/2: their image row exponents (read now, used at
-            // the end of the job)
-            uint32_t rexp[HC / 8];
-#pragma unroll
-            for (int u = 0; u < HC / 8; u++)
-                rexp[u] = __ldg(reinterpret_cast<const uint32_t*>(Ue + a * N0 + half * (HC / 2)) + u);
-            float sum[HC];
-#pragma unroll
-            for (int i = 0; i < HC; i++) sum[i] = 0.f;
-            for (int ch = 0; ch < C::NCH; ch++, gch++) {
-                const int slot = gch & 1, eb = gch & 3;
-                tc::mbar_wait(&e_full[eb], uint32_t(gch >> 2) & 1);
-                const float sv = Es[eb * 128 + vl];
-                tc::mbar_arrive(&e_empty[eb]);
-                tc::mbar_wait(&dfull[slot], uint32_t(gch >> 1) & 1);
-                tc::fence_after_sync();
-                const uint32_t taddr =
-                    tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * C::NB + half * HC);
-#pragma unroll
-                for (int c0 = 0; c0 < HC; c0 += 32) {
-                    float x[32];
-                    tc::tmem_ld_cols<(HC < 32 ? HC : 32)>(taddr + c0, x);
-                    tc::tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < (HC < 32 ? HC : 32); i++) sum[c0 + i] = fmaf(x[i], sv, sum[c0 + i]);
-                }
-                tc::fence_before_sync();
-                tc::mbar_arrive(&dempty[slot]);
-            }
-            // epilogue of the job: 2^{e_j} a_k(x) (staged per job), sum over k, G transposed through Gs
-            asm volatile("bar.sync 1, 256;" ::: "memory");   // the previous job's copy-out is done with Gs / As
-            for (int i = dt; i < NA * N0; i += 256) As[i] = __ldg(ampa + (i / N0) * N + a * N0 + (i % N0));
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-#pragma unroll
-            for (int jj = 0; jj < HC / 2; jj++) {
-                const int j = half * (HC / 2) + jj;
-                const uint32_t be = (rexp[jj >> 2] >> (8 * (jj & 3))) & 0xffu;
-                const float sj = __uint_as_float(be << 23);
-                float2 g = cmul_tc(As[k * N0 + j], make_float2(sum[2 * jj] * sj, sum[2 * jj + 1] * sj));
-#pragma unroll
-                for (int m = 1; m < NA; m <<= 1) {
-                    g.x += __shfl_xor_sync(0xffffffffu, g.x, m);
-                    g.y += __shfl_xor_sync(0xffffffffu, g.y, m);
-                }
-                if ((j % NA) == k) Gs[cl * C::GS_STRIDE + j] = g;
-            }
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            const int c0 = v0 / NA, cw = vw / NA;
-            for (int idx = dt; idx < cw * N0; idx += 256) {
-                const int cc = idx / N0, j = idx % N0;
-                G[a * N0 + j + int64_t(c0 + cc) * ldg] = Gs[cc * C::GS_STRIDE + j];
-            }
-        }
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 0) {
-        tc::fence_after_sync();
-        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
-    }
-}
-
-template <int R, int N0, int NA, int KP>
-static cudaError_t sl_h16_go(const Dims& d, const float2* in, const __half* Uh, const uint8_t* Ue, const float2* ampa,
-                             float2* G, int64_t ldg, int nv, cudaStream_t s)
-{
-    using C = SLH<R, N0, NA, KP>;
-    if constexpr (!C::OK) {
-        return cudaErrorInvalidValue;
-    } else {
-    auto kern = sl_h16_kernel<R, N0, NA, KP>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    if (e != cudaSuccess) return e;
-    const int nvt = (nv + 127) / 128;
-    const int64_t jobs = (d.N / N0) * nvt;
-    const unsigned grid = unsigned(jobs < sm_count() ? jobs : sm_count());
-    CUtensorMap tin;
-    e = make_rows_tmap(&tin, in, d.N * R, nv, KP * R);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, 448, C::SMEM, s>>>(tin, Uh, Ue, ampa, G, ldg, d.LN, nv, nvt);
-    return cudaGetLastError();
-    }
-}
-
-bool sl_h16_shape(const Dims& d)
-{
-    const int n0 = 1 << d.l0;
-#define SLH_OK(RR, N0_, KP_)                                                                     \
-    if (d.R == RR && n0 == N0_)                                                                  \
-        return d.n_amp == 1 ? SLH<RR, N0_, 1, KP_>::OK                                           \
-                            : (d.n_amp == 2 ? SLH<RR, N0_, 2, KP_>::OK : (d.n_amp == 4 && SLH<RR, N0_, 4, KP_>::OK));
-    SLH_OK(6, 64, 4) SLH_OK(8, 64, 4) SLH_OK(10, 64, 4) SLH_OK(12, 64, 2) SLH_OK(16, 64, 2)
-    SLH_OK(6, 32, 4) SLH_OK(8, 32, 4) SLH_OK(10, 32, 4) SLH_OK(12, 32, 2) SLH_OK(16, 32, 2)
-#undef SLH_OK
-    return false;
-}
-
-cudaError_t expand_sl_h16(const Dims& d, const float2* U, void* Uh, void* Ue, cudaStream_t s)
-{
-    if (!leaf_tc_shape(d)) return cudaErrorInvalidValue;
-    expand_sl_h16_kernel<<<148 * 16, 128, 0, s>>>(U, static_cast<__half*>(Uh), static_cast<uint8_t*>(Ue), d.LN, d.l0,
-                                                  d.R, sl_kp_h(d.R));
-    return cudaGetLastError();
-}
-
-cudaError_t launch_sl_h16(const Dims& d, const float2* in, const void* Uh, const void* Ue, const float2* ampa,
-                          float2* G, int64_t ldg, int nv, cudaStream_t s)
-{
-    const int n0 = 1 << d.l0;
-    const __half* X = static_cast<const __half*>(Uh);
-    const uint8_t* E8 = static_cast<const uint8_t*>(Ue);
-#define SLH_NA(RR, N0_, KP_)                                                                        \
-    if (d.R == RR && n0 == N0_) {                                                                   \
-        if (d.n_amp == 1) return sl_h16_go<RR, N0_, 1, KP_>(d, in, X, E8, ampa, G, ldg, nv, s);    \
-        if (d.n_amp == 2) return sl_h16_go<RR, N0_, 2, KP_>(d, in, X, E8, ampa, G, ldg, nv, s);    \
-        if (d.n_amp == 4) return sl_h16_go<RR, N0_, 4, KP_>(d, in, X, E8, ampa, G, ldg, nv, s);    \
-    }
-    SLH_NA(6, 64, 4) SLH_NA(8, 64, 4) SLH_NA(10, 64, 4) SLH_NA(12, 64, 2) SLH_NA(16, 64, 2)
-    SLH_NA(6, 32, 4) SLH_NA(8, 32, 4) SLH_NA(10, 32, 4) SLH_NA(12, 32, 2) SLH_NA(16, 32, 2)
-#undef SLH_NA
-    return cudaErrorInvalidValue;
-}
-
-// Band variant switch (BF_OPT_BAND_PIPELINES): 1 = single TMEM pipeline (default), 0 = two pipelines where
-// they fit.  Measured at cfg4 (tools/band_trace.py, profiles/r1_band_variants.txt): the two-pipeline kernel
-// halves the per-job cycle count on some SMs, but its concurrent tcgen05.st/ld traffic (two epilogues plus
-// the split) slows the tensor pipe on others, and the launch is 1.4x slower overall.
-
-
-
-// ---- timeline trace of the band kernel (diagnostic; CTA 0, first BT_JOBS jobs, SM clock) ----
-constexpr int BT_JOBS = 64, BT_EV = 12;
-__device__ long long g_band_trace[BT_JOBS * BT_EV];
-// (constant bank: the check costs no memory round trip; tracing is off until BF_OPT_BAND_TRACE_J0 is set)
-__constant__ int g_band_trace_j0 = 0;     // first traced job (BF_OPT_BAND_TRACE_J0: job + 65536 * cta)
-__constant__ int g_band_trace_cta = -1;   // traced CTA (-1: off)
-__device__ __forceinline__ void btrace(int64_t J, int ev)
-{
-    const int64_t j = J - g_band_trace_j0;
-    if (int(blockIdx.x) == g_band_trace_cta && j >= 0 && j < BT_JOBS) g_band_trace[j * BT_EV + ev] = clock64();
-}
-void band_trace_window(int v)
-{
-    const int j0 = v & 65535, cta = v >> 16;
-    cudaMemcpyToSymbol(g_band_trace_j0, &j0, sizeof(int));
-    cudaMemcpyToSymbol(g_band_trace_cta, &cta, sizeof(int));
-}
-
-// =============================================================================================
 // Transfer band of two levels (eqn:2 P:748-752 for l <= h, eqn:3 P:780-785 for l > h; the switch
 // P:755-766 is folded into the level-h blocks) on the tensor cores, persistent (one CTA per SM).
 // A group = 4 pairs at the input level closed under the two levels (fixed a0, 4 consecutive b),
@@ -1636,7 +921,6 @@ __global__ void __launch_bounds__(384, 1)
             const int use = J / C::NABUF;
             if (use > 0) tc::mbar_wait(&a_free[slot], uint32_t(use - 1) & 1);
             tc::fence_after_sync();
-            if (tid == 0) btrace(J, 0);
             const float2* rd = reinterpret_cast<const float2*>(raw(e));
 #pragma unroll 1
             for (int s = 0; s < C::P; s++) {
@@ -1653,7 +937,6 @@ __global__ void __launch_bounds__(384, 1)
             }
             tc::tmem_wait_st();
             tc::fence_before_sync();
-            if (tid == 0) btrace(J, 1);
             tc::mbar_arrive(&raw_empty[e]);
             tc::mbar_arrive(&a1_ready[slot]);
         }
@@ -1671,7 +954,6 @@ __global__ void __launch_bounds__(384, 1)
             // input slot of unit 1)
             tc::mbar_wait(&d1_full, ph);
             tc::fence_after_sync();
-            if (v == 0) btrace(J, 3);
 #pragma unroll 1
             for (int u = 0; u < C::U; u++) {
                 float d[C::NU];
@@ -1689,13 +971,11 @@ __global__ void __launch_bounds__(384, 1)
             }
             tc::tmem_wait_st();
             tc::fence_before_sync();
-            if (v == 0) btrace(J, 4);
             tc::mbar_arrive(&d1_free);
             tc::mbar_arrive(&a2_ready[slot]);
 
             tc::mbar_wait(&d2_full, ph);
             tc::fence_after_sync();
-            if (v == 0) btrace(J, 6);
             float d[C::U][C::NU];
 #pragma unroll
             for (int u = 0; u < C::U; u++) tc::tmem_ld_cols<C::NU>(tmem + lb + uint32_t(C::D2_OFF + u * C::NB), d[u]);
@@ -1726,7 +1006,6 @@ __global__ void __launch_bounds__(384, 1)
                 const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
                 const int e = int(J & 1);
                 if (J >= 2) tc::mbar_wait(&raw_empty[e], uint32_t((J >> 1) - 1) & 1);
-                btrace(J, 8);
                 const int v0 = vt * 128, vw = min(128, nv - v0);
                 const uint32_t row_bytes = uint32_t(vw) * 8;
                 tc::mbar_arrive_expect_tx(&raw_full[e], C::P * R * row_bytes);
@@ -1748,7 +1027,6 @@ __global__ void __launch_bounds__(384, 1)
             if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
 #pragma unroll 1
             for (int m = 0; m < 2; m++) {
-                if (lane == 0) btrace(J, m == 0 ? 9 : 10);
                 tc::mbar_wait(m == 0 ? &a1_ready[slot] : &a2_ready[slot], uint32_t(J / C::NABUF) & 1);
                 if (J >= 1) tc::mbar_wait(m == 0 ? &d1_free : &d2_free, uint32_t(J - 1) & 1);
                 tc::fence_after_sync();
@@ -1768,13 +1046,11 @@ __global__ void __launch_bounds__(384, 1)
                                                  (q | ks) ? 1u : 0u);
                     }
                 }
-                if (lane == 0) btrace(J, m == 0 ? 2 : 5);
                 tc::commit_warp(m == 0 ? &d1_full : &d2_full);
             }
             tc::commit_warp(&a_free[slot]);
             if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
             __syncwarp();
-            if (lane == 0) btrace(J, 11);
         }
     } else {
         // ---- weights (warps 10-11): compact r x 2r blocks -> embedded hi/lo B tiles, one group ahead ----
@@ -1836,282 +1112,6 @@ __global__ void __launch_bounds__(384, 1)
 // 4-7 / 8-11 epilogue of pipeline 0 / 1 (E1 and E2 of its jobs), 12 loader, 13 MMA, 14-15 weights.
 // MMA order: L1(J), L1(J+1), L2(J), L2(J+1), L1(J+2), ...
 // ---------------------------------------------------------------------------------------------
-template <int R>
-struct Band2P {
-    using B = BandTC<R>;
-    static constexpr int PCOLS = B::ACOLS + B::DCOLS;   // one pipeline: A (hi, lo) + accumulators
-    static constexpr bool FITS = 2 * PCOLS <= 512;
-    static constexpr int TMEM_COLS = 512;
-};
-
-template <int R>
-__global__ void __launch_bounds__(512, 1)
-    band_tc2p_kernel(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ W1,
-                     const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg, const bfs::PeerOut po)
-{
-    using C = BandTC<R>;
-    using Q = Band2P<R>;
-    extern __shared__ __align__(128) uint8_t sm_band[];
-    auto raw = [&](int e) { return sm_band + e * C::RAW; };
-    auto wtile = [&](int wb, int m, int u, int lo) {
-        return sm_band + C::OFF_W + wb * C::WSET + ((m * C::U + u) * 2 + lo) * C::WT;
-    };
-    __shared__ uint64_t raw_full[2], raw_empty[2], w_full[2], w_free[2];
-    __shared__ uint64_t a1_ready[2], a2_ready[2], a_free[2], d1_full[2], d2_full[2], d2_free[2];   // per pipeline
-    __shared__ uint32_t tmem_base;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t N = int64_t(1) << LN;
-    const int lin = l_first - 1, shg = LN - lin - 2;
-    const int64_t ngroups = N >> 2;
-    const int nvt = (nv + 127) / 128;
-    const int nit = int((ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x);
-    const int njobs = nit * nvt;
-
-    if (warp == 0) tc::tmem_alloc<Q::TMEM_COLS>(&tmem_base);
-    if (tid == 0) {
-        for (int i = 0; i < 2; i++) {
-            tc::mbar_init(&raw_full[i], 1);
-            tc::mbar_init(&raw_empty[i], 128);
-            tc::mbar_init(&w_full[i], 64);
-            tc::mbar_init(&w_free[i], 1);
-            tc::mbar_init(&a1_ready[i], 128);
-            tc::mbar_init(&a2_ready[i], 128);
-            tc::mbar_init(&a_free[i], 1);
-            tc::mbar_init(&d1_full[i], 1);
-            tc::mbar_init(&d2_full[i], 1);
-            tc::mbar_init(&d2_free[i], 128);
-        }
-        tc::mbar_fence_init();
-    }
-    if constexpr (C::NB > C::NU) {   // zero the pad rows of every B tile (never written afterwards)
-        constexpr int PADQ = (C::NB - C::NU) * C::KU / 4;
-        for (int idx = tid; idx < C::NWBUF * 2 * C::U * 2 * PADQ; idx += blockDim.x) {
-            const int tile = idx / PADQ, o = idx % PADQ;
-            const int row = C::NU + o % (C::NB - C::NU), k = 4 * (o / (C::NB - C::NU));
-            st_f4(sm_band + C::OFF_W + tile * C::WT, tc::kmaj_off(row, k, C::NB), make_float4(0, 0, 0, 0));
-        }
-    }
-    tc::fence_proxy_async();
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = tmem_base;
-    auto abuf = [&](int p) { return tmem + uint32_t(p * Q::PCOLS); };               // hi at +0, lo at +P SC
-    auto dbuf = [&](int p) { return tmem + uint32_t(p * Q::PCOLS + C::ACOLS); };    // unit u at +u NB
-
-    if (warp < 4) {
-        // ---- split: raw rows -> the job's pipeline A buffer (TMEM), lane = vector ----
-        const int v = tid;
-        const uint32_t lb = uint32_t(warp * 32) << 16;
-        for (int J = 0; J < njobs; J++) {
-            const int e = J & 1, p = J & 1, use = J >> 1;
-            tc::mbar_wait(&raw_full[e], uint32_t(use & 1));
-            if (use > 0) tc::mbar_wait(&a_free[p], uint32_t(use - 1) & 1);
-            tc::fence_after_sync();
-            if (tid == 0) btrace(J, 0);
-            const float2* rd = reinterpret_cast<const float2*>(raw(e));
-#pragma unroll 1
-            for (int s = 0; s < C::P; s++) {
-                float hi[C::SC], lo[C::SC];
-#pragma unroll
-                for (int t = 0; t < R; t++) {
-                    const float2 x = rd[(s * R + t) * 128 + v];
-                    tc::split(x.x, hi[2 * t], lo[2 * t]);
-                    tc::split(x.y, hi[2 * t + 1], lo[2 * t + 1]);
-                }
-                const uint32_t ta = abuf(p) + lb + uint32_t(s * C::SC);
-                tc::tmem_st_cols<C::SC>(ta, hi);
-                tc::tmem_st_cols<C::SC>(ta + C::P * C::SC, lo);
-            }
-            tc::tmem_wait_st();
-            tc::fence_before_sync();
-            if (tid == 0) btrace(J, 1);
-            tc::mbar_arrive(&raw_empty[e]);
-            tc::mbar_arrive(&a1_ready[p]);
-        }
-    } else if (warp < 12) {
-        // ---- epilogue of pipeline p: level-1 drain + re-split, level-2 drain + store ----
-        const int p = (warp - 4) >> 2;
-        const int v = ((warp - 4) & 3) * 32 + lane;
-        const uint32_t lb = uint32_t(((warp - 4) & 3) * 32) << 16;
-        for (int J = p; J < njobs; J += 2) {
-            const int use = J >> 1;
-            const int it = int(unsigned(J) / unsigned(nvt));
-            const int vt = J - it * nvt;
-            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
-            const uint32_t ph = uint32_t(use & 1);
-            tc::mbar_wait(&d1_full[p], ph);
-            tc::fence_after_sync();
-            if (v == 0) btrace(J, 3);
-#pragma unroll 1
-            for (int u = 0; u < C::U; u++) {
-                float d[C::NU];
-                tc::tmem_ld_cols<C::NU>(dbuf(p) + lb + uint32_t(u * C::NB), d);
-                tc::tmem_wait_ld();
-#pragma unroll
-                for (int e = 0; e < 2; e++) {
-                    float hi[C::SC], lo[C::SC];
-#pragma unroll
-                    for (int i = 0; i < C::SC; i++) tc::split(d[e * C::SC + i], hi[i], lo[i]);
-                    const uint32_t ta = abuf(p) + lb + uint32_t((2 * e + u) * C::SC);
-                    tc::tmem_st_cols<C::SC>(ta, hi);
-                    tc::tmem_st_cols<C::SC>(ta + C::P * C::SC, lo);
-                }
-            }
-            tc::tmem_wait_st();
-            tc::fence_before_sync();
-            if (v == 0) btrace(J, 4);
-            tc::mbar_arrive(&a2_ready[p]);   // A is ready for level 2 and the accumulator is drained
-
-            tc::mbar_wait(&d2_full[p], ph);
-            tc::fence_after_sync();
-            if (v == 0) btrace(J, 6);
-            float d[C::U][C::NU];
-#pragma unroll
-            for (int u = 0; u < C::U; u++) tc::tmem_ld_cols<C::NU>(dbuf(p) + lb + uint32_t(u * C::NB), d[u]);
-            tc::tmem_wait_ld();
-            tc::fence_before_sync();
-            tc::mbar_arrive(&d2_free[p]);
-            const int vg = vt * 128 + v;
-            if (vg < nv) {
-                const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
-#pragma unroll
-                for (int u = 0; u < C::U; u++)
-#pragma unroll
-                    for (int e = 0; e < 2; e++) {
-                        const int64_t q = (((a0 << 2) + 2 * u + e) << shg) + bq;
-                        float2* o = out + q * R * int64_t(nv) + vg;
-#pragma unroll
-                        for (int t = 0; t < R; t++)
-                            o[int64_t(t) * nv] = make_float2(d[u][e * C::SC + 2 * t], d[u][e * C::SC + 2 * t + 1]);
-                    }
-            }
-        }
-    } else if (warp == 12) {
-        // ---- loader ----
-        if (lane == 0) {
-            for (int J = 0; J < njobs; J++) {
-                const int it = int(unsigned(J) / unsigned(nvt));
-                const int vt = J - it * nvt;
-                const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
-                const int e = J & 1;
-                if (J >= 2) tc::mbar_wait(&raw_empty[e], uint32_t((J >> 1) - 1) & 1);
-                btrace(J, 8);
-                const int v0 = vt * 128, vw = min(128, nv - v0);
-                const uint32_t row_bytes = uint32_t(vw) * 8;
-                tc::mbar_arrive_expect_tx(&raw_full[e], C::P * R * row_bytes);
-                const int64_t pin = rh ? bfs::recv_index(g * C::P, rh, rhg) : g * C::P;   // P pairs contiguous
-                for (int row = 0; row < C::P * R; row++)
-                    tc::bulk_g2s(raw(e) + row * 128 * 8, in + (pin * R + row) * int64_t(nv) + v0, row_bytes,
-                                 &raw_full[e]);
-            }
-        }
-    } else if (warp == 13) {
-        // ---- MMA issuer (whole warp, one elected lane issues) ----
-        constexpr uint32_t idesc = tc::idesc_tf32(128, C::NB);
-        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
-        const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_band + C::OFF_W), LBO_B);
-        auto level = [&](int J, int m) {
-            const int it = int(unsigned(J) / unsigned(nvt));
-            const int vt = J - it * nvt;
-            const int wb = it % C::NWBUF, p = J & 1, use = J >> 1;
-            if (lane == 0) btrace(J, m == 0 ? 9 : 10);
-            if (m == 0) {
-                if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
-                tc::mbar_wait(&a1_ready[p], uint32_t(use & 1));
-                if (use > 0) tc::mbar_wait(&d2_free[p], uint32_t(use - 1) & 1);
-            } else {
-                tc::mbar_wait(&a2_ready[p], uint32_t(use & 1));
-            }
-            tc::fence_after_sync();
-#pragma unroll
-            for (int u = 0; u < C::U; u++) {
-                const uint32_t d = dbuf(p) + uint32_t(u * C::NB);
-                const uint32_t ahi = abuf(p) + uint32_t(2 * u * C::SC);
-                const uint64_t bhi = tc::desc_add(dW, wb * C::WSET + ((m * C::U + u) * 2) * C::WT);
-#pragma unroll
-                for (int q = 0; q < 3; q++) {
-                    const int pass = kPassOrder[q];
-                    const uint32_t a = ahi + (pass == 1 ? C::P * C::SC : 0);
-                    const uint64_t b = pass == 2 ? tc::desc_add(bhi, C::WT) : bhi;
-#pragma unroll
-                    for (int ks = 0; ks < C::KU / 8; ks++)
-                        tc::mma_tf32_ts_warp(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc, (q | ks) ? 1u : 0u);
-                }
-            }
-            if (lane == 0) btrace(J, m == 0 ? 2 : 5);
-            if (m == 0) {
-                tc::commit_warp(&d1_full[p]);
-            } else {
-                tc::commit_warp(&d2_full[p]);
-                tc::commit_warp(&a_free[p]);
-                if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
-            }
-            __syncwarp();
-        };
-        for (int J0 = 0; J0 < njobs; J0 += 2) {
-            level(J0, 0);
-            if (J0 + 1 < njobs) level(J0 + 1, 0);
-            level(J0, 1);
-            if (J0 + 1 < njobs) level(J0 + 1, 1);
-        }
-    } else {
-        // ---- weights (warps 14-15): compact r x 2r blocks -> embedded hi/lo B tiles, one group ahead ----
-        const int wt = tid - 448;
-        for (int it = 0; it < nit; it++) {
-            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
-            const int wb = it % C::NWBUF;
-            if (it >= C::NWBUF) tc::mbar_wait(&w_free[wb], uint32_t(it / C::NWBUF - 1) & 1);
-            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
-            constexpr int BATCH = 13;   // loads in flight per thread (bounded registers)
-#pragma unroll 1
-            for (int q0 = 0; q0 < C::WPT; q0 += BATCH) {
-                float2 w[BATCH];
-#pragma unroll
-                for (int q = 0; q < BATCH; q++) {
-                    const int idx = wt + 64 * (q0 + q);
-                    w[q] = make_float2(0.f, 0.f);
-                    if (q0 + q < C::WPT && idx < C::WTASKS) {
-                        const int t = idx % R, kcol = (idx / R) % (2 * R), e = (idx / (2 * R * R)) & 1;
-                        const int mu = idx / (4 * R * R), m = mu / C::U, u = mu % C::U;
-                        const int lv = m + 1, ep = u >> (2 - lv), i = u & ((1 << (2 - lv)) - 1);
-                        const int64_t pr = (((a0 << lv) + 2 * ep + e) << (LN - lin - lv)) + (bq << (2 - lv)) + i;
-                        w[q] = __ldg((lv == 1 ? W1 : W2) + pr * (2 * R * R) + kcol * R + t);
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < BATCH; q++) {
-                    const int idx = wt + 64 * (q0 + q);
-                    if (q0 + q < C::WPT && idx < C::WTASKS) {
-                        const int t = idx % R, kcol = (idx / R) % (2 * R), e = (idx / (2 * R * R)) & 1;
-                        const int mu = idx / (4 * R * R), m = mu / C::U, u = mu % C::U;
-                        float hr, lr, hi_, li;
-                        tc::split(w[q].x, hr, lr);
-                        tc::split(w[q].y, hi_, li);
-                        const int n = e * C::SC + 2 * t, k = 2 * kcol;
-                        uint8_t* th = wtile(wb, m, u, 0);
-                        uint8_t* tl = wtile(wb, m, u, 1);
-                        const uint32_t o0 = tc::kmaj_off(n, k, C::NB), o1 = tc::kmaj_off(n + 1, k, C::NB);
-                        *reinterpret_cast<float2*>(th + o0) = make_float2(hr, -hi_);
-                        *reinterpret_cast<float2*>(tl + o0) = make_float2(lr, -li);
-                        *reinterpret_cast<float2*>(th + o1) = make_float2(hi_, hr);
-                        *reinterpret_cast<float2*>(tl + o1) = make_float2(li, lr);
-                    }
-                }
-            }
-            tc::fence_proxy_async();
-            tc::mbar_arrive(&w_full[wb]);
-        }
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 0) {
-        tc::fence_after_sync();
-        tc::tmem_dealloc<Q::TMEM_COLS>(tmem);
-    }
-}
-
 // =============================================================================================
 // Composed two-level band (the default tensor-core band).  The two transfer levels of a band map a
 // group of 4 input pairs to 4 output pairs, and each output pair reaches each input pair through
@@ -2217,12 +1217,10 @@ __global__ void __launch_bounds__(512, 1)
             const int ab = J % C::NABUF, use = J / C::NABUF;
             if (use > 0) tc::mbar_wait(&a_free[ab], uint32_t(use - 1) & 1);
             tc::fence_after_sync();
-            if (tid == 0) btrace(J, 1);
 #pragma unroll 1
             for (int s = hs * SPW; s < (hs + 1) * SPW; s++) {
                 const int k = J * C::P + s, q = k % C::NQ;
                 tc::mbar_wait(&slot_full[q], uint32_t(k / C::NQ) & 1);
-                if (tid == 0 && s == 0) btrace(J, 0);
                 const float2* rd = reinterpret_cast<const float2*>(sm_cmp + q * C::SLOT);
                 float hi[C::SC], lo[C::SC];
 #pragma unroll
@@ -2244,7 +1242,6 @@ __global__ void __launch_bounds__(512, 1)
             }
             tc::tmem_wait_st();
             tc::fence_before_sync();
-            if (tid == 0) btrace(J, 2);
             tc::mbar_arrive(&a_ready[ab]);
         }
     } else if (warp < 12) {
@@ -2261,7 +1258,6 @@ __global__ void __launch_bounds__(512, 1)
             const int db = J % C::NDBUF;
             tc::mbar_wait(&d_full[db], uint32_t(J / C::NDBUF) & 1);
             tc::fence_after_sync();
-            if (warp == C::NSPLIT && lane == 0) btrace(J, 5);
             const int vg = vt * 128 + v;
             const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
 #pragma unroll 1
@@ -2305,7 +1301,6 @@ __global__ void __launch_bounds__(512, 1)
                     }
                 }
             }
-            if (warp == C::NSPLIT && lane == 0) btrace(J, 6);
         }
     } else if (warp == 12) {
         // ---- loader: the group's 4 r raw coefficient rows of one vector tile, one 2-D tensor copy per pair
@@ -2319,13 +1314,11 @@ __global__ void __launch_bounds__(512, 1)
                 const int k = J * C::P + s, q = k % C::NQ;
                 if (k >= C::NQ) tc::mbar_wait(&slot_empty[q], uint32_t(k / C::NQ - 1) & 1);
                 if (lane == 0) {
-                    if (s == 0) btrace(J, 7);
                     tc::mbar_arrive_expect_tx(&slot_full[q], C::SLOT);   // whole box (ragged tile: zero fill)
                     tc::tma_load_2d(sm_cmp + q * C::SLOT, &tin, 2 * vt * 128, int((pin + s) * R), &slot_full[q]);
                 }
                 __syncwarp();
             }
-            if (lane == 0) btrace(J, 8);
         }
     } else if (warp == 13) {
         // ---- MMA issuer (whole warp, one elected lane issues): one chain of 3 x (8r / 8) MMAs per job ----
@@ -2337,11 +1330,9 @@ __global__ void __launch_bounds__(512, 1)
             const int vt = J - it * nvt;
             const int wb = it % C::NWBUF, ab = J % C::NABUF, db = J % C::NDBUF;
             if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it / C::NWBUF) & 1);
-            if (lane == 0) btrace(J, 11);
             tc::mbar_wait(&a_ready[ab], uint32_t(J / C::NABUF) & 1);
             if (J >= C::NDBUF) tc::mbar_wait(&d_free[db], uint32_t(J / C::NDBUF - 1) & 1);
             tc::fence_after_sync();
-            if (lane == 0) btrace(J, 3);
             const uint32_t d = tmem + uint32_t(C::D_OFF + db * C::NB);
             const uint32_t ahi = tmem + uint32_t(ab * C::ACOLS);
             const uint64_t bhi = tc::desc_add(dW, wb * C::WSET);
@@ -2358,7 +1349,6 @@ __global__ void __launch_bounds__(512, 1)
             tc::commit_warp(&a_free[ab]);
             if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
             __syncwarp();
-            if (lane == 0) btrace(J, 4);
         }
     } else {
         // ---- weights (warps 14-15): stage both levels' compact blocks (bulk copies, one group ahead),
@@ -2384,7 +1374,6 @@ __global__ void __launch_bounds__(512, 1)
             tc::mbar_wait(&wst_full[sb], uint32_t(it >> 1) & 1);
             const float2* st = reinterpret_cast<const float2*>(sm_cmp + C::OFF_WST + sb * C::WST);
             if (it >= C::NWBUF) tc::mbar_wait(&w_free[wb], uint32_t(it / C::NWBUF - 1) & 1);
-            if (wt == 0) btrace(int64_t(it) * nvt, 9);
             uint8_t* th = sm_cmp + C::OFF_W + wb * C::WSET;
             uint8_t* tl = th + C::WT;
             // item = (o, i, t', half of j): R / 2 independent complex accumulators per thread (ILP), the
@@ -2435,355 +1424,8 @@ __global__ void __launch_bounds__(512, 1)
                 }
             }
             tc::fence_proxy_async();
-            if (wt == 0) btrace(int64_t(it) * nvt, 10);
             tc::mbar_arrive(&w_full[wb]);
             asm volatile("bar.sync 1, 64;" ::: "memory");   // staging buffer sb free for group it + 2
-        }
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 0) {
-        tc::fence_after_sync();
-        tc::tmem_dealloc<C::TMEM_COLS>(tmem);
-    }
-}
-
-// =============================================================================================
-// Composed band in FP16 split passes (BF_OPT_BAND_F16 = 1).  Same job structure as band_cmp_kernel; the
-// A operand of a job (4 pairs x r coefficients of one vector) is scaled by 2^{-e_v} with e_v from its max
-// (the two split warps of a lane quadrant exchange their halves' maxima through shared memory), the
-// composed block operator C of a group by 2^{-e_g} (its max), both split into FP16 hi + lo and multiplied
-// with kind::f16 MMAs (K = 16): half the MMAs, half the TMEM stores and half the B bytes of the 3xTF32
-// band.  The epilogue multiplies by 2^{e_v + e_g}.
-// =============================================================================================
-template <int R>
-struct BandH {
-    using B = BandCmp<R>;
-    static constexpr int P = 4, SC = 2 * R, KB = P * SC, NB = KB;
-    static constexpr int ACOLS = KB;                                  // hi KB/2 packed columns, then lo
-    static constexpr int NABUF = 2, NDBUF = 2;
-    static constexpr int D_OFF = NABUF * ACOLS;
-    static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + NDBUF * NB>();
-    static constexpr uint32_t SLOT = B::SLOT, BLK = B::BLK, WST = B::WST;
-    static constexpr uint32_t WT = uint32_t(NB) * KB * 2;             // one FP16 B tile (hi or lo)
-    static constexpr uint32_t WSET = 2 * WT;
-    static constexpr uint32_t CST = uint32_t(P) * P * R * R * 8;      // the composed C (FP32 complex)
-    static constexpr uint32_t XCH = 2 * 2 * 128 * 4 + 4 * 128 * 4 + 4 * 4;   // maxima exchange, e_v ring, e_g ring
-    static constexpr size_t LIM = 232448 - 1024;
-    static constexpr int NQ_FIT = int((LIM - 2 * size_t(WST) - CST - 2 * size_t(WSET) - XCH) / SLOT);
-    static constexpr int NQ = NQ_FIT > 16 ? 16 : NQ_FIT;
-    static constexpr uint32_t OFF_WST = uint32_t(NQ) * SLOT;
-    static constexpr uint32_t OFF_CST = OFF_WST + 2 * WST;
-    static constexpr uint32_t OFF_W = OFF_CST + CST;
-    static constexpr uint32_t OFF_X = OFF_W + 2 * WSET;
-    static constexpr size_t SMEM = size_t(OFF_X) + XCH;
-    static constexpr int ITEMS = P * P * R * 2;
-    static_assert(KB % 16 == 0 && D_OFF + NDBUF * NB <= 512 && OFF_W % 128 == 0 && WT % 128 == 0 && NQ >= 6 &&
-                      SMEM <= LIM, "FP16 band shape");
-};
-
-template <int R>
-__global__ void __launch_bounds__(512, 1)
-    band_h16_kernel(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ W1,
-                    const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg, const bfs::PeerOut po)
-{
-    using C = BandH<R>;
-    extern __shared__ __align__(128) uint8_t sm_bh[];
-    __shared__ uint64_t slot_full[16], slot_empty[16];
-    __shared__ uint64_t a_ready[2], a_free[2], d_full[2], d_free[2], w_full[2], w_free[2], wst_full[2];
-    __shared__ uint64_t e_full[4], e_empty[4], g_full[4], g_empty[4];
-    __shared__ float red[2];
-    __shared__ uint32_t tmem_base;
-    float* Mx = reinterpret_cast<float*>(sm_bh + C::OFF_X);           // [J & 1][half][128] split maxima
-    float* Ev = Mx + 2 * 2 * 128;                                      // [J & 3][128] 2^{e_v}
-    float* Eg = Ev + 4 * 128;                                          // [group & 3] 2^{e_g}
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t N = int64_t(1) << LN;
-    const int lin = l_first - 1, shg = LN - lin - 2;
-    const int64_t ngroups = N >> 2;
-    const int nvt = (nv + 127) / 128;
-    const int nit = int((ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x);
-    const int njobs = nit * nvt;
-
-    if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base);
-    if (tid == 0) {
-        for (int i = 0; i < C::NQ; i++) {
-            tc::mbar_init(&slot_full[i], 1);
-            tc::mbar_init(&slot_empty[i], 128);
-        }
-        for (int i = 0; i < 2; i++) {
-            tc::mbar_init(&a_ready[i], 256);
-            tc::mbar_init(&a_free[i], 1);
-            tc::mbar_init(&d_full[i], 1);
-            tc::mbar_init(&d_free[i], 128);
-            tc::mbar_init(&w_full[i], 64);
-            tc::mbar_init(&w_free[i], 1);
-            tc::mbar_init(&wst_full[i], 1);
-        }
-        for (int i = 0; i < 4; i++) {
-            tc::mbar_init(&e_full[i], 128);
-            tc::mbar_init(&e_empty[i], 128);
-            tc::mbar_init(&g_full[i], 64);
-            tc::mbar_init(&g_empty[i], 128);
-        }
-        tc::mbar_fence_init();
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = tmem_base;
-
-    if (warp < 8) {
-        // ---- split (two warps per lane quadrant, one per half of the group's 4 pair slots) ----
-        const int qd = warp & 3, hs = warp >> 2;
-        const int v = qd * 32 + lane;
-        const uint32_t lb = uint32_t(qd * 32) << 16;
-        for (int J = 0; J < njobs; J++) {
-            const int ab = J & 1, use = J >> 1, eb = J & 3;
-            if (use > 0) tc::mbar_wait(&a_free[ab], uint32_t(use - 1) & 1);
-            if (hs == 0 && J >= 4) tc::mbar_wait(&e_empty[eb], uint32_t((J >> 2) - 1) & 1);
-            tc::fence_after_sync();
-            float mx = 0.f;
-#pragma unroll 1
-            for (int s = 2 * hs; s < 2 * hs + 2; s++) {
-                const int k = J * C::P + s, q = k % C::NQ;
-                tc::mbar_wait(&slot_full[q], uint32_t(k / C::NQ) & 1);
-                const float2* rd = reinterpret_cast<const float2*>(sm_bh + q * C::SLOT);
-#pragma unroll
-                for (int t = 0; t < R; t++) {
-                    const float2 x = rd[t * 128 + v];
-                    mx = fmaxf(mx, fmaxf(fabsf(x.x), fabsf(x.y)));
-                }
-            }
-            Mx[(ab * 2 + hs) * 128 + v] = mx;
-            asm volatile("bar.sync %0, 64;" ::"r"(2 + qd) : "memory");   // the two warps of this quadrant
-            mx = fmaxf(mx, Mx[(ab * 2 + (hs ^ 1)) * 128 + v]);
-            int e = 0;
-            frexpf(mx, &e);
-            e = max(-126, min(126, e));
-            const float sc = ldexpf(1.f, -e);
-            if (hs == 0) {
-                Ev[eb * 128 + v] = ldexpf(1.f, e);
-                tc::mbar_arrive(&e_full[eb]);
-            }
-            float hi[2 * R], lo[2 * R];   // this half's two pair slots, packed (re, im) columns
-#pragma unroll
-            for (int s2 = 0; s2 < 2; s2++) {
-                const int k = J * C::P + 2 * hs + s2, q = k % C::NQ;
-                const float2* rd = reinterpret_cast<const float2*>(sm_bh + q * C::SLOT);
-#pragma unroll
-                for (int t = 0; t < R; t++) {
-                    const float2 x = rd[t * 128 + v];
-                    tc::split_h2(x.x * sc, x.y * sc, hi[s2 * R + t], lo[s2 * R + t]);
-                }
-                tc::mbar_arrive(&slot_empty[q]);
-            }
-            const uint32_t ta = tmem + lb + uint32_t(ab * C::ACOLS + 2 * hs * R);
-            tc::tmem_st_cols<2 * R>(ta, hi);
-            tc::tmem_st_cols<2 * R>(ta + C::KB / 2, lo);
-            tc::tmem_wait_st();
-            tc::fence_before_sync();
-            tc::mbar_arrive(&a_ready[ab]);
-        }
-    } else if (warp < 12) {
-        // ---- epilogue (4 warps): drain the accumulator row in halves, scale by 2^{e_v + e_g}, store ----
-        const int q = warp & 3;
-        const int v = q * 32 + lane;
-        const uint32_t lb = uint32_t(q * 32) << 16;
-        float sg = 1.f;
-        for (int J = 0; J < njobs; J++) {
-            const int it = int(unsigned(J) / unsigned(nvt));
-            const int vt = J - it * nvt;
-            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
-            const int db = J & 1, eb = J & 3;
-            if (vt == 0) {
-                tc::mbar_wait(&g_full[it & 3], uint32_t(it >> 2) & 1);
-                sg = Eg[it & 3];
-                tc::mbar_arrive(&g_empty[it & 3]);
-            }
-            tc::mbar_wait(&e_full[eb], uint32_t(J >> 2) & 1);
-            const float s2 = Ev[eb * 128 + v] * sg;
-            tc::mbar_arrive(&e_empty[eb]);
-            tc::mbar_wait(&d_full[db], uint32_t(J >> 1) & 1);
-            tc::fence_after_sync();
-            const int vg = vt * 128 + v;
-            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
-#pragma unroll 1
-            for (int hf = 0; hf < 2; hf++) {
-                float d[2 * C::SC];
-                tc::tmem_ld_cols<2 * C::SC>(tmem + lb + uint32_t(C::D_OFF + db * C::NB + hf * 2 * C::SC), d);
-                tc::tmem_wait_ld();
-                if (hf == 1) {
-                    tc::fence_before_sync();
-                    tc::mbar_arrive(&d_free[db]);
-                }
-                if (vg < nv) {
-                    if (!po.on) {
-                        const int64_t p = (((a0 << 2) + 2 * hf) << shg) + bq;
-                        float2* o = out + p * R * int64_t(nv) + vg;
-                        const int64_t pstep = (int64_t(1) << shg) * R * int64_t(nv) - int64_t(R) * nv;
-#pragma unroll
-                        for (int oo = 0; oo < 2; oo++) {
-#pragma unroll
-                            for (int t = 0; t < R; t++) {
-                                *o = make_float2(d[oo * C::SC + 2 * t] * s2, d[oo * C::SC + 2 * t + 1] * s2);
-                                o += nv;
-                            }
-                            o += pstep;
-                        }
-                    } else {
-#pragma unroll
-                        for (int oo = 0; oo < 2; oo++) {
-                            const int64_t p = (((a0 << 2) + 2 * hf + oo) << shg) + bq;
-                            float2* o = bfs::pair_out(out, po, p, R, nv) + vg;
-#pragma unroll
-                            for (int t = 0; t < R; t++)
-                                o[int64_t(t) * nv] =
-                                    make_float2(d[oo * C::SC + 2 * t] * s2, d[oo * C::SC + 2 * t + 1] * s2);
-                        }
-                    }
-                }
-            }
-        }
-    } else if (warp == 12) {
-        // ---- loader: one 2-D tensor copy per pair slot ----
-        for (int J = 0; J < njobs; J++) {
-            const int it = int(unsigned(J) / unsigned(nvt));
-            const int vt = J - it * nvt;
-            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
-            const int64_t pin = rh ? bfs::recv_index(g * C::P, rh, rhg) : g * C::P;
-            for (int s = 0; s < C::P; s++) {
-                const int k = J * C::P + s, q = k % C::NQ;
-                if (k >= C::NQ) tc::mbar_wait(&slot_empty[q], uint32_t(k / C::NQ - 1) & 1);
-                if (lane == 0) {
-                    tc::mbar_arrive_expect_tx(&slot_full[q], C::SLOT);
-                    tc::tma_load_2d(sm_bh + q * C::SLOT, &tin, 2 * vt * 128, int((pin + s) * R), &slot_full[q]);
-                }
-                __syncwarp();
-            }
-        }
-    } else if (warp == 13) {
-        // ---- MMA issuer: one chain of 3 x (8r / 16) kind::f16 MMAs per job ----
-        constexpr uint32_t idesc = tc::idesc_f16(128, C::NB);
-        constexpr uint32_t LBO_B = (C::NB / 8) * 128;
-        const uint64_t dW = tc::desc_kmajor(tc::smem_u32(sm_bh + C::OFF_W), LBO_B);
-        for (int J = 0; J < njobs; J++) {
-            const int it = int(unsigned(J) / unsigned(nvt));
-            const int vt = J - it * nvt;
-            const int wb = it & 1, ab = J & 1, db = J & 1;
-            if (vt == 0) tc::mbar_wait(&w_full[wb], uint32_t(it >> 1) & 1);
-            tc::mbar_wait(&a_ready[ab], uint32_t(J >> 1) & 1);
-            if (J >= 2) tc::mbar_wait(&d_free[db], uint32_t((J >> 1) - 1) & 1);
-            tc::fence_after_sync();
-            const uint32_t d = tmem + uint32_t(C::D_OFF + db * C::NB);
-            const uint32_t ahi = tmem + uint32_t(ab * C::ACOLS);
-            const uint64_t bhi = tc::desc_add(dW, wb * C::WSET);
-#pragma unroll
-            for (int qq = 0; qq < 3; qq++) {
-                const int pass = kPassOrder[qq];
-                const uint32_t a = ahi + (pass == 1 ? C::KB / 2 : 0);
-                const uint64_t b = pass == 2 ? tc::desc_add(bhi, C::WT) : bhi;
-#pragma unroll
-                for (int ks = 0; ks < C::KB / 16; ks++)
-                    tc::mma_f16_ts_warp(d, a + ks * 8, tc::desc_add(b, ks * 2 * LBO_B), idesc, (qq | ks) ? 1u : 0u);
-            }
-            tc::commit_warp(&d_full[db]);
-            tc::commit_warp(&a_free[ab]);
-            if (vt == nvt - 1) tc::commit_warp(&w_free[wb]);
-            __syncwarp();
-        }
-    } else {
-        // ---- weights (warps 14-15): stage compact blocks (bulk, one group ahead), compose C in FP32 into
-        //      shared memory, take the group max, write the scaled FP16 hi / lo B tile ----
-        const int wt = tid - 448;
-        auto stage_group = [&](int it, int sb) {
-            const int64_t g = blockIdx.x + int64_t(it) * gridDim.x;
-            const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
-            uint8_t* dst = sm_bh + C::OFF_WST + sb * C::WST;
-            tc::mbar_arrive_expect_tx(&wst_full[sb], C::WST);
-            for (int b = 0; b < 8; b++) {
-                const int m = b >> 2, u = (b >> 1) & 1, e = b & 1;
-                const int64_t p = m == 0 ? ((((a0 << 1) + e) << (LN - lin - 1)) + (bq << 1) + u)
-                                         : ((((a0 << 2) + 2 * u + e) << shg) + bq);
-                tc::bulk_g2s(dst + b * C::BLK * 8, (m == 0 ? W1 : W2) + p * C::BLK, C::BLK * 8, &wst_full[sb]);
-            }
-        };
-        float2* Cs = reinterpret_cast<float2*>(sm_bh + C::OFF_CST);   // [o][t'][i][j]
-        if (wt == 0 && nit > 0) stage_group(0, 0);
-        for (int it = 0; it < nit; it++) {
-            const int wb = it & 1, sb = it & 1, gb = it & 3;
-            if (wt == 0 && it + 1 < nit) stage_group(it + 1, sb ^ 1);
-            tc::mbar_wait(&wst_full[sb], uint32_t(it >> 1) & 1);
-            const float2* st = reinterpret_cast<const float2*>(sm_bh + C::OFF_WST + sb * C::WST);
-            constexpr int H = R / 2;
-            float mx = 0.f;
-#pragma unroll 1
-            for (int item = wt; item < C::ITEMS; item += 64) {
-                const int jh = item & 1, r2 = item >> 1;
-                const int tp = r2 % R, oi = r2 / R, o = oi >> 2, i = oi & 3;
-                const int up = o >> 1, sp = i >> 1, s = i & 1;
-                const float2* L2 = st + (4 + o) * C::BLK + sp * R * R + tp;
-                const float2* L1 = st + (sp * 2 + up) * C::BLK + s * R * R + jh * H * R;
-                float2 c[H];
-#pragma unroll
-                for (int jj = 0; jj < H; jj++) c[jj] = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int jp = 0; jp < R; jp += 2) {
-                    const float2 wa = L2[jp * R], wb2 = L2[(jp + 1) * R];
-#pragma unroll
-                    for (int jj = 0; jj < H; jj++) {
-                        const float4 w1 = *reinterpret_cast<const float4*>(L1 + jj * R + jp);
-                        c[jj].x = fmaf(wa.x, w1.x, c[jj].x);
-                        c[jj].y = fmaf(wa.x, w1.y, c[jj].y);
-                        c[jj].x = fmaf(-wa.y, w1.y, c[jj].x);
-                        c[jj].y = fmaf(wa.y, w1.x, c[jj].y);
-                        c[jj].x = fmaf(wb2.x, w1.z, c[jj].x);
-                        c[jj].y = fmaf(wb2.x, w1.w, c[jj].y);
-                        c[jj].x = fmaf(-wb2.y, w1.w, c[jj].x);
-                        c[jj].y = fmaf(wb2.y, w1.z, c[jj].y);
-                    }
-                }
-#pragma unroll
-                for (int jj = 0; jj < H; jj++) {
-                    Cs[((o * R + tp) * 4 + i) * R + jh * H + jj] = c[jj];
-                    mx = fmaxf(mx, fmaxf(fabsf(c[jj].x), fabsf(c[jj].y)));
-                }
-            }
-            // group max over the 64 weight threads
-#pragma unroll
-            for (int m = 16; m > 0; m >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
-            if (lane == 0) red[wt >> 5] = mx;
-            asm volatile("bar.sync 1, 64;" ::: "memory");   // C and the two warp maxima are in shared memory
-            mx = fmaxf(red[0], red[1]);
-            int e = 0;
-            frexpf(mx, &e);
-            e = max(-126, min(126, e));
-            const float sc = ldexpf(1.f, -e);
-            if (it >= 2) tc::mbar_wait(&w_free[wb], uint32_t((it >> 1) - 1) & 1);
-            uint8_t* th = sm_bh + C::OFF_W + wb * C::WSET;
-            uint8_t* tl = th + C::WT;
-            // real embedding of C[o][t'][i][j] at rows n = o 2r + 2t' (+1), K columns k = i 2r + 2j (+1)
-            for (int idx = wt; idx < C::P * R * C::P * R; idx += 64) {
-                const int orow = idx / (C::P * R), icol = idx - orow * (C::P * R);   // (o, t'), (i, j)
-                const int o = orow / R, tp = orow - o * R, i = icol / R, j = icol - i * R;
-                const float2 cv = Cs[((o * R + tp) * 4 + i) * R + j];
-                float hr, hm, lr, lm;   // packed halves: (re, -im) for row n, (im, re) for row n + 1
-                tc::split_h2(cv.x * sc, -cv.y * sc, hr, lr);
-                tc::split_h2(cv.y * sc, cv.x * sc, hm, lm);
-                const int n = o * C::SC + 2 * tp, k = i * C::SC + 2 * j;
-                const uint32_t o0 = tc::kmaj_off16(n, k, C::NB), o1 = tc::kmaj_off16(n + 1, k, C::NB);
-                *reinterpret_cast<float*>(th + o0) = hr;
-                *reinterpret_cast<float*>(tl + o0) = lr;
-                *reinterpret_cast<float*>(th + o1) = hm;
-                *reinterpret_cast<float*>(tl + o1) = lm;
-            }
-            tc::fence_proxy_async();
-            tc::mbar_arrive(&w_full[wb]);
-            if (it >= 4) tc::mbar_wait(&g_empty[gb], uint32_t((it >> 2) - 1) & 1);
-            if (wt == 0) Eg[gb] = ldexpf(1.f, e);
-            tc::mbar_arrive(&g_full[gb]);
-            asm volatile("bar.sync 1, 64;" ::: "memory");   // staging buffer sb and Cs free for the next group
         }
     }
     tc::fence_before_sync();
@@ -2802,17 +1444,6 @@ static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, floa
     using C = BandTC<R>;
     const int64_t groups = d.N >> 2;
     const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
-    if (compose && bv.f16) {
-        using CH = BandH<R>;
-        auto kern = band_h16_kernel<R>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CH::SMEM));
-        if (e != cudaSuccess) return e;
-        CUtensorMap tin;
-        e = make_rows_tmap(&tin, in, d.N * R, nv, R);
-        if (e != cudaSuccess) return e;
-        kern<<<grid, 512, CH::SMEM, s>>>(tin, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
-        return cudaGetLastError();
-    }
     if (compose) {
         using CC = BandCmp<R>;
         auto kern = band_cmp_kernel<R>;
@@ -2824,26 +1455,11 @@ static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, floa
         kern<<<grid, 512, CC::SMEM, s>>>(tin, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
         return cudaGetLastError();
     }
-    if constexpr (Band2P<R>::FITS) {
-        if (bv.two_pipelines) {
-            auto kern = band_tc2p_kernel<R>;
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-            if (e != cudaSuccess) return e;
-            kern<<<grid, 512, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
-            return cudaGetLastError();
-        }
-    }
     auto kern = band_tc_kernel<R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
     kern<<<grid, 384, C::SMEM, s>>>(in, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
     return cudaGetLastError();
-}
-
-cudaError_t band_trace(long long* out, int n)
-{
-    if (n > BT_JOBS * BT_EV) n = BT_JOBS * BT_EV;
-    return cudaMemcpyFromSymbol(out, g_band_trace, size_t(n) * sizeof(long long));
 }
 
 bool band_tc_supported(const Dims& d, int nv)

@@ -9,7 +9,6 @@
 // Alo Blo term is <= 2^-22 |A||B| and the tf32 truncation of lo another ~2^-21, so
 // every product carries ~FP32-level relative error.
 #pragma once
-#include <cuda_fp16.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -60,50 +59,6 @@ __host__ __device__ constexpr uint64_t desc_add(uint64_t d, uint32_t bytes) { re
 __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n)
 {
     return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
-}
-
-// instruction descriptor, kind::f16 with FP16 operands: D f32 (bits 4-5 = 1), A f16 (7-9 = 0), B f16
-// (10-12 = 0), both K-major, N >> 3 at bit 17, M >> 4 at bit 24 (tools/tc_probe_f16.cu)
-__host__ __device__ constexpr uint32_t idesc_f16(int m, int n)
-{
-    return (1u << 4) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
-}
-// canonical K-major SWIZZLE_NONE offset of a 16-bit element: core matrices of 8 rows x 8 elements (16 B)
-__host__ __device__ constexpr uint32_t kmaj_off16(int row, int k, int rows)
-{
-    return uint32_t((k >> 3) * (rows >> 3) * 128 + (row >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
-}
-// A operand of kind::f16 in TMEM: one 32-bit column holds elements k = 2c (low half) and 2c + 1 (high half),
-// measured in tools/tc_probe_f16.cu
-__device__ __forceinline__ float pack_h2(float lo_elem, float hi_elem)
-{
-    const uint32_t u = uint32_t(__half_as_ushort(__float2half_rn(lo_elem))) |
-                       (uint32_t(__half_as_ushort(__float2half_rn(hi_elem))) << 16);
-    return __uint_as_float(u);
-}
-// FP16 split of a complex value (re, im), already scaled: hi = fp16 pair, lo = fp16 pair of the residuals,
-// both packed (re in the low half: K index 2j, im: 2j + 1) -- one pack conversion per part
-__device__ __forceinline__ void split_h2(float re, float im, float& hi, float& lo)
-{
-    const __half2 h = __floats2half2_rn(re, im);
-    const float2 hf = __half22float2(h);
-    const __half2 l = __floats2half2_rn(re - hf.x, im - hf.y);
-    hi = __uint_as_float(*reinterpret_cast<const uint32_t*>(&h));
-    lo = __uint_as_float(*reinterpret_cast<const uint32_t*>(&l));
-}
-// FP16 split of x (|x| <= 1 after the caller's power-of-two scaling): hi = fp16(x), lo = fp16(x - hi)
-__device__ __forceinline__ void split_h(float x, float& hi, float& lo)
-{
-    hi = __half2float(__float2half_rn(x));
-    lo = x - hi;
-}
-__device__ __forceinline__ void mma_f16_ts_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
-                                                uint32_t acc)
-{
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc)

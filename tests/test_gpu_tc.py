@@ -148,27 +148,6 @@ def test_tc_apply_host_pipelined(pieces):
         assert np.all(d <= PATHS_AGREE), d.max()
 
 
-def test_tc_band_two_pipeline_variant():
-    """The selectable two-TMEM-pipeline band kernel (BF_OPT_BAND_PIPELINES = 2) computes the same
-    result as the default single-pipeline kernel (same MMAs and order per job: bitwise)."""
-    LN, l0, r, nrhs = 14, 5, 10, 64          # two two-level bands (levels 6..9), nv = 128
-    F = W.rhs(1 << LN, nrhs, 31)
-    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
-    plan.set_option(bf.BF_OPT_BAND_COMPOSE, 0)       # the level-by-level kernels
-    with pytest.raises(bf.BFError):
-        plan.set_option(bf.BF_OPT_BAND_PIPELINES, 3)
-    G1 = _apply(plan, F)
-    plan.set_option(bf.BF_OPT_BAND_PIPELINES, 2)
-    try:
-        G2 = _apply(plan, F)
-    finally:
-        plan.set_option(bf.BF_OPT_BAND_PIPELINES, 1)
-    plan.destroy()
-    assert np.array_equal(G1, G2)
-    R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, :3])
-    assert np.all(oracle.rel_l2(G2[:, :3].astype(np.complex128), R, axis=0) <= PARITY)
-
-
 @pytest.mark.parametrize("r,l0,LN,nrhs", [(6, 6, 14, 64), (8, 5, 14, 96), (10, 6, 16, 256), (12, 5, 14, 70)])
 def test_tc_band_composed(r, l0, LN, nrhs):
     """Default band (BF_OPT_BAND_COMPOSE = 1): both levels of a band as one composed 4 x 4 block operator
@@ -191,74 +170,18 @@ def test_tc_band_composed(r, l0, LN, nrhs):
     assert not np.array_equal(Gc, Gl)                 # the composed kernel really ran
 
 
-@pytest.mark.parametrize("kernel,amp,LN,l0,r,nrhs", [(W.K_FIO, W.A_CFG1, 14, 6, 10, 128),
-                                                     (W.K_FIO_JUMP, W.A_CFG3, 12, 5, 16, 32),
-                                                     (W.K_DFT, W.A_ONE, 12, 6, 6, 70)])
-def test_tc_leaf_f16_vs_tf32(kernel, amp, LN, l0, r, nrhs):
-    """BF_OPT_LEAF_F16 = 1 (opt-in): S0 and SL in FP16 split passes with per-row / per-chunk power-of-two
-    scaling; 0 (default): 3xTF32.  Both meet the oracle bar and agree with each other like the two
-    FP32-accurate paths do."""
-    F = W.rhs(1 << LN, nrhs, 60 + r)
-    plan = bf.Plan.build_fio(bf.fio(kernel, amp, LN, l0, r), max_nrhs_chunk=nrhs)
-    assert plan.info()["f16_classes"] == []
-    plan.set_option(bf.BF_OPT_LEAF_F16, 1)
-    assert {"s0", "sl"} <= set(plan.info()["tc_classes"]) and set(plan.info()["f16_classes"]) == {"s0", "sl"}
-    bytes_f16 = plan.info()["tc_weight_bytes"]
-    G16 = _apply(plan, F)
-    plan.set_option(bf.BF_OPT_LEAF_F16, 0)
-    assert {"s0", "sl"} <= set(plan.info()["tc_classes"]) and plan.info()["tc_weight_bytes"] > bytes_f16
-    G32 = _apply(plan, F)
-    with pytest.raises(bf.BFError):
-        plan.set_option(bf.BF_OPT_LEAF_F16, 2)
-    plan.destroy()
-    cols = [0, nrhs - 1]
-    R = oracle.bf_apply(kernel, amp, LN, l0, r, F[:, cols])
-    for G in (G16, G32):
-        assert np.all(oracle.rel_l2(G[:, cols].astype(np.complex128), R, axis=0) <= PARITY)
-    d = oracle.rel_l2(G16.astype(np.complex128), G32.astype(np.complex128), axis=0)
-    assert np.all(d <= PATHS_AGREE), d.max()
-    assert not np.array_equal(G16, G32)
-
-
-@pytest.mark.parametrize("leaf_f16", [0, 1])
-def test_tc_scale_equivariance(leaf_f16):
-    """Both leaf precisions are exactly homogeneous under power-of-two scaling of F: 3xTF32 because every
-    rounding commutes with 2^k, the FP16 passes because they scale each vector by a power of two chosen from
-    its own values (no overflow at 2^60, no precision loss at 2^-60): G(2^k F) == 2^k G(F) bitwise."""
+def test_tc_scale_equivariance():
+    """The 3xTF32 path is exactly homogeneous under power-of-two scaling of F (every rounding, including the
+    tf32 hi/lo split, commutes with 2^k while nothing over- or underflows): G(2^k F) == 2^k G(F) bitwise."""
     LN, l0, r, nrhs = 12, 6, 10, 64
     F = W.rhs(1 << LN, nrhs, 9)
     plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
-    plan.set_option(bf.BF_OPT_LEAF_F16, leaf_f16)
     G = _apply(plan, F)
     for k in (60, -60):
         Gk = _apply(plan, np.asfortranarray(F * np.float32(2.0 ** k)).astype(np.complex64))
         assert np.all(np.isfinite(Gk))
         assert np.array_equal(Gk, (G * np.float32(2.0 ** k)).astype(np.complex64)), k
     plan.destroy()
-
-
-@pytest.mark.parametrize("r,l0,LN,nrhs", [(6, 6, 14, 64), (8, 5, 14, 96), (10, 6, 16, 256), (12, 5, 14, 70)])
-def test_tc_band_f16(r, l0, LN, nrhs):
-    """BF_OPT_BAND_F16 = 1 (per plan): the composed band in FP16 split passes with per-vector and
-    per-group power-of-two scaling.  Oracle bar, agreement with the 3xTF32 band, exact 2^k homogeneity."""
-    F = W.rhs(1 << LN, nrhs, 70 + r)
-    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
-    assert any(k.startswith("xfer") for k in plan.info()["tc_classes"])
-    G32 = _apply(plan, F)
-    plan.set_option(bf.BF_OPT_BAND_F16, 1)
-    try:
-        G16 = _apply(plan, F)
-        Gk = _apply(plan, np.asfortranarray(F * np.float32(2.0 ** -40)).astype(np.complex64))
-    finally:
-        plan.set_option(bf.BF_OPT_BAND_F16, 0)
-    plan.destroy()
-    cols = [0, nrhs - 1]
-    R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, cols])
-    assert np.all(oracle.rel_l2(G16[:, cols].astype(np.complex128), R, axis=0) <= PARITY)
-    d = oracle.rel_l2(G16.astype(np.complex128), G32.astype(np.complex128), axis=0)
-    assert np.all(d <= PATHS_AGREE), d.max()
-    assert not np.array_equal(G16, G32)
-    assert np.array_equal(Gk, (G16 * np.float32(2.0 ** -40)).astype(np.complex64))
 
 
 @pytest.mark.parametrize("LN,nrhs", [(14, 128), (14, 100), (12, 192), (16, 256)])
