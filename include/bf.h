@@ -220,6 +220,12 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        transfer level per launch).  Both compute every output with the same FP32 operation order
  *                        (bitwise equal). */
 #define BF_OPT_SMALL_BATCH 10
+/*   BF_OPT_BAND_PRECOMPOSE 1 (default): plans whose chunks hold at most 256 vectors compose each tensor-core
+ *                        band's two-level operator once at finalization (FP64 products, complex64 result, the
+ *                        same bytes as the two levels' blocks; counted in factor_bytes) and the band kernel only
+ *                        embeds and splits it; 0: the band composes on chip per group (the default for larger
+ *                        chunks, where each group's operator serves several vector tiles). */
+#define BF_OPT_BAND_PRECOMPOSE 11
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Wait for the plan's outstanding work (the last bf_apply enqueued outside a CUDA-graph capture; replays of a

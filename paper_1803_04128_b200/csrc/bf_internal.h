@@ -74,8 +74,15 @@ bool band_tc_supported(const Dims& d, int nv);
 struct BandVariant {
     bool compose = true;         // the composed two-level operator (band_cmp_kernel); else band_tc_kernel
 };
+// Cpre (optional): the band's operator precomposed at finalization (launch_compose_band) -- the kernel then
+// only embeds and splits it instead of composing it on chip per group (small vector batches).
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, const BandVariant& bv);
+                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, const BandVariant& bv,
+                           const float2* Cpre = nullptr);
+// Plan finalization: the composed two-level operator of the band starting at l_first, 16 r^2 complex per group
+// of 4 pairs (FP64 products, complex64 result).
+cudaError_t launch_compose_band(const Dims& d, int l_first, const float2* W1, const float2* W2, float2* Cg,
+                                cudaStream_t s);
 
 
 // Plan finalization: W[p] <- Sw[p] W[p] for npairs blocks (W column-major R x cols, Sw R x R).

@@ -128,6 +128,7 @@ struct Shard {
     float2* sw = nullptr;
     float2* u = nullptr;
     std::vector<float2*> xfer;
+    std::vector<float2*> cmp;  // [level index of a band's first level]: precomposed two-level operator, or null
     float* v0x = nullptr;      // tensor-core image of V0 / U (bf_tc.cu), built at finalize when used
     float* ux = nullptr;
     float2* ws = nullptr;      // two coefficient arrays of (N/G) R nv_max
@@ -160,6 +161,7 @@ struct bf_plan_s {
     int host_pieces = 2;       // BF_OPT_HOST_PIECES: bf_apply_host pipeline pieces per chunk
     bool leaf_multicast = true;  // BF_OPT_LEAF_MULTICAST: TF32 S0 / SL as 2-CTA clusters sharing the weight stream
     bool small_batch = true;      // BF_OPT_SMALL_BATCH: fused bands for small vector batches (bf_small.cu)
+    bool precompose = true;      // BF_OPT_BAND_PRECOMPOSE: use the finalize-time composed band operators
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -278,6 +280,7 @@ void free_plan(bf_plan_s* p)
         cudaFree(s.ux);
         cudaFree(s.u);
         for (auto x : s.xfer) cudaFree(x);
+        for (auto x : s.cmp) cudaFree(x);
         cudaFree(s.ws);
     }
     cudaFree(p->dF);
@@ -434,7 +437,8 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                 const float2* W[2] = {sh.xfer[stp.l_first - p->d.l0 - 1],
                                       stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
                 if (stp.K == 2 && p->tensor_cores && bfk::band_tc_supported(dl, nv))
-                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po, p->band);
+                    return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po, p->band,
+                                               p->precompose ? sh.cmp[stp.l_first - p->d.l0 - 1] : nullptr);
                 if (p->small_batch && bfk::band_sv_supported(dl, nv))
                     return bfk::launch_band_sv(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
                 return bfk::launch_band(dl, lk, stp.K, in, out, W, nv, s, rh, rhg, po);
@@ -623,6 +627,7 @@ bf_status_t alloc_plan(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk
     p->ws_bytes = size_t(2) * size_t(n * r) * size_t(nv) * sizeof(float2);
     for (auto& s : p->sh) {
         s.xfer.assign(nx, nullptr);
+        s.cmp.assign(nx, nullptr);
         if ((st = dalloc(&s.amp_a, p->d.n_amp * n, "amp_a")) || (st = dalloc(&s.amp_b, p->d.n_amp * n, "amp_b")) ||
             (st = dalloc(&s.v0, n * r * n0, "v0")) || (st = dalloc(&s.sw, n * r * r, "sw")) ||
             (st = dalloc(&s.u, n * r * n0, "u")) ||
@@ -814,6 +819,32 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
             if (bf_status_t st = build_leaf_images(p, s); st != BF_OK) return st;
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e, "leaf weight expansion");
+    }
+    // small vector batches (<= 2 tiles of 128 vectors per chunk): precompose every tensor-core band's two-level
+    // operator once (FP64 products), so the band kernel only embeds and splits it per group instead of
+    // composing it on chip -- with one vector tile per group the on-chip compose was the band's critical path
+    // (ncu: weight warps' compose loop; 0.41 of HBM at nv = 64).  Same bytes per group as the compact blocks.
+    {
+        const int nvf = int(p->max_chunk * p->d.n_amp);
+        if (p->tensor_cores && nvf <= 256 && bfk::band_tc_supported(dl, nvf)) {
+            for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE, p->small_batch)) {
+                if (stp.kind != Step::BAND || stp.K != 2) continue;
+                const int li = stp.l_first - p->d.l0 - 1;
+                const int lk = (stp.l_first > p->d.h) ? stp.l_first - p->g : stp.l_first;
+                for (Shard& s : p->sh) {
+                    if (s.cmp[li]) continue;
+                    if (cudaMalloc(&s.cmp[li], size_t(p->nloc()) * 4 * p->d.R * p->d.R * sizeof(float2)) != cudaSuccess) {
+                        cudaGetLastError();   // no memory: that band composes on chip
+                        s.cmp[li] = nullptr;
+                        continue;
+                    }
+                    e = bfk::launch_compose_band(dl, lk, s.xfer[li], s.xfer[li + 1], s.cmp[li], 0);
+                    if (e != cudaSuccess) return cuda_fail(e, "band precompose");
+                }
+            }
+            e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) return cuda_fail(e, "band precompose");
+        }
     }
     p->finalized = true;
     return BF_OK;
@@ -1013,6 +1044,9 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     // the switch blocks are folded into the level-h factor at finalize (freed afterwards)
     info->factor_bytes = nsh * 8 * (2 * p->d.n_amp * n + 2 * n * r * n0 + (p->finalized ? 0 : n * r * r) +
                                     int64_t(nx) * n * 2 * r * r);
+    for (const Shard& s : p->sh)
+        for (auto c : s.cmp)
+            if (c) info->factor_bytes += 8 * n * 4 * r * r;   // precomposed band operators
     info->workspace_bytes = nsh * int64_t(p->ws_bytes);
     info->tc_weight_bytes = 0;
     for (const Shard& s : p->sh) {
@@ -1128,6 +1162,11 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
     if (option == BF_OPT_LEAF_MULTICAST) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_LEAF_MULTICAST takes 0 or 1");
         p->leaf_multicast = value != 0;
+        return BF_OK;
+    }
+    if (option == BF_OPT_BAND_PRECOMPOSE) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND_PRECOMPOSE takes 0 or 1");
+        p->precompose = value != 0;
         return BF_OK;
     }
     if (option == BF_OPT_SMALL_BATCH) {

@@ -1126,7 +1126,9 @@ __global__ void __launch_bounds__(384, 1)
 // Warps: 0-3 split the raw rows into A (TMEM), 4-11 epilogue (lane quadrant warp % 4, output half
 // (warp - 4) / 4), 12 loader, 13 MMA issuer, 14-15 weights (compose one group ahead).
 // =============================================================================================
-template <int R>
+// NS = weight staging depth (groups in flight).  4 instead of 2 for one-tile chunks (nv <= 128) was measured
+// slower (nv = 64: 5.6 vs 4.7 ms per band at cfg4; the raw ring it displaces matters more), so 2 is used.
+template <int R, int NS = 2>
 struct BandCmp {
     static constexpr int P = 4;
     static constexpr int SC = 2 * R;                                  // real columns of one pair slot
@@ -1143,16 +1145,16 @@ struct BandCmp {
     static constexpr uint32_t WT = uint32_t(NB) * KB * 4;             // one B tile (hi or lo)
     static constexpr uint32_t WSET = 2 * WT;
     static constexpr size_t LIM = 232448 - 1024;
-    static constexpr int NWBUF = (8 * size_t(SLOT) + 2 * size_t(WST) + 2 * size_t(WSET) <= LIM) ? 2 : 1;
+    static constexpr int NWBUF = (8 * size_t(SLOT) + NS * size_t(WST) + 2 * size_t(WSET) <= LIM) ? 2 : 1;
     // raw ring of single-pair slots (freed one pair at a time, so more bytes stay in flight)
-    static constexpr int NQ_FIT = int((LIM - 2 * size_t(WST) - NWBUF * size_t(WSET)) / SLOT);
+    static constexpr int NQ_FIT = int((LIM - NS * size_t(WST) - NWBUF * size_t(WSET)) / SLOT);
 #ifdef BF_BAND_NQ
     static constexpr int NQ = NQ_FIT > BF_BAND_NQ ? BF_BAND_NQ : NQ_FIT;
 #else
     static constexpr int NQ = NQ_FIT > 16 ? 16 : NQ_FIT;
 #endif
-    static constexpr uint32_t OFF_WST = uint32_t(NQ) * SLOT;          // two staging buffers (prefetch)
-    static constexpr uint32_t OFF_W = OFF_WST + 2 * WST;
+    static constexpr uint32_t OFF_WST = uint32_t(NQ) * SLOT;          // NS staging buffers (prefetch)
+    static constexpr uint32_t OFF_W = OFF_WST + NS * WST;
     static constexpr size_t SMEM = size_t(OFF_W) + NWBUF * size_t(WSET);
     static constexpr int ITEMS = P * P * R * 2;                       // (o, i, t', j half) compose items
 #ifdef BF_BAND_SPLIT4
@@ -1160,20 +1162,21 @@ struct BandCmp {
 #else
     static constexpr int NSPLIT = 8;
 #endif
-    static_assert(KB % 16 == 0 && D_OFF + NDBUF * NB <= 512 && OFF_W % 128 == 0 && WT % 128 == 0 && NQ >= 8 &&
-                      SMEM <= LIM, "composed band shape");
+    static_assert(KB % 16 == 0 && D_OFF + NDBUF * NB <= 512 && OFF_W % 128 == 0 && WT % 128 == 0 &&
+                      NQ >= (NS > 2 ? 6 : 8) && SMEM <= LIM, "composed band shape");
 };
 
-template <int R>
+template <int R, int NS>
 __global__ void __launch_bounds__(512, 1)
     band_cmp_kernel(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ W1,
-                    const float2* __restrict__ W2, int LN, int l_first, int nv, int rh, int rhg, const bfs::PeerOut po)
+                    const float2* __restrict__ W2, const float2* __restrict__ Cpre, int LN, int l_first, int nv, int rh,
+                    int rhg, const bfs::PeerOut po)
 {
-    using C = BandCmp<R>;
+    using C = BandCmp<R, NS>;
     extern __shared__ __align__(128) uint8_t sm_cmp[];
     __shared__ uint64_t slot_full[16], slot_empty[16];
     __shared__ uint64_t a_ready[2], a_free[2], d_full[2], d_free[2], w_full[2], w_free[2];
-    __shared__ uint64_t wst_full[2];
+    __shared__ uint64_t wst_full[NS];
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1197,8 +1200,8 @@ __global__ void __launch_bounds__(512, 1)
             tc::mbar_init(&d_free[i], 32 * (12 - C::NSPLIT));
             tc::mbar_init(&w_full[i], 64);
             tc::mbar_init(&w_free[i], 1);
-            tc::mbar_init(&wst_full[i], 1);
         }
+        for (int i = 0; i < NS; i++) tc::mbar_init(&wst_full[i], 1);
         tc::mbar_fence_init();
     }
     tc::fence_before_sync();
@@ -1360,6 +1363,10 @@ __global__ void __launch_bounds__(512, 1)
             const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
             uint8_t* dst = sm_cmp + C::OFF_WST + sb * C::WST;
             tc::mbar_arrive_expect_tx(&wst_full[sb], C::WST);
+            if (Cpre) {   // the group's precomposed operator (16 r^2 complex = the bytes of its 8 compact blocks)
+                tc::bulk_g2s(dst, Cpre + g * (C::WST / 8), C::WST, &wst_full[sb]);
+                return;
+            }
             for (int b = 0; b < 8; b++) {
                 const int m = b >> 2, u = (b >> 1) & 1, e = b & 1;
                 const int64_t p = m == 0 ? ((((a0 << 1) + e) << (LN - lin - 1)) + (bq << 1) + u)
@@ -1367,15 +1374,50 @@ __global__ void __launch_bounds__(512, 1)
                 tc::bulk_g2s(dst + b * C::BLK * 8, (m == 0 ? W1 : W2) + p * C::BLK, C::BLK * 8, &wst_full[sb]);
             }
         };
-        if (wt == 0 && nit > 0) stage_group(0, 0);
+        if (wt == 0)
+            for (int q = 0; q < NS - 1 && q < nit; q++) stage_group(q, q);
         for (int it = 0; it < nit; it++) {
-            const int wb = it % C::NWBUF, sb = it & 1;
-            if (wt == 0 && it + 1 < nit) stage_group(it + 1, sb ^ 1);   // its buffer was released by the bar.sync
-            tc::mbar_wait(&wst_full[sb], uint32_t(it >> 1) & 1);
+            const int wb = it % C::NWBUF, sb = it % NS;
+            // group it + NS - 1 into the buffer of group it - 1 (released by the bar.sync that ended it - 1)
+            if (wt == 0 && it + NS - 1 < nit) stage_group(it + NS - 1, (it + NS - 1) % NS);
+            tc::mbar_wait(&wst_full[sb], uint32_t(it / NS) & 1);
             const float2* st = reinterpret_cast<const float2*>(sm_cmp + C::OFF_WST + sb * C::WST);
             if (it >= C::NWBUF) tc::mbar_wait(&w_free[wb], uint32_t(it / C::NWBUF - 1) & 1);
             uint8_t* th = sm_cmp + C::OFF_W + wb * C::WSET;
             uint8_t* tl = th + C::WT;
+            if (Cpre) {
+                // precomposed C[o][i](t', j) (layout [o][i][t'][j], bf_plan finalize): embed + split only.  A thread
+                // takes whole rows (o, i, t') -- r contiguous complex, 16-byte loads -- and writes the 2 x 2 real
+                // blocks [[re, -im], [im, re]] of its row at offsets that are compile-time steps from one base
+                // (rows n = o 2r + 2t', n + 1; columns k = i 2r + 2j, k + 1; i 2r = 0 mod 4 for even r).  Item
+                // order (one complex per thread, as in the compose loop) spent ~3x the instructions on index math;
+                // store orders with fewer bank conflicts cost selects or a second split per complex and measured
+                // slower (the fill is issue-bound on the two weight warps, not bound by shared-memory wavefronts).
+                constexpr uint32_t KSTEP = (C::NB / 8) * 128;   // bytes between K-adjacent core matrices
+#pragma unroll 1
+                for (int row = wt; row < 16 * R; row += 64) {
+                    const int tp = row % R, oi = row / R, o = oi >> 2, i = oi & 3;
+                    const int n = o * C::SC + 2 * tp;
+                    const uint32_t base = tc::kmaj_off(n, i * C::SC, C::NB);
+                    const float2* src = st + row * R;
+#pragma unroll
+                    for (int j2 = 0; j2 < R; j2 += 2) {
+                        const float4 cc = *reinterpret_cast<const float4*>(src + j2);
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            const float re = h ? cc.z : cc.x, im = h ? cc.w : cc.y;
+                            float hr, lr, hi_, li;
+                            tc::split(re, hr, lr);
+                            tc::split(im, hi_, li);
+                            const uint32_t off = base + uint32_t(j2 >> 1) * KSTEP + uint32_t(h) * 8;
+                            *reinterpret_cast<float2*>(th + off) = make_float2(hr, -hi_);
+                            *reinterpret_cast<float2*>(tl + off) = make_float2(lr, -li);
+                            *reinterpret_cast<float2*>(th + off + 16) = make_float2(hi_, hr);
+                            *reinterpret_cast<float2*>(tl + off + 16) = make_float2(li, lr);
+                        }
+                    }
+                }
+            } else {
             // item = (o, i, t', half of j): R / 2 independent complex accumulators per thread (ILP), the
             // L1 row pairs (j, j'), (j, j' + 1) as one 16-byte load
             constexpr int H = R / 2;
@@ -1423,9 +1465,10 @@ __global__ void __launch_bounds__(512, 1)
                     *reinterpret_cast<float2*>(tl + o1) = make_float2(li, lr);
                 }
             }
+            }
             tc::fence_proxy_async();
             tc::mbar_arrive(&w_full[wb]);
-            asm volatile("bar.sync 1, 64;" ::: "memory");   // staging buffer sb free for group it + 2
+            asm volatile("bar.sync 1, 64;" ::: "memory");   // staging buffer sb free for group it + NS
         }
     }
     tc::fence_before_sync();
@@ -1438,21 +1481,23 @@ __global__ void __launch_bounds__(512, 1)
 
 template <int R>
 static cudaError_t band_tc_go(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                              cudaStream_t s, int rh, int rhg, const bfs::PeerOut& po, const BandVariant& bv)
+                              cudaStream_t s, int rh, int rhg, const bfs::PeerOut& po, const BandVariant& bv,
+                              const float2* Cpre)
 {
     const bool compose = bv.compose;
     using C = BandTC<R>;
     const int64_t groups = d.N >> 2;
     const unsigned grid = unsigned(groups < sm_count() ? groups : sm_count());
     if (compose) {
-        using CC = BandCmp<R>;
-        auto kern = band_cmp_kernel<R>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CC::SMEM));
+        using CC = BandCmp<R, 2>;
+        auto kern = band_cmp_kernel<R, 2>;
+        const size_t smem = CC::SMEM;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
         CUtensorMap tin;
         e = make_rows_tmap(&tin, in, d.N * R, nv, R);
         if (e != cudaSuccess) return e;
-        kern<<<grid, 512, CC::SMEM, s>>>(tin, out, W[0], W[1], d.LN, l_first, nv, rh, rhg, po);
+        kern<<<grid, 512, smem, s>>>(tin, out, W[0], W[1], Cpre, d.LN, l_first, nv, rh, rhg, po);
         return cudaGetLastError();
     }
     auto kern = band_tc_kernel<R>;
@@ -1468,16 +1513,58 @@ bool band_tc_supported(const Dims& d, int nv)
 }
 
 cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2* out, const float2* const* W, int nv,
-                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, const BandVariant& bv)
+                           cudaStream_t s, int rh, int rhg, const bfs::PeerOut* po, const BandVariant& bv,
+                           const float2* Cpre)
 {
     const bfs::PeerOut pz = po ? *po : bfs::PeerOut{};
     switch (d.R) {
-    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv);
-    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv);
-    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv);
-    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv);
+    case 6: return band_tc_go<6>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv, Cpre);
+    case 8: return band_tc_go<8>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv, Cpre);
+    case 10: return band_tc_go<10>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv, Cpre);
+    case 12: return band_tc_go<12>(d, l_first, in, out, W, nv, s, rh, rhg, pz, bv, Cpre);
     default: return cudaErrorInvalidValue;
     }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Plan finalization for small vector batches: the composed operator of a two-level band, per group g
+// (fixed a0 at the input level l_first - 1, 4 consecutive b) and block path (o, i):
+//     C_g[o][i](t', j) = sum_{j'} W2[p2(o)](t', (i >> 1) r + j') W1[p1(i >> 1, o >> 1)](j', (i & 1) r + j)
+// with p1(u, e) = (((2 a0 + e) << (LN - l_first)) + 2 bq + u, p2(o) = ((4 a0 + o) << shg) + bq -- the algebra
+// the band kernel otherwise forms on chip per group (band_cmp_kernel), here once in FP64 and rounded to
+// complex64.  Layout [g][o][i][t'][j]: 16 r^2 complex per group, the bytes of the group's 8 compact blocks.
+// ---------------------------------------------------------------------------------------------
+__global__ void compose_band_kernel(const float2* __restrict__ W1, const float2* __restrict__ W2, float2* __restrict__ Cg,
+                                    int LN, int l_first, int R)
+{
+    const int64_t N = int64_t(1) << LN;
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t per = int64_t(16) * R * R;
+    if (idx >= (N >> 2) * per) return;
+    const int64_t g = idx / per;
+    const int r = int(idx % per), j = r % R, tp = (r / R) % R, oi = r / (R * R), o = oi >> 2, i = oi & 3;
+    const int lin = l_first - 1, shg = LN - lin - 2;
+    const int64_t a0 = g >> shg, bq = g & ((int64_t(1) << shg) - 1);
+    const int sp = i >> 1, sv = i & 1, up = o >> 1;
+    const int64_t p1 = ((((a0 << 1) + up) << (LN - lin - 1)) + (bq << 1) + sp);
+    const int64_t p2 = ((((a0 << 2) + o) << shg) + bq);
+    const float2* w2 = W2 + p2 * 2 * R * R;   // column-major r x 2r
+    const float2* w1 = W1 + p1 * 2 * R * R;
+    double cr = 0, ci = 0;
+    for (int jp = 0; jp < R; jp++) {
+        const float2 a = w2[(sp * R + jp) * R + tp], b = w1[(sv * R + j) * R + jp];
+        cr += double(a.x) * b.x - double(a.y) * b.y;
+        ci += double(a.x) * b.y + double(a.y) * b.x;
+    }
+    Cg[idx] = make_float2(float(cr), float(ci));
+}
+
+cudaError_t launch_compose_band(const Dims& d, int l_first, const float2* W1, const float2* W2, float2* Cg,
+                                cudaStream_t s)
+{
+    const int64_t n = (d.N >> 2) * 16 * d.R * d.R;
+    compose_band_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(W1, W2, Cg, d.LN, l_first, d.R);
+    return cudaGetLastError();
 }
 
 }  // namespace bfk

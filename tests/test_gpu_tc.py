@@ -248,19 +248,52 @@ def test_rhs_shards_concatenate_to_one_gpu(world):
     k = bf.fio(W.K_FIO, W.A_CFG1, 14, 6, 10)   # cfg4's shape at N = 2^14
     nrhs = 256
     F = W.rhs(1 << 14, nrhs, 3)
-    full = bf.Plan.build_fio(k, max_nrhs_chunk=nrhs)
-    ref, tc_full = _apply(full, F), set(full.info()["tc_classes"])
-    full.destroy()
-    blocks, same = [], True
-    for q in range(world):
-        c0, c1 = bench.rhs_columns(nrhs, world, q)
-        p = bf.Plan.build_fio(k, max_nrhs_chunk=c1 - c0)
-        same &= set(p.info()["tc_classes"]) == tc_full
-        blocks.append(_apply(p, np.asfortranarray(F[:, c0:c1])))
-        p.destroy()
-    G = np.concatenate(blocks, axis=1)
-    if same:
-        assert np.array_equal(G, ref)
-    else:
-        err = oracle.rel_l2(G.astype(np.complex128), ref.astype(np.complex128), axis=0)
-        assert np.all(err <= PATHS_AGREE), err.max()
+    for pre in (0, 1):   # 0: every plan composes its bands on chip (kernel choice independent of the chunk)
+        full = bf.Plan.build_fio(k, max_nrhs_chunk=nrhs)
+        full.set_option(bf.BF_OPT_BAND_PRECOMPOSE, pre)
+        ref, tc_full = _apply(full, F), set(full.info()["tc_classes"])
+        full.destroy()
+        blocks, same = [], True
+        for q in range(world):
+            c0, c1 = bench.rhs_columns(nrhs, world, q)
+            p = bf.Plan.build_fio(k, max_nrhs_chunk=c1 - c0)
+            p.set_option(bf.BF_OPT_BAND_PRECOMPOSE, pre)
+            same &= set(p.info()["tc_classes"]) == tc_full
+            blocks.append(_apply(p, np.asfortranarray(F[:, c0:c1])))
+            p.destroy()
+        G = np.concatenate(blocks, axis=1)
+        if same and not pre:
+            assert np.array_equal(G, ref)
+        else:
+            err = oracle.rel_l2(G.astype(np.complex128), ref.astype(np.complex128), axis=0)
+            assert np.all(err <= PATHS_AGREE), err.max()
+
+
+@pytest.mark.parametrize("r,l0,LN,nrhs", [(10, 6, 16, 32), (8, 5, 14, 64), (12, 5, 14, 48), (6, 6, 14, 100)])
+def test_tc_band_precomposed(r, l0, LN, nrhs):
+    """Plans of <= 256 vectors per chunk compose each band's two-level operator at finalization (FP64) and the
+    band kernel only embeds and splits it (BF_OPT_BAND_PRECOMPOSE = 1, default); 0 composes on chip in FP32.
+    Both meet the oracle bar and agree like two FP32-accurate paths; the precomposed operators are counted in
+    factor_bytes (16 r^2 complex per group of 4 pairs: the bytes of the two levels' blocks)."""
+    F = W.rhs(1 << LN, nrhs, 80 + r)
+    k = bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r)
+    plan = bf.Plan.build_fio(k, max_nrhs_chunk=nrhs)
+    info = plan.info()
+    assert any(c.startswith("xfer") for c in info["tc_classes"])
+    bands = (LN - 2 * l0) // 2
+    base = bf.Plan.build_fio(k, max_nrhs_chunk=300)       # > 256 vectors: no precomposed operators
+    assert info["factor_bytes"] - base.info()["factor_bytes"] == bands * 8 * (1 << LN) * 4 * r * r
+    base.destroy()
+    Gp = _apply(plan, F)
+    plan.set_option(bf.BF_OPT_BAND_PRECOMPOSE, 0)
+    Gc = _apply(plan, F)
+    with pytest.raises(bf.BFError):
+        plan.set_option(bf.BF_OPT_BAND_PRECOMPOSE, 2)
+    plan.destroy()
+    cols = [0, nrhs - 1]
+    R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, cols])
+    for G in (Gp, Gc):
+        assert np.all(oracle.rel_l2(G[:, cols].astype(np.complex128), R, axis=0) <= PARITY)
+    d = oracle.rel_l2(Gp.astype(np.complex128), Gc.astype(np.complex128), axis=0)
+    assert np.all(d <= PATHS_AGREE), d.max()
+    assert not np.array_equal(Gp, Gc)
