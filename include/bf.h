@@ -231,7 +231,10 @@ bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 /* Wait for the plan's outstanding work (the last bf_apply enqueued outside a CUDA-graph capture; replays of a
  * graph that captured bf_apply must be synchronized by the caller), then free everything it owns.
  * bf_apply / bf_apply_ex only enqueue work (no allocation, no host synchronization), so they can be captured
- * into a CUDA graph (tests/test_gpu_tc.py::test_cuda_graph_capture). */
+ * into a CUDA graph (tests/test_gpu_tc.py::test_cuda_graph_capture).  Index-sharded (NCCL) plans: this wait and
+ * the one inside bf_apply_host poll the communicator; an asynchronous NCCL error, or no progress within
+ * BF_NCCL_TIMEOUT_S seconds (default 300), aborts the communicator and returns BF_ERR_NCCL (bf_apply also returns
+ * BF_ERR_NCCL when an asynchronous error is already pending). */
 bf_status_t bf_plan_destroy(bf_plan_t plan);
 
 /* ---- index-sharded plans: one long vector split by index over world = 2^g ranks ----

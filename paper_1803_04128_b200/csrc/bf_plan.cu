@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <utility>
 #include <vector>
@@ -72,6 +73,7 @@ struct Nccl {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -96,6 +98,7 @@ Nccl& nccl()
     BF_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
     BF_NCCL_SYM(CommInitRank, "ncclCommInitRank");
     BF_NCCL_SYM(CommDestroy, "ncclCommDestroy");
+    BF_NCCL_SYM(CommAbort, "ncclCommAbort");
     BF_NCCL_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
     BF_NCCL_SYM(Send, "ncclSend");
     BF_NCCL_SYM(Recv, "ncclRecv");
@@ -104,13 +107,24 @@ Nccl& nccl()
     BF_NCCL_SYM(GetErrorString, "ncclGetErrorString");
 #undef BF_NCCL_SYM
     n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Send && n.Recv && n.GroupStart && n.GroupEnd &&
-           n.GetErrorString && n.CommGetAsyncError;
+           n.GetErrorString && n.CommGetAsyncError && n.CommAbort;
     return n;
 }
 
 bf_status_t nccl_fail(ncclResult_t r, const char* what)
 {
     return fail(BF_ERR_NCCL, "%s: NCCL error %d (%s)", what, r, nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+}
+
+// Seconds a synchronizing call waits for NCCL work before aborting the communicator (BF_NCCL_TIMEOUT_S, default 300).
+double nccl_timeout_s()
+{
+    static const double t = [] {
+        const char* e = getenv("BF_NCCL_TIMEOUT_S");
+        const double v = e ? atof(e) : 0.0;
+        return v > 0 ? v : 300.0;
+    }();
+    return t;
 }
 
 }  // namespace
@@ -530,11 +544,55 @@ bf_status_t apply_chunk_peer(bf_plan_s* p, const std::vector<Step>& st, size_t e
     return BF_OK;
 }
 
+// NCCL plans: an asynchronous communicator error (a peer died, a network fault) is reported instead of
+// enqueueing more collectives on a broken communicator.
+bf_status_t nccl_check(bf_plan_s* p)
+{
+    if (p->mode != BF_SHARD_NCCL || !p->comm) return BF_OK;
+    ncclResult_t r = 0;
+    const ncclResult_t q = nccl().CommGetAsyncError(p->comm, &r);
+    if (q) return nccl_fail(q, "ncclCommGetAsyncError");
+    if (r) return nccl_fail(r, "NCCL asynchronous error");
+    return BF_OK;
+}
+
+// Wait for `ev` (work enqueued on the plan's stream).  For NCCL plans the wait polls the communicator: an
+// asynchronous error or no progress within nccl_timeout_s() aborts it (the peers' collectives then fail
+// instead of hanging) and returns BF_ERR_NCCL.
+bf_status_t wait_event_nccl(bf_plan_s* p, cudaEvent_t ev)
+{
+    if (p->mode != BF_SHARD_NCCL || !p->comm || p->world == 1) {
+        const cudaError_t e = cudaEventSynchronize(ev);
+        return e == cudaSuccess ? BF_OK : cuda_fail(e, "synchronize");
+    }
+    struct timespec ts0;
+    clock_gettime(CLOCK_MONOTONIC, &ts0);
+    for (;;) {
+        const cudaError_t e = cudaEventQuery(ev);
+        if (e == cudaSuccess) return BF_OK;
+        if (e != cudaErrorNotReady) return cuda_fail(e, "synchronize");
+        bf_status_t st = nccl_check(p);
+        struct timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        const double dt = double(ts.tv_sec - ts0.tv_sec) + 1e-9 * double(ts.tv_nsec - ts0.tv_nsec);
+        if (st == BF_OK && dt > nccl_timeout_s())
+            st = fail(BF_ERR_NCCL, "NCCL exchange made no progress for %.0f s (BF_NCCL_TIMEOUT_S)", dt);
+        if (st != BF_OK) {
+            nccl().CommAbort(p->comm);
+            p->comm = nullptr;
+            return st;
+        }
+        struct timespec nap = {0, 100000};
+        nanosleep(&nap, nullptr);
+    }
+}
+
 bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, int64_t ldg, int64_t nrhs, float2* ws0,
                        cudaStream_t s)
 {
     const int64_t chunk = p->max_chunk;
     const bool sharded = p->mode != BF_SHARD_NONE;
+    if (bf_status_t st = nccl_check(p); st != BF_OK) return st;
     const int nsh = int(p->sh.size());
     std::vector<float2*> ws(nsh);
     for (int i = 0; i < nsh; i++) ws[i] = (i == 0) ? ws0 : p->sh[i].ws;
@@ -1019,6 +1077,8 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
         }
         cudaEventRecord(E[2], p->d2h);
     }
+    // the apply stream (with its NCCL exchanges) first, polled for communicator errors on sharded plans
+    if (st == BF_OK && npieces > 0) st = wait_event_nccl(p, ev[3 * size_t(npieces - 1) + 1]);
     cudaError_t e1 = cudaStreamSynchronize(p->h2d), e2 = cudaStreamSynchronize(p->d2h), e3 = cudaStreamSynchronize(s);
     cleanup();
     if (st != BF_OK) return st;
@@ -1228,14 +1288,13 @@ bf_status_t bf_plan_timing(bf_plan_t p, double* ms, int64_t* launches)
 bf_status_t bf_plan_destroy(bf_plan_t p)
 {
     if (!p) return BF_OK;
-    cudaError_t e = cudaSuccess;
+    bf_status_t st = BF_OK;
     {
         DeviceGuard g(p->device);
-        if (p->done) e = cudaEventSynchronize(p->done);
+        if (p->done) st = wait_event_nccl(p, p->done);
     }
     free_plan(p);
-    if (e != cudaSuccess) return cuda_fail(e, "outstanding work failed");
-    return BF_OK;
+    return st;
 }
 
 bf_status_t bf_shard_pairs(int32_t log2n, int32_t log2leaf, int32_t world, int32_t rank, int32_t which, int64_t* out)

@@ -58,6 +58,19 @@ def _worker(rank, world, port, q):
             a_r = got >> h
             assert np.all(a_r >> (h - g) == rank), "after the exchange a rank holds the pairs of its x-rows"
             assert np.array_equal(np.sort(got), second)
+            # the same exchange moving whole coefficient blocks (r rows x nv vectors per pair, as the level-h
+            # launch writes them in send order), checked word for word against the receive layout the
+            # second-half kernel reads (bfs::recv_index, exported as bf_shard_pairs(which = 1))
+            if LN <= 16:
+                R, nv = 4, 3
+                t = np.arange(R)[:, None]
+                v = np.arange(nv)[None, :]
+                blocks = (send[:, None, None] << 16) | (t << 8) | v          # content names (pair, row, vector)
+                out = torch.empty(blocks.size, dtype=torch.int64)
+                dist.all_to_all_single(out, torch.from_numpy(np.ascontiguousarray(blocks).ravel()))
+                recv = out.numpy().reshape(-1, R, nv)
+                expect = (recv_expect[:, None, None] << 16) | (t << 8) | v
+                assert np.array_equal(recv, expect), "received blocks == receive layout, word for word"
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
