@@ -154,18 +154,28 @@ def _self_launch(args) -> int:
     return subprocess.call(cmd)
 
 
-def cpu_oracle_sample(w):
-    """The oracle as it stands on the host cores: cfg4's full-N butterfly for ONE RHS column
-    (its 2 amplitude vectors), blocks generated on the fly in FP64."""
+def cpu_oracle_sample(w, g0=None):
+    """The oracle as it stands on the host cores: the config's full-N butterfly for ONE RHS column (its n_amp
+    vectors), blocks generated on the fly in FP64 -- timed -- and, untimed, the accuracy triplet of that column
+    on the eps^b row sample: oracle BF vs the direct sum (eps^b), the GPU column g0 vs the direct
+    sum, and the GPU column vs the oracle BF on all N rows (the parity quantity, bar 1e-5)."""
     import oracle
     F = W.rhs(w.n, w.nrhs, w.seed, cols=[0])
     t0 = time.perf_counter()
-    oracle.bf_apply(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank, F)
+    gb = oracle.bf_apply(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank, F)
     dt = time.perf_counter() - t0
-    return {"value": w.n * 1 / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "seconds": dt,
-            "sample": f"cfg4 at full N=2^{w.log2n}, 1 of {w.nrhs} RHS columns (2 amplitude vectors), FP64 "
-                      f"oracle incl. on-the-fly block generation; metric scaled per N*RHS"}
+    out = {"value": w.n * 1 / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+           "seconds": dt,
+           "sample": f"{w.name} at full N=2^{w.log2n}, 1 of {w.nrhs} RHS columns ({w.n_amp} amplitude vectors), "
+                     f"FP64 oracle incl. on-the-fly block generation; metric scaled per N*RHS"}
+    if g0 is not None:
+        rows = W.sample_rows(w.n, w.seed)
+        gd = oracle.direct_rows(w.kernel, w.amp, w.log2n, F, rows)[:, 0]
+        out["accuracy"] = {"column": 0, "rows": len(rows), "eps": w.eps,
+                           "eps_b_oracle_bf_vs_direct": float(oracle.rel_l2(gb[rows, 0], gd)),
+                           "gpu_vs_direct": float(oracle.rel_l2(g0[rows].astype(np.complex128), gd)),
+                           "gpu_vs_oracle_bf_all_rows": float(oracle.rel_l2(g0.astype(np.complex128), gb[:, 0]))}
+    return out
 
 
 def run_reference(args, w, rank, world):
@@ -398,7 +408,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_sample(w)
+        g0 = None if args.index_shard else Gd[0].cpu().numpy()   # column 0 of the last timed apply
+        cpu = cpu_oracle_sample(w, g0)
 
     if rank == 0:
         out = {
@@ -428,6 +439,7 @@ def main():
                             "flops_per_launch": model[k][0], "bytes_per_launch": model[k][1]}
                         for k, v in ktimes.items()},
             "e2e": e2e, "gpu_launches": launches, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "accuracy": cpu.pop("accuracy", None) if cpu else None,
             "plan_build_s": t_build,
         }
         print(json.dumps(out), flush=True)

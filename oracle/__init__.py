@@ -60,6 +60,10 @@ def _load():
         lib.orc_bf_apply.argtypes = [i32, i32, i32, i32, i32, i64, vp, i64, vp, i64, i64]
         lib.orc_bf_apply.restype = i32
         lib.orc_num_threads.restype = i32
+        lib.orc_bf_blocks.argtypes = [i32, i32, i32, i32, i32, i32, vp]
+        lib.orc_bf_blocks.restype = i32
+        lib.orc_bf_apply_stored.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64, vp, i64, i64]
+        lib.orc_bf_apply_stored.restype = i32
         _lib = lib
     return _lib
 
@@ -147,6 +151,34 @@ def bf_apply(kernel: int, amp: int, LN: int, l0: int, r: int, F: np.ndarray, vch
     rc = _load().orc_bf_apply(kernel, amp, LN, l0, r, nrhs, F.ctypes.data, N, G.ctypes.data, N, vchunk)
     if rc:
         raise ValueError(f"orc_bf_apply failed ({rc})")
+    return G
+
+
+def bf_blocks(kernel: int, LN: int, l0: int, r: int, stage: int, level: int = 0) -> np.ndarray:
+    """Every block of one stage in pair order, FP64 (the bf-stored input layout): [N, rows, cols]."""
+    n0 = 1 << l0
+    shape = {0: (r, n0), 1: (r, 2 * r), 2: (r, r), 3: (n0, r)}[stage]
+    out = np.zeros((1 << LN,) + shape, np.complex128)
+    if _load().orc_bf_blocks(kernel, LN, l0, r, stage, level, out.ctypes.data):
+        raise ValueError("orc_bf_blocks: bad arguments")
+    return out
+
+
+def bf_apply_stored(LN: int, l0: int, r: int, a: np.ndarray, b: np.ndarray, v0, xfer, sw, u,
+                    F: np.ndarray, vchunk: int = 64) -> np.ndarray:
+    """bf-stored: O1-O7 with caller-supplied blocks (any precision, upcast to FP64) and amplitude terms
+    a, b ([n_amp][N]); layouts as bf_blocks returns them."""
+    F = np.asfortranarray(F, dtype=np.complex128)
+    N, nrhs = F.shape
+    arrs = [np.ascontiguousarray(x, dtype=np.complex128) for x in (a, b, v0, sw, u)]
+    xs = [np.ascontiguousarray(x, dtype=np.complex128) for x in xfer]
+    xp = (ctypes.c_void_p * max(1, len(xs)))(*[x.ctypes.data for x in xs])
+    G = np.zeros((N, nrhs), np.complex128, order="F")
+    rc = _load().orc_bf_apply_stored(LN, l0, r, arrs[0].shape[0], arrs[0].ctypes.data, arrs[1].ctypes.data,
+                                     arrs[2].ctypes.data, ctypes.cast(xp, ctypes.c_void_p), arrs[3].ctypes.data,
+                                     arrs[4].ctypes.data, nrhs, F.ctypes.data, N, G.ctypes.data, N, vchunk)
+    if rc:
+        raise ValueError(f"orc_bf_apply_stored failed ({rc})")
     return G
 
 

@@ -380,11 +380,37 @@ int orc_bf_block(int kernel, int LN, int l0, int r, int stage, int l, int64_t a,
     }
 }
 
+/* Every block of one stage in pair order (the "bf-stored" input layout): stage 0 init (level l0),
+ * 1 transfer at level l, 2 switch (level h), 3 termination (level D); pair p = a 2^(LN - level) + b. */
+int orc_bf_blocks(int kernel, int LN, int l0, int r, int stage, int l, cplx *out)
+{
+    bfctx c;
+    if (ctx_init(&c, kernel, LN, l0, r) || r > 32 || l0 > 6) return -1;
+    const int level = stage == 0 ? l0 : stage == 1 ? l : stage == 2 ? c.h : c.D;
+    if (stage == 1 && (l <= l0 || l > c.D)) return -1;
+    if (stage < 0 || stage > 3) return -1;
+    const int64_t nb = (int64_t)1 << (LN - level);
+    const int64_t sz = stage == 0 ? r * c.n0 : stage == 1 ? 2 * r * r : stage == 2 ? r * r : c.n0 * r;
+    int rc = 0;
+#pragma omp parallel for schedule(static) reduction(| : rc)
+    for (int64_t p = 0; p < c.N; p++) rc |= orc_bf_block(kernel, LN, l0, r, stage, l, p / nb, p % nb, out + p * sz);
+    return rc;
+}
+
 /* ------------------------------------------------------------------------- */
 /* O1-O7: Algorithm 4.1 applied to nv vectors Y (N x nv, column-major),        */
 /* result U_out (N x nv, column-major).  delta arrays: [pair][t][v].           */
+/* Blocks are generated on the fly from their formulas ("bf-otf")   */
+/* or, when st != NULL, read from caller-supplied arrays ("bf-stored"): every  */
+/* block in pair order, row-major as orc_bf_block returns it (init r x n0,     */
+/* transfer r x 2r per level l0+1..D, switch r x r, termination n0 x r).       */
 /* ------------------------------------------------------------------------- */
-static int butterfly_apply(const bfctx *c, int64_t nv, const cplx *Y, cplx *Uout)
+typedef struct {
+    const cplx *v0, *sw, *u;
+    const cplx *const *xfer;   /* [D - l0] */
+} bfstore;
+
+static int butterfly_apply(const bfctx *c, int64_t nv, const cplx *Y, cplx *Uout, const bfstore *st)
 {
     const int r = c->r;
     const int64_t N = c->N, n0 = c->n0;
@@ -399,7 +425,8 @@ static int butterfly_apply(const bfctx *c, int64_t nv, const cplx *Y, cplx *Uout
         for (int64_t p = 0; p < N; p++) {
             const int64_t a = p / nb, b = p % nb;
             cplx *V = malloc(sizeof(cplx) * (size_t)(r * n0));
-            blk_init(c, a, b, V);
+            if (st) memcpy(V, st->v0 + p * r * n0, sizeof(cplx) * (size_t)(r * n0));
+            else blk_init(c, a, b, V);
             for (int t = 0; t < r; t++)
                 for (int64_t v = 0; v < nv; v++) {
                     cplx s = 0;
@@ -417,7 +444,9 @@ static int butterfly_apply(const bfctx *c, int64_t nv, const cplx *Y, cplx *Uout
             for (int64_t p = 0; p < N; p++) {
                 const int64_t a = p / nbl, b = p % nbl;
                 cplx W[32 * 64];
-                if (l <= c->h) blk_first(c, l, a, b, W); else blk_second(c, l, a, b, W);
+                if (st) memcpy(W, st->xfer[l - c->l0 - 1] + p * 2 * r * r, sizeof(cplx) * (size_t)(2 * r * r));
+                else if (l <= c->h) blk_first(c, l, a, b, W);
+                else blk_second(c, l, a, b, W);
                 for (int t = 0; t < r; t++)
                     for (int64_t v = 0; v < nv; v++) {
                         cplx s = 0;
@@ -436,7 +465,8 @@ static int butterfly_apply(const bfctx *c, int64_t nv, const cplx *Y, cplx *Uout
             for (int64_t p = 0; p < N; p++) {
                 const int64_t a = p / nbh, b = p % nbh;
                 cplx S[32 * 32];
-                blk_switch(c, a, b, S);
+                if (st) memcpy(S, st->sw + p * r * r, sizeof(cplx) * (size_t)(r * r));
+                else blk_switch(c, a, b, S);
                 for (int t = 0; t < r; t++)
                     for (int64_t v = 0; v < nv; v++) {
                         cplx s = 0;
@@ -457,7 +487,8 @@ static int butterfly_apply(const bfctx *c, int64_t nv, const cplx *Y, cplx *Uout
                 for (int64_t v = 0; v < nv; v++) Uout[(a * n0 + j) + v * N] = 0;
             for (int64_t b = 0; b < n0; b++) {
                 const int64_t p = a * n0 + b;   /* pair index at level D: a 2^(LN-D) + b */
-                blk_term(c, a, b, U);
+                if (st) memcpy(U, st->u + p * n0 * r, sizeof(cplx) * (size_t)(n0 * r));
+                else blk_term(c, a, b, U);
                 for (int64_t j = 0; j < n0; j++)
                     for (int64_t v = 0; v < nv; v++) {
                         cplx s = 0;
@@ -476,6 +507,9 @@ static int butterfly_apply(const bfctx *c, int64_t nv, const cplx *Y, cplx *Uout
  *   g = sum_k a_k o BF(b_k o f)   (eqn:tg P:24-28; O7).
  * Vectors are processed in chunks of at most vchunk (memory bound only; the
  * vectors are independent).  Returns 0 on success. */
+static int apply_all(const bfctx *cp, int namp, const cplx *a, const cplx *b, int64_t nrhs, const cplx *F,
+                     int64_t ldf, cplx *G, int64_t ldg, int64_t vchunk, const bfstore *st);
+
 int orc_bf_apply(int kernel, int amp, int LN, int l0, int r, int64_t nrhs, const cplx *F, int64_t ldf,
                  cplx *G, int64_t ldg, int64_t vchunk)
 {
@@ -484,12 +518,36 @@ int orc_bf_apply(int kernel, int amp, int LN, int l0, int r, int64_t nrhs, const
     const int namp = orc_n_amp(amp);
     if (namp < 1) return -1;
     const int64_t N = c.N;
-    if (vchunk < 1) vchunk = 1;
     cplx *a = malloc(sizeof(cplx) * (size_t)(N * namp)), *b = malloc(sizeof(cplx) * (size_t)(N * namp));
     for (int k = 0; k < namp; k++) {
         orc_amp_term(amp, LN, k, 0, a + k * N);
         orc_amp_term(amp, LN, k, 1, b + k * N);
     }
+    const int rc = apply_all(&c, namp, a, b, nrhs, F, ldf, G, ldg, vchunk, NULL);
+    free(a); free(b);
+    return rc;
+}
+
+/* "bf-stored" (SURVEY 8(c) oracle modes): the same O1-O7 steps applied to caller-supplied blocks (complex128,
+ * layouts of butterfly_apply above) and amplitude terms a, b ([namp][N]); kernel-independent.  With the
+ * oracle's own blocks it reproduces orc_bf_apply; with blocks rounded to complex64 it measures what the
+ * factors' storage precision alone contributes to the GPU path's error. */
+int orc_bf_apply_stored(int LN, int l0, int r, int namp, const cplx *a, const cplx *b, const cplx *v0,
+                        const cplx *const *xfer, const cplx *sw, const cplx *u, int64_t nrhs, const cplx *F,
+                        int64_t ldf, cplx *G, int64_t ldg, int64_t vchunk)
+{
+    bfctx c;
+    if (ctx_init(&c, ORC_K_FIO, LN, l0, r) || r > 32 || l0 > 6 || namp < 1) return -1;
+    const bfstore st = {v0, sw, u, xfer};
+    return apply_all(&c, namp, a, b, nrhs, F, ldf, G, ldg, vchunk, &st);
+}
+
+static int apply_all(const bfctx *cp, int namp, const cplx *a, const cplx *b, int64_t nrhs, const cplx *F,
+                     int64_t ldf, cplx *G, int64_t ldg, int64_t vchunk, const bfstore *st)
+{
+    const bfctx c = *cp;
+    const int64_t N = c.N;
+    if (vchunk < 1) vchunk = 1;
     /* vectors v = (column cidx, term k) */
     const int64_t nvec = nrhs * namp;
     for (int64_t v0 = 0; v0 < nvec; v0 += vchunk) {
@@ -499,8 +557,8 @@ int orc_bf_apply(int kernel, int amp, int LN, int l0, int r, int64_t nrhs, const
             const int64_t col = (v0 + v) / namp, k = (v0 + v) % namp;
             for (int64_t j = 0; j < N; j++) Y[j + v * N] = b[k * N + j] * F[j + col * ldf];   /* y = b_k o f */
         }
-        int rc = butterfly_apply(&c, nv, Y, Uo);
-        if (rc) { free(Y); free(Uo); free(a); free(b); return rc; }
+        int rc = butterfly_apply(&c, nv, Y, Uo, st);
+        if (rc) { free(Y); free(Uo); return rc; }
         for (int64_t v = 0; v < nv; v++) {
             const int64_t col = (v0 + v) / namp, k = (v0 + v) % namp;
             for (int64_t i = 0; i < N; i++) {
@@ -510,7 +568,6 @@ int orc_bf_apply(int kernel, int amp, int LN, int l0, int r, int64_t nrhs, const
         }
         free(Y); free(Uo);
     }
-    free(a); free(b);
     return 0;
 }
 

@@ -247,3 +247,46 @@ def test_rhs_generator_column_subset():
     sub = W.rhs(256, 5, 3, cols=[1, 4])
     assert np.array_equal(full[:, [1, 4]], sub)
     assert full.dtype == np.complex64 and full.flags.f_contiguous
+
+
+@pytest.mark.slow
+def test_bf_vs_direct_cfg5():
+    """cfg5 (N = 2^22): r = 10 keeps the BF within eps/2 of the direct sum on the eps^b rows (reading R10 at the
+    largest N; the survey's probe value was 4.3e-7).  ~100 s on 8 cores."""
+    w = W.CONFIGS["cfg5"]
+    F = W.rhs(w.n, w.nrhs, w.seed, cols=[0])
+    rows = W.sample_rows(w.n, w.seed)
+    gd = oracle.direct_rows(w.kernel, w.amp, w.log2n, F, rows)
+    gb = oracle.bf_apply(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank, F)
+    assert oracle.rel_l2(gb[rows], gd) <= w.eps / 2
+
+
+def _stored_inputs(kernel, amp, LN, l0, r, dtype=np.complex128):
+    a, b = oracle.amp_terms(amp, LN)
+    v0 = oracle.bf_blocks(kernel, LN, l0, r, 0).astype(dtype)
+    xf = [oracle.bf_blocks(kernel, LN, l0, r, 1, l).astype(dtype) for l in range(l0 + 1, LN - l0 + 1)]
+    sw = oracle.bf_blocks(kernel, LN, l0, r, 2).astype(dtype)
+    u = oracle.bf_blocks(kernel, LN, l0, r, 3).astype(dtype)
+    return a, b, v0, xf, sw, u
+
+
+@pytest.mark.parametrize("kernel,amp,LN,l0,r", [(W.K_FIO, W.A_CFG1, 10, 4, 12), (W.K_FIO_JUMP, W.A_CFG3, 12, 4, 10)])
+def test_bf_stored_mode(kernel, amp, LN, l0, r):
+    """bf-stored (SURVEY 8(c) oracle modes): O1-O7 applied to supplied blocks.  (1) With the oracle's own FP64
+    blocks it equals the on-the-fly mode; (2) with the blocks rounded to complex64 -- the precision the GPU path
+    stores its factors in -- it stays within a few 1e-7 of it: the factor storage alone accounts for that much
+    of the GPU-vs-oracle error, the rest is FP32 arithmetic; (3) a wrong block is detected."""
+    F = W.rhs(1 << LN, 3, 7)
+    otf = oracle.bf_apply(kernel, amp, LN, l0, r, F)
+    a, b, v0, xf, sw, u = _stored_inputs(kernel, amp, LN, l0, r)
+    st = oracle.bf_apply_stored(LN, l0, r, a, b, v0, xf, sw, u, F)
+    assert np.all(oracle.rel_l2(st, otf, axis=0) <= 1e-14)
+    c64 = [x.astype(np.complex64) for x in (v0, sw, u)]
+    st32 = oracle.bf_apply_stored(LN, l0, r, a.astype(np.complex64), b.astype(np.complex64), c64[0],
+                                  [x.astype(np.complex64) for x in xf], c64[1], c64[2], F)
+    e = oracle.rel_l2(st32, otf, axis=0)
+    assert np.all(e <= 5e-7) and np.all(e >= 1e-9), e
+    xm = [x.copy() for x in xf]
+    xm[0][5] *= -1
+    bad = oracle.bf_apply_stored(LN, l0, r, a, b, v0, xm, sw, u, F)
+    assert np.all(oracle.rel_l2(bad, otf, axis=0) > 1e-3)
