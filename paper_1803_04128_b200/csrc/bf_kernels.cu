@@ -630,6 +630,145 @@ __global__ void __launch_bounds__(256) sl_kernel(const float2* __restrict__ in, 
     }
 }
 
+// a global load ptxas keeps in program order (volatile asm): the tiny kernels issue a whole block of operand
+// loads before their first MAC -- with plain loads the scheduler interleaved one load per MAC pair, one memory
+// round trip each
+__device__ __forceinline__ float2 ldg_early(const float2* p)
+{
+    float2 v;
+    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Tiny vector batches (nv <= 4: cfg1 has nv = 2): one thread per output row and all nv vectors in registers,
+// reduction loops fully unrolled so each thread keeps a dozen independent loads in flight.  The per-column
+// kernels above give such batches a few hundred threads that each walk ~200 dependent load rounds (30-66 us per
+// stage at N = 2^10); these have N r threads.  Every output is accumulated in the same order with the same
+// cmac/cmul as s0_kernel / xfer_kernel / sl_kernel (bitwise equal results).
+// ---------------------------------------------------------------------------
+template <int R, int NV>
+__global__ void __launch_bounds__(256, 1) s0_tiny_kernel(const float2* __restrict__ F, int64_t ldf,
+                                                      const float2* __restrict__ ampb, const float2* __restrict__ V0,
+                                                      float2* __restrict__ out, int LN, int l0, int n_amp)
+{
+    const int64_t N = int64_t(1) << LN;
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= N * R) return;
+    const int64_t p = idx / R;
+    const int t = int(idx % R), n0 = 1 << l0;
+    const int64_t nleaf = N >> l0, b = p % nleaf;
+    float2 acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; v++) acc[v] = make_float2(0.f, 0.f);
+    const float2* Vb = V0 + p * n0 * R + t;   // column-major r x n0: element (t, j) at j R + t
+    for (int j0 = 0; j0 < n0; j0 += 8) {      // n0 >= 8: stage 8 columns' operands, then their MACs
+        float2 w[8], fa[8][NV], fb[8][NV];
+#pragma unroll
+        for (int jj = 0; jj < 8; jj++) {
+            const int64_t x = b * n0 + j0 + jj;
+            w[jj] = ldg_early(Vb + (j0 + jj) * R);
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                const int c = v / n_amp, k = v - c * n_amp;
+                fa[jj][v] = ldg_early(ampb + k * N + x);
+                fb[jj][v] = ldg_early(F + x + c * ldf);
+            }
+        }
+        #pragma unroll
+        for (int jj = 0; jj < 8; jj++)
+#pragma unroll
+            for (int v = 0; v < NV; v++) cmac(acc[v], w[jj], cmul(fa[jj][v], fb[jj][v]));
+    }
+#pragma unroll
+    for (int v = 0; v < NV; v++) out[(p * R + t) * NV + v] = acc[v];
+}
+
+template <int R, int NV>
+__global__ void __launch_bounds__(256, 1) xfer_tiny_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                                        const float2* __restrict__ Wl, int LN, int l, int rh, int rhg,
+                                                        const bfs::PeerOut po)
+{
+    const int64_t N = int64_t(1) << LN;
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= N * R) return;
+    const int64_t p = idx / R;
+    const int t = int(idx % R), sh = LN - l;
+    const int64_t a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
+    const int64_t u = ((a >> 1) << sh) + b;   // the butterfly unit: inputs 2u, 2u+1 of level l-1
+    const int64_t pin = rh ? bfs::recv_index(2 * u, rh, rhg) : 2 * u;
+    const float2* x = in + pin * R * NV;
+    const float2* W = Wl + p * 2 * R * R + t;   // column-major r x 2r: element (t, k) at k R + t
+    float2 acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; v++) acc[v] = make_float2(0.f, 0.f);
+    float2 w[2 * R], xv[2 * R][NV];   // all operands first (one memory round trip), then the 2r MACs
+#pragma unroll
+    for (int k = 0; k < 2 * R; k++) {
+        w[k] = ldg_early(W + k * R);
+#pragma unroll
+        for (int v = 0; v < NV; v++) xv[k][v] = ldg_early(x + k * NV + v);
+    }
+#pragma unroll
+    for (int k = 0; k < 2 * R; k++)
+#pragma unroll
+        for (int v = 0; v < NV; v++) cmac(acc[v], w[k], xv[k][v]);
+    float2* o = bfs::pair_out(out, po, p, R, NV) + t * NV;
+#pragma unroll
+    for (int v = 0; v < NV; v++) o[v] = acc[v];
+}
+
+// SL: a CTA takes LPB whole T_X leaves: their U blocks and coefficient rows (contiguous in HBM) are staged in
+// shared memory with 16-byte loads from all threads at once (one memory round trip), then thread (leaf, x, v)
+// -- v fastest, so the n_amp vectors of a column sit in adjacent lanes -- runs the (b, t) reduction in
+// sl_kernel's order and lane k = 0 forms sum_k a_k(x) u_k(x) from its neighbours (warp shuffles).
+template <int R, int NV, int NA>
+__global__ void __launch_bounds__(256, 1) sl_tiny_kernel(const float2* __restrict__ in, const float2* __restrict__ U,
+                                                         const float2* __restrict__ ampa, float2* __restrict__ G,
+                                                         int64_t ldg, int LN, int l0, int LPB)
+{
+    extern __shared__ float4 smem_sltiny[];
+    const int64_t N = int64_t(1) << LN;
+    const int n0 = 1 << l0;
+    const int64_t nleaf = N >> l0, a0 = int64_t(blockIdx.x) * LPB;
+    const int nl = int(nleaf - a0 < LPB ? nleaf - a0 : LPB);
+    const int ue = n0 * R * n0, xe = n0 * R * NV;   // complex per leaf
+    float2* Us = reinterpret_cast<float2*>(smem_sltiny);
+    float2* Xs = Us + LPB * ue;
+    {   // cp.async: every 16-byte copy in flight at once (a load-then-store loop waited one round trip each)
+        const float2* su = U + a0 * ue;
+        for (int i = threadIdx.x; i < nl * ue / 2; i += blockDim.x) cp_async16(Us + 2 * i, su + 2 * i);
+        const float2* sx = in + a0 * xe;
+        for (int i = threadIdx.x; i < nl * xe / 2; i += blockDim.x) cp_async16(Xs + 2 * i, sx + 2 * i);
+        cp_async_commit();
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    const int li = threadIdx.x / (n0 * NV), rem = threadIdx.x % (n0 * NV), j = rem / NV, v = rem % NV;
+    const bool live = li < nl;
+    float2 acc = make_float2(0.f, 0.f);
+    if (live) {
+        const float2* Ub = Us + li * ue + j;   // column-major n0 x r per pair: element (j, t) at t n0 + j
+        const float2* xb = Xs + li * xe + v;
+        for (int b = 0; b < n0; b++) {
+#pragma unroll
+            for (int t = 0; t < R; t++) cmac(acc, Ub[(b * R + t) * n0], xb[(b * R + t) * NV]);
+        }
+    }
+    float2 uk[NA];
+#pragma unroll
+    for (int k = 0; k < NA; k++) {
+        uk[k].x = __shfl_sync(0xffffffffu, acc.x, (threadIdx.x & 31) + k, 32);
+        uk[k].y = __shfl_sync(0xffffffffu, acc.y, (threadIdx.x & 31) + k, 32);
+    }
+    if (!live || v % NA) return;
+    const int64_t x = (a0 + li) * n0 + j;
+    float2 g = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < NA; k++) cmac(g, __ldg(ampa + k * N + x), uk[k]);
+    G[x + int64_t(v / NA) * ldg] = g;
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -702,9 +841,61 @@ static cudaError_t s0t_go(const Dims& d, const float2* F, int64_t ldf, const flo
 
 static bool tiled_ok(const Dims& d, int nv) { return nv >= 64 && nv % 4 == 0 && d.l0 <= 6; }
 
+template <int R, int NV>
+static cudaError_t s0_tiny_go(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float2* V0,
+                              float2* out, cudaStream_t s)
+{
+    const int64_t n = d.N * R;
+    s0_tiny_kernel<R, NV><<<unsigned((n + 255) / 256), 256, 0, s>>>(F, ldf, ampb, V0, out, d.LN, d.l0, d.n_amp);
+    return cudaGetLastError();
+}
+
+template <int R, int NV>
+static cudaError_t xfer_tiny_go(const Dims& d, int l, const float2* in, float2* out, const float2* W, int rh, int rhg,
+                                const bfs::PeerOut& po, cudaStream_t s)
+{
+    const int64_t n = d.N * R;
+    xfer_tiny_kernel<R, NV><<<unsigned((n + 255) / 256), 256, 0, s>>>(in, out, W, d.LN, l, rh, rhg, po);
+    return cudaGetLastError();
+}
+
+// leaves per CTA of sl_tiny_kernel (0: the leaf does not fit shared memory / 256 threads)
+static int sl_tiny_lpb(const Dims& d, int nv)
+{
+    const int n0 = 1 << d.l0;
+    const size_t leaf = size_t(n0) * d.R * (n0 + nv) * sizeof(float2);
+    int lpb = int((96 * 1024) / leaf);
+    if (lpb * n0 * nv > 256) lpb = 256 / (n0 * nv);
+    return lpb;
+}
+
+template <int R, int NV, int NA>
+static cudaError_t sl_tiny_go(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G,
+                              int64_t ldg, cudaStream_t s)
+{
+    const int n0 = 1 << d.l0, lpb = sl_tiny_lpb(d, NV);
+    const size_t shm = size_t(lpb) * n0 * R * (n0 + NV) * sizeof(float2);
+    auto kern = sl_tiny_kernel<R, NV, NA>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+    if (e != cudaSuccess) return e;
+    const int64_t nleaf = d.N >> d.l0;
+    const int threads = (lpb * n0 * NV + 31) / 32 * 32;
+    kern<<<unsigned((nleaf + lpb - 1) / lpb), threads, shm, s>>>(in, U, ampa, G, ldg, d.LN, d.l0, lpb);
+    return cudaGetLastError();
+}
+
+#define BF_TINY_NV(NVV, CALL)                                                                                  \
+    switch (NVV) {                                                                                             \
+    case 1: { constexpr int NN = 1; BF_DISPATCH_R(d.R, CALL) }                                                 \
+    case 2: { constexpr int NN = 2; BF_DISPATCH_R(d.R, CALL) }                                                 \
+    case 3: { constexpr int NN = 3; BF_DISPATCH_R(d.R, CALL) }                                                 \
+    default: { constexpr int NN = 4; BF_DISPATCH_R(d.R, CALL) }                                                \
+    }
+
 cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float2* V0, float2* out,
                       int nv, cudaStream_t s)
 {
+    if (nv <= 4) BF_TINY_NV(nv, (s0_tiny_go<RR, NN>(d, F, ldf, ampb, V0, out, s)))
     if (tiled_ok(d, nv)) BF_DISPATCH_R(d.R, (s0t_go<RR>(d, F, ldf, ampb, V0, out, nv, s)))
     const int tn = pick_tn(nv, 4);
     if (tn == 4) BF_DISPATCH_R(d.R, (s0_go<RR, 4>(d, F, ldf, ampb, V0, out, nv, s)))
@@ -716,6 +907,7 @@ cudaError_t launch_xfer(const Dims& d, int l, const float2* in, float2* out, con
                         int rh, int rhg, const bfs::PeerOut* po)
 {
     const bfs::PeerOut pz = po ? *po : bfs::PeerOut{};
+    if (nv <= 4) BF_TINY_NV(nv, (xfer_tiny_go<RR, NN>(d, l, in, out, W, rh, rhg, pz, s)))
     const int tn = pick_tn(nv, 2);
     if (tn == 2) BF_DISPATCH_R(d.R, (xfer_go<RR, 2>(d, l, in, out, W, nv, rh, rhg, pz, s)))
     BF_DISPATCH_R(d.R, (xfer_go<RR, 1>(d, l, in, out, W, nv, rh, rhg, pz, s)))
@@ -740,6 +932,14 @@ static cudaError_t slt_go(const Dims& d, const float2* in, const float2* U, cons
 cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,
                       int nv, cudaStream_t s)
 {
+    if (nv <= 4 && sl_tiny_lpb(d, nv) >= 1) {
+        if (d.n_amp == 1) BF_TINY_NV(nv, (sl_tiny_go<RR, NN, 1>(d, in, U, ampa, G, ldg, s)))
+        if (d.n_amp == 2 && nv % 2 == 0) {
+            if (nv == 2) BF_DISPATCH_R(d.R, (sl_tiny_go<RR, 2, 2>(d, in, U, ampa, G, ldg, s)))
+            BF_DISPATCH_R(d.R, (sl_tiny_go<RR, 4, 2>(d, in, U, ampa, G, ldg, s)))
+        }
+        if (d.n_amp == 4 && nv == 4) BF_DISPATCH_R(d.R, (sl_tiny_go<RR, 4, 4>(d, in, U, ampa, G, ldg, s)))
+    }
     if (tiled_ok(d, nv)) {
         if (d.n_amp == 4) BF_DISPATCH_R(d.R, (slt_go<RR, 4>(d, in, U, ampa, G, ldg, nv, s)))
         if (d.n_amp == 2) BF_DISPATCH_R(d.R, (slt_go<RR, 2>(d, in, U, ampa, G, ldg, nv, s)))
