@@ -166,6 +166,17 @@ bf_status_t bf_apply_ex(bf_plan_t plan, const bf_c64 *F, int64_t ldf, bf_c64 *G,
  * of G, all on `stream`; returns after the stream has completed the work. */
 bf_status_t bf_apply_host(bf_plan_t plan, const bf_c64 *F_host, bf_c64 *G_host, int64_t nrhs, void *stream);
 
+/* Asynchronous end-to-end apply with HOST buffers (pinned: cudaHostAlloc / cudaHostRegister; pageable memory
+ * works but the copies then serialize): per RHS chunk of <= max_nrhs_chunk columns, host->device copy of F on the
+ * plan's copy stream, the apply on `stream`, device->host copy of G on a second copy stream, through two device
+ * staging slots used alternately -- and returns at once.  Consecutive calls (and chunks) therefore overlap the
+ * copies of one chunk with the apply of its neighbours (PCIe is full duplex), which bf_apply_host cannot do
+ * across calls.  F_host and G_host must stay valid and untouched until bf_apply_host_wait returns (or the
+ * plan's work is otherwise known complete).  Uses the plan workspace: one async call stream per plan. */
+bf_status_t bf_apply_host_async(bf_plan_t plan, const bf_c64 *F_host, bf_c64 *G_host, int64_t nrhs, void *stream);
+/* Wait until every G copy issued by bf_apply_host_async has landed on the host. */
+bf_status_t bf_apply_host_wait(bf_plan_t plan);
+
 /* Workspace bytes one chunk of `nrhs_chunk` columns needs. */
 size_t bf_workspace_bytes(bf_plan_t plan, int64_t nrhs_chunk);
 

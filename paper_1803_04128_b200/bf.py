@@ -35,7 +35,7 @@ STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALI
 
 # every symbol include/*.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finalize", "bf_apply", "bf_apply_ex",
-           "bf_apply_host", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing", "bf_plan_set_option",
+           "bf_apply_host", "bf_apply_host_async", "bf_apply_host_wait", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing", "bf_plan_set_option",
            "bf_plan_destroy", "bf_last_error", "bf_abi_version", "bf_build_n_amp", "bf_build_amp", "bf_build_blocks",
            "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
            "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated")
@@ -103,6 +103,8 @@ def lib():
             "bf_apply": ([vp, vp, vp, i64, vp], i32),
             "bf_apply_ex": ([vp, vp, i64, vp, i64, i64, vp, sz, vp], i32),
             "bf_apply_host": ([vp, vp, vp, i64, vp], i32),
+            "bf_apply_host_async": ([vp, vp, vp, i64, vp], i32),
+            "bf_apply_host_wait": ([vp], i32),
             "bf_workspace_bytes": ([vp, i64], sz),
             "bf_plan_get_info": ([vp, P(bf_plan_info_t)], i32),
             "bf_plan_set_timing": ([vp, i32], i32),
@@ -257,6 +259,13 @@ class Plan:
     def apply_host(self, F_host, G_host, nrhs: int, stream=None):
         """End to end with host buffers (copies inside the call)."""
         _check(lib().bf_apply_host(self._h, _ptr(F_host), _ptr(G_host), nrhs, _stream(stream)))
+
+    def apply_host_async(self, F_host, G_host, nrhs: int, stream=None):
+        """End to end with (pinned) host buffers, asynchronous: returns at once; see apply_host_wait."""
+        _check(lib().bf_apply_host_async(self._h, _ptr(F_host), _ptr(G_host), nrhs, _stream(stream)))
+
+    def apply_host_wait(self):
+        _check(lib().bf_apply_host_wait(self._h))
 
     # -- introspection -------------------------------------------------------------
     def info(self) -> dict:

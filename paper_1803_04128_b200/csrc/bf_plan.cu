@@ -170,6 +170,11 @@ struct bf_plan_s {
     float2* dG = nullptr;
     int64_t staging_elems = 0;   // complex elements of dF / dG each
     cudaStream_t h2d = nullptr, d2h = nullptr;   // copy streams of the pipelined bf_apply_host
+    // bf_apply_host_async: two staging slots of max_nrhs_chunk columns, used alternately per chunk
+    float2* aF[2] = {nullptr, nullptr};
+    float2* aG[2] = {nullptr, nullptr};
+    cudaEvent_t a_h2d[2] = {}, a_applied[2] = {}, a_d2h[2] = {};
+    int64_t a_uses = 0;                            // chunks issued through the async ring
     bool tensor_cores = true;  // BF_OPT_TENSOR_CORES
     bfk::BandVariant band;     // BF_OPT_BAND_COMPOSE
     int host_pieces = 2;       // BF_OPT_HOST_PIECES: bf_apply_host pipeline pieces per chunk
@@ -299,6 +304,13 @@ void free_plan(bf_plan_s* p)
     }
     cudaFree(p->dF);
     cudaFree(p->dG);
+    for (int i = 0; i < 2; i++) {
+        if (p->a_d2h[i]) cudaEventSynchronize(p->a_d2h[i]);
+        cudaFree(p->aF[i]);
+        cudaFree(p->aG[i]);
+        for (cudaEvent_t ev : {p->a_h2d[i], p->a_applied[i], p->a_d2h[i]})
+            if (ev) cudaEventDestroy(ev);
+    }
     if (p->h2d) cudaStreamDestroy(p->h2d);
     if (p->d2h) cudaStreamDestroy(p->d2h);
     if (p->comm) nccl().CommDestroy(p->comm);
@@ -1084,6 +1096,63 @@ bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int
     if (st != BF_OK) return st;
     if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
         return cuda_fail(e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3, "bf_apply_host");
+    return BF_OK;
+}
+
+bf_status_t bf_apply_host_async(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int64_t nrhs, void* stream)
+{
+    if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
+    if (!p->finalized) return fail(BF_ERR_STATE, "plan not finalized");
+    if (nrhs < 0 || (nrhs > 0 && (!F_host || !G_host))) return fail(BF_ERR_INVALID_ARG, "bad arguments");
+    if (nrhs == 0) return BF_OK;
+    DeviceGuard g(p->device);
+    const int64_t rows = (p->mode == BF_SHARD_NCCL) ? p->nloc() : p->d.N, chunk = p->max_chunk;
+    cudaError_t e = cudaSuccess;
+    if (!p->h2d && ((e = cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+                    (e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking)) != cudaSuccess))
+        return cuda_fail(e, "copy streams");
+    for (int i = 0; i < 2; i++) {
+        if (p->aF[i]) continue;
+        bf_status_t st;
+        if ((st = dalloc(&p->aF[i], rows * chunk, "async F")) || (st = dalloc(&p->aG[i], rows * chunk, "async G")))
+            return st;
+        for (cudaEvent_t* ev : {&p->a_h2d[i], &p->a_applied[i], &p->a_d2h[i]})
+            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "events");
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // per chunk: slot = use % 2.  H2D into slot's F once the apply two chunks back has read it; the apply (on
+    // `stream`) once that H2D landed and the slot's previous G has been copied out; D2H after the apply.  The
+    // host returns at once: the copies of chunk i+1 and i-1 run while chunk i is applied.
+    for (int64_t c0 = 0; c0 < nrhs; c0 += chunk) {
+        const int64_t nc = std::min(chunk, nrhs - c0);
+        const int sl = int(p->a_uses & 1);
+        const bool reuse = p->a_uses >= 2;
+        p->a_uses++;
+        const size_t bytes = size_t(rows * nc) * sizeof(float2);
+        if (reuse) cudaStreamWaitEvent(p->h2d, p->a_applied[sl], 0);
+        if ((e = cudaMemcpyAsync(p->aF[sl], F_host + c0 * rows, bytes, cudaMemcpyHostToDevice, p->h2d)) != cudaSuccess)
+            return cuda_fail(e, "H2D");
+        cudaEventRecord(p->a_h2d[sl], p->h2d);
+        cudaStreamWaitEvent(s, p->a_h2d[sl], 0);
+        if (reuse) cudaStreamWaitEvent(s, p->a_d2h[sl], 0);
+        if (bf_status_t st = apply_impl(p, p->aF[sl], rows, p->aG[sl], rows, nc, p->sh[0].ws, s); st != BF_OK) return st;
+        cudaEventRecord(p->a_applied[sl], s);
+        cudaStreamWaitEvent(p->d2h, p->a_applied[sl], 0);
+        if ((e = cudaMemcpyAsync(G_host + c0 * rows, p->aG[sl], bytes, cudaMemcpyDeviceToHost, p->d2h)) != cudaSuccess)
+            return cuda_fail(e, "D2H");
+        cudaEventRecord(p->a_d2h[sl], p->d2h);
+    }
+    return BF_OK;
+}
+
+bf_status_t bf_apply_host_wait(bf_plan_t p)
+{
+    if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
+    DeviceGuard g(p->device);
+    for (int i = 0; i < 2; i++)
+        if (p->a_d2h[i] && p->a_uses > i) {
+            if (bf_status_t st = wait_event_nccl(p, p->a_d2h[i]); st != BF_OK) return st;
+        }
     return BF_OK;
 }
 

@@ -327,3 +327,20 @@ def test_upload_coverage():
         ref = bf.Plan.from_arrays(LN, l0, r, a, b, v0, xf, sw, u, max_nrhs_chunk=1)
         F = W.rhs(N, 1, 3)
         assert np.array_equal(gpu_apply(p, F), gpu_apply(ref, F))
+
+
+def test_apply_host_async_pipeline():
+    """bf_apply_host_async: several calls in flight (distinct host buffers, chunks alternating between the two
+    staging slots) give exactly bf_apply's results once bf_apply_host_wait returns."""
+    plan = _small_plan(nrhs_chunk=3)
+    N = 1 << 12
+    calls = [W.rhs(N, n, 30 + n) for n in (7, 3, 5, 1)]     # 3 + 1 + 2 + 1 chunks
+    refs = [gpu_apply(plan, F) for F in calls]
+    hosts = [(torch.from_numpy(np.ascontiguousarray(F.T)).pin_memory(),
+              torch.full((F.shape[1], N), float("nan"), dtype=torch.complex64).pin_memory()) for F in calls]
+    for (Fh, Gh), F in zip(hosts, calls):
+        plan.apply_host_async(Fh, Gh, F.shape[1])
+    plan.apply_host_wait()
+    for (_, Gh), ref in zip(hosts, refs):
+        assert np.array_equal(np.asfortranarray(Gh.numpy().T), ref)
+    plan.destroy()
