@@ -433,11 +433,33 @@ __global__ void __launch_bounds__(32 * (SV_MAX_CONSUMERS + 2), 1)
             const int yb = int(k & 1);
             if (k >= 2) tc::mbar_wait(&yempty[yb], uint32_t(((k >> 1) - 1) & 1));
             float2* Yb = Y + yb * n0 * nv;
-            for (int e = lane; e < n0 * nrhs; e += 32) {
-                const int j = e % n0, c = e / n0;
-                const int64_t x = b * n0 + j;
-                const float2 f = __ldg(F + x + c * ldf);
-                for (int kk = 0; kk < n_amp; kk++) Yb[j * nv + c * n_amp + kk] = cmul_sv(__ldg(ampb + kk * N + x), f);
+            // 8 elements per lane per batch: all their loads are issued before the first product (one load, then
+            // its stores, per element cost a memory round trip each -- 16 per leaf at cfg5: the y builder was
+            // the S0 kernel's critical path)
+            for (int e0 = 0; e0 < n0 * nrhs; e0 += 32 * 8) {
+                float2 f[8], am[8][4];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int e = e0 + q * 32 + lane;
+                    f[q] = make_float2(0.f, 0.f);
+                    if (e < n0 * nrhs) {
+                        const int j = e % n0, c = e / n0;
+                        const int64_t x = b * n0 + j;
+                        f[q] = __ldg(F + x + c * ldf);
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++)
+                            if (kk < n_amp) am[q][kk] = __ldg(ampb + kk * N + x);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int e = e0 + q * 32 + lane;
+                    if (e >= n0 * nrhs) continue;
+                    const int j = e % n0, c = e / n0;
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++)
+                        if (kk < n_amp) Yb[j * nv + c * n_amp + kk] = cmul_sv(am[q][kk], f[q]);
+                }
             }
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&yfull[yb]);
@@ -500,11 +522,11 @@ __global__ void __launch_bounds__(32 * (SV_MAX_CONSUMERS + 2), 1)
 
 // SL (eqn:bf3 P:791-797 + eqn:tg P:24-28): G[x, c] = sum_k a_k(x) sum_{b < n0} sum_t U[a n0 + b](j, t)
 // delta[a n0 + b](t)[c n_amp + k], x = a n0 + j.  A consumer warp owns whole T_X leaves a (the reduction over
-// b stays in registers); the producer streams each leaf's pairs in chunks of 2 (coefficients and U blocks,
+// b stays in registers); the producer streams each leaf's pairs in chunks of 4 (coefficients and U blocks,
 // one bulk copy each) through a ring shared by the consumers in round-robin order.  Lane = (j group q < 4,
 // v group vl < 8): rows j = 2 (4 m + q) + {0, 1} (m < n0 / 8: the 4 groups of one load are 4 consecutive
 // 16-byte chunks -- conflict-free) x VPL = nv / 8 vectors (whole RHS columns: VPL % n_amp == 0).
-constexpr int SL_SV_B = 2;   // pairs per chunk
+constexpr int SL_SV_B = 4;   // pairs per chunk (2: twice the bulk copies, cfg5 SL 10.2 vs 9.4 ms)
 
 template <int R, int VPL, int NA, int N0>
 // (9-12 warps put 3 on some SM sub-partition, whose 16K registers then cap a thread at 168 registers; the

@@ -344,3 +344,22 @@ def test_apply_host_async_pipeline():
     for (_, Gh), ref in zip(hosts, refs):
         assert np.array_equal(np.asfortranarray(Gh.numpy().T), ref)
     plan.destroy()
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_cfg4_rhs_shard_launch_configuration(world):
+    """cfg4 at full size in the launch configuration one rank of bench.py --gpus 4 / 8 runs (R19): 256/G columns of
+    the seeded batch in one chunk (nv = 128 / 64: tensor-core leaf stages on part-filled tiles, precomposed bands),
+    sampled columns against the oracle."""
+    import bench
+    w = W.CONFIGS["cfg4"]
+    c0, c1 = bench.rhs_columns(w.nrhs, world, world - 1)      # the last rank's columns
+    F = W.rhs(w.n, w.nrhs, w.seed, cols=range(c0, c1))
+    plan = bf.Plan.build_fio(bf.fio_of(w), max_nrhs_chunk=c1 - c0)
+    info = plan.info()
+    assert {"s0", "sl"} <= set(info["tc_classes"]) and any(k.startswith("xfer") for k in info["tc_classes"])
+    G = gpu_apply(plan, F)
+    plan.destroy()
+    cols = [0, c1 - c0 - 1]
+    R = oracle.bf_apply(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank, F[:, cols])
+    assert np.all(per_col_err(G[:, cols], R) <= PARITY)
