@@ -105,13 +105,15 @@ class ClockSampler:
 
 
 def _ncu_traffic(workload, cls):
-    """DRAM bytes per launch of kernel class `cls` from the committed ncu capture of this workload
-    (profiles/r1_traffic_<workload>.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", f"r1_traffic_{workload}.json")) as f:
-            return json.load(f)["bytes_per_launch"].get(cls)
-    except Exception:
-        return None
+    """DRAM bytes per launch of kernel class `cls` from the newest committed ncu capture of this workload
+    (profiles/r2_traffic_<workload>.json, else r1_), or None."""
+    for rnd in ("r2", "r1"):
+        try:
+            with open(os.path.join(ROOT, "profiles", f"{rnd}_traffic_{workload}.json")) as f:
+                return json.load(f)["bytes_per_launch"].get(cls)
+        except Exception:
+            continue
+    return None
 
 
 def stage_model(w, nvec, info):
