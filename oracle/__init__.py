@@ -64,6 +64,9 @@ def _load():
         lib.orc_bf_blocks.restype = i32
         lib.orc_bf_apply_stored.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64, vp, i64, i64]
         lib.orc_bf_apply_stored.restype = i32
+        lib.orc_bf_apply_adjoint.argtypes = [i32, i32, i32, i32, i32, i64, vp, i64, vp, i64, i64]
+        lib.orc_bf_apply_adjoint.restype = i32
+        lib.orc_direct_adjoint_rows.argtypes = [i32, i32, i32, i64, vp, i64, vp, i64, vp]
         _lib = lib
     return _lib
 
@@ -152,6 +155,30 @@ def bf_apply(kernel: int, amp: int, LN: int, l0: int, r: int, F: np.ndarray, vch
     if rc:
         raise ValueError(f"orc_bf_apply failed ({rc})")
     return G
+
+
+def bf_apply_adjoint(kernel: int, amp: int, LN: int, l0: int, r: int, F: np.ndarray, vchunk: int = 64) -> np.ndarray:
+    """O8: the adjoint apply g = sum_k conj(b_k) o BF*(conj(a_k) o f), F indexed by x (N x nrhs), result by xi."""
+    F = np.asfortranarray(F, dtype=np.complex128)
+    N, nrhs = F.shape
+    assert N == 1 << LN
+    G = np.zeros((N, nrhs), np.complex128, order="F")
+    rc = _load().orc_bf_apply_adjoint(kernel, amp, LN, l0, r, nrhs, F.ctypes.data, N, G.ctypes.data, N, vchunk)
+    if rc:
+        raise ValueError(f"orc_bf_apply_adjoint failed ({rc})")
+    return G
+
+
+def direct_adjoint_rows(kernel: int, amp: int, LN: int, F: np.ndarray, rows) -> np.ndarray:
+    """O0*: xi-rows of g = K* F (F: N x nrhs over x). Returns len(rows) x nrhs complex128."""
+    F = np.asfortranarray(F, dtype=np.complex128)
+    N, nrhs = F.shape
+    assert N == 1 << LN
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros((len(rows), nrhs), np.complex128, order="F")
+    _load().orc_direct_adjoint_rows(kernel, amp, LN, nrhs, F.ctypes.data, N, rows.ctypes.data, len(rows),
+                                    out.ctypes.data)
+    return out
 
 
 def bf_blocks(kernel: int, LN: int, l0: int, r: int, stage: int, level: int = 0) -> np.ndarray:

@@ -15,6 +15,8 @@
  *   O1-O7  the butterfly application of Algorithm 4.1 with the
  *          amplitude split of eqn:tg:  g = sum_k a_k o BF(b_k o f),
  *          every block generated on the fly from its formula.
+ *   O0*, O8  the adjoint: direct sum of conj(K) transposed, and the factors of
+ *          O2-O6 conjugate-transposed in reverse order.
  *
  * Pins: tests/test_oracle_pins.py (closed forms, paper-printed eps^b values of
  * tab:1D-FIO, brute-force dense assembly, Lagrange/grid invariants).
@@ -569,6 +571,164 @@ static int apply_all(const bfctx *cp, int namp, const cplx *a, const cplx *b, in
         free(Y); free(Uo);
     }
     return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O8: the adjoint apply K* (needed by Scenario 2 and FIO  */
+/* composition).  K*(xi_j, x_i) = conj(K(x_i, xi_j)), so    */
+/* with eqn:tg and eqn:BFM  K* ~ sum_k conj(b_k) o BF* (conj(a_k) o .)  and    */
+/* BF* = V^* G_{l0+1}^* ... G_h^* Sw^* G_{h+1}^* ... G_D^* U^*: the factors of */
+/* O2-O6 conjugate-transposed and applied in reverse order.  Written as        */
+/* gathers (each output coefficient sums its own inputs), blocks generated on  */
+/* the fly from the same equations as O1-O7.  Y: N x nv over x; Uout over xi.  */
+/* ------------------------------------------------------------------------- */
+static int butterfly_adjoint(const bfctx *c, int64_t nv, const cplx *Y, cplx *Uout)
+{
+    const int r = c->r;
+    const int64_t N = c->N, n0 = c->n0;
+    cplx *d0 = malloc(sizeof(cplx) * (size_t)(N * r * nv));
+    cplx *d1 = malloc(sizeof(cplx) * (size_t)(N * r * nv));
+    if (!d0 || !d1) { free(d0); free(d1); return -2; }
+
+    /* O6*: gamma_D[a,b] = U[a,b]^* y_A for each T_X leaf a and b < n0 (pair a n0 + b at level D). */
+    {
+#pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < N; p++) {
+            const int64_t a = p / n0, b = p % n0;
+            cplx *U = malloc(sizeof(cplx) * (size_t)(n0 * r));
+            blk_term(c, a, b, U);
+            for (int t = 0; t < r; t++)
+                for (int64_t v = 0; v < nv; v++) {
+                    cplx s = 0;
+                    for (int64_t j = 0; j < n0; j++) s += conj(U[j * r + t]) * Y[(a * n0 + j) + v * N];
+                    d0[(p * r + t) * nv + v] = s;
+                }
+            free(U);
+        }
+    }
+    /* O5* / O4* / O3*: levels D .. l0+1 in reverse, the switch adjoint at l = h before G_h^*. */
+    for (int l = c->D; l >= c->l0; l--) {
+        if (l == c->h) {   /* O4*: gamma_h[p] = Sw[p]^* gamma_h[p] */
+            const int64_t nbh = (int64_t)1 << (c->LN - c->h);
+#pragma omp parallel for schedule(static)
+            for (int64_t p = 0; p < N; p++) {
+                cplx S[32 * 32];
+                blk_switch(c, p / nbh, p % nbh, S);
+                for (int s = 0; s < r; s++)
+                    for (int64_t v = 0; v < nv; v++) {
+                        cplx acc = 0;
+                        for (int t = 0; t < r; t++) acc += conj(S[t * r + s]) * d0[(p * r + t) * nv + v];
+                        d1[(p * r + s) * nv + v] = acc;
+                    }
+            }
+            cplx *tmp = d0; d0 = d1; d1 = tmp;
+        }
+        if (l > c->l0) {   /* G_l^*: pair q = (a', b') at level l-1 gathers from its parents (2a'+e, b'>>1) at l */
+            const int64_t nbl = (int64_t)1 << (c->LN - l);   /* b-range at level l   */
+            const int64_t nbq = 2 * nbl;                     /* b-range at level l-1 */
+#pragma omp parallel for schedule(static)
+            for (int64_t q = 0; q < N; q++) {
+                const int64_t a1 = q / nbq, b1 = q % nbq;
+                const int cc = (int)(b1 & 1);   /* q's B is child cc of the parents' B */
+                cplx W[2][32 * 64];
+                int64_t par[2];
+                for (int e = 0; e < 2; e++) {
+                    const int64_t a = 2 * a1 + e, b = b1 >> 1;
+                    par[e] = a * nbl + b;
+                    if (l <= c->h) blk_first(c, l, a, b, W[e]); else blk_second(c, l, a, b, W[e]);
+                }
+                for (int s = 0; s < r; s++)
+                    for (int64_t v = 0; v < nv; v++) {
+                        cplx acc = 0;
+                        for (int e = 0; e < 2; e++)
+                            for (int t = 0; t < r; t++)
+                                acc += conj(W[e][t * 2 * r + cc * r + s]) * d0[(par[e] * r + t) * nv + v];
+                        d1[(q * r + s) * nv + v] = acc;
+                    }
+            }
+            cplx *tmp = d0; d0 = d1; d1 = tmp;
+        }
+    }
+    /* O2*: u(xi) = sum_{a < n0} (V[a,b]^* gamma_{l0}[a,b])_xi for each leaf b of T_Omega. */
+    {
+        const int64_t nb = N >> c->l0;
+#pragma omp parallel for schedule(static)
+        for (int64_t b = 0; b < nb; b++) {
+            cplx *V = malloc(sizeof(cplx) * (size_t)(r * n0));
+            for (int64_t j = 0; j < n0; j++)
+                for (int64_t v = 0; v < nv; v++) Uout[(b * n0 + j) + v * N] = 0;
+            for (int64_t a = 0; a < n0; a++) {
+                const int64_t p = a * nb + b;
+                blk_init(c, a, b, V);
+                for (int64_t j = 0; j < n0; j++)
+                    for (int64_t v = 0; v < nv; v++) {
+                        cplx s = 0;
+                        for (int t = 0; t < r; t++) s += conj(V[t * n0 + j]) * d0[(p * r + t) * nv + v];
+                        Uout[(b * n0 + j) + v * N] += s;
+                    }
+            }
+            free(V);
+        }
+    }
+    free(d0); free(d1);
+    return 0;
+}
+
+/* G = K* F = sum_k conj(b_k) o BF*(conj(a_k) o F): F indexed by x (N x nrhs), G by xi. */
+int orc_bf_apply_adjoint(int kernel, int amp, int LN, int l0, int r, int64_t nrhs, const cplx *F, int64_t ldf,
+                         cplx *G, int64_t ldg, int64_t vchunk)
+{
+    bfctx c;
+    if (ctx_init(&c, kernel, LN, l0, r) || r > 32 || l0 > 6) return -1;
+    const int namp = orc_n_amp(amp);
+    if (namp < 1) return -1;
+    const int64_t N = c.N;
+    if (vchunk < 1) vchunk = 1;
+    cplx *a = malloc(sizeof(cplx) * (size_t)(N * namp)), *b = malloc(sizeof(cplx) * (size_t)(N * namp));
+    for (int k = 0; k < namp; k++) {
+        orc_amp_term(amp, LN, k, 0, a + k * N);
+        orc_amp_term(amp, LN, k, 1, b + k * N);
+    }
+    const int64_t nvec = nrhs * namp;
+    int rc = 0;
+    for (int64_t v0 = 0; v0 < nvec && !rc; v0 += vchunk) {
+        const int64_t nv = (nvec - v0 < vchunk) ? nvec - v0 : vchunk;
+        cplx *Y = malloc(sizeof(cplx) * (size_t)(N * nv)), *Uo = malloc(sizeof(cplx) * (size_t)(N * nv));
+        for (int64_t v = 0; v < nv; v++) {
+            const int64_t col = (v0 + v) / namp, k = (v0 + v) % namp;
+            for (int64_t i = 0; i < N; i++) Y[i + v * N] = conj(a[k * N + i]) * F[i + col * ldf];   /* conj(a_k) o f */
+        }
+        rc = butterfly_adjoint(&c, nv, Y, Uo);
+        for (int64_t v = 0; v < nv && !rc; v++) {
+            const int64_t col = (v0 + v) / namp, k = (v0 + v) % namp;
+            for (int64_t j = 0; j < N; j++) {
+                if (k == 0) G[j + col * ldg] = 0;
+                G[j + col * ldg] += conj(b[k * N + j]) * Uo[j + v * N];                       /* sum_k conj(b_k) o u_k */
+            }
+        }
+        free(Y); free(Uo);
+    }
+    free(a); free(b);
+    return rc;
+}
+
+/* O0*: the adjoint direct sum on a set of xi-rows:  out[q, c] = sum_i conj(alpha(x_i, xi_j) e^{2 pi i Phi(x_i, xi_j)})
+ * F[i, c] with j = rows[q] -- the definition of K* applied to F. */
+void orc_direct_adjoint_rows(int kernel, int amp, int LN, int64_t nrhs, const cplx *F, int64_t ldf,
+                             const int64_t *rows, int64_t nrows, cplx *out)
+{
+    const int64_t N = (int64_t)1 << LN;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < nrows; q++) {
+        const int64_t j = rows[q];
+        cplx *acc = calloc((size_t)nrhs, sizeof(cplx));
+        for (int64_t i = 0; i < N; i++) {
+            cplx K = conj(orc_alpha(amp, LN, i, j) * E(kernel, LN, i, j, +1, 1));
+            for (int64_t cidx = 0; cidx < nrhs; cidx++) acc[cidx] += K * F[i + cidx * ldf];
+        }
+        for (int64_t cidx = 0; cidx < nrhs; cidx++) out[q + cidx * nrows] = acc[cidx];
+        free(acc);
+    }
 }
 
 int orc_num_threads(void)
