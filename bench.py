@@ -156,23 +156,26 @@ def _self_launch(args) -> int:
     return subprocess.call(cmd)
 
 
-def cpu_oracle_sample(w, g0=None):
+def cpu_oracle_sample(w, g0=None, adjoint=False):
     """The oracle as it stands on the host cores: the config's full-N butterfly for ONE RHS column (its n_amp
     vectors), blocks generated on the fly in FP64 -- timed -- and, untimed, the accuracy triplet of that column
     on the eps^b row sample: oracle BF vs the direct sum (eps^b), the GPU column g0 vs the direct
     sum, and the GPU column vs the oracle BF on all N rows (the parity quantity, bar 1e-5)."""
     import oracle
     F = W.rhs(w.n, w.nrhs, w.seed, cols=[0])
+    bf_apply = oracle.bf_apply_adjoint if adjoint else oracle.bf_apply
+    direct = oracle.direct_adjoint_rows if adjoint else oracle.direct_rows
     t0 = time.perf_counter()
-    gb = oracle.bf_apply(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank, F)
+    gb = bf_apply(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank, F)
     dt = time.perf_counter() - t0
     out = {"value": w.n * 1 / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
            "seconds": dt,
            "sample": f"{w.name} at full N=2^{w.log2n}, 1 of {w.nrhs} RHS columns ({w.n_amp} amplitude vectors), "
-                     f"FP64 oracle incl. on-the-fly block generation; metric scaled per N*RHS"}
+                     f"FP64 oracle {'ADJOINT (O8) ' if adjoint else ''}incl. on-the-fly block generation; "
+                     f"metric scaled per N*RHS"}
     if g0 is not None:
         rows = W.sample_rows(w.n, w.seed)
-        gd = oracle.direct_rows(w.kernel, w.amp, w.log2n, F, rows)[:, 0]
+        gd = direct(w.kernel, w.amp, w.log2n, F, rows)[:, 0]
         out["accuracy"] = {"column": 0, "rows": len(rows), "eps": w.eps,
                            "eps_b_oracle_bf_vs_direct": float(oracle.rel_l2(gb[rows, 0], gd)),
                            "gpu_vs_direct": float(oracle.rel_l2(g0[rows].astype(np.complex128), gd)),
@@ -232,6 +235,8 @@ def main():
                     help="small vector batches: one transfer level per launch (BF_OPT_SMALL_BATCH = 0)")
     ap.add_argument("--band-compose", type=int, default=None, choices=[0, 1],
                     help="tensor-core band: composed two-level operator (1) or level by level (0) (BF_OPT_BAND_COMPOSE)")
+    ap.add_argument("--adjoint", action="store_true",
+                    help="time the adjoint apply K* (bf_plan_create_adjoint from the forward plan)")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -297,7 +302,14 @@ def main():
         rows = w.n // world
         F = np.asfortranarray(F[rank * rows:(rank + 1) * rows])
     else:
-        plan = bf.Plan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=chunk)
+        if args.adjoint:
+            # the forward plan only lends its compact factors (chunk 1: no workspace to speak of, no tensor-core
+            # images); the adjoint plan re-assembles them on the device, then the forward is released
+            fwd = bf.Plan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=1)
+            plan = fwd.adjoint(chunk)
+            fwd.destroy()
+        else:
+            plan = bf.Plan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=chunk)
         # this rank's RHS: columns [c0, c1) of the one seeded global batch (strong scaling)
         F = W.rhs(w.n, w.nrhs, w.seed) if world == 1 else W.rhs(w.n, w.nrhs, w.seed, cols=range(c0, c1))
     t_build = time.perf_counter() - t0
@@ -383,7 +395,7 @@ def main():
         roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "peak_source": "FP32 FFMA from unit counts: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 5)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = _ncu_traffic(args.config if not args.log2n else None, dom)
+    roof["traffic"] = _ncu_traffic(args.config if not (args.log2n or args.adjoint) else None, dom)
     roof["kernel"] = dom
     roof["tensor_cores"] = dom in tc_classes
     roof["avg_launch_ms"] = avg_s * 1e3
@@ -435,7 +447,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         g0 = None if args.index_shard else Gd[0].cpu().numpy()   # column 0 of the last timed apply
-        cpu = cpu_oracle_sample(w, g0)
+        cpu = cpu_oracle_sample(w, g0, adjoint=args.adjoint)
 
     if rank == 0:
         out = {
@@ -447,7 +459,7 @@ def main():
                       ", ".join(f"{k} 3xTF32" for k in sorted(tc_classes)) + ")")
                      if tc_classes else "c64 (fp32 FFMA)",
             "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel; factors from the host builder)",
-            "config": {"workload": args.config, "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
+            "config": {"workload": args.config + ("-adjoint" if args.adjoint else ""), "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
                        "nrhs_per_gpu": nloc, "global_batch": w.nrhs, "max_nrhs_chunk": chunk,
                        "parallelism": (f"index-sharded x{world} (level-h exchange: "
                                        + ("peer stores from the level-h launch)" if args.exchange == "fused"

@@ -135,6 +135,22 @@ typedef struct {
  * The plan is immutable afterwards. */
 bf_status_t bf_plan_create(const bf_desc_t *desc, int device, int64_t max_nrhs_chunk, bf_plan_t *out);
 
+/* The adjoint plan: G = K* F with K*(xi_j, x_i) = conj(K(x_i, xi_j)), i.e.
+ *      G = sum_k conj(b_k) o BF*(conj(a_k) o F),   BF* = (eqn:BFM)^*  (P:613-619),
+ * the operator Scenario 2 and FIO composition need.  F is indexed by x, G by xi (both
+ * N x nrhs column-major, as for bf_apply).  Built on the device from the finalized forward plan `fwd`
+ * (unsharded): the conjugate-transposed factors in reverse order ARE a butterfly of the same shape once the
+ * two trees swap roles (the adjoint's level-m pair (a, b) is the forward's level-(LN - m) pair (b, a)), so
+ * the adjoint plan's blocks are
+ *     V0~[a (N/n0) + b] = U[b n0 + a]^*,     U~[a n0 + b] = V0[b (N/n0) + a]^*,
+ *     XFER~_m[(a,b)](t, c r + s) = conj(XFER_{LN-m+1}[(2b+c, a>>1)](s, (a&1) r + t)),
+ *     amp_a~ = conj(amp_b),  amp_b~ = conj(amp_a)
+ * (the switch rides along inside the forward's level-h factor), and every bf_apply entry point and kernel
+ * class serves it unchanged.  Exact (data movement and conjugation).  The new plan owns its own copies and
+ * workspace (chunks of max_nrhs_chunk columns); `fwd` may be destroyed afterwards.
+ * Errors: BF_ERR_STATE if fwd is not finalized, BF_ERR_NOT_SUPPORTED for index-sharded plans, BF_ERR_OOM. */
+bf_status_t bf_plan_create_adjoint(bf_plan_t fwd, int64_t max_nrhs_chunk, bf_plan_t *out);
+
 /* Streaming construction (factors larger than host RAM): allocate the plan from the
  * shape fields of `meta` (array pointers ignored), upload stage blocks in any order
  * and ranges, then finalize.  block_begin/block_count count blocks of the stage

@@ -38,7 +38,7 @@ EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finaliz
            "bf_apply_host", "bf_apply_host_async", "bf_apply_host_wait", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing", "bf_plan_set_option",
            "bf_plan_destroy", "bf_last_error", "bf_abi_version", "bf_build_n_amp", "bf_build_amp", "bf_build_blocks",
            "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
-           "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated")
+           "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated", "bf_plan_create_adjoint")
 
 
 class BFError(RuntimeError):
@@ -100,6 +100,7 @@ def lib():
             "bf_plan_alloc": ([P(bf_desc_t), ctypes.c_int, i64, P(vp)], i32),
             "bf_plan_upload": ([vp, i32, i64, i64, vp, i32], i32),
             "bf_plan_finalize": ([vp], i32),
+            "bf_plan_create_adjoint": ([vp, i64, P(vp)], i32),
             "bf_apply": ([vp, vp, vp, i64, vp], i32),
             "bf_apply_ex": ([vp, vp, i64, vp, i64, i64, vp, sz, vp], i32),
             "bf_apply_host": ([vp, vp, vp, i64, vp], i32),
@@ -246,6 +247,15 @@ class Plan:
         h = ctypes.c_void_p()
         _check(lib().bf_plan_create(ctypes.byref(d), device, max_nrhs_chunk, ctypes.byref(h)))
         return cls(h.value)
+
+    def adjoint(self, max_nrhs_chunk: int | None = None) -> "Plan":
+        """bf_plan_create_adjoint: a new plan applying K* = sum_k conj(b_k) o BF*(conj(a_k) o .), built on the
+        device from this (finalized, unsharded) plan's factors."""
+        if max_nrhs_chunk is None:
+            max_nrhs_chunk = self.info()["max_nrhs_chunk"]
+        h = ctypes.c_void_p()
+        _check(lib().bf_plan_create_adjoint(self._h, max_nrhs_chunk, ctypes.byref(h)))
+        return Plan(h.value)
 
     # -- apply ---------------------------------------------------------------------
     def apply(self, F, G, nrhs: int, stream=None):

@@ -88,6 +88,13 @@ cudaError_t launch_compose_band(const Dims& d, int l_first, const float2* W1, co
 // Plan finalization: W[p] <- Sw[p] W[p] for npairs blocks (W column-major R x cols, Sw R x R).
 cudaError_t launch_fold_switch(const float2* Sw, float2* W, int64_t npairs, int R, int cols, cudaStream_t s);
 
+// Adjoint plan: the factors of K* (same butterfly shape) from a finalized forward plan's factors (switch folded
+// into the level-h factor): amplitudes conjugated and swapped, V0~ / U~ the conjugate transposes of U / V0 with
+// the pair index transposed, transfer levels reversed and re-assembled (bf_kernels.cu).
+cudaError_t launch_adjoint_factors(const Dims& d, const float2* amp_a, const float2* amp_b, const float2* v0,
+                                   const float2* u, const float2* const* xfer, float2* adj_amp_a, float2* adj_amp_b,
+                                   float2* adj_v0, float2* adj_u, float2* const* adj_xfer, cudaStream_t s);
+
 // SL (eqn:bf3 + eqn:tg): G[x, c] = sum_k a_k(x) sum_{b<n0} sum_t U[a n0 + b](j, t) in[a n0 + b](t)[c n_amp + k],
 // x = a n0 + j.
 cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,

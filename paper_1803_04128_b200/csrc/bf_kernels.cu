@@ -11,6 +11,7 @@
 // Coefficient layout (workspace): delta[pair][t][v], v < nv fastest,
 // v = c * n_amp + k (RHS column c, amplitude term k).  See DESIGN.md section 4.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 #include "bf_internal.h"
@@ -1037,6 +1038,80 @@ cudaError_t launch_fold_switch(const float2* Sw, float2* W, int64_t npairs, int 
     if (R > 16) return cudaErrorInvalidValue;
     const int64_t n = npairs * cols;
     fold_switch_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(Sw, W, npairs, R, cols);
+    return cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------------------
+// Adjoint plan (bf_plan_create_adjoint): K* = sum_k conj(b_k) o BF*(conj(a_k) o .), and BF* is the factor
+// product of eqn:BFM conjugate-transposed in reverse order.  With the roles of the two trees
+// swapped (the adjoint's level-m pair (a~, b~) is the forward's level-(LN - m) pair (b~, a~)) BF* is a
+// butterfly of the same shape, so the adjoint runs the forward kernels on re-assembled blocks.  Pure data
+// movement plus conjugation: exact.
+// ---------------------------------------------------------------------------
+namespace {
+
+// out block q = x K2 + y (cols_in x rows_in, column-major) = conj(in block p = y K1 + x)^T (rows_in x cols_in)
+__global__ void adj_leaf_kernel(const float2* __restrict__ in, float2* __restrict__ out, int rows_in, int cols_in,
+                                int64_t K1, int64_t K2, int64_t total)
+{
+    const int64_t per = int64_t(rows_in) * cols_in;
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t q = g / per;
+        const int e = int(g % per);
+        const int i = e % cols_in, j = e / cols_in;   // out(i, j): i < cols_in, j < rows_in
+        const int64_t p = (q % K2) * K1 + q / K2;
+        const float2 v = in[p * per + int64_t(i) * rows_in + j];
+        out[g] = make_float2(v.x, -v.y);
+    }
+}
+
+// adjoint transfer level m (output pairs (a~, b~), b~ < 2^lnb, lnb = LN - m) from the forward factor of level
+// LN - m + 1, whose pairs are (a, b) with b < 2^(m-1):
+//   W~[(a~,b~)](t, c r + s) = conj(W[(2 b~ + c) 2^(m-1) + (a~ >> 1)](s, (a~ & 1) r + t))
+__global__ void adj_xfer_kernel(const float2* __restrict__ W, float2* __restrict__ out, int R, int lnb, int lfb,
+                                int64_t total)
+{
+    const int64_t per = 2 * int64_t(R) * R;
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t q = g / per;
+        const int e = int(g % per);
+        const int t = e % R, col = e / R, c = col / R, s = col % R;
+        const int64_t a = q >> lnb, b = q & ((int64_t(1) << lnb) - 1);
+        const int64_t qf = ((2 * b + c) << lfb) + (a >> 1);
+        const float2 v = W[qf * per + (int64_t(a & 1) * R + t) * R + s];
+        out[g] = make_float2(v.x, -v.y);
+    }
+}
+
+__global__ void conj_copy_kernel(const float2* __restrict__ in, float2* __restrict__ out, int64_t n)
+{
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
+        const float2 v = in[g];
+        out[g] = make_float2(v.x, -v.y);
+    }
+}
+
+unsigned grid_for(int64_t n) { return unsigned(std::min<int64_t>((n + 255) / 256, int64_t(148) * 16)); }
+
+}  // namespace
+
+cudaError_t launch_adjoint_factors(const Dims& d, const float2* amp_a, const float2* amp_b, const float2* v0,
+                                   const float2* u, const float2* const* xfer, float2* adj_amp_a, float2* adj_amp_b,
+                                   float2* adj_v0, float2* adj_u, float2* const* adj_xfer, cudaStream_t s)
+{
+    const int64_t N = d.N, n0 = int64_t(1) << d.l0, R = d.R, na = int64_t(d.n_amp) * N;
+    conj_copy_kernel<<<grid_for(na), 256, 0, s>>>(amp_b, adj_amp_a, na);   // pre-scale conj(a_k) ...
+    conj_copy_kernel<<<grid_for(na), 256, 0, s>>>(amp_a, adj_amp_b, na);   // ... post-scale conj(b_k)
+    // S0~ pair a~ (N/n0) + b~ = U[b~ n0 + a~]^*;  SL~ pair a~ n0 + b~ = V0[b~ (N/n0) + a~]^*
+    adj_leaf_kernel<<<grid_for(N * n0 * R), 256, 0, s>>>(u, adj_v0, int(n0), int(R), n0, N / n0, N * n0 * R);
+    adj_leaf_kernel<<<grid_for(N * n0 * R), 256, 0, s>>>(v0, adj_u, int(R), int(n0), N / n0, n0, N * n0 * R);
+    const int nx = d.D - d.l0;
+    for (int i = 0; i < nx; i++) {   // adjoint level m = l0 + 1 + i from forward level LN - m + 1 (index nx - 1 - i)
+        const int m = d.l0 + 1 + i;
+        adj_xfer_kernel<<<grid_for(N * 2 * R * R), 256, 0, s>>>(xfer[nx - 1 - i], adj_xfer[i], int(R), d.LN - m, m - 1,
+                                                               N * 2 * R * R);
+    }
     return cudaGetLastError();
 }
 

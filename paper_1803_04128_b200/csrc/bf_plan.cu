@@ -164,6 +164,7 @@ struct bf_plan_s {
     // [shard][stage slot]: block ranges [begin, end) uploaded so far (finalize checks their union covers the stage)
     std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>> uploaded;
     bool finalized = false;
+    bool switch_in_factors = false;   // the factors already contain the switch (adjoint plans): finalize skips the fold
     size_t ws_bytes = 0;       // per shard
     // end-to-end staging (lazily allocated by bf_apply_host)
     float2* dF = nullptr;
@@ -870,6 +871,7 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
     // fold the switch into the factor that produces level h: XFER_h, or V0 when h == l0 (no transfer level
     // precedes h); the apply then has no separate switch product
     for (Shard& s : p->sh) {
+        if (p->switch_in_factors) break;
         const int n0 = 1 << p->d.l0;
         float2* target = (p->d.h > p->d.l0) ? s.xfer[p->d.h - p->d.l0 - 1] : s.v0;
         const int cols = (p->d.h > p->d.l0) ? 2 * p->d.R : n0;
@@ -927,6 +929,49 @@ bf_status_t bf_plan_create(const bf_desc_t* desc, int device, int64_t max_nrhs_c
     bf_status_t st = bf_plan_alloc(desc, device, max_nrhs_chunk, &p);
     if (st != BF_OK) return st;
     if ((st = upload_desc(desc, p)) != BF_OK) {
+        free_plan(p);
+        return st;
+    }
+    *out = p;
+    return BF_OK;
+}
+
+bf_status_t bf_plan_create_adjoint(bf_plan_t fwd, int64_t max_nrhs_chunk, bf_plan_t* out)
+{
+    if (!out) return fail(BF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!fwd) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
+    if (!fwd->finalized) return fail(BF_ERR_STATE, "forward plan not finalized");
+    if (fwd->mode != BF_SHARD_NONE) return fail(BF_ERR_NOT_SUPPORTED, "adjoint of an index-sharded plan");
+    const bfk::Dims& d = fwd->d;
+    bf_desc_t meta{};
+    meta.abi_version = BF_ABI_VERSION;
+    meta.log2n = d.LN;
+    meta.log2leaf = d.l0;
+    meta.rank = d.R;
+    meta.n_amp = d.n_amp;
+    meta.memory = BF_MEM_DEVICE;
+    bf_plan_t p = nullptr;
+    bf_status_t st = alloc_plan(&meta, fwd->device, max_nrhs_chunk, 1, 0, BF_SHARD_NONE, &p);
+    if (st != BF_OK) return st;
+    DeviceGuard g(p->device);
+    Shard& s = p->sh[0];
+    const Shard& f = fwd->sh[0];
+    cudaFree(s.sw);   // the forward's level-h factor carries the switch; its adjoint carries the adjoint switch
+    s.sw = nullptr;
+    p->switch_in_factors = true;
+    cudaError_t e = bfk::launch_adjoint_factors(d, f.amp_a, f.amp_b, f.v0, f.u, f.xfer.data(), s.amp_a, s.amp_b, s.v0,
+                                                s.u, s.xfer.data(), 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        free_plan(p);
+        return cuda_fail(e, "adjoint factors");
+    }
+    for (size_t slot = 0; slot < p->uploaded[0].size(); slot++) {
+        const int stage = slot < 5 ? int(slot) : BF_STAGE_XFER0 + int(slot) - 5;
+        p->uploaded[0][slot].push_back({0, stage_blocks(p, stage)});
+    }
+    if ((st = bf_plan_finalize(p)) != BF_OK) {
         free_plan(p);
         return st;
     }
