@@ -123,6 +123,18 @@ def stage_model(w, nvec, info):
     so it adds no work of its own."""
     N, n0, r, na, nrhs = w.n, w.leaf, w.rank, w.n_amp, nvec // w.n_amp
     c = 8  # bytes per complex64
+    if info.get("structured") and not info["tc_classes"]:
+        # structured factors (DESIGN.md 5.5): per (pair, vector) a phase cmul (6 flops) per input element and a
+        # real x complex MAC (4 flops) per Lagrange weight; one level per launch; level h dense (16 r^2)
+        io = c * 2 * N * r * nvec
+        return {
+            "s0": (N * nvec * (6 * n0 + 4 * r * n0) + 6 * N * nvec,
+                   c * (N * nrhs + na * N + N * n0 + N * r * nvec)),
+            "xfer_first_half": (N * nvec * (12 * r + 8 * r * r), io + c * N * 2 * r),
+            "xfer_switch": (16 * N * r * r * nvec, io + c * N * 2 * r * r),
+            "xfer_second_half": (N * nvec * (8 * r * r + 16 * r), io + c * N * 2 * r),
+            "sl": (N * nvec * n0 * (4 * r + 8) + 8 * N * nvec, c * (N * r * nvec + N * n0 + na * N + N * nrhs)),
+        }
     out = {
         "s0": (8 * N * n0 * r * nvec + 6 * N * nvec, c * (N * nrhs + na * N + N * n0 * r + N * r * nvec)),
         "sl": (8 * N * n0 * r * nvec + 8 * N * nvec, c * (N * r * nvec + N * n0 * r + na * N + N * nrhs)),
@@ -235,6 +247,8 @@ def main():
                     help="small vector batches: one transfer level per launch (BF_OPT_SMALL_BATCH = 0)")
     ap.add_argument("--band-compose", type=int, default=None, choices=[0, 1],
                     help="tensor-core band: composed two-level operator (1) or level by level (0) (BF_OPT_BAND_COMPOSE)")
+    ap.add_argument("--structured", action="store_true",
+                    help="structured interpolative factors: phases + shared Lagrange matrices (NEXT-1)")
     ap.add_argument("--adjoint", action="store_true",
                     help="time the adjoint apply K* (bf_plan_create_adjoint from the forward plan)")
     args = ap.parse_args()
@@ -308,6 +322,8 @@ def main():
             fwd = bf.Plan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=1)
             plan = fwd.adjoint(chunk)
             fwd.destroy()
+        elif args.structured:
+            plan = bf.Plan.build_fio_structured(bf.fio_of(w), device=local, max_nrhs_chunk=chunk)
         else:
             plan = bf.Plan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=chunk)
         # this rank's RHS: columns [c0, c1) of the one seeded global batch (strong scaling)
@@ -395,7 +411,7 @@ def main():
         roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "peak_source": "FP32 FFMA from unit counts: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 5)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = _ncu_traffic(args.config if not (args.log2n or args.adjoint) else None, dom)
+    roof["traffic"] = _ncu_traffic(args.config if not (args.log2n or args.adjoint or args.structured) else None, dom)
     roof["kernel"] = dom
     roof["tensor_cores"] = dom in tc_classes
     roof["avg_launch_ms"] = avg_s * 1e3
@@ -459,7 +475,8 @@ def main():
                       ", ".join(f"{k} 3xTF32" for k in sorted(tc_classes)) + ")")
                      if tc_classes else "c64 (fp32 FFMA)",
             "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel; factors from the host builder)",
-            "config": {"workload": args.config + ("-adjoint" if args.adjoint else ""), "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
+            "config": {"workload": args.config + ("-adjoint" if args.adjoint else "")
+                       + ("-structured" if args.structured else ""), "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
                        "nrhs_per_gpu": nloc, "global_batch": w.nrhs, "max_nrhs_chunk": chunk,
                        "parallelism": (f"index-sharded x{world} (level-h exchange: "
                                        + ("peer stores from the level-h launch)" if args.exchange == "fused"
@@ -468,7 +485,8 @@ def main():
                                             f"(q+1) {w.nrhs}/{world}) (no collective)"),
                        "l2": "no flush: the working set (F 2.1 GB, coefficients 43 GB/level, factors 25 GB) "
                              "exceeds the 126 MB L2",
-                       "tensor_core_classes": info["tc_classes"], "tc_weight_bytes": info["tc_weight_bytes"]},
+                       "tensor_core_classes": info["tc_classes"], "tc_weight_bytes": info["tc_weight_bytes"],
+                       "factor_bytes": info["factor_bytes"], "structured": bool(info["structured"])},
             "roofline": roof,
             "step_roofline": {"level_by_level_ms": lbl * 1e3, "fused_ms": fused * 1e3,
                               "frac_level_by_level": lbl * 1e3 / ms, "frac_fused": fused * 1e3 / ms,

@@ -121,6 +121,7 @@ typedef struct {
     int64_t tc_weight_bytes;     /* device bytes of the tensor-core leaf weight images (0 if not built) */
     int32_t tc_class_mask;       /* bit c set: kernel class c (bf_plan_timing numbering) runs on the tensor
                                     cores (3xTF32) for a full chunk of max_nrhs_chunk columns */
+    int32_t structured;          /* 1: the plan applies structured factors (bf_plan_create_structured) */
 } bf_plan_info_t;
 
 /* index sharding modes */
@@ -150,6 +151,51 @@ bf_status_t bf_plan_create(const bf_desc_t *desc, int device, int64_t max_nrhs_c
  * workspace (chunks of max_nrhs_chunk columns); `fwd` may be destroyed afterwards.
  * Errors: BF_ERR_STATE if fwd is not finalized, BF_ERR_NOT_SUPPORTED for index-sharded plans, BF_ERR_OOM. */
 bf_status_t bf_plan_create_adjoint(bf_plan_t fwd, int64_t max_nrhs_chunk, bf_plan_t *out);
+
+/* ---- structured plans: interpolative factors stored as phases + shared Lagrange ----
+ * Every interpolative block of Algorithm 4.1 is diag(phases) . L . diag(phases) with a real Lagrange matrix L
+ * that the whole level shares, because the grids of one level are translates of each other (eqn:gdA/gdB
+ * P:214-226; eqn:1 P:700, eqn:2 P:750, eqn:3 P:783, eqn:bf3 P:795).  A structured plan stores per pair
+ * only one phase diagonal per level -- the row phases of a level merged with the column phases of the next,
+ * since both act on the same coefficients -- and per level one L (the builder, bf_plan_build_fio_structured,
+ * writes them; DESIGN.md section 5.5 gives the formulas).  The coefficients between levels are then
+ *   eta_l  = e(+Phi(c_A, xi_t^B)) o delta_l   (levels l0 .. h-1)     zeta_l = e(-Phi(x_t^A, c_B)) o delta_l (l >= h)
+ * and the stages compute (all FP32; complex x real = 2 FMA):
+ *   BF_LEVEL_FIRST  (S0)  out[p](t)       = sum_j L(t, j) data[p][j] y_b[j]                    L: r x n0
+ *   BF_LEVEL_FIRST  (l)   out[p](t)       = sum_{c,s} L(t, c r + s) data[p][c r + s] in[q_c](s)   L: r x 2r
+ *   BF_LEVEL_SECOND (l)   out[p](t)       = sum_c data[p][c r + t] sum_s L_{a&1}(t, s) in[q_c](s)  L: 2 x r x r
+ *   BF_LEVEL_DENSE  (l)   out[p]          = data[p] [in[q_0]; in[q_1]]        data: [N][2r][r] as bf_desc_t.xfer
+ *   BF_LEVEL_DENSE  (S0)  out[p]          = data[p] y_b                       data: [N][n0][r] as bf_desc_t.v0
+ *   SL                    G[a n0 + j, c]  = sum_k a_k sum_{b<n0} sl_phase[a n0 + b][j] sum_t sl_lag(j, t) in[a n0+b](t)
+ * (q_c = (a>>1) 2^(LN-l+1) + 2b + c; every L column-major; L_e at offset e r^2).  There is no separate switch:
+ * the level-h factor (or V0 when h == l0) must carry it, with its neighbouring phases, as a DENSE level.
+ * Factor bytes per pair: n0 + 2r per structured level + 2 r^2 (level h) + n0, against r n0 + 2 r^2 per level + n0 r
+ * dense (cfg5: 17 GB instead of 110 GB).  Chunks that run on the tensor cores (nv >= 64) use dense blocks expanded from the
+ * structured ones at finalization (the plan then frees the structured arrays); every other chunk runs the
+ * structured kernels.  Unsharded only; bf_plan_create_adjoint returns BF_ERR_NOT_SUPPORTED for them. */
+#define BF_LEVEL_DENSE 0
+#define BF_LEVEL_FIRST 1
+#define BF_LEVEL_SECOND 2
+typedef struct {
+    int32_t kind;          /* BF_LEVEL_*                                                              */
+    const float *lag;      /* FIRST: r x 2r; SECOND: 2 x r x r; DENSE: unused (NULL)                  */
+    const bf_c64 *data;    /* FIRST / SECOND: [N][2r] phases; DENSE: [N][2r][r] blocks                */
+} bf_slevel_t;
+typedef struct {
+    int32_t abi_version;   /* BF_ABI_VERSION */
+    int32_t log2n, log2leaf, rank, n_amp;   /* as bf_desc_t */
+    int32_t memory;        /* BF_MEM_HOST / BF_MEM_DEVICE: where the arrays below live (lag arrays too)  */
+    const bf_c64 *amp_a, *amp_b;            /* [n_amp][N] */
+    int32_t s0_kind;       /* BF_LEVEL_FIRST (s0_lag r x n0, s0_data [N][n0]) or BF_LEVEL_DENSE (s0_data [N][n0][r]) */
+    const float *s0_lag;
+    const bf_c64 *s0_data;
+    const bf_slevel_t *xfer;                /* D - l0 levels, level l0 + 1 + i */
+    const float *sl_lag;   /* n0 x r */
+    const bf_c64 *sl_phase;                 /* [N][n0] */
+} bf_sdesc_t;
+/* Deep-copies the arrays (the caller may free them on return) and finalizes.  BF_ERR_INVALID_ARG for a missing
+ * array or an unknown kind; otherwise as bf_plan_create. */
+bf_status_t bf_plan_create_structured(const bf_sdesc_t *desc, int device, int64_t max_nrhs_chunk, bf_plan_t *out);
 
 /* Streaming construction (factors larger than host RAM): allocate the plan from the
  * shape fields of `meta` (array pointers ignored), upload stage blocks in any order

@@ -64,6 +64,22 @@ int64_t bf_build_block_elems(const bf_fio_t *k, int32_t stage);
 bf_status_t bf_plan_build_fio(const bf_fio_t *k, int device, int64_t max_nrhs_chunk, int64_t staging_bytes,
                               bf_plan_t *out);
 
+/* The same operator as structured factors (bf.h "structured plans", NEXT-1): phases and shared Lagrange
+ * matrices per level, the switch with its neighbouring phases as the dense level-h factor (V0 when h == l0).
+ * Built on the host in FP64 (phases and the dense level rounded to complex64, Lagrange matrices to FP32) and
+ * streamed into bf_plan_create_structured's layout in slices of at most staging_bytes. */
+bf_status_t bf_plan_build_fio_structured(const bf_fio_t *k, int device, int64_t max_nrhs_chunk,
+                                         int64_t staging_bytes, bf_plan_t *out);
+
+/* Host-side pieces of the structured factors (tests, custom plans): the per-pair data of one stage for blocks
+ * [block_begin, block_begin + block_count) -- BF_STAGE_V0: omega [n0] per pair (the dense r x n0 V0 with the
+ * switch when h == l0); BF_STAGE_XFER0 + i: psi (first half) / chi (second half) [2r] per pair, the dense
+ * r x 2r block at level h; BF_STAGE_U: Omega [n0] -- and the stage's Lagrange matrix (bf.h layouts: S0 r x n0,
+ * first r x 2r, second 2 x r x r, SL n0 x r; unused for the dense level h). */
+bf_status_t bf_build_structured(const bf_fio_t *k, int32_t stage, int64_t block_begin, int64_t block_count,
+                                bf_c64 *out);
+bf_status_t bf_build_structured_lag(const bf_fio_t *k, int32_t stage, float *out);
+
 /* Index-sharded construction (bf.h, "index-sharded plans"): rank `rank` of `world` builds only
  * its own blocks (1/world of every stage) and joins the NCCL communicator of nccl_unique_id. */
 bf_status_t bf_plan_build_fio_sharded(const bf_fio_t *k, int device, int32_t rank, int32_t world,

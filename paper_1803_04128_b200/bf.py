@@ -38,7 +38,9 @@ EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finaliz
            "bf_apply_host", "bf_apply_host_async", "bf_apply_host_wait", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing", "bf_plan_set_option",
            "bf_plan_destroy", "bf_last_error", "bf_abi_version", "bf_build_n_amp", "bf_build_amp", "bf_build_blocks",
            "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
-           "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated", "bf_plan_create_adjoint")
+           "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated", "bf_plan_create_adjoint",
+           "bf_plan_create_structured", "bf_plan_build_fio_structured", "bf_build_structured",
+           "bf_build_structured_lag")
 
 
 class BFError(RuntimeError):
@@ -62,7 +64,7 @@ class bf_plan_info_t(ctypes.Structure):
                 ("device", ctypes.c_int32), ("class_launches", ctypes.c_int32 * 6),
                 ("class_levels", ctypes.c_int32 * 6), ("world", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
                 ("sharding", ctypes.c_int32), ("rows_local", ctypes.c_int64), ("tc_weight_bytes", ctypes.c_int64),
-                ("tc_class_mask", ctypes.c_int32)]
+                ("tc_class_mask", ctypes.c_int32), ("structured", ctypes.c_int32)]
 
 
 class bf_fio_t(ctypes.Structure):
@@ -101,6 +103,10 @@ def lib():
             "bf_plan_upload": ([vp, i32, i64, i64, vp, i32], i32),
             "bf_plan_finalize": ([vp], i32),
             "bf_plan_create_adjoint": ([vp, i64, P(vp)], i32),
+            "bf_plan_create_structured": ([vp, ctypes.c_int, i64, P(vp)], i32),
+            "bf_build_structured": ([P(bf_fio_t), i32, i64, i64, vp], i32),
+            "bf_build_structured_lag": ([P(bf_fio_t), i32, vp], i32),
+            "bf_plan_build_fio_structured": ([P(bf_fio_t), ctypes.c_int, i64, i64, P(vp)], i32),
             "bf_apply": ([vp, vp, vp, i64, vp], i32),
             "bf_apply_ex": ([vp, vp, i64, vp, i64, i64, vp, sz, vp], i32),
             "bf_apply_host": ([vp, vp, vp, i64, vp], i32),
@@ -172,6 +178,19 @@ def build_blocks(k: bf_fio_t, stage: int, begin: int, count: int) -> np.ndarray:
     return out
 
 
+def build_structured(k: bf_fio_t, stage: int, begin: int, count: int, per: int) -> np.ndarray:
+    """Host builder: structured per-pair data of one stage (`per` complex64 per pair; bf_build.h)."""
+    out = np.zeros((count, per), np.complex64)
+    _check(lib().bf_build_structured(ctypes.byref(k), stage, begin, count, out.ctypes.data))
+    return out
+
+
+def build_structured_lag(k: bf_fio_t, stage: int, size: int) -> np.ndarray:
+    out = np.zeros(size, np.float32)
+    _check(lib().bf_build_structured_lag(ctypes.byref(k), stage, out.ctypes.data))
+    return out
+
+
 def nccl_unique_id() -> bytes:
     """128-byte ncclUniqueId (to broadcast to every rank of an index-sharded plan)."""
     buf = ctypes.create_string_buffer(128)
@@ -216,6 +235,15 @@ class Plan:
         """Host builder -> streaming upload -> finalized plan (bf_plan_build_fio)."""
         h = ctypes.c_void_p()
         _check(lib().bf_plan_build_fio(ctypes.byref(k), device, max_nrhs_chunk, staging_bytes, ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def build_fio_structured(cls, k: bf_fio_t, device: int = 0, max_nrhs_chunk: int = 1,
+                             staging_bytes: int = 256 << 20):
+        """Structured interpolative factors (phases + shared Lagrange matrices, NEXT-1) -> finalized plan."""
+        h = ctypes.c_void_p()
+        _check(lib().bf_plan_build_fio_structured(ctypes.byref(k), device, max_nrhs_chunk, staging_bytes,
+                                                  ctypes.byref(h)))
         return cls(h.value)
 
     @classmethod

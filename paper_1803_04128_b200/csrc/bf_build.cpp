@@ -215,6 +215,167 @@ void build_u(const Shape& S, int64_t p0, int64_t cnt, bf_c64* out)
     }
 }
 
+
+// ---------------------------------------------------------------------------------------------------------
+// Structured (interpolative) factors (include/bf.h "structured plans").  Every block of
+// Algorithm 4.1 is diag(row phases) . L . diag(column phases) with L the Lagrange matrix the whole level shares
+// (the grids of one level are translates).  The row phases of one level and the column phases of the
+// next act on the same coefficients, so they are merged: the plan carries eta_l = rowp_l^-1 o delta_l on the
+// first half and zeta_l = colp_{l+1} o delta_l on the second half, and stores per pair only
+//   S0:     omega[p][j]   = e(+Phi(c_A, xi_j))                                   (n0 per pair; L0 = M^B_t(xi_j))
+//   first:  psi[p][c r+s] = e(+Phi(c_A, xi_s^C)) e(-Phi(c_P, xi_s^C))            (2r;  L1 = M^B_t(xi_s^{C_c}))
+//   second: chi[p][c r+t] = e(+Phi(x_t^A, c_{C_c})) e(-Phi(x_t^A, c_B))          (2r;  L2_e = M^P_s(x_t^A))
+//   SL:     Omega[p][j]   = e(+Phi(x_j, c_B))                                    (n0;  L_SL = M^A_t(x_j))
+// with C = C_c = B(l-1, 2b+c), P = A(l-1, a>>1), e = a & 1.  Level h carries the switch with both
+// neighbouring phases as ONE dense r x 2r block (or a dense V0 when h == l0):
+//   W_h[p] = diag(e(-Phi(x_t^A, c_B))) Sw[p] diag(e(-Phi(c_A, xi_t^B))) L1 diag(psi_h[p]).
+// ---------------------------------------------------------------------------------------------------------
+inline cd rowp_first(const Shape& S, int l, int64_t a, int64_t b, const std::vector<int64_t>& gB, int t)
+{   // e(-Phi(c_A, xi_t^B)) for the level-l pair (a, b); gB = nodes(2^l, r)
+    const int64_t nA = S.N >> l, nB = int64_t(1) << l;
+    return expphi(S, mid(a * nA, nA), b * nB + gB[t], -1.0);
+}
+
+inline cd colp_second(const Shape& S, int l, int64_t a, int64_t b, const std::vector<int64_t>& gA, int t)
+{   // e(-Phi(x_t^A, c_B)) for the level-l pair (a, b); gA = nodes(N / 2^l, r)
+    const int64_t nA = S.N >> l, nB = int64_t(1) << l;
+    return expphi(S, a * nA + gA[t], mid(b * nB, nB), -1.0);
+}
+
+void st_lag_s0(const Shape& S, float* L)   // r x n0 column-major
+{
+    const auto g = nodes(S.n0, S.r);
+    for (int64_t j = 0; j < S.n0; j++)
+        for (int t = 0; t < S.r; t++) L[j * S.r + t] = float(lag(g, t, double(j)));
+}
+
+void st_lag_sl(const Shape& S, float* L)   // n0 x r column-major
+{
+    const auto g = nodes(S.n0, S.r);
+    for (int t = 0; t < S.r; t++)
+        for (int64_t j = 0; j < S.n0; j++) L[t * S.n0 + j] = float(lag(g, t, double(j)));
+}
+
+void st_lag_xfer(const Shape& S, int l, float* L)
+{
+    const int r = S.r;
+    const int64_t nB = int64_t(1) << l, nC = nB / 2, nA = S.N >> l;
+    if (l <= S.h) {   // r x 2r column-major: (t, c r + s) = M^B_t(xi_s^{C_c})
+        const auto gB = nodes(nB, r), gC = nodes(nC, r);
+        for (int c = 0; c < 2; c++)
+            for (int sidx = 0; sidx < r; sidx++)
+                for (int t = 0; t < r; t++) L[(c * r + sidx) * r + t] = float(lag(gB, t, double(c * nC + gC[sidx])));
+    } else {          // 2 x (r x r column-major): (e; t, s) = M^P_s(x_t^A), A the e-th child of P
+        const auto gA = nodes(nA, r), gP = nodes(2 * nA, r);
+        for (int e = 0; e < 2; e++)
+            for (int sidx = 0; sidx < r; sidx++)
+                for (int t = 0; t < r; t++) L[(e * r + sidx) * r + t] = float(lag(gP, sidx, double(e * nA + gA[t])));
+    }
+}
+
+// per-pair data of one structured stage: S0 omega, transfer psi / chi, SL Omega
+void st_phase(const Shape& S, int stage, int64_t p0, int64_t cnt, bf_c64* out)
+{
+    const int r = S.r;
+    const int64_t n0 = S.n0;
+    if (stage == BF_STAGE_V0) {
+        const int64_t nleaf = S.N >> S.l0, nA = S.N >> S.l0;
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < cnt; q++) {
+            const int64_t p = p0 + q, a = p / nleaf, b = p % nleaf;
+            for (int64_t j = 0; j < n0; j++) out[q * n0 + j] = c64(expphi(S, mid(a * nA, nA), b * n0 + j, +1.0));
+        }
+    } else if (stage == BF_STAGE_U) {
+        const int64_t nB = S.N >> S.l0;
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < cnt; q++) {
+            const int64_t p = p0 + q, a = p / n0, b = p % n0;
+            for (int64_t j = 0; j < n0; j++) out[q * n0 + j] = c64(expphi(S, a * n0 + j, mid(b * nB, nB), +1.0));
+        }
+    } else {
+        const int l = S.l0 + 1 + (stage - BF_STAGE_XFER0);
+        const int sh = S.LN - l;
+        const int64_t nB = int64_t(1) << l, nC = nB / 2, nA = S.N >> l;
+        if (l <= S.h) {
+            const auto gC = nodes(nC, r);
+#pragma omp parallel for schedule(static)
+            for (int64_t q = 0; q < cnt; q++) {
+                const int64_t p = p0 + q, a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
+                const int64_t cA = mid(a * nA, nA), cP = mid((a >> 1) * 2 * nA, 2 * nA);
+                for (int c = 0; c < 2; c++)
+                    for (int sidx = 0; sidx < r; sidx++) {
+                        const int64_t xi = (2 * b + c) * nC + gC[sidx];
+                        out[q * 2 * r + c * r + sidx] = c64(expphi(S, cA, xi, +1.0) * expphi(S, cP, xi, -1.0));
+                    }
+            }
+        } else {
+            const auto gA = nodes(nA, r);
+#pragma omp parallel for schedule(static)
+            for (int64_t q = 0; q < cnt; q++) {
+                const int64_t p = p0 + q, a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
+                const int64_t cB = mid(b * nB, nB);
+                for (int c = 0; c < 2; c++) {
+                    const int64_t cC = mid((2 * b + c) * nC, nC);
+                    for (int t = 0; t < r; t++) {
+                        const int64_t x = a * nA + gA[t];
+                        out[q * 2 * r + c * r + t] = c64(expphi(S, x, cC, +1.0) * expphi(S, x, cB, -1.0));
+                    }
+                }
+            }
+        }
+    }
+}
+
+// The dense level-h factor of a structured plan (switch and both neighbouring phase diagonals folded in):
+// XFER_h blocks (r x 2r) when h > l0, else V0 blocks (r x n0).
+void st_dense_h(const Shape& S, int64_t p0, int64_t cnt, bf_c64* out)
+{
+    const int r = S.r, h = S.h, sh = S.LN - h;
+    const int64_t nA = S.N >> h, nB = int64_t(1) << h, nC = nB / 2;
+    const bool at_leaf = (h == S.l0);
+    const int64_t cols = at_leaf ? S.n0 : 2 * r;
+    const auto gA = nodes(nA, r), gB = nodes(nB, r);
+    std::vector<float> L(r * cols);
+    if (at_leaf) st_lag_s0(S, L.data()); else st_lag_xfer(S, h, L.data());
+    std::vector<bf_c64> ph(cols);
+#pragma omp parallel for schedule(static) firstprivate(ph)
+    for (int64_t q = 0; q < cnt; q++) {
+        const int64_t p = p0 + q, a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
+        // M = diag(rowp) L diag(colphase)   (r x cols), FP64
+        std::vector<cd> M(r * cols), Y(r * cols);
+        if (at_leaf) {
+            st_phase(S, BF_STAGE_V0, p, 1, ph.data());
+        } else {
+            // psi_h of this pair (same formula as the first-half levels)
+            const auto gC = nodes(nC, r);
+            const int64_t cA = mid(a * nA, nA), cP = mid((a >> 1) * 2 * nA, 2 * nA);
+            for (int c = 0; c < 2; c++)
+                for (int sidx = 0; sidx < r; sidx++) {
+                    const int64_t xi = (2 * b + c) * nC + gC[sidx];
+                    ph[c * r + sidx] = c64(expphi(S, cA, xi, +1.0) * expphi(S, cP, xi, -1.0));
+                }
+        }
+        cd rp[64], cp[64], Sw[64 * 64];
+        for (int t = 0; t < r; t++) {
+            rp[t] = rowp_first(S, h, a, b, gB, t);
+            cp[t] = colp_second(S, h, a, b, gA, t);
+            for (int sidx = 0; sidx < r; sidx++) Sw[t * r + sidx] = expphi(S, a * nA + gA[t], b * nB + gB[sidx], +1.0);
+        }
+        for (int64_t k = 0; k < cols; k++) {
+            const cd pk(ph[k].re, ph[k].im);
+            for (int t = 0; t < r; t++) M[k * r + t] = rp[t] * double(L[k * r + t]) * pk;
+        }
+        // Y = diag(colp) Sw M, Sw(t, s) = e(+Phi(x_t^A, xi_s^B))
+        for (int t = 0; t < r; t++)
+            for (int64_t k = 0; k < cols; k++) {
+                cd acc = 0;
+                for (int sidx = 0; sidx < r; sidx++) acc += Sw[t * r + sidx] * M[k * r + sidx];
+                Y[k * r + t] = cp[t] * acc;
+            }
+        bf_c64* o = out + q * r * cols;
+        for (int64_t k = 0; k < r * cols; k++) o[k] = c64(Y[k]);
+    }
+}
 }  // namespace
 
 extern "C" {
@@ -444,6 +605,149 @@ bf_status_t bf_plan_build_fio(const bf_fio_t* k, int device, int64_t max_nrhs_ch
                               bf_plan_t* out)
 {
     return build_plan(k, device, 1, 0, BF_SHARD_NONE, nullptr, max_nrhs_chunk, staging_bytes, out);
+}
+
+bf_status_t bf_build_structured(const bf_fio_t* k, int32_t stage, int64_t block_begin, int64_t block_count,
+                                bf_c64* out)
+{
+    Shape S;
+    if (!make_shape(k, &S)) return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_structured: bad kernel descriptor");
+    if (S.n0 > 64 || S.r > 16) return bfp_fail(BF_ERR_NOT_SUPPORTED, "bf_build_structured: leaf > 64 or rank > 16");
+    const bool xf = stage >= BF_STAGE_XFER0 && stage < BF_STAGE_XFER0 + (S.D - S.l0);
+    if (!(stage == BF_STAGE_V0 || stage == BF_STAGE_U || xf))
+        return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_structured: bad stage");
+    if (block_begin < 0 || block_count < 0 || block_begin + block_count > S.N || (!out && block_count))
+        return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_structured: bad block range");
+    const bool dense_h = (stage == BF_STAGE_V0 && S.h == S.l0) || (xf && S.l0 + 1 + (stage - BF_STAGE_XFER0) == S.h);
+    if (dense_h) st_dense_h(S, block_begin, block_count, out);
+    else st_phase(S, stage, block_begin, block_count, out);
+    return BF_OK;
+}
+
+bf_status_t bf_build_structured_lag(const bf_fio_t* k, int32_t stage, float* out)
+{
+    Shape S;
+    if (!make_shape(k, &S) || !out) return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_structured_lag: bad arguments");
+    if (stage == BF_STAGE_V0) st_lag_s0(S, out);
+    else if (stage == BF_STAGE_U) st_lag_sl(S, out);
+    else if (stage >= BF_STAGE_XFER0 && stage < BF_STAGE_XFER0 + (S.D - S.l0))
+        st_lag_xfer(S, S.l0 + 1 + (stage - BF_STAGE_XFER0), out);
+    else return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_structured_lag: bad stage");
+    return BF_OK;
+}
+
+bf_status_t bf_plan_build_fio_structured(const bf_fio_t* k, int device, int64_t max_nrhs_chunk, int64_t staging_bytes,
+                                         bf_plan_t* out)
+{
+    Shape S;
+    if (!out) return bfp_fail(BF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!make_shape(k, &S)) return bfp_fail(BF_ERR_INVALID_ARG, "bad kernel descriptor");
+    if (S.n0 > 64 || S.r > 16) return bfp_fail(BF_ERR_NOT_SUPPORTED, "structured build: leaf > 64 or rank > 16");
+    if (staging_bytes < (int64_t(1) << 20)) staging_bytes = int64_t(1) << 20;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        return bfp_fail(BF_ERR_INVALID_ARG, "bad device");
+    }
+    const int r = S.r, nx = S.D - S.l0, na = bf_build_n_amp(S.amp);
+    const int64_t N = S.N, n0 = S.n0;
+    // device staging of every stage (the plan deep-copies them; structured factors are small)
+    std::vector<void*> dev;
+    auto dalloc = [&](size_t bytes) -> void* {
+        void* x = nullptr;
+        if (cudaMalloc(&x, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        dev.push_back(x);
+        return x;
+    };
+    bf_status_t st = BF_OK;
+    std::vector<bf_c64> a(size_t(na) * N), b(size_t(na) * N);
+    bf_build_amp(k, a.data(), b.data());
+    std::vector<float> L0(r * n0), Lsl(n0 * r), Lx(size_t(nx) * 2 * r * r);
+    st_lag_s0(S, L0.data());
+    st_lag_sl(S, Lsl.data());
+    std::vector<bf_slevel_t> lv(nx);
+    bf_sdesc_t d{};
+    d.abi_version = BF_ABI_VERSION;
+    d.log2n = S.LN;
+    d.log2leaf = S.l0;
+    d.rank = r;
+    d.n_amp = na;
+    d.memory = BF_MEM_DEVICE;
+    d.amp_a = a.data();
+    d.amp_b = b.data();
+    d.s0_kind = (S.h == S.l0) ? BF_LEVEL_DENSE : BF_LEVEL_FIRST;
+    d.s0_lag = L0.data();
+    d.sl_lag = Lsl.data();
+    d.xfer = lv.data();
+    // stage list: (what, elems per pair, device array); what: -1 S0, -2 SL, i >= 0 transfer level index
+    std::vector<bf_c64> host(size_t(staging_bytes / sizeof(bf_c64)));
+    auto fill = [&](int what, int64_t per, bf_c64* dst) -> bool {
+        const int64_t chunk = std::max<int64_t>(1, int64_t(host.size()) / per);
+        for (int64_t p0 = 0; p0 < N; p0 += chunk) {
+            const int64_t cnt = std::min(chunk, N - p0);
+            if (what == -1) {
+                if (S.h == S.l0) st_dense_h(S, p0, cnt, host.data()); else st_phase(S, BF_STAGE_V0, p0, cnt, host.data());
+            } else if (what == -2) {
+                st_phase(S, BF_STAGE_U, p0, cnt, host.data());
+            } else if (S.l0 + 1 + what == S.h) {
+                st_dense_h(S, p0, cnt, host.data());
+            } else {
+                st_phase(S, BF_STAGE_XFER0 + what, p0, cnt, host.data());
+            }
+            if (cudaMemcpy(dst + p0 * per, host.data(), size_t(cnt * per) * sizeof(bf_c64), cudaMemcpyHostToDevice) !=
+                cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+        }
+        return true;
+    };
+    do {
+        const int64_t s0per = (S.h == S.l0) ? n0 * r : n0;
+        bf_c64* s0d = static_cast<bf_c64*>(dalloc(size_t(N * s0per) * sizeof(bf_c64)));
+        bf_c64* sld = static_cast<bf_c64*>(dalloc(size_t(N * n0) * sizeof(bf_c64)));
+        if (!s0d || !sld) {
+            st = bfp_fail(BF_ERR_OOM, "structured build: staging allocation failed");
+            break;
+        }
+        if (!fill(-1, s0per, s0d) || !fill(-2, n0, sld)) {
+            st = bfp_fail(BF_ERR_CUDA, "structured build: upload failed");
+            break;
+        }
+        d.s0_data = s0d;
+        d.sl_phase = sld;
+        for (int i = 0; i < nx && st == BF_OK; i++) {
+            const int l = S.l0 + 1 + i;
+            const bool dense = (l == S.h);
+            const int64_t per = dense ? 2 * r * r : 2 * r;
+            bf_c64* xd = static_cast<bf_c64*>(dalloc(size_t(N * per) * sizeof(bf_c64)));
+            if (!xd) {
+                st = bfp_fail(BF_ERR_OOM, "structured build: staging allocation failed");
+                break;
+            }
+            if (!fill(i, per, xd)) {
+                st = bfp_fail(BF_ERR_CUDA, "structured build: upload failed");
+                break;
+            }
+            lv[i].kind = dense ? BF_LEVEL_DENSE : (l <= S.h ? BF_LEVEL_FIRST : BF_LEVEL_SECOND);
+            lv[i].data = xd;
+            lv[i].lag = nullptr;
+            if (!dense) {
+                st_lag_xfer(S, l, Lx.data() + size_t(i) * 2 * r * r);
+                lv[i].lag = Lx.data() + size_t(i) * 2 * r * r;
+            }
+        }
+        if (st != BF_OK) break;
+        st = bf_plan_create_structured(&d, device, max_nrhs_chunk, out);
+    } while (false);
+    for (void* x : dev) cudaFree(x);
+    if (prev >= 0) cudaSetDevice(prev);
+    return st;
 }
 
 bf_status_t bf_plan_build_fio_sharded(const bf_fio_t* k, int device, int32_t rank, int32_t world,

@@ -95,6 +95,18 @@ cudaError_t launch_adjoint_factors(const Dims& d, const float2* amp_a, const flo
                                    const float2* u, const float2* const* xfer, float2* adj_amp_a, float2* adj_amp_b,
                                    float2* adj_v0, float2* adj_u, float2* const* adj_xfer, cudaStream_t s);
 
+// Structured interpolative factors (bf_struct.cu, NEXT-1): generic kernels (any nv, one level per launch).
+// kind: 1 = first-half level (L1 r x 2r, psi [N][2r]), 2 = second-half level (L2 2 x r x r, chi [N][2r]).
+cudaError_t launch_s0_st(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* L0,
+                         const float2* om, float2* out, int nv, cudaStream_t s);
+cudaError_t launch_xfer_st(const Dims& d, int l, int kind, const float* L, const float2* ph, const float2* in,
+                           float2* out, int nv, cudaStream_t s);
+cudaError_t launch_sl_st(const Dims& d, const float2* in, const float* Lsl, const float2* Om, const float2* ampa,
+                         float2* G, int64_t ldg, int nv, cudaStream_t s);
+// dense blocks of a structured stage (kind 0 S0, 1 first, 2 second, 3 SL; l = the transfer level for 1/2)
+cudaError_t launch_expand_st(const Dims& d, int kind, int l, const float* L, const float2* ph, float2* out,
+                             cudaStream_t s);
+
 // SL (eqn:bf3 + eqn:tg): G[x, c] = sum_k a_k(x) sum_{b<n0} sum_t U[a n0 + b](j, t) in[a n0 + b](t)[c n_amp + k],
 // x = a n0 + j.
 cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,

@@ -146,6 +146,21 @@ struct Shard {
     float* v0x = nullptr;      // tensor-core image of V0 / U (bf_tc.cu), built at finalize when used
     float* ux = nullptr;
     float2* ws = nullptr;      // two coefficient arrays of (N/G) R nv_max
+    // structured plans (bf_struct.cu, NEXT-1): a stage whose dense array above is null runs on these
+    float* s0_lag = nullptr;   // r x n0
+    float2* s0_ph = nullptr;   // [N][n0]
+    std::vector<int> kind;     // per transfer level: BF_LEVEL_*
+    std::vector<float*> lag;   // per transfer level (structured kinds): L1 r x 2r or L2 2 x r x r
+    std::vector<float2*> ph;   // per transfer level (structured kinds): [N][2r]
+    float* sl_lag = nullptr;   // n0 x r
+    float2* sl_ph = nullptr;   // [N][n0]
+    bool dense_all() const
+    {
+        if (!v0 || !u) return false;
+        for (auto x : xfer)
+            if (!x) return false;
+        return true;
+    }
 };
 
 struct bf_plan_s {
@@ -164,7 +179,8 @@ struct bf_plan_s {
     // [shard][stage slot]: block ranges [begin, end) uploaded so far (finalize checks their union covers the stage)
     std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>> uploaded;
     bool finalized = false;
-    bool switch_in_factors = false;   // the factors already contain the switch (adjoint plans): finalize skips the fold
+    bool switch_in_factors = false;   // the factors already contain the switch (adjoint and structured plans)
+    bool structured = false;          // built by bf_plan_create_structured
     size_t ws_bytes = 0;       // per shard
     // end-to-end staging (lazily allocated by bf_apply_host)
     float2* dF = nullptr;
@@ -302,6 +318,12 @@ void free_plan(bf_plan_s* p)
         for (auto x : s.xfer) cudaFree(x);
         for (auto x : s.cmp) cudaFree(x);
         cudaFree(s.ws);
+        cudaFree(s.s0_lag);
+        cudaFree(s.s0_ph);
+        cudaFree(s.sl_lag);
+        cudaFree(s.sl_ph);
+        for (auto x : s.lag) cudaFree(x);
+        for (auto x : s.ph) cudaFree(x);
     }
     cudaFree(p->dF);
     cudaFree(p->dG);
@@ -380,11 +402,15 @@ void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool
 // when the band kernel supports the shape, the switch applied inside the launch that produces level h),
 // SL.  With no transfer level (h == l0) the switch runs alone after S0.  Sharded: the bands stop at h,
 // the exchange follows, then the second half.
-std::vector<Step> schedule(const bfk::Dims& d, int nv, bool sharded, bool small_batch)
+std::vector<Step> schedule(const bf_plan_s* p, int nv)
 {
+    const bfk::Dims& d = p->d;
+    const bool sharded = p->mode != BF_SHARD_NONE, small_batch = p->small_batch;
     std::vector<Step> st;
     st.push_back({Step::S0, 0, 1, bfk::KC_S0, 0});
-    const bool band = bfk::band_supported(d.R, nv) || (small_batch && bfk::band_sv_supported(d, nv));
+    // structured plans without dense blocks: one level per launch (bf_struct.cu)
+    const bool band = p->sh[0].dense_all() &&
+                      (bfk::band_supported(d.R, nv) || (small_batch && bfk::band_sv_supported(d, nv)));
     if (!sharded) {
         push_levels(st, d, d.l0 + 1, d.D, band);
     } else {
@@ -455,11 +481,15 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
             case Step::S0:
                 if (p->tensor_cores && sh.v0x && bfk::s0_tc_supported(dl, nv, ldf))
                     return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s, p->leaf_multicast);
+                if (!sh.v0) return bfk::launch_s0_st(dl, F, ldf, sh.amp_b, sh.s0_lag, sh.s0_ph, in, nv, s);
                 if (p->small_batch && nv < 64 && bfk::s0_sv_supported(dl, nv))
                     return bfk::launch_s0_sv(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
                 return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
-            case Step::XFER:
-                return bfk::launch_xfer(dl, lk, in, out, sh.xfer[stp.l_first - p->d.l0 - 1], nv, s, rh, rhg, po);
+            case Step::XFER: {
+                const int li = stp.l_first - p->d.l0 - 1;
+                if (!sh.xfer[li]) return bfk::launch_xfer_st(dl, lk, sh.kind[li], sh.lag[li], sh.ph[li], in, out, nv, s);
+                return bfk::launch_xfer(dl, lk, in, out, sh.xfer[li], nv, s, rh, rhg, po);
+            }
             case Step::BAND: {
                 const float2* W[2] = {sh.xfer[stp.l_first - p->d.l0 - 1],
                                       stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
@@ -473,6 +503,7 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
             case Step::SL:
                 if (p->tensor_cores && sh.ux && bfk::sl_tc_supported(dl, nv))
                     return bfk::launch_sl_tc(dl, in, sh.ux, sh.amp_a, G, ldg, nv, s, p->leaf_multicast);
+                if (!sh.u) return bfk::launch_sl_st(dl, in, sh.sl_lag, sh.sl_ph, sh.amp_a, G, ldg, nv, s);
                 if (p->small_batch && bfk::sl_sv_supported(dl, nv))
                     return bfk::launch_sl_sv(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
                 return bfk::launch_sl(dl, in, sh.u, sh.amp_a, G, ldg, nv, s);
@@ -612,7 +643,7 @@ bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, in
     for (int64_t c0 = 0; c0 < nrhs; c0 += chunk) {
         const int64_t nc = std::min(chunk, nrhs - c0);
         const int nv = int(nc * p->d.n_amp);
-        const auto st = schedule(p->d, nv, sharded, p->small_batch);
+        const auto st = schedule(p, nv);
         const float2* Fc = F + c0 * ldf;
         float2* Gc = G + c0 * ldg;
         if (!sharded) {
@@ -661,7 +692,7 @@ bf_status_t apply_impl(bf_plan_s* p, const float2* F, int64_t ldf, float2* G, in
 }
 
 bf_status_t alloc_plan(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk, int world, int rank, int mode,
-                       bf_plan_t* out)
+                       bf_plan_t* out, bool dense_factors = true)
 {
     if (!out) return fail(BF_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
@@ -699,10 +730,17 @@ bf_status_t alloc_plan(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk
     for (auto& s : p->sh) {
         s.xfer.assign(nx, nullptr);
         s.cmp.assign(nx, nullptr);
+        s.kind.assign(nx, BF_LEVEL_DENSE);
+        s.lag.assign(nx, nullptr);
+        s.ph.assign(nx, nullptr);
         if ((st = dalloc(&s.amp_a, p->d.n_amp * n, "amp_a")) || (st = dalloc(&s.amp_b, p->d.n_amp * n, "amp_b")) ||
-            (st = dalloc(&s.v0, n * r * n0, "v0")) || (st = dalloc(&s.sw, n * r * r, "sw")) ||
-            (st = dalloc(&s.u, n * r * n0, "u")) ||
             (st = dalloc(&s.ws, int64_t(p->ws_bytes / sizeof(float2)), "workspace"))) {
+            free_plan(p);
+            return st;
+        }
+        if (!dense_factors) continue;   // structured plans allocate per stage (bf_plan_create_structured)
+        if ((st = dalloc(&s.v0, n * r * n0, "v0")) || (st = dalloc(&s.sw, n * r * r, "sw")) ||
+            (st = dalloc(&s.u, n * r * n0, "u"))) {
             free_plan(p);
             return st;
         }
@@ -846,12 +884,140 @@ bf_status_t build_leaf_images(bf_plan_s* p, Shard& s)
 }
 }  // namespace
 
+}  // extern "C"
+
+namespace {
+// Dense blocks from a structured plan's stages (bf_struct.cu expand_st_kernel), structured arrays released.
+bf_status_t expand_structured(bf_plan_s* p)
+{
+    const bfk::Dims d = p->local();
+    const int64_t n = p->nloc(), r = d.R, n0 = int64_t(1) << d.l0;
+    Shard& s = p->sh[0];
+    bf_status_t st = BF_OK;
+    cudaError_t e = cudaSuccess;
+    if (!s.v0) {
+        if ((st = dalloc(&s.v0, n * r * n0, "v0 (expanded)")) != BF_OK) return st;
+        e = bfk::launch_expand_st(d, 0, 0, s.s0_lag, s.s0_ph, s.v0, 0);
+    }
+    for (size_t i = 0; i < s.xfer.size() && e == cudaSuccess; i++) {
+        if (s.xfer[i]) continue;
+        if ((st = dalloc(&s.xfer[i], n * 2 * r * r, "xfer (expanded)")) != BF_OK) return st;
+        e = bfk::launch_expand_st(d, s.kind[i], d.l0 + 1 + int(i), s.lag[i], s.ph[i], s.xfer[i], 0);
+    }
+    if (e == cudaSuccess && !s.u) {
+        if ((st = dalloc(&s.u, n * r * n0, "u (expanded)")) != BF_OK) return st;
+        e = bfk::launch_expand_st(d, 3, 0, s.sl_lag, s.sl_ph, s.u, 0);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "structured factor expansion");
+    for (float** x : {&s.s0_lag, &s.sl_lag}) {
+        cudaFree(*x);
+        *x = nullptr;
+    }
+    for (float2** x : {&s.s0_ph, &s.sl_ph}) {
+        cudaFree(*x);
+        *x = nullptr;
+    }
+    for (size_t i = 0; i < s.xfer.size(); i++) {
+        cudaFree(s.lag[i]);
+        cudaFree(s.ph[i]);
+        s.lag[i] = nullptr;
+        s.ph[i] = nullptr;
+        s.kind[i] = BF_LEVEL_DENSE;
+    }
+    return BF_OK;
+}
+
+// copy `bytes` from host or device memory (UVA) into a new device array
+bf_status_t dcopy_v(void** dst, const void* src, size_t bytes, const char* what)
+{
+    if (!src) return fail(BF_ERR_INVALID_ARG, "structured descriptor: %s is NULL", what);
+    cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *dst = nullptr;
+        return fail(BF_ERR_OOM, "cudaMalloc(%s, %zu B) failed", what, bytes);
+    }
+    e = cudaMemcpy(*dst, src, bytes, cudaMemcpyDefault);
+    return e == cudaSuccess ? BF_OK : cuda_fail(e, what);
+}
+bf_status_t dcopy(float** dst, const void* src, size_t bytes, const char* what)
+{
+    return dcopy_v(reinterpret_cast<void**>(dst), src, bytes, what);
+}
+bf_status_t dcopy(float2** dst, const void* src, size_t bytes, const char* what)
+{
+    return dcopy_v(reinterpret_cast<void**>(dst), src, bytes, what);
+}
+}  // namespace
+
+extern "C" {
+
+bf_status_t bf_plan_create_structured(const bf_sdesc_t* sd, int device, int64_t max_nrhs_chunk, bf_plan_t* out)
+{
+    if (!out) return fail(BF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!sd) return fail(BF_ERR_INVALID_ARG, "descriptor is NULL");
+    bf_desc_t meta{};
+    meta.abi_version = sd->abi_version;
+    meta.log2n = sd->log2n;
+    meta.log2leaf = sd->log2leaf;
+    meta.rank = sd->rank;
+    meta.n_amp = sd->n_amp;
+    meta.memory = sd->memory;
+    if (sd->memory != BF_MEM_HOST && sd->memory != BF_MEM_DEVICE) return fail(BF_ERR_INVALID_ARG, "memory=%d", sd->memory);
+    if (sd->s0_kind != BF_LEVEL_FIRST && sd->s0_kind != BF_LEVEL_DENSE)
+        return fail(BF_ERR_INVALID_ARG, "s0_kind=%d", sd->s0_kind);
+    bf_plan_t p = nullptr;
+    bf_status_t st = alloc_plan(&meta, device, max_nrhs_chunk, 1, 0, BF_SHARD_NONE, &p, false);
+    if (st != BF_OK) return st;
+    DeviceGuard g(device);
+    p->structured = true;
+    p->switch_in_factors = true;
+    Shard& s = p->sh[0];
+    const int64_t N = p->d.N, r = p->d.R, n0 = int64_t(1) << p->d.l0, c8 = sizeof(float2);
+    const int nx = int(s.xfer.size());
+    auto done = [&](bf_status_t r2) {
+        if (r2 != BF_OK) free_plan(p);
+        return r2;
+    };
+    if (!sd->amp_a || !sd->amp_b || (nx > 0 && !sd->xfer)) return done(fail(BF_ERR_INVALID_ARG, "structured descriptor: NULL array"));
+    cudaError_t e = cudaMemcpy(s.amp_a, sd->amp_a, size_t(p->d.n_amp * N * c8), cudaMemcpyDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(s.amp_b, sd->amp_b, size_t(p->d.n_amp * N * c8), cudaMemcpyDefault);
+    if (e != cudaSuccess) return done(cuda_fail(e, "amplitudes"));
+    if (sd->s0_kind == BF_LEVEL_DENSE) {
+        if ((st = dcopy(&s.v0, sd->s0_data, size_t(N * r * n0 * c8), "s0_data (dense)")) != BF_OK) return done(st);
+    } else if ((st = dcopy(&s.s0_lag, sd->s0_lag, size_t(r * n0 * 4), "s0_lag")) != BF_OK ||
+               (st = dcopy(&s.s0_ph, sd->s0_data, size_t(N * n0 * c8), "s0_data")) != BF_OK) {
+        return done(st);
+    }
+    for (int i = 0; i < nx; i++) {
+        const bf_slevel_t& lv = sd->xfer[i];
+        if (lv.kind == BF_LEVEL_DENSE) {
+            if ((st = dcopy(&s.xfer[i], lv.data, size_t(N * 2 * r * r * c8), "xfer data (dense)")) != BF_OK) return done(st);
+        } else if (lv.kind == BF_LEVEL_FIRST || lv.kind == BF_LEVEL_SECOND) {
+            s.kind[i] = lv.kind;
+            if ((st = dcopy(&s.lag[i], lv.lag, size_t(2 * r * r * 4), "xfer lag")) != BF_OK ||
+                (st = dcopy(&s.ph[i], lv.data, size_t(N * 2 * r * c8), "xfer data")) != BF_OK)
+                return done(st);
+        } else {
+            return done(fail(BF_ERR_INVALID_ARG, "xfer[%d].kind=%d", i, lv.kind));
+        }
+    }
+    if ((st = dcopy(&s.sl_lag, sd->sl_lag, size_t(n0 * r * 4), "sl_lag")) != BF_OK ||
+        (st = dcopy(&s.sl_ph, sd->sl_phase, size_t(N * n0 * c8), "sl_phase")) != BF_OK)
+        return done(st);
+    if ((st = bf_plan_finalize(p)) != BF_OK) return done(st);
+    *out = p;
+    return BF_OK;
+}
+
 bf_status_t bf_plan_finalize(bf_plan_t p)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
     if (p->finalized) return fail(BF_ERR_STATE, "plan already finalized");
     const int nx = int(p->sh[0].xfer.size());
-    for (size_t i = 0; i < p->sh.size(); i++)
+    for (size_t i = 0; i < p->sh.size() && !p->structured; i++)
         for (int slot = 0; slot < 5 + nx; slot++) {
             const int stage = slot < 5 ? slot : BF_STAGE_XFER0 + (slot - 5);
             // union of the uploaded ranges: the first block not covered (overlapping or repeated uploads of
@@ -884,6 +1050,12 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
         cudaFree(s.sw);
         s.sw = nullptr;
     }
+    // structured plans whose chunks run on the tensor cores: those kernels take dense blocks -- expand every
+    // structured stage once (the structured arrays are then released; the plan behaves as a dense one)
+    const bfk::Dims dl0 = p->local();
+    if (p->structured && p->tensor_cores && bfk::leaf_tc_shape(dl0) && p->max_chunk * p->d.n_amp >= 64) {
+        if (bf_status_t st = expand_structured(p); st != BF_OK) return st;
+    }
     // tensor-core leaf weights: only when a chunk can be a dense contraction (nv >= 64 vectors)
     const bfk::Dims dl = p->local();
     if (p->tensor_cores && bfk::leaf_tc_shape(dl) && p->max_chunk * p->d.n_amp >= 64) {
@@ -899,7 +1071,7 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
     {
         const int nvf = int(p->max_chunk * p->d.n_amp);
         if (p->tensor_cores && nvf <= 256 && bfk::band_tc_supported(dl, nvf)) {
-            for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE, p->small_batch)) {
+            for (const auto& stp : schedule(p, nvf)) {
                 if (stp.kind != Step::BAND || stp.K != 2) continue;
                 const int li = stp.l_first - p->d.l0 - 1;
                 const int lk = (stp.l_first > p->d.h) ? stp.l_first - p->g : stp.l_first;
@@ -943,6 +1115,7 @@ bf_status_t bf_plan_create_adjoint(bf_plan_t fwd, int64_t max_nrhs_chunk, bf_pla
     if (!fwd) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
     if (!fwd->finalized) return fail(BF_ERR_STATE, "forward plan not finalized");
     if (fwd->mode != BF_SHARD_NONE) return fail(BF_ERR_NOT_SUPPORTED, "adjoint of an index-sharded plan");
+    if (!fwd->sh[0].dense_all()) return fail(BF_ERR_NOT_SUPPORTED, "adjoint of a structured plan");
     const bfk::Dims& d = fwd->d;
     bf_desc_t meta{};
     meta.abi_version = BF_ABI_VERSION;
@@ -1216,8 +1389,15 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     info->n = p->d.N;
     info->max_nrhs_chunk = p->max_chunk;
     // the switch blocks are folded into the level-h factor at finalize (freed afterwards)
-    info->factor_bytes = nsh * 8 * (2 * p->d.n_amp * n + 2 * n * r * n0 + (p->finalized ? 0 : n * r * r) +
-                                    int64_t(nx) * n * 2 * r * r);
+    info->factor_bytes = 0;
+    for (const Shard& s : p->sh) {
+        int64_t f = 2 * p->d.n_amp * n + (s.sw ? n * r * r : 0) + (s.v0 ? n * r * n0 : 0) + (s.u ? n * r * n0 : 0) +
+                    (s.s0_ph ? n * n0 : 0) + (s.sl_ph ? n * n0 : 0);
+        for (int i = 0; i < nx; i++) f += (s.xfer[i] ? n * 2 * r * r : 0) + (s.ph[i] ? n * 2 * r : 0);
+        info->factor_bytes += 8 * f;
+        info->factor_bytes += 4 * ((s.s0_lag ? r * n0 : 0) + (s.sl_lag ? r * n0 : 0));
+        for (int i = 0; i < nx; i++) info->factor_bytes += s.lag[i] ? 4 * 2 * r * r : 0;
+    }
     for (const Shard& s : p->sh)
         for (auto c : s.cmp)
             if (c) info->factor_bytes += 8 * n * 4 * r * r;   // precomposed band operators
@@ -1236,11 +1416,11 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
             mask |= 1 << bfk::KC_S0;
         if (p->tensor_cores && p->sh[0].ux && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
         if (p->tensor_cores && bfk::band_tc_supported(dl, nvf))
-            for (const auto& stp : schedule(p->d, nvf, p->mode != BF_SHARD_NONE, p->small_batch))
+            for (const auto& stp : schedule(p, nvf))
                 if (stp.kind == Step::BAND && stp.K == 2) mask |= 1 << stp.cls;
         info->tc_class_mask = mask;
     }
-    const auto st = schedule(p->d, int(p->max_chunk * p->d.n_amp), p->mode != BF_SHARD_NONE, p->small_batch);
+    const auto st = schedule(p, int(p->max_chunk * p->d.n_amp));
     info->launches_per_chunk = 0;
     for (int i = 0; i < BF_NUM_KCLASS; i++) info->class_launches[i] = info->class_levels[i] = 0;
     for (const auto& x : st) {
@@ -1254,6 +1434,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     info->shard_rank = p->rank;
     info->sharding = p->mode;
     info->rows_local = (p->mode == BF_SHARD_NCCL) ? n : p->d.N;
+    info->structured = p->structured ? 1 : 0;
     return BF_OK;
 }
 
