@@ -97,12 +97,24 @@ cudaError_t launch_adjoint_factors(const Dims& d, const float2* amp_a, const flo
 
 // Structured interpolative factors (bf_struct.cu, NEXT-1): generic kernels (any nv, one level per launch).
 // kind: 1 = first-half level (L1 r x 2r, psi [N][2r]), 2 = second-half level (L2 2 x r x r, chi [N][2r]).
-cudaError_t launch_s0_st(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* L0,
+// The Lagrange matrix of a stage travels BY VALUE in the kernel parameters (constant bank 0): with the loops over
+// its rows and columns unrolled, every weight is a compile-time constant-bank operand of its FFMA -- no load
+// instruction at all (a shared-memory copy cost one LDS per two FMAs and made the first version LDS-bound).
+// The plan keeps a host copy of every level's matrix for this.
+struct LagP {
+    float v[1024];   // >= max(r n0, 2 r^2) floats (r <= 16, n0 <= 64)
+};
+cudaError_t launch_s0_st(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const LagP& L0,
                          const float2* om, float2* out, int nv, cudaStream_t s);
-cudaError_t launch_xfer_st(const Dims& d, int l, int kind, const float* L, const float2* ph, const float2* in,
+cudaError_t launch_xfer_st(const Dims& d, int l, int kind, const LagP& L, const float2* ph, const float2* in,
                            float2* out, int nv, cudaStream_t s);
 cudaError_t launch_sl_st(const Dims& d, const float2* in, const float* Lsl, const float2* Om, const float2* ampa,
                          float2* G, int64_t ldg, int nv, cudaStream_t s);
+// two transfer levels l, l+1 per launch on structured (kind 1 / 2) or dense (kind 0) levels; L carries level l's
+// matrix at v[0] and level l+1's at v[512]; w1 / w2 the per-pair data (phases, or blocks for kind 0)
+bool band_st_supported(const Dims& d, int nv);
+cudaError_t launch_band_st(const Dims& d, int l, int k1, int k2, const LagP& L, const float2* w1, const float2* w2,
+                           const float2* in, float2* out, int nv, cudaStream_t s);
 // dense blocks of a structured stage (kind 0 S0, 1 first, 2 second, 3 SL; l = the transfer level for 1/2)
 cudaError_t launch_expand_st(const Dims& d, int kind, int l, const float* L, const float2* ph, float2* out,
                              cudaStream_t s);

@@ -154,6 +154,8 @@ struct Shard {
     std::vector<float2*> ph;   // per transfer level (structured kinds): [N][2r]
     float* sl_lag = nullptr;   // n0 x r
     float2* sl_ph = nullptr;   // [N][n0]
+    bfk::LagP s0_lagh{};            // host copies: the kernels take the Lagrange matrices as parameters
+    std::vector<bfk::LagP> lagh;
     bool dense_all() const
     {
         if (!v0 || !u) return false;
@@ -408,9 +410,10 @@ std::vector<Step> schedule(const bf_plan_s* p, int nv)
     const bool sharded = p->mode != BF_SHARD_NONE, small_batch = p->small_batch;
     std::vector<Step> st;
     st.push_back({Step::S0, 0, 1, bfk::KC_S0, 0});
-    // structured plans without dense blocks: one level per launch (bf_struct.cu)
-    const bool band = p->sh[0].dense_all() &&
-                      (bfk::band_supported(d.R, nv) || (small_batch && bfk::band_sv_supported(d, nv)));
+    // structured plans without dense blocks: bands of the structured kernels (bf_struct.cu) for small batches
+    const bool band = p->sh[0].dense_all()
+                          ? (bfk::band_supported(d.R, nv) || (small_batch && bfk::band_sv_supported(d, nv)))
+                          : (small_batch && bfk::band_st_supported(d, nv));
     if (!sharded) {
         push_levels(st, d, d.l0 + 1, d.D, band);
     } else {
@@ -481,18 +484,40 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
             case Step::S0:
                 if (p->tensor_cores && sh.v0x && bfk::s0_tc_supported(dl, nv, ldf))
                     return bfk::launch_s0_tc(dl, F, ldf, sh.amp_b, sh.v0x, in, nv, s, p->leaf_multicast);
-                if (!sh.v0) return bfk::launch_s0_st(dl, F, ldf, sh.amp_b, sh.s0_lag, sh.s0_ph, in, nv, s);
+                if (!sh.v0) return bfk::launch_s0_st(dl, F, ldf, sh.amp_b, sh.s0_lagh, sh.s0_ph, in, nv, s);
                 if (p->small_batch && nv < 64 && bfk::s0_sv_supported(dl, nv))
                     return bfk::launch_s0_sv(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
                 return bfk::launch_s0(dl, F, ldf, sh.amp_b, sh.v0, in, nv, s);
             case Step::XFER: {
                 const int li = stp.l_first - p->d.l0 - 1;
-                if (!sh.xfer[li]) return bfk::launch_xfer_st(dl, lk, sh.kind[li], sh.lag[li], sh.ph[li], in, out, nv, s);
+                if (!sh.xfer[li]) return bfk::launch_xfer_st(dl, lk, sh.kind[li], sh.lagh[li], sh.ph[li], in, out, nv, s);
+                if (p->small_batch && bfk::band_sv_supported(dl, nv)) {   // a lone dense level (structured plans)
+                    const float2* W1[2] = {sh.xfer[li], nullptr};
+                    return bfk::launch_band_sv(dl, lk, 1, in, out, W1, nv, s, rh, rhg, po);
+                }
                 return bfk::launch_xfer(dl, lk, in, out, sh.xfer[li], nv, s, rh, rhg, po);
             }
             case Step::BAND: {
-                const float2* W[2] = {sh.xfer[stp.l_first - p->d.l0 - 1],
-                                      stp.K > 1 ? sh.xfer[stp.l_first - p->d.l0] : nullptr};
+                const int li = stp.l_first - p->d.l0 - 1;
+                if (!sh.dense_all()) {   // structured plan (bf_struct.cu)
+                    if (stp.K == 1) {
+                        if (sh.xfer[li]) {
+                            const float2* W1[2] = {sh.xfer[li], nullptr};
+                            return bfk::launch_band_sv(dl, lk, 1, in, out, W1, nv, s, rh, rhg, po);
+                        }
+                        return bfk::launch_xfer_st(dl, lk, sh.kind[li], sh.lagh[li], sh.ph[li], in, out, nv, s);
+                    }
+                    bfk::LagP L2{};
+                    const int r2 = 2 * p->d.R * p->d.R;
+                    for (int i = 0; i < r2; i++) {
+                        L2.v[i] = sh.lagh[li].v[i];
+                        L2.v[512 + i] = sh.lagh[li + 1].v[i];
+                    }
+                    const int k1 = sh.xfer[li] ? 0 : sh.kind[li], k2 = sh.xfer[li + 1] ? 0 : sh.kind[li + 1];
+                    return bfk::launch_band_st(dl, lk, k1, k2, L2, sh.xfer[li] ? sh.xfer[li] : sh.ph[li],
+                                               sh.xfer[li + 1] ? sh.xfer[li + 1] : sh.ph[li + 1], in, out, nv, s);
+                }
+                const float2* W[2] = {sh.xfer[li], stp.K > 1 ? sh.xfer[li + 1] : nullptr};
                 if (stp.K == 2 && p->tensor_cores && bfk::band_tc_supported(dl, nv))
                     return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po, p->band,
                                                p->precompose ? sh.cmp[stp.l_first - p->d.l0 - 1] : nullptr);
@@ -732,6 +757,7 @@ bf_status_t alloc_plan(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk
         s.cmp.assign(nx, nullptr);
         s.kind.assign(nx, BF_LEVEL_DENSE);
         s.lag.assign(nx, nullptr);
+        s.lagh.assign(nx, bfk::LagP{});
         s.ph.assign(nx, nullptr);
         if ((st = dalloc(&s.amp_a, p->d.n_amp * n, "amp_a")) || (st = dalloc(&s.amp_b, p->d.n_amp * n, "amp_b")) ||
             (st = dalloc(&s.ws, int64_t(p->ws_bytes / sizeof(float2)), "workspace"))) {
@@ -968,6 +994,8 @@ bf_status_t bf_plan_create_structured(const bf_sdesc_t* sd, int device, int64_t 
     if (sd->memory != BF_MEM_HOST && sd->memory != BF_MEM_DEVICE) return fail(BF_ERR_INVALID_ARG, "memory=%d", sd->memory);
     if (sd->s0_kind != BF_LEVEL_FIRST && sd->s0_kind != BF_LEVEL_DENSE)
         return fail(BF_ERR_INVALID_ARG, "s0_kind=%d", sd->s0_kind);
+    if (sd->log2leaf > 6 || sd->rank > 16)
+        return fail(BF_ERR_NOT_SUPPORTED, "structured plans: leaf <= 64 and rank <= 16");
     bf_plan_t p = nullptr;
     bf_status_t st = alloc_plan(&meta, device, max_nrhs_chunk, 1, 0, BF_SHARD_NONE, &p, false);
     if (st != BF_OK) return st;
@@ -990,6 +1018,8 @@ bf_status_t bf_plan_create_structured(const bf_sdesc_t* sd, int device, int64_t 
     } else if ((st = dcopy(&s.s0_lag, sd->s0_lag, size_t(r * n0 * 4), "s0_lag")) != BF_OK ||
                (st = dcopy(&s.s0_ph, sd->s0_data, size_t(N * n0 * c8), "s0_data")) != BF_OK) {
         return done(st);
+    } else if ((e = cudaMemcpy(s.s0_lagh.v, s.s0_lag, size_t(r * n0 * 4), cudaMemcpyDeviceToHost)) != cudaSuccess) {
+        return done(cuda_fail(e, "s0_lag"));
     }
     for (int i = 0; i < nx; i++) {
         const bf_slevel_t& lv = sd->xfer[i];
@@ -1000,6 +1030,8 @@ bf_status_t bf_plan_create_structured(const bf_sdesc_t* sd, int device, int64_t 
             if ((st = dcopy(&s.lag[i], lv.lag, size_t(2 * r * r * 4), "xfer lag")) != BF_OK ||
                 (st = dcopy(&s.ph[i], lv.data, size_t(N * 2 * r * c8), "xfer data")) != BF_OK)
                 return done(st);
+            if ((e = cudaMemcpy(s.lagh[i].v, s.lag[i], size_t(2 * r * r * 4), cudaMemcpyDeviceToHost)) != cudaSuccess)
+                return done(cuda_fail(e, "xfer lag"));
         } else {
             return done(fail(BF_ERR_INVALID_ARG, "xfer[%d].kind=%d", i, lv.kind));
         }

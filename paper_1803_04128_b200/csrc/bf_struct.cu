@@ -11,9 +11,9 @@
 // FMAs against 4 for the dense complex block, and the factor stream per level drops from 2r^2 to 2r complex per
 // pair.  Level h (switch P:755-766 with both neighbouring phase diagonals) stays a dense block (bf_kernels.cu).
 //
-// This file holds the GENERIC kernels (any nv, one level per launch; a thread owns one (pair, vector) and all r
-// outputs, L staged in shared memory and read as warp-uniform broadcasts) and the expansion of structured
-// factors into dense blocks for the tensor-core path (plan finalization).
+// This file holds the kernels for any vector batch (one level per launch; a thread owns one (pair, vector) and
+// all r outputs, or one output row of SL) and the expansion of structured factors into dense blocks for the
+// tensor-core path (plan finalization).
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
@@ -31,44 +31,55 @@ __device__ __forceinline__ float2 cmul(const float2 a, const float2 b)
 
 unsigned grid_of(int64_t n, int block) { return unsigned((n + block - 1) / block); }
 
+// The Lagrange matrix of a stage travels BY VALUE in the kernel parameters (constant bank 0): with the loops over
+// its rows and columns fully unrolled every weight is a compile-time constant-bank operand of its FFMA -- no load
+// instruction at all (a shared-memory copy cost one LDS per two FMAs and made the first version LDS-bound).
+
+__device__ __forceinline__ void rmac(float2& acc, const float w, const float2 x)
+{
+    acc.x = fmaf(w, x.x, acc.x);
+    acc.y = fmaf(w, x.y, acc.y);
+}
+
+__device__ __forceinline__ void cmac(float2& acc, const float2 f, const float2 x)
+{
+    acc.x = fmaf(f.x, x.x, acc.x);
+    acc.x = fmaf(-f.y, x.y, acc.x);
+    acc.y = fmaf(f.x, x.y, acc.y);
+    acc.y = fmaf(f.y, x.x, acc.y);
+}
+
 // ---- S0: CTA = (leaf b, chunk of VC vectors); y_b staged in shared memory; thread = (a, vector) ----
 constexpr int S0_VC = 32;
 
-template <int R>
+template <int R, int N0>
 __global__ void __launch_bounds__(256) s0_st_kernel(const float2* __restrict__ F, int64_t ldf,
-                                                    const float2* __restrict__ ampb, const float* __restrict__ L0,
+                                                    const float2* __restrict__ ampb, const __grid_constant__ LagP L0,
                                                     const float2* __restrict__ om, float2* __restrict__ out, int LN,
-                                                    int l0, int n_amp, int nv)
+                                                    int n_amp, int nv)
 {
-    extern __shared__ __align__(16) unsigned char st_smem[];
-    const int n0 = 1 << l0;
-    const int64_t N = int64_t(1) << LN, nleaf = N >> l0;
-    float* Ls = reinterpret_cast<float*>(st_smem);                 // [n0][R]
-    float2* Y = reinterpret_cast<float2*>(st_smem + ((R * n0 * 4 + 15) / 16) * 16);   // [n0][VC]
+    __shared__ float2 Y[N0 * S0_VC];   // [j][vl]
+    const int64_t N = int64_t(1) << LN, nleaf = N / N0;
     const int64_t b = blockIdx.x;
     const int v0 = blockIdx.y * S0_VC, vc = min(S0_VC, nv - v0);
-    for (int i = threadIdx.x; i < R * n0; i += blockDim.x) Ls[i] = L0[i];
-    for (int i = threadIdx.x; i < n0 * vc; i += blockDim.x) {
-        const int j = i % n0, vl = i / n0, v = v0 + vl;
-        const int64_t x = b * n0 + j;
+    for (int i = threadIdx.x; i < N0 * vc; i += blockDim.x) {
+        const int j = i % N0, vl = i / N0, v = v0 + vl;
+        const int64_t x = b * N0 + j;
         Y[j * S0_VC + vl] = cmul(__ldg(ampb + int64_t(v % n_amp) * N + x), __ldg(F + x + int64_t(v / n_amp) * ldf));
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n0 * vc; i += blockDim.x) {
+    for (int i = threadIdx.x; i < N0 * vc; i += blockDim.x) {
         const int vl = i % vc, a = i / vc;
         const int64_t p = int64_t(a) * nleaf + b;
-        const float2* o = om + p * n0;
+        const float2* o = om + p * N0;
         float2 acc[R];
 #pragma unroll
         for (int t = 0; t < R; t++) acc[t] = make_float2(0.f, 0.f);
-        for (int j = 0; j < n0; j++) {
+#pragma unroll
+        for (int j = 0; j < N0; j++) {
             const float2 z = cmul(__ldg(o + j), Y[j * S0_VC + vl]);
 #pragma unroll
-            for (int t = 0; t < R; t++) {
-                const float w = Ls[j * R + t];
-                acc[t].x = fmaf(w, z.x, acc[t].x);
-                acc[t].y = fmaf(w, z.y, acc[t].y);
-            }
+            for (int t = 0; t < R; t++) rmac(acc[t], L0.v[j * R + t], z);
         }
         float2* dst = out + p * R * nv + v0 + vl;
 #pragma unroll
@@ -77,14 +88,32 @@ __global__ void __launch_bounds__(256) s0_st_kernel(const float2* __restrict__ F
 }
 
 // ---- one transfer level: thread = (output pair p, vector v) ----
+template <int R, int E>
+__device__ __forceinline__ void second_half(const LagP& L, const float2* __restrict__ php, const float2* __restrict__ x0,
+                                            const float2* __restrict__ x1, int nv, float2 (&acc)[R])
+{
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+        const float2* x = c ? x1 : x0;
+        float2 xs[R], z[R];
+#pragma unroll
+        for (int s = 0; s < R; s++) xs[s] = __ldg(x + int64_t(s) * nv);
+#pragma unroll
+        for (int t = 0; t < R; t++) z[t] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int s = 0; s < R; s++)
+#pragma unroll
+            for (int t = 0; t < R; t++) rmac(z[t], L.v[E * R * R + s * R + t], xs[s]);
+#pragma unroll
+        for (int t = 0; t < R; t++) cmac(acc[t], __ldg(php + c * R + t), z[t]);
+    }
+}
+
 template <int R, int KIND>
-__global__ void __launch_bounds__(256) xfer_st_kernel(const float* __restrict__ L, const float2* __restrict__ ph,
+__global__ void __launch_bounds__(256) xfer_st_kernel(const __grid_constant__ LagP L, const float2* __restrict__ ph,
                                                       const float2* __restrict__ in, float2* __restrict__ out, int LN,
                                                       int l, int nv, int64_t total)
 {
-    __shared__ float Ls[2 * R * R];
-    for (int i = threadIdx.x; i < 2 * R * R; i += blockDim.x) Ls[i] = L[i];
-    __syncthreads();
     const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (g >= total) return;
     const int64_t p = g / nv;
@@ -93,102 +122,207 @@ __global__ void __launch_bounds__(256) xfer_st_kernel(const float* __restrict__ 
     const int64_t a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
     const int64_t q0 = ((a >> 1) << (sh + 1)) + 2 * b;   // input pairs q0, q0 + 1 at level l - 1
     const float2* php = ph + p * 2 * R;
+    const float2* x0 = in + q0 * R * nv + v;
+    const float2* x1 = x0 + int64_t(R) * nv;
     float2 acc[R];
 #pragma unroll
     for (int t = 0; t < R; t++) acc[t] = make_float2(0.f, 0.f);
+    if (KIND == 1) {   // first half: phases on the inputs, then L1
 #pragma unroll
-    for (int c = 0; c < 2; c++) {
-        const float2* x = in + (q0 + c) * R * nv + v;
-        if (KIND == 1) {   // first half: phases on the inputs, then L1
+        for (int c = 0; c < 2; c++) {
+            const float2* x = c ? x1 : x0;
+            float2 y[R];
 #pragma unroll
-            for (int s = 0; s < R; s++) {
-                const float2 y = cmul(__ldg(php + c * R + s), __ldg(x + int64_t(s) * nv));
+            for (int s = 0; s < R; s++) y[s] = cmul(__ldg(php + c * R + s), __ldg(x + int64_t(s) * nv));
 #pragma unroll
-                for (int t = 0; t < R; t++) {
-                    const float w = Ls[(c * R + s) * R + t];
-                    acc[t].x = fmaf(w, y.x, acc[t].x);
-                    acc[t].y = fmaf(w, y.y, acc[t].y);
-                }
-            }
-        } else {           // second half: L2_e on each input, phases on the outputs
-            const float* Le = Ls + int(a & 1) * R * R;
-            float2 z[R];
+            for (int s = 0; s < R; s++)
 #pragma unroll
-            for (int t = 0; t < R; t++) z[t] = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int s = 0; s < R; s++) {
-                const float2 y = __ldg(x + int64_t(s) * nv);
-#pragma unroll
-                for (int t = 0; t < R; t++) {
-                    const float w = Le[s * R + t];
-                    z[t].x = fmaf(w, y.x, z[t].x);
-                    z[t].y = fmaf(w, y.y, z[t].y);
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < R; t++) {
-                const float2 f = __ldg(php + c * R + t);
-                acc[t].x = fmaf(f.x, z[t].x, acc[t].x);
-                acc[t].x = fmaf(-f.y, z[t].y, acc[t].x);
-                acc[t].y = fmaf(f.x, z[t].y, acc[t].y);
-                acc[t].y = fmaf(f.y, z[t].x, acc[t].y);
-            }
+                for (int t = 0; t < R; t++) rmac(acc[t], L.v[(c * R + s) * R + t], y[s]);
         }
+    } else {           // second half: L2_e on each input, phases on the outputs (e uniform over a warp's pairs
+                       // whenever 2^(LN-l) >= 32 / nv)
+        if (a & 1) second_half<R, 1>(L, php, x0, x1, nv, acc);
+        else second_half<R, 0>(L, php, x0, x1, nv, acc);
     }
     float2* dst = out + p * R * nv + v;
 #pragma unroll
     for (int t = 0; t < R; t++) dst[int64_t(t) * nv] = acc[t];
 }
 
-// ---- SL: CTA = (T_X leaf a, chunk of columns); thread = (row j, column c), the sum over k and b in registers
-constexpr int SL_CC = 4;
+// ---- two transfer levels per launch (l, l+1): a JOB is 4 consecutive input pairs 4j .. 4j+3 of level l-1,
+// closed under the two levels (SURVEY 8(a) fusion geometry; the slot algebra of band_sv_kernel in bf_small.cu):
+// level-l output (u, e) is pair ((2 a0 + e) << (LN - l)) + 2 bq + u, reading input slots 2u + c; level-(l+1)
+// output (u, e) is pair ((4 a0 + 2u + e) << shg) + bq, reading level-l slots 2c + u.  Thread = (job, output slot,
+// vector); level l reads its inputs from global memory (each input feeds two threads' pairs: the second read
+// hits L1), keeps its outputs in shared memory, level l+1 writes HBM.  Per level: kind 1 first half, 2 second
+// half, 0 dense block (the level carrying the switch).  L of level l at L.v[0], of level l+1 at L.v[512].
+template <int R, int KIND>
+__device__ __forceinline__ void level_out(const float* __restrict__ Lv, const float2* __restrict__ wp, int e,
+                                          const float2* __restrict__ x0, const float2* __restrict__ x1, int64_t sx,
+                                          float2 (&acc)[R])
+{
+#pragma unroll
+    for (int t = 0; t < R; t++) acc[t] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+        const float2* x = c ? x1 : x0;
+        float2 xs[R];
+#pragma unroll
+        for (int s = 0; s < R; s++) xs[s] = x[s * sx];
+        if (KIND == 1) {
+#pragma unroll
+            for (int s = 0; s < R; s++) {
+                const float2 y = cmul(__ldg(wp + c * R + s), xs[s]);
+#pragma unroll
+                for (int t = 0; t < R; t++) rmac(acc[t], Lv[(c * R + s) * R + t], y);
+            }
+        } else if (KIND == 2) {
+            float2 z[R];
+#pragma unroll
+            for (int t = 0; t < R; t++) z[t] = make_float2(0.f, 0.f);
+            if (e) {
+#pragma unroll
+                for (int s = 0; s < R; s++)
+#pragma unroll
+                    for (int t = 0; t < R; t++) rmac(z[t], Lv[R * R + s * R + t], xs[s]);
+            } else {
+#pragma unroll
+                for (int s = 0; s < R; s++)
+#pragma unroll
+                    for (int t = 0; t < R; t++) rmac(z[t], Lv[s * R + t], xs[s]);
+            }
+#pragma unroll
+            for (int t = 0; t < R; t++) cmac(acc[t], __ldg(wp + c * R + t), z[t]);
+        } else {   // dense r x 2r block, column-major
+#pragma unroll
+            for (int s = 0; s < R; s++)
+#pragma unroll
+                for (int t = 0; t < R; t++) cmac(acc[t], __ldg(wp + (c * R + s) * R + t), xs[s]);
+        }
+    }
+}
 
-template <int R>
+template <int R, int K1, int K2>
+__global__ void __launch_bounds__(256) band_st_kernel(const __grid_constant__ LagP L, const float2* __restrict__ w1,
+                                                      const float2* __restrict__ w2, const float2* __restrict__ in,
+                                                      float2* __restrict__ out, int LN, int l, int nv, int64_t njobs)
+{
+    extern __shared__ __align__(16) unsigned char st_smem[];
+    const int per_job = 4 * nv, jobs_cta = blockDim.x / per_job;
+    const int jl = threadIdx.x / per_job, os = (threadIdx.x / nv) % 4, v = threadIdx.x % nv;
+    const int u = os >> 1, e = os & 1;
+    const int shg = LN - l - 1;
+    float2* X1 = reinterpret_cast<float2*>(st_smem) + jl * 4 * R * nv;   // [slot][t][v] of this job
+    constexpr int WS1 = K1 == 0 ? 2 * R * R : 2 * R, WS2 = K2 == 0 ? 2 * R * R : 2 * R;
+    for (int64_t j0 = int64_t(blockIdx.x) * jobs_cta; j0 < njobs; j0 += int64_t(gridDim.x) * jobs_cta) {
+        const int64_t j = j0 + jl;
+        const bool live = jl < jobs_cta && j < njobs;
+        const int64_t a0 = j >> shg, bq = j & ((int64_t(1) << shg) - 1);
+        float2 acc[R];
+        if (live) {   // level l: output (u, e) from input slots 2u, 2u + 1 (global)
+            const int64_t p1 = (((a0 << 1) + e) << (LN - l)) + (bq << 1) + u;
+            const float2* x0 = in + (4 * j + 2 * u) * R * int64_t(nv) + v;
+            level_out<R, K1>(L.v, w1 + p1 * WS1, e, x0, x0 + int64_t(R) * nv, nv, acc);
+            float2* d = X1 + os * R * nv + v;
+#pragma unroll
+            for (int t = 0; t < R; t++) d[t * nv] = acc[t];
+        }
+        __syncthreads();
+        if (live) {   // level l + 1: output (u, e) from level-l slots u (c = 0) and u + 2 (c = 1)
+            const int64_t p2 = (((a0 << 2) + 2 * u + e) << shg) + bq;
+            const float2* x0 = X1 + u * R * nv + v;
+            level_out<R, K2>(L.v + 512, w2 + p2 * WS2, e, x0, x0 + 2 * R * nv, nv, acc);
+            float2* d = out + p2 * R * int64_t(nv) + v;
+#pragma unroll
+            for (int t = 0; t < R; t++) d[int64_t(t) * nv] = acc[t];
+        }
+        __syncthreads();
+    }
+}
+
+// ---- SL: CTA = (T_X leaf a, chunk of VC = VG VPT vectors).  The leaf's coefficients zeta[a n0 + b](t)[chunk]
+// (n0 r VC complex) and phases Omega[a n0 + b][j] (n0^2 complex) are staged in shared memory with cp.async by
+// every thread (high memory-level parallelism: the first version streamed them per warp from L2 and was latency-
+// bound); thread = (row j, vector group) holds its r weights Lsl(j, .) in registers and VPT accumulators; the
+// coefficient loads are broadcasts (all rows of a warp read the same address) ----
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+template <int R, int VPT>
 __global__ void __launch_bounds__(256) sl_st_kernel(const float2* __restrict__ in, const float* __restrict__ Lsl,
                                                     const float2* __restrict__ Om, const float2* __restrict__ ampa,
                                                     float2* __restrict__ G, int64_t ldg, int LN, int l0, int n_amp,
-                                                    int nrhs)
+                                                    int nv, int VG)
 {
     extern __shared__ __align__(16) unsigned char st_smem[];
-    const int n0 = 1 << l0;
     const int64_t N = int64_t(1) << LN;
-    const int nv = nrhs * n_amp;
-    float* Ls = reinterpret_cast<float*>(st_smem);   // [R][n0]
-    for (int i = threadIdx.x; i < R * n0; i += blockDim.x) Ls[i] = Lsl[i];
-    __syncthreads();
+    const int n0 = 1 << l0, VC = VG * VPT;
+    float2* Z = reinterpret_cast<float2*>(st_smem);   // [b][t][VC]
+    float2* Os = Z + n0 * R * VC;                      // [b][j]
     const int64_t a = blockIdx.x;
-    const int c0 = blockIdx.y * SL_CC, cc = min(SL_CC, nrhs - c0);
-    for (int i = threadIdx.x; i < n0 * cc; i += blockDim.x) {
-        const int j = i % n0, c = c0 + i / n0;
-        const int64_t x = a * n0 + j;
-        float2 g = make_float2(0.f, 0.f);
-        for (int k = 0; k < n_amp; k++) {
-            const int v = c * n_amp + k;
-            float2 u = make_float2(0.f, 0.f);
-            for (int b = 0; b < n0; b++) {
-                const int64_t p = a * n0 + b;
-                const float2* z = in + p * R * nv + v;
-                float2 s = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int t = 0; t < R; t++) {
-                    const float2 y = __ldg(z + int64_t(t) * nv);
-                    const float w = Ls[t * n0 + j];
-                    s.x = fmaf(w, y.x, s.x);
-                    s.y = fmaf(w, y.y, s.y);
-                }
-                const float2 f = __ldg(Om + p * n0 + j);
-                u.x = fmaf(f.x, s.x, u.x);
-                u.x = fmaf(-f.y, s.y, u.x);
-                u.y = fmaf(f.x, s.y, u.y);
-                u.y = fmaf(f.y, s.x, u.y);
-            }
-            const float2 am = __ldg(ampa + int64_t(k) * N + x);
-            g.x = fmaf(am.x, u.x, g.x);
-            g.x = fmaf(-am.y, u.y, g.x);
-            g.y = fmaf(am.x, u.y, g.y);
-            g.y = fmaf(am.y, u.x, g.y);
+    const int v0 = blockIdx.y * VC;
+    const float2* zsrc = in + a * n0 * R * int64_t(nv) + v0;
+    if (VPT >= 2) {   // 16-byte pieces: nv and v0 even
+        const int pr = VC / 2;   // pieces per (b, t) row
+        for (int i = threadIdx.x; i < n0 * R * pr; i += blockDim.x) {
+            const int row = i / pr, q = i % pr;
+            cp_async16(Z + row * VC + 2 * q, zsrc + int64_t(row) * nv + 2 * q);
         }
-        G[x + int64_t(c) * ldg] = g;
+    } else {
+        for (int i = threadIdx.x; i < n0 * R * VC; i += blockDim.x) Z[i] = __ldg(zsrc + int64_t(i / VC) * nv + i % VC);
+    }
+    const float2* osrc = Om + a * n0 * int64_t(n0);
+    for (int i = threadIdx.x; i < n0 * n0 / 2; i += blockDim.x) cp_async16(Os + 2 * i, osrc + 2 * i);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const int j = threadIdx.x % n0, vg = threadIdx.x / n0;
+    if (vg >= VG) return;
+    const int64_t x = a * n0 + j;
+    float Lr[R];
+#pragma unroll
+    for (int t = 0; t < R; t++) Lr[t] = __ldg(Lsl + t * n0 + j);
+    float2 acc[VPT];
+#pragma unroll
+    for (int q = 0; q < VPT; q++) acc[q] = make_float2(0.f, 0.f);
+    for (int b = 0; b < n0; b++) {
+        const float2* z = Z + (b * R) * VC + vg * VPT;
+        float2 sacc[VPT];
+#pragma unroll
+        for (int q = 0; q < VPT; q++) sacc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int t = 0; t < R; t++) {
+            float2 zt[VPT];
+            if constexpr (VPT == 1) {
+                zt[0] = z[t * VC];
+            } else {
+#pragma unroll
+                for (int q = 0; q < VPT / 2; q++) {
+                    const float4 f = reinterpret_cast<const float4*>(z + t * VC)[q];
+                    zt[2 * q] = make_float2(f.x, f.y);
+                    zt[2 * q + 1] = make_float2(f.z, f.w);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < VPT; q++) rmac(sacc[q], Lr[t], zt[q]);
+        }
+        const float2 f = Os[b * n0 + j];
+#pragma unroll
+        for (int q = 0; q < VPT; q++) cmac(acc[q], f, sacc[q]);
+    }
+    // a_k(x) and the sum over the n_amp vectors of each column (consecutive within the thread)
+    const int vb = v0 + vg * VPT;
+    float2 g = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < VPT; q++) {
+        const int k = q % n_amp;
+        cmac(g, __ldg(ampa + int64_t(k) * N + x), acc[q]);
+        if (k == n_amp - 1) {
+            G[x + int64_t((vb + q) / n_amp) * ldg] = g;
+            g = make_float2(0.f, 0.f);
+        }
     }
 }
 
@@ -207,9 +341,8 @@ __global__ void expand_st_kernel(const float* __restrict__ L, const float2* __re
         float w;
         float2 f;
         if (kind == 0) {
-            const int j = e / R;
             w = L[e];
-            f = ph[p * n0 + j];
+            f = ph[p * n0 + e / R];
         } else if (kind == 1) {
             w = L[e];
             f = ph[p * 2 * R + e / R];
@@ -218,9 +351,8 @@ __global__ void expand_st_kernel(const float* __restrict__ L, const float2* __re
             w = L[int((p >> sh) & 1) * R * R + s * R + t];
             f = ph[p * 2 * R + c * R + t];
         } else {
-            const int j = e % n0;
             w = L[e];
-            f = ph[p * n0 + j];
+            f = ph[p * n0 + e % n0];
         }
         out[g] = make_float2(w * f.x, w * f.y);
     }
@@ -238,24 +370,30 @@ __global__ void expand_st_kernel(const float* __restrict__ L, const float2* __re
     case 16: CALL(16); break;     \
     default: return cudaErrorInvalidValue; \
     }
+#define ST_N0(N0_, R, CALL)       \
+    switch (N0_) {                \
+    case 8: CALL(R, 8); break;    \
+    case 16: CALL(R, 16); break;  \
+    case 32: CALL(R, 32); break;  \
+    case 64: CALL(R, 64); break;  \
+    default: return cudaErrorInvalidValue; \
+    }
 
-cudaError_t launch_s0_st(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* L0,
+cudaError_t launch_s0_st(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const LagP& L0,
                          const float2* om, float2* out, int nv, cudaStream_t s)
 {
     const int n0 = 1 << d.l0;
-    const size_t shm = size_t((d.R * n0 * 4 + 15) / 16) * 16 + size_t(n0) * S0_VC * 8;
     const dim3 grid(unsigned(d.N >> d.l0), unsigned((nv + S0_VC - 1) / S0_VC));
-#define S0_CALL(R)                                                                                        \
-    {                                                                                                     \
-        cudaFuncSetAttribute(s0_st_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));     \
-        s0_st_kernel<R><<<grid, 256, shm, s>>>(F, ldf, ampb, L0, om, out, d.LN, d.l0, d.n_amp, nv);        \
-    }
-    ST_R(d.R, S0_CALL)
+    const int threads = std::min(256, ((n0 * std::min(nv, S0_VC) + 31) / 32) * 32);
+#define S0_CALL(R, N0) s0_st_kernel<R, N0><<<grid, threads, 0, s>>>(F, ldf, ampb, L0, om, out, d.LN, d.n_amp, nv)
+#define S0_N(R) ST_N0(n0, R, S0_CALL)
+    ST_R(d.R, S0_N)
+#undef S0_N
 #undef S0_CALL
     return cudaGetLastError();
 }
 
-cudaError_t launch_xfer_st(const Dims& d, int l, int kind, const float* L, const float2* ph, const float2* in,
+cudaError_t launch_xfer_st(const Dims& d, int l, int kind, const LagP& L, const float2* ph, const float2* in,
                            float2* out, int nv, cudaStream_t s)
 {
     const int64_t total = d.N * nv;
@@ -273,14 +411,63 @@ cudaError_t launch_xfer_st(const Dims& d, int l, int kind, const float* L, const
 cudaError_t launch_sl_st(const Dims& d, const float2* in, const float* Lsl, const float2* Om, const float2* ampa,
                          float2* G, int64_t ldg, int nv, cudaStream_t s)
 {
-    const int n0 = 1 << d.l0, nrhs = nv / d.n_amp;
-    const size_t shm = size_t(d.R) * n0 * 4;
-    const dim3 grid(unsigned(d.N >> d.l0), unsigned((nrhs + SL_CC - 1) / SL_CC));
-    const int threads = std::min(256, ((n0 * std::min(SL_CC, nrhs) + 31) / 32) * 32);
-#define SL_CALL(R) \
-    sl_st_kernel<R><<<grid, threads, shm, s>>>(in, Lsl, Om, ampa, G, ldg, d.LN, d.l0, d.n_amp, nrhs);
+    const int n0 = 1 << d.l0;
+    int vpt = 8;   // vectors per thread: a power of two dividing nv and a multiple of n_amp
+    while (vpt > 1 && (nv % vpt || vpt % d.n_amp)) vpt >>= 1;
+    if (vpt % d.n_amp) return cudaErrorInvalidValue;
+    int vg = 1;    // vector groups per CTA: up to 256 threads, at most ~100 KB of staged coefficients
+    while (vg < 4 && nv % (2 * vg * vpt) == 0 && n0 * 2 * vg <= 256 &&
+           size_t(n0) * d.R * 2 * vg * vpt * 8 <= 96 * 1024)
+        vg *= 2;
+    const int vc = vg * vpt;
+    const size_t shm = size_t(n0) * d.R * vc * 8 + size_t(n0) * n0 * 8;
+    const dim3 grid(unsigned(d.N >> d.l0), unsigned(nv / vc));
+    const int threads = n0 * vg < 32 ? 32 : n0 * vg;
+#define SL_GO(R, V)                                                                                                \
+    {                                                                                                              \
+        cudaFuncSetAttribute(sl_st_kernel<R, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));          \
+        sl_st_kernel<R, V><<<grid, threads, shm, s>>>(in, Lsl, Om, ampa, G, ldg, d.LN, d.l0, d.n_amp, nv, vg);    \
+    }
+#define SL_CALL(R)                      \
+    switch (vpt) {                      \
+    case 8: SL_GO(R, 8) break;          \
+    case 4: SL_GO(R, 4) break;          \
+    case 2: SL_GO(R, 2) break;          \
+    default: SL_GO(R, 1) break;         \
+    }
     ST_R(d.R, SL_CALL)
 #undef SL_CALL
+#undef SL_GO
+    return cudaGetLastError();
+}
+
+bool band_st_supported(const Dims& d, int nv) { return nv >= 1 && 4 * nv <= 256 && d.R <= 16; }
+
+cudaError_t launch_band_st(const Dims& d, int l, int k1, int k2, const LagP& L, const float2* w1, const float2* w2,
+                           const float2* in, float2* out, int nv, cudaStream_t s)
+{
+    if (!band_st_supported(d, nv)) return cudaErrorInvalidValue;
+    const int jobs_cta = 256 / (4 * nv);
+    const int threads = jobs_cta * 4 * nv;
+    const size_t shm = size_t(jobs_cta) * 4 * d.R * nv * 8;
+    const int64_t njobs = d.N / 4;
+    const unsigned grid = unsigned(std::min<int64_t>((njobs + jobs_cta - 1) / jobs_cta, int64_t(148) * 8));
+    const int kk = k1 * 3 + k2;
+#define B_GO(R, A, B)                                                                                              \
+    band_st_kernel<R, A, B><<<grid, threads, shm, s>>>(L, w1, w2, in, out, d.LN, l, nv, njobs)
+#define B_CALL(R)                                      \
+    switch (kk) {                                      \
+    case 1 * 3 + 1: B_GO(R, 1, 1); break;              \
+    case 2 * 3 + 2: B_GO(R, 2, 2); break;              \
+    case 1 * 3 + 0: B_GO(R, 1, 0); break;              \
+    case 0 * 3 + 2: B_GO(R, 0, 2); break;              \
+    case 0 * 3 + 1: B_GO(R, 0, 1); break;              \
+    case 2 * 3 + 0: B_GO(R, 2, 0); break;              \
+    default: return cudaErrorInvalidValue;             \
+    }
+    ST_R(d.R, B_CALL)
+#undef B_CALL
+#undef B_GO
     return cudaGetLastError();
 }
 
@@ -296,5 +483,6 @@ cudaError_t launch_expand_st(const Dims& d, int kind, int l, const float* L, con
 }
 
 #undef ST_R
+#undef ST_N0
 
 }  // namespace bfk

@@ -112,3 +112,18 @@ def test_structured_bad_descriptor():
     assert st == 1 and not h.value   # BF_ERR_INVALID_ARG: NULL arrays
     d.s0_kind = 7
     assert bf.lib().bf_plan_create_structured(ctypes.byref(d), 0, 1, ctypes.byref(h)) == 1
+
+
+@pytest.mark.parametrize("LN,l0,nrhs", [(16, 6, 8), (14, 5, 16), (12, 4, 1)])
+def test_structured_band_vs_single_levels(LN, l0, nrhs):
+    # the fused two-level structured band (BF_OPT_SMALL_BATCH = 1) against one level per launch: the first- and
+    # second-half levels compute in the same FP32 order (bitwise); the dense level h differs in order only
+    k = bf.fio(W.K_FIO, W.A_CFG1, LN, l0, 10)
+    F = W.rhs(1 << LN, nrhs, 91)
+    plan = bf.Plan.build_fio_structured(k, max_nrhs_chunk=nrhs)
+    G1 = gpu_apply(plan, F)
+    plan.set_option(bf.BF_OPT_SMALL_BATCH, 0)
+    G0 = gpu_apply(plan, F)
+    plan.destroy()
+    err = oracle.rel_l2(G1.astype(np.complex128), G0.astype(np.complex128), axis=0)
+    assert np.all(err <= 1e-6), err
