@@ -164,22 +164,25 @@ bf_status_t bf_plan_create_adjoint(bf_plan_t fwd, int64_t max_nrhs_chunk, bf_pla
  *   BF_LEVEL_FIRST  (S0)  out[p](t)       = sum_j L(t, j) data[p][j] y_b[j]                    L: r x n0
  *   BF_LEVEL_FIRST  (l)   out[p](t)       = sum_{c,s} L(t, c r + s) data[p][c r + s] in[q_c](s)   L: r x 2r
  *   BF_LEVEL_SECOND (l)   out[p](t)       = sum_c data[p][c r + t] sum_s L_{a&1}(t, s) in[q_c](s)  L: 2 x r x r
+ *   BF_LEVEL_FIRST_SWITCH (l) out[p](t)   = sum_s Sw'[p](t, s) sum_{c,s'} L(s, c r + s') psi[p][c r + s'] in[q_c](s')
+ *                          data[p] = [psi (2r) | Sw' (r x r)], L: r x 2r   (level h: the switch with its phases)
  *   BF_LEVEL_DENSE  (l)   out[p]          = data[p] [in[q_0]; in[q_1]]        data: [N][2r][r] as bf_desc_t.xfer
  *   BF_LEVEL_DENSE  (S0)  out[p]          = data[p] y_b                       data: [N][n0][r] as bf_desc_t.v0
  *   SL                    G[a n0 + j, c]  = sum_k a_k sum_{b<n0} sl_phase[a n0 + b][j] sum_t sl_lag(j, t) in[a n0+b](t)
  * (q_c = (a>>1) 2^(LN-l+1) + 2b + c; every L column-major; L_e at offset e r^2).  There is no separate switch:
- * the level-h factor (or V0 when h == l0) must carry it, with its neighbouring phases, as a DENSE level.
- * Factor bytes per pair: n0 + 2r per structured level + 2 r^2 (level h) + n0, against r n0 + 2 r^2 per level + n0 r
- * dense (cfg5: 17 GB instead of 110 GB).  Chunks that run on the tensor cores (nv >= 64) use dense blocks expanded from the
+ * the level-h factor must carry it with its neighbouring phases (FIRST_SWITCH or DENSE; V0 DENSE when h == l0).
+ * Factor bytes per pair: n0 + 2r per structured level + r^2 (the switch) + n0, against r n0 + 2 r^2 per level + n0 r
+ * dense (cfg5: 14.4 GB instead of 110 GB).  Chunks that run on the tensor cores (nv >= 64) use dense blocks expanded from the
  * structured ones at finalization (the plan then frees the structured arrays); every other chunk runs the
  * structured kernels.  Unsharded only; bf_plan_create_adjoint returns BF_ERR_NOT_SUPPORTED for them. */
 #define BF_LEVEL_DENSE 0
 #define BF_LEVEL_FIRST 1
 #define BF_LEVEL_SECOND 2
+#define BF_LEVEL_FIRST_SWITCH 3
 typedef struct {
     int32_t kind;          /* BF_LEVEL_*                                                              */
-    const float *lag;      /* FIRST: r x 2r; SECOND: 2 x r x r; DENSE: unused (NULL)                  */
-    const bf_c64 *data;    /* FIRST / SECOND: [N][2r] phases; DENSE: [N][2r][r] blocks                */
+    const float *lag;      /* FIRST, FIRST_SWITCH: r x 2r; SECOND: 2 x r x r; DENSE: unused (NULL)    */
+    const bf_c64 *data;    /* FIRST / SECOND: [N][2r]; FIRST_SWITCH: [N][2r + r^2]; DENSE: [N][2r][r] */
 } bf_slevel_t;
 typedef struct {
     int32_t abi_version;   /* BF_ABI_VERSION */

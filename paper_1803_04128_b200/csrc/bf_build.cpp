@@ -376,6 +376,35 @@ void st_dense_h(const Shape& S, int64_t p0, int64_t cnt, bf_c64* out)
         for (int64_t k = 0; k < r * cols; k++) o[k] = c64(Y[k]);
     }
 }
+
+// The level-h factor of a structured plan as kind BF_LEVEL_FIRST_SWITCH: per pair [psi_h (2r) | Sw' (r x r,
+// column-major)], Sw'(t, s) = e(-Phi(x_t^A, c_B)) e(+Phi(x_t^A, xi_s^B)) e(-Phi(c_A, xi_s^B)) -- the switch
+// with the row phases of level h and the column phases of level h+1; the level computes
+// Sw' L1 (psi o x).  2r + r^2 complex per pair instead of the 2r^2 of the dense block.
+void st_switch_h(const Shape& S, int64_t p0, int64_t cnt, bf_c64* out)
+{
+    const int r = S.r, h = S.h, sh = S.LN - h;
+    const int64_t nA = S.N >> h, nB = int64_t(1) << h, nC = nB / 2;
+    const auto gA = nodes(nA, r), gB = nodes(nB, r), gC = nodes(nC, r);
+    const int per = 2 * r + r * r;
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < cnt; q++) {
+        const int64_t p = p0 + q, a = p >> sh, b = p & ((int64_t(1) << sh) - 1);
+        bf_c64* o = out + q * per;
+        const int64_t cA = mid(a * nA, nA), cP = mid((a >> 1) * 2 * nA, 2 * nA);
+        for (int c = 0; c < 2; c++)
+            for (int sidx = 0; sidx < r; sidx++) {
+                const int64_t xi = (2 * b + c) * nC + gC[sidx];
+                o[c * r + sidx] = c64(expphi(S, cA, xi, +1.0) * expphi(S, cP, xi, -1.0));
+            }
+        for (int sidx = 0; sidx < r; sidx++) {
+            const cd rp = rowp_first(S, h, a, b, gB, sidx);
+            for (int t = 0; t < r; t++)
+                o[2 * r + sidx * r + t] =
+                    c64(colp_second(S, h, a, b, gA, t) * expphi(S, a * nA + gA[t], b * nB + gB[sidx], +1.0) * rp);
+        }
+    }
+}
 }  // namespace
 
 extern "C" {
@@ -618,8 +647,8 @@ bf_status_t bf_build_structured(const bf_fio_t* k, int32_t stage, int64_t block_
         return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_structured: bad stage");
     if (block_begin < 0 || block_count < 0 || block_begin + block_count > S.N || (!out && block_count))
         return bfp_fail(BF_ERR_INVALID_ARG, "bf_build_structured: bad block range");
-    const bool dense_h = (stage == BF_STAGE_V0 && S.h == S.l0) || (xf && S.l0 + 1 + (stage - BF_STAGE_XFER0) == S.h);
-    if (dense_h) st_dense_h(S, block_begin, block_count, out);
+    if (stage == BF_STAGE_V0 && S.h == S.l0) st_dense_h(S, block_begin, block_count, out);
+    else if (xf && S.l0 + 1 + (stage - BF_STAGE_XFER0) == S.h) st_switch_h(S, block_begin, block_count, out);
     else st_phase(S, stage, block_begin, block_count, out);
     return BF_OK;
 }
@@ -695,7 +724,7 @@ bf_status_t bf_plan_build_fio_structured(const bf_fio_t* k, int device, int64_t 
             } else if (what == -2) {
                 st_phase(S, BF_STAGE_U, p0, cnt, host.data());
             } else if (S.l0 + 1 + what == S.h) {
-                st_dense_h(S, p0, cnt, host.data());
+                st_switch_h(S, p0, cnt, host.data());
             } else {
                 st_phase(S, BF_STAGE_XFER0 + what, p0, cnt, host.data());
             }
@@ -723,8 +752,8 @@ bf_status_t bf_plan_build_fio_structured(const bf_fio_t* k, int device, int64_t 
         d.sl_phase = sld;
         for (int i = 0; i < nx && st == BF_OK; i++) {
             const int l = S.l0 + 1 + i;
-            const bool dense = (l == S.h);
-            const int64_t per = dense ? 2 * r * r : 2 * r;
+            const bool at_h = (l == S.h);
+            const int64_t per = at_h ? 2 * r + r * r : 2 * r;
             bf_c64* xd = static_cast<bf_c64*>(dalloc(size_t(N * per) * sizeof(bf_c64)));
             if (!xd) {
                 st = bfp_fail(BF_ERR_OOM, "structured build: staging allocation failed");
@@ -734,13 +763,10 @@ bf_status_t bf_plan_build_fio_structured(const bf_fio_t* k, int device, int64_t 
                 st = bfp_fail(BF_ERR_CUDA, "structured build: upload failed");
                 break;
             }
-            lv[i].kind = dense ? BF_LEVEL_DENSE : (l <= S.h ? BF_LEVEL_FIRST : BF_LEVEL_SECOND);
+            lv[i].kind = at_h ? BF_LEVEL_FIRST_SWITCH : (l < S.h ? BF_LEVEL_FIRST : BF_LEVEL_SECOND);
             lv[i].data = xd;
-            lv[i].lag = nullptr;
-            if (!dense) {
-                st_lag_xfer(S, l, Lx.data() + size_t(i) * 2 * r * r);
-                lv[i].lag = Lx.data() + size_t(i) * 2 * r * r;
-            }
+            st_lag_xfer(S, l, Lx.data() + size_t(i) * 2 * r * r);
+            lv[i].lag = Lx.data() + size_t(i) * 2 * r * r;
         }
         if (st != BF_OK) break;
         st = bf_plan_create_structured(&d, device, max_nrhs_chunk, out);

@@ -113,9 +113,10 @@ cudaError_t launch_sl_st(const Dims& d, const float2* in, const float* Lsl, cons
 // two transfer levels l, l+1 per launch on structured (kind 1 / 2) or dense (kind 0) levels; L carries level l's
 // matrix at v[0] and level l+1's at v[512]; w1 / w2 the per-pair data (phases, or blocks for kind 0)
 bool band_st_supported(const Dims& d, int nv);
+bool band_st_kinds(int k1, int k2);   // level kinds (0 dense, 1 first, 2 second, 3 first + switch) the band fuses
 cudaError_t launch_band_st(const Dims& d, int l, int k1, int k2, const LagP& L, const float2* w1, const float2* w2,
                            const float2* in, float2* out, int nv, cudaStream_t s);
-// dense blocks of a structured stage (kind 0 S0, 1 first, 2 second, 3 SL; l = the transfer level for 1/2)
+// dense blocks of a structured stage (kind 0 S0, 1 first, 2 second, 3 first + switch, 4 SL; l = the level)
 cudaError_t launch_expand_st(const Dims& d, int kind, int l, const float* L, const float2* ph, float2* out,
                              cudaStream_t s);
 

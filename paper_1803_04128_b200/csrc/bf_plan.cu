@@ -388,10 +388,11 @@ struct Step {
     int levels = 0;    // transfer levels this launch performs
 };
 
-void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool band)
+template <class Ok>
+void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool band, Ok&& pair_ok)
 {
     for (int l = lo; l <= hi;) {
-        const int K = band ? std::min(2, hi - l + 1) : 1;
+        const int K = (band && l < hi && pair_ok(l)) ? 2 : 1;
         const int last = l + K - 1;
         const bool has_h = (l <= d.h && d.h <= last);
         const int cls = has_h ? bfk::KC_SWITCH : (last < d.h ? bfk::KC_XFER1 : bfk::KC_XFER2);
@@ -414,12 +415,16 @@ std::vector<Step> schedule(const bf_plan_s* p, int nv)
     const bool band = p->sh[0].dense_all()
                           ? (bfk::band_supported(d.R, nv) || (small_batch && bfk::band_sv_supported(d, nv)))
                           : (small_batch && bfk::band_st_supported(d, nv));
+    // structured levels: only the kind pairs the structured band fuses
+    const Shard& s0 = p->sh[0];
+    auto kind_of = [&](int l) { return s0.xfer[l - d.l0 - 1] ? 0 : s0.kind[l - d.l0 - 1]; };
+    auto pair_ok = [&](int l) { return s0.dense_all() || bfk::band_st_kinds(kind_of(l), kind_of(l + 1)); };
     if (!sharded) {
-        push_levels(st, d, d.l0 + 1, d.D, band);
+        push_levels(st, d, d.l0 + 1, d.D, band, pair_ok);
     } else {
-        push_levels(st, d, d.l0 + 1, d.h, band);
+        push_levels(st, d, d.l0 + 1, d.h, band, pair_ok);
         st.push_back({Step::EXCHANGE, 0, 1, KC_EXCHANGE, 0});
-        push_levels(st, d, d.h + 1, d.D, band);
+        push_levels(st, d, d.h + 1, d.D, band, pair_ok);
     }
     st.push_back({Step::SL, 0, 1, bfk::KC_SL, 0});
     return st;
@@ -932,7 +937,7 @@ bf_status_t expand_structured(bf_plan_s* p)
     }
     if (e == cudaSuccess && !s.u) {
         if ((st = dalloc(&s.u, n * r * n0, "u (expanded)")) != BF_OK) return st;
-        e = bfk::launch_expand_st(d, 3, 0, s.sl_lag, s.sl_ph, s.u, 0);
+        e = bfk::launch_expand_st(d, 4, 0, s.sl_lag, s.sl_ph, s.u, 0);
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "structured factor expansion");
@@ -1025,10 +1030,11 @@ bf_status_t bf_plan_create_structured(const bf_sdesc_t* sd, int device, int64_t 
         const bf_slevel_t& lv = sd->xfer[i];
         if (lv.kind == BF_LEVEL_DENSE) {
             if ((st = dcopy(&s.xfer[i], lv.data, size_t(N * 2 * r * r * c8), "xfer data (dense)")) != BF_OK) return done(st);
-        } else if (lv.kind == BF_LEVEL_FIRST || lv.kind == BF_LEVEL_SECOND) {
+        } else if (lv.kind == BF_LEVEL_FIRST || lv.kind == BF_LEVEL_SECOND || lv.kind == BF_LEVEL_FIRST_SWITCH) {
             s.kind[i] = lv.kind;
+            const int64_t per = lv.kind == BF_LEVEL_FIRST_SWITCH ? 2 * r + r * r : 2 * r;
             if ((st = dcopy(&s.lag[i], lv.lag, size_t(2 * r * r * 4), "xfer lag")) != BF_OK ||
-                (st = dcopy(&s.ph[i], lv.data, size_t(N * 2 * r * c8), "xfer data")) != BF_OK)
+                (st = dcopy(&s.ph[i], lv.data, size_t(N * per * c8), "xfer data")) != BF_OK)
                 return done(st);
             if ((e = cudaMemcpy(s.lagh[i].v, s.lag[i], size_t(2 * r * r * 4), cudaMemcpyDeviceToHost)) != cudaSuccess)
                 return done(cuda_fail(e, "xfer lag"));
@@ -1425,7 +1431,9 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     for (const Shard& s : p->sh) {
         int64_t f = 2 * p->d.n_amp * n + (s.sw ? n * r * r : 0) + (s.v0 ? n * r * n0 : 0) + (s.u ? n * r * n0 : 0) +
                     (s.s0_ph ? n * n0 : 0) + (s.sl_ph ? n * n0 : 0);
-        for (int i = 0; i < nx; i++) f += (s.xfer[i] ? n * 2 * r * r : 0) + (s.ph[i] ? n * 2 * r : 0);
+        for (int i = 0; i < nx; i++)
+            f += (s.xfer[i] ? n * 2 * r * r : 0) +
+                 (s.ph[i] ? n * (s.kind[i] == BF_LEVEL_FIRST_SWITCH ? 2 * r + r * r : 2 * r) : 0);
         info->factor_bytes += 8 * f;
         info->factor_bytes += 4 * ((s.s0_lag ? r * n0 : 0) + (s.sl_lag ? r * n0 : 0));
         for (int i = 0; i < nx; i++) info->factor_bytes += s.lag[i] ? 4 * 2 * r * r : 0;

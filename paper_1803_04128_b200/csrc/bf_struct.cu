@@ -127,17 +127,30 @@ __global__ void __launch_bounds__(256) xfer_st_kernel(const __grid_constant__ La
     float2 acc[R];
 #pragma unroll
     for (int t = 0; t < R; t++) acc[t] = make_float2(0.f, 0.f);
-    if (KIND == 1) {   // first half: phases on the inputs, then L1
+    if (KIND == 1 || KIND == 3) {   // first half: phases on the inputs, then L1 (then the switch: KIND 3)
+        const float2* pc = ph + p * (KIND == 3 ? 2 * R + R * R : 2 * R);
 #pragma unroll
         for (int c = 0; c < 2; c++) {
             const float2* x = c ? x1 : x0;
             float2 y[R];
 #pragma unroll
-            for (int s = 0; s < R; s++) y[s] = cmul(__ldg(php + c * R + s), __ldg(x + int64_t(s) * nv));
+            for (int s = 0; s < R; s++) y[s] = cmul(__ldg(pc + c * R + s), __ldg(x + int64_t(s) * nv));
 #pragma unroll
             for (int s = 0; s < R; s++)
 #pragma unroll
                 for (int t = 0; t < R; t++) rmac(acc[t], L.v[(c * R + s) * R + t], y[s]);
+        }
+        if (KIND == 3) {
+            float2 y[R];
+#pragma unroll
+            for (int t = 0; t < R; t++) {
+                y[t] = acc[t];
+                acc[t] = make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int s = 0; s < R; s++)
+#pragma unroll
+                for (int t = 0; t < R; t++) cmac(acc[t], __ldg(pc + 2 * R + s * R + t), y[s]);
         }
     } else {           // second half: L2_e on each input, phases on the outputs (e uniform over a warp's pairs
                        // whenever 2^(LN-l) >= 32 / nv)
@@ -169,10 +182,10 @@ __device__ __forceinline__ void level_out(const float* __restrict__ Lv, const fl
         float2 xs[R];
 #pragma unroll
         for (int s = 0; s < R; s++) xs[s] = x[s * sx];
-        if (KIND == 1) {
+        if (KIND == 1 || KIND == 3) {
 #pragma unroll
             for (int s = 0; s < R; s++) {
-                const float2 y = cmul(__ldg(wp + c * R + s), xs[s]);
+                const float2 y = cmul(wp[c * R + s], xs[s]);
 #pragma unroll
                 for (int t = 0; t < R; t++) rmac(acc[t], Lv[(c * R + s) * R + t], y);
             }
@@ -192,51 +205,113 @@ __device__ __forceinline__ void level_out(const float* __restrict__ Lv, const fl
                     for (int t = 0; t < R; t++) rmac(z[t], Lv[s * R + t], xs[s]);
             }
 #pragma unroll
-            for (int t = 0; t < R; t++) cmac(acc[t], __ldg(wp + c * R + t), z[t]);
+            for (int t = 0; t < R; t++) cmac(acc[t], wp[c * R + t], z[t]);
         } else {   // dense r x 2r block, column-major
 #pragma unroll
             for (int s = 0; s < R; s++)
 #pragma unroll
-                for (int t = 0; t < R; t++) cmac(acc[t], __ldg(wp + (c * R + s) * R + t), xs[s]);
+                for (int t = 0; t < R; t++) cmac(acc[t], wp[(c * R + s) * R + t], xs[s]);
         }
     }
+    if (KIND == 3) {   // the switch with its phases: acc <- Sw' acc (Sw' column-major after the 2r phases)
+        float2 y[R];
+#pragma unroll
+        for (int t = 0; t < R; t++) {
+            y[t] = acc[t];
+            acc[t] = make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int s = 0; s < R; s++)
+#pragma unroll
+            for (int t = 0; t < R; t++) cmac(acc[t], wp[2 * R + s * R + t], y[s]);
+    }
+}
+
+// The CTA takes jobs_cta consecutive jobs per iteration; their inputs (contiguous), the per-pair data of both
+// levels and (next iteration) are staged with cp.async into a 2-deep ring while the current iteration computes,
+// so every thread has a whole iteration of copies in flight (the unpipelined version, which loaded its inputs
+// from global memory inside the level-l loop, ran at 0.27 of HBM).
+__device__ __forceinline__ void cp_async16_g(void* smem, const void* gmem)
+{
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
 template <int R, int K1, int K2>
 __global__ void __launch_bounds__(256) band_st_kernel(const __grid_constant__ LagP L, const float2* __restrict__ w1,
                                                       const float2* __restrict__ w2, const float2* __restrict__ in,
-                                                      float2* __restrict__ out, int LN, int l, int nv, int64_t njobs)
+                                                      float2* __restrict__ out, int LN, int l, int nv, int64_t njobs,
+                                                      int jobs_cta)
 {
     extern __shared__ __align__(16) unsigned char st_smem[];
-    const int per_job = 4 * nv, jobs_cta = blockDim.x / per_job;
-    const int jl = threadIdx.x / per_job, os = (threadIdx.x / nv) % 4, v = threadIdx.x % nv;
-    const int u = os >> 1, e = os & 1;
+    constexpr int WS1 = K1 == 0 ? 2 * R * R : (K1 == 3 ? 2 * R + R * R : 2 * R);
+    constexpr int WS2 = K2 == 0 ? 2 * R * R : (K2 == 3 ? 2 * R + R * R : 2 * R);
+    const int per_job = 4 * nv;
+    // thread = (job, e, u, vector): with nv >= 16 a warp's threads share e (the second-half Lagrange matrix)
+    const int jl = threadIdx.x / per_job, v = threadIdx.x % nv;
+    const int u = (threadIdx.x / nv) & 1, e = (threadIdx.x / (2 * nv)) & 1, os = 2 * u + e;
     const int shg = LN - l - 1;
-    float2* X1 = reinterpret_cast<float2*>(st_smem) + jl * 4 * R * nv;   // [slot][t][v] of this job
-    constexpr int WS1 = K1 == 0 ? 2 * R * R : 2 * R, WS2 = K2 == 0 ? 2 * R * R : 2 * R;
-    for (int64_t j0 = int64_t(blockIdx.x) * jobs_cta; j0 < njobs; j0 += int64_t(gridDim.x) * jobs_cta) {
+    const int xin = jobs_cta * 4 * R * nv;   // complex per input buffer
+    float2* X0 = reinterpret_cast<float2*>(st_smem);          // [2][jobs][4 slots][R][nv]
+    float2* X1 = X0 + 2 * xin;                                 // [jobs][4][R][nv]
+    float2* P1 = X1 + xin;                                     // [2][jobs][4][WS1]
+    float2* P2 = P1 + 2 * jobs_cta * 4 * WS1;                  // [2][jobs][4][WS2]
+    const int64_t stride = int64_t(gridDim.x) * jobs_cta;
+    auto pair1 = [&](int64_t j, int uu, int ee) {
+        const int64_t a0 = j >> shg, bq = j & ((int64_t(1) << shg) - 1);
+        return (((a0 << 1) + ee) << (LN - l)) + (bq << 1) + uu;
+    };
+    auto pair2 = [&](int64_t j, int uu, int ee) {
+        const int64_t a0 = j >> shg, bq = j & ((int64_t(1) << shg) - 1);
+        return (((a0 << 2) + 2 * uu + ee) << shg) + bq;
+    };
+    auto issue = [&](int64_t j0, int buf) {
+        const int64_t nj = njobs - j0 < jobs_cta ? njobs - j0 : jobs_cta;
+        const int pieces = int(nj) * 4 * R * nv / 2;   // 16-byte pieces of the inputs (nv even)
+        const float2* src = in + 4 * j0 * R * int64_t(nv);
+        float2* dst = X0 + buf * xin;
+        for (int i = threadIdx.x; i < pieces; i += blockDim.x) cp_async16_g(dst + 2 * i, src + 2 * i);
+        const int p1n = int(nj) * 4 * (WS1 / 2), p2n = int(nj) * 4 * (WS2 / 2);
+        for (int i = threadIdx.x; i < p1n; i += blockDim.x) {
+            const int q = i / (WS1 / 2), k = i % (WS1 / 2), jj = q / 4, o = q % 4;
+            cp_async16_g(P1 + ((buf * jobs_cta + jj) * 4 + o) * WS1 + 2 * k, w1 + pair1(j0 + jj, o >> 1, o & 1) * WS1 + 2 * k);
+        }
+        for (int i = threadIdx.x; i < p2n; i += blockDim.x) {
+            const int q = i / (WS2 / 2), k = i % (WS2 / 2), jj = q / 4, o = q % 4;
+            cp_async16_g(P2 + ((buf * jobs_cta + jj) * 4 + o) * WS2 + 2 * k, w2 + pair2(j0 + jj, o >> 1, o & 1) * WS2 + 2 * k);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int64_t j0 = int64_t(blockIdx.x) * jobs_cta;
+    if (j0 < njobs) issue(j0, 0);
+    for (int it = 0; j0 < njobs; it++, j0 += stride) {
+        const int buf = it & 1;
+        if (j0 + stride < njobs) {
+            issue(j0 + stride, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
         const int64_t j = j0 + jl;
         const bool live = jl < jobs_cta && j < njobs;
-        const int64_t a0 = j >> shg, bq = j & ((int64_t(1) << shg) - 1);
         float2 acc[R];
-        if (live) {   // level l: output (u, e) from input slots 2u, 2u + 1 (global)
-            const int64_t p1 = (((a0 << 1) + e) << (LN - l)) + (bq << 1) + u;
-            const float2* x0 = in + (4 * j + 2 * u) * R * int64_t(nv) + v;
-            level_out<R, K1>(L.v, w1 + p1 * WS1, e, x0, x0 + int64_t(R) * nv, nv, acc);
-            float2* d = X1 + os * R * nv + v;
+        if (live) {   // level l: output (u, e) from input slots 2u, 2u + 1
+            const float2* x0 = X0 + buf * xin + ((jl * 4) + 2 * u) * R * nv + v;
+            level_out<R, K1>(L.v, P1 + ((buf * jobs_cta + jl) * 4 + os) * WS1, e, x0, x0 + R * nv, nv, acc);
+            float2* d = X1 + (jl * 4 + os) * R * nv + v;
 #pragma unroll
             for (int t = 0; t < R; t++) d[t * nv] = acc[t];
         }
         __syncthreads();
         if (live) {   // level l + 1: output (u, e) from level-l slots u (c = 0) and u + 2 (c = 1)
-            const int64_t p2 = (((a0 << 2) + 2 * u + e) << shg) + bq;
-            const float2* x0 = X1 + u * R * nv + v;
-            level_out<R, K2>(L.v + 512, w2 + p2 * WS2, e, x0, x0 + 2 * R * nv, nv, acc);
-            float2* d = out + p2 * R * int64_t(nv) + v;
+            const float2* x0 = X1 + (jl * 4 + u) * R * nv + v;
+            level_out<R, K2>(L.v + 512, P2 + ((buf * jobs_cta + jl) * 4 + os) * WS2, e, x0, x0 + 2 * R * nv, nv, acc);
+            float2* d = out + pair2(j, u, e) * R * int64_t(nv) + v;
 #pragma unroll
             for (int t = 0; t < R; t++) d[int64_t(t) * nv] = acc[t];
         }
-        __syncthreads();
+        __syncthreads();   // buffer `buf` and X1 are free for the copies issued next iteration
     }
 }
 
@@ -330,12 +405,13 @@ __global__ void __launch_bounds__(256) sl_st_kernel(const float2* __restrict__ i
 // kind 0 (S0):     V[p](t, j)      = L0(t, j) omega[p][j]                 (r x n0 column-major)
 // kind 1 (first):  W[p](t, k)      = L1(t, k) psi[p][k]                   (r x 2r)
 // kind 2 (second): W[p](t, c r+s)  = chi[p][c r + t] L2_{a&1}(t, s)       (r x 2r)
-// kind 3 (SL):     U[p](j, t)      = Omega[p][j] Lsl(j, t)                (n0 x r column-major)
+// kind 3 (switch): W[p](t, k)      = sum_s Sw'[p](t, s) L1(s, k) psi[p][k] (r x 2r)
+// kind 4 (SL):     U[p](j, t)      = Omega[p][j] Lsl(j, t)                (n0 x r column-major)
 __global__ void expand_st_kernel(const float* __restrict__ L, const float2* __restrict__ ph, float2* __restrict__ out,
                                  int kind, int R, int n0, int sh, int64_t total)
 {
     for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
-        const int per = (kind == 1 || kind == 2) ? 2 * R * R : R * n0;
+        const int per = (kind == 1 || kind == 2 || kind == 3) ? 2 * R * R : R * n0;
         const int64_t p = g / per;
         const int e = int(g % per);
         float w;
@@ -350,6 +426,18 @@ __global__ void expand_st_kernel(const float* __restrict__ L, const float2* __re
             const int t = e % R, col = e / R, c = col / R, s = col % R;
             w = L[int((p >> sh) & 1) * R * R + s * R + t];
             f = ph[p * 2 * R + c * R + t];
+        } else if (kind == 3) {
+            const int t = e % R, k = e / R;
+            const float2* pp = ph + p * (2 * R + R * R);
+            float2 acc = make_float2(0.f, 0.f);
+            for (int s = 0; s < R; s++) {
+                const float2 sw = pp[2 * R + s * R + t];
+                const float lw = L[k * R + s];
+                acc.x = fmaf(sw.x, lw, acc.x);
+                acc.y = fmaf(sw.y, lw, acc.y);
+            }
+            out[g] = cmul(acc, pp[k]);
+            continue;
         } else {
             w = L[e];
             f = ph[p * n0 + e % n0];
@@ -397,10 +485,12 @@ cudaError_t launch_xfer_st(const Dims& d, int l, int kind, const LagP& L, const 
                            float2* out, int nv, cudaStream_t s)
 {
     const int64_t total = d.N * nv;
-    if (kind != 1 && kind != 2) return cudaErrorInvalidValue;
+    if (kind != 1 && kind != 2 && kind != 3) return cudaErrorInvalidValue;
 #define X_CALL(R)                                                                                                 \
     {                                                                                                             \
         if (kind == 1) xfer_st_kernel<R, 1><<<grid_of(total, 256), 256, 0, s>>>(L, ph, in, out, d.LN, l, nv, total); \
+        else if (kind == 3)                                                                                       \
+            xfer_st_kernel<R, 3><<<grid_of(total, 256), 256, 0, s>>>(L, ph, in, out, d.LN, l, nv, total);          \
         else xfer_st_kernel<R, 2><<<grid_of(total, 256), 256, 0, s>>>(L, ph, in, out, d.LN, l, nv, total);          \
     }
     ST_R(d.R, X_CALL)
@@ -441,28 +531,43 @@ cudaError_t launch_sl_st(const Dims& d, const float2* in, const float* Lsl, cons
     return cudaGetLastError();
 }
 
-bool band_st_supported(const Dims& d, int nv) { return nv >= 1 && 4 * nv <= 256 && d.R <= 16; }
+bool band_st_supported(const Dims& d, int nv) { return nv >= 2 && nv % 2 == 0 && 4 * nv <= 256 && d.R <= 16; }
+
+bool band_st_kinds(int k1, int k2)
+{
+    const int kk = k1 * 4 + k2;
+    return kk == 1 * 4 + 1 || kk == 2 * 4 + 2 || kk == 1 * 4 + 3 || kk == 3 * 4 + 2 || kk == 1 * 4 + 0 ||
+           kk == 0 * 4 + 2 || kk == 0 * 4 + 0;
+}
 
 cudaError_t launch_band_st(const Dims& d, int l, int k1, int k2, const LagP& L, const float2* w1, const float2* w2,
                            const float2* in, float2* out, int nv, cudaStream_t s)
 {
     if (!band_st_supported(d, nv)) return cudaErrorInvalidValue;
-    const int jobs_cta = 256 / (4 * nv);
+    auto ws = [&](int k) { return k == 0 ? 2 * d.R * d.R : (k == 3 ? 2 * d.R + d.R * d.R : 2 * d.R); };
+    const int ws1 = ws(k1), ws2 = ws(k2);
+    const size_t per_job = size_t(4) * (3 * size_t(d.R) * nv + 2 * ws1 + 2 * ws2) * 8;
+    // up to 256 threads, and at most ~100 KB of shared memory (two CTAs per SM)
+    const int jobs_cta = int(std::max<size_t>(1, std::min<size_t>(256 / (4 * nv), (100 << 10) / per_job)));
     const int threads = jobs_cta * 4 * nv;
-    const size_t shm = size_t(jobs_cta) * 4 * d.R * nv * 8;
+    const size_t shm = size_t(jobs_cta) * per_job;
     const int64_t njobs = d.N / 4;
-    const unsigned grid = unsigned(std::min<int64_t>((njobs + jobs_cta - 1) / jobs_cta, int64_t(148) * 8));
-    const int kk = k1 * 3 + k2;
+    const unsigned grid = unsigned(std::min<int64_t>((njobs + jobs_cta - 1) / jobs_cta, int64_t(148) * 4));
+    const int kk = k1 * 4 + k2;
 #define B_GO(R, A, B)                                                                                              \
-    band_st_kernel<R, A, B><<<grid, threads, shm, s>>>(L, w1, w2, in, out, d.LN, l, nv, njobs)
+    {                                                                                                              \
+        cudaFuncSetAttribute(band_st_kernel<R, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));     \
+        band_st_kernel<R, A, B><<<grid, threads, shm, s>>>(L, w1, w2, in, out, d.LN, l, nv, njobs, jobs_cta);      \
+    }
 #define B_CALL(R)                                      \
     switch (kk) {                                      \
-    case 1 * 3 + 1: B_GO(R, 1, 1); break;              \
-    case 2 * 3 + 2: B_GO(R, 2, 2); break;              \
-    case 1 * 3 + 0: B_GO(R, 1, 0); break;              \
-    case 0 * 3 + 2: B_GO(R, 0, 2); break;              \
-    case 0 * 3 + 1: B_GO(R, 0, 1); break;              \
-    case 2 * 3 + 0: B_GO(R, 2, 0); break;              \
+    case 1 * 4 + 1: B_GO(R, 1, 1); break;              \
+    case 2 * 4 + 2: B_GO(R, 2, 2); break;              \
+    case 1 * 4 + 3: B_GO(R, 1, 3); break;              \
+    case 3 * 4 + 2: B_GO(R, 3, 2); break;              \
+    case 1 * 4 + 0: B_GO(R, 1, 0); break;              \
+    case 0 * 4 + 2: B_GO(R, 0, 2); break;              \
+    case 0 * 4 + 0: B_GO(R, 0, 0); break;              \
     default: return cudaErrorInvalidValue;             \
     }
     ST_R(d.R, B_CALL)
@@ -475,7 +580,7 @@ cudaError_t launch_expand_st(const Dims& d, int kind, int l, const float* L, con
                              cudaStream_t s)
 {
     const int n0 = 1 << d.l0;
-    const int64_t per = (kind == 1 || kind == 2) ? 2 * int64_t(d.R) * d.R : int64_t(d.R) * n0;
+    const int64_t per = (kind == 1 || kind == 2 || kind == 3) ? 2 * int64_t(d.R) * d.R : int64_t(d.R) * n0;
     const int64_t total = d.N * per;
     const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, int64_t(148) * 32));
     expand_st_kernel<<<grid, 256, 0, s>>>(L, ph, out, kind, d.R, n0, d.LN - l, total);

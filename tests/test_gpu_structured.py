@@ -83,14 +83,14 @@ def test_structured_vs_dense_and_factor_bytes():
 
 
 def test_structured_cfg5_full():
-    """cfg5 at full size (N = 2^22, 8 RHS) on structured factors (17 GB instead of 110 GB); sampled column."""
+    """cfg5 at full size (N = 2^22, 8 RHS) on structured factors (14.4 GB instead of 110 GB); sampled column."""
     w = W.CONFIGS["cfg5"]
     F = W.rhs(w.n, w.nrhs, w.seed)
     plan = bf.Plan.build_fio_structured(bf.fio_of(w), max_nrhs_chunk=w.nrhs)
     fb = plan.info()["factor_bytes"]
     G = gpu_apply(plan, F)
     plan.destroy()
-    assert fb < 18e9, fb
+    assert fb < 15e9, fb
     cols = [5]
     R = oracle.bf_apply(w.kernel, w.amp, w.log2n, w.log2leaf, w.rank, F[:, cols])
     err = oracle.rel_l2(G[:, cols].astype(np.complex128), R, axis=0)
