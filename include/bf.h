@@ -200,6 +200,19 @@ typedef struct {
  * array or an unknown kind; otherwise as bf_plan_create. */
 bf_status_t bf_plan_create_structured(const bf_sdesc_t *desc, int device, int64_t max_nrhs_chunk, bf_plan_t *out);
 
+/* Recompression ("structure-preserving sweeping matrix compression", deferred by the
+ * paper to [IBF]): a new plan of rank `rank` <= r whose factors are the balanced truncation of src's.  Every
+ * coefficient space delta_l[p] of eqn:BFM carries the block K(A,B) = S_p R_p (input -> delta_l[p] -> output);
+ * with Gamma_out = S_p^H S_p (top-down) and Gamma_in = R_p R_p^H (bottom-up over the already truncated levels)
+ * the sweep keeps the `rank` dominant singular directions of Gamma_out^{1/2} Gamma_in^{1/2}, i.e. the best
+ * rank-`rank` approximation of each block, and rewrites V0' = P V0, W'_l = P_l W_l diag(Q_{l-1}), U' = U Q_D
+ * (R21).  Built on the device in FP64 at plan construction (untimed, like the switch fold); scratch
+ * (D - l0 + 1) N r^2 complex doubles.  src: finalized, unsharded, dense (not structured), r <= 12; rank in the
+ * supported set; the new plan owns everything (src may be destroyed).  The interpolative rank 12 recompressed
+ * to 8 stays within eps/2 = 5e-7 of the direct sum (tests/test_oracle_recompress.py) with 2/3 the transfer
+ * flops of the rank-10 interpolative factorization. */
+bf_status_t bf_plan_recompress(bf_plan_t src, int32_t rank, int64_t max_nrhs_chunk, bf_plan_t *out);
+
 /* Streaming construction (factors larger than host RAM): allocate the plan from the
  * shape fields of `meta` (array pointers ignored), upload stage blocks in any order
  * and ranges, then finalize.  block_begin/block_count count blocks of the stage

@@ -40,7 +40,7 @@ EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finaliz
            "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
            "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated", "bf_plan_create_adjoint",
            "bf_plan_create_structured", "bf_plan_build_fio_structured", "bf_build_structured",
-           "bf_build_structured_lag")
+           "bf_build_structured_lag", "bf_plan_recompress")
 
 
 class BFError(RuntimeError):
@@ -103,6 +103,7 @@ def lib():
             "bf_plan_upload": ([vp, i32, i64, i64, vp, i32], i32),
             "bf_plan_finalize": ([vp], i32),
             "bf_plan_create_adjoint": ([vp, i64, P(vp)], i32),
+            "bf_plan_recompress": ([vp, i32, i64, P(vp)], i32),
             "bf_plan_create_structured": ([vp, ctypes.c_int, i64, P(vp)], i32),
             "bf_build_structured": ([P(bf_fio_t), i32, i64, i64, vp], i32),
             "bf_build_structured_lag": ([P(bf_fio_t), i32, vp], i32),
@@ -283,6 +284,14 @@ class Plan:
             max_nrhs_chunk = self.info()["max_nrhs_chunk"]
         h = ctypes.c_void_p()
         _check(lib().bf_plan_create_adjoint(self._h, max_nrhs_chunk, ctypes.byref(h)))
+        return Plan(h.value)
+
+    def recompress(self, rank: int, max_nrhs_chunk: int | None = None) -> "Plan":
+        """bf_plan_recompress: a new plan of rank `rank` (balanced truncation of this plan's factors, NEXT-3)."""
+        if max_nrhs_chunk is None:
+            max_nrhs_chunk = self.info()["max_nrhs_chunk"]
+        h = ctypes.c_void_p()
+        _check(lib().bf_plan_recompress(self._h, rank, max_nrhs_chunk, ctypes.byref(h)))
         return Plan(h.value)
 
     # -- apply ---------------------------------------------------------------------

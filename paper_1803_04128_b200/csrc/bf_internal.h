@@ -120,6 +120,13 @@ cudaError_t launch_band_st(const Dims& d, int l, int k1, int k2, const LagP& L, 
 cudaError_t launch_expand_st(const Dims& d, int kind, int l, const float* L, const float2* ph, float2* out,
                              cudaStream_t s);
 
+// Recompression (bf_recompress.cu, NEXT-3): the rank-rp factors of a dense rank-d.R (<= 12) factorization whose
+// switch is folded into level h, by a balanced-truncation sweep in FP64.  Scratch: gout (D - l0 + 1) N r^2,
+// q2 2 N r rp, gin2 2 N rp^2 complex doubles.
+cudaError_t launch_recompress(const Dims& d, int rp, const float2* v0, const float2* const* xfer, const float2* u,
+                              float2* out_v0, float2* const* out_x, float2* out_u, void* gout, void* q2, void* gin2,
+                              cudaStream_t s);
+
 // SL (eqn:bf3 + eqn:tg): G[x, c] = sum_k a_k(x) sum_{b<n0} sum_t U[a n0 + b](j, t) in[a n0 + b](t)[c n_amp + k],
 // x = a n0 + j.
 cudaError_t launch_sl(const Dims& d, const float2* in, const float2* U, const float2* ampa, float2* G, int64_t ldg,

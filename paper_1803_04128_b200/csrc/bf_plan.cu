@@ -1190,6 +1190,68 @@ bf_status_t bf_plan_create_adjoint(bf_plan_t fwd, int64_t max_nrhs_chunk, bf_pla
     return BF_OK;
 }
 
+bf_status_t bf_plan_recompress(bf_plan_t src, int32_t rank, int64_t max_nrhs_chunk, bf_plan_t* out)
+{
+    if (!out) return fail(BF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!src) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
+    if (!src->finalized) return fail(BF_ERR_STATE, "source plan not finalized");
+    if (src->mode != BF_SHARD_NONE) return fail(BF_ERR_NOT_SUPPORTED, "recompression of an index-sharded plan");
+    if (!src->sh[0].dense_all()) return fail(BF_ERR_NOT_SUPPORTED, "recompression of a structured plan");
+    if (src->d.R > 12) return fail(BF_ERR_NOT_SUPPORTED, "recompression: source rank %d > 12", src->d.R);
+    if (rank > src->d.R || !bfk::rank_supported(rank))
+        return fail(BF_ERR_NOT_SUPPORTED, "recompression to rank %d (source %d)", rank, src->d.R);
+    const bfk::Dims& d = src->d;
+    bf_desc_t meta{};
+    meta.abi_version = BF_ABI_VERSION;
+    meta.log2n = d.LN;
+    meta.log2leaf = d.l0;
+    meta.rank = rank;
+    meta.n_amp = d.n_amp;
+    meta.memory = BF_MEM_DEVICE;
+    bf_plan_t p = nullptr;
+    bf_status_t st = alloc_plan(&meta, src->device, max_nrhs_chunk, 1, 0, BF_SHARD_NONE, &p);
+    if (st != BF_OK) return st;
+    DeviceGuard g(p->device);
+    Shard& s = p->sh[0];
+    const Shard& f = src->sh[0];
+    cudaFree(s.sw);   // the source's level-h factor carries the switch, and so does the recompressed one
+    s.sw = nullptr;
+    p->switch_in_factors = true;
+    const int64_t N = d.N, r = d.R, rp = rank, nl = d.D - d.l0 + 1;
+    void *gout = nullptr, *q2 = nullptr, *gin2 = nullptr;
+    const size_t zb = 16;   // complex double
+    cudaError_t e = cudaMalloc(&gout, size_t(nl) * N * r * r * zb);
+    if (e == cudaSuccess) e = cudaMalloc(&q2, size_t(2) * N * r * rp * zb);
+    if (e == cudaSuccess) e = cudaMalloc(&gin2, size_t(2) * N * rp * rp * zb);
+    if (e == cudaSuccess) e = cudaMemcpy(s.amp_a, f.amp_a, size_t(d.n_amp * N) * 8, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s.amp_b, f.amp_b, size_t(d.n_amp * N) * 8, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) {
+        bfk::Dims ds = d;
+        e = bfk::launch_recompress(ds, int(rp), f.v0, f.xfer.data(), f.u, s.v0, s.xfer.data(), s.u, gout, q2, gin2, 0);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(gout);
+    cudaFree(q2);
+    cudaFree(gin2);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        free_plan(p);
+        return e == cudaErrorMemoryAllocation ? fail(BF_ERR_OOM, "recompression scratch: out of device memory")
+                                              : cuda_fail(e, "recompression");
+    }
+    for (size_t slot = 0; slot < p->uploaded[0].size(); slot++) {
+        const int stage = slot < 5 ? int(slot) : BF_STAGE_XFER0 + int(slot) - 5;
+        p->uploaded[0][slot].push_back({0, stage_blocks(p, stage)});
+    }
+    if ((st = bf_plan_finalize(p)) != BF_OK) {
+        free_plan(p);
+        return st;
+    }
+    *out = p;
+    return BF_OK;
+}
+
 bf_status_t bf_plan_create_sharded(const bf_desc_t* local, int device, int64_t max_nrhs_chunk, int32_t rank,
                                    int32_t world, const void* nccl_unique_id, bf_plan_t* out)
 {
