@@ -56,7 +56,8 @@ def test_recompressed_parity(kernel, amp, LN, l0, r, rp, nrhs):
 
 
 def test_recompressed_cfg4_shape_vs_direct():
-    # cfg4's kernel at N = 2^16 with 256 RHS (tensor cores): rank 12 -> 8 stays within eps of the direct sum
+    # cfg4's kernel at N = 2^16 with 256 RHS (tensor cores): rank 12 -> 8 within eps/2 of the direct sum plus the
+    # 3xTF32 path's own error (~1.5e-6, the same bound as the dense plan's test_parity_config)
     w = W.CONFIGS["cfg4"].with_(log2n=16)
     F = W.rhs(w.n, w.nrhs, 9, cols=[0, 255])
     Fb = np.asfortranarray(np.repeat(F, 128, axis=1))
@@ -69,7 +70,7 @@ def test_recompressed_cfg4_shape_vs_direct():
     rows = W.sample_rows(w.n, w.seed)
     gd = oracle.direct_rows(w.kernel, w.amp, w.log2n, F, rows)
     err = oracle.rel_l2(G[rows][:, [0, 255]].astype(np.complex128), gd, axis=0)
-    assert np.all(err <= w.eps), err
+    assert np.all(err <= w.eps / 2 + 2e-6), err
 
 
 def test_recompress_errors():
@@ -82,3 +83,27 @@ def test_recompress_errors():
         st.recompress(8)              # structured plans: not supported
     st.destroy()
     src.destroy()
+
+
+def test_recompressed_cfg4_full():
+    """cfg4 at full size (N = 2^20, 256 RHS) in the bench's launch configuration (rank 12 recompressed to 8, one
+    chunk of 256 columns): sampled columns against the oracle's own recompression of its FP64 blocks (needs
+    ~90 GB of host memory) and against the direct sum."""
+    import os
+    w = W.CONFIGS["cfg4"]
+    mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    if mem < 150e9:
+        pytest.skip(f"the oracle's full-size recompression needs ~90 GB of host memory ({mem / 1e9:.0f} GB)")
+    F = W.rhs(w.n, w.nrhs, w.seed)
+    src = bf.Plan.build_fio(bf.fio(w.kernel, w.amp, w.log2n, w.log2leaf, 12), max_nrhs_chunk=1)
+    plan = src.recompress(8, max_nrhs_chunk=w.nrhs)
+    src.destroy()
+    G = gpu_apply(plan, F)
+    plan.destroy()
+    cols = [0, 200]
+    R = RC.bf_apply_recompressed(w.kernel, w.amp, w.log2n, w.log2leaf, 12, 8, F[:, cols].astype(np.complex128))
+    err = oracle.rel_l2(G[:, cols].astype(np.complex128), R, axis=0)
+    assert np.all(err <= PARITY), err
+    rows = W.sample_rows(w.n, w.seed)
+    gd = oracle.direct_rows(w.kernel, w.amp, w.log2n, F[:, cols], rows)
+    assert np.all(oracle.rel_l2(G[rows][:, cols].astype(np.complex128), gd, axis=0) <= w.eps / 2 + 2e-6)
