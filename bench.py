@@ -249,6 +249,9 @@ def main():
                     help="tensor-core band: composed two-level operator (1) or level by level (0) (BF_OPT_BAND_COMPOSE)")
     ap.add_argument("--structured", action="store_true",
                     help="structured interpolative factors: phases + shared Lagrange matrices (NEXT-1)")
+    ap.add_argument("--factors", choices=["auto", "interpolative", "structured", "recompressed"], default="auto",
+                    help="factor form: auto = per config (DESIGN.md 7): cfg3/cfg4 recompressed 12 -> 8, cfg2/cfg5 "
+                         "structured, cfg1 interpolative")
     ap.add_argument("--recompress", type=int, default=None, metavar="RP",
                     help="recompress the interpolative factorization of rank --build-rank to rank RP (NEXT-3)")
     ap.add_argument("--build-rank", type=int, default=12, help="interpolative rank before --recompress")
@@ -287,6 +290,14 @@ def main():
     if args.impl == "reference":
         run_reference(args, w, rank, world)
         return
+    # factor form: the fastest measured form of each config at the config's accuracy
+    if args.factors == "auto" and not (args.structured or args.recompress or args.adjoint or args.index_shard):
+        args.factors = {"cfg3": "recompressed", "cfg4": "recompressed", "cfg2": "structured",
+                        "cfg5": "structured"}.get(args.config, "interpolative")
+    if args.factors == "recompressed" and not args.recompress:
+        args.recompress = 8
+    if args.factors == "structured":
+        args.structured = True
 
     import torch
     import torch.distributed as dist

@@ -87,13 +87,11 @@ def test_recompress_errors():
 
 def test_recompressed_cfg4_full():
     """cfg4 at full size (N = 2^20, 256 RHS) in the bench's launch configuration (rank 12 recompressed to 8, one
-    chunk of 256 columns): sampled columns against the oracle's own recompression of its FP64 blocks (needs
-    ~90 GB of host memory) and against the direct sum."""
+    chunk of 256 columns): sampled columns against the direct sum (a property at any size: within eps/2 plus the
+    3xTF32 error) and -- with BF_FULL_RECOMPRESS_PARITY=1, ~12 min and ~90 GB of host memory -- against the
+    oracle's own recompression of its FP64 blocks (profiles/r2_v3_pytest_recompress_full.txt)."""
     import os
     w = W.CONFIGS["cfg4"]
-    mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
-    if mem < 150e9:
-        pytest.skip(f"the oracle's full-size recompression needs ~90 GB of host memory ({mem / 1e9:.0f} GB)")
     F = W.rhs(w.n, w.nrhs, w.seed)
     src = bf.Plan.build_fio(bf.fio(w.kernel, w.amp, w.log2n, w.log2leaf, 12), max_nrhs_chunk=1)
     plan = src.recompress(8, max_nrhs_chunk=w.nrhs)
@@ -101,9 +99,10 @@ def test_recompressed_cfg4_full():
     G = gpu_apply(plan, F)
     plan.destroy()
     cols = [0, 200]
-    R = RC.bf_apply_recompressed(w.kernel, w.amp, w.log2n, w.log2leaf, 12, 8, F[:, cols].astype(np.complex128))
-    err = oracle.rel_l2(G[:, cols].astype(np.complex128), R, axis=0)
-    assert np.all(err <= PARITY), err
     rows = W.sample_rows(w.n, w.seed)
     gd = oracle.direct_rows(w.kernel, w.amp, w.log2n, F[:, cols], rows)
     assert np.all(oracle.rel_l2(G[rows][:, cols].astype(np.complex128), gd, axis=0) <= w.eps / 2 + 2e-6)
+    if os.environ.get("BF_FULL_RECOMPRESS_PARITY") == "1":
+        R = RC.bf_apply_recompressed(w.kernel, w.amp, w.log2n, w.log2leaf, 12, 8, F[:, cols].astype(np.complex128))
+        err = oracle.rel_l2(G[:, cols].astype(np.complex128), R, axis=0)
+        assert np.all(err <= PARITY), err
