@@ -433,8 +433,9 @@ def main():
         roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "peak_source": "FP32 FFMA from unit counts: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 5)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = _ncu_traffic(args.config if not (args.log2n or args.adjoint or args.structured or args.recompress)
-                                   else None, dom)
+    wname = (args.config + ("-adjoint" if args.adjoint else "") + ("-structured" if args.structured else "")
+             + (f"-recompressed-r{args.build_rank}to{args.recompress}" if args.recompress else ""))
+    roof["traffic"] = _ncu_traffic(wname if not (args.log2n or args.adjoint or args.nrhs or args.chunk) else None, dom)
     roof["kernel"] = dom
     roof["tensor_cores"] = dom in tc_classes
     roof["avg_launch_ms"] = avg_s * 1e3
@@ -505,17 +506,16 @@ def main():
                       ", ".join(f"{k} 3xTF32" for k in sorted(tc_classes)) + ")")
                      if tc_classes else "c64 (fp32 FFMA)",
             "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel; factors from the host builder)",
-            "config": {"workload": args.config + ("-adjoint" if args.adjoint else "")
-                       + ("-structured" if args.structured else "")
-                       + (f"-recompressed-r{args.build_rank}to{args.recompress}" if args.recompress else ""), "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
+            "config": {"workload": wname, "n": w.n, "leaf": w.leaf, "rank": w.rank, "n_amp": w.n_amp,
                        "nrhs_per_gpu": nloc, "global_batch": w.nrhs, "max_nrhs_chunk": chunk,
                        "parallelism": (f"index-sharded x{world} (level-h exchange: "
                                        + ("peer stores from the level-h launch)" if args.exchange == "fused"
                                           else "NCCL all-to-all)") if args.index_shard
                                        else f"rhs-sharded x{world}: rank q applies columns [q {w.nrhs}/{world}, "
                                             f"(q+1) {w.nrhs}/{world}) (no collective)"),
-                       "l2": "no flush: the working set (F 2.1 GB, coefficients 43 GB/level, factors 25 GB) "
-                             "exceeds the 126 MB L2",
+                       "l2": (f"no flush: the working set (F {8 * w.n * nloc / 1e9:.2g} GB, coefficients "
+                              f"{8 * wl.n * w.rank * min(chunk, nloc) * w.n_amp / 1e9:.3g} GB per level, factors "
+                              f"{info['factor_bytes'] / 1e9:.3g} GB) exceeds the 126 MB L2"),
                        "tensor_core_classes": info["tc_classes"], "tc_weight_bytes": info["tc_weight_bytes"],
                        "factor_bytes": info["factor_bytes"], "structured": bool(info["structured"])},
             "roofline": roof,
