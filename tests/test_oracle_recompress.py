@@ -146,3 +146,14 @@ def test_grams_against_brute_force():
                 S[:, s] = down(d)
             assert np.allclose(Go[l][p], S.conj().T @ S, rtol=1e-10, atol=1e-10 * np.abs(Go[l][p]).max())
             assert np.allclose(Gi[l][p], R[p] @ R[p].conj().T, rtol=1e-10, atol=1e-10 * np.abs(Gi[l][p]).max())
+
+
+def test_rank_rule():
+    """Reading R21: r' = 8 is the smallest even rank whose recompression stays within eps/2 = 5e-7 of the direct
+    sum at eps = 1e-6 (cfg4's kernel and leaf 64, at N = 2^14); r' = 6 does not."""
+    LN, l0 = 14, 6
+    F = W.rhs(1 << LN, 1, 11).astype(np.complex128)
+    rows = W.sample_rows(1 << LN, 3)
+    gd = oracle.direct_rows(W.K_FIO, W.A_CFG1, LN, F, rows)
+    e = {rp: oracle.rel_l2(RC.bf_apply_recompressed(W.K_FIO, W.A_CFG1, LN, l0, 12, rp, F)[rows], gd) for rp in (6, 8)}
+    assert e[8] <= 5e-7 < e[6], e
