@@ -315,6 +315,14 @@ bf_status_t bf_plan_timing(bf_plan_t plan, double *ms, int64_t *launches);
  *                        embeds and splits it; 0: the band composes on chip per group (the default for larger
  *                        chunks, where each group's operator serves several vector tiles). */
 #define BF_OPT_BAND_PRECOMPOSE 11
+/*   BF_OPT_BAND3         1 (default): unsharded dense plans with r in {6, 8} whose chunks hold >= 128 vectors run
+ *                        the transfer levels as three-level tensor-core bands where they leave no lone level
+ *                        (8 levels: 3 + 3 + 2; bf_band3.cu): three adjacent factors of eqn:BFM applied
+ *                        as one 8 x 8 block operator per group of 8 pairs, composed once at finalization in FP64
+ *                        (64 r^2 complex per group, counted in factor_bytes); 0: two-level bands only.  The
+ *                        operators are built at finalization whatever the option; without the memory for all of
+ *                        them none is built and the plan runs two-level bands. */
+#define BF_OPT_BAND3 12
 bf_status_t bf_plan_set_option(bf_plan_t plan, int32_t option, int64_t value);
 
 /* Wait for the plan's outstanding work (the last bf_apply enqueued outside a CUDA-graph capture; replays of a

@@ -30,6 +30,7 @@ BF_OPT_HOST_PIECES = 8
 BF_OPT_LEAF_MULTICAST = 9
 BF_OPT_SMALL_BATCH = 10
 BF_OPT_BAND_PRECOMPOSE = 11
+BF_OPT_BAND3 = 12
 STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALIGNMENT", 4: "BF_ERR_OOM",
           5: "BF_ERR_CUDA", 6: "BF_ERR_NCCL", 7: "BF_ERR_NOT_SUPPORTED", 8: "BF_ERR_STATE"}
 

@@ -84,6 +84,15 @@ cudaError_t launch_band_tc(const Dims& d, int l_first, const float2* in, float2*
 cudaError_t launch_compose_band(const Dims& d, int l_first, const float2* W1, const float2* W2, float2* Cg,
                                 cudaStream_t s);
 
+// Band of 3 transfer levels on the tensor cores (bf_band3.cu, r in {6, 8}, nv >= 128): the band's precomposed
+// 8 x 8 block operator per group of 8 pairs (launch_compose3 at finalization, band3_operator_elems complex).
+bool band3_supported(const Dims& d, int nv);
+int64_t band3_operator_elems(const Dims& d);
+cudaError_t launch_band3(const Dims& d, int l_first, const float2* in, float2* out, const float2* Cpre, int nv,
+                         cudaStream_t s);
+cudaError_t launch_compose3(const Dims& d, int l_first, const float2* W1, const float2* W2, const float2* W3,
+                            float2* Cg, cudaStream_t s);
+
 
 // Plan finalization: W[p] <- Sw[p] W[p] for npairs blocks (W column-major R x cols, Sw R x R).
 cudaError_t launch_fold_switch(const float2* Sw, float2* W, int64_t npairs, int R, int cols, cudaStream_t s);

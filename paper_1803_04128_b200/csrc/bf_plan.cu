@@ -143,6 +143,7 @@ struct Shard {
     float2* u = nullptr;
     std::vector<float2*> xfer;
     std::vector<float2*> cmp;  // [level index of a band's first level]: precomposed two-level operator, or null
+    std::vector<float2*> cmp3; // [level index of a band's first level]: precomposed three-level operator, or null
     float* v0x = nullptr;      // tensor-core image of V0 / U (bf_tc.cu), built at finalize when used
     float* ux = nullptr;
     float2* ws = nullptr;      // two coefficient arrays of (N/G) R nv_max
@@ -200,6 +201,7 @@ struct bf_plan_s {
     bool leaf_multicast = true;  // BF_OPT_LEAF_MULTICAST: TF32 S0 / SL as 2-CTA clusters sharing the weight stream
     bool small_batch = true;      // BF_OPT_SMALL_BATCH: fused bands for small vector batches (bf_small.cu)
     bool precompose = true;      // BF_OPT_BAND_PRECOMPOSE: use the finalize-time composed band operators
+    bool band3 = true;           // BF_OPT_BAND3: three-level tensor-core bands (bf_band3.cu) where built
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -319,6 +321,7 @@ void free_plan(bf_plan_s* p)
         cudaFree(s.u);
         for (auto x : s.xfer) cudaFree(x);
         for (auto x : s.cmp) cudaFree(x);
+        for (auto x : s.cmp3) cudaFree(x);
         cudaFree(s.ws);
         cudaFree(s.s0_lag);
         cudaFree(s.s0_ph);
@@ -388,11 +391,15 @@ struct Step {
     int levels = 0;    // transfer levels this launch performs
 };
 
-template <class Ok>
-void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool band, Ok&& pair_ok)
+// K = 3 where can3(l) (three-level tensor-core bands): 3s while they leave no lone level behind (8 levels:
+// 3 + 3 + 2, 10: 3 + 3 + 2 + 2).
+template <class Ok, class Ok3>
+void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool band, Ok&& pair_ok, Ok3&& can3)
 {
     for (int l = lo; l <= hi;) {
-        const int K = (band && l < hi && pair_ok(l)) ? 2 : 1;
+        const int rem = hi - l + 1;
+        int K = (band && l < hi && pair_ok(l)) ? 2 : 1;
+        if (K == 2 && rem >= 3 && rem != 4 && can3(l)) K = 3;
         const int last = l + K - 1;
         const bool has_h = (l <= d.h && d.h <= last);
         const int cls = has_h ? bfk::KC_SWITCH : (last < d.h ? bfk::KC_XFER1 : bfk::KC_XFER2);
@@ -405,7 +412,7 @@ void push_levels(std::vector<Step>& st, const bfk::Dims& d, int lo, int hi, bool
 // when the band kernel supports the shape, the switch applied inside the launch that produces level h),
 // SL.  With no transfer level (h == l0) the switch runs alone after S0.  Sharded: the bands stop at h,
 // the exchange follows, then the second half.
-std::vector<Step> schedule(const bf_plan_s* p, int nv)
+std::vector<Step> schedule(const bf_plan_s* p, int nv, bool plan3 = false)
 {
     const bfk::Dims& d = p->d;
     const bool sharded = p->mode != BF_SHARD_NONE, small_batch = p->small_batch;
@@ -419,12 +426,16 @@ std::vector<Step> schedule(const bf_plan_s* p, int nv)
     const Shard& s0 = p->sh[0];
     auto kind_of = [&](int l) { return s0.xfer[l - d.l0 - 1] ? 0 : s0.kind[l - d.l0 - 1]; };
     auto pair_ok = [&](int l) { return s0.dense_all() || bfk::band_st_kinds(kind_of(l), kind_of(l + 1)); };
+    // three-level bands: unsharded dense plans on the tensor cores whose operator was composed at finalization
+    // (plan3: the schedule finalization builds those operators for)
+    const bool use3 = !sharded && p->band3 && p->tensor_cores && s0.dense_all() && bfk::band3_supported(d, nv);
+    auto can3 = [&](int l) { return use3 && (plan3 || s0.cmp3[l - d.l0 - 1] != nullptr); };
     if (!sharded) {
-        push_levels(st, d, d.l0 + 1, d.D, band, pair_ok);
+        push_levels(st, d, d.l0 + 1, d.D, band, pair_ok, can3);
     } else {
-        push_levels(st, d, d.l0 + 1, d.h, band, pair_ok);
+        push_levels(st, d, d.l0 + 1, d.h, band, pair_ok, can3);
         st.push_back({Step::EXCHANGE, 0, 1, KC_EXCHANGE, 0});
-        push_levels(st, d, d.h + 1, d.D, band, pair_ok);
+        push_levels(st, d, d.h + 1, d.D, band, pair_ok, can3);
     }
     st.push_back({Step::SL, 0, 1, bfk::KC_SL, 0});
     return st;
@@ -522,6 +533,7 @@ bf_status_t run_steps(bf_plan_s* p, Shard& sh, const std::vector<Step>& st, size
                     return bfk::launch_band_st(dl, lk, k1, k2, L2, sh.xfer[li] ? sh.xfer[li] : sh.ph[li],
                                                sh.xfer[li + 1] ? sh.xfer[li + 1] : sh.ph[li + 1], in, out, nv, s);
                 }
+                if (stp.K == 3) return bfk::launch_band3(dl, lk, in, out, sh.cmp3[li], nv, s);
                 const float2* W[2] = {sh.xfer[li], stp.K > 1 ? sh.xfer[li + 1] : nullptr};
                 if (stp.K == 2 && p->tensor_cores && bfk::band_tc_supported(dl, nv))
                     return bfk::launch_band_tc(dl, lk, in, out, W, nv, s, rh, rhg, po, p->band,
@@ -760,6 +772,7 @@ bf_status_t alloc_plan(const bf_desc_t* meta, int device, int64_t max_nrhs_chunk
     for (auto& s : p->sh) {
         s.xfer.assign(nx, nullptr);
         s.cmp.assign(nx, nullptr);
+        s.cmp3.assign(nx, nullptr);
         s.kind.assign(nx, BF_LEVEL_DENSE);
         s.lag.assign(nx, nullptr);
         s.lagh.assign(nx, bfk::LagP{});
@@ -1101,6 +1114,38 @@ bf_status_t bf_plan_finalize(bf_plan_t p)
             if (bf_status_t st = build_leaf_images(p, s); st != BF_OK) return st;
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e, "leaf weight expansion");
+    }
+    // three-level tensor-core bands (bf_band3.cu): compose each band's 8 x 8 block operator per group of 8 pairs
+    // once (FP64 products).  Without the memory for one, that band's levels fall back to two-level bands.
+    {
+        const int nvf = int(p->max_chunk * p->d.n_amp);
+        for (const auto& stp : schedule(p, nvf, true)) {
+            if (stp.kind != Step::BAND || stp.K != 3) continue;
+            const int li = stp.l_first - p->d.l0 - 1;
+            for (Shard& s : p->sh) {
+                if (s.cmp3[li]) continue;
+                if (cudaMalloc(&s.cmp3[li], size_t(bfk::band3_operator_elems(dl)) * sizeof(float2)) != cudaSuccess) {
+                    cudaGetLastError();
+                    s.cmp3[li] = nullptr;
+                    continue;
+                }
+                e = bfk::launch_compose3(dl, stp.l_first, s.xfer[li], s.xfer[li + 1], s.xfer[li + 2], s.cmp3[li], 0);
+                if (e != cudaSuccess) return cuda_fail(e, "band3 precompose");
+            }
+        }
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(e, "band3 precompose");
+        // a band whose operator is missing would break the 3-level grouping of the ones after it: keep all or none
+        bool all = true;
+        for (const auto& stp : schedule(p, nvf, true))
+            if (stp.kind == Step::BAND && stp.K == 3)
+                for (Shard& s : p->sh) all = all && s.cmp3[stp.l_first - p->d.l0 - 1] != nullptr;
+        if (!all)
+            for (Shard& s : p->sh)
+                for (auto& x : s.cmp3) {
+                    cudaFree(x);
+                    x = nullptr;
+                }
     }
     // small vector batches (<= 2 tiles of 128 vectors per chunk): precompose every tensor-core band's two-level
     // operator once (FP64 products), so the band kernel only embeds and splits it per group instead of
@@ -1503,6 +1548,9 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     for (const Shard& s : p->sh)
         for (auto c : s.cmp)
             if (c) info->factor_bytes += 8 * n * 4 * r * r;   // precomposed band operators
+    for (const Shard& s : p->sh)
+        for (auto c : s.cmp3)
+            if (c) info->factor_bytes += 8 * n * 8 * r * r;   // precomposed three-level band operators
     info->workspace_bytes = nsh * int64_t(p->ws_bytes);
     info->tc_weight_bytes = 0;
     for (const Shard& s : p->sh) {
@@ -1519,7 +1567,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
         if (p->tensor_cores && p->sh[0].ux && bfk::sl_tc_supported(dl, nvf)) mask |= 1 << bfk::KC_SL;
         if (p->tensor_cores && bfk::band_tc_supported(dl, nvf))
             for (const auto& stp : schedule(p, nvf))
-                if (stp.kind == Step::BAND && stp.K == 2) mask |= 1 << stp.cls;
+                if (stp.kind == Step::BAND && stp.K >= 2) mask |= 1 << stp.cls;
         info->tc_class_mask = mask;
     }
     const auto st = schedule(p, int(p->max_chunk * p->d.n_amp));
@@ -1619,6 +1667,11 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
     if (option == BF_OPT_LEAF_MULTICAST) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_LEAF_MULTICAST takes 0 or 1");
         p->leaf_multicast = value != 0;
+        return BF_OK;
+    }
+    if (option == BF_OPT_BAND3) {
+        if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_BAND3 takes 0 or 1");
+        p->band3 = value != 0;
         return BF_OK;
     }
     if (option == BF_OPT_BAND_PRECOMPOSE) {

@@ -1567,4 +1567,11 @@ cudaError_t launch_compose_band(const Dims& d, int l_first, const float2* W1, co
     return cudaGetLastError();
 }
 
+// shared with bf_band3.cu
+cudaError_t rows_tmap(CUtensorMap* m, const float2* base, int64_t rows, int nv, int box_rows)
+{
+    return make_rows_tmap(m, base, rows, nv, box_rows);
+}
+int tc_sm_count() { return sm_count(); }
+
 }  // namespace bfk

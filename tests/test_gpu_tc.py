@@ -297,3 +297,43 @@ def test_tc_band_precomposed(r, l0, LN, nrhs):
     d = oracle.rel_l2(Gp.astype(np.complex128), Gc.astype(np.complex128), axis=0)
     assert np.all(d <= PATHS_AGREE), d.max()
     assert not np.array_equal(Gp, Gc)
+
+
+@pytest.mark.parametrize("r,l0,LN,nrhs,chunk", [(8, 5, 16, 128, 128),   # 6 levels: 3 + 3, 2 vector tiles
+                                                (6, 5, 16, 100, 100),   # r = 6, nv = 200: full + ragged tile
+                                                (8, 6, 18, 64, 64),     # one vector tile per group
+                                                (8, 5, 18, 128, 128),   # 8 levels: 3 + 3 + 2 (cfg4's schedule)
+                                                (8, 5, 16, 150, 64)])   # chunks of 128 + 128 + 44 vectors
+def test_tc_band3(r, l0, LN, nrhs, chunk):
+    """Three-level tensor-core bands (bf_band3.cu, BF_OPT_BAND3 = 1, default for r in {6, 8} and >= 128 vectors):
+    three adjacent factors of eqn:BFM applied as one 8 x 8 block operator per group of 8 pairs, composed at
+    finalization in FP64.  Against the oracle at the bar, against the two-level bands (BF_OPT_BAND3 = 0) like two
+    FP32-accurate paths; the schedule (launches per class) and the operator bytes in factor_bytes."""
+    N = 1 << LN
+    F = W.rhs(N, nrhs, 90 + r + LN)
+    k = bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r)
+    plan = bf.Plan.build_fio(k, max_nrhs_chunk=chunk)
+    info = plan.info()
+    nlev = LN - 2 * l0
+    n3 = {6: 2, 8: 2}[nlev]
+    nb = n3 + (nlev - 3 * n3) // 2
+    assert sum(info["class_launches"][c] for c in ("xfer_first_half", "xfer_switch", "xfer_second_half")) == nb, info
+    assert any(c.startswith("xfer") for c in info["tc_classes"])
+    G3 = _apply(plan, F)
+    plan.set_option(bf.BF_OPT_BAND3, 0)
+    G2 = _apply(plan, F)
+    with pytest.raises(bf.BFError):
+        plan.set_option(bf.BF_OPT_BAND3, 2)
+    plan.destroy()
+    base = bf.Plan.build_fio(k, max_nrhs_chunk=16)          # 32 vectors: no three-level operators
+    # three-level operators (64 r^2 complex per 8 pairs) + the remaining two-level bands' precomposed operators
+    cmp2 = ((nlev - 3 * n3) // 2) * 8 * N * 4 * r * r if 2 * chunk <= 256 else 0
+    assert info["factor_bytes"] - base.info()["factor_bytes"] == n3 * 8 * N * 8 * r * r + cmp2, info
+    base.destroy()
+    assert np.all(np.isfinite(G3))
+    cols = [0, nrhs // 2, nrhs - 1]
+    R = oracle.bf_apply(W.K_FIO, W.A_CFG1, LN, l0, r, F[:, cols])
+    for G in (G3, G2):
+        assert np.all(oracle.rel_l2(G[:, cols].astype(np.complex128), R, axis=0) <= PARITY)
+    d = oracle.rel_l2(G3.astype(np.complex128), G2.astype(np.complex128), axis=0)
+    assert np.all(d <= PATHS_AGREE), d.max()

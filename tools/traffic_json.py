@@ -19,7 +19,7 @@ rows = list(csv.DictReader(io.StringIO("".join(lines))))
 launches = OrderedDict()
 for r in rows:
     launches.setdefault(r["ID"], {"kernel": r["Kernel Name"]})[r["Metric Name"]] = float(r["Metric Value"])
-seq = list(launches.values())
+seq = [s for s in launches.values() if not s["kernel"].startswith(("expand_", "compose"))]   # plan finalization
 names = [s["kernel"] for s in seq]
 # one apply: the first S0 launch through the next SL launch; the bands in between follow the schedule order
 i0 = next(i for i, n in enumerate(names) if "s0_" in n)
