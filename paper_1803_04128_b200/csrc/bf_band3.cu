@@ -21,11 +21,12 @@
 //   warps 0-7           split them hi/lo into A in TMEM (lane quadrant warp & 3; K half warp >> 2 = input
 //                       pairs 4 kh .. 4 kh + 3),
 //   warp 13             per job and K half: 3 passes (3xTF32, corrections first) x (8r / 8) MMAs into one of two
-//                       TMEM accumulators (N = 16 r); A and B are released per K half, so the split and the
-//                       weight fill of the next job / group overlap the MMAs of the other half,
+//                       TMEM accumulators (N = 16 r); A is released per K half, so the split of the next job
+//                       overlaps the MMAs of the other half; B is released after the group's last tile,
 //   warps 8-11          drain the accumulator (lane = vector) and store the 8 output pairs (pointer walk),
 //   warps 14-15         embed + split the group's precomposed operator into the B tile (hi | lo, canonical
-//                       K-major), per K half, its loads issued before the half is free.
+//                       K-major), per K half (the MMAs of a group's first tile start on half 0), its loads issued
+//                       before the tile is free.
 // TMEM: A hi/lo 2 x 16r columns + 2 accumulators of 16r = 64 r <= 512, hence r <= 8.
 // Shared memory: the B tile (2 x (16r)^2 x 4 B = 128 KB at r = 8) + the raw ring (12 slots of r x 1 KB).
 #include <cuda.h>
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(512, 1)
     using C = Band3<R>;
     extern __shared__ __align__(128) uint8_t sm3[];
     __shared__ uint64_t slot_full[16], slot_empty[16];
-    __shared__ uint64_t a_ready[2], a_free[2], d_full[2], d_free[2], w_full[2], w_free[2];
+    __shared__ uint64_t a_ready[2], a_free[2], d_full[2], d_free[2], w_full[2], w_free;
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -101,8 +102,8 @@ __global__ void __launch_bounds__(512, 1)
             tc::mbar_init(&d_full[i], 1);
             tc::mbar_init(&d_free[i], 128);
             tc::mbar_init(&w_full[i], 64);
-            tc::mbar_init(&w_free[i], 1);
         }
+        tc::mbar_init(&w_free, 1);
         tc::mbar_fence_init();
     }
     tc::fence_before_sync();
@@ -219,7 +220,11 @@ __global__ void __launch_bounds__(512, 1)
                                              (kh | qq | ks) ? 1u : 0u);
                 }
                 tc::commit_warp(&a_free[kh]);
-                if (vt == nvt - 1) tc::commit_warp(&w_free[kh]);
+                // the B tile is released whole, after the group's last K half: releasing it per K half (the fill of
+                // the next group's K half 0 overlapping the last tile's K-half-1 MMAs) corrupted the next group's
+                // first vector tile on B200, non-deterministically (measured; the halves are disjoint bytes, and
+                // the hazard is not understood), so that overlap is not used
+                if (vt == nvt - 1 && kh == 1) tc::commit_warp(&w_free);
             }
             tc::commit_warp(&d_full[db]);
             __syncwarp();
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                     for (int j2 = 0; j2 < R / 2; j2++) c[rr][j2] = __ldg(src + j2);
                 }
-                if (it >= 1) tc::mbar_wait(&w_free[kh], uint32_t(it - 1) & 1);
+                if (it >= 1 && kh == 0) tc::mbar_wait(&w_free, uint32_t(it - 1) & 1);
 #pragma unroll
                 for (int rr = 0; rr < C::RPT; rr++) {
                     const int row = wt + 64 * rr, tp = row % R, oi = row / R, o = oi >> 2, i = 4 * kh + (oi & 3);

@@ -526,18 +526,31 @@ struct SLTC {
     static constexpr uint32_t BT = uint32_t(NB) * KC * 4;   // one of hi / lo
     static constexpr uint32_t GS_STRIDE = N0 + 1;
     static constexpr uint32_t GS_BYTES = uint32_t(128 / NA) * GS_STRIDE * 8;
-    static constexpr uint32_t AS_BYTES = uint32_t(NA) * N0 * 8;
+    static constexpr uint32_t AS_BYTES = 2 * uint32_t(NA) * N0 * 8;   // a_k(x) of two jobs (double-buffered)
     // separate rings: the coefficient rows come from DRAM (deep ring), the Ux tiles mostly from L2 (2 deep)
+#ifdef BF_SL_NBR
+    static constexpr int NB_R = BF_SL_NBR;
+#else
     static constexpr int NB_R = 3;                                   // Ux ring depth
+#endif
     static constexpr int NR_FIT = int((232448 - 1024 - GS_BYTES - AS_BYTES - NB_R * 2 * BT) / RAW);
     static constexpr int NR = NR_FIT > 8 ? 8 : NR_FIT;               // raw ring depth
     static constexpr uint32_t OFF_B = NR * RAW, OFF_GS = OFF_B + 2 * NB_R * BT, OFF_AS = OFF_GS + GS_BYTES;
     static constexpr size_t SMEM = size_t(OFF_AS) + AS_BYTES;
     // TMEM: two A stages (hi KC columns, then lo KC columns) and two accumulators of NB columns
-    static constexpr int A_COLS = 2 * KC, D_OFF = 2 * A_COLS;
+    // A stages: as many as TMEM holds beside the two accumulators (up to 4): the split of chunk g + NAS overlaps
+    // the MMAs of the chunks before it instead of waiting for chunk g's MMAs to finish (2 stages left the tensor
+    // pipe idle across every split + mbarrier round trip)
+    static constexpr int A_COLS = 2 * KC;
+#ifdef BF_SL_NAS
+    static constexpr int NAS = BF_SL_NAS;
+#else
+    static constexpr int NAS = (512 - 2 * NB) / A_COLS >= 4 ? 4 : (512 - 2 * NB) / A_COLS;
+#endif
+    static constexpr int D_OFF = NAS * A_COLS;
     static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * NB>();
     static_assert(KC % 8 == 0, "K chunk must be whole MMA K steps");
-    static_assert(D_OFF + 2 * NB <= 512, "TMEM budget");
+    static_assert(NAS >= 2 && D_OFF + 2 * NB <= 512, "TMEM budget");
     static_assert(SMEM <= 232448 - 1024 && NR >= 2, "shared memory budget");
 };
 
@@ -554,8 +567,8 @@ __global__ void __launch_bounds__(448, 1)
     auto raw = [&](int e) { return sm_sltc + e * C::RAW; };
     auto opB = [&](int e, int lo) { return sm_sltc + C::OFF_B + (2 * e + lo) * C::BT; };
     float2* Gs = reinterpret_cast<float2*>(sm_sltc + C::OFF_GS);   // [128/NA][GS_STRIDE]
-    float2* As = reinterpret_cast<float2*>(sm_sltc + C::OFF_AS);   // [NA][N0] a_k(x) of the current job
-    __shared__ uint64_t raw_full[C::NR], raw_empty[C::NR], b_full[C::NB_R], b_empty[C::NB_R], a_full[2], a_empty[2],
+    float2* As = reinterpret_cast<float2*>(sm_sltc + C::OFF_AS);   // [2][NA][N0] a_k(x) of the current / next job
+    __shared__ uint64_t raw_full[C::NR], raw_empty[C::NR], b_full[C::NB_R], b_empty[C::NB_R], a_full[4], a_empty[4],
         dfull[2], dempty[2];
     __shared__ uint32_t tmem_base;
     constexpr int TMEM_COLS = C::TMEM_COLS;
@@ -587,10 +600,12 @@ __global__ void __launch_bounds__(448, 1)
             tc::mbar_init(&b_empty[i], CL);   // released by the MMA commit of every CTA of the cluster
         }
         for (int i = 0; i < 2; i++) {
-            tc::mbar_init(&a_full[i], 128);
-            tc::mbar_init(&a_empty[i], 1);
             tc::mbar_init(&dfull[i], 1);
             tc::mbar_init(&dempty[i], 256);
+        }
+        for (int i = 0; i < C::NAS; i++) {
+            tc::mbar_init(&a_full[i], 128);
+            tc::mbar_init(&a_empty[i], 1);
         }
         tc::mbar_fence_init();
     }
@@ -641,10 +656,10 @@ __global__ void __launch_bounds__(448, 1)
         int gseg = 0;   // accumulation segments issued (slots alternate across jobs)
         for (int gch = 0; gch < nch_all; gch++) {
             const int ch = gch % C::NCH;
-            const int e = gch % C::NB_R, sa = gch & 1, slot = gseg & 1, first = (ch % C::SEG) == 0;
+            const int e = gch % C::NB_R, sa = gch % C::NAS, slot = gseg & 1, first = (ch % C::SEG) == 0;
             const bool last = (ch % C::SEG) == C::SEG - 1 || ch == C::NCH - 1;
             if (first && gseg >= 2) tc::mbar_wait(&dempty[slot], uint32_t((gseg >> 1) - 1) & 1);
-            tc::mbar_wait(&a_full[sa], uint32_t(gch >> 1) & 1);
+            tc::mbar_wait(&a_full[sa], uint32_t(gch / C::NAS) & 1);
             tc::mbar_wait(&b_full[e], uint32_t(gch / C::NB_R) & 1);
             tc::fence_after_sync();
             const uint32_t d = tmem + uint32_t(C::D_OFF + slot * C::NB);
@@ -674,9 +689,9 @@ __global__ void __launch_bounds__(448, 1)
         const int v = tid;
         const uint32_t lb = uint32_t(warp * 32) << 16;
         for (int gch = 0; gch < nch_all; gch++) {
-            const int e = gch % C::NR, sa = gch & 1;
+            const int e = gch % C::NR, sa = gch % C::NAS;
             tc::mbar_wait(&raw_full[e], uint32_t(gch / C::NR) & 1);
-            if (gch >= 2) tc::mbar_wait(&a_empty[sa], uint32_t((gch >> 1) - 1) & 1);
+            if (gch >= C::NAS) tc::mbar_wait(&a_empty[sa], uint32_t(gch / C::NAS - 1) & 1);
             tc::fence_after_sync();
             const float2* rd = reinterpret_cast<const float2*>(raw(e));   // [KP R][128]
             float hi[C::KC], lo[C::KC];   // column (pl, t, c) = pl 2R + 2t + c
@@ -706,6 +721,15 @@ __global__ void __launch_bounds__(448, 1)
             int v0;
             job_of(jl, a, v0);
             const int vw = min(128, nv - v0);
+            // a_k(x) of this job's leaf: cp.async into the job's half of the double-buffered As now, so the
+            // global-load latency hides behind the segment drains (it sat on the epilogue's critical path, while
+            // the MMA can run only two segments ahead)
+            float2* Asj = As + (jl & 1) * (NA * N0);
+            for (int i = dt; i < NA * N0; i += 256)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(tc::smem_u32(Asj + i)),
+                             "l"(ampa + (i / N0) * N + a * N0 + (i % N0))
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
             float sum[HC];
 #pragma unroll
             for (int i = 0; i < HC; i++) sum[i] = 0.f;
@@ -727,13 +751,12 @@ __global__ void __launch_bounds__(448, 1)
                 tc::mbar_arrive(&dempty[slot]);
             }
             // epilogue of the job: a_k(x) (staged per job), sum over k, G transposed through Gs
-            asm volatile("bar.sync 1, 256;" ::: "memory");   // the previous job's copy-out is done with Gs / As
-            for (int i = dt; i < NA * N0; i += 256) As[i] = __ldg(ampa + (i / N0) * N + a * N0 + (i % N0));
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            asm volatile("bar.sync 1, 256;" ::: "memory");   // Asj complete; the previous job is done with Gs
 #pragma unroll
             for (int jj = 0; jj < HC / 2; jj++) {
                 const int j = half * (HC / 2) + jj;
-                float2 g = cmul_tc(As[k * N0 + j], make_float2(sum[2 * jj], sum[2 * jj + 1]));
+                float2 g = cmul_tc(Asj[k * N0 + j], make_float2(sum[2 * jj], sum[2 * jj + 1]));
 #pragma unroll
                 for (int m = 1; m < NA; m <<= 1) {
                     g.x += __shfl_xor_sync(0xffffffffu, g.x, m);

@@ -320,6 +320,8 @@ def test_tc_band3(r, l0, LN, nrhs, chunk):
     assert sum(info["class_launches"][c] for c in ("xfer_first_half", "xfer_switch", "xfer_second_half")) == nb, info
     assert any(c.startswith("xfer") for c in info["tc_classes"])
     G3 = _apply(plan, F)
+    for _ in range(3):   # run-to-run bitwise (a B-tile hazard once showed up as non-determinism in one vector tile)
+        assert np.array_equal(_apply(plan, F), G3)
     plan.set_option(bf.BF_OPT_BAND3, 0)
     G2 = _apply(plan, F)
     with pytest.raises(bf.BFError):
