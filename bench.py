@@ -222,6 +222,92 @@ def run_reference(args, w, rank, world):
     }), flush=True)
 
 
+def run_nufft(args, w, rank, world, local):
+    """--path nufft: the NUFFT path (include/bf_nufft.h) on the config's workload, RHS-sharded like the butterfly.
+    Roofline: the whole apply (place + cuFFT + interpolation) against HBM, algorithmic bytes = F and G once plus
+    the fine grids' M placed frequencies written once, the grids read and written once by the FFT and read once
+    by the interpolation (3.5 x 8 n_sub nv n_f)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1803_04128_b200 import bf
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c0, c1 = rhs_columns(w.nrhs, world, rank)
+    nloc = c1 - c0
+    chunk = args.chunk or nloc
+    t0 = time.perf_counter()
+    plan = bf.NufftPlan.build_fio(bf.fio_of(w), device=local, max_nrhs_chunk=chunk, eps=w.eps)
+    t_build = time.perf_counter() - t0
+    info = plan.info()
+    F = W.rhs(w.n, w.nrhs, w.seed) if world == 1 else W.rhs(w.n, w.nrhs, w.seed, cols=range(c0, c1))
+    Fd = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()
+    Gd = torch.empty_like(Fd)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.apply(Fd, Gd, nloc, stream=stream)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.apply(Fd, Gd, nloc, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    hbm, hbm_src, _, _ = _peaks()
+    nv = min(chunk, nloc) * w.n_amp
+    grid_bytes = 8 * 2 * nv * info["grid"] * (-(-nloc // chunk))
+    byts = 16 * w.n * nloc + 3.5 * grid_bytes + 8 * 2 * w.n_amp * w.n
+    roof = {"bound": "hbm", "achieved": byts / (ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})", "traffic": None,
+            "kernel": "whole apply: place_kernel + cuFFT C2C (library) + interp_kernel",
+            "algorithmic_bytes": byts}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    acc = cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        rows = W.sample_rows(w.n, w.seed)
+        F0 = W.rhs(w.n, w.nrhs, w.seed, cols=[0])
+        ts = time.perf_counter()
+        gd = oracle.direct_rows(w.kernel, w.amp, w.log2n, F0, rows)[:, 0]
+        dt = time.perf_counter() - ts
+        g0 = Gd[0].cpu().numpy().astype(np.complex128)
+        acc = {"column": 0, "rows": len(rows), "gpu_vs_direct": float(oracle.rel_l2(g0[rows], gd)),
+               "eps": w.eps, "width": info["width"]}
+        cpu = {"value": len(rows) / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+               "seconds": dt, "sample": f"{w.name}: {len(rows)} rows of RHS column 0 by the direct sum O0 (FP64; "
+                                        "the oracle evaluates eqn:tg3 by its definition), one row = one N*RHS unit"}
+    if rank == 0:
+        out = {"metric": METRIC, "value": w.n * w.nrhs / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "impl": "nufft-path",
+               "dtype": "c64 (fp32 place/interp, cuFFT C2C single precision)",
+               "data": "synthetic (seeded Gaussian complex64 RHS; closed-form FIO kernel)",
+               "config": {"workload": f"{w.name}-nufft", "n": w.n, "n_amp": w.n_amp, "nrhs_per_gpu": nloc,
+                          "global_batch": w.nrhs, "max_nrhs_chunk": chunk, "width": info["width"],
+                          "grid": info["grid"], "submatrices": 2,
+                          "parallelism": f"rhs-sharded x{world} (no collective)",
+                          "l2": f"no flush: the fine grids ({grid_bytes / 1e9:.3g} GB) exceed the 126 MB L2"},
+               "roofline": roof, "e2e": None, "gpu_launches": info["launches_per_chunk"] * (-(-nloc // chunk))
+               * args.steps, "cpu_baseline": cpu, "clocks": clk.summary(), "accuracy": acc,
+               "plan_build_s": t_build}
+        print(json.dumps(out), flush=True)
+    plan.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -255,6 +341,9 @@ def main():
     ap.add_argument("--recompress", type=int, default=None, metavar="RP",
                     help="recompress the interpolative factorization of rank --build-rank to rank RP (NEXT-3)")
     ap.add_argument("--build-rank", type=int, default=12, help="interpolative rank before --recompress")
+    ap.add_argument("--path", choices=["bf", "nufft"], default="bf",
+                    help="bf: the IBF-MAT butterfly (the north_star path); nufft: the NUFFT path of the unified "
+                         "framework (eqn:tg3 with type-2 NUFFTs on the xi<0 / xi>=0 submatrices, DESIGN.md 5.8)")
     ap.add_argument("--adjoint", action="store_true",
                     help="time the adjoint apply K* (bf_plan_create_adjoint from the forward plan)")
     args = ap.parse_args()
@@ -289,6 +378,9 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, w, rank, world)
+        return
+    if args.path == "nufft":
+        run_nufft(args, w, rank, world, local)
         return
     # factor form: the fastest measured form of each config at the config's accuracy
     if args.factors == "auto" and not (args.structured or args.recompress or args.adjoint or args.index_shard):

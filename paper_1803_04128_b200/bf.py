@@ -41,7 +41,8 @@ EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finaliz
            "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
            "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated", "bf_plan_create_adjoint",
            "bf_plan_create_structured", "bf_plan_build_fio_structured", "bf_build_structured",
-           "bf_build_structured_lag", "bf_plan_recompress")
+           "bf_build_structured_lag", "bf_plan_recompress", "bf_nufft_create", "bf_nufft_apply",
+           "bf_nufft_get_info", "bf_nufft_destroy", "bf_nufft_build_fio")
 
 
 class BFError(RuntimeError):
@@ -74,6 +75,17 @@ class bf_fio_t(ctypes.Structure):
 
 
 _lib = None
+
+
+class bf_nufft_desc_t(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_int32), ("log2n", ctypes.c_int32), ("n_amp", ctypes.c_int32),
+                ("n_sub", ctypes.c_int32), ("targets", ctypes.c_void_p), ("amp_a", ctypes.c_void_p),
+                ("amp_b", ctypes.c_void_p), ("eps", ctypes.c_double)]
+
+
+class bf_nufft_info_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("width", ctypes.c_int32), ("beta", ctypes.c_double), ("grid", ctypes.c_int64),
+                ("workspace_bytes", ctypes.c_int64), ("launches_per_chunk", ctypes.c_int32)]
 
 
 def lib():
@@ -133,6 +145,11 @@ def lib():
             "bf_shard_pairs": ([i32, i32, i32, i32, i32, vp], i32),
             "bf_plan_build_fio_sharded": ([P(bf_fio_t), ctypes.c_int, i32, i32, vp, i64, i64, P(vp)], i32),
             "bf_plan_build_fio_emulated": ([P(bf_fio_t), ctypes.c_int, i32, i64, i64, P(vp)], i32),
+            "bf_nufft_create": ([P(bf_nufft_desc_t), ctypes.c_int, i64, P(vp)], i32),
+            "bf_nufft_apply": ([vp, vp, i64, vp, i64, i64, vp], i32),
+            "bf_nufft_get_info": ([vp, P(bf_nufft_info_t)], i32),
+            "bf_nufft_destroy": ([vp], i32),
+            "bf_nufft_build_fio": ([P(bf_fio_t), ctypes.c_int, i64, ctypes.c_double, P(vp)], i32),
         }
         for name, (args, res) in sigs.items():
             f = getattr(L, name)
@@ -354,3 +371,51 @@ class Plan:
                 lib().bf_plan_destroy(self._h)
         except Exception:
             pass
+
+
+class NufftPlan:
+    """Owns a bf_nufft_t: the NUFFT path of include/bf_nufft.h (eqn:tg3 with one-dimensional type-2 NUFFTs on the
+    frequency submatrices)."""
+
+    def __init__(self, handle: int):
+        self._h = ctypes.c_void_p(handle)
+
+    @classmethod
+    def build_fio(cls, k: bf_fio_t, device: int = 0, max_nrhs_chunk: int = 1, eps: float = 1e-6):
+        """Closed-form targets t_-(x) = x - c(x), t_+(x) = x + c(x) and the amplitude split (bf_nufft_build_fio)."""
+        h = ctypes.c_void_p()
+        _check(lib().bf_nufft_build_fio(ctypes.byref(k), device, max_nrhs_chunk, eps, ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def create(cls, targets: np.ndarray, amp_a: np.ndarray, amp_b: np.ndarray, eps: float = 1e-6, device: int = 0,
+               max_nrhs_chunk: int = 1):
+        """targets: float64 [n_sub][N]; amp_a, amp_b: complex64 [n_amp][N] (host arrays, copied)."""
+        t = np.ascontiguousarray(targets, np.float64)
+        a = np.ascontiguousarray(amp_a, np.complex64)
+        b = np.ascontiguousarray(amp_b, np.complex64)
+        n_sub, N = t.shape
+        d = bf_nufft_desc_t(BF_ABI_VERSION, int(N).bit_length() - 1, a.shape[0], n_sub, t.ctypes.data, a.ctypes.data,
+                            b.ctypes.data, eps)
+        h = ctypes.c_void_p()
+        _check(lib().bf_nufft_create(ctypes.byref(d), device, max_nrhs_chunk, ctypes.byref(h)))
+        return cls(h.value)
+
+    def apply(self, F, G, nrhs: int, ldf: int = 0, ldg: int = 0, stream=None):
+        """G = the NUFFT path applied to F (device buffers, N x nrhs column-major; ld 0 = N)."""
+        n = self.n
+        _check(lib().bf_nufft_apply(self._h, _ptr(F), ldf or n, _ptr(G), ldg or n, nrhs, _stream(stream)))
+
+    def info(self) -> dict:
+        i = bf_nufft_info_t()
+        _check(lib().bf_nufft_get_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in bf_nufft_info_t._fields_}
+
+    @property
+    def n(self) -> int:
+        return int(self.info()["n"])
+
+    def destroy(self):
+        if self._h is not None and self._h.value:
+            _check(lib().bf_nufft_destroy(self._h))
+        self._h = None

@@ -20,7 +20,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas"
 NVCC_FLAGS += [f"-D{m}" for m in os.environ.get("BF_NVCC_DEFINES", "").split()]   # tuning experiments only
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-march=x86-64-v3", "-ffp-contract=off", "-Wall"]
 
-CU_SOURCES = ["bf_kernels.cu", "bf_small.cu", "bf_struct.cu", "bf_recompress.cu", "bf_tc.cu", "bf_band3.cu", "bf_plan.cu"]
+CU_SOURCES = ["bf_kernels.cu", "bf_small.cu", "bf_struct.cu", "bf_recompress.cu", "bf_tc.cu", "bf_band3.cu", "bf_nufft.cu", "bf_plan.cu"]
 CXX_SOURCES = ["bf_build.cpp"]
 HEADERS = ["bf_internal.h", "bf_plan_internal.h", "bf_shard.h", "tc_sm100.cuh"]
 
@@ -63,7 +63,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
             f.result()
     objs = [o for _, _, o in jobs]
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp"]
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp",
+           "-L/usr/local/cuda/lib64", "-lcufft", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     _run(cmd, None, verbose)
     os.replace(tmp, LIB)
     with open(stamp, "w") as f:

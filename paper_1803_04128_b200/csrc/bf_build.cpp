@@ -15,6 +15,7 @@
 
 #include "../../include/bf.h"
 #include "../../include/bf_build.h"
+#include "../../include/bf_nufft.h"
 #include "bf_plan_internal.h"
 
 namespace {
@@ -787,6 +788,43 @@ bf_status_t bf_plan_build_fio_emulated(const bf_fio_t* k, int device, int32_t wo
                                        int64_t staging_bytes, bf_plan_t* out)
 {
     return build_plan(k, device, world, 0, BF_SHARD_EMULATED, nullptr, max_nrhs_chunk, staging_bytes, out);
+}
+
+// NUFFT path (include/bf_nufft.h): the configs' phases are exactly rank 1 on xi < 0 and xi >= 0,
+// Phi(x, xi) = (x -+ c(x)) xi there (eqn:phlr P:1125-1131 for the wave-equation FIO; P:571 submatrices), so the
+// targets are t_-(x) = x - c(x) and t_+(x) = x + c(x), in FP64; the amplitude split is bf_build_amp's.
+bf_status_t bf_nufft_build_fio(const bf_fio_t* k, int device, int64_t max_nrhs_chunk, double eps, bf_nufft_t* out)
+{
+    if (!k || !out) return bfp_fail(BF_ERR_INVALID_ARG, "bf_nufft_build_fio: null");
+    if (k->abi_version != BF_ABI_VERSION || k->kernel < 0 || k->kernel > 3 || bf_build_n_amp(k->amp) < 1 ||
+        k->log2n < 4 || k->log2n > 26)
+        return bfp_fail(BF_ERR_SHAPE, "bf_nufft_build_fio: kernel, amplitude or log2n");
+    const int64_t N = int64_t(1) << k->log2n;
+    const int na = bf_build_n_amp(k->amp);
+    std::vector<double> t(size_t(2 * N));
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < N; i++) {
+        const double x = std::ldexp(double(i), -k->log2n), c = cfun(k->kernel, x);
+        t[size_t(i)] = x - c;
+        t[size_t(N + i)] = x + c;
+    }
+    std::vector<bf_c64> a(size_t(na) * N), b(size_t(na) * N);
+    bf_fio_t kk = *k;
+    if (kk.log2leaf < 1 || 2 * kk.log2leaf > kk.log2n) kk.log2leaf = 1;   // bf_build_amp checks a BF shape
+    if (kk.rank < 2 || kk.rank > (1 << kk.log2leaf)) kk.rank = 2;
+    if (kk.log2n % 2) return bfp_fail(BF_ERR_SHAPE, "bf_nufft_build_fio: log2n must be even");
+    bf_status_t st = bf_build_amp(&kk, a.data(), b.data());
+    if (st != BF_OK) return st;
+    bf_nufft_desc_t d{};
+    d.abi_version = BF_ABI_VERSION;
+    d.log2n = k->log2n;
+    d.n_amp = na;
+    d.n_sub = 2;
+    d.targets = t.data();
+    d.amp_a = a.data();
+    d.amp_b = b.data();
+    d.eps = eps;
+    return bf_nufft_create(&d, device, max_nrhs_chunk, out);
 }
 
 }  // extern "C"

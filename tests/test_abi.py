@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared_functions():
     names = set()
-    for h in ("bf.h", "bf_build.h"):
+    for h in ("bf.h", "bf_build.h", "bf_nufft.h"):
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\*?\s*(bf_[a-z0-9_]+)\s*\(", src, re.M):
@@ -35,7 +35,7 @@ def test_header_declarations_are_exported():
 
 
 def test_no_torch_in_the_abi():
-    for h in ("bf.h", "bf_build.h"):
+    for h in ("bf.h", "bf_build.h", "bf_nufft.h"):
         src = open(os.path.join(ROOT, "include", h)).read()
         assert "torch" not in src.lower().replace("no torch", "") and "at::" not in src
     out = subprocess.run(["ldd", bf.LIB_PATH], capture_output=True, text=True).stdout
@@ -78,3 +78,19 @@ def test_no_device_fails_loudly():
     assert st in (1, 5) and not h.value      # BF_ERR_INVALID_ARG (no device) or BF_ERR_CUDA
     with pytest.raises(bf.BFError):
         bf.Plan.build_fio(bf.fio(0, 1, 12, 4, 10))
+
+
+def test_nufft_validation_without_gpu():
+    L = bf.lib()
+    h = ctypes.c_void_p()
+    t = (ctypes.c_double * 32)()
+    a = (ctypes.c_float * 64)()
+    d = bf.bf_nufft_desc_t(bf.BF_ABI_VERSION, 4, 1, 3, ctypes.addressof(t), ctypes.addressof(a), ctypes.addressof(a), 1e-6)
+    assert L.bf_nufft_create(ctypes.byref(d), 0, 1, ctypes.byref(h)) == 2          # n_sub 3: BF_ERR_SHAPE
+    d.n_sub, d.eps = 2, 0.5
+    assert L.bf_nufft_create(ctypes.byref(d), 0, 1, ctypes.byref(h)) == 2          # eps out of range
+    assert "eps" in L.bf_last_error().decode()
+    d.targets = None
+    assert L.bf_nufft_create(ctypes.byref(d), 0, 1, ctypes.byref(h)) == 1          # null array
+    assert L.bf_nufft_apply(None, None, 16, None, 16, 1, None) == 1
+    assert L.bf_nufft_destroy(None) == 0
