@@ -73,6 +73,27 @@ bf_status_t bf_nufft_get_info(bf_nufft_t plan, bf_nufft_info_t *info);
 /* Waits for the plan's work and frees it. */
 bf_status_t bf_nufft_destroy(bf_nufft_t plan);
 
+/* Algorithm 6 with r = 1 on the host (plan construction, untimed, FP64): does the NUFFT apply to
+ * K = (U2 V2^T) o e^{2 pi i U1 V1^T} (m rows x_i, n columns xi_j)?  Steps: the leading singular pair of the phase
+ * U1 V1^T by a randomized range finder (r1 + 4 Gaussian test vectors, seeded), P q^T; rq = q sampled columns of
+ * (U2 V2^T) o e^{2 pi i (U1 V1^T - P q^T)}; Householder QR with column pivoting; n_rank = the number of |R_kk| >
+ * |R_11| eps; y = 1 iff n_rank <= rank_budget (reading R24).  If y = 1 and `targets` is not NULL, the
+ * column factor must be a multiple of xi (q_j = alpha xi_j: uniform frequencies, the type-2 NUFFT of
+ * bf_nufft_create) and targets[i] = alpha P_i, so that P q^T = t(x_i) xi_j -- else BF_ERR_NOT_SUPPORTED.
+ * Layouts: u1 [r1][m], v1 [r1][n] real; u2 [r2][m], v2 [r2][n] complex as interleaved doubles; xi [n]. */
+typedef struct {
+    int64_t m, n;            /* rows, columns (>= 2) */
+    int32_t r1, r2;          /* phase / amplitude factor ranks, 1..16 */
+    const double *u1, *v1;   /* phase factors */
+    const double *u2, *v2;   /* amplitude factors (complex, {re, im} pairs) */
+    const double *xi;        /* [n] column frequencies (for the targets; may be NULL when targets is NULL) */
+    int32_t rank_budget;     /* r_eps */
+    int32_t q;               /* columns sampled (r q with r = 1) */
+    double eps;              /* rank threshold relative to |R_11| */
+    uint64_t seed;
+} bf_nufft_decide_t;
+bf_status_t bf_nufft_decide(const bf_nufft_decide_t *d, int32_t *y, int32_t *n_rank, double *targets);
+
 /* The closed-form kernels of bf_build.h as an NUFFT plan: n_sub = 2 (xi < 0, xi >= 0) with
  * t_-(x) = x - c(x), t_+(x) = x + c(x) (the DFT kernel: t = x on both), and the amplitude split of bf_build_amp
  * (cfg3's jump folded into it, DESIGN R8).  k->log2leaf and k->rank are ignored. */

@@ -42,7 +42,7 @@ EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finaliz
            "bf_plan_create_sharded", "bf_shard_pairs", "bf_plan_build_fio_sharded", "bf_plan_build_fio_emulated", "bf_plan_create_adjoint",
            "bf_plan_create_structured", "bf_plan_build_fio_structured", "bf_build_structured",
            "bf_build_structured_lag", "bf_plan_recompress", "bf_nufft_create", "bf_nufft_apply",
-           "bf_nufft_get_info", "bf_nufft_destroy", "bf_nufft_build_fio")
+           "bf_nufft_get_info", "bf_nufft_destroy", "bf_nufft_build_fio", "bf_nufft_decide")
 
 
 class BFError(RuntimeError):
@@ -81,6 +81,32 @@ class bf_nufft_desc_t(ctypes.Structure):
     _fields_ = [("abi_version", ctypes.c_int32), ("log2n", ctypes.c_int32), ("n_amp", ctypes.c_int32),
                 ("n_sub", ctypes.c_int32), ("targets", ctypes.c_void_p), ("amp_a", ctypes.c_void_p),
                 ("amp_b", ctypes.c_void_p), ("eps", ctypes.c_double)]
+
+
+class bf_nufft_decide_t(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("n", ctypes.c_int64), ("r1", ctypes.c_int32), ("r2", ctypes.c_int32),
+                ("u1", ctypes.c_void_p), ("v1", ctypes.c_void_p), ("u2", ctypes.c_void_p), ("v2", ctypes.c_void_p),
+                ("xi", ctypes.c_void_p), ("rank_budget", ctypes.c_int32), ("q", ctypes.c_int32),
+                ("eps", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
+def nufft_decide(u1, v1, u2, v2, xi=None, rank_budget: int = 4, q: int = 8, eps: float = 1e-9, seed: int = 0,
+                 want_targets: bool = True):
+    """Algorithm 6 (bf_nufft_decide) on host factors: u1 [r1][m], v1 [r1][n] real; u2 [r2][m], v2 [r2][n] complex.
+    Returns (y, n_rank, targets or None)."""
+    u1 = np.ascontiguousarray(u1, np.float64)
+    v1 = np.ascontiguousarray(v1, np.float64)
+    u2 = np.ascontiguousarray(u2, np.complex128)
+    v2 = np.ascontiguousarray(v2, np.complex128)
+    m, n = u1.shape[1], v1.shape[1]
+    xa = None if xi is None else np.ascontiguousarray(xi, np.float64)
+    d = bf_nufft_decide_t(m, n, u1.shape[0], u2.shape[0], u1.ctypes.data, v1.ctypes.data, u2.ctypes.data,
+                          v2.ctypes.data, None if xa is None else xa.ctypes.data, rank_budget, q, eps, seed)
+    y, nr = ctypes.c_int32(), ctypes.c_int32()
+    t = np.zeros(m, np.float64) if (want_targets and xa is not None) else None
+    _check(lib().bf_nufft_decide(ctypes.byref(d), ctypes.byref(y), ctypes.byref(nr),
+                                 None if t is None else t.ctypes.data))
+    return int(y.value), int(nr.value), (t if y.value else None)
 
 
 class bf_nufft_info_t(ctypes.Structure):
@@ -150,6 +176,7 @@ def lib():
             "bf_nufft_get_info": ([vp, P(bf_nufft_info_t)], i32),
             "bf_nufft_destroy": ([vp], i32),
             "bf_nufft_build_fio": ([P(bf_fio_t), ctypes.c_int, i64, ctypes.c_double, P(vp)], i32),
+            "bf_nufft_decide": ([P(bf_nufft_decide_t), P(i32), P(i32), vp], i32),
         }
         for name, (args, res) in sigs.items():
             f = getattr(L, name)

@@ -21,7 +21,7 @@ NVCC_FLAGS += [f"-D{m}" for m in os.environ.get("BF_NVCC_DEFINES", "").split()] 
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-march=x86-64-v3", "-ffp-contract=off", "-Wall"]
 
 CU_SOURCES = ["bf_kernels.cu", "bf_small.cu", "bf_struct.cu", "bf_recompress.cu", "bf_tc.cu", "bf_band3.cu", "bf_nufft.cu", "bf_plan.cu"]
-CXX_SOURCES = ["bf_build.cpp"]
+CXX_SOURCES = ["bf_build.cpp", "bf_decide.cpp"]
 HEADERS = ["bf_internal.h", "bf_plan_internal.h", "bf_shard.h", "tc_sm100.cuh"]
 
 
