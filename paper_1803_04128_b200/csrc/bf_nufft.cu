@@ -195,14 +195,15 @@ __global__ void __launch_bounds__(256) interp_win_kernel(const float2* __restric
         if (2 * np <= kLWMAX) {
             // every row's window with asynchronous 16-byte copies, all in flight at once (one load round trip
             // per block instead of one per row and pass)
-            for (int x = tid; x < nrow * np; x += 256) {
-                const int r = x / np, t = x - r * np;
+            for (int t = tid; t < np; t += 256) {   // a thread copies pair t of every row (no index division)
                 int l = mn2 + 2 * t;
                 l = l < 0 ? l + int(nf) : (l >= int(nf) ? l - int(nf) : l);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                 uint32_t(__cvta_generic_to_shared(win + r * kLWMAX + 2 * t))),
-                             "l"(gs + int64_t(r) * nf + l)
-                             : "memory");
+                const uint32_t dst = uint32_t(__cvta_generic_to_shared(win + 2 * t));
+                const float2* src = gs + l;
+                for (int r = 0; r < nrow; r++)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + uint32_t(r * kLWMAX * 8)),
+                                 "l"(src + int64_t(r) * nf)
+                                 : "memory");
             }
             asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
             __syncthreads();

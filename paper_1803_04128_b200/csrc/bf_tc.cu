@@ -199,12 +199,20 @@ struct S0TC {
     static constexpr int K = 2 * N0;
     static constexpr int KS = K / S0X_KC;                 // 32-wide K tiles per chunk (2 or 4)
     static constexpr int NCH = N0 * 2 * R / S0X_NC;       // 128-row N chunks per job
+#ifdef BF_S0_NSTAGE
+    static constexpr int NSTAGE = BF_S0_NSTAGE;
+#else
     static constexpr int NSTAGE = KS + 1;                 // weight ring depth (32 KB tiles)
+#endif
     static constexpr uint32_t TILE = S0X_TILE_FLOATS * 4;  // 16 KB
     static constexpr uint32_t STAGE = 2 * TILE;            // hi + lo
     // staging row stride (complex): padded (bank spread) where shared memory allows, else dense
     static constexpr int FS = (N0 == 64) ? N0 : N0 + 2;
+#ifdef BF_S0_FCOLS
+    static constexpr uint32_t FBYTES = uint32_t(BF_S0_FCOLS) * FS * 8;   // experiment: n_amp >= 128 / FCOLS only
+#else
     static constexpr uint32_t FBYTES = 128u * FS * 8;      // up to 128 F columns (n_amp = 1)
+#endif
     static constexpr uint32_t OFF_F = NSTAGE * STAGE, OFF_BK = OFF_F + FBYTES;
     static constexpr size_t SMEM = size_t(OFF_BK) + 4 * N0 * 8;
     static constexpr int A_COLS = K;                       // hi at +0, lo at +K
