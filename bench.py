@@ -187,7 +187,14 @@ def cpu_oracle_sample(w, g0=None, adjoint=False):
                      f"metric scaled per N*RHS"}
     if g0 is not None:
         rows = W.sample_rows(w.n, w.seed)
+        t1 = time.perf_counter()
         gd = direct(w.kernel, w.amp, w.log2n, F, rows)[:, 0]
+        dt_direct = time.perf_counter() - t1
+        # the other oracle leg SURVEY 8(d) names: the direct O(N^2) sum, timed on its 256-row sample (one row of one
+        # column = one N*RHS unit)
+        out["legs"] = {"bf_otf_incl_block_generation": {"value": out["value"], "seconds": dt},
+                       "direct_sum_row_sample": {"value": len(rows) / dt_direct, "seconds": dt_direct,
+                                                 "rows": len(rows)}}
         out["accuracy"] = {"column": 0, "rows": len(rows), "eps": w.eps,
                            "eps_b_oracle_bf_vs_direct": float(oracle.rel_l2(gb[rows, 0], gd)),
                            "gpu_vs_direct": float(oracle.rel_l2(g0[rows].astype(np.complex128), gd)),
