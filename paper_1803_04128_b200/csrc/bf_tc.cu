@@ -536,8 +536,9 @@ struct SLTC {
     static constexpr uint32_t GS_BYTES = uint32_t(128 / NA) * GS_STRIDE * 8;
     static constexpr uint32_t AS_BYTES = 2 * uint32_t(NA) * N0 * 8;   // a_k(x) of two jobs (double-buffered)
     // separate rings: the coefficient rows come from DRAM (deep ring), the Ux tiles mostly from L2 (2 deep)
+    static constexpr int nr_fit(int nbr) { return int((232448 - 1024 - GS_BYTES - AS_BYTES - nbr * 2 * BT) / RAW); }
 #ifdef BF_SL_NBR
-    static constexpr int NB_R = BF_SL_NBR;
+    static constexpr int NB_R = nr_fit(BF_SL_NBR) >= 3 ? BF_SL_NBR : 3;   // experiment where it fits
 #else
     static constexpr int NB_R = 3;                                   // Ux ring depth
 #endif
