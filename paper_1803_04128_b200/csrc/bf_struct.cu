@@ -326,67 +326,93 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
+// The leaf is streamed in chunks of BC b's through two shared-memory stages (cp.async, double-buffered): the copies of
+// chunk c + 1 overlap the MACs of chunk c, and the smaller footprint lets more CTAs share an SM (the whole-leaf version
+// waited for all its copies before the first MAC: 0.37 of the FP32 peak at cfg5).
 template <int R, int VPT>
 __global__ void __launch_bounds__(256) sl_st_kernel(const float2* __restrict__ in, const float* __restrict__ Lsl,
                                                     const float2* __restrict__ Om, const float2* __restrict__ ampa,
                                                     float2* __restrict__ G, int64_t ldg, int LN, int l0, int n_amp,
-                                                    int nv, int VG)
+                                                    int nv, int VG, int BC)
 {
     extern __shared__ __align__(16) unsigned char st_smem[];
     const int64_t N = int64_t(1) << LN;
     const int n0 = 1 << l0, VC = VG * VPT;
-    float2* Z = reinterpret_cast<float2*>(st_smem);   // [b][t][VC]
-    float2* Os = Z + n0 * R * VC;                      // [b][j]
+    const int zst = BC * R * VC, ost = BC * n0;               // complex per stage
+    float2* Zs = reinterpret_cast<float2*>(st_smem);          // [2][BC][t][VC]
+    float2* Oss = Zs + 2 * zst;                               // [2][BC][j]
     const int64_t a = blockIdx.x;
     const int v0 = blockIdx.y * VC;
     const float2* zsrc = in + a * n0 * R * int64_t(nv) + v0;
-    if (VPT >= 2) {   // 16-byte pieces: nv and v0 even
-        const int pr = VC / 2;   // pieces per (b, t) row
-        for (int i = threadIdx.x; i < n0 * R * pr; i += blockDim.x) {
-            const int row = i / pr, q = i % pr;
-            cp_async16(Z + row * VC + 2 * q, zsrc + int64_t(row) * nv + 2 * q);
-        }
-    } else {
-        for (int i = threadIdx.x; i < n0 * R * VC; i += blockDim.x) Z[i] = __ldg(zsrc + int64_t(i / VC) * nv + i % VC);
-    }
     const float2* osrc = Om + a * n0 * int64_t(n0);
-    for (int i = threadIdx.x; i < n0 * n0 / 2; i += blockDim.x) cp_async16(Os + 2 * i, osrc + 2 * i);
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
+    const int nch = n0 / BC;
+    auto stage = [&](int c) {   // chunk c -> stage c & 1
+        float2* Z = Zs + (c & 1) * zst;
+        float2* O = Oss + (c & 1) * ost;
+        const float2* zc = zsrc + int64_t(c) * BC * R * nv;
+        if (VPT >= 2) {   // 16-byte pieces: nv and v0 even
+            const int pr = VC / 2;
+            for (int i = threadIdx.x; i < BC * R * pr; i += blockDim.x) {
+                const int row = i / pr, q = i % pr;
+                cp_async16(Z + row * VC + 2 * q, zc + int64_t(row) * nv + 2 * q);
+            }
+        } else {
+            for (int i = threadIdx.x; i < BC * R * VC; i += blockDim.x) Z[i] = __ldg(zc + int64_t(i / VC) * nv + i % VC);
+        }
+        const float2* oc = osrc + int64_t(c) * BC * n0;
+        for (int i = threadIdx.x; i < BC * n0 / 2; i += blockDim.x) cp_async16(O + 2 * i, oc + 2 * i);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     const int j = threadIdx.x % n0, vg = threadIdx.x / n0;
-    if (vg >= VG) return;
+    const bool active = vg < VG;
     const int64_t x = a * n0 + j;
     float Lr[R];
 #pragma unroll
-    for (int t = 0; t < R; t++) Lr[t] = __ldg(Lsl + t * n0 + j);
+    for (int t = 0; t < R; t++) Lr[t] = active ? __ldg(Lsl + t * n0 + j) : 0.f;
     float2 acc[VPT];
 #pragma unroll
     for (int q = 0; q < VPT; q++) acc[q] = make_float2(0.f, 0.f);
-    for (int b = 0; b < n0; b++) {
-        const float2* z = Z + (b * R) * VC + vg * VPT;
-        float2 sacc[VPT];
-#pragma unroll
-        for (int q = 0; q < VPT; q++) sacc[q] = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int t = 0; t < R; t++) {
-            float2 zt[VPT];
-            if constexpr (VPT == 1) {
-                zt[0] = z[t * VC];
-            } else {
-#pragma unroll
-                for (int q = 0; q < VPT / 2; q++) {
-                    const float4 f = reinterpret_cast<const float4*>(z + t * VC)[q];
-                    zt[2 * q] = make_float2(f.x, f.y);
-                    zt[2 * q + 1] = make_float2(f.z, f.w);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < VPT; q++) rmac(sacc[q], Lr[t], zt[q]);
+    stage(0);
+    for (int c = 0; c < nch; c++) {
+        if (c + 1 < nch) {
+            stage(c + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        const float2 f = Os[b * n0 + j];
+        __syncthreads();
+        if (active) {
+            const float2* Zc = Zs + (c & 1) * zst;
+            const float2* Oc = Oss + (c & 1) * ost;
+            for (int bb = 0; bb < BC; bb++) {
+                const float2* z = Zc + (bb * R) * VC + vg * VPT;
+                float2 sacc[VPT];
 #pragma unroll
-        for (int q = 0; q < VPT; q++) cmac(acc[q], f, sacc[q]);
+                for (int q = 0; q < VPT; q++) sacc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int t = 0; t < R; t++) {
+                    float2 zt[VPT];
+                    if constexpr (VPT == 1) {
+                        zt[0] = z[t * VC];
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < VPT / 2; q++) {
+                            const float4 f = reinterpret_cast<const float4*>(z + t * VC)[q];
+                            zt[2 * q] = make_float2(f.x, f.y);
+                            zt[2 * q + 1] = make_float2(f.z, f.w);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < VPT; q++) rmac(sacc[q], Lr[t], zt[q]);
+                }
+                const float2 f = Oc[bb * n0 + j];
+#pragma unroll
+                for (int q = 0; q < VPT; q++) cmac(acc[q], f, sacc[q]);
+            }
+        }
+        __syncthreads();   // stage c & 1 is refilled by the copies of chunk c + 2, issued next iteration
     }
+    if (!active) return;
     // a_k(x) and the sum over the n_amp vectors of each column (consecutive within the thread)
     const int vb = v0 + vg * VPT;
     float2 g = make_float2(0.f, 0.f);
@@ -510,13 +536,18 @@ cudaError_t launch_sl_st(const Dims& d, const float2* in, const float* Lsl, cons
            size_t(n0) * d.R * 2 * vg * vpt * 8 <= 96 * 1024)
         vg *= 2;
     const int vc = vg * vpt;
-    const size_t shm = size_t(n0) * d.R * vc * 8 + size_t(n0) * n0 * 8;
+#ifdef BF_SL_ST_BC
+    const int bc = n0 >= BF_SL_ST_BC ? BF_SL_ST_BC : n0;
+#else
+    const int bc = n0 >= 16 ? 16 : n0;   // b's per pipeline chunk
+#endif
+    const size_t shm = 2 * (size_t(bc) * d.R * vc + size_t(bc) * n0) * 8;
     const dim3 grid(unsigned(d.N >> d.l0), unsigned(nv / vc));
     const int threads = n0 * vg < 32 ? 32 : n0 * vg;
 #define SL_GO(R, V)                                                                                                \
     {                                                                                                              \
         cudaFuncSetAttribute(sl_st_kernel<R, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));          \
-        sl_st_kernel<R, V><<<grid, threads, shm, s>>>(in, Lsl, Om, ampa, G, ldg, d.LN, d.l0, d.n_amp, nv, vg);    \
+        sl_st_kernel<R, V><<<grid, threads, shm, s>>>(in, Lsl, Om, ampa, G, ldg, d.LN, d.l0, d.n_amp, nv, vg, bc); \
     }
 #define SL_CALL(R)                      \
     switch (vpt) {                      \
