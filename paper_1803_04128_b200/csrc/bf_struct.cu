@@ -583,11 +583,19 @@ cudaError_t launch_band_st(const Dims& d, int l, int k1, int k2, const LagP& L, 
     const int threads = jobs_cta * 4 * nv;
     const size_t shm = size_t(jobs_cta) * per_job;
     const int64_t njobs = d.N / 4;
-    const unsigned grid = unsigned(std::min<int64_t>((njobs + jobs_cta - 1) / jobs_cta, int64_t(148) * 4));
     const int kk = k1 * 4 + k2;
+    // persistent grid = the CTAs that are resident at once (occupancy), not a fixed 4 per SM: a CTA that does not fit
+    // would start after a resident one finishes and, with an equal share of the jobs, double the kernel's time
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
 #define B_GO(R, A, B)                                                                                              \
     {                                                                                                              \
         cudaFuncSetAttribute(band_st_kernel<R, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));     \
+        int occ = 1;                                                                                               \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, band_st_kernel<R, A, B>, threads, shm);                \
+        const unsigned grid = unsigned(std::min<int64_t>((njobs + jobs_cta - 1) / jobs_cta,                        \
+                                                         int64_t(nsm) * std::max(1, occ)));                        \
         band_st_kernel<R, A, B><<<grid, threads, shm, s>>>(L, w1, w2, in, out, d.LN, l, nv, njobs, jobs_cta);      \
     }
 #define B_CALL(R)                                      \
