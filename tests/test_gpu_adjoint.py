@@ -48,6 +48,7 @@ CASES = [  # (config, overrides, columns compared)
     ("cfg4", dict(log2n=14, nrhs=128), [0, 77, 127]),         # nv = 256: tensor cores, composed bands
     ("cfg4", dict(log2n=12, nrhs=3), None),                   # odd nv: FP32 kernels
     ("cfg2", dict(log2n=10, log2leaf=5, nrhs=4), None),       # h == l0: no transfer level before the switch
+    ("cfg4", dict(log2n=16, log2leaf=5, rank=8, nrhs=64), [0, 63]),   # r = 8, 128 vectors: three-level bands 3 + 3
 ]
 
 

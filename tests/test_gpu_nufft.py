@@ -135,3 +135,22 @@ def test_nufft_agrees_with_butterfly_and_invariants():
     with pytest.raises(bf.BFError):
         nu.apply(Ft, Ft, nrhs)
     nu.destroy()
+
+
+def test_nufft_minimum_size_and_alignment():
+    """N = 16 (the smallest plan: two submatrices of 8 frequencies) against the direct sum; an odd ldf or a
+    misaligned F is refused (the placement reads F in 16-byte pieces)."""
+    LN = 4
+    N = 1 << LN
+    F = W.rhs(N, 3, 6)
+    plan = bf.NufftPlan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, 1, 2), max_nrhs_chunk=3)
+    G = _apply(plan, F)
+    R = oracle.direct_rows(W.K_FIO, W.A_CFG1, LN, F.astype(np.complex128), np.arange(N))
+    assert np.all(oracle.rel_l2(G, R, axis=0) <= PARITY)
+    Fb = torch.zeros(3 * (N + 1) + 1, dtype=torch.complex64, device="cuda")
+    Gb = torch.zeros(3 * N, dtype=torch.complex64, device="cuda")
+    with pytest.raises(bf.BFError):
+        plan.apply(Fb, Gb, 3, ldf=N + 1)                 # odd ldf
+    with pytest.raises(bf.BFError):
+        plan.apply(Fb[1:], Gb, 3)                        # F at 8 mod 16 bytes
+    plan.destroy()
