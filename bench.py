@@ -55,6 +55,18 @@ def _peaks():
     return hbm, src, bf16 * 1.1 / 2.25, tsrc
 
 
+def _sustained():
+    """Measured sustained device rates (tools/sustained_peaks.py: >= 4 s FFMA and kind::tf32 MMA loads on every SM,
+    under the power cap) from the newest committed capture, or None."""
+    for rnd in ("r2",):
+        try:
+            with open(os.path.join(ROOT, "profiles", f"{rnd}_sustained_peaks.json")) as f:
+                return json.load(f)
+        except Exception:
+            continue
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -532,6 +544,13 @@ def main():
         roof = {"bound": "alu", "achieved": flops / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "peak_source": "FP32 FFMA from unit counts: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 5)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    sus = _sustained()
+    if sus and roof["bound"] in ("tensor", "alu"):
+        # the same achieved rate against the rate a seconds-long load of that unit sustains on this pool's B200s
+        key = "tf32_tflops_sustained" if roof["bound"] == "tensor" else "ffma_tflops_sustained"
+        roof["peak_sustained_measured"] = sus[key]
+        roof["frac_of_sustained_measured"] = roof["achieved"] / sus[key]
+        roof["sustained_source"] = "profiles/r2_sustained_peaks.json (tools/sustained_peaks.cu)"
     wname = (args.config + ("-adjoint" if args.adjoint else "") + ("-structured" if args.structured else "")
              + (f"-recompressed-r{args.build_rank}to{args.recompress}" if args.recompress else ""))
     roof["traffic"] = _ncu_traffic(wname if not (args.log2n or args.adjoint or args.nrhs or args.chunk) else None, dom)
