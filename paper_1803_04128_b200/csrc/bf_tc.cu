@@ -678,9 +678,13 @@ __global__ void __launch_bounds__(448, 1)
                 const uint32_t aa = tmem + uint32_t(sa * C::A_COLS + (pass == 1 ? C::KC : 0));
                 const uint64_t bb = tc::desc_add(dB0, (2 * e + (pass == 2)) * C::BT);
 #pragma unroll
-                for (int ks = 0; ks < C::KC / 8; ks++)
+                for (int ks = 0; ks < C::KC / 8; ks++) {
+#ifdef BF_SL_EXP_NO_MMA   // diagnostics: the kernel without its MMAs (data movement, split, drain only)
+                    if (q < 0)
+#endif
                     tc::mma_tf32_ts_warp(d, aa + ks * 8, tc::desc_add(bb, ks * 2 * LBO_B), idesc,
                                          (first && q == 0 && ks == 0) ? 0u : 1u);
+                }
             }
             tc::commit_warp(&a_empty[sa]);
             if constexpr (CL == 2)
@@ -713,8 +717,12 @@ __global__ void __launch_bounds__(448, 1)
             tc::fence_before_sync();
             tc::mbar_arrive(&raw_empty[e]);   // the raw rows are in registers now
             const uint32_t ta = tmem + lb + uint32_t(sa * C::A_COLS);
+#ifndef BF_SL_EXP_NO_TMEM_ST   // diagnostics: the split without its TMEM stores
             tc::tmem_st_cols<C::KC>(ta, hi);
             tc::tmem_st_cols<C::KC>(ta + C::KC, lo);
+#else
+            if (hi[0] == 1234.5f && lo[1] == 0.5f) tc::tmem_st_cols<4>(ta, hi);
+#endif
             tc::tmem_wait_st();
             tc::fence_before_sync();
             tc::mbar_arrive(&a_full[sa]);
@@ -751,8 +759,13 @@ __global__ void __launch_bounds__(448, 1)
 #pragma unroll
                 for (int c0 = 0; c0 < HC; c0 += 32) {
                     float x[32];
+#ifndef BF_SL_EXP_NO_DRAIN   // diagnostics: segments released without reading the accumulators
                     tc::tmem_ld_cols<(HC < 32 ? HC : 32)>(taddr + c0, x);
                     tc::tmem_wait_ld();
+#else
+#pragma unroll
+                    for (int i = 0; i < 32; i++) x[i] = 0.f;
+#endif
 #pragma unroll
                     for (int i = 0; i < (HC < 32 ? HC : 32); i++) sum[c0 + i] += x[i];
                 }
