@@ -922,7 +922,7 @@ bf_status_t build_leaf_images(bf_plan_s* p, Shard& s)
     };
     cudaError_t e = cudaSuccess;
     if (!s.v0x && alloc(&s.v0x, lx * sizeof(float))) e = bfk::expand_leaf_weights(dl, s.v0, s.u, s.v0x, nullptr, 0);
-    if (e == cudaSuccess && !s.ux && alloc(&s.ux, lx * sizeof(float)))
+    if (e == cudaSuccess && !s.ux && alloc(&s.ux, size_t(bfk::ux_floats(dl)) * sizeof(float)))
         e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
     return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf weight images");
 }
@@ -1556,7 +1556,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     for (const Shard& s : p->sh) {
         const int64_t lx = bfk::leafx_floats(p->local());
         if (s.v0x) info->tc_weight_bytes += lx * int64_t(sizeof(float));
-        if (s.ux) info->tc_weight_bytes += lx * int64_t(sizeof(float));
+        if (s.ux) info->tc_weight_bytes += bfk::ux_floats(p->local()) * int64_t(sizeof(float));
     }
     {
         const bfk::Dims dl = p->local();

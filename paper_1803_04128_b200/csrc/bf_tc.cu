@@ -123,11 +123,23 @@ __global__ void expand_s0_kernel(const float2* __restrict__ V0, float* __restric
 // [leaf][K chunk of KP pairs][hi | lo][canonical K-major 2 n0 x KP 2r tile].
 static int sl_kp(int R) { return R >= 12 ? 1 : 2; }
 
-__global__ void expand_sl_kernel(const float2* __restrict__ U, float* __restrict__ X, int LN, int l0, int R, int KP)
+// The 2x SL image (rows n = c' n0 + j holding Ur / Ui, K = (b, t); SLTC I2) where the chunk's K (KP r) is a whole
+// number of MMA K steps: r = 8 (KP 2) and r = 16 (KP 1).  BF_SL_IMAGE4 builds keep the 4x image everywhere.
+constexpr bool sl_i2(int R)
+{
+#ifdef BF_SL_IMAGE4
+    return false && R;
+#else
+    return R == 8 || R == 16;
+#endif
+}
+
+__global__ void expand_sl_kernel(const float2* __restrict__ U, float* __restrict__ X, int LN, int l0, int R, int KP,
+                                 int i2)
 {
     const int n0 = 1 << l0;
     const int64_t nleaf = (int64_t(1) << LN) >> l0;
-    const int rows = 2 * n0, K = n0 * 2 * R, KC = KP * 2 * R;
+    const int rows = 2 * n0, K = i2 ? n0 * R : n0 * 2 * R, KC = i2 ? KP * R : KP * 2 * R;
     const int nch = n0 / KP;
     const int64_t tile = int64_t(rows) * KC;
     const int64_t total = nleaf * rows * int64_t(K);
@@ -135,10 +147,19 @@ __global__ void expand_sl_kernel(const float2* __restrict__ U, float* __restrict
         const int64_t a = g / (int64_t(rows) * K);
         const int rem = int(g - a * rows * K);
         const int n = rem / K, k = rem - n * K;
-        const int j = n >> 1, cp = n & 1, b = k / (2 * R), t = (k / 2) % R, c = k & 1;
-        const float2 w = U[(a * n0 + b) * (n0 * R) + int64_t(t) * n0 + j];
         float hi, lo;
-        tc::split(embed(w, cp, c), hi, lo);
+        int b;
+        if (i2) {   // n = c' n0 + j, k = b r + t: Ur (c' = 0) / Ui (c' = 1), no embedding
+            const int cp = n / n0, j = n - cp * n0, t = k % R;
+            b = k / R;
+            const float2 w = U[(a * n0 + b) * (n0 * R) + int64_t(t) * n0 + j];
+            tc::split(cp ? w.y : w.x, hi, lo);
+        } else {
+            const int j = n >> 1, cp = n & 1, t = (k / 2) % R, c = k & 1;
+            b = k / (2 * R);
+            const float2 w = U[(a * n0 + b) * (n0 * R) + int64_t(t) * n0 + j];
+            tc::split(embed(w, cp, c), hi, lo);
+        }
         const int ch = b / KP, kk = k - ch * KC;
         float* tl = X + ((a * nch + ch) * 2) * tile;
         const uint32_t off = tc::kmaj_off(n, kk, rows) / 4;
@@ -163,7 +184,7 @@ cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    if (Ux) expand_sl_kernel<<<grid, 256, 0, s>>>(U, Ux, d.LN, d.l0, d.R, sl_kp(d.R));
+    if (Ux) expand_sl_kernel<<<grid, 256, 0, s>>>(U, Ux, d.LN, d.l0, d.R, sl_kp(d.R), sl_i2(d.R) ? 1 : 0);
     return cudaGetLastError();
 }
 
@@ -519,10 +540,17 @@ cudaError_t launch_s0_tc(const Dims& d, const float2* F, int64_t ldf, const floa
 //                         and write G through a dedicated shared-memory transpose buffer, while the
 //                         other roles already stream the next job.
 // =============================================================================================
-template <int R, int N0, int NA, int KP>
+// I2: the "2x" Ux image (hi/lo of the compact blocks stacked [Ur; Ui], rows n = c' n0 + j, K = (pl, t)) instead of
+// the real-embedded 4x image; the MMA schedule forms the complex product (section 5.1): per K step of 8
+//   D[:, 0:NB]      += A_R [Ur; Ui]^T          (N = NB)
+//   D[:, 0:NB/2]    += A_I (-Ui)^T             (N = NB/2, negate-B bit)
+//   D[:, NB/2:NB]   += A_I Ur^T                (N = NB/2)
+// with A = [A_R | A_I] (re / im parts of the chunk's coefficients as separate K blocks).
+template <int R, int N0, int NA, int KP, bool I2 = false>
 struct SLTC {
     static constexpr int NB = 2 * N0;
-    static constexpr int KC = KP * 2 * R;
+    static constexpr int KC = I2 ? KP * R : KP * 2 * R;      // B tile K (real columns) per chunk
+    static constexpr int AH = I2 ? 2 * KC : KC;              // A columns of one split part (hi or lo)
     static constexpr int NCH = N0 / KP;
 #ifdef BF_SL_SEG
     static constexpr int SEG = BF_SL_SEG;                        // chunks per accumulation segment
@@ -550,7 +578,7 @@ struct SLTC {
     // A stages: as many as TMEM holds beside the two accumulators (up to 4): the split of chunk g + NAS overlaps
     // the MMAs of the chunks before it instead of waiting for chunk g's MMAs to finish (2 stages left the tensor
     // pipe idle across every split + mbarrier round trip)
-    static constexpr int A_COLS = 2 * KC;
+    static constexpr int A_COLS = 2 * AH;
 #ifdef BF_SL_NAS
     static constexpr int NAS = BF_SL_NAS;
 #else
@@ -566,12 +594,12 @@ struct SLTC {
 // CL = 2: launched as clusters of two CTAs that work on the two halves of a leaf's vector tiles at the same
 // time; each CTA bulk-copies half of every Ux stage and multicasts it to both (half the L2 -> SM traffic of
 // the 1.3 MB-per-job Ux stream), and a stage is refilled only after both CTAs' MMAs released it.
-template <int R, int N0, int NA, int KP, int CL>
+template <int R, int N0, int NA, int KP, int CL, bool I2>
 __global__ void __launch_bounds__(448, 1)
     sl_tc_kernel(const __grid_constant__ CUtensorMap tin, const float* __restrict__ Ux, const float2* __restrict__ ampa,
                  float2* __restrict__ G, int64_t ldg, int LN, int nv, int nvt)
 {
-    using C = SLTC<R, N0, NA, KP>;
+    using C = SLTC<R, N0, NA, KP, I2>;
     extern __shared__ __align__(128) uint8_t sm_sltc[];
     auto raw = [&](int e) { return sm_sltc + e * C::RAW; };
     auto opB = [&](int e, int lo) { return sm_sltc + C::OFF_B + (2 * e + lo) * C::BT; };
@@ -675,15 +703,23 @@ __global__ void __launch_bounds__(448, 1)
 #pragma unroll
             for (int q = 0; q < 3; q++) {
                 const int pass = kPassOrder[q];
-                const uint32_t aa = tmem + uint32_t(sa * C::A_COLS + (pass == 1 ? C::KC : 0));
+                const uint32_t aa = tmem + uint32_t(sa * C::A_COLS + (pass == 1 ? C::AH : 0));
                 const uint64_t bb = tc::desc_add(dB0, (2 * e + (pass == 2)) * C::BT);
 #pragma unroll
                 for (int ks = 0; ks < C::KC / 8; ks++) {
 #ifdef BF_SL_EXP_NO_MMA   // diagnostics: the kernel without its MMAs (data movement, split, drain only)
                     if (q < 0)
 #endif
-                    tc::mma_tf32_ts_warp(d, aa + ks * 8, tc::desc_add(bb, ks * 2 * LBO_B), idesc,
-                                         (first && q == 0 && ks == 0) ? 0u : 1u);
+                    {
+                        const uint64_t bk = tc::desc_add(bb, ks * 2 * LBO_B);
+                        tc::mma_tf32_ts_warp(d, aa + ks * 8, bk, idesc, (first && q == 0 && ks == 0) ? 0u : 1u);
+                        if constexpr (I2) {
+                            constexpr uint32_t idh = tc::idesc_tf32(128, C::NB / 2);
+                            constexpr uint32_t HALF = (C::NB / 2 / 8) * 128;   // bytes to the Ui rows
+                            tc::mma_tf32_ts_warp(d, aa + C::KC + ks * 8, tc::desc_add(bk, HALF), idh | (1u << 14), 1u);
+                            tc::mma_tf32_ts_warp(d + C::NB / 2, aa + C::KC + ks * 8, bk, idh, 1u);
+                        }
+                    }
                 }
             }
             tc::commit_warp(&a_empty[sa]);
@@ -707,19 +743,24 @@ __global__ void __launch_bounds__(448, 1)
             if (gch >= C::NAS) tc::mbar_wait(&a_empty[sa], uint32_t(gch / C::NAS - 1) & 1);
             tc::fence_after_sync();
             const float2* rd = reinterpret_cast<const float2*>(raw(e));   // [KP R][128]
-            float hi[C::KC], lo[C::KC];   // column (pl, t, c) = pl 2R + 2t + c
+            float hi[C::AH], lo[C::AH];   // column (pl, t, c) = pl 2R + 2t + c; I2: c KC + pl R + t
 #pragma unroll
             for (int row = 0; row < KP * R; row++) {
                 const float2 x = rd[row * 128 + v];
-                tc::split(x.x, hi[2 * row], lo[2 * row]);
-                tc::split(x.y, hi[2 * row + 1], lo[2 * row + 1]);
+                if constexpr (I2) {
+                    tc::split(x.x, hi[row], lo[row]);
+                    tc::split(x.y, hi[C::KC + row], lo[C::KC + row]);
+                } else {
+                    tc::split(x.x, hi[2 * row], lo[2 * row]);
+                    tc::split(x.y, hi[2 * row + 1], lo[2 * row + 1]);
+                }
             }
             tc::fence_before_sync();
             tc::mbar_arrive(&raw_empty[e]);   // the raw rows are in registers now
             const uint32_t ta = tmem + lb + uint32_t(sa * C::A_COLS);
 #ifndef BF_SL_EXP_NO_TMEM_ST   // diagnostics: the split without its TMEM stores
-            tc::tmem_st_cols<C::KC>(ta, hi);
-            tc::tmem_st_cols<C::KC>(ta + C::KC, lo);
+            tc::tmem_st_cols<C::AH>(ta, hi);
+            tc::tmem_st_cols<C::AH>(ta + C::AH, lo);
 #else
             if (hi[0] == 1234.5f && lo[1] == 0.5f) tc::tmem_st_cols<4>(ta, hi);
 #endif
@@ -754,8 +795,26 @@ __global__ void __launch_bounds__(448, 1)
                 const int slot = gseg & 1;
                 tc::mbar_wait(&dfull[slot], uint32_t(gseg >> 1) & 1);
                 tc::fence_after_sync();
-                const uint32_t taddr =
-                    tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * C::NB + half * HC);
+                // I2: a thread's half of the leaf (j in [half HC/2, (half + 1) HC/2)) has its re parts at columns
+                // half HC/2 .. and its im parts NB/2 further; sum[0, HC/2) = re, sum[HC/2, HC) = im
+                const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) +
+                                       uint32_t(C::D_OFF + slot * C::NB + (I2 ? half * (HC / 2) : half * HC));
+#pragma unroll
+                if constexpr (I2) {
+#pragma unroll
+                    for (int hpart = 0; hpart < 2; hpart++) {
+                        float x[HC / 2];
+#ifndef BF_SL_EXP_NO_DRAIN
+                        tc::tmem_ld_cols<HC / 2>(taddr + hpart * (C::NB / 2), x);
+                        tc::tmem_wait_ld();
+#else
+#pragma unroll
+                        for (int i = 0; i < HC / 2; i++) x[i] = 0.f;
+#endif
+#pragma unroll
+                        for (int i = 0; i < HC / 2; i++) sum[hpart * (HC / 2) + i] += x[i];
+                    }
+                } else {
 #pragma unroll
                 for (int c0 = 0; c0 < HC; c0 += 32) {
                     float x[32];
@@ -769,6 +828,7 @@ __global__ void __launch_bounds__(448, 1)
 #pragma unroll
                     for (int i = 0; i < (HC < 32 ? HC : 32); i++) sum[c0 + i] += x[i];
                 }
+                }
                 tc::fence_before_sync();
                 tc::mbar_arrive(&dempty[slot]);
             }
@@ -778,7 +838,8 @@ __global__ void __launch_bounds__(448, 1)
 #pragma unroll
             for (int jj = 0; jj < HC / 2; jj++) {
                 const int j = half * (HC / 2) + jj;
-                float2 g = cmul_tc(Asj[k * N0 + j], make_float2(sum[2 * jj], sum[2 * jj + 1]));
+                float2 g = cmul_tc(Asj[k * N0 + j], I2 ? make_float2(sum[jj], sum[HC / 2 + jj])
+                                                       : make_float2(sum[2 * jj], sum[2 * jj + 1]));
 #pragma unroll
                 for (int m = 1; m < NA; m <<= 1) {
                     g.x += __shfl_xor_sync(0xffffffffu, g.x, m);
@@ -808,14 +869,15 @@ template <int R, int N0, int NA, int KP>
 static cudaError_t sl_tc_go(const Dims& d, const float2* in, const float* Ux, const float2* ampa, float2* G, int64_t ldg,
                             int nv, cudaStream_t s, bool multicast)
 {
-    using C = SLTC<R, N0, NA, KP>;
+    constexpr bool I2 = sl_i2(R);
+    using C = SLTC<R, N0, NA, KP, I2>;
     const int nvt = (nv + 127) / 128;
     CUtensorMap tin;
     cudaError_t e = make_rows_tmap(&tin, in, d.N * R, nv, KP * R);
     if (e != cudaSuccess) return e;
     const int64_t leaves = d.N / N0;
     if (multicast && nvt % 2 == 0 && sm_count() >= 2) {
-        auto kern = sl_tc_kernel<R, N0, NA, KP, 2>;
+        auto kern = sl_tc_kernel<R, N0, NA, KP, 2, I2>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
         if (e != cudaSuccess) return e;
         const int64_t pairs = leaves * (nvt / 2);
@@ -834,7 +896,7 @@ static cudaError_t sl_tc_go(const Dims& d, const float2* in, const float* Ux, co
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, kern, tin, Ux, ampa, G, ldg, d.LN, nv, nvt);
     }
-    auto kern = sl_tc_kernel<R, N0, NA, KP, 1>;
+    auto kern = sl_tc_kernel<R, N0, NA, KP, 1, I2>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
     const int64_t jobs = leaves * nvt;
@@ -1618,5 +1680,7 @@ cudaError_t rows_tmap(CUtensorMap* m, const float2* base, int64_t rows, int nv, 
     return make_rows_tmap(m, base, rows, nv, box_rows);
 }
 int tc_sm_count() { return sm_count(); }
+
+int64_t ux_floats(const Dims& d) { return sl_i2(d.R) ? leafx_floats(d) / 2 : leafx_floats(d); }
 
 }  // namespace bfk
