@@ -536,11 +536,7 @@ cudaError_t launch_sl_st(const Dims& d, const float2* in, const float* Lsl, cons
            size_t(n0) * d.R * 2 * vg * vpt * 8 <= 96 * 1024)
         vg *= 2;
     const int vc = vg * vpt;
-#ifdef BF_SL_ST_BC
-    const int bc = n0 >= BF_SL_ST_BC ? BF_SL_ST_BC : n0;
-#else
     const int bc = n0 >= 8 ? 8 : n0;     // b's per pipeline chunk (8 / 16 / 32 measured: cfg5 5.96 / 5.95 / 6.44 ms, cfg2 0.112 / 0.132 / 0.189 ms)
-#endif
     const size_t shm = 2 * (size_t(bc) * d.R * vc + size_t(bc) * n0) * 8;
     const dim3 grid(unsigned(d.N >> d.l0), unsigned(nv / vc));
     const int threads = n0 * vg < 32 ? 32 : n0 * vg;

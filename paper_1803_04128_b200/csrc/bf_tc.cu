@@ -220,20 +220,12 @@ struct S0TC {
     static constexpr int K = 2 * N0;
     static constexpr int KS = K / S0X_KC;                 // 32-wide K tiles per chunk (2 or 4)
     static constexpr int NCH = N0 * 2 * R / S0X_NC;       // 128-row N chunks per job
-#ifdef BF_S0_NSTAGE
-    static constexpr int NSTAGE = BF_S0_NSTAGE;
-#else
-    static constexpr int NSTAGE = KS + 1;                 // weight ring depth (32 KB tiles)
-#endif
+    static constexpr int NSTAGE = KS + 1;                 // weight ring depth (32 KB tiles; 6 measured: no change)
     static constexpr uint32_t TILE = S0X_TILE_FLOATS * 4;  // 16 KB
     static constexpr uint32_t STAGE = 2 * TILE;            // hi + lo
     // staging row stride (complex): padded (bank spread) where shared memory allows, else dense
     static constexpr int FS = (N0 == 64) ? N0 : N0 + 2;
-#ifdef BF_S0_FCOLS
-    static constexpr uint32_t FBYTES = uint32_t(BF_S0_FCOLS) * FS * 8;   // experiment: n_amp >= 128 / FCOLS only
-#else
     static constexpr uint32_t FBYTES = 128u * FS * 8;      // up to 128 F columns (n_amp = 1)
-#endif
     static constexpr uint32_t OFF_F = NSTAGE * STAGE, OFF_BK = OFF_F + FBYTES;
     static constexpr size_t SMEM = size_t(OFF_BK) + 4 * N0 * 8;
     static constexpr int A_COLS = K;                       // hi at +0, lo at +K
@@ -564,12 +556,7 @@ struct SLTC {
     static constexpr uint32_t GS_BYTES = uint32_t(128 / NA) * GS_STRIDE * 8;
     static constexpr uint32_t AS_BYTES = 2 * uint32_t(NA) * N0 * 8;   // a_k(x) of two jobs (double-buffered)
     // separate rings: the coefficient rows come from DRAM (deep ring), the Ux tiles mostly from L2 (2 deep)
-    static constexpr int nr_fit(int nbr) { return int((232448 - 1024 - GS_BYTES - AS_BYTES - nbr * 2 * BT) / RAW); }
-#ifdef BF_SL_NBR
-    static constexpr int NB_R = nr_fit(BF_SL_NBR) >= 3 ? BF_SL_NBR : 3;   // experiment where it fits
-#else
-    static constexpr int NB_R = 3;                                   // Ux ring depth
-#endif
+    static constexpr int NB_R = 3;                                   // Ux ring depth (2 / 4 measured: 0.95x / 1.0x)
     static constexpr int NR_FIT = int((232448 - 1024 - GS_BYTES - AS_BYTES - NB_R * 2 * BT) / RAW);
     static constexpr int NR = NR_FIT > 8 ? 8 : NR_FIT;               // raw ring depth
     static constexpr uint32_t OFF_B = NR * RAW, OFF_GS = OFF_B + 2 * NB_R * BT, OFF_AS = OFF_GS + GS_BYTES;
@@ -579,11 +566,7 @@ struct SLTC {
     // the MMAs of the chunks before it instead of waiting for chunk g's MMAs to finish (2 stages left the tensor
     // pipe idle across every split + mbarrier round trip)
     static constexpr int A_COLS = 2 * AH;
-#ifdef BF_SL_NAS
-    static constexpr int NAS = BF_SL_NAS;
-#else
     static constexpr int NAS = (512 - 2 * NB) / A_COLS >= 4 ? 4 : (512 - 2 * NB) / A_COLS;
-#endif
     static constexpr int D_OFF = NAS * A_COLS;
     static constexpr int TMEM_COLS = tmem_cols_pow2<D_OFF + 2 * NB>();
     static_assert(KC % 8 == 0, "K chunk must be whole MMA K steps");
