@@ -28,7 +28,8 @@ cudaError_t launch_s0(const Dims& d, const float2* F, int64_t ldf, const float2*
 // (leafx_floats(d) floats each for V0 and U).
 bool leaf_tc_shape(const Dims& d);
 int64_t leafx_floats(const Dims& d);
-int64_t ux_floats(const Dims& d);   // the SL image: leafx_floats, or half of it for the 2x image (r in {8, 16})
+int64_t ux_floats(const Dims& d);
+int64_t v0x_floats(const Dims& d);  // the S0 image: leafx_floats, or half of it for the 2x image   // the SL image: leafx_floats, or half of it for the 2x image (r in {8, 16})
 cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U, float* V0x, float* Ux, cudaStream_t s);
 // S0 on the tensor cores: same contract as launch_s0, weights from V0x.
 bool s0_tc_supported(const Dims& d, int nv, int64_t ldf);

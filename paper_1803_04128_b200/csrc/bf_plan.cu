@@ -913,7 +913,6 @@ namespace {
 bf_status_t build_leaf_images(bf_plan_s* p, Shard& s)
 {
     const bfk::Dims dl = p->local();
-    const size_t lx = size_t(bfk::leafx_floats(dl));
     auto alloc = [](float** x, size_t bytes) {
         if (cudaMalloc(x, bytes) == cudaSuccess) return true;
         cudaGetLastError();
@@ -921,7 +920,7 @@ bf_status_t build_leaf_images(bf_plan_s* p, Shard& s)
         return false;
     };
     cudaError_t e = cudaSuccess;
-    if (!s.v0x && alloc(&s.v0x, lx * sizeof(float))) e = bfk::expand_leaf_weights(dl, s.v0, s.u, s.v0x, nullptr, 0);
+    if (!s.v0x && alloc(&s.v0x, size_t(bfk::v0x_floats(dl)) * sizeof(float))) e = bfk::expand_leaf_weights(dl, s.v0, s.u, s.v0x, nullptr, 0);
     if (e == cudaSuccess && !s.ux && alloc(&s.ux, size_t(bfk::ux_floats(dl)) * sizeof(float)))
         e = bfk::expand_leaf_weights(dl, s.v0, s.u, nullptr, s.ux, 0);
     return e == cudaSuccess ? BF_OK : cuda_fail(e, "leaf weight images");
@@ -1554,8 +1553,7 @@ bf_status_t bf_plan_get_info(bf_plan_t p, bf_plan_info_t* info)
     info->workspace_bytes = nsh * int64_t(p->ws_bytes);
     info->tc_weight_bytes = 0;
     for (const Shard& s : p->sh) {
-        const int64_t lx = bfk::leafx_floats(p->local());
-        if (s.v0x) info->tc_weight_bytes += lx * int64_t(sizeof(float));
+        if (s.v0x) info->tc_weight_bytes += bfk::v0x_floats(p->local()) * int64_t(sizeof(float));
         if (s.ux) info->tc_weight_bytes += bfk::ux_floats(p->local()) * int64_t(sizeof(float));
     }
     {

@@ -94,28 +94,49 @@ static cudaError_t make_rows_tmap(CUtensorMap* m, const float2* base, int64_t ro
 constexpr int S0X_NC = 128, S0X_KC = 32;
 constexpr int64_t S0X_TILE_FLOATS = int64_t(S0X_NC) * S0X_KC;
 
+// The 2x S0 image (S0TC I2): any leaf shape whose N chunks hold whole (a, t) halves (n0 r a multiple of 64);
+// BF_S0_IMAGE4 builds keep the 4x image.
+constexpr bool s0_i2(int R, int N0)
+{
+#ifdef BF_S0_IMAGE4
+    return false && R && N0;
+#else
+    return (N0 * R) % 64 == 0;
+#endif
+}
+
 int64_t leafx_floats(const Dims& d) { return d.N * int64_t(2 * d.R) * int64_t(2 << d.l0) * 2; }
 
-__global__ void expand_s0_kernel(const float2* __restrict__ V0, float* __restrict__ X, int LN, int l0, int R)
+// i2: the 2x image (section 5.1): per N chunk of 128 rows, rows c' 64 + m hold V0r / V0i of output m of the chunk's
+// 64 (a, t); K = j in tiles of 16 (8 KB hi + 8 KB lo per tile), no real embedding
+__global__ void expand_s0_kernel(const float2* __restrict__ V0, float* __restrict__ X, int LN, int l0, int R, int i2)
 {
     const int n0 = 1 << l0;
     const int64_t nleaf = (int64_t(1) << LN) >> l0;
-    const int rows = n0 * 2 * R, K = 2 * n0;
-    const int nch = rows / S0X_NC, kch = K / S0X_KC;
+    const int rows = n0 * 2 * R, K = i2 ? n0 : 2 * n0;
+    const int KT = i2 ? S0X_KC / 2 : S0X_KC;
+    const int64_t TF = int64_t(S0X_NC) * KT;   // floats of one tile (hi or lo)
+    const int nch = rows / S0X_NC, kch = K / KT;
     const int64_t total = nleaf * rows * int64_t(K);
     for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
         const int64_t b = g / (int64_t(rows) * K);
         const int rem = int(g - b * rows * K);
         const int n = rem / K, k = rem - n * K;
-        const int a = n / (2 * R), t = (n / 2) % R, cp = n & 1, j = k >> 1, c = k & 1;
-        const float2 w = V0[(int64_t(a) * nleaf + b) * (n0 * R) + int64_t(j) * R + t];
         float hi, lo;
-        tc::split(embed(w, cp, c), hi, lo);
-        const int nc = n / S0X_NC, kc = k / S0X_KC;
-        float* tile = X + ((b * nch + nc) * kch + kc) * 2 * S0X_TILE_FLOATS;
-        const uint32_t off = tc::kmaj_off(n % S0X_NC, k % S0X_KC, S0X_NC) / 4;
+        if (i2) {
+            const int nc = n / S0X_NC, m = n % S0X_NC, cp = m / 64, q = nc * 64 + (m % 64), a = q / R, t = q % R;
+            const float2 w = V0[(int64_t(a) * nleaf + b) * (n0 * R) + int64_t(k) * R + t];
+            tc::split(cp ? w.y : w.x, hi, lo);
+        } else {
+            const int a = n / (2 * R), t = (n / 2) % R, cp = n & 1, j = k >> 1, c = k & 1;
+            const float2 w = V0[(int64_t(a) * nleaf + b) * (n0 * R) + int64_t(j) * R + t];
+            tc::split(embed(w, cp, c), hi, lo);
+        }
+        const int nc = n / S0X_NC, kc = k / KT;
+        float* tile = X + ((b * nch + nc) * kch + kc) * 2 * TF;
+        const uint32_t off = tc::kmaj_off(n % S0X_NC, k % KT, S0X_NC) / 4;
         tile[off] = hi;
-        tile[S0X_TILE_FLOATS + off] = lo;
+        tile[TF + off] = lo;
     }
 }
 
@@ -180,7 +201,7 @@ cudaError_t expand_leaf_weights(const Dims& d, const float2* V0, const float2* U
     if (!leaf_tc_shape(d)) return cudaErrorInvalidValue;
     const unsigned grid = 148 * 16;
     if (V0x) {
-        expand_s0_kernel<<<grid, 256, 0, s>>>(V0, V0x, d.LN, d.l0, d.R);
+        expand_s0_kernel<<<grid, 256, 0, s>>>(V0, V0x, d.LN, d.l0, d.R, s0_i2(d.R, 1 << d.l0) ? 1 : 0);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -215,13 +236,15 @@ static int sm_count()
     return n;
 }
 
-template <int R, int N0>
+template <int R, int N0, bool I2 = false>
 struct S0TC {
     static constexpr int K = 2 * N0;
-    static constexpr int KS = K / S0X_KC;                 // 32-wide K tiles per chunk (2 or 4)
+    static constexpr int KS = K / S0X_KC;                 // K tiles per chunk (2 or 4): 16 complex j each
+    static constexpr int KT = I2 ? S0X_KC / 2 : S0X_KC;   // B tile K (real columns)
     static constexpr int NCH = N0 * 2 * R / S0X_NC;       // 128-row N chunks per job
-    static constexpr int NSTAGE = KS + 1;                 // weight ring depth (32 KB tiles; 6 measured: no change)
-    static constexpr uint32_t TILE = S0X_TILE_FLOATS * 4;  // 16 KB
+    static constexpr int NSTAGE = I2 ? 2 * KS + 1 : KS + 1;   // weight ring depth (32 KB stages, 16 KB for I2)
+    static constexpr int64_t TILE_FLOATS = int64_t(S0X_NC) * KT;
+    static constexpr uint32_t TILE = uint32_t(TILE_FLOATS) * 4;   // 16 KB (8 KB for I2)
     static constexpr uint32_t STAGE = 2 * TILE;            // hi + lo
     // staging row stride (complex): padded (bank spread) where shared memory allows, else dense
     static constexpr int FS = (N0 == 64) ? N0 : N0 + 2;
@@ -238,12 +261,12 @@ struct S0TC {
 // CL = 2: clusters of two CTAs on the two halves of a leaf's vector tiles at the same time; each CTA bulk-copies
 // one of the two 16 KB tiles (hi or lo) of every V0x stage and multicasts it to both (half the L2 -> SM
 // traffic of the 1.3 MB-per-job weight stream); cluster-multicast MMA commits release a stage in both CTAs.
-template <int R, int N0, int CL>
+template <int R, int N0, int CL, bool I2>
 __global__ void __launch_bounds__(448, 1)
     s0_tc_kernel(const float2* __restrict__ F, int64_t ldf, const float2* __restrict__ ampb,
                  const float* __restrict__ V0x, float2* __restrict__ out, int LN, int n_amp, int nv, int nvt)
 {
-    using C = S0TC<R, N0>;
+    using C = S0TC<R, N0, I2>;
     extern __shared__ __align__(128) uint8_t sm_s0tc[];
     uint8_t* ring = sm_s0tc;
     float2* Fs = reinterpret_cast<float2*>(sm_s0tc + C::OFF_F);    // [column][FS]
@@ -320,9 +343,9 @@ __global__ void __launch_bounds__(448, 1)
                     const int st = int(it % C::NSTAGE);
                     if (it >= C::NSTAGE) tc::mbar_wait(&empty[st], uint32_t(it / C::NSTAGE - 1) & 1);
                     tc::mbar_arrive_expect_tx(&full[st], C::STAGE);   // both tiles land here
-                    const float* src = V0x + (b * WPJ + w) * 2 * S0X_TILE_FLOATS;
+                    const float* src = V0x + (b * WPJ + w) * 2 * C::TILE_FLOATS;
                     if constexpr (CL == 2)
-                        tc::bulk_g2s_mc(ring + st * C::STAGE + cr * C::TILE, src + cr * S0X_TILE_FLOATS, C::TILE,
+                        tc::bulk_g2s_mc(ring + st * C::STAGE + cr * C::TILE, src + cr * C::TILE_FLOATS, C::TILE,
                                         &full[st], uint16_t(3));
                     else
                         tc::bulk_g2s(ring + st * C::STAGE, src, C::STAGE, &full[st]);
@@ -360,13 +383,28 @@ __global__ void __launch_bounds__(448, 1)
                     float2 y0 = cmul_tc(make_float2(a.x, a.y), make_float2(f.x, f.y));
                     float2 y1 = cmul_tc(make_float2(a.z, a.w), make_float2(f.z, f.w));
                     if (!ok) y0 = y1 = make_float2(0.f, 0.f);
-                    tc::split(y0.x, hi[2 * jj], lo[2 * jj]);
-                    tc::split(y0.y, hi[2 * jj + 1], lo[2 * jj + 1]);
-                    tc::split(y1.x, hi[2 * jj + 2], lo[2 * jj + 2]);
-                    tc::split(y1.y, hi[2 * jj + 3], lo[2 * jj + 3]);
+                    if constexpr (I2) {   // [re of the tile's 16 j | im of them]: hi[0..8) re, hi[8..16) im
+                        tc::split(y0.x, hi[jj], lo[jj]);
+                        tc::split(y1.x, hi[jj + 1], lo[jj + 1]);
+                        tc::split(y0.y, hi[8 + jj], lo[8 + jj]);
+                        tc::split(y1.y, hi[8 + jj + 1], lo[8 + jj + 1]);
+                    } else {
+                        tc::split(y0.x, hi[2 * jj], lo[2 * jj]);
+                        tc::split(y0.y, hi[2 * jj + 1], lo[2 * jj + 1]);
+                        tc::split(y1.x, hi[2 * jj + 2], lo[2 * jj + 2]);
+                        tc::split(y1.y, hi[2 * jj + 3], lo[2 * jj + 3]);
+                    }
                 }
-                tc::tmem_st16(tmem + lb + uint32_t(2 * j0), hi);
-                tc::tmem_st16(tmem + lb + uint32_t(C::A_COLS + 2 * j0), lo);
+                if constexpr (I2) {
+                    const uint32_t cb = uint32_t(kt * S0X_KC + (j0 % (S0X_KC / 2)));
+                    tc::tmem_st8(tmem + lb + cb, hi);
+                    tc::tmem_st8(tmem + lb + cb + S0X_KC / 2, hi + 8);
+                    tc::tmem_st8(tmem + lb + uint32_t(C::A_COLS) + cb, lo);
+                    tc::tmem_st8(tmem + lb + uint32_t(C::A_COLS) + cb + S0X_KC / 2, lo + 8);
+                } else {
+                    tc::tmem_st16(tmem + lb + uint32_t(2 * j0), hi);
+                    tc::tmem_st16(tmem + lb + uint32_t(C::A_COLS + 2 * j0), lo);
+                }
                 if ((j0 + 8) % (S0X_KC / 2) == 0) {
                     tc::tmem_wait_st();
                     tc::fence_before_sync();
@@ -397,10 +435,24 @@ __global__ void __launch_bounds__(448, 1)
                         const int pass = kPassOrder[q];
                         const uint64_t b = tc::desc_add(dB0, st * C::STAGE + (pass == 2 ? C::TILE : 0));
                         const uint32_t a = tmem + uint32_t((pass == 1 ? C::A_COLS : 0) + ks * S0X_KC);
+                        if constexpr (I2) {
+                            // D[:, 0:128] += A_R [V0r; V0i]^T, D[:, 0:64] += A_I (-V0i)^T, D[:, 64:128] += A_I V0r^T
+                            constexpr uint32_t idh = tc::idesc_tf32(128, S0X_NC / 2);
+                            constexpr uint32_t HALF = (S0X_NC / 2 / 8) * 128;
+#pragma unroll
+                            for (int kk = 0; kk < C::KT / 8; kk++) {
+                                const uint64_t bk = tc::desc_add(b, kk * 2 * LBO_B);
+                                tc::mma_tf32_ts_warp(d, a + kk * 8, bk, idesc, (q | ks | kk) ? 1u : 0u);
+                                tc::mma_tf32_ts_warp(d, a + S0X_KC / 2 + kk * 8, tc::desc_add(bk, HALF), idh | (1u << 14),
+                                                     1u);
+                                tc::mma_tf32_ts_warp(d + S0X_NC / 2, a + S0X_KC / 2 + kk * 8, bk, idh, 1u);
+                            }
+                        } else {
 #pragma unroll
                         for (int kk = 0; kk < S0X_KC / 8; kk++)
                             tc::mma_tf32_ts_warp(d, a + kk * 8, tc::desc_add(b, kk * 2 * LBO_B), idesc,
                                                  (q | ks | kk) ? 1u : 0u);
+                        }
                     }
                     if constexpr (CL == 2)
                         tc::commit_mc_warp(&empty[st], uint16_t(3));   // free in both CTAs of the cluster
@@ -428,16 +480,31 @@ __global__ void __launch_bounds__(448, 1)
                 const int slot = int(gc & 1);
                 tc::mbar_wait(&dfull[slot], uint32_t(gc >> 1) & 1);
                 tc::fence_after_sync();
-                const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(C::D_OFF + slot * S0X_NC + cbase);
+                // I2: output m of the chunk has its re part in column m, its im part in column 64 + m; this thread
+                // takes m in [half 32, half 32 + 32) -- the same outputs (a, t) as the interleaved layout
+                const uint32_t taddr = tmem + (uint32_t(q4 * 32) << 16) +
+                                       uint32_t(C::D_OFF + slot * S0X_NC + (I2 ? cbase / 2 : cbase));
                 const int q0 = (nc * S0X_NC + cbase) >> 1;
                 int t = q0 % R;
                 float2* o = obase + int64_t(q0 / R) * strideA + int64_t(t) * nv;
 #pragma unroll
                 for (int c0 = 0; c0 < 64; c0 += 32) {
                     float x[32];
-                    tc::tmem_ld16(taddr + c0, x);
-                    tc::tmem_ld16(taddr + c0 + 16, x + 16);
-                    tc::tmem_wait_ld();
+                    if constexpr (I2) {   // x[2i] = re, x[2i + 1] = im of output c0/2 + i
+                        float xr[16], xi[16];
+                        tc::tmem_ld16(taddr + c0 / 2, xr);
+                        tc::tmem_ld16(taddr + S0X_NC / 2 + c0 / 2, xi);
+                        tc::tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; i++) {
+                            x[2 * i] = xr[i];
+                            x[2 * i + 1] = xi[i];
+                        }
+                    } else {
+                        tc::tmem_ld16(taddr + c0, x);
+                        tc::tmem_ld16(taddr + c0 + 16, x + 16);
+                        tc::tmem_wait_ld();
+                    }
                     if (c0 == 32) {
                         tc::fence_before_sync();
                         tc::mbar_arrive(&dempty[slot]);
@@ -468,12 +535,13 @@ template <int R, int N0>
 static cudaError_t s0_tc_go(const Dims& d, const float2* F, int64_t ldf, const float2* ampb, const float* V0x,
                             float2* out, int nv, cudaStream_t s, bool multicast)
 {
-    using C = S0TC<R, N0>;
+    constexpr bool I2 = s0_i2(R, N0);
+    using C = S0TC<R, N0, I2>;
     const int nvt = (nv + 127) / 128;
     const int64_t leaves = d.N / N0;
     cudaError_t e;
     if (multicast && nvt % 2 == 0 && sm_count() >= 2) {
-        auto kern = s0_tc_kernel<R, N0, 2>;
+        auto kern = s0_tc_kernel<R, N0, 2, I2>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
         if (e != cudaSuccess) return e;
         const int64_t ncl = std::min<int64_t>(leaves * (nvt / 2), sm_count() / 2);
@@ -491,7 +559,7 @@ static cudaError_t s0_tc_go(const Dims& d, const float2* F, int64_t ldf, const f
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, kern, F, ldf, ampb, V0x, out, d.LN, d.n_amp, nv, nvt);
     }
-    auto kern = s0_tc_kernel<R, N0, 1>;
+    auto kern = s0_tc_kernel<R, N0, 1, I2>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
     const int64_t jobs = leaves * nvt;
@@ -1665,5 +1733,6 @@ cudaError_t rows_tmap(CUtensorMap* m, const float2* base, int64_t rows, int nv, 
 int tc_sm_count() { return sm_count(); }
 
 int64_t ux_floats(const Dims& d) { return sl_i2(d.R) ? leafx_floats(d) / 2 : leafx_floats(d); }
+int64_t v0x_floats(const Dims& d) { return s0_i2(d.R, 1 << d.l0) ? leafx_floats(d) / 2 : leafx_floats(d); }
 
 }  // namespace bfk
