@@ -39,6 +39,8 @@ UNIT = "N*RHS/s"
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
+L2_BYTES = 126 << 20   # B200 L2
+
 def _peaks():
     """HBM GB/s and the TF32 tensor peak (TFLOP/s) with their sources.  TF32 = the measured sustained cuBLAS
     bf16 rate x the guide's nominal tf32/bf16 ratio (1.1 / 2.25): the kernels run inside a ~100 ms step under
@@ -339,6 +341,8 @@ def main():
     ap.add_argument("--log2n", type=int, default=None, help="override N (profiling of a smaller instance only)")
     ap.add_argument("--index-shard", action="store_true",
                     help="split ONE batch by index over the ranks (NCCL all-to-all at level h; cfg5's mode)")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="one CUDA-graph launch per step (bf_apply_graph); auto: for steps of <= 2^22 N*vectors")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exchange", choices=["copy", "fused"], default="copy",
@@ -477,22 +481,47 @@ def main():
     Gd = torch.empty_like(Fd)
     stream = torch.cuda.current_stream()
 
+    # launch: one CUDA-graph launch per step (bf_apply_graph) where the step's kernels run for microseconds and
+    # the host launch rate would bound it, else the eager stream launches of bf_apply
+    use_graph = args.graph == "on" or (args.graph == "auto" and not args.index_shard
+                                       and w.n * nloc * w.n_amp <= (1 << 22))
+    if use_graph and args.index_shard:
+        raise SystemExit("--graph on: bf_apply_graph does not take NCCL index-sharded plans")
+
+    def step():
+        (plan.apply_graph if use_graph else plan.apply)(Fd, Gd, nloc, stream)
+
     for _ in range(args.warmup):
-        plan.apply(Fd, Gd, nloc, stream)
+        step()
     torch.cuda.synchronize()
+    # L2: a working set that fits the 126 MB L2 would stay resident between steps, so those configs flush it
+    # (a 256 MB write between steps, outside the timed spans) and time every step alone
+    work_bytes = 2 * 8 * w.n * nloc + 8 * (w.n >> ((world.bit_length() - 1) if args.index_shard else 0)) * w.rank * min(chunk, nloc) * w.n_amp + info["factor_bytes"]
+    flush = work_bytes < 2 * L2_BYTES
+    scratch = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device="cuda") if flush else None
 
     # ---- timed region: K steps, device-timed with CUDA events on the launching stream ----
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            plan.apply(Fd, Gd, nloc, stream)
-        ev1.record(stream)
+        if flush:
+            spans = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                     for _ in range(args.steps)]
+            for i, (a, b) in enumerate(spans):
+                scratch.fill_(i & 0xFF)
+                a.record(stream)
+                step()
+                b.record(stream)
+        else:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                step()
+            ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = (sum(a.elapsed_time(b) for a, b in spans) if flush else ev0.elapsed_time(ev1)) / args.steps
+    del scratch
     # per-kernel times: the same K steps again with the library's CUDA events around every launch (a separate
     # pass, so the events' own cost stays out of ms_per_step; for the millisecond-scale steps the two agree)
     plan.set_timing(True)
@@ -631,9 +660,14 @@ def main():
                                           else "NCCL all-to-all)") if args.index_shard
                                        else f"rhs-sharded x{world}: rank q applies columns [q {w.nrhs}/{world}, "
                                             f"(q+1) {w.nrhs}/{world}) (no collective)"),
-                       "l2": (f"no flush: the working set (F {8 * w.n * nloc / 1e9:.2g} GB, coefficients "
-                              f"{8 * wl.n * w.rank * min(chunk, nloc) * w.n_amp / 1e9:.3g} GB per level, factors "
-                              f"{info['factor_bytes'] / 1e9:.3g} GB) exceeds the 126 MB L2"),
+                       "l2": ((f"flushed: the working set ({work_bytes / 1e6:.3g} MB) fits the 126 MB L2, so a "
+                               f"{2 * L2_BYTES >> 20} MB buffer is written between steps and each step is timed "
+                               "alone") if flush else
+                              (f"no flush: the working set (F {8 * w.n * nloc / 1e9:.2g} GB, coefficients "
+                               f"{8 * wl.n * w.rank * min(chunk, nloc) * w.n_amp / 1e9:.3g} GB per level, factors "
+                               f"{info['factor_bytes'] / 1e9:.3g} GB) exceeds the 126 MB L2")),
+                       "launch": ("one CUDA-graph launch per step (bf_apply_graph)" if use_graph
+                                  else "stream launches (bf_apply)"),
                        "tensor_core_classes": info["tc_classes"], "tc_weight_bytes": info["tc_weight_bytes"],
                        "factor_bytes": info["factor_bytes"], "structured": bool(info["structured"])},
             "roofline": roof,

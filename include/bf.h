@@ -239,6 +239,17 @@ bf_status_t bf_apply(bf_plan_t plan, const bf_c64 *F, bf_c64 *G, int64_t nrhs, v
 bf_status_t bf_apply_ex(bf_plan_t plan, const bf_c64 *F, int64_t ldf, bf_c64 *G, int64_t ldg, int64_t nrhs,
                         void *workspace, size_t workspace_bytes, void *stream);
 
+/* bf_apply as ONE graph launch (same operation, eqn:tg P:24-28 with BF in the form eqn:BFM P:613-619, same
+ * arguments and errors).  The first call with a given (F, G, nrhs) captures bf_apply's kernel sequence into a
+ * CUDA graph on a private stream and instantiates it (host work of a few hundred microseconds, nothing
+ * runs); every call then launches that graph on `stream`, so a step of several kernels costs one launch — for
+ * the small configurations, whose kernels run for microseconds, the host launch rate otherwise bounds the
+ * step.  The plan keeps ONE graph: a call with other F, G or nrhs re-captures, and bf_plan_set_option /
+ * bf_plan_set_timing drop it (with timing on, the call is an eager bf_apply so every launch is timed).  F and
+ * G must stay allocated while the graph is cached; their contents are read / written at every launch.
+ * BF_ERR_NOT_SUPPORTED for NCCL index-sharded plans. */
+bf_status_t bf_apply_graph(bf_plan_t plan, const bf_c64 *F, bf_c64 *G, int64_t nrhs, void *stream);
+
 /* End-to-end apply with HOST buffers (N x nrhs column-major, ld = N; pinned memory
  * recommended): per RHS chunk, host->device copy of F, the apply, device->host copy
  * of G, all on `stream`; returns after the stream has completed the work. */

@@ -35,7 +35,7 @@ STATUS = {0: "BF_OK", 1: "BF_ERR_INVALID_ARG", 2: "BF_ERR_SHAPE", 3: "BF_ERR_ALI
           5: "BF_ERR_CUDA", 6: "BF_ERR_NCCL", 7: "BF_ERR_NOT_SUPPORTED", 8: "BF_ERR_STATE"}
 
 # every symbol include/*.h declares (checked by tests/test_abi.py)
-EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finalize", "bf_apply", "bf_apply_ex",
+EXPORTS = ("bf_plan_create", "bf_plan_alloc", "bf_plan_upload", "bf_plan_finalize", "bf_apply", "bf_apply_ex", "bf_apply_graph",
            "bf_apply_host", "bf_apply_host_async", "bf_apply_host_wait", "bf_workspace_bytes", "bf_plan_get_info", "bf_plan_set_timing", "bf_plan_timing", "bf_plan_set_option",
            "bf_plan_destroy", "bf_last_error", "bf_abi_version", "bf_build_n_amp", "bf_build_amp", "bf_build_blocks",
            "bf_build_block_elems", "bf_plan_build_fio", "bf_nccl_get_unique_id", "bf_plan_alloc_sharded",
@@ -149,6 +149,7 @@ def lib():
             "bf_plan_build_fio_structured": ([P(bf_fio_t), ctypes.c_int, i64, i64, P(vp)], i32),
             "bf_apply": ([vp, vp, vp, i64, vp], i32),
             "bf_apply_ex": ([vp, vp, i64, vp, i64, i64, vp, sz, vp], i32),
+            "bf_apply_graph": ([vp, vp, vp, i64, vp], i32),
             "bf_apply_host": ([vp, vp, vp, i64, vp], i32),
             "bf_apply_host_async": ([vp, vp, vp, i64, vp], i32),
             "bf_apply_host_wait": ([vp], i32),
@@ -343,6 +344,11 @@ class Plan:
     def apply(self, F, G, nrhs: int, stream=None):
         """G = sum_k a_k o BF(b_k o F) on device buffers (N x nrhs column-major, ld = N)."""
         _check(lib().bf_apply(self._h, _ptr(F), _ptr(G), nrhs, _stream(stream)))
+
+    def apply_graph(self, F, G, nrhs: int, stream=None):
+        """As apply, as one launch of the plan's cached CUDA graph of it (captured at the first call with these
+        F, G, nrhs; include/bf.h bf_apply_graph)."""
+        _check(lib().bf_apply_graph(self._h, _ptr(F), _ptr(G), nrhs, _stream(stream)))
 
     def apply_ex(self, F, ldf, G, ldg, nrhs, workspace=None, workspace_bytes=0, stream=None):
         _check(lib().bf_apply_ex(self._h, _ptr(F), ldf, _ptr(G), ldg, nrhs,

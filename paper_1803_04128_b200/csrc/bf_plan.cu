@@ -209,6 +209,13 @@ struct bf_plan_s {
     double ms[BF_NUM_KCLASS] = {0};
     int64_t nlaunch[BF_NUM_KCLASS] = {0};
     cudaEvent_t done = nullptr;
+    // bf_apply_graph: the instantiated CUDA graph of one bf_apply with the argument set (g_F, g_G, g_nrhs),
+    // captured on the private stream `cap`; dropped by any option change and by bf_plan_set_timing
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap = nullptr;
+    const void* g_F = nullptr;
+    const void* g_G = nullptr;
+    int64_t g_nrhs = -1;
 
     int64_t nloc() const { return d.N >> g; }   // pairs / rows per shard
     bfk::Dims local() const
@@ -297,6 +304,18 @@ bf_status_t validate_sharding(const bf_desc_t* d, int world, int rank)
     return BF_OK;
 }
 
+void drop_graph(bf_plan_s* p)
+{
+    if (p->gexec) {
+        DeviceGuard g(p->device);
+        if (p->done) cudaEventSynchronize(p->done);   // no replay may still be running
+        cudaGraphExecDestroy(p->gexec);
+    }
+    p->gexec = nullptr;
+    p->g_F = p->g_G = nullptr;
+    p->g_nrhs = -1;
+}
+
 void free_plan(bf_plan_s* p)
 {
     if (!p) return;
@@ -341,6 +360,8 @@ void free_plan(bf_plan_s* p)
     }
     if (p->h2d) cudaStreamDestroy(p->h2d);
     if (p->d2h) cudaStreamDestroy(p->d2h);
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    if (p->cap) cudaStreamDestroy(p->cap);
     if (p->comm) nccl().CommDestroy(p->comm);
     delete p;
 }
@@ -1363,6 +1384,48 @@ bf_status_t bf_apply(bf_plan_t p, const bf_c64* F, bf_c64* G, int64_t nrhs, void
     return bf_apply_ex(p, F, rows, G, rows, nrhs, nullptr, 0, stream);
 }
 
+bf_status_t bf_apply_graph(bf_plan_t p, const bf_c64* F, bf_c64* G, int64_t nrhs, void* stream)
+{
+    if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
+    if (!p->finalized) return fail(BF_ERR_STATE, "plan not finalized");
+    if (p->mode == BF_SHARD_NCCL) return fail(BF_ERR_NOT_SUPPORTED, "bf_apply_graph on an NCCL plan");
+    if (nrhs <= 0) return bf_apply(p, F, G, nrhs, stream);   // argument errors and the empty batch as bf_apply
+    if (p->timing) return bf_apply(p, F, G, nrhs, stream);   // per-launch events need the eager launches
+    DeviceGuard g(p->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!(p->gexec && p->g_F == F && p->g_G == G && p->g_nrhs == nrhs)) {
+        drop_graph(p);
+        cudaError_t e = cudaSuccess;
+        if (!p->cap && (e = cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "capture stream");
+        // the capture stream must see the caller's prior work on `stream` only at replay time: the graph is
+        // launched on `stream`, so nothing is ordered here
+        if ((e = cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+            return cuda_fail(e, "begin capture");
+        const bf_status_t st = bf_apply(p, F, G, nrhs, p->cap);
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamEndCapture(p->cap, &graph);
+        if (st != BF_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "end capture");
+        e = cudaGraphInstantiate(&p->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            p->gexec = nullptr;
+            return cuda_fail(e, "graph instantiate");
+        }
+        p->g_F = F;
+        p->g_G = G;
+        p->g_nrhs = nrhs;
+    }
+    cudaError_t e = cudaGraphLaunch(p->gexec, s);
+    if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+    cudaEventRecord(p->done, s);
+    return BF_OK;
+}
+
 bf_status_t bf_apply_host(bf_plan_t p, const bf_c64* F_host, bf_c64* G_host, int64_t nrhs, void* stream)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
@@ -1645,6 +1708,7 @@ bf_status_t setup_peer_exchange(bf_plan_s* p)
 bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
+    drop_graph(p);   // the captured launch sequence depends on the options
     if (option == BF_OPT_TENSOR_CORES) {
         if (value != 0 && value != 1) return fail(BF_ERR_INVALID_ARG, "BF_OPT_TENSOR_CORES takes 0 or 1");
         p->tensor_cores = value != 0;
@@ -1698,6 +1762,7 @@ bf_status_t bf_plan_set_option(bf_plan_t p, int32_t option, int64_t value)
 bf_status_t bf_plan_set_timing(bf_plan_t p, int32_t enable)
 {
     if (!p) return fail(BF_ERR_INVALID_ARG, "plan is NULL");
+    drop_graph(p);
     DeviceGuard g(p->device);
     for (auto& tl : p->pending) {
         cudaEventSynchronize(tl.stop);

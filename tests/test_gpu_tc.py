@@ -238,6 +238,51 @@ def test_cuda_graph_capture(nrhs):
     plan.destroy()
 
 
+@pytest.mark.parametrize("nrhs", [128, 8, 1])
+def test_apply_graph(nrhs):
+    """bf_apply_graph (include/bf.h): one launch of the plan's cached graph of bf_apply equals the eager apply
+    bitwise (tensor-core, small-batch and tiny kernels: nrhs 128 / 8 / 1); new inputs in the same buffer are
+    read at every launch; other buffers or nrhs re-capture; an option change drops the graph and the next
+    call captures the new kernel sequence."""
+    LN, l0, r = 14, 6, 10
+    plan = bf.Plan.build_fio(bf.fio(W.K_FIO, W.A_CFG1, LN, l0, r), max_nrhs_chunk=nrhs)
+    F1 = torch.from_numpy(np.ascontiguousarray(W.rhs(1 << LN, nrhs, 5).T)).cuda()
+    F2 = torch.from_numpy(np.ascontiguousarray(W.rhs(1 << LN, nrhs, 6).T)).cuda()
+    ref1, ref2 = torch.empty_like(F1), torch.empty_like(F1)
+    plan.apply(F1, ref1, nrhs)
+    plan.apply(F2, ref2, nrhs)
+    torch.cuda.synchronize()
+    Fin, G = F1.clone(), torch.zeros_like(F1)
+    s = torch.cuda.Stream()
+    plan.apply_graph(Fin, G, nrhs, stream=s)
+    s.synchronize()
+    assert torch.equal(G, ref1)
+    Fin.copy_(F2)
+    torch.cuda.synchronize()
+    G.zero_()
+    torch.cuda.synchronize()
+    plan.apply_graph(Fin, G, nrhs, stream=s)
+    s.synchronize()
+    assert torch.equal(G, ref2)
+    G2 = torch.zeros_like(F1)
+    plan.apply_graph(F1, G2, nrhs)          # other buffers: re-captured, default stream
+    torch.cuda.synchronize()
+    assert torch.equal(G2, ref1)
+    if nrhs > 1:                            # fewer columns of the same buffers
+        G3 = torch.zeros_like(F1)
+        plan.apply_graph(F1, G3, nrhs // 2)
+        torch.cuda.synchronize()
+        assert torch.equal(G3[: nrhs // 2], ref1[: nrhs // 2]) and not G3[nrhs // 2:].any()
+    plan.set_tensor_cores(False)            # drops the graph; the FP32 kernels agree within parity
+    G4 = torch.zeros_like(F1)
+    plan.apply_graph(F1, G4, nrhs)
+    ref4 = torch.empty_like(F1)
+    plan.apply(F1, ref4, nrhs)
+    torch.cuda.synchronize()
+    assert torch.equal(G4, ref4)
+    plan.destroy()
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_rhs_shards_concatenate_to_one_gpu(world):
     """bench.py's RHS sharding: each rank applies columns [q nrhs/G, (q+1) nrhs/G) with its own
