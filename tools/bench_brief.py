@@ -9,8 +9,9 @@ except Exception as e:  # noqa: BLE001
     sys.exit(0)
 print(f"{d['config']['workload']} n_gpus={d['n_gpus']} value={d['value']:.4g} ms={d['ms_per_step']:.3f} "
       f"e2e={d['e2e']['value'] if d.get('e2e') else None} clocks={d.get('clocks')}")
-for k, v in d["kernels"].items():
-    if v["launches"]:
+for k, v in d.get("kernels", {}).items():
+    if v.get("launches"):
         print(f"  {k:18s} n={v['launches']:3d} avg={v['ms_avg']:.4f} ms")
-r = d["roofline"]
-print(f"  roofline {r['kernel']} {r['bound']} frac={r['frac']:.3f} step lbl={d['step_roofline']['frac_level_by_level']:.3f}")
+r = d.get("roofline") or {}
+lbl = (d.get("step_roofline") or {}).get("frac_level_by_level")
+print(f"  roofline {r.get('kernel')} {r.get('bound')} frac={r.get('frac')} step lbl={lbl}")
